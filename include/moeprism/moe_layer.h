@@ -1,0 +1,176 @@
+/*
+ * moe_layer.h -- C-ABI of the B200-native MoE-Prism sub-expert MoE layer.
+ *
+ * The reference (MoE-Prism, /root/reference/proj) exposes its hot path only
+ * as header-only C++ free functions; it has no FFI.  This header is the thin
+ * C boundary a binding (ctypes / cgo / JNI / N-API) would load, and the C++
+ * wrapper moe_layer.hpp sits on top of it with the reference's own
+ * signatures.  Each entry point names the reference interface it replaces:
+ *
+ *   mp_layer_forward           <- per-token loop of partitioned_forward
+ *                                 (inc/expert.hpp:101-135) composed over the
+ *                                 selected sub-experts, plus the router
+ *
+ *   mp_layer_forward_selected  <- partitioned_forward with an explicit active
+ *                                 set per token (inc/expert.hpp:101-135)
+ *   mp_layer_route             <- select_topk_subexperts over router scores
+ *                                 (inc/gating.hpp:129-145), linear or proxy
+ *                                 (proxy_scores, inc/gating.hpp:107-125)
+ *   mp_layer_load_expert[_file]<- ToyExpert / load_toy_expert
+ *                                 (inc/expert.hpp:17-39, inc/io.hpp:225-251)
+ *   mp_layer_set_partition     <- Partition + validate (inc/partition.hpp:15-46)
+ *   mp_layer_load_partition_map<- read_ndjson + partition_doc_from_json
+ *                                 (inc/serde.hpp:113-151, gates :160-168)
+ *   mp_layer_set_gates         <- GateSet + validate (inc/gating.hpp:19-43)
+ *
+ * Conventions (mirroring inc/error.hpp:8-16):
+ *   status 0 ok; 1 validation error (ValidationError); 2 I/O error (IoError);
+ *   3 CUDA error.  mp_last_error() returns the calling thread's message.
+ * Ownership: the layer owns its (packed, device-resident) weights; the caller
+ * owns activations.  Device pointers are CUDA global memory on the layer's
+ * device.  `stream` is a cudaStream_t (NULL = legacy default stream).
+ * Threading: one handle per stream; forward is stream-ordered and not
+ * re-entrant on one handle; distinct handles are independent.
+ * There is no CPU fallback: every compute entry point launches CUDA kernels
+ * and fails with status 3 when no sm_100a device is usable.
+ */
+#ifndef MOEPRISM_MOE_LAYER_H
+#define MOEPRISM_MOE_LAYER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MP_OK 0
+#define MP_ERR_VALIDATION 1
+#define MP_ERR_IO 2
+#define MP_ERR_CUDA 3
+
+#define MP_DTYPE_F32 0  /* fp32 end to end: SIMT FFMA grouped GEMMs (1e-5 mode) */
+#define MP_DTYPE_BF16 1 /* bf16 activations/weights, fp32 accumulate: tcgen05 */
+
+#define MP_ROUTER_LINEAR 0 /* logits = x . W_r (fp32) */
+#define MP_ROUTER_PROXY 1  /* proxy gate neurons, inc/gating.hpp:107-125 */
+
+#define MP_WEIGHT_UNIT 0           /* y = sum of selected sub-expert outputs (reference) */
+#define MP_WEIGHT_SOFTMAX_RENORM 1 /* y = sum p_g / sum_sel p * o_g */
+
+#define MP_SEL_NONE 0xFFFFFFFFu /* padding in [T x k_max] selection arrays */
+
+typedef int mp_status;
+typedef struct mp_layer_s* mp_layer_t;
+
+typedef struct {
+    uint32_t n_experts;    /* E parent experts */
+    uint32_t n_subexperts; /* S sub-experts per expert (Partition::n_subexperts) */
+    uint32_t d_model;      /* d */
+    uint32_t d_ff;         /* ffn neurons per expert */
+    uint32_t dtype;        /* MP_DTYPE_* of x, y and the packed weights */
+    uint32_t router_mode;  /* MP_ROUTER_* */
+    uint32_t weight_mode;  /* MP_WEIGHT_* */
+    uint32_t k_max;        /* max active sub-experts per token (<= E*S) */
+    uint32_t max_tokens;   /* workspace capacity, tokens per forward */
+    int32_t device;        /* CUDA device ordinal */
+} mp_layer_desc;
+
+/* Library / device info.  mp_device_check fails (3) unless device `dev` is an
+ * sm_100 part this build has code for. */
+const char* mp_version(void);
+const char* mp_last_error(void);
+mp_status mp_device_check(int32_t dev);
+
+mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out);
+mp_status mp_layer_destroy(mp_layer_t h);
+mp_status mp_layer_get_desc(mp_layer_t h, mp_layer_desc* out);
+
+/* Expert e's weights in the MPEX layout (inc/io.hpp:210-223): w_gate, w_up
+ * d_model x d_ff row-major fp32, w_down d_ff x d_model row-major fp32.
+ * Host or device pointers.  Rejects non-finite weights (inc/expert.hpp:34).
+ * The packer (neurons grouped per sub-expert, gate/up interleaved, zero
+ * padded, cast to dtype) runs on the GPU once both the weights and the
+ * partition of expert e are known. */
+mp_status mp_layer_load_expert(mp_layer_t h, uint32_t e, const float* w_gate, const float* w_up, const float* w_down);
+mp_status mp_layer_load_expert_file(mp_layer_t h, uint32_t e, const char* mpex_path);
+
+/* Partition of expert e (inc/partition.hpp:15-46): assignment[j] = label of
+ * neuron j, n == d_ff, balanced, all labels < n_sub == desc.n_subexperts. */
+mp_status mp_layer_set_partition(mp_layer_t h, uint32_t e, uint32_t n_sub, const uint32_t* assignment, size_t n);
+/* NDJSON partition map (inc/serde.hpp:100-151): one document per expert,
+ * "expert_id" selects e.  Documents carrying "r"/"gates" also set the gate
+ * set of that expert (inc/serde.hpp:156-168). */
+mp_status mp_layer_load_partition_map(mp_layer_t h, const char* ndjson_path);
+
+/* Linear router: w_r is d_model x (E*S) row-major fp32, host or device. */
+mp_status mp_layer_set_router(mp_layer_t h, const float* w_r);
+/* Proxy router gate set of expert e (inc/gating.hpp:19-43) in CSR form:
+ * ids[offsets[s] .. offsets[s+1]) are the ascending gate neurons of s. */
+mp_status mp_layer_set_gates(mp_layer_t h, uint32_t e, uint32_t r, const uint32_t* offsets, const uint32_t* ids);
+
+/* Layer forward on device buffers.  x, y: T x d_model of desc.dtype.
+ * k_per_token (device, nullable): per-token active count, each in
+ * [1, k_max]; when NULL every token uses k.  Optional device outputs:
+ * sel_out T x k_max (ascending ids, MP_SEL_NONE padded), w_out T x k_max
+ * combine weights, offsets_out E*S+1 bucket offsets. */
+mp_status mp_layer_forward(mp_layer_t h, const void* x, uint32_t n_tokens, const uint32_t* k_per_token, uint32_t k,
+                           void* y, uint32_t* sel_out, float* w_out, uint32_t* offsets_out, void* stream);
+
+/* Same, on HOST buffers (pinned or pageable): copies x (and k_per_token) in,
+ * runs, copies y (and the optional outputs) out, synchronises the stream. */
+mp_status mp_layer_forward_host(mp_layer_t h, const void* x, uint32_t n_tokens, const uint32_t* k_per_token,
+                                uint32_t k, void* y, uint32_t* sel_out, float* w_out, uint32_t* offsets_out,
+                                void* stream);
+
+/* Forward with an explicit selection (device, T x k_max, ascending global
+ * sub-expert ids e*S+s, MP_SEL_NONE padded; duplicates rejected on the
+ * host path).  w (device, nullable): per-slot weights; NULL = unit weights,
+ * i.e. partitioned_forward semantics summed over experts. */
+mp_status mp_layer_forward_selected(mp_layer_t h, const void* x, uint32_t n_tokens, const uint32_t* sel,
+                                    const float* w, void* y, uint32_t* offsets_out, void* stream);
+
+/* Router only: selection + weights (device outputs, T x k_max). */
+mp_status mp_layer_route(mp_layer_t h, const void* x, uint32_t n_tokens, const uint32_t* k_per_token, uint32_t k,
+                         uint32_t* sel_out, float* w_out, void* stream);
+
+/* Device-side validation flags raised by forwards on device buffers (k out of
+ * range, duplicate / out-of-range selection, non-finite input): synchronises
+ * `stream`, returns 1 with the message if any were raised, then clears them.
+ * (mp_layer_forward_host checks them itself.) */
+mp_status mp_layer_check_errors(mp_layer_t h, void* stream);
+
+/* Per-stage device timing with CUDA events on the forward's stream.
+ * names: comma-separated stage list; ms/launches: per stage accumulated
+ * since the last reset.  Returns the number of stages in *n. */
+mp_status mp_layer_set_profiling(mp_layer_t h, int on);
+mp_status mp_layer_stage_times(mp_layer_t h, char* names, size_t names_len, double* ms, uint64_t* launches,
+                               uint32_t* n, uint32_t cap);
+mp_status mp_layer_reset_stage_times(mp_layer_t h);
+/* Kernels launched by this handle since creation. */
+uint64_t mp_layer_launch_count(mp_layer_t h);
+
+/* Counter-based synthetic data (the generator of oracle/moe_oracle.c
+ * orc_synth_fill, bit-identical): dst[j] = dtype(float((u*2-1)*scale)),
+ * u = stream(seed) element first+j.  Device dst. */
+mp_status mp_synth_fill(void* dst, uint32_t dtype, size_t n, uint64_t seed, uint64_t first, double scale,
+                        void* stream);
+
+/* Host-only readers (no GPU touched), format-compatible with the reference.
+ * mp_format_read_mpex <- load_toy_expert (inc/io.hpp:225-251): call with
+ * null weight pointers to learn the dims, then with d_model*d_ff buffers.
+ * mp_format_read_partition_doc <- read_ndjson + partition_doc_from_json +
+ * gate_set_from_json (inc/serde.hpp:113-168): document `index`; null output
+ * pointers are skipped (two-phase like the MPEX reader).
+ * mp_validate_partition <- validate(Partition) (inc/partition.hpp:34-46). */
+mp_status mp_format_read_mpex(const char* path, uint32_t* d_model, uint32_t* d_ff, float* w_gate, float* w_up,
+                              float* w_down);
+mp_status mp_format_read_partition_doc(const char* path, size_t index, size_t* n_docs, uint64_t* expert_id,
+                                       uint32_t* n_sub, size_t* n, uint32_t* assignment, uint32_t* r,
+                                       size_t* n_gate_ids, uint32_t* gate_offsets, uint32_t* gate_ids);
+mp_status mp_validate_partition(uint32_t n_sub, const uint32_t* assignment, size_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOEPRISM_MOE_LAYER_H */

@@ -1,0 +1,277 @@
+// gemm_tc.cu -- grouped GEMMs of the sub-expert SwiGLU FFN on the 5th-gen
+// tensor cores (tcgen05.mma, accumulators in TMEM, operands staged by TMA).
+//
+//   gemm1 (SWIGLU=true):  H[r][n*128 + c] = silu(acc[r][c]) * acc[r][128 + c]
+//       A = x_perm (rows x d_pad), B = W1[g] rows n*256 .. n*256+255
+//       (128 gate rows then the 128 up rows of the same neurons, packed by
+//       pack.cu), so one 128x256 TMEM accumulator holds both halves of the
+//       SwiGLU for 128 neurons and the activation is fused in the epilogue.
+//   gemm2 (SWIGLU=false): O[r][n*256 + c] = acc[r][c]
+//       A = H (rows x w_pad), B = W2[g] (d_pad x w_pad).
+// Variable-size groups: sub-expert g owns rows [offsets[g], offsets[g+1])
+// (written by the bucket scan on the device); tiles are enumerated (g, n, m)
+// from the device prefix of ceil(count_g / 128) by a persistent grid of one
+// CTA per SM, m fastest so the CTAs sharing one weight tile run together and
+// the tile is fetched from HBM once.  Rows of a partial M tile that belong to
+// the next group are computed and discarded (masked stores).
+//
+// Warp roles (192 threads): warp 0 = TMA producer (one elected lane),
+// warp 1 = TMEM allocator + MMA issuer (one lane), warps 2..5 = epilogue
+// (TMEM lane quarter = warp % 4).  Pipelines: 4-stage smem ring (full /
+// empty mbarriers, tcgen05.commit frees a stage), 2 TMEM accumulators of 256
+// columns (tmem_full / tmem_empty) so the epilogue of tile i overlaps the
+// MMAs of tile i+1.
+#include <cstdio>
+
+#include "mp_common.cuh"
+#include "mp_kernels.h"
+
+namespace mp {
+
+namespace {
+
+constexpr uint32_t BM = kTcBM;  // 128
+constexpr uint32_t BN = 256;
+constexpr uint32_t BK = 64;  // one 128-byte swizzle row of bf16
+constexpr uint32_t STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK * 2;
+constexpr uint32_t B_BYTES = BN * BK * 2;
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr uint32_t kThreads = 192;
+constexpr uint32_t kTmemCols = 512;
+constexpr size_t kSmemBytes = 1024 + STAGES * STAGE_BYTES + 256;
+
+struct TcParams {
+    uint32_t G, K, N_group, n_valid, ld_out, NT;
+    const uint32_t* offsets;
+    const uint32_t* mprefix;
+    __nv_bfloat16* out;
+};
+
+__device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix, uint32_t G, uint32_t NT,
+                                         uint32_t& g, uint32_t& m, uint32_t& n) {
+    uint32_t lo = 0, hi = G;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_prefix[mid] * NT <= tile)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    g = lo - 1;
+    const uint32_t local = tile - s_prefix[g] * NT;
+    const uint32_t mt = s_prefix[g + 1] - s_prefix[g];
+    n = local / mt;
+    m = local - n * mt;
+}
+
+template <bool SWIGLU>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint32_t s_prefix[kMaxG + 1];
+    __shared__ uint32_t s_off[kMaxG + 1];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = base;
+    uint8_t* sB = base + STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = threadIdx.x / 32;
+    const uint32_t lane = threadIdx.x % 32;
+
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (uint32_t a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+    }
+    if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+    for (uint32_t q = threadIdx.x; q <= p.G; q += kThreads) {
+        s_prefix[q] = p.mprefix[q];
+        s_off[q] = p.offsets[q];
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t total = s_prefix[p.G] * p.NT;
+    const uint32_t nkb = p.K / BK;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+                uint32_t g, m, n;
+                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM);
+                const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN);
+                for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
+                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    mbar_expect_tx(&full[s], STAGE_BYTES);
+                    tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], static_cast<int32_t>(kb * BK), arow);
+                    tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+            uint32_t it = 0, tc = 0;
+            for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+                const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+                mbar_wait(&tempty[acc], aph ^ 1u);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
+                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + s * A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+                    for (uint32_t k = 0; k < BK / 16; ++k)
+                        umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                                  (kb | k) != 0u);
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[acc]);
+            }
+        }
+        __syncwarp();
+    } else {
+        const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
+        uint32_t tc = 0;
+        for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+            uint32_t g, m, n;
+            map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+            const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            const uint32_t row_local = m * BM + q * 32 + lane;
+            const bool valid = row_local < s_off[g + 1] - s_off[g];
+            __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN;
+            if constexpr (SWIGLU) {
+#pragma unroll 1
+                for (uint32_t c = 0; c < 4; ++c) {
+                    uint32_t gr[32], ur[32];
+                    tmem_ld32(taddr + c * 32, gr);
+                    tmem_ld32(taddr + 128 + c * 32, ur);
+                    tmem_ld_wait();
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float g0 = __uint_as_float(gr[2 * i]), g1 = __uint_as_float(gr[2 * i + 1]);
+                        const float u0 = __uint_as_float(ur[2 * i]), u1 = __uint_as_float(ur[2 * i + 1]);
+                        pk[i] = pack_bf16x2(silu_f32(g0) * u0, silu_f32(g1) * u1);
+                    }
+                    if (valid) {
+                        __nv_bfloat16* dst = orow + n * 128 + c * 32;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+                            st_global_v4(dst + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (uint32_t c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(taddr + c * 32, r);
+                    tmem_ld_wait();
+                    const uint32_t col = n * BN + c * 32;
+                    if (valid && col < p.n_valid) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+                        __nv_bfloat16* dst = orow + col;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+                            st_global_v4(dst + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<kTmemCols>(tmem_base);
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+}  // namespace
+
+size_t gemm_tc_smem_bytes() { return kSmemBytes; }
+
+bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                       uint32_t box_cols) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return false;
+    const cuuint64_t gdim[2] = {cols, rows};
+    const cuuint64_t gstride[1] = {cols * 2};
+    const cuuint32_t box[2] = {box_cols, box_rows};
+    const cuuint32_t estride[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estride,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
+                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s) {
+    TcParams p;
+    p.G = sh.G;
+    p.K = sh.K;
+    p.N_group = sh.N_group;
+    p.n_valid = sh.n_valid;
+    p.ld_out = sh.ld_out;
+    p.NT = (sh.N_group + BN - 1) / BN;
+    p.offsets = offsets;
+    p.mprefix = mprefix;
+    p.out = static_cast<__nv_bfloat16*>(out);
+    // upper bound on tiles; the kernel reads the exact count from the device
+    const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
+    const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
+    if (swiglu) {
+        cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+    } else {
+        cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        gemm_tc_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+    }
+}
+
+}  // namespace mp

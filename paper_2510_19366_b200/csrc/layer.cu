@@ -1,0 +1,791 @@
+// layer.cu -- the C-ABI (include/moeprism/moe_layer.h): layer state, weight
+// loading + packing, and the stream-ordered forward that chains the kernels
+//   router -> bucket (histogram) -> bucket (scan) -> dispatch -> gemm1
+//   (SwiGLU) -> gemm2 -> combine.
+// Everything runs on the GPU; a missing / non-sm_100 device is a status-3
+// error, never a CPU fallback.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "moeprism/moe_layer.h"
+#include "mp_kernels.h"
+#include "mp_layer_impl.h"
+
+#define MP_API extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Err {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Err{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(MP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ck_launch(const char* what) { ck(cudaGetLastError(), what); }
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return MP_OK;
+    } catch (const Err& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const mp::Failure& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host out of memory";
+        return MP_ERR_CUDA;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) ck(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <class T>
+T* dalloc(size_t n, const char* what) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    ck(cudaMalloc(&p, n * sizeof(T)), what);
+    return static_cast<T*>(p);
+}
+
+uint32_t round_up(uint32_t v, uint32_t m) { return (v + m - 1) / m * m; }
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+const char* kStageNames[] = {"router", "bucket", "dispatch", "gemm1", "gemm2", "combine"};
+constexpr int kStages = 6;
+
+}  // namespace
+
+struct mp_layer_s {
+    mp_layer_desc desc{};
+    uint32_t E = 0, S = 0, G = 0, d = 0, ff = 0, dtype = 0, k_max = 0, max_tokens = 0;
+    uint32_t w_pad = 0, d_pad = 0, G_pad = 0, rows_cap = 0, w2_rows = 0;
+    size_t esz = 4;
+    int num_sms = 0;
+    bool use_tc = false;
+
+    std::vector<std::vector<uint32_t>> assignment;
+    std::vector<uint8_t> has_part, packed;
+    std::vector<float*> raw;  // staged fp32 MPEX weights (wg | wu | wd) until packed
+    bool router_set = false;
+
+    // proxy router state
+    std::vector<uint32_t> gate_r;
+    std::vector<std::vector<std::vector<uint32_t>>> gates;  // [e][s] -> neurons
+    std::vector<uint8_t> has_gates;
+    float* gate_rows = nullptr;  // [n_gate][d] w_gate columns of the gate neurons
+    float* up_rows = nullptr;
+    uint32_t* gate_off = nullptr;  // [G+1] CSR over the gate rows
+    uint32_t n_gate_rows = 0;
+    bool gates_packed = false;
+    double* scores = nullptr;  // [max_tokens][G]
+
+    void* W1 = nullptr;
+    void* W2 = nullptr;
+    float* wrT = nullptr;
+    int32_t* d_nmap = nullptr;
+
+    uint32_t* sel = nullptr;
+    float* wsel = nullptr;
+    uint32_t* kpt_dev = nullptr;
+    mp::BucketWs ws{};
+    void* x_perm = nullptr;
+    void* h = nullptr;
+    void* o = nullptr;
+    void* x_stage = nullptr;
+    void* y_stage = nullptr;
+    CUtensorMap tm_xperm{}, tm_h{}, tm_w1{}, tm_w2{};
+
+    bool profiling = false;
+    cudaEvent_t ev[kStages + 1] = {};
+    double stage_ms[kStages] = {};
+    uint64_t stage_launches[kStages] = {};
+    uint64_t launches = 0;
+};
+
+namespace {
+
+void free_layer(mp_layer_s* L) {
+    for (float* p : L->raw)
+        if (p) cudaFree(p);
+    void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->d_nmap, L->sel,
+                    L->wsel, L->kpt_dev, L->ws.lrank, L->ws.block_counts, L->ws.block_base, L->ws.offsets,
+                    L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
+                    L->x_perm, L->h, L->o, L->x_stage, L->y_stage};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (auto& e : L->ev)
+        if (e) cudaEventDestroy(e);
+    delete L;
+}
+
+// Gathers sub-expert members (ascending, inc/partition.hpp:49-55) and packs
+// expert e once both its weights and its partition are known.
+void maybe_pack(mp_layer_s* L, uint32_t e) {
+    if (L->packed[e] || !L->has_part[e] || !L->raw[e]) return;
+    std::vector<int32_t> nmap(static_cast<size_t>(L->S) * L->w_pad, -1);
+    std::vector<uint32_t> fill(L->S, 0);
+    const auto& a = L->assignment[e];
+    for (uint32_t j = 0; j < L->ff; ++j) {
+        const uint32_t s = a[j];
+        nmap[static_cast<size_t>(s) * L->w_pad + fill[s]++] = static_cast<int32_t>(j);
+    }
+    ck(cudaMemcpy(L->d_nmap, nmap.data(), nmap.size() * sizeof(int32_t), cudaMemcpyHostToDevice), "nmap upload");
+    const size_t n = static_cast<size_t>(L->d) * L->ff;
+    const float* wg = L->raw[e];
+    const float* wu = wg + n;
+    const float* wd = wu + n;
+    char* W1e = static_cast<char*>(L->W1) + static_cast<size_t>(e) * L->S * 2 * L->w_pad * L->d_pad * L->esz;
+    char* W2e = static_cast<char*>(L->W2) + static_cast<size_t>(e) * L->S * L->d_pad * L->w_pad * L->esz;
+    mp::launch_pack_w1(L->dtype, wg, wu, L->d, L->ff, L->d_nmap, L->S, L->w_pad, L->d_pad, W1e, 0);
+    ck_launch("pack_w1");
+    mp::launch_pack_w2(L->dtype, wd, L->d, L->ff, L->d_nmap, L->S, L->w_pad, L->d_pad, W2e, 0);
+    ck_launch("pack_w2");
+    ck(cudaDeviceSynchronize(), "pack");
+    // proxy gate rows need the raw columns: keep raw only while gates are pending
+    if (L->desc.router_mode != MP_ROUTER_PROXY) {
+        cudaFree(L->raw[e]);
+        L->raw[e] = nullptr;
+    }
+    L->packed[e] = 1;
+    L->gates_packed = false;
+}
+
+void pack_gates(mp_layer_s* L) {
+    if (L->gates_packed) return;
+    for (uint32_t e = 0; e < L->E; ++e) {
+        if (!L->has_gates[e]) fail(MP_ERR_VALIDATION, "proxy router: expert " + std::to_string(e) + " has no gate set");
+        if (!L->raw[e]) fail(MP_ERR_VALIDATION, "proxy router: expert " + std::to_string(e) + " weights not loaded");
+    }
+    std::vector<uint32_t> off(L->G + 1, 0);
+    for (uint32_t e = 0; e < L->E; ++e)
+        for (uint32_t s = 0; s < L->S; ++s) off[e * L->S + s + 1] = off[e * L->S + s] + L->gates[e][s].size();
+    L->n_gate_rows = off[L->G];
+    if (L->scores) cudaFree(L->scores);
+    // [T][G] double scores followed by the [T][n_gate_rows] |activation| scratch
+    L->scores = reinterpret_cast<double*>(
+        dalloc<char>((size_t)L->max_tokens * (L->G * sizeof(double) + L->n_gate_rows * sizeof(float)), "scores"));
+    if (L->gate_rows) cudaFree(L->gate_rows);
+    if (L->up_rows) cudaFree(L->up_rows);
+    L->gate_rows = dalloc<float>(static_cast<size_t>(L->n_gate_rows) * L->d, "gate rows");
+    L->up_rows = dalloc<float>(static_cast<size_t>(L->n_gate_rows) * L->d, "up rows");
+    ck(cudaMemcpy(L->gate_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice), "gate offsets");
+    uint32_t* d_neur = dalloc<uint32_t>(L->n_gate_rows, "gate neuron ids");
+    for (uint32_t e = 0; e < L->E; ++e) {
+        std::vector<uint32_t> neur;
+        for (uint32_t s = 0; s < L->S; ++s)
+            for (uint32_t j : L->gates[e][s]) neur.push_back(j);
+        if (neur.empty()) continue;
+        ck(cudaMemcpy(d_neur, neur.data(), neur.size() * 4, cudaMemcpyHostToDevice), "gate neurons");
+        const size_t n = static_cast<size_t>(L->d) * L->ff;
+        const size_t row0 = off[e * L->S];
+        mp::launch_pack_gate_rows(L->raw[e], L->raw[e] + n, L->d, L->ff, d_neur, static_cast<uint32_t>(neur.size()),
+                                  L->gate_rows + row0 * L->d, L->up_rows + row0 * L->d, 0);
+        ck_launch("pack_gate_rows");
+        ck(cudaDeviceSynchronize(), "pack gates");
+    }
+    cudaFree(d_neur);
+    L->gates_packed = true;
+}
+
+void check_ready(mp_layer_s* L) {
+    for (uint32_t e = 0; e < L->E; ++e)
+        if (!L->packed[e])
+            fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " is not ready (weights and partition required)");
+}
+
+struct StageTimer {
+    mp_layer_s* L;
+    cudaStream_t s;
+    int cur = -1;
+    StageTimer(mp_layer_s* l, cudaStream_t st) : L(l), s(st) {}
+    void begin(int stage) {
+        if (!L->profiling) return;
+        if (cur < 0) cudaEventRecord(L->ev[0], s);
+        cur = stage;
+    }
+    void end(int stage, int n_launch) {
+        L->launches += n_launch;
+        if (!L->profiling) return;
+        L->stage_launches[stage] += n_launch;
+        cudaEventRecord(L->ev[stage + 1], s);
+    }
+    void finish(const int* order, int n) {
+        if (!L->profiling || cur < 0) return;
+        cudaEventSynchronize(L->ev[order[n - 1] + 1]);
+        cudaEvent_t prev = L->ev[0];
+        for (int q = 0; q < n; ++q) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, prev, L->ev[order[q] + 1]);
+            L->stage_ms[order[q]] += ms;
+            prev = L->ev[order[q] + 1];
+        }
+    }
+};
+
+// bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
+void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, void* y,
+                 cudaStream_t s, StageTimer& tm) {
+    tm.begin(1);
+    mp::launch_bucket_local(sel, T, L->k_max, L->G, L->ws, s);
+    mp::launch_bucket_scan(T, L->G, L->ws, s);
+    ck_launch("bucket");
+    tm.end(1, 2);
+    tm.begin(2);
+    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, L->x_perm, s);
+    ck_launch("dispatch");
+    tm.end(2, 1);
+    mp::GemmShape g1{L->G, L->d_pad, 2 * L->w_pad, T * L->k_max, L->w_pad, 2 * L->w_pad};
+    mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
+    tm.begin(3);
+    if (L->use_tc)
+        mp::launch_gemm_tc(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
+    else
+        mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
+    ck_launch("gemm1");
+    tm.end(3, 1);
+    tm.begin(4);
+    if (L->use_tc)
+        mp::launch_gemm_tc(false, &L->tm_h, &L->tm_w2, L->o, g2, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
+    else
+        mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
+    ck_launch("gemm2");
+    tm.end(4, 1);
+    tm.begin(5);
+    mp::launch_combine(L->dtype, L->o, L->d, L->d_pad, L->ws.slot_row, w, L->k_max, T, y, s);
+    ck_launch("combine");
+    tm.end(5, 1);
+}
+
+void route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32_t k, cudaStream_t s,
+           StageTimer& tm) {
+    if (!kpt && (k < 1 || k > L->k_max || k > L->G))
+        fail(MP_ERR_VALIDATION, "k_active = " + std::to_string(k) + " out of range [1, " +
+                                    std::to_string(std::min(L->k_max, L->G)) + "]");
+    tm.begin(0);
+    if (L->desc.router_mode == MP_ROUTER_PROXY) {
+        pack_gates(L);
+        mp::launch_proxy_scores(L->dtype, x, T, L->d, L->gate_rows, L->up_rows, L->gate_off, L->n_gate_rows, L->G,
+                                reinterpret_cast<float*>(L->scores), s);
+        mp::launch_router_scores_topk(reinterpret_cast<const float*>(L->scores), T, L->G, L->k_max, kpt, k,
+                                      L->desc.weight_mode, L->sel, L->wsel, L->ws.err, s);
+        ck_launch("router(proxy)");
+        tm.end(0, 2);
+    } else {
+        if (!L->router_set) fail(MP_ERR_VALIDATION, "router weights not set (mp_layer_set_router)");
+        mp::launch_router_linear(L->dtype, x, T, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode, L->sel,
+                                 L->wsel, L->ws.err, s);
+        ck_launch("router");
+        tm.end(0, 1);
+    }
+}
+
+void copy_outputs(mp_layer_s* L, uint32_t T, uint32_t* sel_out, float* w_out, uint32_t* off_out, cudaStream_t s,
+                  cudaMemcpyKind kind) {
+    if (sel_out) ck(cudaMemcpyAsync(sel_out, L->sel, (size_t)T * L->k_max * 4, kind, s), "sel_out");
+    if (w_out) ck(cudaMemcpyAsync(w_out, L->wsel, (size_t)T * L->k_max * 4, kind, s), "w_out");
+    if (off_out) ck(cudaMemcpyAsync(off_out, L->ws.offsets, (size_t)(L->G + 1) * 4, kind, s), "offsets_out");
+}
+
+void check_tokens(mp_layer_s* L, uint32_t T) {
+    if (T > L->max_tokens)
+        fail(MP_ERR_VALIDATION,
+             "n_tokens " + std::to_string(T) + " exceeds max_tokens " + std::to_string(L->max_tokens));
+}
+
+void raise_device_errors(int flags) {
+    if (flags & 2) fail(MP_ERR_VALIDATION, "input vector is not finite");
+    if (flags & 1) fail(MP_ERR_VALIDATION, "selection out of range or duplicated (k_active / active sub-expert)");
+}
+
+}  // namespace
+
+// ============================================================== C-ABI
+
+MP_API const char* mp_version(void) { return "moeprism-b200 0.1 (sm_100a)"; }
+MP_API const char* mp_last_error(void) { return g_err.c_str(); }
+
+MP_API mp_status mp_device_check(int32_t dev) {
+    return guarded([&] {
+        int n = 0;
+        ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (dev < 0 || dev >= n) fail(MP_ERR_CUDA, "no CUDA device " + std::to_string(dev));
+        cudaDeviceProp p;
+        ck(cudaGetDeviceProperties(&p, dev), "cudaGetDeviceProperties");
+        if (p.major != 10 || p.minor != 0)
+            fail(MP_ERR_CUDA, std::string("device ") + p.name + " is sm_" + std::to_string(p.major) +
+                                  std::to_string(p.minor) + "; this library carries sm_100a code only");
+    });
+}
+
+MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
+    return guarded([&] {
+        if (!desc || !out) fail(MP_ERR_VALIDATION, "null argument");
+        const mp_layer_desc& D = *desc;
+        if (D.n_experts < 1 || D.n_subexperts < 1) fail(MP_ERR_VALIDATION, "need n_experts >= 1 and n_subexperts >= 1");
+        if (D.d_model < 1 || D.d_ff < 1) fail(MP_ERR_VALIDATION, "toy expert needs d_model >= 1 and d_ff >= 1");
+        if (D.d_ff < D.n_subexperts) fail(MP_ERR_VALIDATION, "partition needs at least as many neurons as sub-experts");
+        const uint64_t G = (uint64_t)D.n_experts * D.n_subexperts;
+        if (G > mp::kMaxG) fail(MP_ERR_VALIDATION, "E*S = " + std::to_string(G) + " exceeds " + std::to_string(mp::kMaxG));
+        if (D.k_max < 1 || D.k_max > G || D.k_max > 64)
+            fail(MP_ERR_VALIDATION, "k_max must be in [1, min(E*S, 64)]");
+        if (D.dtype != MP_DTYPE_F32 && D.dtype != MP_DTYPE_BF16) fail(MP_ERR_VALIDATION, "unknown dtype");
+        if (D.router_mode > MP_ROUTER_PROXY || D.weight_mode > MP_WEIGHT_SOFTMAX_RENORM)
+            fail(MP_ERR_VALIDATION, "unknown router / weight mode");
+        if (D.max_tokens < 1) fail(MP_ERR_VALIDATION, "max_tokens must be >= 1");
+        {
+            int rc = mp_device_check(D.device);
+            if (rc) fail(rc, g_err);
+        }
+        DeviceGuard dg(D.device);
+        auto* L = new mp_layer_s;
+        try {
+            L->desc = D;
+            L->E = D.n_experts;
+            L->S = D.n_subexperts;
+            L->G = static_cast<uint32_t>(G);
+            L->d = D.d_model;
+            L->ff = D.d_ff;
+            L->dtype = D.dtype;
+            L->k_max = D.k_max;
+            L->max_tokens = D.max_tokens;
+            L->esz = D.dtype == MP_DTYPE_BF16 ? 2 : 4;
+            L->use_tc = D.dtype == MP_DTYPE_BF16;
+            if (const char* env = std::getenv("MOEPRISM_BF16_GEMM"))
+                if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
+            const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
+            L->w_pad = round_up(w_sub, 128);
+            L->d_pad = round_up(L->d, 64);
+            L->G_pad = round_up(L->G, 64);
+            L->rows_cap = round_up(std::max<uint32_t>(L->max_tokens * L->k_max, 1), 128);
+            L->w2_rows = round_up(L->G * L->d_pad, 256);
+            int dev = D.device;
+            ck(cudaDeviceGetAttribute(&L->num_sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+            L->assignment.resize(L->E);
+            L->has_part.assign(L->E, 0);
+            L->packed.assign(L->E, 0);
+            L->raw.assign(L->E, nullptr);
+            L->gate_r.assign(L->E, 0);
+            L->gates.resize(L->E);
+            L->has_gates.assign(L->E, 0);
+            const size_t w1 = (size_t)L->G * 2 * L->w_pad * L->d_pad;
+            const size_t w2 = (size_t)L->w2_rows * L->w_pad;
+            L->W1 = dalloc<char>(w1 * L->esz, "W1");
+            L->W2 = dalloc<char>(w2 * L->esz, "W2");
+            ck(cudaMemset(L->W2, 0, w2 * L->esz), "memset W2");
+            L->wrT = dalloc<float>((size_t)L->G_pad * L->d, "router");
+            L->d_nmap = dalloc<int32_t>((size_t)L->S * L->w_pad, "nmap");
+            const size_t tk = (size_t)L->max_tokens * L->k_max;
+            const uint32_t nblk = (L->max_tokens + mp::kRouteTokensPerBlock - 1) / mp::kRouteTokensPerBlock;
+            L->sel = dalloc<uint32_t>(tk, "sel");
+            L->wsel = dalloc<float>(tk, "w");
+            L->kpt_dev = dalloc<uint32_t>(L->max_tokens, "k per token");
+            L->ws.lrank = dalloc<uint32_t>(tk, "lrank");
+            L->ws.block_counts = dalloc<uint32_t>((size_t)nblk * L->G, "block counts");
+            L->ws.block_base = dalloc<uint32_t>((size_t)nblk * L->G, "block base");
+            L->ws.offsets = dalloc<uint32_t>(L->G + 1, "offsets");
+            L->ws.mprefix_tc = dalloc<uint32_t>(L->G + 1, "mprefix");
+            L->ws.mprefix_simt = dalloc<uint32_t>(L->G + 1, "mprefix");
+            L->ws.perm_tok = dalloc<uint32_t>(L->rows_cap, "perm");
+            L->ws.perm_w = dalloc<float>(L->rows_cap, "perm w");
+            L->ws.slot_row = dalloc<uint32_t>(tk, "slot row");
+            L->ws.err = dalloc<int>(1, "err");
+            ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset err");
+            L->x_perm = dalloc<char>((size_t)L->rows_cap * L->d_pad * L->esz, "x_perm");
+            L->h = dalloc<char>((size_t)L->rows_cap * L->w_pad * L->esz, "h");
+            L->o = dalloc<char>((size_t)L->rows_cap * L->d_pad * L->esz, "o");
+            L->x_stage = dalloc<char>((size_t)L->max_tokens * L->d * L->esz, "x stage");
+            L->y_stage = dalloc<char>((size_t)L->max_tokens * L->d * L->esz, "y stage");
+            if (D.router_mode == MP_ROUTER_PROXY) L->gate_off = dalloc<uint32_t>(L->G + 1, "gate offsets");
+            if (L->use_tc) {
+                bool ok = mp::make_tmap_bf16_2d(&L->tm_xperm, L->x_perm, L->rows_cap, L->d_pad, 128, 64) &&
+                          mp::make_tmap_bf16_2d(&L->tm_w1, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 256, 64) &&
+                          mp::make_tmap_bf16_2d(&L->tm_h, L->h, L->rows_cap, L->w_pad, 128, 64) &&
+                          mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64);
+                if (!ok) fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+            }
+            for (auto& e : L->ev) ck(cudaEventCreate(&e), "event");
+        } catch (...) {
+            free_layer(L);
+            throw;
+        }
+        *out = L;
+    });
+}
+
+MP_API mp_status mp_layer_destroy(mp_layer_t h) {
+    return guarded([&] {
+        if (!h) return;
+        DeviceGuard dg(h->desc.device);
+        cudaDeviceSynchronize();
+        free_layer(h);
+    });
+}
+
+MP_API mp_status mp_layer_get_desc(mp_layer_t h, mp_layer_desc* out) {
+    return guarded([&] {
+        if (!h || !out) fail(MP_ERR_VALIDATION, "null argument");
+        *out = h->desc;
+    });
+}
+
+MP_API mp_status mp_layer_load_expert(mp_layer_t L, uint32_t e, const float* wg, const float* wu, const float* wd) {
+    return guarded([&] {
+        if (!L || !wg || !wu || !wd) fail(MP_ERR_VALIDATION, "null argument");
+        if (e >= L->E) fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " out of range");
+        DeviceGuard dg(L->desc.device);
+        const size_t n = (size_t)L->d * L->ff;
+        if (!L->raw[e]) L->raw[e] = dalloc<float>(3 * n, "expert staging");
+        float* dst = L->raw[e];
+        const float* srcs[3] = {wg, wu, wd};
+        for (int m = 0; m < 3; ++m)
+            ck(cudaMemcpy(dst + m * n, srcs[m], n * sizeof(float), cudaMemcpyDefault), "expert upload");
+        // validate(ToyExpert): every weight finite (inc/expert.hpp:34-37)
+        ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset");
+        mp::launch_finite_check(dst, 3 * n, L->ws.err, 0);
+        ck_launch("finite check");
+        int flag = 0;
+        ck(cudaMemcpy(&flag, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+        if (flag) {
+            cudaFree(L->raw[e]);
+            L->raw[e] = nullptr;
+            fail(MP_ERR_VALIDATION, "toy expert weight is not finite");
+        }
+        L->packed[e] = 0;
+        maybe_pack(L, e);
+    });
+}
+
+MP_API mp_status mp_layer_load_expert_file(mp_layer_t L, uint32_t e, const char* path) {
+    return guarded([&] {
+        if (!L || !path) fail(MP_ERR_VALIDATION, "null argument");
+        mp::MpexData m = mp::read_mpex(path);
+        if (m.d_model != L->d || m.d_ff != L->ff)
+            fail(MP_ERR_VALIDATION, std::string(path) + " holds a " + std::to_string(m.d_model) + "x" +
+                                        std::to_string(m.d_ff) + " expert; the layer expects " +
+                                        std::to_string(L->d) + "x" + std::to_string(L->ff));
+        int rc = mp_layer_load_expert(L, e, m.w_gate.data(), m.w_up.data(), m.w_down.data());
+        if (rc) fail(rc, g_err);
+    });
+}
+
+MP_API mp_status mp_layer_set_partition(mp_layer_t L, uint32_t e, uint32_t n_sub, const uint32_t* a, size_t n) {
+    return guarded([&] {
+        if (!L || !a) fail(MP_ERR_VALIDATION, "null argument");
+        if (e >= L->E) fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " out of range");
+        mp::validate_partition(n_sub, a, n);
+        if (n_sub != L->S)
+            fail(MP_ERR_VALIDATION, "partition has " + std::to_string(n_sub) + " sub-experts; the layer expects " +
+                                        std::to_string(L->S));
+        if (n != L->ff)
+            fail(MP_ERR_VALIDATION, "partition covers " + std::to_string(n) + " neurons but the expert has d_ff " +
+                                        std::to_string(L->ff));
+        DeviceGuard dg(L->desc.device);
+        if (L->packed[e] && !L->raw[e])
+            fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) +
+                                        " is already packed; reload its weights to change the partition");
+        L->assignment[e].assign(a, a + n);
+        L->has_part[e] = 1;
+        L->packed[e] = 0;
+        maybe_pack(L, e);
+    });
+}
+
+MP_API mp_status mp_layer_load_partition_map(mp_layer_t L, const char* path) {
+    return guarded([&] {
+        if (!L || !path) fail(MP_ERR_VALIDATION, "null argument");
+        auto docs = mp::read_partition_map(path);
+        for (const auto& d : docs) {
+            if (d.expert_id >= L->E)
+                fail(MP_ERR_VALIDATION, "partition map expert_id " + std::to_string(d.expert_id) + " out of range");
+            int rc = mp_layer_set_partition(L, static_cast<uint32_t>(d.expert_id), d.n_subexperts,
+                                            d.assignment.data(), d.assignment.size());
+            if (rc) fail(rc, g_err);
+            if (d.has_gates) {
+                std::vector<uint32_t> off(1, 0), ids;
+                for (const auto& l : d.gates) {
+                    ids.insert(ids.end(), l.begin(), l.end());
+                    off.push_back(static_cast<uint32_t>(ids.size()));
+                }
+                rc = mp_layer_set_gates(L, static_cast<uint32_t>(d.expert_id), d.r, off.data(), ids.data());
+                if (rc) fail(rc, g_err);
+            }
+        }
+    });
+}
+
+MP_API mp_status mp_layer_set_router(mp_layer_t L, const float* w_r) {
+    return guarded([&] {
+        if (!L || !w_r) fail(MP_ERR_VALIDATION, "null argument");
+        DeviceGuard dg(L->desc.device);
+        const size_t n = (size_t)L->d * L->G;
+        float* tmp = dalloc<float>(n, "router staging");
+        cudaError_t e1 = cudaMemcpy(tmp, w_r, n * sizeof(float), cudaMemcpyDefault);
+        if (e1 != cudaSuccess) {
+            cudaFree(tmp);
+            ck(e1, "router upload");
+        }
+        ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset");
+        mp::launch_finite_check(tmp, n, L->ws.err, 0);
+        mp::launch_transpose_router(tmp, L->d, L->G, L->G_pad, L->wrT, 0);
+        ck_launch("router transpose");
+        int flag = 0;
+        ck(cudaMemcpy(&flag, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+        cudaFree(tmp);
+        if (flag) fail(MP_ERR_VALIDATION, "router weight is not finite");
+        L->router_set = true;
+    });
+}
+
+MP_API mp_status mp_layer_set_gates(mp_layer_t L, uint32_t e, uint32_t r, const uint32_t* off, const uint32_t* ids) {
+    return guarded([&] {
+        if (!L || !off || !ids) fail(MP_ERR_VALIDATION, "null argument");
+        if (e >= L->E) fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " out of range");
+        // validate(GateSet), inc/gating.hpp:33-43
+        if (r < 1) fail(MP_ERR_VALIDATION, "gate set shape is inconsistent");
+        std::vector<std::vector<uint32_t>> g(L->S);
+        for (uint32_t s = 0; s < L->S; ++s) {
+            if (off[s + 1] <= off[s]) fail(MP_ERR_VALIDATION, "every sub-expert needs at least one gate neuron");
+            g[s].assign(ids + off[s], ids + off[s + 1]);
+            for (size_t q = 0; q < g[s].size(); ++q) {
+                if (q && g[s][q] < g[s][q - 1]) fail(MP_ERR_VALIDATION, "gate neuron lists must be ascending");
+                if (g[s][q] >= L->ff)
+                    fail(MP_ERR_VALIDATION, "gate neuron " + std::to_string(g[s][q]) + " out of range for d_ff " +
+                                                std::to_string(L->ff));
+            }
+        }
+        L->gates[e] = std::move(g);
+        L->gate_r[e] = r;
+        L->has_gates[e] = 1;
+        L->gates_packed = false;
+    });
+}
+
+MP_API mp_status mp_layer_forward(mp_layer_t L, const void* x, uint32_t T, const uint32_t* kpt, uint32_t k, void* y,
+                                  uint32_t* sel_out, float* w_out, uint32_t* offsets_out, void* stream) {
+    return guarded([&] {
+        if (!L || (T && (!x || !y))) fail(MP_ERR_VALIDATION, "null argument");
+        check_tokens(L, T);
+        check_ready(L);
+        if (T == 0) return;
+        DeviceGuard dg(L->desc.device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        StageTimer tm(L, s);
+        route(L, x, T, kpt, k, s, tm);
+        run_experts(L, x, T, L->sel, L->wsel, y, s, tm);
+        copy_outputs(L, T, sel_out, w_out, offsets_out, s, cudaMemcpyDeviceToDevice);
+        static const int order[] = {0, 1, 2, 3, 4, 5};
+        tm.finish(order, 6);
+    });
+}
+
+MP_API mp_status mp_layer_forward_host(mp_layer_t L, const void* x, uint32_t T, const uint32_t* kpt, uint32_t k,
+                                       void* y, uint32_t* sel_out, float* w_out, uint32_t* offsets_out, void* stream) {
+    return guarded([&] {
+        if (!L || (T && (!x || !y))) fail(MP_ERR_VALIDATION, "null argument");
+        check_tokens(L, T);
+        check_ready(L);
+        if (T == 0) return;
+        if (kpt)
+            for (uint32_t t = 0; t < T; ++t)
+                if (kpt[t] < 1 || kpt[t] > L->k_max || kpt[t] > L->G)
+                    fail(MP_ERR_VALIDATION, "k_active = " + std::to_string(kpt[t]) + " out of range [1, " +
+                                                std::to_string(std::min(L->k_max, L->G)) + "]");
+        DeviceGuard dg(L->desc.device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t xbytes = (size_t)T * L->d * L->esz;
+        ck(cudaMemsetAsync(L->ws.err, 0, sizeof(int), s), "memset err");
+        ck(cudaMemcpyAsync(L->x_stage, x, xbytes, cudaMemcpyHostToDevice, s), "x upload");
+        const uint32_t* kd = nullptr;
+        if (kpt) {
+            ck(cudaMemcpyAsync(L->kpt_dev, kpt, (size_t)T * 4, cudaMemcpyHostToDevice, s), "k upload");
+            kd = L->kpt_dev;
+        }
+        StageTimer tm(L, s);
+        route(L, L->x_stage, T, kd, k, s, tm);
+        run_experts(L, L->x_stage, T, L->sel, L->wsel, L->y_stage, s, tm);
+        ck(cudaMemcpyAsync(y, L->y_stage, xbytes, cudaMemcpyDeviceToHost, s), "y download");
+        copy_outputs(L, T, sel_out, w_out, offsets_out, s, cudaMemcpyDeviceToHost);
+        int flags = 0;
+        ck(cudaMemcpyAsync(&flags, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost, s), "flags");
+        ck(cudaStreamSynchronize(s), "forward");
+        static const int order[] = {0, 1, 2, 3, 4, 5};
+        tm.finish(order, 6);
+        raise_device_errors(flags);
+    });
+}
+
+MP_API mp_status mp_layer_forward_selected(mp_layer_t L, const void* x, uint32_t T, const uint32_t* sel,
+                                           const float* w, void* y, uint32_t* offsets_out, void* stream) {
+    return guarded([&] {
+        if (!L || (T && (!x || !y || !sel))) fail(MP_ERR_VALIDATION, "null argument");
+        check_tokens(L, T);
+        check_ready(L);
+        if (T == 0) return;
+        DeviceGuard dg(L->desc.device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        StageTimer tm(L, s);
+        run_experts(L, x, T, sel, w, y, s, tm);
+        if (offsets_out)
+            ck(cudaMemcpyAsync(offsets_out, L->ws.offsets, (size_t)(L->G + 1) * 4, cudaMemcpyDeviceToDevice, s),
+               "offsets_out");
+        static const int order[] = {1, 2, 3, 4, 5};
+        tm.finish(order, 5);
+    });
+}
+
+MP_API mp_status mp_layer_route(mp_layer_t L, const void* x, uint32_t T, const uint32_t* kpt, uint32_t k,
+                                uint32_t* sel_out, float* w_out, void* stream) {
+    return guarded([&] {
+        if (!L || (T && (!x || !sel_out || !w_out))) fail(MP_ERR_VALIDATION, "null argument");
+        check_tokens(L, T);
+        if (T == 0) return;
+        DeviceGuard dg(L->desc.device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        StageTimer tm(L, s);
+        route(L, x, T, kpt, k, s, tm);
+        copy_outputs(L, T, sel_out, w_out, nullptr, s, cudaMemcpyDeviceToDevice);
+        static const int order[] = {0};
+        tm.finish(order, 1);
+    });
+}
+
+MP_API mp_status mp_layer_check_errors(mp_layer_t L, void* stream) {
+    return guarded([&] {
+        if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        DeviceGuard dg(L->desc.device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        int flags = 0;
+        ck(cudaMemcpyAsync(&flags, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost, s), "flags");
+        ck(cudaStreamSynchronize(s), "sync");
+        ck(cudaMemsetAsync(L->ws.err, 0, sizeof(int), s), "memset err");
+        raise_device_errors(flags);
+    });
+}
+
+MP_API mp_status mp_layer_set_profiling(mp_layer_t L, int on) {
+    return guarded([&] {
+        if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        L->profiling = on != 0;
+    });
+}
+
+MP_API mp_status mp_layer_stage_times(mp_layer_t L, char* names, size_t names_len, double* ms, uint64_t* launches,
+                                      uint32_t* n, uint32_t cap) {
+    return guarded([&] {
+        if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        std::string all;
+        for (int q = 0; q < kStages; ++q) {
+            if (q) all += ",";
+            all += kStageNames[q];
+            if (ms && (uint32_t)q < cap) ms[q] = L->stage_ms[q];
+            if (launches && (uint32_t)q < cap) launches[q] = L->stage_launches[q];
+        }
+        if (names && names_len) {
+            std::strncpy(names, all.c_str(), names_len - 1);
+            names[names_len - 1] = 0;
+        }
+        if (n) *n = kStages;
+    });
+}
+
+MP_API mp_status mp_layer_reset_stage_times(mp_layer_t L) {
+    return guarded([&] {
+        if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        for (int q = 0; q < kStages; ++q) L->stage_ms[q] = 0, L->stage_launches[q] = 0;
+    });
+}
+
+MP_API uint64_t mp_layer_launch_count(mp_layer_t L) { return L ? L->launches : 0; }
+
+MP_API mp_status mp_synth_fill(void* dst, uint32_t dtype, size_t n, uint64_t seed, uint64_t first, double scale,
+                               void* stream) {
+    return guarded([&] {
+        if (!dst) fail(MP_ERR_VALIDATION, "null argument");
+        if (dtype != MP_DTYPE_F32 && dtype != MP_DTYPE_BF16) fail(MP_ERR_VALIDATION, "unknown dtype");
+        if (!is_device_ptr(dst)) fail(MP_ERR_VALIDATION, "mp_synth_fill needs a device pointer");
+        mp::launch_synth_fill(dst, (int)dtype, n, seed, first, scale, static_cast<cudaStream_t>(stream));
+        ck_launch("synth fill");
+    });
+}
+
+// ---- host-only format readers (no GPU needed) ----
+
+MP_API mp_status mp_format_read_mpex(const char* path, uint32_t* d_model, uint32_t* d_ff, float* w_gate, float* w_up,
+                                     float* w_down) {
+    return guarded([&] {
+        if (!path || !d_model || !d_ff) fail(MP_ERR_VALIDATION, "null argument");
+        mp::MpexData m = mp::read_mpex(path);
+        *d_model = m.d_model;
+        *d_ff = m.d_ff;
+        const size_t n = (size_t)m.d_model * m.d_ff;
+        if (w_gate) std::memcpy(w_gate, m.w_gate.data(), n * 4);
+        if (w_up) std::memcpy(w_up, m.w_up.data(), n * 4);
+        if (w_down) std::memcpy(w_down, m.w_down.data(), n * 4);
+    });
+}
+
+MP_API mp_status mp_format_read_partition_doc(const char* path, size_t index, size_t* n_docs, uint64_t* expert_id,
+                                              uint32_t* n_sub, size_t* n, uint32_t* assignment, uint32_t* r,
+                                              size_t* n_gate_ids, uint32_t* gate_offsets, uint32_t* gate_ids) {
+    return guarded([&] {
+        if (!path || !n_docs) fail(MP_ERR_VALIDATION, "null argument");
+        auto docs = mp::read_partition_map(path);
+        *n_docs = docs.size();
+        if (index >= docs.size()) fail(MP_ERR_VALIDATION, "document index out of range");
+        const auto& d = docs[index];
+        if (expert_id) *expert_id = d.expert_id;
+        if (n_sub) *n_sub = d.n_subexperts;
+        if (n) *n = d.assignment.size();
+        if (assignment) std::memcpy(assignment, d.assignment.data(), d.assignment.size() * 4);
+        if (r) *r = d.has_gates ? d.r : 0;
+        size_t tot = 0;
+        if (d.has_gates) {
+            if (gate_offsets) gate_offsets[0] = 0;
+            for (size_t s = 0; s < d.gates.size(); ++s) {
+                if (gate_ids) std::memcpy(gate_ids + tot, d.gates[s].data(), d.gates[s].size() * 4);
+                tot += d.gates[s].size();
+                if (gate_offsets) gate_offsets[s + 1] = static_cast<uint32_t>(tot);
+            }
+        }
+        if (n_gate_ids) *n_gate_ids = tot;
+    });
+}
+
+MP_API mp_status mp_validate_partition(uint32_t n_sub, const uint32_t* a, size_t n) {
+    return guarded([&] {
+        if (!a && n) fail(MP_ERR_VALIDATION, "null argument");
+        mp::validate_partition(n_sub, a, n);
+    });
+}

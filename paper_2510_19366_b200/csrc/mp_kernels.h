@@ -1,0 +1,77 @@
+// mp_kernels.h -- host-side launchers for the sm_100a kernels (internal).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace mp {
+
+constexpr uint32_t kRouteTokensPerBlock = 32;  // tokens per router / bucket CTA
+constexpr uint32_t kTcBM = 128;                // tcgen05 grouped GEMM tile M
+constexpr uint32_t kSimtBM = 64;               // SIMT grouped GEMM tile M
+constexpr uint32_t kMaxG = 256;                // max E*S sub-experts (Qwen: 240)
+
+// Device scratch for the bucketing of one forward.
+struct BucketWs {
+    uint32_t* lrank;         // [T][k_max] rank inside (block, bucket)
+    uint32_t* block_counts;  // [nblk][G]
+    uint32_t* block_base;    // [nblk][G]
+    uint32_t* offsets;       // [G+1]
+    uint32_t* mprefix_tc;    // [G+1] prefix of ceil(count/128)
+    uint32_t* mprefix_simt;  // [G+1] prefix of ceil(count/64)
+    uint32_t* perm_tok;      // [rows]
+    float* perm_w;           // [rows]
+    uint32_t* slot_row;      // [T][k_max]
+    int* err;                // device error flags (bit 0: bad k / selection, bit 1: non-finite x)
+};
+
+// dtype: 0 f32, 1 bf16
+void launch_router_linear(int dtype, const void* x, uint32_t T, uint32_t d, const float* wrT, uint32_t G,
+                          uint32_t k_max, const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
+                          int* err, cudaStream_t s);
+void launch_router_scores_topk(const float* scores, uint32_t T, uint32_t G, uint32_t k_max, const uint32_t* kpt,
+                               uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err, cudaStream_t s);
+void launch_proxy_scores(int dtype, const void* x, uint32_t T, uint32_t d, const float* gate_w, const float* up_w,
+                         const uint32_t* gate_off, uint32_t n_gate_rows, uint32_t G, float* scores, cudaStream_t s);
+void launch_bucket_local(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32_t G, BucketWs& ws,
+                         cudaStream_t s);
+void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s);
+void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t d_pad, const uint32_t* sel,
+                     const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s);
+void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row, const float* w,
+                    uint32_t k_max, uint32_t T, void* y, cudaStream_t s);
+
+// Packing (load time).
+void launch_pack_w1(int dtype, const float* wg, const float* wu, uint32_t d, uint32_t ff, const int32_t* nmap,
+                    uint32_t S, uint32_t w_pad, uint32_t d_pad, void* W1_e, cudaStream_t s);
+void launch_pack_w2(int dtype, const float* wd, uint32_t d, uint32_t ff, const int32_t* nmap, uint32_t S,
+                    uint32_t w_pad, uint32_t d_pad, void* W2_e, cudaStream_t s);
+void launch_transpose_router(const float* wr, uint32_t d, uint32_t G, uint32_t G_pad, float* wrT, cudaStream_t s);
+void launch_pack_gate_rows(const float* wg, const float* wu, uint32_t d, uint32_t ff, const uint32_t* neurons,
+                           uint32_t n, float* gate_rows, float* up_rows, cudaStream_t s);
+void launch_finite_check(const float* p, size_t n, int* flag, cudaStream_t s);
+void launch_synth_fill(void* dst, int dtype, size_t n, uint64_t seed, uint64_t first, double scale, cudaStream_t s);
+
+// Grouped GEMMs.  Rows of group g live at [offsets[g], offsets[g+1]) of the
+// permuted row space; weights of group g at W + g * (rows per group).
+struct GemmShape {
+    uint32_t G, K, N_group;  // per group: N_group output rows of W (gate/up interleaved for gemm1)
+    uint32_t max_rows;       // row capacity of A / out
+    uint32_t ld_out;         // elements per output row
+    uint32_t n_valid;        // columns < n_valid are stored (gemm2: d_pad) -- gemm1 stores all
+};
+void launch_gemm1_simt(int dtype, const void* A, const void* W1, void* H, const GemmShape& sh,
+                       const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
+void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const GemmShape& sh,
+                       const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
+void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
+                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s);
+size_t gemm_tc_smem_bytes();
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point.
+bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                       uint32_t box_cols);
+
+}  // namespace mp

@@ -1,0 +1,494 @@
+// route.cu -- router (linear fp32 logits + elastic per-token top-k +
+// softmax renormalisation), bucketing (warp-level histogram + prefix scan +
+// stable scatter), token dispatch (permute/gather) and the weighted combine.
+//
+// Reference anchors: select_topk_subexperts inc/gating.hpp:129-145 (total
+// order score desc / index asc, ascending output); the linear router and
+// softmax renormalisation are the SURVEY 8(c) restatement;
+// bucketing / combine are SURVEY 8(a) a14/a15.  All HBM-bound: coalesced
+// 16-byte vector accesses, no atomics, fixed reduction orders (deterministic).
+#include <cfloat>
+#include <cmath>
+
+#include "mp_common.cuh"
+#include "mp_kernels.h"
+
+namespace mp {
+
+namespace {
+
+constexpr uint32_t TB = kRouteTokensPerBlock;  // tokens per CTA
+constexpr uint32_t GB = 64;                    // router outputs per pass
+constexpr uint32_t KC = 32;                    // K chunk staged in smem
+constexpr uint32_t kRouterThreads = 256;
+
+// ---------------------------------------------------------------- top-k
+// One warp selects the k_t best of G scores for one token (score desc,
+// index asc -- inc/gating.hpp:138-141), emits them in ascending index order
+// (inc/gating.hpp:143) with their softmax-renormalised weights.
+__device__ void warp_topk_token(const double* __restrict__ sc, uint32_t G, uint32_t k, uint32_t k_max,
+                                int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row) {
+    const uint32_t lane = lane_id();
+    constexpr int NC = kMaxG / 32;
+    const uint32_t nc = (G + 31) / 32;
+    double v[NC];
+    uint32_t taken = 0;  // bit c: value c of this lane selected
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const uint32_t g = lane + 32u * c;
+        v[c] = (c < (int)nc && g < G) ? sc[g] : -DBL_MAX;
+    }
+    double vmax = 0.0;
+    for (uint32_t r = 0; r < k; ++r) {
+        double bv = -INFINITY;
+        uint32_t bi = 0xFFFFFFFFu;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const uint32_t g = lane + 32u * c;
+            if (c < (int)nc && g < G && !((taken >> c) & 1u) && v[c] > bv) {
+                bv = v[c];
+                bi = g;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+            const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (ov > bv || (ov == bv && oi < bi)) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if (r == 0) vmax = bv;
+        if (bi != 0xFFFFFFFFu && (bi & 31u) == lane) taken |= 1u << (bi >> 5);
+    }
+    // softmax over all G cancels in the renormalisation: w_g = e^(l_g - m) / sum_sel
+    double z = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if ((taken >> c) & 1u) z += exp(v[c] - vmax);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
+    // ascending-index emission: index order is (c, lane)
+    uint32_t base = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (c >= (int)nc) break;
+        const bool mine = (taken >> c) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+        if (mine) {
+            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
+            sel_row[pos] = lane + 32u * c;
+            w_row[pos] = weight_mode == 1 ? static_cast<float>(exp(v[c] - vmax) / z) : 1.0f;
+        }
+        base += __popc(bal);
+    }
+    for (uint32_t j = k + lane; j < k_max; j += 32) {
+        sel_row[j] = kSelNone;
+        w_row[j] = 0.0f;
+    }
+}
+
+__device__ __forceinline__ uint32_t token_k(const uint32_t* kpt, uint32_t k, uint32_t t, uint32_t k_max, uint32_t G,
+                                            int* err) {
+    uint32_t kt = kpt ? kpt[t] : k;
+    if (kt < 1 || kt > k_max || kt > G) {
+        if (err) atomicOr(err, 1);
+        kt = kt < 1 ? 1 : (kt > k_max ? k_max : kt);
+        if (kt > G) kt = G;
+    }
+    return kt;
+}
+
+// ---------------------------------------------------------------- linear router
+// logits[t][g] = sum_i x[t][i] * W_r[i][g].  fp32 FFMA partials over 16
+// consecutive i (products exact inside the FMA), accumulated in fp64 in
+// ascending i: |error| ~1e-7, well under the 1e-6 near-tie window of the
+// bit-exact routing contract.  CTA: 32 tokens x all G.
+template <typename Tx>
+__global__ void __launch_bounds__(kRouterThreads) router_linear_kernel(
+    const Tx* __restrict__ x, uint32_t T, uint32_t d, const float* __restrict__ wrT, uint32_t G, uint32_t k_max,
+    const uint32_t* __restrict__ kpt, uint32_t k_scalar, int weight_mode, uint32_t* __restrict__ sel,
+    float* __restrict__ wout, int* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* lg = reinterpret_cast<double*>(smem_raw);                 // [TB][G]
+    float* xs = reinterpret_cast<float*>(lg + TB * G);                // [KC][TB+1]
+    float* ws = xs + KC * (TB + 1);                                   // [KC][GB+4]
+    const uint32_t tid = threadIdx.x;
+    const uint32_t t0 = blockIdx.x * TB;
+    const uint32_t tx = tid % 16, ty = tid / 16;  // 4 outputs (g) x 2 tokens per thread
+    bool nonfinite = false;
+
+    for (uint32_t g0 = 0; g0 < G; g0 += GB) {
+        double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        float part[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+        for (uint32_t k0 = 0; k0 < d; k0 += KC) {
+            __syncthreads();
+            for (uint32_t q = tid; q < TB * KC; q += kRouterThreads) {
+                const uint32_t t = q / KC, kk = q % KC;
+                float v = 0.0f;
+                if (t0 + t < T && k0 + kk < d) {
+                    v = to_f32(x[(size_t)(t0 + t) * d + k0 + kk]);
+                    if (g0 == 0 && !isfinite(v)) nonfinite = true;
+                }
+                xs[kk * (TB + 1) + t] = v;
+            }
+            for (uint32_t q = tid; q < GB * KC; q += kRouterThreads) {
+                const uint32_t g = q / KC, kk = q % KC;
+                float v = 0.0f;
+                if (g0 + g < G && k0 + kk < d) v = wrT[(size_t)(g0 + g) * d + k0 + kk];
+                ws[kk * (GB + 4) + g] = v;
+            }
+            __syncthreads();
+#pragma unroll
+            for (uint32_t kk = 0; kk < KC; ++kk) {
+                const float xa = xs[kk * (TB + 1) + 2 * ty];
+                const float xb = xs[kk * (TB + 1) + 2 * ty + 1];
+                const float4 wv = *reinterpret_cast<const float4*>(&ws[kk * (GB + 4) + 4 * tx]);
+                part[0][0] = fmaf(xa, wv.x, part[0][0]);
+                part[0][1] = fmaf(xa, wv.y, part[0][1]);
+                part[0][2] = fmaf(xa, wv.z, part[0][2]);
+                part[0][3] = fmaf(xa, wv.w, part[0][3]);
+                part[1][0] = fmaf(xb, wv.x, part[1][0]);
+                part[1][1] = fmaf(xb, wv.y, part[1][1]);
+                part[1][2] = fmaf(xb, wv.z, part[1][2]);
+                part[1][3] = fmaf(xb, wv.w, part[1][3]);
+                if ((kk & 15u) == 15u) {
+#pragma unroll
+                    for (int a = 0; a < 2; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            acc[a][b] += static_cast<double>(part[a][b]);
+                            part[a][b] = 0.0f;
+                        }
+                }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t g = g0 + 4 * tx + b;
+                if (g < G) lg[(2 * ty + a) * G + g] = acc[a][b];
+            }
+    }
+    if (nonfinite && err) atomicOr(err, 2);
+    __syncthreads();
+    const uint32_t warp = tid / 32;
+    for (uint32_t t = warp; t < TB; t += kRouterThreads / 32) {
+        const uint32_t tg = t0 + t;
+        if (tg >= T) break;
+        const uint32_t kt = token_k(kpt, k_scalar, tg, k_max, G, err);
+        warp_topk_token(lg + t * G, G, kt, k_max, weight_mode, sel + (size_t)tg * k_max, wout + (size_t)tg * k_max);
+    }
+}
+
+// Top-k over precomputed double scores [T][G] (proxy router).
+__global__ void __launch_bounds__(256) scores_topk_kernel(const double* __restrict__ scores, uint32_t T, uint32_t G,
+                                                          uint32_t k_max, const uint32_t* __restrict__ kpt,
+                                                          uint32_t k_scalar, int weight_mode,
+                                                          uint32_t* __restrict__ sel, float* __restrict__ wout,
+                                                          int* __restrict__ err) {
+    const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32;
+    if (t >= T) return;
+    const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
+    warp_topk_token(scores + (size_t)t * G, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
+                    wout + (size_t)t * k_max);
+}
+
+// ---------------------------------------------------------------- bucketing
+// Per CTA of 32 tokens: selection bitmasks in smem, then one thread per
+// sub-expert walks the tokens in order -> rank of each (t, slot) inside its
+// (CTA, bucket) and the CTA's histogram.  Stable by construction.
+__global__ void __launch_bounds__(256) bucket_local_kernel(const uint32_t* __restrict__ sel, uint32_t T,
+                                                           uint32_t k_max, uint32_t G, uint32_t* __restrict__ lrank,
+                                                           uint32_t* __restrict__ block_counts,
+                                                           int* __restrict__ err) {
+    __shared__ uint32_t msk[TB][kMaxG / 32];
+    __shared__ uint16_t slot_of[TB][kMaxG];  // slot index of g in token t (valid where selected)
+    const uint32_t t0 = blockIdx.x * TB;
+    const uint32_t words = (G + 31) / 32;
+    for (uint32_t q = threadIdx.x; q < TB * words; q += blockDim.x) msk[q / words][q % words] = 0;
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < TB * k_max; q += blockDim.x) {
+        const uint32_t t = q / k_max, j = q % k_max;
+        if (t0 + t >= T) continue;
+        const uint32_t g = sel[(size_t)(t0 + t) * k_max + j];
+        if (g == kSelNone) continue;
+        if (g >= G) {
+            atomicOr(err, 1);
+            continue;
+        }
+        const uint32_t old = atomicOr(&msk[t][g >> 5], 1u << (g & 31));
+        if (old & (1u << (g & 31))) atomicOr(err, 1);  // duplicate (inc/expert.hpp:117)
+        slot_of[t][g] = static_cast<uint16_t>(j);
+    }
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) {
+        uint32_t cnt = 0;
+        for (uint32_t t = 0; t < TB && t0 + t < T; ++t) {
+            if ((msk[t][g >> 5] >> (g & 31)) & 1u) lrank[(size_t)(t0 + t) * k_max + slot_of[t][g]] = cnt++;
+        }
+        block_counts[(size_t)blockIdx.x * G + g] = cnt;
+    }
+}
+
+// Exclusive scans: over CTAs per bucket (-> block_base), over buckets
+// (-> offsets), and the GEMM tile prefixes.  One CTA of 1024 threads.
+__device__ uint32_t block_exclusive_scan_1024(uint32_t v, uint32_t* total, uint32_t* wsum) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t n = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= (uint32_t)off) inc += n;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t s = wsum[lane];
+        uint32_t si = s;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t n = __shfl_up_sync(0xffffffffu, si, off);
+            if (lane >= (uint32_t)off) si += n;
+        }
+        wsum[lane] = si - s;
+        if (lane == 31) *total = si;
+    }
+    __syncthreads();
+    const uint32_t r = wsum[warp] + inc - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32_t G,
+                                                           const uint32_t* __restrict__ block_counts,
+                                                           uint32_t* __restrict__ block_base,
+                                                           uint32_t* __restrict__ offsets,
+                                                           uint32_t* __restrict__ mprefix_tc,
+                                                           uint32_t* __restrict__ mprefix_simt) {
+    __shared__ uint32_t totals[1024];
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t tot;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t g = warp; g < G; g += 32) {
+        uint32_t running = 0;
+        for (uint32_t b0 = 0; b0 < nblk; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            const uint32_t v = b < nblk ? block_counts[(size_t)b * G + g] : 0;
+            uint32_t inc = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t n = __shfl_up_sync(0xffffffffu, inc, off);
+                if (lane >= (uint32_t)off) inc += n;
+            }
+            if (b < nblk) block_base[(size_t)b * G + g] = running + inc - v;
+            running += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) totals[g] = running;
+    }
+    __syncthreads();
+    const uint32_t g = threadIdx.x;
+    const uint32_t cnt = g < G ? totals[g] : 0;
+    const uint32_t off = block_exclusive_scan_1024(cnt, &tot, wsum);
+    if (g < G) offsets[g] = off;
+    if (g == 0) offsets[G] = tot;
+    const uint32_t mt = g < G ? (cnt + kTcBM - 1) / kTcBM : 0;
+    const uint32_t mpre = block_exclusive_scan_1024(mt, &tot, wsum);
+    if (g < G) mprefix_tc[g] = mpre;
+    if (g == 0) mprefix_tc[G] = tot;
+    const uint32_t ms = g < G ? (cnt + kSimtBM - 1) / kSimtBM : 0;
+    const uint32_t spre = block_exclusive_scan_1024(ms, &tot, wsum);
+    if (g < G) mprefix_simt[g] = spre;
+    if (g == 0) mprefix_simt[G] = tot;
+    __syncthreads();
+    if (g < G) totals[g] = off;
+    __syncthreads();
+    for (uint32_t gg = warp; gg < G; gg += 32)
+        for (uint32_t b = lane; b < nblk; b += 32) block_base[(size_t)b * G + gg] += totals[gg];
+}
+
+// ---------------------------------------------------------------- dispatch
+// Warp per token: position of each selected slot, permutation tables, and
+// the token's row copied (zero padded to d_pad) to every selected bucket.
+template <typename Tx>
+__global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x, uint32_t T, uint32_t d,
+                                                       uint32_t d_pad, const uint32_t* __restrict__ sel,
+                                                       const float* __restrict__ w, uint32_t k_max, uint32_t G,
+                                                       const uint32_t* __restrict__ lrank,
+                                                       const uint32_t* __restrict__ block_base,
+                                                       uint32_t* __restrict__ perm_tok, float* __restrict__ perm_w,
+                                                       uint32_t* __restrict__ slot_row, Tx* __restrict__ x_perm) {
+    const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32;
+    const uint32_t lane = threadIdx.x & 31;
+    if (t >= T) return;
+    const uint32_t blk = t / TB;
+    for (uint32_t j = lane; j < k_max; j += 32) {
+        const uint32_t g = sel[(size_t)t * k_max + j];
+        uint32_t pos = kSelNone;
+        if (g != kSelNone && g < G) {
+            pos = block_base[(size_t)blk * G + g] + lrank[(size_t)t * k_max + j];
+            perm_tok[pos] = t;
+            perm_w[pos] = w ? w[(size_t)t * k_max + j] : 1.0f;
+        }
+        slot_row[(size_t)t * k_max + j] = pos;
+    }
+    __syncwarp();
+    constexpr uint32_t VE = 16 / sizeof(Tx);  // elements per 16-byte vector
+    const bool vec_ok = (d % VE) == 0;
+    const Tx* xr = x + (size_t)t * d;
+    for (uint32_t j = 0; j < k_max; ++j) {
+        const uint32_t pos = slot_row[(size_t)t * k_max + j];
+        if (pos == kSelNone) continue;
+        Tx* dst = x_perm + (size_t)pos * d_pad;
+        if (vec_ok) {
+            for (uint32_t c = lane * VE; c < d_pad; c += 32 * VE) {
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (c < d) v = __ldg(reinterpret_cast<const uint4*>(xr + c));
+                *reinterpret_cast<uint4*>(dst + c) = v;
+            }
+        } else {
+            for (uint32_t c = lane; c < d_pad; c += 32) dst[c] = c < d ? xr[c] : from_f32<Tx>(0.0f);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- combine
+// y[t] = sum_{j ascending} w[t][j] * o[slot_row[t][j]]  (fp32 accumulate,
+// fixed order = ascending sub-expert id).  CTA per token,
+// 8 columns (one 16-byte bf16 vector) per thread per step.
+template <typename Tx>
+__global__ void __launch_bounds__(256) combine_kernel(const Tx* __restrict__ o, uint32_t d, uint32_t d_pad,
+                                                      const uint32_t* __restrict__ slot_row,
+                                                      const float* __restrict__ w, uint32_t k_max, uint32_t T,
+                                                      Tx* __restrict__ y) {
+    __shared__ uint32_t rows[64];
+    __shared__ float wts[64];
+    const uint32_t t = blockIdx.x;
+    for (uint32_t j = threadIdx.x; j < k_max; j += blockDim.x) {
+        rows[j] = slot_row[(size_t)t * k_max + j];
+        wts[j] = w ? w[(size_t)t * k_max + j] : 1.0f;
+    }
+    __syncthreads();
+    Tx* yr = y + (size_t)t * d;
+    constexpr uint32_t VE = 8;
+    if ((d % VE) == 0 && (d_pad % VE) == 0) {
+        for (uint32_t c = threadIdx.x * VE; c < d; c += blockDim.x * VE) {
+            float acc[VE];
+#pragma unroll
+            for (int q = 0; q < (int)VE; ++q) acc[q] = 0.0f;
+            for (uint32_t j = 0; j < k_max; ++j) {
+                const uint32_t r = rows[j];
+                if (r == kSelNone) continue;
+                const float wj = wts[j];
+                const Tx* src = o + (size_t)r * d_pad + c;
+                if constexpr (sizeof(Tx) == 2) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
+                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 f = __bfloat1622float2(h[q]);
+                        acc[2 * q] = fmaf(wj, f.x, acc[2 * q]);
+                        acc[2 * q + 1] = fmaf(wj, f.y, acc[2 * q + 1]);
+                    }
+                } else {
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(src + 4));
+                    acc[0] = fmaf(wj, a.x, acc[0]);
+                    acc[1] = fmaf(wj, a.y, acc[1]);
+                    acc[2] = fmaf(wj, a.z, acc[2]);
+                    acc[3] = fmaf(wj, a.w, acc[3]);
+                    acc[4] = fmaf(wj, b.x, acc[4]);
+                    acc[5] = fmaf(wj, b.y, acc[5]);
+                    acc[6] = fmaf(wj, b.z, acc[6]);
+                    acc[7] = fmaf(wj, b.w, acc[7]);
+                }
+            }
+            if constexpr (sizeof(Tx) == 2) {
+                uint4 out;
+                out.x = pack_bf16x2(acc[0], acc[1]);
+                out.y = pack_bf16x2(acc[2], acc[3]);
+                out.z = pack_bf16x2(acc[4], acc[5]);
+                out.w = pack_bf16x2(acc[6], acc[7]);
+                *reinterpret_cast<uint4*>(yr + c) = out;
+            } else {
+                *reinterpret_cast<float4*>(yr + c) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                *reinterpret_cast<float4*>(yr + c + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+            }
+        }
+    } else {
+        for (uint32_t c = threadIdx.x; c < d; c += blockDim.x) {
+            float acc = 0.0f;
+            for (uint32_t j = 0; j < k_max; ++j) {
+                const uint32_t r = rows[j];
+                if (r == kSelNone) continue;
+                acc = fmaf(wts[j], to_f32(o[(size_t)r * d_pad + c]), acc);
+            }
+            yr[c] = from_f32<Tx>(acc);
+        }
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+
+void launch_router_linear(int dtype, const void* x, uint32_t T, uint32_t d, const float* wrT, uint32_t G,
+                          uint32_t k_max, const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
+                          int* err, cudaStream_t s) {
+    const size_t smem = sizeof(double) * TB * G + sizeof(float) * (KC * (TB + 1) + KC * (GB + 4));
+    const dim3 grid((T + TB - 1) / TB);
+    if (dtype == 1) {
+        auto kern = router_linear_kernel<__nv_bfloat16>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, kRouterThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, d, wrT, G, k_max, kpt, k,
+                                                weight_mode, sel, w, err);
+    } else {
+        auto kern = router_linear_kernel<float>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, kRouterThreads, smem, s>>>(static_cast<const float*>(x), T, d, wrT, G, k_max, kpt, k,
+                                                weight_mode, sel, w, err);
+    }
+}
+
+void launch_router_scores_topk(const float* scores, uint32_t T, uint32_t G, uint32_t k_max, const uint32_t* kpt,
+                               uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err, cudaStream_t s) {
+    scores_topk_kernel<<<(T + 7) / 8, 256, 0, s>>>(reinterpret_cast<const double*>(scores), T, G, k_max, kpt, k,
+                                                   weight_mode, sel, w, err);
+}
+
+void launch_bucket_local(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32_t G, BucketWs& ws,
+                         cudaStream_t s) {
+    bucket_local_kernel<<<(T + TB - 1) / TB, 256, 0, s>>>(sel, T, k_max, G, ws.lrank, ws.block_counts, ws.err);
+}
+
+void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s) {
+    bucket_scan_kernel<<<1, 1024, 0, s>>>((T + TB - 1) / TB, G, ws.block_counts, ws.block_base, ws.offsets,
+                                          ws.mprefix_tc, ws.mprefix_simt);
+}
+
+void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t d_pad, const uint32_t* sel,
+                     const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s) {
+    const dim3 grid((T + 7) / 8);
+    if (dtype == 1)
+        dispatch_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(x), T, d, d_pad, sel, w, k_max, G, ws.lrank, ws.block_base,
+            ws.perm_tok, ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm));
+    else
+        dispatch_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), T, d, d_pad, sel, w, k_max, G,
+                                                    ws.lrank, ws.block_base, ws.perm_tok, ws.perm_w, ws.slot_row,
+                                                    static_cast<float*>(x_perm));
+}
+
+void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row, const float* w,
+                    uint32_t k_max, uint32_t T, void* y, cudaStream_t s) {
+    if (dtype == 1)
+        combine_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(o), d, d_pad, slot_row, w,
+                                                        k_max, T, static_cast<__nv_bfloat16*>(y));
+    else
+        combine_kernel<float><<<T, 256, 0, s>>>(static_cast<const float*>(o), d, d_pad, slot_row, w, k_max, T,
+                                                static_cast<float*>(y));
+}
+
+}  // namespace mp

@@ -1,0 +1,60 @@
+"""Shared helpers for the GPU parity tests: build a layer and the matching
+oracle inputs from the same seeds."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+U32 = 0xFFFFFFFF
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round float32 to the nearest bfloat16 (ties to even), returned as float32."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def close_mask(got, want, tol):
+    """Reference tolerance form |got - want| <= tol * (1 + |want|) (tests/test_expert.cpp:16-18)."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    return np.abs(got - want) <= tol * (1.0 + np.abs(want))
+
+
+def toy_setup(oracle, E, S, d, ff, T, seed_x=11, seed_r=7, seed_w=5000, seed_p=6000, contiguous=False):
+    """Reference fixtures: random_expert weights (U(-1,1)), balanced partitions,
+    W_r = U(-1,1)/sqrt(d), x = U(-1,1) (SURVEY 8(d) C1 recipe)."""
+    experts = [oracle.random_expert(d, ff, seed_w + e) for e in range(E)]
+    parts = [oracle.contiguous_partition(ff, S) if contiguous else oracle.random_balanced_partition(ff, S, seed_p + e)
+             for e in range(E)]
+    wr = oracle.uniform_pm1(seed_r, d * E * S, 1.0 / math.sqrt(d))
+    x = oracle.uniform_pm1(seed_x, T * d).reshape(T, d)
+    return experts, parts, wr, x
+
+
+def make_layer(experts, parts, wr, S, dtype, weights="softmax_renorm", k_max=8, max_tokens=256, router="linear"):
+    from paper_2510_19366_b200 import MoeLayer
+    E = len(experts)
+    ff = parts[0].size
+    d = experts[0][0].size // ff
+    L = MoeLayer(E, S, d, ff, dtype=dtype, router=router, weights=weights, k_max=k_max, max_tokens=max_tokens)
+    for e in range(E):
+        L.set_partition(e, parts[e])
+        L.load_expert(e, *experts[e])
+    if wr is not None:
+        L.set_router(wr)
+    return L
+
+
+def routing_agreement(gpu_sel, ora_sel, gap, k_per_token, tie_eps=1e-6):
+    """Counts (mismatched tokens outside the near-tie window, near-tie tokens)."""
+    bad, ties = [], 0
+    for t in range(gpu_sel.shape[0]):
+        k = int(k_per_token[t])
+        near = gap[t] < tie_eps
+        ties += int(near)
+        if not np.array_equal(gpu_sel[t, :k], ora_sel[t, :k]) and not near:
+            bad.append(t)
+    return bad, ties

@@ -1,0 +1,336 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Contract (BASELINE north_star): selected sub-expert indices
+and bucket offsets bit-exact (tokens whose oracle k-th/(k+1)-th logit gap is
+< 1e-6 are counted separately); outputs within 1e-5 * (1 + |y|) in fp32 mode
+and 2e-2 * (1 + |y|) in bf16 mode (against the oracle run on bf16-rounded
+weights and inputs).
+"""
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from gpu_util import U32, bf16_round, close_mask, make_layer, routing_agreement, toy_setup
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+TOL_F32, TOL_BF16 = 1e-5, 2e-2
+
+
+@pytest.fixture(scope="module")
+def torch_cuda(cuda_lib):
+    import torch
+    return torch
+
+
+def _u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+# ------------------------------------------------------------ C1 toy (golden)
+
+@pytest.mark.parametrize("mode", ["softmax_renorm", "unit"])
+def test_c1_fp32_against_reference_golden(oracle, torch_cuda, mode):
+    torch = torch_cuda
+    E, S, d, ff, T, K = 8, 4, 512, 1024, 256, 4
+    g = np.load(GOLD / "c1_toy.npz")
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    L = make_layer(experts, parts, wr, S, "f32", weights=mode, k_max=K, max_tokens=T)
+    xd = torch.from_numpy(x).cuda()
+    y, sel, w, off = L.forward(xd, k=K, return_routing=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(_u32(sel), g["sel"])  # routing bit-exact (golden has no near ties)
+    assert np.array_equal(_u32(off), g["offsets"])
+    yh = y.cpu().numpy()
+    if mode == "softmax_renorm":
+        assert np.allclose(w.cpu().numpy(), g["w"], rtol=1e-6, atol=1e-7)
+        assert close_mask(yh, g["y_w"], TOL_F32).all()
+    else:
+        assert (w.cpu().numpy() == 1.0).all()
+        assert close_mask(yh[:64], g["y_u"], TOL_F32).all()
+
+
+def test_c1_bf16_tensor_core_path(oracle, torch_cuda):
+    torch = torch_cuda
+    E, S, d, ff, T, K = 8, 4, 512, 1024, 256, 4
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    L = make_layer(experts, parts, wr, S, "bf16", k_max=K, max_tokens=T)
+    xb = bf16_round(x)
+    xd = torch.from_numpy(xb).cuda().to(torch.bfloat16)
+    y, sel, w, off = L.forward(xd, k=K, return_routing=True)
+    logits = oracle.router_logits(xb, wr, T, d, E * S)
+    osel, ow, gap = oracle.route(logits, K, K, 1)
+    bad, ties = routing_agreement(_u32(sel), osel, gap, np.full(T, K))
+    assert not bad, f"routing mismatch outside near-ties: {bad[:5]}"
+    _, ooff, _, _ = oracle.bucket(_u32(sel), E * S)
+    assert np.array_equal(_u32(off), ooff)
+    ex_b = [tuple(bf16_round(a) for a in e) for e in experts]
+    yo = oracle.layer_forward(ex_b, parts, S, xb, _u32(sel), w.cpu().numpy(), 1)
+    yh = y.float().cpu().numpy()
+    ok = close_mask(yh, yo, TOL_BF16)
+    assert ok.all(), f"{(~ok).sum()} elements off; max rel {np.max(np.abs(yh - yo) / (1 + np.abs(yo))):.3g}"
+
+
+# ------------------------------------------------------------ Mixtral shape
+
+@pytest.mark.parametrize("k", [2, 4, 8, 16])
+def test_mixtral_layer_bf16_k_sweep(oracle, torch_cuda, k, mixtral):
+    torch = torch_cuda
+    L, x_dev, xb, wr, parts, ex_nm_b, logits = mixtral
+    E, S, d, ff, T = 8, 8, 4096, 14336, x_dev.shape[0]
+    y, sel, w, off = L.forward(x_dev, k=k, return_routing=True)
+    torch.cuda.synchronize()
+    osel, ow, gap = oracle.route(logits, k, L.k_max, 1)
+    gsel = _u32(sel)
+    bad, ties = routing_agreement(gsel, osel, gap, np.full(T, k))
+    print(f"k={k}: near-ties {ties}/{T}")
+    assert not bad, f"routing mismatch outside near-ties at tokens {bad[:5]}"
+    _, ooff, _, _ = oracle.bucket(gsel, E * S)
+    assert np.array_equal(_u32(off), ooff)
+    if ties == 0:
+        _, ooff2, _, _ = oracle.bucket(osel, E * S)
+        assert np.array_equal(_u32(off), ooff2)
+    # outputs on a fixed 32-token subsample
+    sub = np.linspace(0, T - 1, 32).astype(np.int64)
+    yo = oracle.layer_forward(ex_nm_b, parts, S, xb[sub], gsel[sub], w.cpu().numpy()[sub], 1, layout=1)
+    yh = y.float().cpu().numpy()[sub]
+    ok = close_mask(yh, yo, TOL_BF16)
+    assert ok.all(), f"{(~ok).sum()} off; max rel {np.max(np.abs(yh - yo) / (1 + np.abs(yo))):.3g}"
+
+
+@pytest.fixture(scope="module")
+def mixtral(oracle, torch_cuda):
+    """Mixtral-8x7B layer shape: W_gate/W_up U(-1,1)/sqrt(d),
+    W_down U(-1,1)/sqrt(ffn), W_r U(-1,1)/sqrt(d) fp32, x U(-1,1); counter-based
+    synthetic stream on both sides (bit-identical)."""
+    torch = torch_cuda
+    from paper_2510_19366_b200 import MoeLayer, synth_fill
+    E, S, d, ff, T = 8, 8, 4096, 14336, 4096
+    L = MoeLayer(E, S, d, ff, dtype="bf16", k_max=16, max_tokens=T)
+    parts = [oracle.random_balanced_partition(ff, S, 6000 + e) for e in range(E)]
+    ex_nm_b = []
+    buf = torch.empty(d * ff, dtype=torch.float32, device="cuda")
+    for e in range(E):
+        ws = []
+        for m, (seed, scale) in enumerate(((100 + 3 * e, 1 / math.sqrt(d)), (101 + 3 * e, 1 / math.sqrt(d)),
+                                           (102 + 3 * e, 1 / math.sqrt(ff)))):
+            t = torch.empty(d * ff, dtype=torch.float32, device="cuda")
+            synth_fill(t, seed, scale)
+            ws.append(t)
+        L.set_partition(e, parts[e])
+        L.load_expert(e, *ws)
+        # oracle side: neuron-major gate/up (same numbers, contiguous per neuron), bf16-rounded
+        wg = bf16_round(oracle.synth_t(100 + 3 * e, d, ff, 1 / math.sqrt(d)))
+        wu = bf16_round(oracle.synth_t(101 + 3 * e, d, ff, 1 / math.sqrt(d)))
+        wd = bf16_round(oracle.synth(102 + 3 * e, d * ff, 1 / math.sqrt(ff)))
+        if e == 0:  # the two generators agree bit for bit
+            assert np.array_equal(ws[2].cpu().numpy(), oracle.synth(102, d * ff, 1 / math.sqrt(ff)))
+        ex_nm_b.append((wg, wu, wd))
+        del ws
+    del buf
+    wr = oracle.synth(7, d * E * S, 1 / math.sqrt(d))
+    L.set_router(wr)
+    xt = torch.empty((T, d), dtype=torch.bfloat16, device="cuda")
+    synth_fill(xt, 11, 1.0)
+    xb = bf16_round(oracle.synth(11, T * d, 1.0)).reshape(T, d)
+    assert np.array_equal(xt.float().cpu().numpy(), xb)
+    logits = oracle.router_logits(xb, wr, T, d, E * S)
+    yield L, xt, xb, wr, parts, ex_nm_b, logits
+    L.close()
+
+
+# ------------------------------------------------------------ edge cases
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("T", [1, 31, 33, 100])
+def test_ragged_tokens_and_per_token_k(oracle, torch_cuda, dtype, T):
+    torch = torch_cuda
+    E, S, d, ff = 4, 4, 128, 256
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T, seed_x=T)
+    L = make_layer(experts, parts, wr, S, dtype, k_max=16, max_tokens=128)
+    rng = np.random.default_rng(T)
+    kpt = rng.integers(1, 17, T).astype(np.uint32)
+    xin = x if dtype == "f32" else bf16_round(x)
+    xd = torch.from_numpy(xin).cuda().to(L.torch_dtype)
+    y, sel, w, off = L.forward(xd, k_per_token=torch.from_numpy(kpt.astype(np.int32)), return_routing=True)
+    L.check_errors()
+    logits = oracle.router_logits(xin, wr, T, d, E * S)
+    osel, ow, gap = oracle.route(logits, 0, 16, 1, k_per_token=kpt)
+    bad, _ = routing_agreement(_u32(sel), osel, gap, kpt)
+    assert not bad
+    exs = experts if dtype == "f32" else [tuple(bf16_round(a) for a in e) for e in experts]
+    yo = oracle.layer_forward(exs, parts, S, xin, _u32(sel), w.cpu().numpy(), 1)
+    tol = TOL_F32 if dtype == "f32" else TOL_BF16
+    assert close_mask(y.float().cpu().numpy(), yo, tol).all()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_all_subexperts_and_k1(oracle, torch_cuda, dtype):
+    torch = torch_cuda
+    E, S, d, ff, T = 2, 8, 64, 128, 40
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    L = make_layer(experts, parts, wr, S, dtype, weights="unit", k_max=16, max_tokens=T)
+    xin = x if dtype == "f32" else bf16_round(x)
+    xd = torch.from_numpy(xin).cuda().to(L.torch_dtype)
+    exs = experts if dtype == "f32" else [tuple(bf16_round(a) for a in e) for e in experts]
+    tol = TOL_F32 if dtype == "f32" else TOL_BF16
+    for k in (1, 16):
+        y, sel, w, off = L.forward(xd, k=k, return_routing=True)
+        if k == 16:  # every sub-expert of every expert: the full toy_ffn_forward sum
+            assert (_u32(sel) == np.arange(16)).all()
+            for t in range(T):
+                want = sum(oracle.toy_ffn_forward(d, ff, *exs[e], xin[t])[0].astype(np.float64) for e in range(E))
+                assert close_mask(y[t].float().cpu().numpy(), want, tol).all()
+        yo = oracle.layer_forward(exs, parts, S, xin, _u32(sel), w.cpu().numpy(), 0)
+        assert close_mask(y.float().cpu().numpy(), yo, tol).all()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_dropin_partitioned_forward_acceptance_c1(oracle, torch_cuda, dtype):
+    """tests/acceptance.cpp:69-100 through the GPU: one expert, explicit active
+    sets (forward_selected, unit weights) == partitioned_forward / toy_ffn_forward."""
+    torch = torch_cuda
+    from paper_2510_19366_b200 import MoeLayer
+    rng = np.random.default_rng(1)
+    tol = TOL_F32 if dtype == "f32" else TOL_BF16
+    for trial in range(12):
+        n = (2, 4, 8)[trial % 3]
+        d = int(rng.integers(1, 65))
+        ff = int(n + rng.integers(0, 129 - n))
+        e = oracle.random_expert(d, ff, 5000 + trial)
+        p = oracle.random_balanced_partition(ff, n, 6000 + trial)
+        T = 5
+        x = oracle.uniform_pm1(1000 + trial, T * d).reshape(T, d)
+        if dtype == "bf16":
+            x = bf16_round(x)
+            e = tuple(bf16_round(a) for a in e)
+        L = MoeLayer(1, n, d, ff, dtype=dtype, weights="unit", k_max=n, max_tokens=T)
+        L.set_partition(0, p)
+        L.load_expert(0, *e)
+        sel = np.full((T, n), U32, np.uint32)
+        actives = [list(range(n)), [], [trial % n], sorted({0, n - 1}), list(range(0, n, 2))]
+        for t, act in enumerate(actives):
+            sel[t, :len(act)] = act
+        y = L.forward_selected(torch.from_numpy(x).cuda().to(L.torch_dtype),
+                               torch.from_numpy(sel.view(np.int32))).float().cpu().numpy()
+        for t, act in enumerate(actives):
+            want = oracle.partitioned_forward(d, ff, *e, n, p, x[t], act)
+            assert close_mask(y[t], want, tol).all(), (trial, t)
+        full, _ = oracle.toy_ffn_forward(d, ff, *e, x[0])
+        assert close_mask(y[0], full, tol).all()
+        assert not y[1].any()  # empty active set -> exactly zero (tests/test_expert.cpp:90-96)
+        L.close()
+
+
+def test_validation_errors(oracle, torch_cuda):
+    torch = torch_cuda
+    from paper_2510_19366_b200 import MoeLayer, ValidationError
+    E, S, d, ff, T = 2, 4, 32, 64, 8
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    L = MoeLayer(E, S, d, ff, dtype="f32", k_max=4, max_tokens=T)
+    xd = torch.from_numpy(x).cuda()
+    with pytest.raises(ValidationError):  # not ready
+        L.forward(xd, k=2)
+    with pytest.raises(ValidationError):  # unbalanced partition
+        L.set_partition(0, np.r_[np.zeros(40), np.arange(24) % 4].astype(np.uint32))
+    with pytest.raises(ValidationError):  # wrong width
+        L.set_partition(0, parts[0][:60])
+    bad = experts[0][0].copy()
+    bad[3] = np.nan
+    with pytest.raises(ValidationError):  # non-finite weight (inc/expert.hpp:34)
+        L.load_expert(0, bad, experts[0][1], experts[0][2])
+    for e in range(E):
+        L.set_partition(e, parts[e])
+        L.load_expert(e, *experts[e])
+    with pytest.raises(ValidationError):  # router missing
+        L.forward(xd, k=2)
+    L.set_router(wr)
+    for k in (0, 5):
+        with pytest.raises(ValidationError):  # k_active out of range (inc/gating.hpp:131-134)
+            L.forward(xd, k=k)
+    with pytest.raises(ValidationError):
+        L.forward_host(x, k_per_token=np.array([1, 2, 3, 4, 5, 1, 1, 1], np.uint32))
+    xn = x.copy()
+    xn[2, 3] = np.inf
+    with pytest.raises(ValidationError):  # non-finite input (inc/expert.hpp:55-57)
+        L.forward_host(xn, k=2)
+    sel = np.full((T, 4), U32, np.uint32)
+    sel[0, :2] = [3, 3]  # duplicate (inc/expert.hpp:117)
+    L.forward_selected(xd, torch.from_numpy(sel.view(np.int32)))
+    with pytest.raises(ValidationError):
+        L.check_errors()
+    y = L.forward_host(x, k=2)  # layer still usable after errors
+    assert np.isfinite(y).all()
+
+
+def test_host_path_matches_device_path(oracle, torch_cuda):
+    torch = torch_cuda
+    E, S, d, ff, T = 4, 4, 128, 256, 64
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    L = make_layer(experts, parts, wr, S, "f32", k_max=8, max_tokens=T)
+    yd = L.forward(torch.from_numpy(x).cuda(), k=3).cpu().numpy()
+    yh, sel, w, off = L.forward_host(x, k=3, return_routing=True)
+    assert np.array_equal(yd, yh)  # deterministic: same kernels, same order
+
+
+def test_files_path(oracle, ref, torch_cuda, tmp_path):
+    """MPEX + NDJSON written by the reference, loaded by the layer."""
+    torch = torch_cuda
+    from paper_2510_19366_b200 import MoeLayer
+    E, S, d, ff, T = 3, 4, 16, 32, 10
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    pm = tmp_path / "map.ndjson"
+    for e in range(E):
+        ref.save_toy_expert(tmp_path / f"e{e}.mpex", d, ff, *experts[e])
+        ref.append_partition_doc(pm, e, S, parts[e], truncate=(e == 0))
+    L = MoeLayer(E, S, d, ff, dtype="f32", k_max=4, max_tokens=T)
+    L.load_partition_map(pm)
+    for e in range(E):
+        L.load_expert_file(e, tmp_path / f"e{e}.mpex")
+    L.set_router(wr)
+    y, sel, w, off = L.forward(torch.from_numpy(x).cuda(), k=3, return_routing=True)
+    yo = oracle.layer_forward(experts, parts, S, x, _u32(sel), w.cpu().numpy(), 1)
+    assert close_mask(y.cpu().numpy(), yo, TOL_F32).all()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_proxy_router(oracle, torch_cuda, dtype):
+    torch = torch_cuda
+    E, S, d, ff, T, K = 2, 4, 64, 128, 48, 3
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    members = [[np.flatnonzero(p == s).tolist() for s in range(S)] for p in parts]
+    gates = [members[e][s][:4] for e in range(E) for s in range(S)]
+    L = make_layer(experts, parts, None, S, dtype, k_max=K, max_tokens=T, router="proxy")
+    for e in range(E):
+        L.set_gates(e, 4, gates[e * S:(e + 1) * S])
+    xin = x if dtype == "f32" else bf16_round(x)
+    y, sel, w, off = L.forward(torch.from_numpy(xin).cuda().to(L.torch_dtype), k=K, return_routing=True)
+    scores = oracle.proxy_router_scores(experts, S, gates, xin)
+    osel, ow, gap = oracle.route(scores, K, K, 1)
+    bad, ties = routing_agreement(_u32(sel), osel, gap, np.full(T, K))
+    assert not bad
+
+
+def test_synth_fill_matches_oracle(oracle, torch_cuda):
+    torch = torch_cuda
+    from paper_2510_19366_b200 import synth_fill
+    t = synth_fill(torch.empty(100003, dtype=torch.float32, device="cuda"), 42, 0.125, first=17)
+    assert np.array_equal(t.cpu().numpy(), oracle.synth(42, 100003, 0.125, first=17))
+    b = synth_fill(torch.empty(1000, dtype=torch.bfloat16, device="cuda"), 42, 0.125, first=17)
+    assert np.array_equal(b.float().cpu().numpy(), bf16_round(oracle.synth(42, 1000, 0.125, first=17)))
+
+
+def test_profiling_stage_times(oracle, torch_cuda):
+    torch = torch_cuda
+    E, S, d, ff, T = 4, 4, 128, 256, 64
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    L = make_layer(experts, parts, wr, S, "bf16", k_max=8, max_tokens=T)
+    L.set_profiling(True)
+    n0 = L.launch_count()
+    L.forward(torch.from_numpy(x).cuda().to(torch.bfloat16), k=4)
+    st = L.stage_times()
+    assert set(st) == {"router", "bucket", "dispatch", "gemm1", "gemm2", "combine"}
+    assert all(v[0] > 0 for v in st.values())
+    assert L.launch_count() - n0 == 7
