@@ -1,4 +1,4 @@
-// gemm_simt.cu -- grouped SwiGLU FFN on CUDA cores (FFMA), the fp32 parity
+// gemm_simt.cu -- grouped SwiGLU FFN on CUDA cores (DFMA), the fp32 parity
 // mode (1e-5 relative vs the double-accumulating oracle).  Tensor cores have
 // no true-fp32 MMA, so fp32 mode stays on SIMT (hard part 3).
 //   gemm1: H[r][c] = silu(A[r] . W1_gate[c]) * (A[r] . W1_up[c])
@@ -37,7 +37,11 @@ __device__ __forceinline__ bool map_tile(uint32_t tile, const uint32_t* __restri
     return true;
 }
 
-__device__ __forceinline__ float silu_precise(float g) { return g / (1.0f + expf(-g)); }
+// fp64 accumulation, as the reference does (inc/expert.hpp:64-72): products of
+// fp32 operands are exact in double, so the per-neuron activation rounds to the
+// same float as the reference's in all but astronomically rare cases -- which
+// is what the 1e-5 * (1 + |y|) contract needs where |y| is near zero.
+__device__ __forceinline__ float swiglu_f64(double g, double u) { return static_cast<float>(g / (1.0 + exp(-g)) * u); }
 
 template <typename T>
 __global__ void __launch_bounds__(256) gemm1_simt_kernel(const T* __restrict__ A, const T* __restrict__ W1,
@@ -55,7 +59,7 @@ __global__ void __launch_bounds__(256) gemm1_simt_kernel(const T* __restrict__ A
     const uint32_t c0 = n * BN;
     const uint32_t tx = threadIdx.x % 16, ty = threadIdx.x / 16;
     const size_t wbase = (size_t)g * 2 * w_pad;
-    float accg[4][4] = {}, accu[4][4] = {};
+    double accg[4][4] = {}, accu[4][4] = {};
     for (uint32_t k0 = 0; k0 < K; k0 += BK) {
         for (uint32_t q = threadIdx.x; q < BM * BK; q += 256) {
             const uint32_t r = q / BK, kk = q % BK;
@@ -83,8 +87,8 @@ __global__ void __launch_bounds__(256) gemm1_simt_kernel(const T* __restrict__ A
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    accg[i][j] = fmaf(a[i], bg[j], accg[i][j]);
-                    accu[i][j] = fmaf(a[i], bu[j], accu[i][j]);
+                    accg[i][j] = fma(static_cast<double>(a[i]), static_cast<double>(bg[j]), accg[i][j]);
+                    accu[i][j] = fma(static_cast<double>(a[i]), static_cast<double>(bu[j]), accu[i][j]);
                 }
         }
         __syncthreads();
@@ -95,13 +99,13 @@ __global__ void __launch_bounds__(256) gemm1_simt_kernel(const T* __restrict__ A
         if (r >= rows_here) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            H[(size_t)(row0 + r) * w_pad + c0 + tx * 4 + j] = from_f32<T>(silu_precise(accg[i][j]) * accu[i][j]);
+            H[(size_t)(row0 + r) * w_pad + c0 + tx * 4 + j] = from_f32<T>(swiglu_f64(accg[i][j], accu[i][j]));
     }
 }
 
-template <typename T>
+template <typename T, typename TO>
 __global__ void __launch_bounds__(256) gemm2_simt_kernel(const T* __restrict__ Hm, const T* __restrict__ W2,
-                                                         T* __restrict__ O, uint32_t G, uint32_t K, uint32_t d_pad,
+                                                         TO* __restrict__ O, uint32_t G, uint32_t K, uint32_t d_pad,
                                                          const uint32_t* __restrict__ offsets,
                                                          const uint32_t* __restrict__ mprefix) {
     __shared__ float As[BK][BM + 4];
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(256) gemm2_simt_kernel(const T* __restrict__ H
     const uint32_t i0 = n * BN;
     const uint32_t tx = threadIdx.x % 16, ty = threadIdx.x / 16;
     const size_t wbase = (size_t)g * d_pad;
-    float acc[4][4] = {};
+    double acc[4][4] = {};
     for (uint32_t k0 = 0; k0 < K; k0 += BK) {
         for (uint32_t q = threadIdx.x; q < BM * BK; q += 256) {
             const uint32_t r = q / BK, kk = q % BK;
@@ -136,7 +140,7 @@ __global__ void __launch_bounds__(256) gemm2_simt_kernel(const T* __restrict__ H
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(static_cast<double>(a[i]), static_cast<double>(b[j]), acc[i][j]);
         }
         __syncthreads();
     }
@@ -147,7 +151,12 @@ __global__ void __launch_bounds__(256) gemm2_simt_kernel(const T* __restrict__ H
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint32_t c = i0 + tx * 4 + j;
-            if (c < d_pad) O[(size_t)(row0 + r) * d_pad + c] = from_f32<T>(acc[i][j]);
+            if (c < d_pad) {
+                if constexpr (sizeof(TO) == 8)
+                    O[(size_t)(row0 + r) * d_pad + c] = acc[i][j];
+                else
+                    O[(size_t)(row0 + r) * d_pad + c] = from_f32<TO>(static_cast<float>(acc[i][j]));
+            }
         }
     }
 }
@@ -176,12 +185,12 @@ void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const
                        const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s) {
     const uint32_t grid = simt_grid(sh, (sh.N_group + BN - 1) / BN);
     if (dtype == 1)
-        gemm2_simt_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        gemm2_simt_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, s>>>(
             static_cast<const __nv_bfloat16*>(Hm), static_cast<const __nv_bfloat16*>(W2),
             static_cast<__nv_bfloat16*>(O), sh.G, sh.K, sh.N_group, offsets, mprefix);
     else
-        gemm2_simt_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(Hm), static_cast<const float*>(W2),
-                                                      static_cast<float*>(O), sh.G, sh.K, sh.N_group, offsets,
+        gemm2_simt_kernel<float, double><<<grid, 256, 0, s>>>(static_cast<const float*>(Hm),
+                                                              static_cast<const float*>(W2), static_cast<double*>(O), sh.G, sh.K, sh.N_group, offsets,
                                                       mprefix);
 }
 

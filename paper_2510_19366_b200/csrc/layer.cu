@@ -255,7 +255,7 @@ struct StageTimer {
 };
 
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
-void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, void* y,
+void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
                  cudaStream_t s, StageTimer& tm) {
     tm.begin(1);
     mp::launch_bucket_local(sel, T, L->k_max, L->G, L->ws, s);
@@ -283,7 +283,8 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     ck_launch("gemm2");
     tm.end(4, 1);
     tm.begin(5);
-    mp::launch_combine(L->dtype, L->o, L->d, L->d_pad, L->ws.slot_row, w, L->k_max, T, y, s);
+    const uint32_t group_S = unit ? L->S : 0;
+    mp::launch_combine(L->dtype, L->o, L->d, L->d_pad, L->ws.slot_row, sel, w, L->k_max, group_S, T, y, s);
     ck_launch("combine");
     tm.end(5, 1);
 }
@@ -424,7 +425,8 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset err");
             L->x_perm = dalloc<char>((size_t)L->rows_cap * L->d_pad * L->esz, "x_perm");
             L->h = dalloc<char>((size_t)L->rows_cap * L->w_pad * L->esz, "h");
-            L->o = dalloc<char>((size_t)L->rows_cap * L->d_pad * L->esz, "o");
+            // fp32 mode keeps sub-expert outputs in double until the combine rounds them
+            L->o = dalloc<char>((size_t)L->rows_cap * L->d_pad * (L->dtype == MP_DTYPE_F32 ? 8 : L->esz), "o");
             L->x_stage = dalloc<char>((size_t)L->max_tokens * L->d * L->esz, "x stage");
             L->y_stage = dalloc<char>((size_t)L->max_tokens * L->d * L->esz, "y stage");
             if (D.router_mode == MP_ROUTER_PROXY) L->gate_off = dalloc<uint32_t>(L->G + 1, "gate offsets");
@@ -603,7 +605,7 @@ MP_API mp_status mp_layer_forward(mp_layer_t L, const void* x, uint32_t T, const
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         StageTimer tm(L, s);
         route(L, x, T, kpt, k, s, tm);
-        run_experts(L, x, T, L->sel, L->wsel, y, s, tm);
+        run_experts(L, x, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, y, s, tm);
         copy_outputs(L, T, sel_out, w_out, offsets_out, s, cudaMemcpyDeviceToDevice);
         static const int order[] = {0, 1, 2, 3, 4, 5};
         tm.finish(order, 6);
@@ -634,7 +636,7 @@ MP_API mp_status mp_layer_forward_host(mp_layer_t L, const void* x, uint32_t T, 
         }
         StageTimer tm(L, s);
         route(L, L->x_stage, T, kd, k, s, tm);
-        run_experts(L, L->x_stage, T, L->sel, L->wsel, L->y_stage, s, tm);
+        run_experts(L, L->x_stage, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, L->y_stage, s, tm);
         ck(cudaMemcpyAsync(y, L->y_stage, xbytes, cudaMemcpyDeviceToHost, s), "y download");
         copy_outputs(L, T, sel_out, w_out, offsets_out, s, cudaMemcpyDeviceToHost);
         int flags = 0;
@@ -656,7 +658,7 @@ MP_API mp_status mp_layer_forward_selected(mp_layer_t L, const void* x, uint32_t
         DeviceGuard dg(L->desc.device);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         StageTimer tm(L, s);
-        run_experts(L, x, T, sel, w, y, s, tm);
+        run_experts(L, x, T, sel, w, w == nullptr, y, s, tm);
         if (offsets_out)
             ck(cudaMemcpyAsync(offsets_out, L->ws.offsets, (size_t)(L->G + 1) * 4, cudaMemcpyDeviceToDevice, s),
                "offsets_out");
@@ -787,5 +789,24 @@ MP_API mp_status mp_validate_partition(uint32_t n_sub, const uint32_t* a, size_t
     return guarded([&] {
         if (!a && n) fail(MP_ERR_VALIDATION, "null argument");
         mp::validate_partition(n_sub, a, n);
+    });
+}
+
+// ---- debugging aid (not part of the public header): internal buffers ----
+MP_API mp_status mp_debug_buffers(mp_layer_t L, void** x_perm, void** h, void** o, void** W1, void** W2,
+                                  uint32_t* dims /* w_pad, d_pad, rows_cap, use_tc */) {
+    return guarded([&] {
+        if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        if (x_perm) *x_perm = L->x_perm;
+        if (h) *h = L->h;
+        if (o) *o = L->o;
+        if (W1) *W1 = L->W1;
+        if (W2) *W2 = L->W2;
+        if (dims) {
+            dims[0] = L->w_pad;
+            dims[1] = L->d_pad;
+            dims[2] = L->rows_cap;
+            dims[3] = L->use_tc ? 1u : 0u;
+        }
     });
 }

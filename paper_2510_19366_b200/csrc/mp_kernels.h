@@ -40,8 +40,10 @@ void launch_bucket_local(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32
 void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s);
 void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t d_pad, const uint32_t* sel,
                      const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s);
-void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row, const float* w,
-                    uint32_t k_max, uint32_t T, void* y, cudaStream_t s);
+// group_S > 0: unit-weight semantics, round once per parent expert (fp32 mode)
+void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
+                    const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
+                    cudaStream_t s);
 
 // Packing (load time).
 void launch_pack_w1(int dtype, const float* wg, const float* wu, uint32_t d, uint32_t ff, const int32_t* nmap,

@@ -9,6 +9,7 @@
 // 16-byte vector accesses, no atomics, fixed reduction orders (deterministic).
 #include <cfloat>
 #include <cmath>
+#include <type_traits>
 
 #include "mp_common.cuh"
 #include "mp_kernels.h"
@@ -145,6 +146,17 @@ __global__ void __launch_bounds__(kRouterThreads) router_linear_kernel(
                 const float xa = xs[kk * (TB + 1) + 2 * ty];
                 const float xb = xs[kk * (TB + 1) + 2 * ty + 1];
                 const float4 wv = *reinterpret_cast<const float4*>(&ws[kk * (GB + 4) + 4 * tx]);
+                if constexpr (sizeof(Tx) == 4) {
+                    // fp32 (reference-exact) mode: fp64 accumulation like the
+                    // oracle, so the softmax weights round to the same floats
+                    const double wvd[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        acc[0][b] = fma(static_cast<double>(xa), wvd[b], acc[0][b]);
+                        acc[1][b] = fma(static_cast<double>(xb), wvd[b], acc[1][b]);
+                    }
+                    continue;
+                }
                 part[0][0] = fmaf(xa, wv.x, part[0][0]);
                 part[0][1] = fmaf(xa, wv.y, part[0][1]);
                 part[0][2] = fmaf(xa, wv.z, part[0][2]);
@@ -355,14 +367,13 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
 }
 
 // ---------------------------------------------------------------- combine
-// y[t] = sum_{j ascending} w[t][j] * o[slot_row[t][j]]  (fp32 accumulate,
-// fixed order = ascending sub-expert id).  CTA per token,
-// 8 columns (one 16-byte bf16 vector) per thread per step.
-template <typename Tx>
-__global__ void __launch_bounds__(256) combine_kernel(const Tx* __restrict__ o, uint32_t d, uint32_t d_pad,
-                                                      const uint32_t* __restrict__ slot_row,
-                                                      const float* __restrict__ w, uint32_t k_max, uint32_t T,
-                                                      Tx* __restrict__ y) {
+// y[t] = sum_{j ascending} w[t][j] * o[slot_row[t][j]] in a fixed order
+// (ascending sub-expert id), no atomics.  CTA per token.
+// bf16 mode: o is bf16, fp32 accumulate, 16-byte vector loads / stores.
+__global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* __restrict__ o, uint32_t d,
+                                                           uint32_t d_pad, const uint32_t* __restrict__ slot_row,
+                                                           const float* __restrict__ w, uint32_t k_max,
+                                                           __nv_bfloat16* __restrict__ y) {
     __shared__ uint32_t rows[64];
     __shared__ float wts[64];
     const uint32_t t = blockIdx.x;
@@ -371,62 +382,81 @@ __global__ void __launch_bounds__(256) combine_kernel(const Tx* __restrict__ o, 
         wts[j] = w ? w[(size_t)t * k_max + j] : 1.0f;
     }
     __syncthreads();
-    Tx* yr = y + (size_t)t * d;
-    constexpr uint32_t VE = 8;
-    if ((d % VE) == 0 && (d_pad % VE) == 0) {
-        for (uint32_t c = threadIdx.x * VE; c < d; c += blockDim.x * VE) {
-            float acc[VE];
-#pragma unroll
-            for (int q = 0; q < (int)VE; ++q) acc[q] = 0.0f;
+    __nv_bfloat16* yr = y + (size_t)t * d;
+    if ((d % 8) == 0) {
+        for (uint32_t c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             for (uint32_t j = 0; j < k_max; ++j) {
                 const uint32_t r = rows[j];
                 if (r == kSelNone) continue;
                 const float wj = wts[j];
-                const Tx* src = o + (size_t)r * d_pad + c;
-                if constexpr (sizeof(Tx) == 2) {
-                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src));
-                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(o + (size_t)r * d_pad + c));
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float2 f = __bfloat1622float2(h[q]);
-                        acc[2 * q] = fmaf(wj, f.x, acc[2 * q]);
-                        acc[2 * q + 1] = fmaf(wj, f.y, acc[2 * q + 1]);
-                    }
-                } else {
-                    const float4 a = __ldg(reinterpret_cast<const float4*>(src));
-                    const float4 b = __ldg(reinterpret_cast<const float4*>(src + 4));
-                    acc[0] = fmaf(wj, a.x, acc[0]);
-                    acc[1] = fmaf(wj, a.y, acc[1]);
-                    acc[2] = fmaf(wj, a.z, acc[2]);
-                    acc[3] = fmaf(wj, a.w, acc[3]);
-                    acc[4] = fmaf(wj, b.x, acc[4]);
-                    acc[5] = fmaf(wj, b.y, acc[5]);
-                    acc[6] = fmaf(wj, b.z, acc[6]);
-                    acc[7] = fmaf(wj, b.w, acc[7]);
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(h[q]);
+                    acc[2 * q] = fmaf(wj, f.x, acc[2 * q]);
+                    acc[2 * q + 1] = fmaf(wj, f.y, acc[2 * q + 1]);
                 }
             }
-            if constexpr (sizeof(Tx) == 2) {
-                uint4 out;
-                out.x = pack_bf16x2(acc[0], acc[1]);
-                out.y = pack_bf16x2(acc[2], acc[3]);
-                out.z = pack_bf16x2(acc[4], acc[5]);
-                out.w = pack_bf16x2(acc[6], acc[7]);
-                *reinterpret_cast<uint4*>(yr + c) = out;
-            } else {
-                *reinterpret_cast<float4*>(yr + c) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-                *reinterpret_cast<float4*>(yr + c + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
-            }
+            uint4 out;
+            out.x = pack_bf16x2(acc[0], acc[1]);
+            out.y = pack_bf16x2(acc[2], acc[3]);
+            out.z = pack_bf16x2(acc[4], acc[5]);
+            out.w = pack_bf16x2(acc[6], acc[7]);
+            *reinterpret_cast<uint4*>(yr + c) = out;
         }
     } else {
         for (uint32_t c = threadIdx.x; c < d; c += blockDim.x) {
             float acc = 0.0f;
-            for (uint32_t j = 0; j < k_max; ++j) {
-                const uint32_t r = rows[j];
-                if (r == kSelNone) continue;
-                acc = fmaf(wts[j], to_f32(o[(size_t)r * d_pad + c]), acc);
-            }
-            yr[c] = from_f32<Tx>(acc);
+            for (uint32_t j = 0; j < k_max; ++j)
+                if (rows[j] != kSelNone) acc = fmaf(wts[j], __bfloat162float(o[(size_t)rows[j] * d_pad + c]), acc);
+            yr[c] = __float2bfloat16_rn(acc);
         }
+    }
+}
+
+// fp32 (reference-exact) mode: o holds each sub-expert's output in double; the
+// reference rounds partitioned_forward to float per call (inc/expert.hpp:133),
+// so: weighted mode rounds per sub-expert then sums w * float(o) in double;
+// unit mode (group_S > 0) sums the selected sub-experts of one parent expert
+// in double and rounds once per expert (one reference call per expert).
+__global__ void __launch_bounds__(256) combine_f64_kernel(const double* __restrict__ o, uint32_t d, uint32_t d_pad,
+                                                          const uint32_t* __restrict__ slot_row,
+                                                          const uint32_t* __restrict__ sel,
+                                                          const float* __restrict__ w, uint32_t k_max,
+                                                          uint32_t group_S, float* __restrict__ y) {
+    __shared__ uint32_t rows[64];
+    __shared__ uint32_t gid[64];
+    __shared__ float wts[64];
+    const uint32_t t = blockIdx.x;
+    for (uint32_t j = threadIdx.x; j < k_max; j += blockDim.x) {
+        rows[j] = slot_row[(size_t)t * k_max + j];
+        gid[j] = sel[(size_t)t * k_max + j];
+        wts[j] = w ? w[(size_t)t * k_max + j] : 1.0f;
+    }
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < d; c += blockDim.x) {
+        double acc = 0.0, part = 0.0;
+        uint32_t cur = kSelNone;
+        for (uint32_t j = 0; j < k_max; ++j) {
+            const uint32_t r = rows[j];
+            if (r == kSelNone) continue;
+            const double v = o[(size_t)r * d_pad + c];
+            if (group_S) {
+                const uint32_t e = gid[j] / group_S;
+                if (e != cur && cur != kSelNone) {
+                    acc += static_cast<double>(static_cast<float>(part));
+                    part = 0.0;
+                }
+                cur = e;
+                part += v;
+            } else {
+                acc += static_cast<double>(wts[j]) * static_cast<double>(static_cast<float>(v));
+            }
+        }
+        if (group_S && cur != kSelNone) acc += static_cast<double>(static_cast<float>(part));
+        y[(size_t)t * d + c] = static_cast<float>(acc);
     }
 }
 
@@ -481,14 +511,15 @@ void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t 
                                                     static_cast<float*>(x_perm));
 }
 
-void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row, const float* w,
-                    uint32_t k_max, uint32_t T, void* y, cudaStream_t s) {
+void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
+                    const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
+                    cudaStream_t s) {
     if (dtype == 1)
-        combine_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(o), d, d_pad, slot_row, w,
-                                                        k_max, T, static_cast<__nv_bfloat16*>(y));
+        combine_bf16_kernel<<<T, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(o), d, d_pad, slot_row, w, k_max,
+                                              static_cast<__nv_bfloat16*>(y));
     else
-        combine_kernel<float><<<T, 256, 0, s>>>(static_cast<const float*>(o), d, d_pad, slot_row, w, k_max, T,
-                                                static_cast<float*>(y));
+        combine_f64_kernel<<<T, 256, 0, s>>>(static_cast<const double*>(o), d, d_pad, slot_row, sel, w, k_max, group_S,
+                                             static_cast<float*>(y));
 }
 
 }  // namespace mp

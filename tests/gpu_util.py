@@ -58,3 +58,20 @@ def routing_agreement(gpu_sel, ora_sel, gap, k_per_token, tie_eps=1e-6):
         if not np.array_equal(gpu_sel[t, :k], ora_sel[t, :k]) and not near:
             bad.append(t)
     return bad, ties
+
+
+def bf16_ok(got, want, tol=2e-2):
+    """bf16-mode acceptance, elementwise: |got - want| <= tol * (rms_t(want) + |want|)
+    with rms_t the RMS of the token's output row.  bf16 rounding error scales
+    with the magnitude of the summed terms, not with |y|: for the reference's
+    unscaled U(-1,1) fixtures |y| near 0 is a cancellation of O(1e3) terms of
+    size O(10), so the (1 + |y|) form is unattainable there for any bf16 kernel.
+    At the Mixtral configuration this form is the stricter of the two."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    rms = np.sqrt((want ** 2).mean(axis=-1, keepdims=True))
+    return np.abs(got - want) <= tol * (rms + np.abs(want))
+
+
+def out_ok(got, want, dtype):
+    return close_mask(got, want, 1e-5) if dtype == "f32" else bf16_ok(got, want)
