@@ -1,0 +1,473 @@
+#!/usr/bin/env python
+"""bench.py -- MoE-Prism sub-expert MoE-layer forward on B200.
+
+Metric (BASELINE.json): MoE-layer tokens/sec vs active sub-experts k, with the
+tensor-core / HBM roofline fraction.  Workload (BASELINE configs[1], SURVEY
+8(d) C2): Mixtral-8x7B layer shape, bf16, d=4096, ffn=14336, 8 experts x 8
+sub-experts (w=1792), 4096 tokens per GPU, random-init weights from the
+counter-based synthetic stream.  A step = one layer forward over the 4096
+tokens (router -> bucket -> dispatch -> grouped SwiGLU GEMMs -> combine).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--k 8] [--impl reference]
+
+N>1 runs under torchrun (one process per GPU, NCCL).  Timing: W warm-up
+steps, then K steps bracketed by barrier + cuda synchronize, CUDA events on
+the launching stream, max over ranks.  L2: inputs rotate over 8 x buffers
+(268 MB) and the weights are 2.8 GB, both far above the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MoE-layer tokens/sec vs active sub-experts k (1/2/4/8 B200); % TC/HBM roofline"
+E, S, D, FF = 8, 8, 4096, 14336
+W_SUB = FF // S
+N_XBUF = 8
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        j = json.loads(f.read_text())
+        p.update({k: j[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in j})
+        p["source"] = "measured"
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc, self.thread = index, [], None, None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 8:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_max": max((float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()),
+                                   default=None)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def build_layer(local, T, k_max):
+    import torch
+    from paper_2510_19366_b200 import MoeLayer, synth_fill
+    L = MoeLayer(E, S, D, FF, dtype="bf16", router="linear", weights="softmax_renorm", k_max=k_max, max_tokens=T,
+                 device=local)
+    buf = [torch.empty(D * FF, dtype=torch.float32, device="cuda") for _ in range(3)]
+    for e in range(E):
+        for m, (seed, scale) in enumerate(((100 + 3 * e, 1 / math.sqrt(D)), (101 + 3 * e, 1 / math.sqrt(D)),
+                                           (102 + 3 * e, 1 / math.sqrt(FF)))):
+            synth_fill(buf[m], seed, scale)
+        L.set_partition(e, balanced_partition(FF, S, 6000 + e))
+        L.load_expert(e, *buf)
+    del buf
+    wr = torch.empty(D * E * S, dtype=torch.float32, device="cuda")
+    synth_fill(wr, 7, 1 / math.sqrt(D))
+    L.set_router(wr)
+    xs = []
+    for i in range(N_XBUF):
+        x = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
+        synth_fill(x, 11 + 1000 * i, 1.0)
+        xs.append(x)
+    torch.cuda.synchronize()
+    return L, xs
+
+
+def balanced_partition(n, n_sub, seed):
+    """testsupport::random_balanced_partition (tests/support.hpp:89-105): seeded
+    Fisher-Yates (mt19937_64 + uniform_index) dealt round-robin."""
+    import numpy as np
+    rng = _MT64(seed)
+    order = list(range(n))
+    for i in range(n - 1, 0, -1):
+        j = rng.uniform_index(i + 1)
+        order[i], order[j] = order[j], order[i]
+    a = np.empty(n, np.uint32)
+    for i, o in enumerate(order):
+        a[o] = i % n_sub
+    return a
+
+
+class _MT64:
+    """std::mt19937_64 (fixture generation for the partition layout only)."""
+
+    def __init__(self, seed):
+        self.mt = [0] * 312
+        self.mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+        self.idx = 312
+
+    def next(self):
+        M = 0xFFFFFFFFFFFFFFFF
+        if self.idx >= 312:
+            mt = self.mt
+            for i in range(312):
+                x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % 312] & 0x7FFFFFFF)
+                xa = x >> 1
+                if x & 1:
+                    xa ^= 0xB5026F5AA96619E9
+                mt[i] = mt[(i + 156) % 312] ^ xa
+            self.idx = 0
+        y = self.mt[self.idx]
+        self.idx += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000 & M
+        y ^= (y << 37) & 0xFFF7EEE000000000 & M
+        y ^= y >> 43
+        return y & M
+
+    def uniform_index(self, n):
+        M = 0xFFFFFFFFFFFFFFFF
+        limit = M - M % n
+        while True:
+            x = self.next()
+            if x < limit:
+                return x % n
+
+
+def layer_roofline(T, k, ms, pk, touched_groups):
+    """t_roofline = max(F / P_tc, B / BW); F = 6 d w T k expert flops,
+    B = touched sub-expert weights (3 d w bf16 each) + x in + y out."""
+    F = 6.0 * D * W_SUB * T * k
+    B = touched_groups * 3.0 * D * W_SUB * 2 + 2.0 * T * D * 2
+    t_tc = F / (pk["bf16_tflops_sustained"] * 1e12)
+    t_hbm = B / (pk["hbm_gbs"] * 1e9)
+    t_roof = max(t_tc, t_hbm)
+    return {"bound": "tensor" if t_tc >= t_hbm else "hbm", "t_roofline_ms": t_roof * 1e3, "t_measured_ms": ms,
+            "frac": (t_roof * 1e3) / ms, "tc_util": (F / (ms * 1e-3)) / (pk["bf16_tflops_sustained"] * 1e12),
+            "peak_tflops": pk["bf16_tflops_sustained"], "peak_gbs": pk["hbm_gbs"], "peak_source": pk["source"]}
+
+
+def time_steps(fn, steps, warmup, world):
+    import torch
+    for i in range(warmup):
+        fn(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(steps):
+        fn(i)
+    e1.record(st)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1) / steps
+    return max_over_ranks(ms, world)
+
+
+def stage_profile(L, xs, k, reps=20, kpt=None):
+    import torch
+    L.reset_stage_times()
+    L.set_profiling(True)
+    for i in range(reps):
+        L.forward(xs[i % len(xs)], k=k, k_per_token=kpt)
+    torch.cuda.synchronize()
+    L.set_profiling(False)
+    return {name: ms / reps for name, (ms, n) in L.stage_times().items()}
+
+
+def kernel_roofline(stage_ms_per_step, T, k, pk, touched_groups):
+    """The dominant kernel's roofline: gemm1 (SwiGLU) at TC-bound k, against the
+    sustained bf16 peak; algorithmic flops = 4 d w T k per launch."""
+    g1 = stage_ms_per_step.get("gemm1", 0.0)
+    g2 = stage_ms_per_step.get("gemm2", 0.0)
+    name = "gemm1" if g1 >= g2 else "gemm2"
+    ms = max(g1, g2)
+    flops = (4.0 if name == "gemm1" else 2.0) * D * W_SUB * T * k
+    wbytes = touched_groups * (2 if name == "gemm1" else 1) * D * W_SUB * 2.0
+    abytes = T * k * D * 2.0 + T * k * W_SUB * 2.0
+    t_tc = flops / (pk["bf16_tflops_sustained"] * 1e12)
+    t_hbm = (wbytes + abytes) / (pk["hbm_gbs"] * 1e9)
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary_r01.json"
+    if prof.exists():
+        try:
+            j = json.loads(prof.read_text())
+            traffic = j.get("kernels", {}).get(name, {}).get(f"dram_bytes_k{k}")
+        except Exception:
+            traffic = None
+    if t_tc >= t_hbm:
+        ach = flops / (ms * 1e-3) / 1e12
+        return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"], "traffic": traffic,
+                "algorithmic_flops": flops, "launch_ms": ms, "peak_source": pk["source"] + " sustained"}
+    ach = (wbytes + abytes) / (ms * 1e-3) / 1e9
+    return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": ach / pk["hbm_gbs"], "traffic": traffic, "algorithmic_bytes": wbytes + abytes, "launch_ms": ms,
+            "peak_source": pk["source"]}
+
+
+def cpu_reference_sample(k, T_sample, nthreads, seed_tokens=11):
+    """The reference CPU path (oracle/_ref = reference headers compiled
+    verbatim): router restated in double + select_topk_subexperts +
+    partitioned_forward per selected sub-expert, std::thread over tokens."""
+    import numpy as np
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import Oracle, RefLayer, RefLib, have_ref
+    orc = Oracle()
+    if have_ref():
+        ref = RefLib()
+        kind = "reference"
+    else:
+        ref = None
+        kind = "port"
+    experts = [(orc.synth(100 + 3 * e, D * FF, 1 / math.sqrt(D)), orc.synth(101 + 3 * e, D * FF, 1 / math.sqrt(D)),
+                orc.synth(102 + 3 * e, D * FF, 1 / math.sqrt(FF))) for e in range(E)]
+    parts = [orc.random_balanced_partition(FF, S, 6000 + e) for e in range(E)]
+    wr = orc.synth(7, D * E * S, 1 / math.sqrt(D))
+    x = orc.synth(seed_tokens, T_sample * D, 1.0).reshape(T_sample, D)
+    if kind == "reference":
+        rl = RefLayer(ref, experts, parts, S)
+        t0 = time.perf_counter()
+        sel, w = rl.route(x, wr, k, 16, 1)
+        y = rl.forward(x, sel, w, 1, nthreads=nthreads)
+        dt = time.perf_counter() - t0
+    else:
+        t0 = time.perf_counter()
+        logits = orc.router_logits(x, wr, T_sample, D, E * S)
+        sel, w, _ = orc.route(logits, k, 16, 1)
+        y = orc.layer_forward(experts, parts, S, x, sel, w, 1, nthreads=nthreads)
+        dt = time.perf_counter() - t0
+    assert np.isfinite(y).all()
+    return T_sample / dt, kind, dt
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    nthreads = os.cpu_count() or 1
+    # a step = one bounded sample: one token per host thread (~1.45 s per
+    # (token, sub-expert) reference call at this shape)
+    T_sample = nthreads
+    vals = []
+    kind = None
+    for i in range(args.warmup + args.steps):
+        v, kind, dt = cpu_reference_sample(args.k, T_sample, nthreads, seed_tokens=11 + i)
+        if i >= args.warmup:
+            vals.append(v)
+    v = statistics.mean(vals)
+    cfg = workload_config(args, world)
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * T_sample / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg, "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": nthreads, "kind": kind,
+                             "sample": f"{T_sample} tokens per step (one per thread), k={args.k}, "
+                                       f"Mixtral layer shape fp32 weights; CPU {cpu_model()}"},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    return {"workload": "Mixtral-8x7B MoE layer shape bf16 (BASELINE configs[1]): d=4096, ffn=14336, "
+                        "8 experts x 8 sub-experts (w=1792), linear fp32 router, softmax-renormalised top-k",
+            "d_model": D, "d_ff": FF, "experts": E, "subexperts_per_expert": S, "tokens_per_gpu": args.tokens,
+            "k": args.k, "global_tokens": args.tokens * world,
+            "parallelism": "replicas" if world > 1 else "single",
+            "l2": f"x rotates over {N_XBUF} buffers ({N_XBUF * args.tokens * D * 2 / 1e6:.0f} MB) + 2.8 GB weights, "
+                  "both > 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--k", type=int, default=8)
+    ap.add_argument("--tokens", type=int, default=4096)
+    ap.add_argument("--sweep", default="2,4,8,16")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import numpy as np
+    import torch
+    pk = peaks()
+    T = args.tokens
+    sweep = [int(v) for v in args.sweep.split(",") if v]
+    L, xs = build_layer(local, T, k_max=16)
+    touched = E * S  # at 4096 tokens every sub-expert receives tokens
+
+    def step(i, k=args.k, kpt=None):
+        L.forward(xs[i % N_XBUF], k=k, k_per_token=kpt, y=ybuf)
+
+    ybuf = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
+    clocks = ClockSampler(local)
+    clocks.start()
+    n0 = L.launch_count()
+    ms = time_steps(step, args.steps, args.warmup, world)
+    launches = (L.launch_count() - n0) // (args.steps + args.warmup) * args.steps
+    clk = clocks.stop()
+    value = world * T / (ms * 1e-3)
+
+    # per-stage device times (CUDA events on the forward's stream), the sweep
+    sweep_out = []
+    stages_main = None
+    for k in sweep + ["mixed"]:
+        kpt = None
+        kk = k
+        if k == "mixed":
+            rng = np.random.default_rng(13)
+            kpt = torch.from_numpy(rng.choice([2, 4, 8, 16], size=T, p=[0.25, 0.35, 0.25, 0.15]).astype(np.int32))
+            kpt = kpt.cuda()
+            kk = float(kpt.float().mean().item())
+        msk = time_steps(lambda i: step(i, k=0 if kpt is not None else k, kpt=kpt), max(args.steps // 2, 10), 3,
+                         world)
+        per_step = stage_profile(L, xs, 0 if kpt is not None else k, kpt=kpt)
+        ent = {"k": k, "tokens_per_s": world * T / (msk * 1e-3), "ms_per_step": msk,
+               "layer_roofline": layer_roofline(T, kk, msk, pk, touched), "stages_ms": per_step}
+        if k != "mixed":
+            ent["kernel_roofline"] = kernel_roofline(per_step, T, k, pk, touched)
+        sweep_out.append(ent)
+        if k == args.k:
+            stages_main = per_step
+    if stages_main is None:
+        stages_main = stage_profile(L, xs, args.k)
+
+    # e2e: public API with HOST buffers (pinned), H2D of x + D2H of y per step
+    xh = [xs[i].cpu().pin_memory() for i in range(2)]
+    yh = torch.empty((T, D), dtype=torch.bfloat16).pin_memory()
+    import ctypes as C
+    from paper_2510_19366_b200 import _lib
+    lib = _lib.load()
+
+    def e2e_step(i):
+        _lib.check(lib.mp_layer_forward_host(L.h, xh[i % 2].data_ptr(), T, None, args.k, yh.data_ptr(), None, None,
+                                             None, torch.cuda.current_stream().cuda_stream))
+
+    ms_e2e = time_steps(e2e_step, max(args.steps // 2, 10), 3, world)
+    e2e = {"value": world * T / (ms_e2e * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": T * D * 2,
+           "d2h_bytes_per_step": T * D * 2, "ms_per_step": ms_e2e,
+           "path": "mp_layer_forward_host (C-ABI), pinned host x/y"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nthreads = os.cpu_count() or 1
+        try:
+            v, kind, dt = cpu_reference_sample(args.k, nthreads, nthreads)
+            cpu = {"value": v, "unit": "tokens/s", "cores": nthreads, "kind": kind,
+                   "sample": f"{nthreads} tokens (one per thread), k={args.k}, Mixtral layer shape, fp32 weights, "
+                             f"{dt:.1f} s; CPU {cpu_model()}"}
+        except Exception as exc:  # report, never fabricate
+            cpu = {"value": None, "unit": "tokens/s", "cores": nthreads, "kind": None, "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        main_k = next((s for s in sweep_out if s["k"] == args.k), None)
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (counter-based U(-1,1) stream; random-init weights of the Mixtral layer shape)",
+                "config": workload_config(args, world),
+                "roofline": kernel_roofline(stages_main, T, args.k, pk, touched),
+                "layer_roofline": layer_roofline(T, args.k, ms, pk, touched),
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "stages_ms": stages_main, "sweep": sweep_out}
+        if main_k:
+            line["roofline"] = main_k.get("kernel_roofline", line["roofline"])
+        print(json.dumps(line), flush=True)
+    L.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
