@@ -360,8 +360,8 @@ def workload_config(args, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--tokens", type=int, default=4096)
     ap.add_argument("--sweep", default="2,4,8,16")
@@ -395,7 +395,6 @@ def main():
     n0 = L.launch_count()
     ms = time_steps(step, args.steps, args.warmup, world)
     launches = (L.launch_count() - n0) // (args.steps + args.warmup) * args.steps
-    clk = clocks.stop()
     value = world * T / (ms * 1e-3)
 
     # per-stage device times (CUDA events on the forward's stream), the sweep
@@ -437,6 +436,7 @@ def main():
     e2e = {"value": world * T / (ms_e2e * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": T * D * 2,
            "d2h_bytes_per_step": T * D * 2, "ms_per_step": ms_e2e,
            "path": "mp_layer_forward_host (C-ABI), pinned host x/y"}
+    clk = clocks.stop()  # sampled across the main timed loop, the k sweep and the e2e loop
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

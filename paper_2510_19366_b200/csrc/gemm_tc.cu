@@ -265,13 +265,16 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
-    if (swiglu) {
+    static bool attr_set = false;  // once per process (device-independent attribute)
+    if (!attr_set) {
         cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
-    } else {
         cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        gemm_tc_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+        attr_set = true;
     }
+    if (swiglu)
+        gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+    else
+        gemm_tc_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
 }
 
 }  // namespace mp

@@ -82,6 +82,12 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Error bound used to certify tensor-core router selections (measured max
+// |logit - fp64| is ~1e-7 at d=4096 with 256-deep chunks; 4e-6 leaves a wide
+// margin).  Tokens whose k-th/(k+1)-th gap is < 2 * guard are re-selected from
+// exact fp64 logits.
+constexpr double kRouterGuard = 4e-6;
+
 const char* kStageNames[] = {"router", "bucket", "dispatch", "gemm1", "gemm2", "combine"};
 constexpr int kStages = 6;
 
@@ -114,6 +120,13 @@ struct mp_layer_s {
     void* W1 = nullptr;
     void* W2 = nullptr;
     float* wrT = nullptr;
+    // tensor-core router: W_r as three bf16 planes + fp64 K-split partials
+    bool router_tc = false;
+    uint32_t r_npad = 0, r_last_ks = 0, r_last_T = 0;
+    void* wr_planes = nullptr;
+    double* r_partial = nullptr;
+    uint32_t* r_flagged = nullptr;  // [1 + max_tokens]: count, then tokens re-selected in fp64
+    CUtensorMap tm_wplanes{};
     int32_t* d_nmap = nullptr;
 
     uint32_t* sel = nullptr;
@@ -128,7 +141,12 @@ struct mp_layer_s {
     CUtensorMap tm_xperm{}, tm_h{}, tm_w1{}, tm_w2{};
 
     bool profiling = false;
-    cudaEvent_t ev[kStages + 1] = {};
+    struct EventSet {
+        cudaEvent_t ev[kStages + 1];
+        int order[kStages];
+        int n = 0;
+    };
+    std::vector<EventSet*> ev_pool, ev_pending;
     double stage_ms[kStages] = {};
     uint64_t stage_launches[kStages] = {};
     uint64_t launches = 0;
@@ -139,14 +157,17 @@ namespace {
 void free_layer(mp_layer_s* L) {
     for (float* p : L->raw)
         if (p) cudaFree(p);
-    void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->d_nmap, L->sel,
+    void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_flagged, L->d_nmap, L->sel,
                     L->wsel, L->kpt_dev, L->ws.lrank, L->ws.block_counts, L->ws.block_base, L->ws.offsets,
                     L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
                     L->x_perm, L->h, L->o, L->x_stage, L->y_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    for (auto& e : L->ev)
-        if (e) cudaEventDestroy(e);
+    for (auto* v : {&L->ev_pool, &L->ev_pending})
+        for (auto* es : *v) {
+            for (auto& e : es->ev) cudaEventDestroy(e);
+            delete es;
+        }
     delete L;
 }
 
@@ -225,34 +246,54 @@ void check_ready(mp_layer_s* L) {
             fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " is not ready (weights and partition required)");
 }
 
+// Per-stage device time: CUDA events recorded on the forward's stream and
+// resolved lazily (no host sync inside a forward, so the CPU stays ahead and
+// the events measure GPU time, not launch gaps).
 struct StageTimer {
     mp_layer_s* L;
     cudaStream_t s;
-    int cur = -1;
+    mp_layer_s::EventSet* es = nullptr;
     StageTimer(mp_layer_s* l, cudaStream_t st) : L(l), s(st) {}
     void begin(int stage) {
-        if (!L->profiling) return;
-        if (cur < 0) cudaEventRecord(L->ev[0], s);
-        cur = stage;
+        (void)stage;
+        if (!L->profiling || es) return;
+        if (L->ev_pool.empty()) {
+            auto* n = new mp_layer_s::EventSet;
+            for (auto& e : n->ev) ck(cudaEventCreate(&e), "event");
+            L->ev_pool.push_back(n);
+        }
+        es = L->ev_pool.back();
+        L->ev_pool.pop_back();
+        es->n = 0;
+        cudaEventRecord(es->ev[0], s);
     }
     void end(int stage, int n_launch) {
         L->launches += n_launch;
-        if (!L->profiling) return;
+        if (!L->profiling || !es) return;
         L->stage_launches[stage] += n_launch;
-        cudaEventRecord(L->ev[stage + 1], s);
+        cudaEventRecord(es->ev[stage + 1], s);
+        es->order[es->n++] = stage;
     }
-    void finish(const int* order, int n) {
-        if (!L->profiling || cur < 0) return;
-        cudaEventSynchronize(L->ev[order[n - 1] + 1]);
-        cudaEvent_t prev = L->ev[0];
-        for (int q = 0; q < n; ++q) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, prev, L->ev[order[q] + 1]);
-            L->stage_ms[order[q]] += ms;
-            prev = L->ev[order[q] + 1];
-        }
+    void finish(const int*, int) {
+        if (es) L->ev_pending.push_back(es);
+        es = nullptr;
     }
 };
+
+void resolve_timings(mp_layer_s* L) {
+    for (auto* es : L->ev_pending) {
+        if (es->n) cudaEventSynchronize(es->ev[es->order[es->n - 1] + 1]);
+        cudaEvent_t prev = es->ev[0];
+        for (int q = 0; q < es->n; ++q) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, prev, es->ev[es->order[q] + 1]);
+            L->stage_ms[es->order[q]] += ms;
+            prev = es->ev[es->order[q] + 1];
+        }
+        L->ev_pool.push_back(es);
+    }
+    L->ev_pending.clear();
+}
 
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
@@ -305,10 +346,26 @@ void route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
         tm.end(0, 2);
     } else {
         if (!L->router_set) fail(MP_ERR_VALIDATION, "router weights not set (mp_layer_set_router)");
-        mp::launch_router_linear(L->dtype, x, T, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode, L->sel,
-                                 L->wsel, L->ws.err, s);
-        ck_launch("router");
-        tm.end(0, 1);
+        if (L->router_tc && (reinterpret_cast<uintptr_t>(x) % 16) == 0) {
+            const mp::RouterTcPlan pl = mp::plan_router_tc(T, L->d, L->G, L->num_sms);
+            CUtensorMap tmX;
+            if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "router tensor map");
+            mp::launch_router_tc(&tmX, &L->tm_wplanes, pl, T, L->r_partial, s);
+            L->r_last_ks = pl.ks;
+            L->r_last_T = T;
+            ck(cudaMemsetAsync(L->r_flagged, 0, sizeof(uint32_t), s), "memset flagged");
+            mp::launch_partials_topk(L->r_partial, pl.ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
+                                     L->sel, L->wsel, L->ws.err, kRouterGuard, L->r_flagged, s);
+            mp::launch_router_fixup(L->dtype, x, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode, L->sel,
+                                    L->wsel, L->ws.err, L->r_flagged, L->num_sms, s);
+            ck_launch("router(tc)");
+            tm.end(0, 3);
+        } else {
+            mp::launch_router_linear(L->dtype, x, T, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode,
+                                     L->sel, L->wsel, L->ws.err, s);
+            ck_launch("router");
+            tm.end(0, 1);
+        }
     }
 }
 
@@ -406,6 +463,18 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             L->W2 = dalloc<char>(w2 * L->esz, "W2");
             ck(cudaMemset(L->W2, 0, w2 * L->esz), "memset W2");
             L->wrT = dalloc<float>((size_t)L->G_pad * L->d, "router");
+            L->router_tc = D.dtype == MP_DTYPE_BF16 && (L->d % 8) == 0 && D.router_mode == MP_ROUTER_LINEAR;
+            if (const char* env = std::getenv("MOEPRISM_ROUTER"))
+                if (std::string(env) == "simt") L->router_tc = false;  // diagnostics only
+            if (L->router_tc) {
+                L->r_npad = round_up(L->G, 32);
+                const uint32_t n_chunks = (L->d + 255) / 256;  // upper bound of the router's K splits
+                L->wr_planes = dalloc<char>((size_t)3 * L->r_npad * L->d * 2, "router planes");
+                L->r_partial = dalloc<double>((size_t)n_chunks * L->max_tokens * L->r_npad, "router partials");
+                L->r_flagged = dalloc<uint32_t>((size_t)L->max_tokens + 1, "router flagged");
+                if (!mp::make_tmap_bf16_2d(&L->tm_wplanes, L->wr_planes, 3ull * L->r_npad, L->d, L->r_npad, 64))
+                    fail(MP_ERR_CUDA, "router planes tensor map");
+            }
             L->d_nmap = dalloc<int32_t>((size_t)L->S * L->w_pad, "nmap");
             const size_t tk = (size_t)L->max_tokens * L->k_max;
             const uint32_t nblk = (L->max_tokens + mp::kRouteTokensPerBlock - 1) / mp::kRouteTokensPerBlock;
@@ -437,7 +506,6 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                           mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64);
                 if (!ok) fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
             }
-            for (auto& e : L->ev) ck(cudaEventCreate(&e), "event");
         } catch (...) {
             free_layer(L);
             throw;
@@ -561,6 +629,7 @@ MP_API mp_status mp_layer_set_router(mp_layer_t L, const float* w_r) {
         ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset");
         mp::launch_finite_check(tmp, n, L->ws.err, 0);
         mp::launch_transpose_router(tmp, L->d, L->G, L->G_pad, L->wrT, 0);
+        if (L->router_tc) mp::launch_split_router(tmp, L->d, L->G, L->r_npad, L->wr_planes, 0);
         ck_launch("router transpose");
         int flag = 0;
         ck(cudaMemcpy(&flag, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost), "flag");
@@ -707,6 +776,7 @@ MP_API mp_status mp_layer_stage_times(mp_layer_t L, char* names, size_t names_le
                                       uint32_t* n, uint32_t cap) {
     return guarded([&] {
         if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        resolve_timings(L);
         std::string all;
         for (int q = 0; q < kStages; ++q) {
             if (q) all += ",";
@@ -725,6 +795,7 @@ MP_API mp_status mp_layer_stage_times(mp_layer_t L, char* names, size_t names_le
 MP_API mp_status mp_layer_reset_stage_times(mp_layer_t L) {
     return guarded([&] {
         if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        resolve_timings(L);
         for (int q = 0; q < kStages; ++q) L->stage_ms[q] = 0, L->stage_launches[q] = 0;
     });
 }
@@ -808,5 +879,19 @@ MP_API mp_status mp_debug_buffers(mp_layer_t L, void** x_perm, void** h, void** 
             dims[2] = L->rows_cap;
             dims[3] = L->use_tc ? 1u : 0u;
         }
+    });
+}
+
+// debugging aid: fp64 K-split partials of the last tensor-core router call,
+// [ks][T][npad]; logits = sum over ks (fixed order).
+MP_API mp_status mp_debug_router_partials(mp_layer_t L, void** partial, uint32_t* ks, uint32_t* T, uint32_t* npad,
+                                          uint32_t* n_flagged) {
+    return guarded([&] {
+        if (!L || !L->router_tc) fail(MP_ERR_VALIDATION, "no tensor-core router on this layer");
+        ck(cudaMemcpy(n_flagged, L->r_flagged, sizeof(uint32_t), cudaMemcpyDeviceToHost), "flagged");
+        *partial = L->r_partial;
+        *ks = L->r_last_ks;
+        *T = L->r_last_T;
+        *npad = L->r_npad;
     });
 }

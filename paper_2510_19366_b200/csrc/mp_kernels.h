@@ -45,6 +45,26 @@ void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const 
                     const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
                     cudaStream_t s);
 
+// Tensor-core linear router (router_tc.cu): plan, weight split, launch, and
+// the fixed-order fp64 reduction of the K-split partials + top-k (route.cu).
+struct RouterTcPlan {
+    uint32_t Npad, kb_total, kb_per_split, ks, m_tiles, stages;
+    size_t smem;
+};
+RouterTcPlan plan_router_tc(uint32_t T, uint32_t d, uint32_t G, int num_sms);
+void launch_split_router(const float* wr, uint32_t d, uint32_t G, uint32_t Npad, void* planes, cudaStream_t s);
+void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const RouterTcPlan& pl, uint32_t T,
+                      double* partial, cudaStream_t s);
+// guard: tensor-core logit error bound; tokens whose k-th/(k+1)-th gap is below
+// 2*guard are appended to flagged[1..] (count in flagged[0], zeroed by the
+// caller) and re-selected from exact fp64 logits by launch_router_fixup.
+void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
+                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
+                          double guard, uint32_t* flagged, cudaStream_t s);
+void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
+                         const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
+                         const uint32_t* flagged, int num_sms, cudaStream_t s);
+
 // Packing (load time).
 void launch_pack_w1(int dtype, const float* wg, const float* wu, uint32_t d, uint32_t ff, const int32_t* nmap,
                     uint32_t S, uint32_t w_pad, uint32_t d_pad, void* W1_e, cudaStream_t s);

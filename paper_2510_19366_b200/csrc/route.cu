@@ -27,8 +27,10 @@ constexpr uint32_t kRouterThreads = 256;
 // One warp selects the k_t best of G scores for one token (score desc,
 // index asc -- inc/gating.hpp:138-141), emits them in ascending index order
 // (inc/gating.hpp:143) with their softmax-renormalised weights.
-__device__ void warp_topk_token(const double* __restrict__ sc, uint32_t G, uint32_t k, uint32_t k_max,
-                                int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row) {
+// Returns (to every lane) the gap between the k-th and (k+1)-th best score
+// (+inf when k == G): the near-tie measure of the routing contract.
+__device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uint32_t k, uint32_t k_max,
+                                  int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row) {
     const uint32_t lane = lane_id();
     constexpr int NC = kMaxG / 32;
     const uint32_t nc = (G + 31) / 32;
@@ -39,8 +41,9 @@ __device__ void warp_topk_token(const double* __restrict__ sc, uint32_t G, uint3
         const uint32_t g = lane + 32u * c;
         v[c] = (c < (int)nc && g < G) ? sc[g] : -DBL_MAX;
     }
-    double vmax = 0.0;
-    for (uint32_t r = 0; r < k; ++r) {
+    double vmax = 0.0, vk = 0.0, vk1 = -INFINITY;
+    const uint32_t rounds = k < G ? k + 1 : k;
+    for (uint32_t r = 0; r < rounds; ++r) {
         double bv = -INFINITY;
         uint32_t bi = 0xFFFFFFFFu;
 #pragma unroll
@@ -61,6 +64,11 @@ __device__ void warp_topk_token(const double* __restrict__ sc, uint32_t G, uint3
             }
         }
         if (r == 0) vmax = bv;
+        if (r == k) {  // the (k+1)-th best: measured, not taken
+            vk1 = bv;
+            break;
+        }
+        vk = bv;
         if (bi != 0xFFFFFFFFu && (bi & 31u) == lane) taken |= 1u << (bi >> 5);
     }
     // softmax over all G cancels in the renormalisation: w_g = e^(l_g - m) / sum_sel
@@ -88,6 +96,7 @@ __device__ void warp_topk_token(const double* __restrict__ sc, uint32_t G, uint3
         sel_row[j] = kSelNone;
         w_row[j] = 0.0f;
     }
+    return k < G ? vk - vk1 : INFINITY;
 }
 
 __device__ __forceinline__ uint32_t token_k(const uint32_t* kpt, uint32_t k, uint32_t t, uint32_t k_max, uint32_t G,
@@ -208,6 +217,67 @@ __global__ void __launch_bounds__(256) scores_topk_kernel(const double* __restri
                     wout + (size_t)t * k_max);
 }
 
+// Tensor-core router epilogue: logits[t][g] = sum_{s ascending} partial[s][t][g]
+// (fixed order, fp64), then the per-token top-k.  Warp per token.
+__global__ void __launch_bounds__(256) partials_topk_kernel(const double* __restrict__ partial, uint32_t ks,
+                                                            uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
+                                                            const uint32_t* __restrict__ kpt, uint32_t k_scalar,
+                                                            int weight_mode, uint32_t* __restrict__ sel,
+                                                            float* __restrict__ wout, int* __restrict__ err,
+                                                            double guard, uint32_t* __restrict__ flagged) {
+    __shared__ double sc[8][kMaxG];
+    const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t t = blockIdx.x * 8 + warp;
+    if (t >= T) return;
+    for (uint32_t g = lane; g < G; g += 32) {
+        double v = 0.0;
+        for (uint32_t s = 0; s < ks; ++s) v += partial[((size_t)s * T + t) * Npad + g];
+        sc[warp][g] = v;
+    }
+    __syncwarp();
+    const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
+    const double gap = warp_topk_token(sc[warp], G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
+                                       wout + (size_t)t * k_max);
+    // the selection is certified only when the k-th / (k+1)-th gap exceeds
+    // twice the tensor-core error bound; otherwise recompute exactly (fp64)
+    if (gap < 2.0 * guard && lane == 0) flagged[1 + atomicAdd(&flagged[0], 1u)] = t;
+}
+
+// Exact fp64 logits for the flagged tokens (x bf16/f32 . W_r fp32, products
+// exact in double, fixed-order reduction), then the top-k again.
+template <typename Tx>
+__global__ void __launch_bounds__(256) router_fixup_kernel(const Tx* __restrict__ x, uint32_t d,
+                                                           const float* __restrict__ wrT, uint32_t G, uint32_t k_max,
+                                                           const uint32_t* __restrict__ kpt, uint32_t k_scalar,
+                                                           int weight_mode, uint32_t* __restrict__ sel,
+                                                           float* __restrict__ wout, int* __restrict__ err,
+                                                           const uint32_t* __restrict__ flagged) {
+    __shared__ double lg[kMaxG];
+    __shared__ double red[256];
+    const uint32_t n = flagged[0];
+    for (uint32_t f = blockIdx.x; f < n; f += gridDim.x) {
+        const uint32_t t = flagged[1 + f];
+        const Tx* xr = x + (size_t)t * d;
+        // 256 threads: 4 threads per output over interleaved quarters of K
+        for (uint32_t g0 = 0; g0 < G; g0 += 64) {
+            const uint32_t g = g0 + threadIdx.x / 4, q = threadIdx.x % 4;
+            double acc = 0.0;
+            if (g < G)
+                for (uint32_t i = q; i < d; i += 4)
+                    acc = fma(static_cast<double>(to_f32(xr[i])), static_cast<double>(wrT[(size_t)g * d + i]), acc);
+            red[threadIdx.x] = acc;
+            __syncthreads();
+            if (q == 0 && g < G) lg[g] = ((red[threadIdx.x] + red[threadIdx.x + 1]) + red[threadIdx.x + 2]) + red[threadIdx.x + 3];
+            __syncthreads();
+        }
+        if (threadIdx.x < 32) {
+            const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
+            warp_topk_token(lg, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max);
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- bucketing
 // Per CTA of 32 tokens: selection bitmasks in smem, then one thread per
 // sub-expert walks the tokens in order -> rank of each (t, slot) inside its
@@ -280,45 +350,58 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32
                                                            uint32_t* __restrict__ offsets,
                                                            uint32_t* __restrict__ mprefix_tc,
                                                            uint32_t* __restrict__ mprefix_simt) {
-    __shared__ uint32_t totals[1024];
+    // thread (g, q): bucket g, q-th contiguous range of CTA-blocks; consecutive
+    // threads read consecutive buckets of one block row (coalesced)
+    __shared__ uint32_t part[1024];
+    __shared__ uint32_t goff[kMaxG];
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t tot;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint32_t g = warp; g < G; g += 32) {
-        uint32_t running = 0;
-        for (uint32_t b0 = 0; b0 < nblk; b0 += 32) {
-            const uint32_t b = b0 + lane;
-            const uint32_t v = b < nblk ? block_counts[(size_t)b * G + g] : 0;
-            uint32_t inc = v;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t n = __shfl_up_sync(0xffffffffu, inc, off);
-                if (lane >= (uint32_t)off) inc += n;
-            }
-            if (b < nblk) block_base[(size_t)b * G + g] = running + inc - v;
-            running += __shfl_sync(0xffffffffu, inc, 31);
+    const uint32_t Q = blockDim.x / G;
+    const uint32_t g = threadIdx.x % G, q = threadIdx.x / G;
+    const bool active = q < Q;
+    const uint32_t per = (nblk + Q - 1) / Q;
+    const uint32_t b0 = q * per, b1 = min(b0 + per, nblk);
+    uint32_t sum = 0;
+    if (active)
+        for (uint32_t b = b0; b < b1; ++b) sum += block_counts[(size_t)b * G + g];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    // exclusive prefix over the Q ranges of each bucket, and bucket totals
+    uint32_t qbase = 0, total = 0;
+    if (active) {
+        for (uint32_t r = 0; r < Q; ++r) {
+            const uint32_t v = part[r * G + g];
+            if (r < q) qbase += v;
+            total += v;
         }
-        if (lane == 0) totals[g] = running;
     }
     __syncthreads();
-    const uint32_t g = threadIdx.x;
-    const uint32_t cnt = g < G ? totals[g] : 0;
-    const uint32_t off = block_exclusive_scan_1024(cnt, &tot, wsum);
-    if (g < G) offsets[g] = off;
-    if (g == 0) offsets[G] = tot;
-    const uint32_t mt = g < G ? (cnt + kTcBM - 1) / kTcBM : 0;
+    const uint32_t gi = threadIdx.x;
+    if (active && q == 0) goff[g] = total;
+    __syncthreads();
+    const uint32_t c = gi < G ? goff[gi] : 0;
+    const uint32_t off = block_exclusive_scan_1024(c, &tot, wsum);
+    if (gi < G) offsets[gi] = off;
+    if (gi == 0) offsets[G] = tot;
+    const uint32_t mt = gi < G ? (c + kTcBM - 1) / kTcBM : 0;
     const uint32_t mpre = block_exclusive_scan_1024(mt, &tot, wsum);
-    if (g < G) mprefix_tc[g] = mpre;
-    if (g == 0) mprefix_tc[G] = tot;
-    const uint32_t ms = g < G ? (cnt + kSimtBM - 1) / kSimtBM : 0;
+    if (gi < G) mprefix_tc[gi] = mpre;
+    if (gi == 0) mprefix_tc[G] = tot;
+    const uint32_t ms = gi < G ? (c + kSimtBM - 1) / kSimtBM : 0;
     const uint32_t spre = block_exclusive_scan_1024(ms, &tot, wsum);
-    if (g < G) mprefix_simt[g] = spre;
-    if (g == 0) mprefix_simt[G] = tot;
+    if (gi < G) mprefix_simt[gi] = spre;
+    if (gi == 0) mprefix_simt[G] = tot;
     __syncthreads();
-    if (g < G) totals[g] = off;
+    if (gi < G) goff[gi] = off;
     __syncthreads();
-    for (uint32_t gg = warp; gg < G; gg += 32)
-        for (uint32_t b = lane; b < nblk; b += 32) block_base[(size_t)b * G + gg] += totals[gg];
+    if (active) {
+        uint32_t running = goff[g] + qbase;
+        for (uint32_t b = b0; b < b1; ++b) {
+            const uint32_t v = block_counts[(size_t)b * G + g];
+            block_base[(size_t)b * G + g] = running;
+            running += v;
+        }
+    }
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -331,7 +414,8 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
                                                        const uint32_t* __restrict__ lrank,
                                                        const uint32_t* __restrict__ block_base,
                                                        uint32_t* __restrict__ perm_tok, float* __restrict__ perm_w,
-                                                       uint32_t* __restrict__ slot_row, Tx* __restrict__ x_perm) {
+                                                       uint32_t* __restrict__ slot_row, Tx* __restrict__ x_perm,
+                                                       int* __restrict__ err) {
     const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32;
     const uint32_t lane = threadIdx.x & 31;
     if (t >= T) return;
@@ -347,23 +431,35 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
         slot_row[(size_t)t * k_max + j] = pos;
     }
     __syncwarp();
+    // slot positions in registers (k_max <= 64): lane j holds slots j, j + 32
+    uint32_t pos_a = lane < k_max ? slot_row[(size_t)t * k_max + lane] : kSelNone;
+    uint32_t pos_b = lane + 32 < k_max ? slot_row[(size_t)t * k_max + lane + 32] : kSelNone;
     constexpr uint32_t VE = 16 / sizeof(Tx);  // elements per 16-byte vector
     const bool vec_ok = (d % VE) == 0;
     const Tx* xr = x + (size_t)t * d;
-    for (uint32_t j = 0; j < k_max; ++j) {
-        const uint32_t pos = slot_row[(size_t)t * k_max + j];
-        if (pos == kSelNone) continue;
-        Tx* dst = x_perm + (size_t)pos * d_pad;
+    bool bad = false;
+    // each 16-byte chunk of the row is read once and stored to every bucket
+    for (uint32_t c0 = 0; c0 < d_pad; c0 += 32 * VE) {
+        const uint32_t c = c0 + lane * VE;
+        uint4 v = make_uint4(0, 0, 0, 0);
         if (vec_ok) {
-            for (uint32_t c = lane * VE; c < d_pad; c += 32 * VE) {
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (c < d) v = __ldg(reinterpret_cast<const uint4*>(xr + c));
-                *reinterpret_cast<uint4*>(dst + c) = v;
-            }
+            if (c < d) v = __ldg(reinterpret_cast<const uint4*>(xr + c));
         } else {
-            for (uint32_t c = lane; c < d_pad; c += 32) dst[c] = c < d ? xr[c] : from_f32<Tx>(0.0f);
+            Tx tmp[VE];
+#pragma unroll
+            for (uint32_t q = 0; q < VE; ++q) tmp[q] = (c + q < d) ? xr[c + q] : from_f32<Tx>(0.0f);
+            v = *reinterpret_cast<uint4*>(tmp);
+        }
+        const Tx* tv = reinterpret_cast<const Tx*>(&v);
+#pragma unroll
+        for (uint32_t q = 0; q < VE; ++q) bad |= !isfinite(to_f32(tv[q]));
+        for (uint32_t j = 0; j < k_max; ++j) {
+            const uint32_t pos = __shfl_sync(0xffffffffu, j < 32 ? pos_a : pos_b, j & 31);
+            if (pos == kSelNone) continue;
+            if (c < d_pad) *reinterpret_cast<uint4*>(x_perm + (size_t)pos * d_pad + c) = v;
         }
     }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && err) atomicOr(err, 2);
 }
 
 // ---------------------------------------------------------------- combine
@@ -482,6 +578,24 @@ void launch_router_linear(int dtype, const void* x, uint32_t T, uint32_t d, cons
     }
 }
 
+void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
+                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
+                          double guard, uint32_t* flagged, cudaStream_t s) {
+    partials_topk_kernel<<<(T + 7) / 8, 256, 0, s>>>(partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w,
+                                                     err, guard, flagged);
+}
+
+void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
+                         const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
+                         const uint32_t* flagged, int num_sms, cudaStream_t s) {
+    if (dtype == 1)
+        router_fixup_kernel<__nv_bfloat16><<<num_sms, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), d, wrT, G,
+                                                                   k_max, kpt, k, weight_mode, sel, w, err, flagged);
+    else
+        router_fixup_kernel<float><<<num_sms, 256, 0, s>>>(static_cast<const float*>(x), d, wrT, G, k_max, kpt, k,
+                                                           weight_mode, sel, w, err, flagged);
+}
+
 void launch_router_scores_topk(const float* scores, uint32_t T, uint32_t G, uint32_t k_max, const uint32_t* kpt,
                                uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err, cudaStream_t s) {
     scores_topk_kernel<<<(T + 7) / 8, 256, 0, s>>>(reinterpret_cast<const double*>(scores), T, G, k_max, kpt, k,
@@ -504,11 +618,11 @@ void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t 
     if (dtype == 1)
         dispatch_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
             static_cast<const __nv_bfloat16*>(x), T, d, d_pad, sel, w, k_max, G, ws.lrank, ws.block_base,
-            ws.perm_tok, ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm));
+            ws.perm_tok, ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), ws.err);
     else
         dispatch_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), T, d, d_pad, sel, w, k_max, G,
                                                     ws.lrank, ws.block_base, ws.perm_tok, ws.perm_w, ws.slot_row,
-                                                    static_cast<float*>(x_perm));
+                                                    static_cast<float*>(x_perm), ws.err);
 }
 
 void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,

@@ -331,4 +331,26 @@ def test_profiling_stage_times(oracle, torch_cuda):
     st = L.stage_times()
     assert set(st) == {"router", "bucket", "dispatch", "gemm1", "gemm2", "combine"}
     assert all(v[0] > 0 for v in st.values())
-    assert L.launch_count() - n0 == 7
+    assert L.launch_count() - n0 == sum(v[1] for v in st.values()) >= 7
+
+
+def test_tensor_core_router_logit_error(oracle, torch_cuda, mixtral):
+    """Accuracy of the split-bf16 tensor-core router vs the fp64 oracle logits:
+    must sit well inside the 1e-6 near-tie window of the routing contract."""
+    import ctypes as C
+    torch = torch_cuda
+    from debug_tc import as_tensor
+    from paper_2510_19366_b200 import _lib
+    L, x_dev, xb, wr, parts, ex_nm_b, logits = mixtral
+    L.route(x_dev, k=8)
+    torch.cuda.synchronize()
+    lib = _lib.load()
+    lib.mp_debug_router_partials.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)] + [C.POINTER(C.c_uint32)] * 4
+    p, ks, T, npad, nf = C.c_void_p(), C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+    _lib.check(lib.mp_debug_router_partials(L.h, C.byref(p), C.byref(ks), C.byref(T), C.byref(npad), C.byref(nf)))
+    part = as_tensor(p.value, (ks.value, T.value, npad.value), torch.float64).cpu().numpy()
+    got = part.sum(axis=0)[:, :logits.shape[1]]
+    err = np.abs(got - logits)
+    print(f"router logit error: max {err.max():.3g}, p99 {np.quantile(err, 0.99):.3g} (K splits {ks.value}); "
+          f"{nf.value}/{T.value} tokens re-selected from fp64 logits")
+    assert err.max() < 4e-6  # kRouterGuard (layer.cu): the certification bound must hold
