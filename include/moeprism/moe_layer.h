@@ -129,6 +129,10 @@ mp_status mp_layer_forward_host(mp_layer_t h, const void* x, uint32_t n_tokens, 
  * i.e. partitioned_forward semantics summed over experts. */
 mp_status mp_layer_forward_selected(mp_layer_t h, const void* x, uint32_t n_tokens, const uint32_t* sel,
                                     const float* w, void* y, uint32_t* offsets_out, void* stream);
+/* Same on HOST buffers (sel / w host too); validates the selection on the
+ * host first (range, duplicates: inc/expert.hpp:111-118), synchronises. */
+mp_status mp_layer_forward_selected_host(mp_layer_t h, const void* x, uint32_t n_tokens, const uint32_t* sel,
+                                         const float* w, void* y, void* stream);
 
 /* Router only: selection + weights (device outputs, T x k_max). */
 mp_status mp_layer_route(mp_layer_t h, const void* x, uint32_t n_tokens, const uint32_t* k_per_token, uint32_t k,

@@ -25,7 +25,7 @@ EXPORTS = (
     "mp_layer_set_router", "mp_layer_set_gates", "mp_layer_forward", "mp_layer_forward_host",
     "mp_layer_forward_selected", "mp_layer_route", "mp_layer_check_errors", "mp_layer_set_profiling",
     "mp_layer_stage_times", "mp_layer_reset_stage_times", "mp_layer_launch_count", "mp_synth_fill",
-    "mp_format_read_mpex", "mp_format_read_partition_doc", "mp_validate_partition",
+    "mp_format_read_mpex", "mp_format_read_partition_doc", "mp_validate_partition", "mp_layer_forward_selected_host",
 )
 
 
@@ -81,6 +81,7 @@ def _sig(L):
     L.mp_format_read_partition_doc.argtypes = [C.c_char_p, sz, C.POINTER(sz), C.POINTER(u64), C.POINTER(u32),
                                                C.POINTER(sz), vp, C.POINTER(u32), C.POINTER(sz), vp, vp]
     L.mp_validate_partition.argtypes = [u32, vp, sz]
+    L.mp_layer_forward_selected_host.argtypes = [vp, vp, u32, vp, vp, vp, vp]
 
 
 def load():

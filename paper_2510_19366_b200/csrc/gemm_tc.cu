@@ -45,6 +45,7 @@ struct TcParams {
     uint32_t G, K, N_group, n_valid, ld_out, NT;
     const uint32_t* offsets;
     const uint32_t* mprefix;
+    const uint32_t* perm;  // GATHER: token id of every permuted row
     __nv_bfloat16* out;
 };
 
@@ -65,7 +66,7 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
     m = local - n * mt;
 }
 
-template <bool SWIGLU>
+template <bool SWIGLU, bool GATHER>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -111,7 +112,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t nkb = p.K / BK;
 
     if (warp == 0) {
-        if (lane == 0) {
+        if constexpr (GATHER) {
+            // A rows gathered straight from the token matrix x by TMA gather4:
+            // lane q streams rows 4q..4q+3 of the tile (token ids from the
+            // bucket permutation), lane 0 arms the barrier and loads B.
+            uint32_t it = 0;
+            for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+                uint32_t g, m, n;
+                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+                const uint32_t arow = s_off[g] + m * BM;
+                const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN);
+                int32_t tok[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t r = arow + lane * 4 + j;
+                    tok[j] = r < s_off[p.G] ? static_cast<int32_t>(p.perm[r]) : 0;  // pad rows: any valid token
+                }
+                for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
+                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    if (lane == 0) {
+                        mbar_expect_tx(&full[s], STAGE_BYTES);
+                        tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow);
+                    }
+                    __syncwarp();
+                    tma_gather4(sA + s * A_BYTES + lane * 512, &tmA, &full[s], static_cast<int32_t>(kb * BK), tok);
+                }
+            }
+        } else if (lane == 0) {
             uint32_t it = 0;
             for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
                 uint32_t g, m, n;
@@ -251,7 +279,8 @@ bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t
 }
 
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s) {
+                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
+                    const uint32_t* gather_perm) {
     TcParams p;
     p.G = sh.G;
     p.K = sh.K;
@@ -261,20 +290,24 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.NT = (sh.N_group + BN - 1) / BN;
     p.offsets = offsets;
     p.mprefix = mprefix;
+    p.perm = gather_perm;
     p.out = static_cast<__nv_bfloat16*>(out);
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
     static bool attr_set = false;  // once per process (device-independent attribute)
     if (!attr_set) {
-        cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         attr_set = true;
     }
-    if (swiglu)
-        gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+    if (swiglu && gather_perm)
+        gemm_tc_kernel<true, true><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+    else if (swiglu)
+        gemm_tc_kernel<true, false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
     else
-        gemm_tc_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+        gemm_tc_kernel<false, false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
 }
 
 }  // namespace mp

@@ -100,6 +100,7 @@ struct mp_layer_s {
     size_t esz = 4;
     int num_sms = 0;
     bool use_tc = false;
+    bool gather_ok = true;  // gemm1 gathers A rows by TMA (MOEPRISM_GATHER=0 disables, diagnostics)
 
     std::vector<std::vector<uint32_t>> assignment;
     std::vector<uint8_t> has_part, packed;
@@ -297,21 +298,32 @@ void resolve_timings(mp_layer_s* L) {
 
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
-                 cudaStream_t s, StageTimer& tm) {
+                 cudaStream_t s, StageTimer& tm, bool check_finite = false) {
+    // bf16 tensor-core path: gemm1 gathers its A rows straight from x (TMA
+    // gather4), so dispatch only writes the permutation tables
+    // -- only when gemm1 has at most 2 N tiles: gather4 moves 512 B per TMA op and
+    // the A tile is re-gathered for every N tile (measured 2.3x slower than
+    // dispatch + tile loads at the Mixtral shape, 14 N tiles)
+    const bool gather = L->use_tc && L->gather_ok && L->w_pad <= 256 && (L->d % 8) == 0 &&
+                        (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+    CUtensorMap tmX;
+    if (gather && !mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 1, 64)) fail(MP_ERR_CUDA, "x gather tensor map");
     tm.begin(1);
     mp::launch_bucket_local(sel, T, L->k_max, L->G, L->ws, s);
     mp::launch_bucket_scan(T, L->G, L->ws, s);
     ck_launch("bucket");
     tm.end(1, 2);
     tm.begin(2);
-    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, L->x_perm, s);
+    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, gather ? nullptr : L->x_perm, s,
+                        check_finite || !gather);
     ck_launch("dispatch");
     tm.end(2, 1);
     mp::GemmShape g1{L->G, L->d_pad, 2 * L->w_pad, T * L->k_max, L->w_pad, 2 * L->w_pad};
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
     if (L->use_tc)
-        mp::launch_gemm_tc(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
+        mp::launch_gemm_tc(true, gather ? &tmX : &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc,
+                           L->num_sms, s, gather ? L->ws.perm_tok : nullptr);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
@@ -442,6 +454,8 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             L->use_tc = D.dtype == MP_DTYPE_BF16;
             if (const char* env = std::getenv("MOEPRISM_BF16_GEMM"))
                 if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
+            if (const char* env = std::getenv("MOEPRISM_GATHER"))
+                if (std::string(env) == "0") L->gather_ok = false;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
             L->d_pad = round_up(L->d, 64);
@@ -705,7 +719,7 @@ MP_API mp_status mp_layer_forward_host(mp_layer_t L, const void* x, uint32_t T, 
         }
         StageTimer tm(L, s);
         route(L, L->x_stage, T, kd, k, s, tm);
-        run_experts(L, L->x_stage, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, L->y_stage, s, tm);
+        run_experts(L, L->x_stage, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, L->y_stage, s, tm, true);
         ck(cudaMemcpyAsync(y, L->y_stage, xbytes, cudaMemcpyDeviceToHost, s), "y download");
         copy_outputs(L, T, sel_out, w_out, offsets_out, s, cudaMemcpyDeviceToHost);
         int flags = 0;
@@ -893,5 +907,45 @@ MP_API mp_status mp_debug_router_partials(mp_layer_t L, void** partial, uint32_t
         *ks = L->r_last_ks;
         *T = L->r_last_T;
         *npad = L->r_npad;
+    });
+}
+
+MP_API mp_status mp_layer_forward_selected_host(mp_layer_t L, const void* x, uint32_t T, const uint32_t* sel,
+                                                const float* w, void* y, void* stream) {
+    return guarded([&] {
+        if (!L || (T && (!x || !y || !sel))) fail(MP_ERR_VALIDATION, "null argument");
+        check_tokens(L, T);
+        check_ready(L);
+        if (T == 0) return;
+        // host validation with the reference's verdicts (inc/expert.hpp:111-118)
+        std::vector<uint8_t> seen(L->G);
+        for (uint32_t t = 0; t < T; ++t) {
+            std::fill(seen.begin(), seen.end(), 0);
+            for (uint32_t j = 0; j < L->k_max; ++j) {
+                const uint32_t g = sel[(size_t)t * L->k_max + j];
+                if (g == MP_SEL_NONE) continue;
+                if (g >= L->G)
+                    fail(MP_ERR_VALIDATION, "active sub-expert " + std::to_string(g % L->S) + " out of range for N=" +
+                                                std::to_string(L->S));
+                if (seen[g]) fail(MP_ERR_VALIDATION, "active sub-expert list has duplicates");
+                seen[g] = 1;
+            }
+        }
+        DeviceGuard dg(L->desc.device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const size_t xbytes = (size_t)T * L->d * L->esz;
+        const size_t sbytes = (size_t)T * L->k_max * 4;
+        ck(cudaMemsetAsync(L->ws.err, 0, sizeof(int), s), "memset err");
+        ck(cudaMemcpyAsync(L->x_stage, x, xbytes, cudaMemcpyHostToDevice, s), "x upload");
+        ck(cudaMemcpyAsync(L->sel, sel, sbytes, cudaMemcpyHostToDevice, s), "sel upload");
+        if (w) ck(cudaMemcpyAsync(L->wsel, w, sbytes, cudaMemcpyHostToDevice, s), "w upload");
+        StageTimer tm(L, s);
+        run_experts(L, L->x_stage, T, L->sel, w ? L->wsel : nullptr, w == nullptr, L->y_stage, s, tm, true);
+        ck(cudaMemcpyAsync(y, L->y_stage, xbytes, cudaMemcpyDeviceToHost, s), "y download");
+        int flags = 0;
+        ck(cudaMemcpyAsync(&flags, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost, s), "flags");
+        ck(cudaStreamSynchronize(s), "forward");
+        tm.finish(nullptr, 0);
+        raise_device_errors(flags);
     });
 }

@@ -83,6 +83,17 @@ MP_DEV void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t 
         "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+// Four arbitrary rows (row indices r[0..3], columns c0 .. c0+box) of a 2D
+// tensor map whose box is {cols, 1}: written as four consecutive tile rows,
+// swizzled exactly as a tile load would place them (verified on B200 by
+// tests/probes/probe_gather4.cu).
+MP_DEV void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, const int32_t (&r)[4]) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(smem_u32(bar))
+        : "memory");
+}
 MP_DEV void tma_load_2d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1,
                              uint64_t policy) {
     asm volatile(

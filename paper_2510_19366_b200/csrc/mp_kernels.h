@@ -38,8 +38,11 @@ void launch_proxy_scores(int dtype, const void* x, uint32_t T, uint32_t d, const
 void launch_bucket_local(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32_t G, BucketWs& ws,
                          cudaStream_t s);
 void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s);
+// x_perm == null: permutation tables only (the GEMM gathers the rows itself)
+// check_finite: also scan x for non-finite values (err bit 2)
 void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t d_pad, const uint32_t* sel,
-                     const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s);
+                     const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s,
+                     bool check_finite = true);
 // group_S > 0: unit-weight semantics, round once per parent expert (fp32 mode)
 void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
                     const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
@@ -88,8 +91,11 @@ void launch_gemm1_simt(int dtype, const void* A, const void* W1, void* H, const 
                        const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
 void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const GemmShape& sh,
                        const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
+// gather_perm != null (gemm1 only): tmA is the token matrix x (box {64, 1}) and
+// the A rows are gathered by TMA gather4 through the bucket permutation.
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s);
+                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
+                    const uint32_t* gather_perm = nullptr);
 size_t gemm_tc_smem_bytes();
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point.

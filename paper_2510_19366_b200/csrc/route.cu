@@ -244,7 +244,9 @@ __global__ void __launch_bounds__(256) partials_topk_kernel(const double* __rest
 }
 
 // Exact fp64 logits for the flagged tokens (x bf16/f32 . W_r fp32, products
-// exact in double, fixed-order reduction), then the top-k again.
+// exact in double, fixed-order reduction), then the top-k again.  CTA per
+// flagged token: the row of x is staged in smem as double, each warp owns
+// G/8 outputs and its lanes stride over K with coalesced W_r row reads.
 template <typename Tx>
 __global__ void __launch_bounds__(256) router_fixup_kernel(const Tx* __restrict__ x, uint32_t d,
                                                            const float* __restrict__ wrT, uint32_t G, uint32_t k_max,
@@ -252,25 +254,36 @@ __global__ void __launch_bounds__(256) router_fixup_kernel(const Tx* __restrict_
                                                            int weight_mode, uint32_t* __restrict__ sel,
                                                            float* __restrict__ wout, int* __restrict__ err,
                                                            const uint32_t* __restrict__ flagged) {
+    extern __shared__ double xs_d[];  // [d]
     __shared__ double lg[kMaxG];
-    __shared__ double red[256];
     const uint32_t n = flagged[0];
+    const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (uint32_t f = blockIdx.x; f < n; f += gridDim.x) {
         const uint32_t t = flagged[1 + f];
         const Tx* xr = x + (size_t)t * d;
-        // 256 threads: 4 threads per output over interleaved quarters of K
-        for (uint32_t g0 = 0; g0 < G; g0 += 64) {
-            const uint32_t g = g0 + threadIdx.x / 4, q = threadIdx.x % 4;
-            double acc = 0.0;
-            if (g < G)
-                for (uint32_t i = q; i < d; i += 4)
-                    acc = fma(static_cast<double>(to_f32(xr[i])), static_cast<double>(wrT[(size_t)g * d + i]), acc);
-            red[threadIdx.x] = acc;
-            __syncthreads();
-            if (q == 0 && g < G) lg[g] = ((red[threadIdx.x] + red[threadIdx.x + 1]) + red[threadIdx.x + 2]) + red[threadIdx.x + 3];
-            __syncthreads();
+        for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) xs_d[i] = static_cast<double>(to_f32(xr[i]));
+        __syncthreads();
+        for (uint32_t g = warp; g < G; g += 8) {
+            const float* wrow = wrT + (size_t)g * d;
+            // 8 independent accumulators so the W_r loads stay in flight;
+            // combined in a fixed order (deterministic)
+            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            uint32_t i = lane;
+            for (; i + 7 * 32 < d; i += 8 * 32) {
+                float wv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) wv[u] = __ldg(wrow + i + u * 32);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[u] = fma(xs_d[i + u * 32], static_cast<double>(wv[u]), acc[u]);
+            }
+            for (; i < d; i += 32) acc[0] = fma(xs_d[i], static_cast<double>(__ldg(wrow + i)), acc[0]);
+            double a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+            if (lane == 0) lg[g] = a;
         }
-        if (threadIdx.x < 32) {
+        __syncthreads();
+        if (warp == 0) {
             const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
             warp_topk_token(lg, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max);
         }
@@ -415,7 +428,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
                                                        const uint32_t* __restrict__ block_base,
                                                        uint32_t* __restrict__ perm_tok, float* __restrict__ perm_w,
                                                        uint32_t* __restrict__ slot_row, Tx* __restrict__ x_perm,
-                                                       int* __restrict__ err) {
+                                                       int* __restrict__ err, bool check_finite) {
     const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32;
     const uint32_t lane = threadIdx.x & 31;
     if (t >= T) return;
@@ -438,6 +451,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
     const bool vec_ok = (d % VE) == 0;
     const Tx* xr = x + (size_t)t * d;
     bool bad = false;
+    if (!x_perm && !check_finite) return;  // tables only: the GEMM gathers the rows itself
     // each 16-byte chunk of the row is read once and stored to every bucket
     for (uint32_t c0 = 0; c0 < d_pad; c0 += 32 * VE) {
         const uint32_t c = c0 + lane * VE;
@@ -453,6 +467,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
         const Tx* tv = reinterpret_cast<const Tx*>(&v);
 #pragma unroll
         for (uint32_t q = 0; q < VE; ++q) bad |= !isfinite(to_f32(tv[q]));
+        if (!x_perm) continue;
         for (uint32_t j = 0; j < k_max; ++j) {
             const uint32_t pos = __shfl_sync(0xffffffffu, j < 32 ? pos_a : pos_b, j & 31);
             if (pos == kSelNone) continue;
@@ -588,12 +603,21 @@ void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
                          const uint32_t* flagged, int num_sms, cudaStream_t s) {
+    const size_t smem = sizeof(double) * d;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(router_fixup_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        cudaFuncSetAttribute(router_fixup_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
     if (dtype == 1)
-        router_fixup_kernel<__nv_bfloat16><<<num_sms, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), d, wrT, G,
-                                                                   k_max, kpt, k, weight_mode, sel, w, err, flagged);
+        router_fixup_kernel<__nv_bfloat16><<<num_sms, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), d, wrT,
+                                                                      G, k_max, kpt, k, weight_mode, sel, w, err,
+                                                                      flagged);
     else
-        router_fixup_kernel<float><<<num_sms, 256, 0, s>>>(static_cast<const float*>(x), d, wrT, G, k_max, kpt, k,
-                                                           weight_mode, sel, w, err, flagged);
+        router_fixup_kernel<float><<<num_sms, 256, smem, s>>>(static_cast<const float*>(x), d, wrT, G, k_max, kpt, k,
+                                                              weight_mode, sel, w, err, flagged);
 }
 
 void launch_router_scores_topk(const float* scores, uint32_t T, uint32_t G, uint32_t k_max, const uint32_t* kpt,
@@ -613,16 +637,17 @@ void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s) {
 }
 
 void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t d_pad, const uint32_t* sel,
-                     const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s) {
+                     const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s,
+                     bool check_finite) {
     const dim3 grid((T + 7) / 8);
     if (dtype == 1)
         dispatch_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
             static_cast<const __nv_bfloat16*>(x), T, d, d_pad, sel, w, k_max, G, ws.lrank, ws.block_base,
-            ws.perm_tok, ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), ws.err);
+            ws.perm_tok, ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), ws.err, check_finite);
     else
         dispatch_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), T, d, d_pad, sel, w, k_max, G,
                                                     ws.lrank, ws.block_base, ws.perm_tok, ws.perm_w, ws.slot_row,
-                                                    static_cast<float*>(x_perm), ws.err);
+                                                    static_cast<float*>(x_perm), ws.err, check_finite);
 }
 
 void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
