@@ -74,7 +74,15 @@ typedef struct {
     uint32_t k_max;        /* max active sub-experts per token (<= E*S) */
     uint32_t max_tokens;   /* workspace capacity, tokens per forward */
     int32_t device;        /* CUDA device ordinal */
+    uint32_t flags;        /* MP_LAYER_* role flags (0 = full layer) */
 } mp_layer_desc;
+
+/* Role flags for expert parallelism: a replicated router-only
+ * layer routes every local token over all E*S sub-experts; an experts-only
+ * layer holds this rank's E_local experts and runs mp_layer_forward_selected
+ * on the tokens received from all ranks. */
+#define MP_LAYER_ROUTER_ONLY 1u  /* no expert storage; mp_layer_route only */
+#define MP_LAYER_EXPERTS_ONLY 2u /* no router; mp_layer_forward_selected only */
 
 /* Library / device info.  mp_device_check fails (3) unless device `dev` is an
  * sm_100 part this build has code for. */
@@ -159,6 +167,34 @@ uint64_t mp_layer_launch_count(mp_layer_t h);
  * u = stream(seed) element first+j.  Device dst. */
 mp_status mp_synth_fill(void* dst, uint32_t dtype, size_t n, uint64_t seed, uint64_t first, double scale,
                         void* stream);
+
+/* ---- expert parallelism: token dispatch / combine across ranks ----
+ * Sub-experts are sharded by parent expert: rank r owns the global ids
+ * [r * experts_per_rank * S, (r + 1) * experts_per_rank * S).  For one layer:
+ *   mp_layer_route (router-only layer) -> sel, w  [T x k_max], global ids
+ *   mp_ep_plan:    destination ranks per token (deduplicated, ascending),
+ *                  per-rank send counts (host), stable order by token
+ *   mp_ep_pack:    send rows x[t] once per destination rank, with the
+ *                  selection re-expressed in that rank's local ids + weights
+ *   -- all-to-all of rows / metadata (NCCL, by the host runtime) --
+ *   mp_layer_forward_selected (experts-only layer) on the received rows
+ *   -- all-to-all of the per-(token, rank) partial outputs back --
+ *   mp_ep_combine: y[t] = sum over destination ranks in ascending order
+ *                  (deterministic; fp32 accumulate).
+ * send_sel / send_w are [rows x k_max]; rows are grouped by destination rank
+ * in rank order, tokens ascending inside a group. */
+typedef struct mp_ep_s* mp_ep_t;
+mp_status mp_ep_create(uint32_t world, uint32_t rank, uint32_t experts_per_rank, uint32_t n_subexperts,
+                       uint32_t d_model, uint32_t k_max, uint32_t max_tokens, uint32_t dtype, int32_t device,
+                       mp_ep_t* out);
+mp_status mp_ep_destroy(mp_ep_t ep);
+/* sel: device [T x k_max] global ids.  send_counts: HOST [world] (synchronises). */
+mp_status mp_ep_plan(mp_ep_t ep, const uint32_t* sel, uint32_t n_tokens, uint32_t* send_counts, void* stream);
+/* x: device [T x d] of dtype; outputs device [sum(send_counts) x ...]. */
+mp_status mp_ep_pack(mp_ep_t ep, const void* x, const uint32_t* sel, const float* w, uint32_t n_tokens,
+                     void* send_x, uint32_t* send_sel, float* send_w, void* stream);
+/* back: device [sum(send_counts) x d] partial outputs (dtype), in send order. */
+mp_status mp_ep_combine(mp_ep_t ep, const void* back, uint32_t n_tokens, void* y, void* stream);
 
 /* Host-only readers (no GPU touched), format-compatible with the reference.
  * mp_format_read_mpex <- load_toy_expert (inc/io.hpp:225-251): call with

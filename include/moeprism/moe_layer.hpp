@@ -127,7 +127,7 @@ public:
     explicit MoeLayer(const LayerConfig& c) : cfg_(c) {
         const mp_layer_desc d{c.n_experts, c.n_subexperts, c.d_model, c.d_ff, static_cast<std::uint32_t>(c.dtype),
                               static_cast<std::uint32_t>(c.router), static_cast<std::uint32_t>(c.weights), c.k_max,
-                              c.max_tokens, c.device};
+                              c.max_tokens, c.device, 0u};
         detail::check(mp_layer_create(&d, &h_));
     }
     ~MoeLayer() {

@@ -16,6 +16,7 @@ MP_DTYPE_F32, MP_DTYPE_BF16 = 0, 1
 MP_ROUTER_LINEAR, MP_ROUTER_PROXY = 0, 1
 MP_WEIGHT_UNIT, MP_WEIGHT_SOFTMAX_RENORM = 0, 1
 MP_SEL_NONE = 0xFFFFFFFF
+MP_LAYER_ROUTER_ONLY, MP_LAYER_EXPERTS_ONLY = 1, 2
 
 # The exported C-ABI (include/moeprism/moe_layer.h); tests check the .so
 # exports every one of these.
@@ -26,6 +27,7 @@ EXPORTS = (
     "mp_layer_forward_selected", "mp_layer_route", "mp_layer_check_errors", "mp_layer_set_profiling",
     "mp_layer_stage_times", "mp_layer_reset_stage_times", "mp_layer_launch_count", "mp_synth_fill",
     "mp_format_read_mpex", "mp_format_read_partition_doc", "mp_validate_partition", "mp_layer_forward_selected_host",
+    "mp_ep_create", "mp_ep_destroy", "mp_ep_plan", "mp_ep_pack", "mp_ep_combine",
 )
 
 
@@ -45,7 +47,7 @@ class LayerDesc(C.Structure):
     _fields_ = [
         ("n_experts", C.c_uint32), ("n_subexperts", C.c_uint32), ("d_model", C.c_uint32), ("d_ff", C.c_uint32),
         ("dtype", C.c_uint32), ("router_mode", C.c_uint32), ("weight_mode", C.c_uint32), ("k_max", C.c_uint32),
-        ("max_tokens", C.c_uint32), ("device", C.c_int32),
+        ("max_tokens", C.c_uint32), ("device", C.c_int32), ("flags", C.c_uint32),
     ]
 
 
@@ -82,6 +84,11 @@ def _sig(L):
                                                C.POINTER(sz), vp, C.POINTER(u32), C.POINTER(sz), vp, vp]
     L.mp_validate_partition.argtypes = [u32, vp, sz]
     L.mp_layer_forward_selected_host.argtypes = [vp, vp, u32, vp, vp, vp, vp]
+    L.mp_ep_create.argtypes = [u32, u32, u32, u32, u32, u32, u32, u32, i32, C.POINTER(vp)]
+    L.mp_ep_destroy.argtypes = [vp]
+    L.mp_ep_plan.argtypes = [vp, vp, u32, vp, vp]
+    L.mp_ep_pack.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp]
+    L.mp_ep_combine.argtypes = [vp, vp, u32, vp, vp]
 
 
 def load():

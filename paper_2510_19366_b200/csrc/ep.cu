@@ -1,0 +1,270 @@
+// ep.cu -- expert-parallel token dispatch / combine.
+//
+// Sub-experts are sharded by parent expert: rank r owns global ids
+// [r*epr*S, (r+1)*epr*S).  A token is sent ONCE to every rank owning at least
+// one of its selected sub-experts (dedup), together with its selection
+// re-expressed in that rank's local ids and the combine weights; the owner
+// returns one weighted partial per (token, rank) and the source sums them in
+// ascending rank order (deterministic).  The per-destination ordering reuses
+// the layer's bucketing kernels (buckets = ranks, stable by token), so send
+// rows are grouped by rank, tokens ascending -- the layout an NCCL
+// all-to-allv (grouped ncclSend/ncclRecv) consumes directly.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "moeprism/moe_layer.h"
+#include "mp_common.cuh"
+#include "mp_kernels.h"
+
+#define MP_API extern "C" __attribute__((visibility("default")))
+
+namespace mp {
+namespace {
+
+// dest[t][0..world): ascending destination ranks of token t, MP_SEL_NONE padded
+__global__ void ep_dest_kernel(const uint32_t* __restrict__ sel, uint32_t T, uint32_t k_max, uint32_t per_rank,
+                               uint32_t world, uint32_t* __restrict__ dest) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    uint32_t mask = 0;  // world <= 32
+    for (uint32_t j = 0; j < k_max; ++j) {
+        const uint32_t g = sel[(size_t)t * k_max + j];
+        if (g != kSelNone) mask |= 1u << min(g / per_rank, 31u);
+    }
+    uint32_t n = 0;
+    for (uint32_t r = 0; r < world; ++r)
+        if ((mask >> r) & 1u) dest[(size_t)t * world + n++] = r;
+    for (; n < world; ++n) dest[(size_t)t * world + n] = kSelNone;
+}
+
+template <typename Tx>
+__global__ void __launch_bounds__(256) ep_pack_kernel(const Tx* __restrict__ x, const uint32_t* __restrict__ sel,
+                                                      const float* __restrict__ w, uint32_t T, uint32_t d,
+                                                      uint32_t k_max, uint32_t per_rank, uint32_t world,
+                                                      const uint32_t* __restrict__ dest,
+                                                      const uint32_t* __restrict__ slot_row, Tx* __restrict__ send_x,
+                                                      uint32_t* __restrict__ send_sel, float* __restrict__ send_w) {
+    const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32;
+    const uint32_t lane = threadIdx.x & 31;
+    if (t >= T) return;
+    for (uint32_t j = 0; j < world; ++j) {
+        const uint32_t r = dest[(size_t)t * world + j];
+        if (r == kSelNone) break;
+        const uint32_t pos = slot_row[(size_t)t * world + j];
+        // metadata: the token's selection restricted to rank r, local ids
+        if (lane == 0) {
+            uint32_t n = 0;
+            for (uint32_t q = 0; q < k_max; ++q) {
+                const uint32_t g = sel[(size_t)t * k_max + q];
+                if (g != kSelNone && g / per_rank == r) {
+                    send_sel[(size_t)pos * k_max + n] = g - r * per_rank;
+                    send_w[(size_t)pos * k_max + n] = w ? w[(size_t)t * k_max + q] : 1.0f;
+                    ++n;
+                }
+            }
+            for (; n < k_max; ++n) {
+                send_sel[(size_t)pos * k_max + n] = kSelNone;
+                send_w[(size_t)pos * k_max + n] = 0.0f;
+            }
+        }
+        // the row itself, 16-byte vectors when aligned
+        constexpr uint32_t VE = 16 / sizeof(Tx);
+        const Tx* src = x + (size_t)t * d;
+        Tx* dst = send_x + (size_t)pos * d;
+        if ((d % VE) == 0) {
+            for (uint32_t c = lane * VE; c < d; c += 32 * VE)
+                *reinterpret_cast<uint4*>(dst + c) = __ldg(reinterpret_cast<const uint4*>(src + c));
+        } else {
+            for (uint32_t c = lane; c < d; c += 32) dst[c] = src[c];
+        }
+    }
+}
+
+template <typename Tx>
+__global__ void __launch_bounds__(256) ep_combine_kernel(const Tx* __restrict__ back, uint32_t T, uint32_t d,
+                                                         uint32_t world, const uint32_t* __restrict__ slot_row,
+                                                         Tx* __restrict__ y) {
+    __shared__ uint32_t rows[32];
+    const uint32_t t = blockIdx.x;
+    if (threadIdx.x < world) rows[threadIdx.x] = slot_row[(size_t)t * world + threadIdx.x];
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < d; c += blockDim.x) {
+        float acc = 0.0f;  // partials summed in ascending rank order
+        for (uint32_t j = 0; j < world; ++j) {
+            const uint32_t r = rows[j];
+            if (r == kSelNone) break;
+            acc += to_f32(back[(size_t)r * d + c]);
+        }
+        y[(size_t)t * d + c] = from_f32<Tx>(acc);
+    }
+}
+
+}  // namespace
+}  // namespace mp
+
+struct mp_ep_s {
+    uint32_t world, rank, epr, S, d, k_max, max_tokens, dtype;
+    int device;
+    uint32_t* dest = nullptr;
+    mp::BucketWs ws{};
+    uint32_t last_T = 0;
+};
+
+namespace {
+thread_local std::string g_ep_err;
+struct EpErr {
+    int code;
+    std::string msg;
+};
+[[noreturn]] void ep_fail(int code, const std::string& m) { throw EpErr{code, m}; }
+void ep_ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) ep_fail(MP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+template <class F>
+int ep_guarded(F&& f);
+void ep_free(mp_ep_s* E) {
+    void* ptrs[] = {E->dest, E->ws.lrank, E->ws.block_counts, E->ws.block_base, E->ws.offsets, E->ws.mprefix_tc,
+                    E->ws.mprefix_simt, E->ws.perm_tok, E->ws.perm_w, E->ws.slot_row, E->ws.err};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    delete E;
+}
+template <class T>
+T* ep_alloc(size_t n) {
+    void* p = nullptr;
+    ep_ck(cudaMalloc(&p, (n ? n : 1) * sizeof(T)), "ep alloc");
+    return static_cast<T*>(p);
+}
+}  // namespace
+
+// Errors surface through mp_last_error(); layer.cu owns that buffer, so the
+// EP entry points report through a setter it exports.
+extern "C" void mp_internal_set_error(const char* msg);
+
+namespace {
+template <class F>
+int ep_guarded(F&& f) {
+    try {
+        f();
+        return MP_OK;
+    } catch (const EpErr& e) {
+        mp_internal_set_error(e.msg.c_str());
+        return e.code;
+    }
+}
+}  // namespace
+
+MP_API mp_status mp_ep_create(uint32_t world, uint32_t rank, uint32_t epr, uint32_t S, uint32_t d, uint32_t k_max,
+                              uint32_t max_tokens, uint32_t dtype, int32_t device, mp_ep_t* out) {
+    return ep_guarded([&] {
+        if (!out) ep_fail(MP_ERR_VALIDATION, "null argument");
+        if (world < 1 || world > 32 || rank >= world) ep_fail(MP_ERR_VALIDATION, "bad world / rank");
+        if (epr < 1 || S < 1 || d < 1 || k_max < 1 || k_max > 64 || max_tokens < 1)
+            ep_fail(MP_ERR_VALIDATION, "bad expert-parallel shape");
+        if (dtype != MP_DTYPE_F32 && dtype != MP_DTYPE_BF16) ep_fail(MP_ERR_VALIDATION, "unknown dtype");
+        ep_ck(cudaSetDevice(device), "cudaSetDevice");
+        auto* E = new mp_ep_s{world, rank, epr, S, d, k_max, max_tokens, dtype, device};
+        try {
+            const size_t tw = (size_t)max_tokens * world;
+            const uint32_t nblk = (max_tokens + mp::kRouteTokensPerBlock - 1) / mp::kRouteTokensPerBlock;
+            E->dest = ep_alloc<uint32_t>(tw);
+            E->ws.lrank = ep_alloc<uint32_t>(tw);
+            E->ws.block_counts = ep_alloc<uint32_t>((size_t)nblk * world);
+            E->ws.block_base = ep_alloc<uint32_t>((size_t)nblk * world);
+            E->ws.offsets = ep_alloc<uint32_t>(world + 1);
+            E->ws.mprefix_tc = ep_alloc<uint32_t>(world + 1);
+            E->ws.mprefix_simt = ep_alloc<uint32_t>(world + 1);
+            E->ws.perm_tok = ep_alloc<uint32_t>(tw);
+            E->ws.perm_w = ep_alloc<float>(tw);
+            E->ws.slot_row = ep_alloc<uint32_t>(tw);
+            E->ws.err = ep_alloc<int>(1);
+            ep_ck(cudaMemset(E->ws.err, 0, sizeof(int)), "memset");
+        } catch (...) {
+            ep_free(E);
+            throw;
+        }
+        *out = E;
+    });
+}
+
+MP_API mp_status mp_ep_destroy(mp_ep_t E) {
+    return ep_guarded([&] {
+        if (E) {
+            cudaSetDevice(E->device);
+            cudaDeviceSynchronize();
+            ep_free(E);
+        }
+    });
+}
+
+MP_API mp_status mp_ep_plan(mp_ep_t E, const uint32_t* sel, uint32_t T, uint32_t* send_counts, void* stream) {
+    return ep_guarded([&] {
+        if (!E || !send_counts || (T && !sel)) ep_fail(MP_ERR_VALIDATION, "null argument");
+        if (T > E->max_tokens) ep_fail(MP_ERR_VALIDATION, "n_tokens exceeds max_tokens");
+        E->last_T = T;
+        if (T == 0) {
+            for (uint32_t r = 0; r < E->world; ++r) send_counts[r] = 0;
+            return;
+        }
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        mp::launch_ep_dest(sel, T, E->k_max, E->epr * E->S, E->world, E->dest, s);
+        mp::launch_bucket_local(E->dest, T, E->world, E->world, E->ws, s);
+        mp::launch_bucket_scan(T, E->world, E->ws, s);
+        ep_ck(cudaGetLastError(), "ep plan");
+        std::vector<uint32_t> off(E->world + 1);
+        ep_ck(cudaMemcpyAsync(off.data(), E->ws.offsets, (E->world + 1) * 4, cudaMemcpyDeviceToHost, s), "counts");
+        ep_ck(cudaStreamSynchronize(s), "ep plan sync");
+        for (uint32_t r = 0; r < E->world; ++r) send_counts[r] = off[r + 1] - off[r];
+    });
+}
+
+MP_API mp_status mp_ep_pack(mp_ep_t E, const void* x, const uint32_t* sel, const float* w, uint32_t T, void* send_x,
+                            uint32_t* send_sel, float* send_w, void* stream) {
+    return ep_guarded([&] {
+        if (!E || (T && (!x || !sel || !send_x || !send_sel || !send_w))) ep_fail(MP_ERR_VALIDATION, "null argument");
+        if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_pack must follow mp_ep_plan for the same tokens");
+        if (T == 0) return;
+        mp::launch_ep_pack(E->dtype, x, sel, w, T, E->d, E->k_max, E->epr * E->S, E->world, E->dest, E->ws.slot_row,
+                           send_x, send_sel, send_w, static_cast<cudaStream_t>(stream));
+        ep_ck(cudaGetLastError(), "ep pack");
+    });
+}
+
+MP_API mp_status mp_ep_combine(mp_ep_t E, const void* back, uint32_t T, void* y, void* stream) {
+    return ep_guarded([&] {
+        if (!E || (T && (!back || !y))) ep_fail(MP_ERR_VALIDATION, "null argument");
+        if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_combine must follow mp_ep_plan for the same tokens");
+        if (T == 0) return;
+        mp::launch_ep_combine(E->dtype, back, T, E->d, E->world, E->ws.slot_row, y, static_cast<cudaStream_t>(stream));
+        ep_ck(cudaGetLastError(), "ep combine");
+    });
+}
+
+namespace mp {
+void launch_ep_dest(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32_t per_rank, uint32_t world, uint32_t* dest,
+                    cudaStream_t s) {
+    ep_dest_kernel<<<(T + 255) / 256, 256, 0, s>>>(sel, T, k_max, per_rank, world, dest);
+}
+void launch_ep_pack(int dtype, const void* x, const uint32_t* sel, const float* w, uint32_t T, uint32_t d,
+                    uint32_t k_max, uint32_t per_rank, uint32_t world, const uint32_t* dest, const uint32_t* slot_row,
+                    void* send_x, uint32_t* send_sel, float* send_w, cudaStream_t s) {
+    if (dtype == 1)
+        ep_pack_kernel<__nv_bfloat16><<<(T + 7) / 8, 256, 0, s>>>(
+            static_cast<const __nv_bfloat16*>(x), sel, w, T, d, k_max, per_rank, world, dest, slot_row,
+            static_cast<__nv_bfloat16*>(send_x), send_sel, send_w);
+    else
+        ep_pack_kernel<float><<<(T + 7) / 8, 256, 0, s>>>(static_cast<const float*>(x), sel, w, T, d, k_max, per_rank,
+                                                          world, dest, slot_row, static_cast<float*>(send_x),
+                                                          send_sel, send_w);
+}
+void launch_ep_combine(int dtype, const void* back, uint32_t T, uint32_t d, uint32_t world, const uint32_t* slot_row,
+                       void* y, cudaStream_t s) {
+    if (dtype == 1)
+        ep_combine_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(back), T, d, world,
+                                                           slot_row, static_cast<__nv_bfloat16*>(y));
+    else
+        ep_combine_kernel<float><<<T, 256, 0, s>>>(static_cast<const float*>(back), T, d, world, slot_row,
+                                                   static_cast<float*>(y));
+}
+}  // namespace mp

@@ -100,7 +100,8 @@ struct mp_layer_s {
     size_t esz = 4;
     int num_sms = 0;
     bool use_tc = false;
-    bool gather_ok = true;  // gemm1 gathers A rows by TMA (MOEPRISM_GATHER=0 disables, diagnostics)
+    bool gather_ok = true;
+    bool has_experts = true, has_router = true;  // MP_LAYER_* role flags  // gemm1 gathers A rows by TMA (MOEPRISM_GATHER=0 disables, diagnostics)
 
     std::vector<std::vector<uint32_t>> assignment;
     std::vector<uint8_t> has_part, packed;
@@ -242,6 +243,7 @@ void pack_gates(mp_layer_s* L) {
 }
 
 void check_ready(mp_layer_s* L) {
+    if (!L->has_experts) fail(MP_ERR_VALIDATION, "router-only layer (MP_LAYER_ROUTER_ONLY) has no experts");
     for (uint32_t e = 0; e < L->E; ++e)
         if (!L->packed[e])
             fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " is not ready (weights and partition required)");
@@ -357,6 +359,7 @@ void route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
         ck_launch("router(proxy)");
         tm.end(0, 2);
     } else {
+        if (!L->has_router) fail(MP_ERR_VALIDATION, "experts-only layer (MP_LAYER_EXPERTS_ONLY) has no router");
         if (!L->router_set) fail(MP_ERR_VALIDATION, "router weights not set (mp_layer_set_router)");
         if (L->router_tc && (reinterpret_cast<uintptr_t>(x) % 16) == 0) {
             const mp::RouterTcPlan pl = mp::plan_router_tc(T, L->d, L->G, L->num_sms);
@@ -434,6 +437,9 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
         if (D.router_mode > MP_ROUTER_PROXY || D.weight_mode > MP_WEIGHT_SOFTMAX_RENORM)
             fail(MP_ERR_VALIDATION, "unknown router / weight mode");
         if (D.max_tokens < 1) fail(MP_ERR_VALIDATION, "max_tokens must be >= 1");
+        if (D.flags & ~(MP_LAYER_ROUTER_ONLY | MP_LAYER_EXPERTS_ONLY) ||
+            D.flags == (MP_LAYER_ROUTER_ONLY | MP_LAYER_EXPERTS_ONLY))
+            fail(MP_ERR_VALIDATION, "invalid layer role flags");
         {
             int rc = mp_device_check(D.device);
             if (rc) fail(rc, g_err);
@@ -471,54 +477,65 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             L->gate_r.assign(L->E, 0);
             L->gates.resize(L->E);
             L->has_gates.assign(L->E, 0);
-            const size_t w1 = (size_t)L->G * 2 * L->w_pad * L->d_pad;
-            const size_t w2 = (size_t)L->w2_rows * L->w_pad;
-            L->W1 = dalloc<char>(w1 * L->esz, "W1");
-            L->W2 = dalloc<char>(w2 * L->esz, "W2");
-            ck(cudaMemset(L->W2, 0, w2 * L->esz), "memset W2");
-            L->wrT = dalloc<float>((size_t)L->G_pad * L->d, "router");
-            L->router_tc = D.dtype == MP_DTYPE_BF16 && (L->d % 8) == 0 && D.router_mode == MP_ROUTER_LINEAR;
-            if (const char* env = std::getenv("MOEPRISM_ROUTER"))
-                if (std::string(env) == "simt") L->router_tc = false;  // diagnostics only
-            if (L->router_tc) {
-                L->r_npad = round_up(L->G, 32);
-                const uint32_t n_chunks = (L->d + 255) / 256;  // upper bound of the router's K splits
-                L->wr_planes = dalloc<char>((size_t)3 * L->r_npad * L->d * 2, "router planes");
-                L->r_partial = dalloc<double>((size_t)n_chunks * L->max_tokens * L->r_npad, "router partials");
-                L->r_flagged = dalloc<uint32_t>((size_t)L->max_tokens + 1, "router flagged");
-                if (!mp::make_tmap_bf16_2d(&L->tm_wplanes, L->wr_planes, 3ull * L->r_npad, L->d, L->r_npad, 64))
-                    fail(MP_ERR_CUDA, "router planes tensor map");
+            const bool experts = !(D.flags & MP_LAYER_ROUTER_ONLY);
+            const bool router = !(D.flags & MP_LAYER_EXPERTS_ONLY);
+            L->has_experts = experts;
+            L->has_router = router;
+            if (experts) {
+                const size_t w1 = (size_t)L->G * 2 * L->w_pad * L->d_pad;
+                const size_t w2 = (size_t)L->w2_rows * L->w_pad;
+                L->W1 = dalloc<char>(w1 * L->esz, "W1");
+                L->W2 = dalloc<char>(w2 * L->esz, "W2");
+                ck(cudaMemset(L->W2, 0, w2 * L->esz), "memset W2");
+                L->d_nmap = dalloc<int32_t>((size_t)L->S * L->w_pad, "nmap");
             }
-            L->d_nmap = dalloc<int32_t>((size_t)L->S * L->w_pad, "nmap");
+            if (router) {
+                L->wrT = dalloc<float>((size_t)L->G_pad * L->d, "router");
+                L->router_tc = D.dtype == MP_DTYPE_BF16 && (L->d % 8) == 0 && D.router_mode == MP_ROUTER_LINEAR;
+                if (const char* env = std::getenv("MOEPRISM_ROUTER"))
+                    if (std::string(env) == "simt") L->router_tc = false;  // diagnostics only
+                if (L->router_tc) {
+                    L->r_npad = round_up(L->G, 32);
+                    const uint32_t n_chunks = (L->d + 255) / 256;  // upper bound of the router's K splits
+                    L->wr_planes = dalloc<char>((size_t)3 * L->r_npad * L->d * 2, "router planes");
+                    L->r_partial = dalloc<double>((size_t)n_chunks * L->max_tokens * L->r_npad, "router partials");
+                    L->r_flagged = dalloc<uint32_t>((size_t)L->max_tokens + 1, "router flagged");
+                    if (!mp::make_tmap_bf16_2d(&L->tm_wplanes, L->wr_planes, 3ull * L->r_npad, L->d, L->r_npad, 64))
+                        fail(MP_ERR_CUDA, "router planes tensor map");
+                }
+                if (D.router_mode == MP_ROUTER_PROXY) L->gate_off = dalloc<uint32_t>(L->G + 1, "gate offsets");
+            }
             const size_t tk = (size_t)L->max_tokens * L->k_max;
             const uint32_t nblk = (L->max_tokens + mp::kRouteTokensPerBlock - 1) / mp::kRouteTokensPerBlock;
             L->sel = dalloc<uint32_t>(tk, "sel");
             L->wsel = dalloc<float>(tk, "w");
             L->kpt_dev = dalloc<uint32_t>(L->max_tokens, "k per token");
-            L->ws.lrank = dalloc<uint32_t>(tk, "lrank");
-            L->ws.block_counts = dalloc<uint32_t>((size_t)nblk * L->G, "block counts");
-            L->ws.block_base = dalloc<uint32_t>((size_t)nblk * L->G, "block base");
-            L->ws.offsets = dalloc<uint32_t>(L->G + 1, "offsets");
-            L->ws.mprefix_tc = dalloc<uint32_t>(L->G + 1, "mprefix");
-            L->ws.mprefix_simt = dalloc<uint32_t>(L->G + 1, "mprefix");
-            L->ws.perm_tok = dalloc<uint32_t>(L->rows_cap, "perm");
-            L->ws.perm_w = dalloc<float>(L->rows_cap, "perm w");
-            L->ws.slot_row = dalloc<uint32_t>(tk, "slot row");
             L->ws.err = dalloc<int>(1, "err");
             ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset err");
-            L->x_perm = dalloc<char>((size_t)L->rows_cap * L->d_pad * L->esz, "x_perm");
-            L->h = dalloc<char>((size_t)L->rows_cap * L->w_pad * L->esz, "h");
-            // fp32 mode keeps sub-expert outputs in double until the combine rounds them
-            L->o = dalloc<char>((size_t)L->rows_cap * L->d_pad * (L->dtype == MP_DTYPE_F32 ? 8 : L->esz), "o");
             L->x_stage = dalloc<char>((size_t)L->max_tokens * L->d * L->esz, "x stage");
-            L->y_stage = dalloc<char>((size_t)L->max_tokens * L->d * L->esz, "y stage");
-            if (D.router_mode == MP_ROUTER_PROXY) L->gate_off = dalloc<uint32_t>(L->G + 1, "gate offsets");
-            if (L->use_tc) {
-                bool ok = mp::make_tmap_bf16_2d(&L->tm_xperm, L->x_perm, L->rows_cap, L->d_pad, 128, 64) &&
-                          mp::make_tmap_bf16_2d(&L->tm_w1, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 256, 64) &&
-                          mp::make_tmap_bf16_2d(&L->tm_h, L->h, L->rows_cap, L->w_pad, 128, 64) &&
-                          mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64);
-                if (!ok) fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+            if (experts) {
+                L->ws.lrank = dalloc<uint32_t>(tk, "lrank");
+                L->ws.block_counts = dalloc<uint32_t>((size_t)nblk * L->G, "block counts");
+                L->ws.block_base = dalloc<uint32_t>((size_t)nblk * L->G, "block base");
+                L->ws.offsets = dalloc<uint32_t>(L->G + 1, "offsets");
+                L->ws.mprefix_tc = dalloc<uint32_t>(L->G + 1, "mprefix");
+                L->ws.mprefix_simt = dalloc<uint32_t>(L->G + 1, "mprefix");
+                L->ws.perm_tok = dalloc<uint32_t>(L->rows_cap, "perm");
+                L->ws.perm_w = dalloc<float>(L->rows_cap, "perm w");
+                L->ws.slot_row = dalloc<uint32_t>(tk, "slot row");
+                L->x_perm = dalloc<char>((size_t)L->rows_cap * L->d_pad * L->esz, "x_perm");
+                L->h = dalloc<char>((size_t)L->rows_cap * L->w_pad * L->esz, "h");
+                // fp32 mode keeps sub-expert outputs in double until the combine rounds them
+                L->o = dalloc<char>((size_t)L->rows_cap * L->d_pad * (L->dtype == MP_DTYPE_F32 ? 8 : L->esz), "o");
+                L->y_stage = dalloc<char>((size_t)L->max_tokens * L->d * L->esz, "y stage");
+                if (L->use_tc) {
+                    bool ok =
+                        mp::make_tmap_bf16_2d(&L->tm_xperm, L->x_perm, L->rows_cap, L->d_pad, 128, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_w1, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 256, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_h, L->h, L->rows_cap, L->w_pad, 128, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64);
+                    if (!ok) fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                }
             }
         } catch (...) {
             free_layer(L);
@@ -548,6 +565,7 @@ MP_API mp_status mp_layer_load_expert(mp_layer_t L, uint32_t e, const float* wg,
     return guarded([&] {
         if (!L || !wg || !wu || !wd) fail(MP_ERR_VALIDATION, "null argument");
         if (e >= L->E) fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " out of range");
+        if (!L->has_experts) fail(MP_ERR_VALIDATION, "router-only layer holds no expert weights");
         DeviceGuard dg(L->desc.device);
         const size_t n = (size_t)L->d * L->ff;
         if (!L->raw[e]) L->raw[e] = dalloc<float>(3 * n, "expert staging");
@@ -632,6 +650,7 @@ MP_API mp_status mp_layer_load_partition_map(mp_layer_t L, const char* path) {
 MP_API mp_status mp_layer_set_router(mp_layer_t L, const float* w_r) {
     return guarded([&] {
         if (!L || !w_r) fail(MP_ERR_VALIDATION, "null argument");
+        if (!L->has_router) fail(MP_ERR_VALIDATION, "experts-only layer has no router");
         DeviceGuard dg(L->desc.device);
         const size_t n = (size_t)L->d * L->G;
         float* tmp = dalloc<float>(n, "router staging");
@@ -949,3 +968,6 @@ MP_API mp_status mp_layer_forward_selected_host(mp_layer_t L, const void* x, uin
         raise_device_errors(flags);
     });
 }
+
+// error channel shared with the other C-ABI translation units (ep.cu)
+extern "C" void mp_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }

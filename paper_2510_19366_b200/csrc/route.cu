@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(256) partials_topk_kernel(const double* __rest
 // flagged token: the row of x is staged in smem as double, each warp owns
 // G/8 outputs and its lanes stride over K with coalesced W_r row reads.
 template <typename Tx>
-__global__ void __launch_bounds__(256) router_fixup_kernel(const Tx* __restrict__ x, uint32_t d,
+__global__ void __launch_bounds__(1024) router_fixup_kernel(const Tx* __restrict__ x, uint32_t d,
                                                            const float* __restrict__ wrT, uint32_t G, uint32_t k_max,
                                                            const uint32_t* __restrict__ kpt, uint32_t k_scalar,
                                                            int weight_mode, uint32_t* __restrict__ sel,
@@ -263,20 +263,37 @@ __global__ void __launch_bounds__(256) router_fixup_kernel(const Tx* __restrict_
         const Tx* xr = x + (size_t)t * d;
         for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) xs_d[i] = static_cast<double>(to_f32(xr[i]));
         __syncthreads();
-        for (uint32_t g = warp; g < G; g += 8) {
+        const uint32_t nwarps = blockDim.x / 32;
+        for (uint32_t g = warp; g < G; g += nwarps) {
             const float* wrow = wrT + (size_t)g * d;
-            // 8 independent accumulators so the W_r loads stay in flight;
+            // float4 loads, 8 in flight per lane, 8 independent accumulators
             // combined in a fixed order (deterministic)
             double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            uint32_t i = lane;
-            for (; i + 7 * 32 < d; i += 8 * 32) {
-                float wv[8];
+            const uint32_t d4 = (d % 4 == 0) ? d / 4 : 0;
+            const float4* w4 = reinterpret_cast<const float4*>(wrow);
+            uint32_t i4 = lane;
+            for (; i4 + 7 * 32 < d4; i4 += 8 * 32) {
+                float4 wv[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) wv[u] = __ldg(wrow + i + u * 32);
+                for (int u = 0; u < 8; ++u) wv[u] = __ldg(w4 + i4 + u * 32);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) acc[u] = fma(xs_d[i + u * 32], static_cast<double>(wv[u]), acc[u]);
+                for (int u = 0; u < 8; ++u) {
+                    const double* xd = xs_d + 4 * (i4 + u * 32);
+                    acc[u] = fma(xd[0], (double)wv[u].x, acc[u]);
+                    acc[u] = fma(xd[1], (double)wv[u].y, acc[u]);
+                    acc[u] = fma(xd[2], (double)wv[u].z, acc[u]);
+                    acc[u] = fma(xd[3], (double)wv[u].w, acc[u]);
+                }
             }
-            for (; i < d; i += 32) acc[0] = fma(xs_d[i], static_cast<double>(__ldg(wrow + i)), acc[0]);
+            for (; i4 < d4; i4 += 32) {
+                const float4 wv = __ldg(w4 + i4);
+                const double* xd = xs_d + 4 * i4;
+                acc[0] = fma(xd[0], (double)wv.x, acc[0]);
+                acc[0] = fma(xd[1], (double)wv.y, acc[0]);
+                acc[0] = fma(xd[2], (double)wv.z, acc[0]);
+                acc[0] = fma(xd[3], (double)wv.w, acc[0]);
+            }
+            for (uint32_t i = 4 * d4 + lane; i < d; i += 32) acc[1] = fma(xs_d[i], (double)__ldg(wrow + i), acc[1]);
             double a = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
@@ -612,11 +629,11 @@ void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT,
         attr = true;
     }
     if (dtype == 1)
-        router_fixup_kernel<__nv_bfloat16><<<num_sms, 256, smem, s>>>(static_cast<const __nv_bfloat16*>(x), d, wrT,
+        router_fixup_kernel<__nv_bfloat16><<<num_sms, 1024, smem, s>>>(static_cast<const __nv_bfloat16*>(x), d, wrT,
                                                                       G, k_max, kpt, k, weight_mode, sel, w, err,
                                                                       flagged);
     else
-        router_fixup_kernel<float><<<num_sms, 256, smem, s>>>(static_cast<const float*>(x), d, wrT, G, k_max, kpt, k,
+        router_fixup_kernel<float><<<num_sms, 1024, smem, s>>>(static_cast<const float*>(x), d, wrT, G, k_max, kpt, k,
                                                               weight_mode, sel, w, err, flagged);
 }
 

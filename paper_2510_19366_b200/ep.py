@@ -1,0 +1,151 @@
+"""Expert parallelism across GPUs: one process per GPU, the
+parent experts sharded over the ranks, NCCL all-to-all(v) for the token
+dispatch and the partial-output return.
+
+Per layer and rank (T local tokens):
+  1. route      replicated router-only layer: sel, w [T x k_max] (global ids)
+  2. plan       mp_ep_plan: destination ranks per token (dedup), send counts
+  3. pack       mp_ep_pack: each token row once per destination rank, with its
+                selection in that rank's local ids and its combine weights
+  4. exchange   all_to_all_single of counts, rows and metadata (NCCL/NVLink)
+  5. experts    experts-only layer: mp_layer_forward_selected on the received
+                rows -> one weighted partial per (token, rank)
+  6. return     all_to_all_single of the partials back to the token owners
+  7. combine    mp_ep_combine: y[t] = sum of partials in ascending rank order
+
+PyTorch is the plumbing (process group, NCCL collectives, buffers); every
+data-path computation runs in libmoeprism_b200.so.  The exchange logic is
+backend-agnostic (``ops``) so the multi-process protocol is also exercised by
+world-size-2 gloo tests on CPU with the oracle standing in for the kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+from . import _lib
+from ._lib import MP_DTYPE_BF16, MP_LAYER_EXPERTS_ONLY, MP_LAYER_ROUTER_ONLY, check
+from .layer import MoeLayer, _ptr, _stream_handle
+
+
+def _dist():
+    import torch.distributed as dist
+    return dist
+
+
+class CudaEpOps:
+    """The data-path steps on the GPU, through the C-ABI."""
+
+    def __init__(self, E, S, d, ff, rank, world, dtype="bf16", k_max=16, max_tokens=4096, device=0):
+        import torch
+        self.torch = torch
+        self.rank, self.world, self.d, self.k_max = rank, world, d, k_max
+        self.epr = E // world
+        self.router = MoeLayer(E, S, d, ff, dtype=dtype, k_max=k_max, max_tokens=max_tokens, device=device,
+                               flags=MP_LAYER_ROUTER_ONLY)
+        self.local = MoeLayer(self.epr, S, d, ff, dtype=dtype, weights="softmax_renorm", k_max=k_max,
+                              max_tokens=max_tokens * world, device=device, flags=MP_LAYER_EXPERTS_ONLY)
+        self.dtype = self.router.torch_dtype
+        h = C.c_void_p()
+        check(_lib.load().mp_ep_create(world, rank, self.epr, S, d, k_max, max_tokens,
+                                       1 if self.dtype == torch.bfloat16 else 0, device, C.byref(h)))
+        self.ep = h
+
+    def route(self, x, k, k_per_token):
+        return self.router.route(x, k=k, k_per_token=k_per_token)
+
+    def plan(self, sel):
+        counts = (C.c_uint32 * self.world)()
+        check(_lib.load().mp_ep_plan(self.ep, _ptr(sel), sel.shape[0], counts, _stream_handle(None)))
+        return [int(c) for c in counts]
+
+    def pack(self, x, sel, w, n_send):
+        torch = self.torch
+        send_x = torch.empty((n_send, self.d), dtype=self.dtype, device=x.device)
+        send_sel = torch.empty((n_send, self.k_max), dtype=torch.int32, device=x.device)
+        send_w = torch.empty((n_send, self.k_max), dtype=torch.float32, device=x.device)
+        check(_lib.load().mp_ep_pack(self.ep, _ptr(x), _ptr(sel), _ptr(w), x.shape[0], _ptr(send_x), _ptr(send_sel),
+                                     _ptr(send_w), _stream_handle(None)))
+        return send_x, send_sel, send_w
+
+    def experts(self, recv_x, recv_sel, recv_w):
+        if recv_x.shape[0] == 0:
+            return recv_x.new_empty((0, self.d))
+        return self.local.forward_selected(recv_x, recv_sel, recv_w)
+
+    def combine(self, back, T):
+        y = back.new_empty((T, self.d))
+        check(_lib.load().mp_ep_combine(self.ep, _ptr(back), T, _ptr(y), _stream_handle(None)))
+        return y
+
+    # weights: experts are addressed by their GLOBAL id; non-owned ones are skipped
+    def owns(self, e):
+        return e // self.epr == self.rank
+
+    def load_expert(self, e, wg, wu, wd):
+        if self.owns(e):
+            self.local.load_expert(e - self.rank * self.epr, wg, wu, wd)
+
+    def set_partition(self, e, assignment):
+        if self.owns(e):
+            self.local.set_partition(e - self.rank * self.epr, assignment)
+
+    def set_router(self, w_r):
+        self.router.set_router(w_r)
+
+    def close(self):
+        if getattr(self, "ep", None):
+            _lib.load().mp_ep_destroy(self.ep)
+            self.ep = None
+        self.router.close()
+        self.local.close()
+
+
+class ExpertParallelLayer:
+    """A MoE-Prism layer sharded expert-parallel over the process group."""
+
+    def __init__(self, ops, group=None):
+        self.ops = ops
+        self.group = group
+
+    def _a2a(self, out, inp, out_splits, in_splits):
+        dist = _dist()
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits,
+                                   group=self.group)
+        else:
+            out.copy_(inp)
+        return out
+
+    def exchange_counts(self, counts, device):
+        import torch
+        dist = _dist()
+        send = torch.tensor(counts, dtype=torch.int64, device=device)
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            recv = torch.empty_like(send)
+            dist.all_to_all_single(recv, send, group=self.group)
+            return [int(v) for v in recv.tolist()]
+        return list(counts)
+
+    def forward(self, x, k: int = 0, k_per_token=None, return_routing: bool = False):
+        import torch
+        ops = self.ops
+        T = x.shape[0]
+        sel, w = ops.route(x, k, k_per_token)
+        counts = ops.plan(sel)
+        send_x, send_sel, send_w = ops.pack(x, sel, w, sum(counts))
+        recv_counts = self.exchange_counts(counts, x.device)
+        n_recv = sum(recv_counts)
+        recv_x = self._a2a(send_x.new_empty((n_recv, send_x.shape[1])), send_x, recv_counts, counts)
+        # selection + weights in one message: [rows x 2*k_max] int32 (weights bit-cast)
+        meta = torch.cat([send_sel, send_w.view(torch.int32)], dim=1).contiguous()
+        recv_meta = self._a2a(meta.new_empty((n_recv, meta.shape[1])), meta, recv_counts, counts)
+        kk = send_sel.shape[1]
+        recv_sel = recv_meta[:, :kk].contiguous()
+        recv_w = recv_meta[:, kk:].contiguous().view(torch.float32)
+        part = ops.experts(recv_x, recv_sel, recv_w)
+        back = self._a2a(part.new_empty((sum(counts), part.shape[1])), part.contiguous(), counts, recv_counts)
+        y = ops.combine(back, T)
+        if return_routing:
+            return y, sel, w, counts, recv_counts
+        return y

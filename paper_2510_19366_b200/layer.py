@@ -53,14 +53,14 @@ def _stream_handle(stream) -> Optional[int]:
 class MoeLayer:
     def __init__(self, n_experts: int, n_subexperts: int, d_model: int, d_ff: int, dtype: str = "bf16",
                  router: str = "linear", weights: str = "softmax_renorm", k_max: int = 16,
-                 max_tokens: int = 4096, device: int = 0):
+                 max_tokens: int = 4096, device: int = 0, flags: int = 0):
         self.lib = _lib.load()
         self.E, self.S, self.d, self.ff = n_experts, n_subexperts, d_model, d_ff
         self.G = n_experts * n_subexperts
         self.dtype_code = _DTYPES[dtype]
         self.k_max, self.max_tokens, self.device = k_max, max_tokens, device
         desc = LayerDesc(n_experts, n_subexperts, d_model, d_ff, self.dtype_code, _ROUTERS[router], _WEIGHTS[weights],
-                         k_max, max_tokens, device)
+                         k_max, max_tokens, device, flags)
         h = C.c_void_p()
         check(self.lib.mp_layer_create(C.byref(desc), C.byref(h)))
         self.h = h
