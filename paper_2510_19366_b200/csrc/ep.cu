@@ -38,6 +38,19 @@ __global__ void ep_dest_kernel(const uint32_t* __restrict__ sel, uint32_t T, uin
     for (; n < world; ++n) dest[(size_t)t * world + n] = kSelNone;
 }
 
+// slot_row[t][j] = position of (token t, its j-th destination rank) in the
+// rank-grouped send buffer = bucket base of (t's CTA block, rank) + local rank
+__global__ void ep_slot_kernel(const uint32_t* __restrict__ dest, const uint32_t* __restrict__ lrank,
+                               const uint32_t* __restrict__ block_base, uint32_t T, uint32_t world,
+                               uint32_t* __restrict__ slot_row) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= T * world) return;
+    const uint32_t t = q / world;
+    const uint32_t r = dest[q];
+    slot_row[q] = r == kSelNone ? kSelNone
+                                : block_base[(size_t)(t / kRouteTokensPerBlock) * world + r] + lrank[q];
+}
+
 template <typename Tx>
 __global__ void __launch_bounds__(256) ep_pack_kernel(const Tx* __restrict__ x, const uint32_t* __restrict__ sel,
                                                       const float* __restrict__ w, uint32_t T, uint32_t d,
@@ -211,6 +224,7 @@ MP_API mp_status mp_ep_plan(mp_ep_t E, const uint32_t* sel, uint32_t T, uint32_t
         mp::launch_ep_dest(sel, T, E->k_max, E->epr * E->S, E->world, E->dest, s);
         mp::launch_bucket_local(E->dest, T, E->world, E->world, E->ws, s);
         mp::launch_bucket_scan(T, E->world, E->ws, s);
+        mp::launch_ep_slot(E->dest, E->ws.lrank, E->ws.block_base, T, E->world, E->ws.slot_row, s);
         ep_ck(cudaGetLastError(), "ep plan");
         std::vector<uint32_t> off(E->world + 1);
         ep_ck(cudaMemcpyAsync(off.data(), E->ws.offsets, (E->world + 1) * 4, cudaMemcpyDeviceToHost, s), "counts");
@@ -245,6 +259,10 @@ namespace mp {
 void launch_ep_dest(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32_t per_rank, uint32_t world, uint32_t* dest,
                     cudaStream_t s) {
     ep_dest_kernel<<<(T + 255) / 256, 256, 0, s>>>(sel, T, k_max, per_rank, world, dest);
+}
+void launch_ep_slot(const uint32_t* dest, const uint32_t* lrank, const uint32_t* block_base, uint32_t T, uint32_t world,
+                    uint32_t* slot_row, cudaStream_t s) {
+    ep_slot_kernel<<<(T * world + 255) / 256, 256, 0, s>>>(dest, lrank, block_base, T, world, slot_row);
 }
 void launch_ep_pack(int dtype, const void* x, const uint32_t* sel, const float* w, uint32_t T, uint32_t d,
                     uint32_t k_max, uint32_t per_rank, uint32_t world, const uint32_t* dest, const uint32_t* slot_row,
