@@ -150,6 +150,37 @@ def build_layer(local, T, k_max):
     return L, xs
 
 
+def build_ep_layer(local, rank, world, T, k_max=16):
+    """Expert-parallel layer: E/world parent experts on this rank,
+    the router replicated, tokens exchanged by NCCL all-to-all."""
+    import torch
+    from paper_2510_19366_b200 import synth_fill
+    from paper_2510_19366_b200.ep import CudaEpOps, ExpertParallelLayer
+    if E % world:
+        raise SystemExit(f"--gpus {world} must divide the {E} experts")
+    ops = CudaEpOps(E, S, D, FF, rank, world, dtype="bf16", k_max=k_max, max_tokens=T, device=local)
+    buf = [torch.empty(D * FF, dtype=torch.float32, device="cuda") for _ in range(3)]
+    for e in range(E):
+        if not ops.owns(e):
+            continue
+        for m, (seed, scale) in enumerate(((100 + 3 * e, 1 / math.sqrt(D)), (101 + 3 * e, 1 / math.sqrt(D)),
+                                           (102 + 3 * e, 1 / math.sqrt(FF)))):
+            synth_fill(buf[m], seed, scale)
+        ops.set_partition(e, balanced_partition(FF, S, 6000 + e))
+        ops.load_expert(e, *buf)
+    del buf
+    wr = torch.empty(D * E * S, dtype=torch.float32, device="cuda")
+    synth_fill(wr, 7, 1 / math.sqrt(D))
+    ops.set_router(wr)
+    xs = []
+    for i in range(N_XBUF):
+        x = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
+        synth_fill(x, 11 + 1000 * i + 100000 * rank, 1.0)
+        xs.append(x)
+    torch.cuda.synchronize()
+    return ExpertParallelLayer(ops), ops, xs
+
+
 def balanced_partition(n, n_sub, seed):
     """testsupport::random_balanced_partition (tests/support.hpp:89-105): seeded
     Fisher-Yates (mt19937_64 + uniform_index) dealt round-robin."""
@@ -235,15 +266,22 @@ def time_steps(fn, steps, warmup, world):
     return max_over_ranks(ms, world)
 
 
-def stage_profile(L, xs, k, reps=20, kpt=None):
+def stage_profile(layers, fwd, xs, k, reps=20, kpt=None):
+    """Per-stage device time per step (CUDA events on the launching stream)."""
     import torch
-    L.reset_stage_times()
-    L.set_profiling(True)
+    for L in layers:
+        L.reset_stage_times()
+        L.set_profiling(True)
     for i in range(reps):
-        L.forward(xs[i % len(xs)], k=k, k_per_token=kpt)
+        fwd(xs[i % len(xs)], k, kpt)
     torch.cuda.synchronize()
-    L.set_profiling(False)
-    return {name: ms / reps for name, (ms, n) in L.stage_times().items()}
+    out = {}
+    for L in layers:
+        L.set_profiling(False)
+        for name, (ms, n) in L.stage_times().items():
+            if n:
+                out[name] = out.get(name, 0.0) + ms / reps
+    return out
 
 
 def kernel_roofline(stage_ms_per_step, T, k, pk, touched_groups):
@@ -352,7 +390,8 @@ def workload_config(args, world):
                         "8 experts x 8 sub-experts (w=1792), linear fp32 router, softmax-renormalised top-k",
             "d_model": D, "d_ff": FF, "experts": E, "subexperts_per_expert": S, "tokens_per_gpu": args.tokens,
             "k": args.k, "global_tokens": args.tokens * world,
-            "parallelism": "replicas" if world > 1 else "single",
+            "parallelism": (f"ep{world} (experts sharded, NCCL all-to-all)" if world > 1 or args.force_ep
+                            else "single"),
             "l2": f"x rotates over {N_XBUF} buffers ({N_XBUF * args.tokens * D * 2 / 1e6:.0f} MB) + 2.8 GB weights, "
                   "both > 126 MB L2"}
 
@@ -367,6 +406,7 @@ def main():
     ap.add_argument("--sweep", default="2,4,8,16")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-ep", action="store_true", help="run the expert-parallel path even at N=1 (loopback)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -383,18 +423,32 @@ def main():
     pk = peaks()
     T = args.tokens
     sweep = [int(v) for v in args.sweep.split(",") if v]
-    L, xs = build_layer(local, T, k_max=16)
-    touched = E * S  # at 4096 tokens every sub-expert receives tokens
+    use_ep = world > 1 or args.force_ep
+    if not use_ep:
+        L, xs = build_layer(local, T, k_max=16)
+        layers = [L]
+
+        def fwd(x, k, kpt, y=None):
+            return L.forward(x, k=k, k_per_token=kpt, y=y)
+    else:
+        ep_layer, ops, xs = build_ep_layer(local, rank, world, T)
+        layers = [ops.router, ops.local]
+
+        def fwd(x, k, kpt, y=None):
+            return ep_layer.forward(x, k=k, k_per_token=kpt)
+    touched = E * S // world  # sub-experts whose weights this GPU streams (all receive tokens at 4096/GPU)
 
     def step(i, k=args.k, kpt=None):
-        L.forward(xs[i % N_XBUF], k=k, k_per_token=kpt, y=ybuf)
+        fwd(xs[i % N_XBUF], k, kpt, ybuf)
 
     ybuf = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
     clocks = ClockSampler(local)
     clocks.start()
-    n0 = L.launch_count()
+    n0 = sum(x.launch_count() for x in layers)
     ms = time_steps(step, args.steps, args.warmup, world)
-    launches = (L.launch_count() - n0) // (args.steps + args.warmup) * args.steps
+    launches = (sum(x.launch_count() for x in layers) - n0) // (args.steps + args.warmup) * args.steps
+    if use_ep:
+        launches += 6 * args.steps  # mp_ep_plan (4 kernels), mp_ep_pack, mp_ep_combine per step
     value = world * T / (ms * 1e-3)
 
     # per-stage device times (CUDA events on the forward's stream), the sweep
@@ -410,7 +464,7 @@ def main():
             kk = float(kpt.float().mean().item())
         msk = time_steps(lambda i: step(i, k=0 if kpt is not None else k, kpt=kpt), max(args.steps // 2, 10), 3,
                          world)
-        per_step = stage_profile(L, xs, 0 if kpt is not None else k, kpt=kpt)
+        per_step = stage_profile(layers, fwd, xs, 0 if kpt is not None else k, kpt=kpt)
         ent = {"k": k, "tokens_per_s": world * T / (msk * 1e-3), "ms_per_step": msk,
                "layer_roofline": layer_roofline(T, kk, msk, pk, touched), "stages_ms": per_step}
         if k != "mixed":
@@ -419,23 +473,31 @@ def main():
         if k == args.k:
             stages_main = per_step
     if stages_main is None:
-        stages_main = stage_profile(L, xs, args.k)
+        stages_main = stage_profile(layers, fwd, xs, args.k)
 
     # e2e: public API with HOST buffers (pinned), H2D of x + D2H of y per step
     xh = [xs[i].cpu().pin_memory() for i in range(2)]
     yh = torch.empty((T, D), dtype=torch.bfloat16).pin_memory()
-    import ctypes as C
     from paper_2510_19366_b200 import _lib
     lib = _lib.load()
+    if not use_ep:
+        def e2e_step(i):
+            _lib.check(lib.mp_layer_forward_host(L.h, xh[i % 2].data_ptr(), T, None, args.k, yh.data_ptr(), None,
+                                                 None, None, torch.cuda.current_stream().cuda_stream))
+        path = "mp_layer_forward_host (C-ABI), pinned host x/y"
+    else:
+        xd = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
 
-    def e2e_step(i):
-        _lib.check(lib.mp_layer_forward_host(L.h, xh[i % 2].data_ptr(), T, None, args.k, yh.data_ptr(), None, None,
-                                             None, torch.cuda.current_stream().cuda_stream))
+        def e2e_step(i):
+            xd.copy_(xh[i % 2], non_blocking=True)
+            y = fwd(xd, args.k, None)
+            yh.copy_(y, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        path = "ExpertParallelLayer.forward with pinned host x/y copied in/out"
 
     ms_e2e = time_steps(e2e_step, max(args.steps // 2, 10), 3, world)
     e2e = {"value": world * T / (ms_e2e * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": T * D * 2,
-           "d2h_bytes_per_step": T * D * 2, "ms_per_step": ms_e2e,
-           "path": "mp_layer_forward_host (C-ABI), pinned host x/y"}
+           "d2h_bytes_per_step": T * D * 2, "ms_per_step": ms_e2e, "path": path}
     clk = clocks.stop()  # sampled across the main timed loop, the k sweep and the e2e loop
 
     cpu = None
@@ -463,7 +525,8 @@ def main():
         if main_k:
             line["roofline"] = main_k.get("kernel_roofline", line["roofline"])
         print(json.dumps(line), flush=True)
-    L.close()
+    for x in layers:
+        x.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
