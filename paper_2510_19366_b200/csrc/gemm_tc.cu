@@ -22,6 +22,7 @@
 // columns (tmem_full / tmem_empty) so the epilogue of tile i overlaps the
 // MMAs of tile i+1.
 #include <cstdio>
+#include <cstdlib>
 
 #include "mp_common.cuh"
 #include "mp_kernels.h"
@@ -38,6 +39,7 @@ constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr uint32_t B_BYTES = BN * BK * 2;
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t kThreads = 192;
+constexpr uint32_t kGatherThreads = 128;  // GATHER: 4 extra warps stream the A rows by cp.async
 constexpr uint32_t kTmemCols = 512;
 constexpr size_t kSmemBytes = 1024 + STAGES * STAGE_BYTES + 256;
 
@@ -45,7 +47,10 @@ struct TcParams {
     uint32_t G, K, N_group, n_valid, ld_out, NT;
     const uint32_t* offsets;
     const uint32_t* mprefix;
-    const uint32_t* perm;  // GATHER: token id of every permuted row
+    const uint32_t* perm;        // GATHER: token id of every permuted row
+    const __nv_bfloat16* gx;     // GATHER: the token matrix x [T][gd]
+    uint32_t gd;                 // GATHER: row length of x (elements, multiple of 8)
+    uint32_t nstages;
     __nv_bfloat16* out;
 };
 
@@ -67,7 +72,7 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
 }
 
 template <bool SWIGLU, bool GATHER>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], GATHER ? 1 + kGatherThreads : 1);
             mbar_init(&empty[s], 1);
         }
         for (uint32_t a = 0; a < 2; ++a) {
@@ -100,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmB);
     }
     if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
-    for (uint32_t q = threadIdx.x; q <= p.G; q += kThreads) {
+    for (uint32_t q = threadIdx.x; q <= p.G; q += blockDim.x) {
         s_prefix[q] = p.mprefix[q];
         s_off[q] = p.offsets[q];
     }
@@ -110,33 +115,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t total = s_prefix[p.G] * p.NT;
     const uint32_t nkb = p.K / BK;
+    const uint32_t NS = p.nstages;  // ring depth in use (<= STAGES; MOEPRISM_TC_STAGES, diagnostics)
 
     if (warp == 0) {
         if constexpr (GATHER) {
-            // A rows gathered straight from the token matrix x by TMA gather4:
-            // lane q streams rows 4q..4q+3 of the tile (token ids from the
-            // bucket permutation), lane 0 arms the barrier and loads B.
-            uint32_t it = 0;
-            for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-                uint32_t g, m, n;
-                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const uint32_t arow = s_off[g] + m * BM;
-                const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN);
-                int32_t tok[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const uint32_t r = arow + lane * 4 + j;
-                    tok[j] = r < s_off[p.G] ? static_cast<int32_t>(p.perm[r]) : 0;  // pad rows: any valid token
-                }
-                for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
-                    mbar_wait(&empty[s], ph ^ 1u);
-                    if (lane == 0) {
-                        mbar_expect_tx(&full[s], STAGE_BYTES);
+            // B tiles only (TMA); the A rows are streamed by the gather warps
+            if (lane == 0) {
+                uint32_t it = 0;
+                for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+                    uint32_t g, m, n;
+                    map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+                    const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN);
+                    for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
+                        const uint32_t s = it % NS, ph = (it / NS) & 1u;
+                        mbar_wait(&empty[s], ph ^ 1u);
+                        mbar_expect_tx(&full[s], B_BYTES);
                         tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow);
                     }
-                    __syncwarp();
-                    tma_gather4(sA + s * A_BYTES + lane * 512, &tmA, &full[s], static_cast<int32_t>(kb * BK), tok);
                 }
             }
         } else if (lane == 0) {
@@ -147,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM);
                 const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN);
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+                    const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
                     mbar_expect_tx(&full[s], STAGE_BYTES);
                     tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], static_cast<int32_t>(kb * BK), arow);
@@ -165,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+                    const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + s * A_BYTES);
@@ -180,6 +175,45 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         __syncwarp();
+    } else if (GATHER && warp >= kThreads / 32) {
+        // A-row gather: thread r owns row r of every tile; each k-block it
+        // copies the row's 128 bytes as 8 x 16-byte cp.async into the 128B-
+        // swizzled slot (chunk c of row r lands at chunk c ^ (r & 7), the
+        // layout a SW128 TMA tile load produces), zero-filling rows outside
+        // the group.  Completion: wait for the group issued STAGES-1 k-blocks
+        // ago, fence the generic->async proxy, arrive on that stage's full
+        // barrier (count 1 + 128).
+        const uint32_t LAG = NS - 1;
+        const uint32_t r = threadIdx.x - kThreads;
+        const uint32_t sw = (r & 7u) << 4;
+        uint32_t it = 0;
+        for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+            uint32_t g, m, n;
+            map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+            const uint32_t row_local = m * BM + r;
+            const bool valid = row_local < s_off[g + 1] - s_off[g];
+            const __nv_bfloat16* src = p.gx + (valid ? static_cast<size_t>(p.perm[s_off[g] + row_local]) * p.gd : 0);
+            for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
+                const uint32_t s = it % NS, ph = (it / NS) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                const uint32_t dst = smem_u32(sA + s * A_BYTES + r * 128);
+#pragma unroll
+                for (uint32_t c = 0; c < 8; ++c) {
+                    const uint32_t col = kb * BK + c * 8;
+                    const uint32_t bytes = (valid && col < p.gd) ? 16u : 0u;
+                    cp_async_16(dst + ((c << 4) ^ sw), src + (bytes ? col : 0), bytes);
+                }
+                cp_async_commit();
+                if (it >= LAG) {
+                    cp_async_wait<STAGES - 1>();  // groups <= it - LAG complete (gather requires NS == STAGES)
+                    fence_proxy_async_smem();
+                    mbar_arrive(&full[(it - LAG) % NS]);
+                }
+            }
+        }
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        for (uint32_t j = it > LAG ? it - LAG : 0; j < it; ++j) mbar_arrive(&full[j % NS]);
     } else {
         const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
         uint32_t tc = 0;
@@ -280,7 +314,7 @@ bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t
 
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                    const uint32_t* gather_perm) {
+                    const uint32_t* gather_perm, const void* gather_x, uint32_t gather_d) {
     TcParams p;
     p.G = sh.G;
     p.K = sh.K;
@@ -291,6 +325,14 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.offsets = offsets;
     p.mprefix = mprefix;
     p.perm = gather_perm;
+    p.gx = static_cast<const __nv_bfloat16*>(gather_x);
+    p.gd = gather_d;
+    static const uint32_t ns_env = [] {
+        const char* e = std::getenv("MOEPRISM_TC_STAGES");
+        const int v = e ? std::atoi(e) : (int)STAGES;
+        return (uint32_t)(v >= 2 && v <= (int)STAGES ? v : STAGES);
+    }();
+    p.nstages = ns_env;
     p.out = static_cast<__nv_bfloat16*>(out);
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
@@ -303,7 +345,7 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
         attr_set = true;
     }
     if (swiglu && gather_perm)
-        gemm_tc_kernel<true, true><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+        gemm_tc_kernel<true, true><<<grid, kThreads + kGatherThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
     else if (swiglu)
         gemm_tc_kernel<true, false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
     else

@@ -100,7 +100,7 @@ struct mp_layer_s {
     size_t esz = 4;
     int num_sms = 0;
     bool use_tc = false;
-    bool gather_ok = true;
+    bool gather_ok = false;
     bool has_experts = true, has_router = true;  // MP_LAYER_* role flags  // gemm1 gathers A rows by TMA (MOEPRISM_GATHER=0 disables, diagnostics)
 
     std::vector<std::vector<uint32_t>> assignment;
@@ -303,13 +303,8 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
                  cudaStream_t s, StageTimer& tm, bool check_finite = false) {
     // bf16 tensor-core path: gemm1 gathers its A rows straight from x (TMA
     // gather4), so dispatch only writes the permutation tables
-    // -- only when gemm1 has at most 2 N tiles: gather4 moves 512 B per TMA op and
-    // the A tile is re-gathered for every N tile (measured 2.3x slower than
-    // dispatch + tile loads at the Mixtral shape, 14 N tiles)
-    const bool gather = L->use_tc && L->gather_ok && L->w_pad <= 256 && (L->d % 8) == 0 &&
-                        (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-    CUtensorMap tmX;
-    if (gather && !mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 1, 64)) fail(MP_ERR_CUDA, "x gather tensor map");
+    // (cp.async warps inside gemm1; rows are 16-byte aligned when d % 8 == 0)
+    const bool gather = L->use_tc && L->gather_ok && (L->d % 8) == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
     tm.begin(1);
     mp::launch_bucket_local(sel, T, L->k_max, L->G, L->ws, s);
     mp::launch_bucket_scan(T, L->G, L->ws, s);
@@ -324,8 +319,8 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
     if (L->use_tc)
-        mp::launch_gemm_tc(true, gather ? &tmX : &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc,
-                           L->num_sms, s, gather ? L->ws.perm_tok : nullptr);
+        mp::launch_gemm_tc(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s,
+                           gather ? L->ws.perm_tok : nullptr, x, L->d);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
@@ -461,7 +456,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             if (const char* env = std::getenv("MOEPRISM_BF16_GEMM"))
                 if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
             if (const char* env = std::getenv("MOEPRISM_GATHER"))
-                if (std::string(env) == "0") L->gather_ok = false;
+                L->gather_ok = std::string(env) == "1";
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
             L->d_pad = round_up(L->d, 64);

@@ -94,6 +94,18 @@ MP_DEV void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t 
         "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(smem_u32(bar))
         : "memory");
 }
+// 16-byte cp.async (L2 only), zero-filling dst beyond src_bytes (0 or 16)
+MP_DEV void cp_async_16(uint32_t dst_smem, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes) : "memory");
+}
+MP_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+MP_DEV void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// make generic-proxy smem writes (st.shared / cp.async) visible to the async
+// proxy (tcgen05.mma operand reads, TMA)
+MP_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 MP_DEV void tma_load_2d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1,
                              uint64_t policy) {
     asm volatile(
