@@ -100,8 +100,12 @@ struct mp_layer_s {
     size_t esz = 4;
     int num_sms = 0;
     bool use_tc = false;
+    // gemm1 gathering its A rows from x inside the GEMM (cp.async warps) instead of
+    // dispatch materialising x_perm: correct, but 2.6x slower at the Mixtral
+    // shape (each A tile is re-gathered for every N tile at L2 latency), so off
+    // unless MOEPRISM_GATHER=1 (experiments)
     bool gather_ok = false;
-    bool has_experts = true, has_router = true;  // MP_LAYER_* role flags  // gemm1 gathers A rows by TMA (MOEPRISM_GATHER=0 disables, diagnostics)
+    bool has_experts = true, has_router = true;  // MP_LAYER_* role flags
 
     std::vector<std::vector<uint32_t>> assignment;
     std::vector<uint8_t> has_part, packed;
