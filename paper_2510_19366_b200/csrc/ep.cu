@@ -138,7 +138,7 @@ template <class F>
 int ep_guarded(F&& f);
 void ep_free(mp_ep_s* E) {
     void* ptrs[] = {E->dest, E->ws.lrank, E->ws.block_counts, E->ws.block_base, E->ws.offsets, E->ws.mprefix_tc,
-                    E->ws.mprefix_simt, E->ws.perm_tok, E->ws.perm_w, E->ws.slot_row, E->ws.err};
+                    E->ws.mprefix_simt, E->ws.mprefix_tc2, E->ws.perm_tok, E->ws.perm_w, E->ws.slot_row, E->ws.err};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete E;
@@ -188,6 +188,7 @@ MP_API mp_status mp_ep_create(uint32_t world, uint32_t rank, uint32_t epr, uint3
             E->ws.offsets = ep_alloc<uint32_t>(world + 1);
             E->ws.mprefix_tc = ep_alloc<uint32_t>(world + 1);
             E->ws.mprefix_simt = ep_alloc<uint32_t>(world + 1);
+            E->ws.mprefix_tc2 = ep_alloc<uint32_t>(world + 1);
             E->ws.perm_tok = ep_alloc<uint32_t>(tw);
             E->ws.perm_w = ep_alloc<float>(tw);
             E->ws.slot_row = ep_alloc<uint32_t>(tw);

@@ -51,6 +51,9 @@ struct TcParams {
     const __nv_bfloat16* gx;     // GATHER: the token matrix x [T][gd]
     uint32_t gd;                 // GATHER: row length of x (elements, multiple of 8)
     uint32_t nstages;
+    uint32_t prefetch;  // L2 prefetch distance in k-blocks (0 = off)
+    uint64_t* trace;    // [grid][4] MMA-issuer timing (diagnostics) or null
+    uint32_t hints;     // L2 cache-policy hints on the TMA loads
     __nv_bfloat16* out;
 };
 
@@ -135,6 +138,33 @@ __global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
                 }
             }
         } else if (lane == 0) {
+            // L2 prefetch cursor PF k-blocks ahead of the loads (it walks into the
+            // next tile): the first CTA to touch a weight tile otherwise waits
+            // the full HBM latency with only ~3 slots of smem lookahead.
+            const uint32_t PF = p.prefetch;
+            uint32_t pf_tile = blockIdx.x, pf_kb = 0;
+            int32_t pf_arow = 0, pf_brow = 0;
+            auto pf_coords = [&]() {
+                uint32_t g, m, n;
+                map_tile(pf_tile, s_prefix, p.G, p.NT, g, m, n);
+                pf_arow = static_cast<int32_t>(s_off[g] + m * BM);
+                pf_brow = static_cast<int32_t>(g * p.N_group + n * BN);
+            };
+            auto pf_issue_advance = [&]() {
+                if (pf_tile >= total) return;
+                tma_prefetch_l2_2d(&tmA, static_cast<int32_t>(pf_kb * BK), pf_arow);
+                tma_prefetch_l2_2d(&tmB, static_cast<int32_t>(pf_kb * BK), pf_brow);
+                if (++pf_kb == nkb) {
+                    pf_kb = 0;
+                    pf_tile += gridDim.x;
+                    if (pf_tile < total) pf_coords();
+                }
+            };
+            if (PF && pf_tile < total) {
+                pf_coords();
+                for (uint32_t q = 0; q < PF; ++q) pf_issue_advance();
+            }
+            const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
             uint32_t it = 0;
             for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
                 uint32_t g, m, n;
@@ -145,8 +175,16 @@ __global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
                     mbar_expect_tx(&full[s], STAGE_BYTES);
-                    tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], static_cast<int32_t>(kb * BK), arow);
-                    tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow);
+                    if (p.hints) {
+                        // A tiles are re-read by every N tile of the group: keep;
+                        // a weight tile is read by the group's few M tiles at once
+                        tma_load_2d_hint(sA + s * A_BYTES, &tmA, &full[s], static_cast<int32_t>(kb * BK), arow, pol_a);
+                        tma_load_2d_hint(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow, pol_b);
+                    } else {
+                        tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], static_cast<int32_t>(kb * BK), arow);
+                        tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow);
+                    }
+                    if (PF) pf_issue_advance();
                 }
             }
         }
@@ -154,14 +192,22 @@ __global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
             uint32_t it = 0, tc = 0;
+            // optional timing trace (MOEPRISM_TC_TRACE): cycles the MMA issuer
+            // waits for accumulators (epilogue) and for smem stages (loads)
+            const uint64_t t_start = p.trace ? clock64() : 0;
+            uint64_t w_acc = 0, w_full = 0;
             for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
                 const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+                uint64_t t0 = p.trace ? clock64() : 0;
                 mbar_wait(&tempty[acc], aph ^ 1u);
+                if (p.trace) w_acc += clock64() - t0;
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
+                    t0 = p.trace ? clock64() : 0;
                     mbar_wait(&full[s], ph);
+                    if (p.trace) w_full += clock64() - t0;
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + s * A_BYTES);
                     const uint32_t b0 = smem_u32(sB + s * B_BYTES);
@@ -172,6 +218,13 @@ __global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[acc]);
+            }
+            if (p.trace) {
+                uint64_t* tr = p.trace + blockIdx.x * 4;
+                tr[0] = clock64() - t_start;
+                tr[1] = w_acc;
+                tr[2] = w_full;
+                tr[3] = tc;
             }
         }
         __syncwarp();
@@ -312,6 +365,21 @@ bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// MOEPRISM_TC_TRACE=1: per-CTA MMA-issuer timing of the last gemm1 / gemm2
+// launch, readable with mp_debug_gemm_trace (diagnostics only).
+static uint64_t* g_trace[2] = {nullptr, nullptr};
+uint64_t* gemm_trace_buffer(bool swiglu) {
+    static const bool on = [] {
+        const char* e = std::getenv("MOEPRISM_TC_TRACE");
+        return e && e[0] == '1';
+    }();
+    if (!on) return nullptr;
+    uint64_t*& b = g_trace[swiglu ? 0 : 1];
+    if (!b) cudaMalloc(&b, 1024 * 4 * sizeof(uint64_t));
+    return b;
+}
+uint64_t* gemm_trace_ptr(int which) { return g_trace[which & 1]; }
+
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                     const uint32_t* gather_perm, const void* gather_x, uint32_t gather_d) {
@@ -333,6 +401,17 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
         return (uint32_t)(v >= 2 && v <= (int)STAGES ? v : STAGES);
     }();
     p.nstages = ns_env;
+    static const uint32_t pf_env = [] {
+        const char* e = std::getenv("MOEPRISM_TC_PREFETCH");
+        return (uint32_t)(e ? std::atoi(e) : 0);  // measured: prefetching slows the loads (tests/probes/pf_sweep.sh)
+    }();
+    p.prefetch = pf_env;
+    p.trace = gemm_trace_buffer(swiglu);
+    static const uint32_t hint_env = [] {
+        const char* e = std::getenv("MOEPRISM_TC_HINTS");
+        return (uint32_t)(e ? std::atoi(e) : 0);
+    }();
+    p.hints = hint_env;
     p.out = static_cast<__nv_bfloat16*>(out);
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;

@@ -105,6 +105,7 @@ struct mp_layer_s {
     // shape (each A tile is re-gathered for every N tile at L2 latency), so off
     // unless MOEPRISM_GATHER=1 (experiments)
     bool gather_ok = false;
+    bool tile256 = false;  // gemm_tc2 (256-row tiles) instead of gemm_tc; MOEPRISM_TC_TILE=256|128
     bool has_experts = true, has_router = true;  // MP_LAYER_* role flags
 
     std::vector<std::vector<uint32_t>> assignment;
@@ -165,7 +166,7 @@ void free_layer(mp_layer_s* L) {
         if (p) cudaFree(p);
     void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_flagged, L->d_nmap, L->sel,
                     L->wsel, L->kpt_dev, L->ws.lrank, L->ws.block_counts, L->ws.block_base, L->ws.offsets,
-                    L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
+                    L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.mprefix_tc2, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
                     L->x_perm, L->h, L->o, L->x_stage, L->y_stage};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -322,7 +323,9 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::GemmShape g1{L->G, L->d_pad, 2 * L->w_pad, T * L->k_max, L->w_pad, 2 * L->w_pad};
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
-    if (L->use_tc)
+    if (L->use_tc && L->tile256 && !gather)
+        mp::launch_gemm_tc2(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s);
+    else if (L->use_tc)
         mp::launch_gemm_tc(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s,
                            gather ? L->ws.perm_tok : nullptr, x, L->d);
     else
@@ -330,7 +333,9 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     ck_launch("gemm1");
     tm.end(3, 1);
     tm.begin(4);
-    if (L->use_tc)
+    if (L->use_tc && L->tile256)
+        mp::launch_gemm_tc2(false, &L->tm_h, &L->tm_w2, L->o, g2, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s);
+    else if (L->use_tc)
         mp::launch_gemm_tc(false, &L->tm_h, &L->tm_w2, L->o, g2, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
     else
         mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
@@ -461,6 +466,8 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
             if (const char* env = std::getenv("MOEPRISM_GATHER"))
                 L->gather_ok = std::string(env) == "1";
+            if (const char* env = std::getenv("MOEPRISM_TC_TILE"))
+                L->tile256 = std::string(env) == "256";
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
             L->d_pad = round_up(L->d, 64);
@@ -519,6 +526,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 L->ws.offsets = dalloc<uint32_t>(L->G + 1, "offsets");
                 L->ws.mprefix_tc = dalloc<uint32_t>(L->G + 1, "mprefix");
                 L->ws.mprefix_simt = dalloc<uint32_t>(L->G + 1, "mprefix");
+                L->ws.mprefix_tc2 = dalloc<uint32_t>(L->G + 1, "mprefix");
                 L->ws.perm_tok = dalloc<uint32_t>(L->rows_cap, "perm");
                 L->ws.perm_w = dalloc<float>(L->rows_cap, "perm w");
                 L->ws.slot_row = dalloc<uint32_t>(tk, "slot row");
@@ -970,3 +978,14 @@ MP_API mp_status mp_layer_forward_selected_host(mp_layer_t L, const void* x, uin
 
 // error channel shared with the other C-ABI translation units (ep.cu)
 extern "C" void mp_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
+
+// debugging aid: MMA-issuer timing of the last gemm1 (which=0) / gemm2 (1)
+// launch when MOEPRISM_TC_TRACE=1: per CTA {total cycles, waiting for the
+// accumulator (epilogue), waiting for smem stages (loads), tiles}.
+MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) {
+    return guarded([&] {
+        uint64_t* p = mp::gemm_trace_ptr(which);
+        if (!p) fail(MP_ERR_VALIDATION, "trace off (MOEPRISM_TC_TRACE=1)");
+        ck(cudaMemcpy(out, p, (size_t)n_ctas * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost), "trace");
+    });
+}

@@ -94,6 +94,12 @@ MP_DEV void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t 
         "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(smem_u32(bar))
         : "memory");
 }
+// TMA bulk prefetch of one box into L2 (no smem, no barrier)
+MP_DEV void tma_prefetch_l2_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 // 16-byte cp.async (L2 only), zero-filling dst beyond src_bytes (0 or 16)
 MP_DEV void cp_async_16(uint32_t dst_smem, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes) : "memory");

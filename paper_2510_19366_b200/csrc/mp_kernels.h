@@ -21,6 +21,7 @@ struct BucketWs {
     uint32_t* offsets;       // [G+1]
     uint32_t* mprefix_tc;    // [G+1] prefix of ceil(count/128)
     uint32_t* mprefix_simt;  // [G+1] prefix of ceil(count/64)
+    uint32_t* mprefix_tc2;   // [G+1] prefix of ceil(count/256)
     uint32_t* perm_tok;      // [rows]
     float* perm_w;           // [rows]
     uint32_t* slot_row;      // [T][k_max]
@@ -98,6 +99,11 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                     const uint32_t* gather_perm = nullptr, const void* gather_x = nullptr, uint32_t gather_d = 0);
 size_t gemm_tc_smem_bytes();
+uint64_t* gemm_trace_buffer(bool swiglu);
+uint64_t* gemm_trace_ptr(int which);
+// 256-row tiles, two M=128 accumulators sharing B (gemm_tc2.cu)
+void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
+                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s);
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point.
 bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,

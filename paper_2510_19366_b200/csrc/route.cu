@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32
                                                            uint32_t* __restrict__ block_base,
                                                            uint32_t* __restrict__ offsets,
                                                            uint32_t* __restrict__ mprefix_tc,
-                                                           uint32_t* __restrict__ mprefix_simt) {
+                                                           uint32_t* __restrict__ mprefix_simt,
+                                                           uint32_t* __restrict__ mprefix_tc2) {
     // thread (g, q): bucket g, q-th contiguous range of CTA-blocks; consecutive
     // threads read consecutive buckets of one block row (coalesced)
     __shared__ uint32_t part[1024];
@@ -421,6 +422,10 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32
     const uint32_t spre = block_exclusive_scan_1024(ms, &tot, wsum);
     if (gi < G) mprefix_simt[gi] = spre;
     if (gi == 0) mprefix_simt[G] = tot;
+    const uint32_t m2 = gi < G ? (c + 255) / 256 : 0;
+    const uint32_t pre2 = block_exclusive_scan_1024(m2, &tot, wsum);
+    if (gi < G) mprefix_tc2[gi] = pre2;
+    if (gi == 0) mprefix_tc2[G] = tot;
     __syncthreads();
     if (gi < G) goff[gi] = off;
     __syncthreads();
@@ -650,7 +655,7 @@ void launch_bucket_local(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32
 
 void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s) {
     bucket_scan_kernel<<<1, 1024, 0, s>>>((T + TB - 1) / TB, G, ws.block_counts, ws.block_base, ws.offsets,
-                                          ws.mprefix_tc, ws.mprefix_simt);
+                                          ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2);
 }
 
 void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t d_pad, const uint32_t* sel,

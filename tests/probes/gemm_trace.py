@@ -1,0 +1,20 @@
+"""MMA-issuer timing breakdown of the tcgen05 grouped GEMMs (diagnostic).
+Run with MOEPRISM_TC_TRACE=1."""
+import ctypes as C, sys, numpy as np, torch
+sys.path.insert(0, '.')
+import bench
+from paper_2510_19366_b200 import _lib
+L, xs = bench.build_layer(0, 4096, 16)
+lib = _lib.load()
+lib.mp_debug_gemm_trace.argtypes = [C.c_int, C.c_void_p, C.c_uint32]
+for k in (2, 8, 16):
+    for i in range(3):
+        L.forward(xs[i], k=k)
+    torch.cuda.synchronize()
+    for which, name in ((0, 'gemm1'), (1, 'gemm2')):
+        tr = np.zeros((148, 4), np.uint64)
+        _lib.check(lib.mp_debug_gemm_trace(which, tr.ctypes.data, 148))
+        tot, wacc, wfull, tiles = (tr[:, i].astype(np.float64) for i in range(4))
+        print(f"k={k} {name}: cycles max {tot.max():.0f} mean {tot.mean():.0f} | wait accumulator {100*wacc.sum()/tot.sum():.1f}% "
+              f"| wait smem stage {100*wfull.sum()/tot.sum():.1f}% | tiles/CTA {tiles.min():.0f}-{tiles.max():.0f} "
+              f"| CTA imbalance {(tot.max()-tot.mean())/tot.max()*100:.1f}%")
