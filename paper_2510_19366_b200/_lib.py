@@ -7,9 +7,12 @@ library is missing, ``load()`` raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libmoeprism_b200.so"
+if os.environ.get("MOEPRISM_LIB"):  # alternative in-tree build (kernel A/B experiments)
+    LIB_PATH = Path(os.environ["MOEPRISM_LIB"]).resolve()
 
 MP_OK, MP_ERR_VALIDATION, MP_ERR_IO, MP_ERR_CUDA = 0, 1, 2, 3
 MP_DTYPE_F32, MP_DTYPE_BF16 = 0, 1

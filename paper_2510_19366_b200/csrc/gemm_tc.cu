@@ -15,17 +15,28 @@
 // the tile is fetched from HBM once.  Rows of a partial M tile that belong to
 // the next group are computed and discarded (masked stores).
 //
-// Warp roles (192 threads): warp 0 = TMA producer (one elected lane),
-// warp 1 = TMEM allocator + MMA issuer (one lane), warps 2..5 = epilogue
-// (TMEM lane quarter = warp % 4).  Pipelines: 4-stage smem ring (full /
-// empty mbarriers, tcgen05.commit frees a stage), 2 TMEM accumulators of 256
-// columns (tmem_full / tmem_empty) so the epilogue of tile i overlaps the
-// MMAs of tile i+1.
+// Warp roles (192 threads): warp 0 = TMA producer (one lane), warp 1 = TMEM
+// allocator + MMA issuer (one lane), warps 2..5 = epilogue (TMEM lane quarter
+// = warp % 4).  Operand rings: A and B have SEPARATE smem rings (NA x 16 KB,
+// NB x 32 KB), each slot refilled the moment the MMAs reading it complete.
+// Measured with the MMA-issuer trace (MOEPRISM_TC_TRACE,
+// tests/probes/gemm_trace.py + ring_ab.sh): split 4+4 rings take 6% fewer
+// cycles than one 4 x 48 KB ring; 3+5, 4+3, 3+4 are 9-17% slower, 5+4 equal
+// -- both operands stream from HBM/L2 and need >= 4 k-blocks of lookahead.
+// 2 TMEM accumulators of 256 columns (tmem_full / tmem_empty) let the
+// epilogue of tile i overlap the MMAs of tile i+1.
 #include <cstdio>
 #include <cstdlib>
 
 #include "mp_common.cuh"
 #include "mp_kernels.h"
+
+#ifndef MP_TC_NA
+#define MP_TC_NA 4
+#endif
+#ifndef MP_TC_NB
+#define MP_TC_NB 4
+#endif
 
 namespace mp {
 
@@ -34,27 +45,19 @@ namespace {
 constexpr uint32_t BM = kTcBM;  // 128
 constexpr uint32_t BN = 256;
 constexpr uint32_t BK = 64;  // one 128-byte swizzle row of bf16
-constexpr uint32_t STAGES = 4;
+constexpr uint32_t NA = MP_TC_NA, NB = MP_TC_NB;
 constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr uint32_t B_BYTES = BN * BK * 2;
-constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t kThreads = 192;
-constexpr uint32_t kGatherThreads = 128;  // GATHER: 4 extra warps stream the A rows by cp.async
 constexpr uint32_t kTmemCols = 512;
-constexpr size_t kSmemBytes = 1024 + STAGES * STAGE_BYTES + 256;
+constexpr size_t kSmemBytes = 1024 + NA * A_BYTES + NB * B_BYTES + 256;
 
 struct TcParams {
     uint32_t G, K, N_group, n_valid, ld_out, NT;
     const uint32_t* offsets;
     const uint32_t* mprefix;
-    const uint32_t* perm;        // GATHER: token id of every permuted row
-    const __nv_bfloat16* gx;     // GATHER: the token matrix x [T][gd]
-    uint32_t gd;                 // GATHER: row length of x (elements, multiple of 8)
-    uint32_t nstages;
-    uint32_t prefetch;  // L2 prefetch distance in k-blocks (0 = off)
-    uint64_t* trace;    // [grid][4] MMA-issuer timing (diagnostics) or null
-    uint32_t hints;     // L2 cache-policy hints on the TMA loads
     __nv_bfloat16* out;
+    uint64_t* trace;  // [grid][4] MMA-issuer timing (diagnostics) or null
 };
 
 __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix, uint32_t G, uint32_t NT,
@@ -74,18 +77,26 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
     m = local - n * mt;
 }
 
-template <bool SWIGLU, bool GATHER>
-__global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
+// (tile, k-block) cursor of one operand stream of a CTA
+struct Cursor {
+    uint32_t tile, kb;
+    int32_t row;  // A row (arow) or B row (brow) of the current tile
+};
+
+template <bool SWIGLU>
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = base;
-    uint8_t* sB = base + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    uint8_t* sB = base;                 // NB x 32 KB (1024-aligned)
+    uint8_t* sA = base + NB * B_BYTES;  // NA x 16 KB
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(sA + NA * A_BYTES);
+    uint64_t* emptyA = fullA + NA;
+    uint64_t* fullB = emptyA + NA;
+    uint64_t* emptyB = fullB + NB;
+    uint64_t* tfull = emptyB + NB;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -93,9 +104,13 @@ __global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
     const uint32_t lane = threadIdx.x % 32;
 
     if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], GATHER ? 1 + kGatherThreads : 1);
-            mbar_init(&empty[s], 1);
+        for (uint32_t s = 0; s < NA; ++s) {
+            mbar_init(&fullA[s], 1);
+            mbar_init(&emptyA[s], 1);
+        }
+        for (uint32_t s = 0; s < NB; ++s) {
+            mbar_init(&fullB[s], 1);
+            mbar_init(&emptyB[s], 1);
         }
         for (uint32_t a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -118,73 +133,55 @@ __global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t total = s_prefix[p.G] * p.NT;
     const uint32_t nkb = p.K / BK;
-    const uint32_t NS = p.nstages;  // ring depth in use (<= STAGES; MOEPRISM_TC_STAGES, diagnostics)
 
     if (warp == 0) {
-        if constexpr (GATHER) {
-            // B tiles only (TMA); the A rows are streamed by the gather warps
-            if (lane == 0) {
-                uint32_t it = 0;
-                for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-                    uint32_t g, m, n;
-                    map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                    const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN);
-                    for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-                        const uint32_t s = it % NS, ph = (it / NS) & 1u;
-                        mbar_wait(&empty[s], ph ^ 1u);
-                        mbar_expect_tx(&full[s], B_BYTES);
-                        tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow);
-                    }
-                }
-            }
-        } else if (lane == 0) {
-            // L2 prefetch cursor PF k-blocks ahead of the loads (it walks into the
-            // next tile): the first CTA to touch a weight tile otherwise waits
-            // the full HBM latency with only ~3 slots of smem lookahead.
-            const uint32_t PF = p.prefetch;
-            uint32_t pf_tile = blockIdx.x, pf_kb = 0;
-            int32_t pf_arow = 0, pf_brow = 0;
-            auto pf_coords = [&]() {
+        if (lane == 0) {
+            // one ordered issue stream: B(j) then A(j - (NB - NA)), each behind
+            // its own empty barrier
+            auto set_rows = [&](Cursor& c, bool is_a) {
+                if (c.tile >= total) return;
                 uint32_t g, m, n;
-                map_tile(pf_tile, s_prefix, p.G, p.NT, g, m, n);
-                pf_arow = static_cast<int32_t>(s_off[g] + m * BM);
-                pf_brow = static_cast<int32_t>(g * p.N_group + n * BN);
+                map_tile(c.tile, s_prefix, p.G, p.NT, g, m, n);
+                c.row = is_a ? static_cast<int32_t>(s_off[g] + m * BM) : static_cast<int32_t>(g * p.N_group + n * BN);
             };
-            auto pf_issue_advance = [&]() {
-                if (pf_tile >= total) return;
-                tma_prefetch_l2_2d(&tmA, static_cast<int32_t>(pf_kb * BK), pf_arow);
-                tma_prefetch_l2_2d(&tmB, static_cast<int32_t>(pf_kb * BK), pf_brow);
-                if (++pf_kb == nkb) {
-                    pf_kb = 0;
-                    pf_tile += gridDim.x;
-                    if (pf_tile < total) pf_coords();
+            auto advance = [&](Cursor& c, bool is_a) {
+                if (++c.kb == nkb) {
+                    c.kb = 0;
+                    c.tile += gridDim.x;
+                    set_rows(c, is_a);
                 }
             };
-            if (PF && pf_tile < total) {
-                pf_coords();
-                for (uint32_t q = 0; q < PF; ++q) pf_issue_advance();
-            }
-            const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
-            uint32_t it = 0;
-            for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-                uint32_t g, m, n;
-                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM);
-                const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN);
-                for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-                    const uint32_t s = it % NS, ph = (it / NS) & 1u;
-                    mbar_wait(&empty[s], ph ^ 1u);
-                    mbar_expect_tx(&full[s], STAGE_BYTES);
-                    if (p.hints) {
-                        // A tiles are re-read by every N tile of the group: keep;
-                        // a weight tile is read by the group's few M tiles at once
-                        tma_load_2d_hint(sA + s * A_BYTES, &tmA, &full[s], static_cast<int32_t>(kb * BK), arow, pol_a);
-                        tma_load_2d_hint(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow, pol_b);
-                    } else {
-                        tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], static_cast<int32_t>(kb * BK), arow);
-                        tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow);
-                    }
-                    if (PF) pf_issue_advance();
+            Cursor cb{blockIdx.x, 0, 0}, ca{blockIdx.x, 0, 0};
+            set_rows(cb, false);
+            set_rows(ca, true);
+            uint32_t ib = 0, ia = 0;  // loads issued per stream
+            auto issue_b = [&]() {
+                const uint32_t s = ib % NB, ph = (ib / NB) & 1u;
+                mbar_wait(&emptyB[s], ph ^ 1u);
+                mbar_expect_tx(&fullB[s], B_BYTES);
+                tma_load_2d(sB + s * B_BYTES, &tmB, &fullB[s], static_cast<int32_t>(cb.kb * BK), cb.row);
+                advance(cb, false);
+                ++ib;
+            };
+            auto issue_a = [&]() {
+                const uint32_t s = ia % NA, ph = (ia / NA) & 1u;
+                mbar_wait(&emptyA[s], ph ^ 1u);
+                mbar_expect_tx(&fullA[s], A_BYTES);
+                tma_load_2d(sA + s * A_BYTES, &tmA, &fullA[s], static_cast<int32_t>(ca.kb * BK), ca.row);
+                advance(ca, true);
+                ++ia;
+            };
+            // the deeper ring's stream runs |NA - NB| loads ahead of the other
+            // one; each load waits only for its own slot to drain
+            while (cb.tile < total || ca.tile < total) {
+                if (NB >= NA) {
+                    if (cb.tile < total) issue_b();
+                    if (ca.tile < total && ib >= ia + (NB - NA)) issue_a();
+                    else if (cb.tile >= total && ca.tile < total) issue_a();
+                } else {
+                    if (ca.tile < total) issue_a();
+                    if (cb.tile < total && ia >= ib + (NA - NB)) issue_b();
+                    else if (ca.tile >= total && cb.tile < total) issue_b();
                 }
             }
         }
@@ -193,7 +190,7 @@ __global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
             constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
             uint32_t it = 0, tc = 0;
             // optional timing trace (MOEPRISM_TC_TRACE): cycles the MMA issuer
-            // waits for accumulators (epilogue) and for smem stages (loads)
+            // waits for accumulators (epilogue) and for operand stages (loads)
             const uint64_t t_start = p.trace ? clock64() : 0;
             uint64_t w_acc = 0, w_full = 0;
             for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
@@ -204,18 +201,21 @@ __global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-                    const uint32_t s = it % NS, ph = (it / NS) & 1u;
+                    const uint32_t sa = it % NA, pa = (it / NA) & 1u;
+                    const uint32_t sb = it % NB, pb = (it / NB) & 1u;
                     t0 = p.trace ? clock64() : 0;
-                    mbar_wait(&full[s], ph);
+                    mbar_wait(&fullB[sb], pb);
+                    mbar_wait(&fullA[sa], pa);
                     if (p.trace) w_full += clock64() - t0;
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(sA + s * A_BYTES);
-                    const uint32_t b0 = smem_u32(sB + s * B_BYTES);
+                    const uint32_t a0 = smem_u32(sA + sa * A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + sb * B_BYTES);
 #pragma unroll
                     for (uint32_t k = 0; k < BK / 16; ++k)
                         umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
                                   (kb | k) != 0u);
-                    umma_commit(&empty[s]);
+                    umma_commit(&emptyA[sa]);
+                    umma_commit(&emptyB[sb]);
                 }
                 umma_commit(&tfull[acc]);
             }
@@ -228,45 +228,6 @@ __global__ void __launch_bounds__(kThreads + (GATHER ? kGatherThreads : 0), 1)
             }
         }
         __syncwarp();
-    } else if (GATHER && warp >= kThreads / 32) {
-        // A-row gather: thread r owns row r of every tile; each k-block it
-        // copies the row's 128 bytes as 8 x 16-byte cp.async into the 128B-
-        // swizzled slot (chunk c of row r lands at chunk c ^ (r & 7), the
-        // layout a SW128 TMA tile load produces), zero-filling rows outside
-        // the group.  Completion: wait for the group issued STAGES-1 k-blocks
-        // ago, fence the generic->async proxy, arrive on that stage's full
-        // barrier (count 1 + 128).
-        const uint32_t LAG = NS - 1;
-        const uint32_t r = threadIdx.x - kThreads;
-        const uint32_t sw = (r & 7u) << 4;
-        uint32_t it = 0;
-        for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-            uint32_t g, m, n;
-            map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-            const uint32_t row_local = m * BM + r;
-            const bool valid = row_local < s_off[g + 1] - s_off[g];
-            const __nv_bfloat16* src = p.gx + (valid ? static_cast<size_t>(p.perm[s_off[g] + row_local]) * p.gd : 0);
-            for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-                const uint32_t s = it % NS, ph = (it / NS) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                const uint32_t dst = smem_u32(sA + s * A_BYTES + r * 128);
-#pragma unroll
-                for (uint32_t c = 0; c < 8; ++c) {
-                    const uint32_t col = kb * BK + c * 8;
-                    const uint32_t bytes = (valid && col < p.gd) ? 16u : 0u;
-                    cp_async_16(dst + ((c << 4) ^ sw), src + (bytes ? col : 0), bytes);
-                }
-                cp_async_commit();
-                if (it >= LAG) {
-                    cp_async_wait<STAGES - 1>();  // groups <= it - LAG complete (gather requires NS == STAGES)
-                    fence_proxy_async_smem();
-                    mbar_arrive(&full[(it - LAG) % NS]);
-                }
-            }
-        }
-        cp_async_wait<0>();
-        fence_proxy_async_smem();
-        for (uint32_t j = it > LAG ? it - LAG : 0; j < it; ++j) mbar_arrive(&full[j % NS]);
     } else {
         const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
         uint32_t tc = 0;
@@ -348,9 +309,25 @@ EncodeTiledFn get_encode_fn() {
     return fn;
 }
 
+uint64_t* g_trace[2] = {nullptr, nullptr};
+
 }  // namespace
 
 size_t gemm_tc_smem_bytes() { return kSmemBytes; }
+
+// MOEPRISM_TC_TRACE=1: per-CTA MMA-issuer timing of the last gemm1 / gemm2
+// launch, readable with mp_debug_gemm_trace (diagnostics only).
+uint64_t* gemm_trace_buffer(bool swiglu) {
+    static const bool on = [] {
+        const char* e = std::getenv("MOEPRISM_TC_TRACE");
+        return e && e[0] == '1';
+    }();
+    if (!on) return nullptr;
+    uint64_t*& b = g_trace[swiglu ? 0 : 1];
+    if (!b) cudaMalloc(&b, 1024 * 4 * sizeof(uint64_t));
+    return b;
+}
+uint64_t* gemm_trace_ptr(int which) { return g_trace[which & 1]; }
 
 bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                        uint32_t box_cols) {
@@ -365,24 +342,8 @@ bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// MOEPRISM_TC_TRACE=1: per-CTA MMA-issuer timing of the last gemm1 / gemm2
-// launch, readable with mp_debug_gemm_trace (diagnostics only).
-static uint64_t* g_trace[2] = {nullptr, nullptr};
-uint64_t* gemm_trace_buffer(bool swiglu) {
-    static const bool on = [] {
-        const char* e = std::getenv("MOEPRISM_TC_TRACE");
-        return e && e[0] == '1';
-    }();
-    if (!on) return nullptr;
-    uint64_t*& b = g_trace[swiglu ? 0 : 1];
-    if (!b) cudaMalloc(&b, 1024 * 4 * sizeof(uint64_t));
-    return b;
-}
-uint64_t* gemm_trace_ptr(int which) { return g_trace[which & 1]; }
-
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                    const uint32_t* gather_perm, const void* gather_x, uint32_t gather_d) {
+                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s) {
     TcParams p;
     p.G = sh.G;
     p.K = sh.K;
@@ -392,43 +353,21 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.NT = (sh.N_group + BN - 1) / BN;
     p.offsets = offsets;
     p.mprefix = mprefix;
-    p.perm = gather_perm;
-    p.gx = static_cast<const __nv_bfloat16*>(gather_x);
-    p.gd = gather_d;
-    static const uint32_t ns_env = [] {
-        const char* e = std::getenv("MOEPRISM_TC_STAGES");
-        const int v = e ? std::atoi(e) : (int)STAGES;
-        return (uint32_t)(v >= 2 && v <= (int)STAGES ? v : STAGES);
-    }();
-    p.nstages = ns_env;
-    static const uint32_t pf_env = [] {
-        const char* e = std::getenv("MOEPRISM_TC_PREFETCH");
-        return (uint32_t)(e ? std::atoi(e) : 0);  // measured: prefetching slows the loads (tests/probes/pf_sweep.sh)
-    }();
-    p.prefetch = pf_env;
-    p.trace = gemm_trace_buffer(swiglu);
-    static const uint32_t hint_env = [] {
-        const char* e = std::getenv("MOEPRISM_TC_HINTS");
-        return (uint32_t)(e ? std::atoi(e) : 0);
-    }();
-    p.hints = hint_env;
     p.out = static_cast<__nv_bfloat16*>(out);
+    p.trace = gemm_trace_buffer(swiglu);
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
     static bool attr_set = false;  // once per process (device-independent attribute)
     if (!attr_set) {
-        cudaFuncSetAttribute(gemm_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         attr_set = true;
     }
-    if (swiglu && gather_perm)
-        gemm_tc_kernel<true, true><<<grid, kThreads + kGatherThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
-    else if (swiglu)
-        gemm_tc_kernel<true, false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+    if (swiglu)
+        gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
     else
-        gemm_tc_kernel<false, false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+        gemm_tc_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
 }
 
 }  // namespace mp

@@ -100,11 +100,6 @@ struct mp_layer_s {
     size_t esz = 4;
     int num_sms = 0;
     bool use_tc = false;
-    // gemm1 gathering its A rows from x inside the GEMM (cp.async warps) instead of
-    // dispatch materialising x_perm: correct, but 2.6x slower at the Mixtral
-    // shape (each A tile is re-gathered for every N tile at L2 latency), so off
-    // unless MOEPRISM_GATHER=1 (experiments)
-    bool gather_ok = false;
     bool tile256 = false;  // gemm_tc2 (256-row tiles) instead of gemm_tc; MOEPRISM_TC_TILE=256|128
     bool has_experts = true, has_router = true;  // MP_LAYER_* role flags
 
@@ -306,28 +301,22 @@ void resolve_timings(mp_layer_s* L) {
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
                  cudaStream_t s, StageTimer& tm, bool check_finite = false) {
-    // bf16 tensor-core path: gemm1 gathers its A rows straight from x (TMA
-    // gather4), so dispatch only writes the permutation tables
-    // (cp.async warps inside gemm1; rows are 16-byte aligned when d % 8 == 0)
-    const bool gather = L->use_tc && L->gather_ok && (L->d % 8) == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
     tm.begin(1);
     mp::launch_bucket_local(sel, T, L->k_max, L->G, L->ws, s);
     mp::launch_bucket_scan(T, L->G, L->ws, s);
     ck_launch("bucket");
     tm.end(1, 2);
     tm.begin(2);
-    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, gather ? nullptr : L->x_perm, s,
-                        check_finite || !gather);
+    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, L->x_perm, s, true);
     ck_launch("dispatch");
     tm.end(2, 1);
     mp::GemmShape g1{L->G, L->d_pad, 2 * L->w_pad, T * L->k_max, L->w_pad, 2 * L->w_pad};
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
-    if (L->use_tc && L->tile256 && !gather)
+    if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s);
     else if (L->use_tc)
-        mp::launch_gemm_tc(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s,
-                           gather ? L->ws.perm_tok : nullptr, x, L->d);
+        mp::launch_gemm_tc(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
@@ -464,8 +453,6 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             L->use_tc = D.dtype == MP_DTYPE_BF16;
             if (const char* env = std::getenv("MOEPRISM_BF16_GEMM"))
                 if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
-            if (const char* env = std::getenv("MOEPRISM_GATHER"))
-                L->gather_ok = std::string(env) == "1";
             if (const char* env = std::getenv("MOEPRISM_TC_TILE"))
                 L->tile256 = std::string(env) == "256";
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;

@@ -92,12 +92,8 @@ void launch_gemm1_simt(int dtype, const void* A, const void* W1, void* H, const 
                        const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
 void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const GemmShape& sh,
                        const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
-// gather_perm != null (gemm1 only): the A rows are gathered from the token
-// matrix gather_x [T][gather_d] bf16 through the bucket permutation by
-// cp.async warps inside the GEMM (no x_perm materialisation); tmA unused.
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                    const uint32_t* gather_perm = nullptr, const void* gather_x = nullptr, uint32_t gather_d = 0);
+                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s);
 size_t gemm_tc_smem_bytes();
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
