@@ -247,6 +247,129 @@ def layer_roofline(T, k, ms, pk, touched_groups):
             "peak_tflops": pk["bf16_tflops_sustained"], "peak_gbs": pk["hbm_gbs"], "peak_source": pk["source"]}
 
 
+def roofline_fb(F, B, ms, pk):
+    """t_roofline = max(F / P_tc, B / BW) for F flops and B algorithmic bytes."""
+    t_tc = F / (pk["bf16_tflops_sustained"] * 1e12)
+    t_hbm = B / (pk["hbm_gbs"] * 1e9)
+    t_roof = max(t_tc, t_hbm)
+    return {"bound": "tensor" if t_tc >= t_hbm else "hbm", "t_roofline_ms": t_roof * 1e3, "t_measured_ms": ms,
+            "frac": (t_roof * 1e3) / ms, "tc_util": (F / (ms * 1e-3)) / (pk["bf16_tflops_sustained"] * 1e12)}
+
+
+def bench_stack(pk, n_layers=32, T=4096, ks=(2, 8), steps=10):
+    """BASELINE configs[2] / SURVEY 8(d) C3 on one GPU: a Mixtral-shape 32-layer
+    MoE stack, x_{l+1} = x_l + MoE_l(x_l) (residual fused into each layer's
+    combine), 32 independently seeded layers (90 GB of bf16 weights)."""
+    import torch
+    from paper_2510_19366_b200 import MoeLayer, synth_fill
+    layers = []
+    buf = [torch.empty(D * FF, dtype=torch.float32, device="cuda") for _ in range(3)]
+    for l in range(n_layers):
+        L = MoeLayer(E, S, D, FF, dtype="bf16", k_max=max(ks), max_tokens=T)
+        for e in range(E):
+            for m, (seed, scale) in enumerate(((100 + 3 * e, 1 / math.sqrt(D)), (101 + 3 * e, 1 / math.sqrt(D)),
+                                               (102 + 3 * e, 1 / math.sqrt(FF)))):
+                synth_fill(buf[m], seed + 7919 * l, scale)
+            L.set_partition(e, balanced_partition(FF, S, 6000 + e + 64 * l))
+            L.load_expert(e, *buf)
+        synth_fill(buf[0][:D * E * S], 7 + 7919 * l, 1 / math.sqrt(D))
+        L.set_router(buf[0][:D * E * S])
+        L.set_residual(True)
+        layers.append(L)
+    del buf
+    xa = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
+    synth_fill(xa, 11, 1.0)
+    xb = torch.empty_like(xa)
+    out = []
+    for k in ks:
+        def step(i, k=k):
+            x, y = xa, xb
+            for L in layers:
+                L.forward(x, k=k, y=y)
+                x, y = y, x
+        ms = time_steps(step, steps, 3, 1)
+        F = n_layers * 6.0 * D * W_SUB * T * k
+        B = n_layers * (E * S * 3.0 * D * W_SUB * 2 + 2.0 * T * D * 2)
+        out.append({"k": k, "tokens_per_s": T / (ms * 1e-3), "ms_per_pass": ms,
+                    "roofline": roofline_fb(F, B, ms, pk)})
+    for L in layers:
+        L.close()
+    torch.cuda.synchronize()
+    return {"workload": f"Mixtral-8x7B {n_layers}-layer MoE stack on 1 GPU (BASELINE configs[2] at N=1), "
+                        f"{T} tokens, residual x + MoE(x) fused, independently seeded layers",
+            "weights_gb": n_layers * E * S * 3 * D * W_SUB * 2 / 1e9, "sweep": out}
+
+
+QW = {"E": 60, "S": 4, "d": 2048, "ff": 1408, "ff_sh": 5632}
+
+
+def bench_qwen(pk, steps=30):
+    """BASELINE configs[3] / SURVEY 8(d) C4: Qwen1.5-MoE-A2.7B layer shape (60
+    experts x 4 sub-experts of w=352, E*S=240, plus the always-on shared expert
+    ffn=5632 with a sigmoid gate), decode T=64 and prefill T=8192."""
+    import numpy as np
+    import torch
+    from paper_2510_19366_b200 import MoeLayer, synth_fill
+    q = QW
+    Eq, Sq, d, ff, ffs = q["E"], q["S"], q["d"], q["ff"], q["ff_sh"]
+    w = ff // Sq
+    L = MoeLayer(Eq, Sq, d, ff, dtype="bf16", k_max=16, max_tokens=8192)
+    buf = [torch.empty(d * ff, dtype=torch.float32, device="cuda") for _ in range(3)]
+    for e in range(Eq):
+        for m, (seed, scale) in enumerate(((300 + 3 * e, 1 / math.sqrt(d)), (301 + 3 * e, 1 / math.sqrt(d)),
+                                           (302 + 3 * e, 1 / math.sqrt(ff)))):
+            synth_fill(buf[m], seed, scale)
+        L.set_partition(e, balanced_partition(ff, Sq, 6000 + e))
+        L.load_expert(e, *buf)
+    sh = [synth_fill(torch.empty(d * ffs, dtype=torch.float32, device="cuda"), 900 + m,
+                     1 / math.sqrt(ffs if m == 2 else d)) for m in range(3)]
+    gate = synth_fill(torch.empty(d, dtype=torch.float32, device="cuda"), 903, 1 / math.sqrt(d))
+    L.set_shared_expert(*sh, gate=gate)
+    wr = synth_fill(torch.empty(d * Eq * Sq, dtype=torch.float32, device="cuda"), 17, 1 / math.sqrt(d))
+    L.set_router(wr)
+    del buf, sh
+    out = []
+    for T in (64, 8192):
+        xs = [synth_fill(torch.empty((T, d), dtype=torch.bfloat16, device="cuda"), 19 + 1000 * i, 1.0)
+              for i in range(4)]
+        y = torch.empty((T, d), dtype=torch.bfloat16, device="cuda")
+        for k in (4, 8, 16):
+            _, _, _, off = L.forward(xs[0], k=k, return_routing=True)
+            touched = int((np.diff(off.cpu().numpy().view(np.uint32).astype(np.int64)) > 0).sum())
+            ms = time_steps(lambda i, k=k: L.forward(xs[i % 4], k=k, y=y), steps, 3, 1)
+            F = 6.0 * d * w * T * k + 6.0 * d * ffs * T
+            B = touched * 3.0 * d * w * 2 + 3.0 * d * ffs * 2 + 2.0 * T * d * 2
+            out.append({"tokens": T, "k": k, "tokens_per_s": T / (ms * 1e-3), "ms_per_step": ms,
+                        "touched_subexperts": touched, "roofline": roofline_fb(F, B, ms, pk)})
+        del xs
+    L.close()
+    torch.cuda.synchronize()
+    return {"workload": "Qwen1.5-MoE-A2.7B layer shape bf16 (BASELINE configs[3]): d=2048, 60 experts x 4 "
+                        "sub-experts (w=352, GEMM-padded to 384) + shared expert ffn=5632 (sigmoid gate); "
+                        "flops/bytes counted at w=352", "sweep": out}
+
+
+def bench_mixed_qos_32k(L32, pk, steps=10):
+    """BASELINE configs[4] / SURVEY 8(d) C5 on one GPU: 32768 tokens with
+    per-token elastic k from the 4 SLO tiers {2,4,8,16} (pmf .25/.35/.25/.15)."""
+    import numpy as np
+    import torch
+    from paper_2510_19366_b200 import synth_fill
+    T = 32768
+    xs = [synth_fill(torch.empty((T, D), dtype=torch.bfloat16, device="cuda"), 5011 + i, 1.0) for i in range(2)]
+    rng = np.random.default_rng(13)
+    kpt = torch.from_numpy(rng.choice([2, 4, 8, 16], size=T, p=[0.25, 0.35, 0.25, 0.15]).astype(np.int32)).cuda()
+    y = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
+    ms = time_steps(lambda i: L32.forward(xs[i % 2], k_per_token=kpt, y=y), steps, 3, 1)
+    kk = float(kpt.float().mean().item())
+    F = 6.0 * D * W_SUB * T * kk
+    B = E * S * 3.0 * D * W_SUB * 2 + 2.0 * T * D * 2
+    del xs
+    return {"workload": "mixed-QoS batch (BASELINE configs[4]) at N=1: 32768 tokens, Mixtral layer shape, "
+                        "per-token k tiers {2,4,8,16} pmf {.25,.35,.25,.15} seed 13",
+            "mean_k": kk, "tokens_per_s": T / (ms * 1e-3), "ms_per_step": ms, "roofline": roofline_fb(F, B, ms, pk)}
+
+
 def time_steps(fn, steps, warmup, world):
     import torch
     for i in range(warmup):
@@ -396,6 +519,10 @@ def workload_config(args, world):
                   "both > 126 MB L2"}
 
 
+def use_ep_flag(args, world):
+    return world > 1 or args.force_ep
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -407,6 +534,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-ep", action="store_true", help="run the expert-parallel path even at N=1 (loopback)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the other BASELINE configs (Qwen shape, 32-layer stack, 32k mixed-QoS batch)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -424,8 +553,10 @@ def main():
     T = args.tokens
     sweep = [int(v) for v in args.sweep.split(",") if v]
     use_ep = world > 1 or args.force_ep
+    extras = not args.no_extras and world == 1 and not use_ep_flag(args, world)
     if not use_ep:
-        L, xs = build_layer(local, T, k_max=16)
+        L, xs = build_layer(local, max(T, 32768) if extras else T, k_max=16)
+        xs = [x[:T] for x in xs] if extras and T < 32768 else xs
         layers = [L]
 
         def fwd(x, k, kpt, y=None):
@@ -500,6 +631,15 @@ def main():
            "d2h_bytes_per_step": T * D * 2, "ms_per_step": ms_e2e, "path": path}
     clk = clocks.stop()  # sampled across the main timed loop, the k sweep and the e2e loop
 
+    other = None
+    if extras:
+        other = {"mixed_qos_32k": bench_mixed_qos_32k(L, pk)}
+        other["qwen"] = bench_qwen(pk)
+        L.close()
+        layers = []
+        torch.cuda.empty_cache()
+        other["stack32"] = bench_stack(pk)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nthreads = os.cpu_count() or 1
@@ -522,6 +662,8 @@ def main():
                 "layer_roofline": layer_roofline(T, args.k, ms, pk, touched),
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
                 "stages_ms": stages_main, "sweep": sweep_out}
+        if other:
+            line["other_configs"] = other
         if main_k:
             line["roofline"] = main_k.get("kernel_roofline", line["roofline"])
         print(json.dumps(line), flush=True)

@@ -113,6 +113,23 @@ mp_status mp_layer_load_partition_map(mp_layer_t h, const char* ndjson_path);
 
 /* Linear router: w_r is d_model x (E*S) row-major fp32, host or device. */
 mp_status mp_layer_set_router(mp_layer_t h, const float* w_r);
+/* Shared (always-on) expert, Qwen1.5-MoE style (no
+ * reference counterpart, restated in the oracle): every token adds
+ * sigmoid(x . shared_gate) * toy_ffn_forward(shared, x) (inc/expert.hpp:79-96)
+ * after its routed sub-experts.  MPEX layout (d_model x d_ff_shared w_gate /
+ * w_up, d_ff_shared x d_model w_down), fp32, host or device; shared_gate is
+ * d_model fp32 or NULL (weight 1).  bf16 full layers only; applied by
+ * mp_layer_forward / mp_layer_forward_host (not by forward_selected, whose
+ * semantics are partitioned_forward's explicit active sets). */
+mp_status mp_layer_set_shared_expert(mp_layer_t h, uint32_t d_ff_shared, const float* w_gate, const float* w_up,
+                                     const float* w_down, const float* shared_gate);
+
+/* Fused residual (bf16 layers): mp_layer_forward / _host write
+ * y = x + MoE(x) (the x_{l+1} = x_l + MoE_l(x_l) step of a layer stack,
+ * SURVEY 8(d) C3), the residual being the combine's accumulator start value.
+ * y must not alias x.  Off by default. */
+mp_status mp_layer_set_residual(mp_layer_t h, int on);
+
 /* Proxy router gate set of expert e (inc/gating.hpp:19-43) in CSR form:
  * ids[offsets[s] .. offsets[s+1]) are the ascending gate neurons of s. */
 mp_status mp_layer_set_gates(mp_layer_t h, uint32_t e, uint32_t r, const uint32_t* offsets, const uint32_t* ids);

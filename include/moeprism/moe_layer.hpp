@@ -163,6 +163,15 @@ public:
             throw ValidationError("router weight must be d_model x (E*S)");
         detail::check(mp_layer_set_router(h_, w_r.data()));
     }
+    void set_residual(bool on) { detail::check(mp_layer_set_residual(h_, on ? 1 : 0)); }
+    // Qwen-style always-on shared expert; gate empty = weight 1 (moe_layer.h).
+    void set_shared_expert(const ToyExpert& x, std::span<const float> gate = {}) {
+        validate(x);
+        if (x.d_model != cfg_.d_model) throw ValidationError("shared expert d_model does not match the layer");
+        if (!gate.empty() && gate.size() != cfg_.d_model) throw ValidationError("shared gate must have d_model entries");
+        detail::check(mp_layer_set_shared_expert(h_, x.d_ff, x.w_gate.data(), x.w_up.data(), x.w_down.data(),
+                                                 gate.empty() ? nullptr : gate.data()));
+    }
     void set_gates(std::uint32_t e, const GateSet& g) {
         std::vector<std::uint32_t> off(1, 0), ids;
         for (const auto& l : g.gate_neurons) {

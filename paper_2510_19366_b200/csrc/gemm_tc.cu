@@ -53,6 +53,13 @@ constexpr uint32_t BM = kTcBM;  // 128
 constexpr uint32_t BN = 256;
 constexpr uint32_t BK = 64;  // one 128-byte swizzle row of bf16
 constexpr uint32_t NA = MP_TC_NA, NB = MP_TC_NB;
+#ifndef MP_TC_KCHAIN
+#define MP_TC_KCHAIN 0
+#endif
+// KCHAIN (experiment): two K-interleaved accumulator chains per tile (TMEM
+// holds one tile, no epilogue overlap) to hide the MMA dependency latency
+constexpr bool KCHAIN = MP_TC_KCHAIN != 0;
+constexpr uint32_t NACC = KCHAIN ? 1 : 2;
 constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr uint32_t B_BYTES = BN * BK * 2;
 constexpr uint32_t kThreads = 192;
@@ -202,11 +209,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t t_start = p.trace ? clock64() : 0;
             uint64_t w_acc = 0, w_full = 0;
             for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
-                const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+                const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
                 uint32_t g, m, n;
                 map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
                 const uint32_t rows = s_off[g + 1] - s_off[g] - m * BM;
-                const bool swapped = p.swap_tail && rows < BM;
+                const bool swapped = !KCHAIN && p.swap_tail && rows < BM;
                 // swapped tail: D^T = W . X^T, M = 128 weight rows per half, N = rows rounded to 16
                 const uint32_t idesc_sw = umma_idesc_bf16(BM, (rows + 15u) & ~15u);
                 uint64_t t0 = p.trace ? clock64() : 0;
@@ -226,9 +233,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b0 = smem_u32(sB + sb * B_BYTES);
                     if (!swapped) {
 #pragma unroll
-                        for (uint32_t k = 0; k < BK / 16; ++k)
-                            umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                                      (kb | k) != 0u);
+                        for (uint32_t k = 0; k < BK / 16; ++k) {
+                            if constexpr (KCHAIN)  // even / odd k-steps into two accumulators
+                                umma_bf16(d_tmem + (k & 1u) * BN, umma_desc_sw128(a0 + k * 32),
+                                          umma_desc_sw128(b0 + k * 32), idesc, (kb | (k >> 1)) != 0u);
+                            else
+                                umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                                          (kb | k) != 0u);
+                        }
                     } else {
 #pragma unroll
                         for (uint32_t k = 0; k < BK / 16; ++k) {
@@ -258,11 +270,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
             uint32_t g, m, n;
             map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-            const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+            const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
             const uint32_t rows = s_off[g + 1] - s_off[g] - m * BM;
-            if (p.swap_tail && rows < BM) {
+            if (!KCHAIN && p.swap_tail && rows < BM) {
                 // swapped tail: TMEM lane = weight row, column = token of the tile;
                 // half h (columns [128 h, 128 h + rows)) = weight rows 128 h + lane
                 const uint32_t i = q * 32 + lane;
@@ -311,6 +323,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld32(taddr + c * 32, gr);
                     tmem_ld32(taddr + 128 + c * 32, ur);
                     tmem_ld_wait();
+                    if constexpr (KCHAIN) {
+                        uint32_t g2[32], u2[32];
+                        tmem_ld32(taddr + BN + c * 32, g2);
+                        tmem_ld32(taddr + BN + 128 + c * 32, u2);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            gr[i] = __float_as_uint(__uint_as_float(gr[i]) + __uint_as_float(g2[i]));
+                            ur[i] = __float_as_uint(__uint_as_float(ur[i]) + __uint_as_float(u2[i]));
+                        }
+                    }
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -331,6 +354,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t r[32];
                     tmem_ld32(taddr + c * 32, r);
                     tmem_ld_wait();
+                    if constexpr (KCHAIN) {
+                        uint32_t r2[32];
+                        tmem_ld32(taddr + BN + c * 32, r2);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) + __uint_as_float(r2[i]));
+                    }
                     const uint32_t col = n * BN + c * 32;
                     if (valid && col < p.n_valid) {
                         uint32_t pk[16];

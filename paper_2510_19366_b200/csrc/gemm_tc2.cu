@@ -1,32 +1,131 @@
-// gemm_tc2.cu -- grouped GEMM with 256-row tiles on one SM: two M=128
-// tcgen05 accumulators (rows 0-127 / 128-255 of the tile, TMEM columns
-// [0,256) / [256,512)) share every 256-wide B k-slice.  Operand bytes per MMA
-// cycle drop by a third versus 128x256 tiles (A 32 KB + B 32 KB feed 1024
-// MMA cycles per 64-deep k-block), so the 3-stage smem ring covers 3072
-// cycles of TMA latency instead of 2048 -- the ring-depth sweep showed the
-// 128-row kernel is latency-limited.  The price: TMEM holds one tile, so the
-// epilogue (8 warps, one per 32 rows x accumulator) is not overlapped with
-// the next tile's MMAs.  Tiles whose last rows fit in 128 issue only the first
-// accumulator's MMAs, so the M-tail waste stays at 128-row granularity.
-// Same data layout, tile order and epilogues as gemm_tc.cu.
+// gemm_tc2.cu -- grouped GEMMs on CTA PAIRS (tcgen05.mma.cta_group::2): a
+// cluster of two CTAs on the two SMs of one TPC computes a 256 x 256 tile,
+// each CTA holding 128 rows of A and 128 of the 256 B rows in its own shared
+// memory; the MMA (issued by the leader CTA only) reads both halves and
+// writes each CTA's 128 rows x 256 columns into that CTA's TMEM.
+//
+// Why (measured, gemm_tc.cu trace + tests/probes/mma_cost.cu): the 1-SM
+// 128 x 256 kernel runs its MMAs at ~95% of the N/2-cycle floor while fed,
+// but waits 17-19% of the time for operand stages at k >= 8 -- every SM
+// pulls 48 KB of A+B per 64-deep k-block from L2 (~26 TB/s chip-wide at the
+// MMA floor).  A pair shares B: 32 KB per SM per k-block, one third less L2
+// -> SM traffic and shared-memory fill bandwidth for the same MMA work.
+//
+// Layout / semantics are gemm_tc.cu's (same packed weights, same epilogues):
+//   gemm1 (SWIGLU): B tile = W1 rows n*256 .. +255 (128 gate rows, then the
+//     128 up rows of the same neurons); CTA r loads rows n*256 + 128 r .. +127,
+//     so accumulator columns [0,128) are gate, [128,256) up, in both CTAs.
+//   gemm2: B tile = W2 rows n*256 .. +255 = output columns; CTA r loads its half.
+// Tiles are (g, n, m) with 256-row m tiles (prefix of ceil(count_g / 256)),
+// m fastest, strided over the clusters of a persistent grid.  Rows past the
+// group end are computed and discarded (masked stores).
+//
+// Barriers: full[s] lives in the leader CTA (both CTAs' TMA loads complete_tx
+// on it; the leader's expect_tx covers both); empty[s], tfull[a] are signalled
+// in both CTAs by a multicast tcgen05.commit; tempty[a] lives in the leader and
+// counts one arrival per epilogue warp of both CTAs (remote arrive for the
+// peer).  TMEM: 2 accumulators x 256 columns per CTA (epilogue of tile i
+// overlaps the MMAs of tile i+1), allocated with cta_group::2 by both CTAs.
+#include <cstdio>
+#include <cstdlib>
+
 #include "mp_common.cuh"
 #include "mp_kernels.h"
+
+#ifndef MP_PAIR_STAGES
+#define MP_PAIR_STAGES 6
+#endif
 
 namespace mp {
 
 namespace {
 
-constexpr uint32_t BM = 256, HM = 128, BN = 256, BK = 64, STAGES = 3;
-constexpr uint32_t A_BYTES = BM * BK * 2, AH_BYTES = HM * BK * 2, B_BYTES = BN * BK * 2;
-constexpr uint32_t kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
-constexpr size_t kSmemBytes = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+constexpr uint32_t BM = 256;  // rows per pair tile (128 per CTA)
+constexpr uint32_t HM = 128;
+constexpr uint32_t BN = 256;
+constexpr uint32_t BK = 64;
+constexpr uint32_t NS = MP_PAIR_STAGES;
+constexpr uint32_t A_BYTES = HM * BK * 2;   // 16 KB per CTA
+constexpr uint32_t B_BYTES = 128 * BK * 2;  // 16 KB per CTA (half of the 256-row B tile)
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr uint32_t kThreads = 192;  // warp 0 TMA, warp 1 TMEM alloc + MMA (leader), warps 2..5 epilogue
+constexpr uint32_t kTmemCols = 512;
+constexpr size_t kSmemBytes = 1024 + NS * STAGE_BYTES + 256;
 
-struct Tc2Params {
+struct PairParams {
     uint32_t G, K, N_group, n_valid, ld_out, NT;
     const uint32_t* offsets;
     const uint32_t* mprefix;  // prefix of ceil(count_g / 256)
     __nv_bfloat16* out;
 };
+
+MP_DEV uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+MP_DEV void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of `p` (own smem offset) in CTA `rank` of the cluster
+MP_DEV uint32_t mapa(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+MP_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+MP_DEV bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+MP_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait_cluster(bar, parity)) {
+    }
+}
+// TMA 2D tile load into own smem, completion signalled on an mbarrier that
+// may live in the peer CTA (cluster address)
+MP_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+}
+MP_DEV void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive (once) on the barrier at this smem offset in both CTAs of the pair
+// when all prior tcgen05 ops of this thread complete
+MP_DEV void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+MP_DEV void tmem_alloc_pair(uint32_t* smem_dst) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+MP_DEV void tmem_dealloc_pair(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kTmemCols) : "memory");
+}
 
 __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix, uint32_t G, uint32_t NT,
                                          uint32_t& g, uint32_t& m, uint32_t& n) {
@@ -46,41 +145,49 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
 }
 
 template <bool SWIGLU>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Tc2Params p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, PairParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = base;
-    uint8_t* sB = base + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    // identical offsets in both CTAs (same dynamic smem layout)
+    uint8_t* sA = base;                // NS x 16 KB
+    uint8_t* sB = base + NS * A_BYTES;  // NS x 16 KB
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + NS * STAGE_BYTES);
+    uint64_t* empty = full + NS;
+    uint64_t* tfull = empty + NS;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t warp = threadIdx.x / 32;
+    const uint32_t lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
     if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < STAGES; ++s) {
+        for (uint32_t s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, 256);
+        for (uint32_t a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+        }
         fence_mbar_init();
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
     }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
-    for (uint32_t q = threadIdx.x; q <= p.G; q += kThreads) {
+    if (warp == 1) tmem_alloc_pair(tmem_slot);
+    for (uint32_t q = threadIdx.x; q <= p.G; q += blockDim.x) {
         s_prefix[q] = p.mprefix[q];
         s_off[q] = p.offsets[q];
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // peer barriers initialised before any remote signal
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t total = s_prefix[p.G] * p.NT;
@@ -88,71 +195,65 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
+            const uint32_t full_leader = mapa(&full[0], 0);  // full[s] of the leader: + 8 s
             uint32_t it = 0;
-            for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+            for (uint32_t tile = pair; tile < total; tile += npairs) {
                 uint32_t g, m, n;
                 map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const uint32_t rows = min(BM, s_off[g + 1] - s_off[g] - m * BM);
-                const bool two = rows > HM;
-                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM);
-                const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN);
+                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * HM);
+                const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN + rank * 128);
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+                    const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
-                    mbar_expect_tx(&full[s], (two ? 2 : 1) * AH_BYTES + B_BYTES);
-                    uint8_t* a = sA + s * A_BYTES;
-                    tma_load_2d(a, &tmA, &full[s], static_cast<int32_t>(kb * BK), arow);
-                    if (two) tma_load_2d(a + AH_BYTES, &tmA, &full[s], static_cast<int32_t>(kb * BK), arow + HM);
-                    tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], static_cast<int32_t>(kb * BK), brow);
+                    if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+                    const uint32_t fb = full_leader + s * 8;
+                    tma_load_2d_pair(sA + s * A_BYTES, &tmA, fb, static_cast<int32_t>(kb * BK), arow);
+                    tma_load_2d_pair(sB + s * B_BYTES, &tmB, fb, static_cast<int32_t>(kb * BK), brow);
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_bf16(HM, BN);
+        if (rank == 0 && lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
             uint32_t it = 0, tc = 0;
-            for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
-                uint32_t g, m, n;
-                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const bool two = min(BM, s_off[g + 1] - s_off[g] - m * BM) > HM;
-                mbar_wait(tempty, (tc & 1u) ^ 1u);
+            for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
+                const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+                mbar_wait_cluster(&tempty[acc], aph ^ 1u);
                 tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
-                    const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+                    const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + s * A_BYTES);
                     const uint32_t b0 = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-                    for (uint32_t k = 0; k < BK / 16; ++k) {
-                        const uint64_t bd = umma_desc_sw128(b0 + k * 32);
-                        umma_bf16(tmem_base, umma_desc_sw128(a0 + k * 32), bd, idesc, (kb | k) != 0u);
-                        if (two)
-                            umma_bf16(tmem_base + BN, umma_desc_sw128(a0 + AH_BYTES + k * 32), bd, idesc,
-                                      (kb | k) != 0u);
-                    }
-                    umma_commit(&empty[s]);
+                    for (uint32_t k = 0; k < BK / 16; ++k)
+                        umma_bf16_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                                       (kb | k) != 0u);
+                    umma_commit_pair(&empty[s]);
                 }
-                umma_commit(tfull);
+                umma_commit_pair(&tfull[acc]);
             }
         }
         __syncwarp();
     } else {
-        const uint32_t q = warp & 3u;          // TMEM lane quarter
-        const uint32_t h = (warp - 2) >> 2;    // accumulator (tile half)
+        const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
+        const uint32_t tempty_leader = mapa(&tempty[0], 0);
         uint32_t tc = 0;
-        for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+        for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
             uint32_t g, m, n;
             map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-            const uint32_t cnt = s_off[g + 1] - s_off[g];
-            const bool two = min(BM, cnt - m * BM) > HM;
-            mbar_wait(tfull, tc & 1u);
+            const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+            mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            if (h == 0 || two) {
-                const uint32_t row_local = m * BM + h * HM + q * 32 + lane;
-                const bool valid = row_local < cnt;
-                __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + h * BN;
+            const uint32_t row_local = m * BM + rank * HM + q * 32 + lane;
+            const uint32_t cnt = s_off[g + 1] - s_off[g];
+            const bool valid = row_local < cnt;
+            const bool any = m * BM + rank * HM + q * 32 < cnt;  // warp has a valid row
+            __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN;
+            if (any) {
                 if constexpr (SWIGLU) {
 #pragma unroll 1
                     for (uint32_t c = 0; c < 4; ++c) {
@@ -197,35 +298,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(tempty);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader + acc * 8);
         }
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // the leader's last MMAs / the peer's last TMEM reads are done
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        tmem_dealloc_pair(tmem_base);
     }
 }
 
 }  // namespace
 
+size_t gemm_pair_smem_bytes() { return kSmemBytes; }
+
+// tmB: box of 128 rows (each CTA loads half of the 256-row B tile)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s) {
-    Tc2Params p{sh.G, sh.K, sh.N_group, sh.n_valid, sh.ld_out, (sh.N_group + BN - 1) / BN, offsets, mprefix256,
-                static_cast<__nv_bfloat16*>(out)};
+    PairParams p{sh.G, sh.K, sh.N_group, sh.n_valid, sh.ld_out, (sh.N_group + BN - 1) / BN, offsets, mprefix256,
+                 static_cast<__nv_bfloat16*>(out)};
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
-    const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
+    uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;
+    if (max_tiles < pairs) pairs = max_tiles;
+    if (pairs == 0) pairs = 1;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(gemm_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         attr_set = true;
     }
     if (swiglu)
-        gemm_tc2_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+        gemm_pair_kernel<true><<<2 * pairs, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
     else
-        gemm_tc2_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+        gemm_pair_kernel<false><<<2 * pairs, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
 }
 
 }  // namespace mp

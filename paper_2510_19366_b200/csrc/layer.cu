@@ -100,7 +100,10 @@ struct mp_layer_s {
     size_t esz = 4;
     int num_sms = 0;
     bool use_tc = false;
-    bool tile256 = false;  // gemm_tc2 (256-row tiles) instead of gemm_tc; MOEPRISM_TC_TILE=256|128
+    // grouped-GEMM kernel: 0 auto (CTA pairs, gemm_tc2, when the mean bucket has
+    // >= 192 rows, else 1-SM 128-row tiles, gemm_tc); MOEPRISM_TC_TILE=128|256 forces
+    int tile_mode = 0;
+    bool tile256 = false;  // this forward's choice
     bool has_experts = true, has_router = true;  // MP_LAYER_* role flags
 
     std::vector<std::vector<uint32_t>> assignment;
@@ -141,6 +144,20 @@ struct mp_layer_s {
     void* x_stage = nullptr;
     void* y_stage = nullptr;
     CUtensorMap tm_xperm{}, tm_h{}, tm_w1{}, tm_w2{};
+    CUtensorMap tm_w1h{}, tm_w2h{};  // 128-row boxes: each CTA of a pair loads half a B tile
+
+    // shared (always-on) expert, Qwen-style: one dense group of sh_w_pad neurons
+    uint32_t sh_ff = 0, sh_w_pad = 0, sh_w2_rows = 0;
+    void* W1s = nullptr;
+    void* W2s = nullptr;
+    float* sh_gate = nullptr;  // [d] or null (weight 1)
+    void* sh_h = nullptr;      // [max_tokens][sh_w_pad]
+    void* sh_o = nullptr;      // [max_tokens][d_pad]
+    float* sh_w = nullptr;     // [max_tokens]
+    uint32_t* sh_meta = nullptr;  // offsets {0, T}, tile prefixes {0, ceil(T/128)}, {0, ceil(T/256)}
+    CUtensorMap tm_w1s{}, tm_w2s{}, tm_hs{}, tm_w1sh{}, tm_w2sh{};
+
+    bool residual = false;  // mp_layer_set_residual: y = x + MoE(x), fused into the combine
 
     bool profiling = false;
     struct EventSet {
@@ -162,7 +179,8 @@ void free_layer(mp_layer_s* L) {
     void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_flagged, L->d_nmap, L->sel,
                     L->wsel, L->kpt_dev, L->ws.lrank, L->ws.block_counts, L->ws.block_base, L->ws.offsets,
                     L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.mprefix_tc2, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
-                    L->x_perm, L->h, L->o, L->x_stage, L->y_stage};
+                    L->x_perm, L->h, L->o, L->x_stage, L->y_stage, L->W1s, L->W2s, L->sh_gate, L->sh_h,
+                    L->sh_o, L->sh_w, L->sh_meta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto* v : {&L->ev_pool, &L->ev_pending})
@@ -300,7 +318,15 @@ void resolve_timings(mp_layer_s* L) {
 
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
-                 cudaStream_t s, StageTimer& tm, bool check_finite = false) {
+                 cudaStream_t s, StageTimer& tm, bool check_finite = false, bool with_shared = false,
+                 uint32_t kscalar = 0) {
+    // CTA-pair tiles pay up to 255 wasted rows per (sub-expert, N tile) against
+    // 127 for 128-row tiles; measured break-even near 192 rows per bucket
+    // (Mixtral shape: pairs win at k >= 4, lose at k = 2).  Per-token k: k_max.
+    {
+        const double rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
+        L->tile256 = L->tile_mode == 2 || (L->tile_mode == 0 && rows >= 192.0);
+    }
     tm.begin(1);
     mp::launch_bucket_local(sel, T, L->k_max, L->G, L->ws, s);
     mp::launch_bucket_scan(T, L->G, L->ws, s);
@@ -314,35 +340,62 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
     if (L->use_tc && L->tile256)
-        mp::launch_gemm_tc2(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s);
+        mp::launch_gemm_tc2(true, &L->tm_xperm, &L->tm_w1h, L->h, g1, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s);
     else if (L->use_tc)
         mp::launch_gemm_tc(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
-    tm.end(3, 1);
+    const bool shared = with_shared && L->sh_ff;
+    const bool sh_pair = L->tile_mode == 2 || (L->tile_mode == 0 && T >= 192);
+    if (shared) {  // shared expert: A = x itself (every token), one group
+        CUtensorMap tmX;
+        if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "shared expert tensor map");
+        mp::GemmShape s1{1, L->d_pad, 2 * L->sh_w_pad, T, L->sh_w_pad, 2 * L->sh_w_pad};
+        if (sh_pair)
+            mp::launch_gemm_tc2(true, &tmX, &L->tm_w1sh, L->sh_h, s1, L->sh_meta, L->sh_meta + 4, L->num_sms, s);
+        else
+            mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, L->num_sms, s);
+        ck_launch("shared gemm1");
+    }
+    tm.end(3, shared ? 2 : 1);
     tm.begin(4);
     if (L->use_tc && L->tile256)
-        mp::launch_gemm_tc2(false, &L->tm_h, &L->tm_w2, L->o, g2, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s);
+        mp::launch_gemm_tc2(false, &L->tm_h, &L->tm_w2h, L->o, g2, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s);
     else if (L->use_tc)
         mp::launch_gemm_tc(false, &L->tm_h, &L->tm_w2, L->o, g2, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
     else
         mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm2");
-    tm.end(4, 1);
+    if (shared) {
+        mp::GemmShape s2{1, L->sh_w_pad, L->d_pad, T, L->d_pad, L->d_pad};
+        if (sh_pair)
+            mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, s);
+        else
+            mp::launch_gemm_tc(false, &L->tm_hs, &L->tm_w2s, L->sh_o, s2, L->sh_meta, L->sh_meta + 2, L->num_sms, s);
+        ck_launch("shared gemm2");
+    }
+    tm.end(4, shared ? 2 : 1);
     tm.begin(5);
     const uint32_t group_S = unit ? L->S : 0;
-    mp::launch_combine(L->dtype, L->o, L->d, L->d_pad, L->ws.slot_row, sel, w, L->k_max, group_S, T, y, s);
+    mp::launch_combine(L->dtype, L->o, L->d, L->d_pad, L->ws.slot_row, sel, w, L->k_max, group_S, T, y, s,
+                       shared ? L->sh_o : nullptr, shared ? L->sh_w : nullptr,
+                       (with_shared && L->residual) ? x : nullptr);
     ck_launch("combine");
     tm.end(5, 1);
 }
 
 void route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32_t k, cudaStream_t s,
-           StageTimer& tm) {
+           StageTimer& tm, bool with_shared = false) {
     if (!kpt && (k < 1 || k > L->k_max || k > L->G))
         fail(MP_ERR_VALIDATION, "k_active = " + std::to_string(k) + " out of range [1, " +
                                     std::to_string(std::min(L->k_max, L->G)) + "]");
     tm.begin(0);
+    if (with_shared && L->sh_ff) {
+        if (reinterpret_cast<uintptr_t>(x) % 16) fail(MP_ERR_VALIDATION, "shared expert needs 16-byte aligned x");
+        mp::launch_shared_gate(x, T, L->d, L->sh_gate, L->sh_w, L->sh_meta, L->sh_meta + 2, s);
+        L->launches += 1;
+    }
     if (L->desc.router_mode == MP_ROUTER_PROXY) {
         pack_gates(L);
         mp::launch_proxy_scores(L->dtype, x, T, L->d, L->gate_rows, L->up_rows, L->gate_off, L->n_gate_rows, L->G,
@@ -454,7 +507,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             if (const char* env = std::getenv("MOEPRISM_BF16_GEMM"))
                 if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
             if (const char* env = std::getenv("MOEPRISM_TC_TILE"))
-                L->tile256 = std::string(env) == "256";
+                L->tile_mode = std::string(env) == "256" ? 2 : std::string(env) == "128" ? 1 : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
             L->d_pad = round_up(L->d, 64);
@@ -527,7 +580,9 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                         mp::make_tmap_bf16_2d(&L->tm_xperm, L->x_perm, L->rows_cap, L->d_pad, 128, 64) &&
                         mp::make_tmap_bf16_2d(&L->tm_w1, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 256, 64) &&
                         mp::make_tmap_bf16_2d(&L->tm_h, L->h, L->rows_cap, L->w_pad, 128, 64) &&
-                        mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64);
+                        mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_w1h, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 128, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_w2h, L->W2, L->w2_rows, L->w_pad, 128, 64);
                     if (!ok) fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                 }
             }
@@ -666,6 +721,86 @@ MP_API mp_status mp_layer_set_router(mp_layer_t L, const float* w_r) {
     });
 }
 
+MP_API mp_status mp_layer_set_shared_expert(mp_layer_t L, uint32_t ff_sh, const float* wg, const float* wu,
+                                            const float* wd, const float* gate) {
+    return guarded([&] {
+        if (!L || !wg || !wu || !wd) fail(MP_ERR_VALIDATION, "null argument");
+        if (!L->has_experts || !L->has_router)
+            fail(MP_ERR_VALIDATION, "the shared expert belongs to a full layer (no EP role flags)");
+        if (L->dtype != MP_DTYPE_BF16 || !L->use_tc) fail(MP_ERR_VALIDATION, "the shared expert needs the bf16 dtype");
+        if (ff_sh < 1) fail(MP_ERR_VALIDATION, "shared expert needs d_ff >= 1");
+        if (L->d % 8) fail(MP_ERR_VALIDATION, "shared expert needs d_model % 8 == 0 (16-byte rows for TMA)");
+        if (L->sh_ff) fail(MP_ERR_VALIDATION, "shared expert already set");
+        DeviceGuard dg(L->desc.device);
+        const uint32_t w_pad = round_up(ff_sh, 128);
+        const uint32_t w2_rows = round_up(L->d_pad, 256);
+        const size_t n = (size_t)L->d * ff_sh;
+        float* raw = dalloc<float>(3 * n, "shared staging");
+        int32_t* nmap = nullptr;
+        try {
+            const float* srcs[3] = {wg, wu, wd};
+            for (int m = 0; m < 3; ++m)
+                ck(cudaMemcpy(raw + m * n, srcs[m], n * sizeof(float), cudaMemcpyDefault), "shared upload");
+            ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset");
+            mp::launch_finite_check(raw, 3 * n, L->ws.err, 0);
+            int flag = 0;
+            ck(cudaMemcpy(&flag, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+            if (flag) fail(MP_ERR_VALIDATION, "shared expert weight is not finite");
+            std::vector<int32_t> id(w_pad, -1);
+            for (uint32_t j = 0; j < ff_sh; ++j) id[j] = static_cast<int32_t>(j);
+            nmap = dalloc<int32_t>(w_pad, "shared nmap");
+            ck(cudaMemcpy(nmap, id.data(), w_pad * 4, cudaMemcpyHostToDevice), "nmap");
+            L->W1s = dalloc<char>((size_t)2 * w_pad * L->d_pad * 2, "W1 shared");
+            L->W2s = dalloc<char>((size_t)w2_rows * w_pad * 2, "W2 shared");
+            ck(cudaMemset(L->W2s, 0, (size_t)w2_rows * w_pad * 2), "memset");
+            mp::launch_pack_w1(L->dtype, raw, raw + n, L->d, ff_sh, nmap, 1, w_pad, L->d_pad, L->W1s, 0);
+            mp::launch_pack_w2(L->dtype, raw + 2 * n, L->d, ff_sh, nmap, 1, w_pad, L->d_pad, L->W2s, 0);
+            ck_launch("shared pack");
+            if (gate) {
+                L->sh_gate = dalloc<float>(L->d, "shared gate");
+                ck(cudaMemcpy(L->sh_gate, gate, L->d * sizeof(float), cudaMemcpyDefault), "shared gate");
+                ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset");
+                mp::launch_finite_check(L->sh_gate, L->d, L->ws.err, 0);
+                ck(cudaMemcpy(&flag, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+                if (flag) fail(MP_ERR_VALIDATION, "shared expert gate is not finite");
+            }
+            L->sh_h = dalloc<char>((size_t)L->max_tokens * w_pad * 2, "shared h");
+            L->sh_o = dalloc<char>((size_t)L->max_tokens * L->d_pad * 2, "shared o");
+            L->sh_w = dalloc<float>(L->max_tokens, "shared w");
+            L->sh_meta = dalloc<uint32_t>(6, "shared meta");
+            bool ok = mp::make_tmap_bf16_2d(&L->tm_w1s, L->W1s, 2ull * w_pad, L->d_pad, 256, 64) &&
+                      mp::make_tmap_bf16_2d(&L->tm_w2s, L->W2s, w2_rows, w_pad, 256, 64) &&
+                      mp::make_tmap_bf16_2d(&L->tm_hs, L->sh_h, L->max_tokens, w_pad, 128, 64) &&
+                      mp::make_tmap_bf16_2d(&L->tm_w1sh, L->W1s, 2ull * w_pad, L->d_pad, 128, 64) &&
+                      mp::make_tmap_bf16_2d(&L->tm_w2sh, L->W2s, w2_rows, w_pad, 128, 64);
+            if (!ok) fail(MP_ERR_CUDA, "shared expert tensor maps");
+            ck(cudaDeviceSynchronize(), "shared pack");
+        } catch (...) {
+            cudaFree(raw);
+            if (nmap) cudaFree(nmap);
+            for (void** p : {&L->W1s, &L->W2s, reinterpret_cast<void**>(&L->sh_gate), &L->sh_h, &L->sh_o,
+                             reinterpret_cast<void**>(&L->sh_w), reinterpret_cast<void**>(&L->sh_meta)}) {
+                if (*p) cudaFree(*p);
+                *p = nullptr;
+            }
+            throw;
+        }
+        cudaFree(raw);
+        cudaFree(nmap);
+        L->sh_ff = ff_sh;
+        L->sh_w_pad = w_pad;
+        L->sh_w2_rows = w2_rows;
+    });
+}
+
+MP_API mp_status mp_layer_set_residual(mp_layer_t L, int on) {
+    return guarded([&] {
+        if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        if (on && L->dtype != MP_DTYPE_BF16) fail(MP_ERR_VALIDATION, "the fused residual needs the bf16 dtype");
+        L->residual = on != 0;
+    });
+}
+
 MP_API mp_status mp_layer_set_gates(mp_layer_t L, uint32_t e, uint32_t r, const uint32_t* off, const uint32_t* ids) {
     return guarded([&] {
         if (!L || !off || !ids) fail(MP_ERR_VALIDATION, "null argument");
@@ -700,8 +835,9 @@ MP_API mp_status mp_layer_forward(mp_layer_t L, const void* x, uint32_t T, const
         DeviceGuard dg(L->desc.device);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         StageTimer tm(L, s);
-        route(L, x, T, kpt, k, s, tm);
-        run_experts(L, x, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, y, s, tm);
+        route(L, x, T, kpt, k, s, tm, true);
+        run_experts(L, x, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, y, s, tm, false, true,
+                    kpt ? 0 : k);
         copy_outputs(L, T, sel_out, w_out, offsets_out, s, cudaMemcpyDeviceToDevice);
         static const int order[] = {0, 1, 2, 3, 4, 5};
         tm.finish(order, 6);
@@ -731,8 +867,9 @@ MP_API mp_status mp_layer_forward_host(mp_layer_t L, const void* x, uint32_t T, 
             kd = L->kpt_dev;
         }
         StageTimer tm(L, s);
-        route(L, L->x_stage, T, kd, k, s, tm);
-        run_experts(L, L->x_stage, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, L->y_stage, s, tm, true);
+        route(L, L->x_stage, T, kd, k, s, tm, true);
+        run_experts(L, L->x_stage, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, L->y_stage, s, tm, true,
+                    true, kpt ? 0 : k);
         ck(cudaMemcpyAsync(y, L->y_stage, xbytes, cudaMemcpyDeviceToHost, s), "y download");
         copy_outputs(L, T, sel_out, w_out, offsets_out, s, cudaMemcpyDeviceToHost);
         int flags = 0;
@@ -974,5 +1111,15 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
         uint64_t* p = mp::gemm_trace_ptr(which);
         if (!p) fail(MP_ERR_VALIDATION, "trace off (MOEPRISM_TC_TRACE=1)");
         ck(cudaMemcpy(out, p, (size_t)n_ctas * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost), "trace");
+    });
+}
+
+// Diagnostics (not in the public header): grouped-GEMM kernel choice of a
+// layer at run time, 0 auto / 1 one-SM 128-row tiles / 2 CTA-pair 256-row
+// tiles, for in-process A/B timing (tests/probes/tile_ab.py).
+MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
+    return guarded([&] {
+        if (!L || mode < 0 || mode > 2) fail(MP_ERR_VALIDATION, "bad argument");
+        L->tile_mode = mode;
     });
 }

@@ -45,9 +45,15 @@ void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t 
                      const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s,
                      bool check_finite = true);
 // group_S > 0: unit-weight semantics, round once per parent expert (fp32 mode)
+// o_sh / w_sh (bf16 only, nullable): shared-expert output rows [T][d_pad] and
+// per-token weights, added after the routed sub-experts; x_res (bf16 only,
+// nullable): residual input [T][d], y = x_res + sum (accumulator start value)
 void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
                     const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
-                    cudaStream_t s);
+                    cudaStream_t s, const void* o_sh = nullptr, const float* w_sh = nullptr,
+                    const void* x_res = nullptr);
+void launch_shared_gate(const void* x, uint32_t T, uint32_t d, const float* gate, float* w_sh, uint32_t* sh_off,
+                        uint32_t* sh_mprefix, cudaStream_t s);
 
 // Tensor-core linear router (router_tc.cu): plan, weight split, launch, and
 // the fixed-order fp64 reduction of the K-split partials + top-k (route.cu).
@@ -97,7 +103,7 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
 size_t gemm_tc_smem_bytes();
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
-// 256-row tiles, two M=128 accumulators sharing B (gemm_tc2.cu)
+// CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s);
 

@@ -506,6 +506,9 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
 __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* __restrict__ o, uint32_t d,
                                                            uint32_t d_pad, const uint32_t* __restrict__ slot_row,
                                                            const float* __restrict__ w, uint32_t k_max,
+                                                           const __nv_bfloat16* __restrict__ o_sh,
+                                                           const float* __restrict__ w_sh,
+                                                           const __nv_bfloat16* __restrict__ x_res,
                                                            __nv_bfloat16* __restrict__ y) {
     __shared__ uint32_t rows[64];
     __shared__ float wts[64];
@@ -519,6 +522,16 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
     if ((d % 8) == 0) {
         for (uint32_t c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
             float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (x_res) {  // fused residual: y = x + MoE(x)
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(x_res + (size_t)t * d + c));
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(h[q]);
+                    acc[2 * q] = f.x;
+                    acc[2 * q + 1] = f.y;
+                }
+            }
             for (uint32_t j = 0; j < k_max; ++j) {
                 const uint32_t r = rows[j];
                 if (r == kSelNone) continue;
@@ -532,6 +545,17 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
                     acc[2 * q + 1] = fmaf(wj, f.y, acc[2 * q + 1]);
                 }
             }
+            if (o_sh) {  // shared expert last (its ids follow the routed ones)
+                const float ws = w_sh[t];
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(o_sh + (size_t)t * d_pad + c));
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(h[q]);
+                    acc[2 * q] = fmaf(ws, f.x, acc[2 * q]);
+                    acc[2 * q + 1] = fmaf(ws, f.y, acc[2 * q + 1]);
+                }
+            }
             uint4 out;
             out.x = pack_bf16x2(acc[0], acc[1]);
             out.y = pack_bf16x2(acc[2], acc[3]);
@@ -541,9 +565,10 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
         }
     } else {
         for (uint32_t c = threadIdx.x; c < d; c += blockDim.x) {
-            float acc = 0.0f;
+            float acc = x_res ? __bfloat162float(x_res[(size_t)t * d + c]) : 0.0f;
             for (uint32_t j = 0; j < k_max; ++j)
                 if (rows[j] != kSelNone) acc = fmaf(wts[j], __bfloat162float(o[(size_t)rows[j] * d_pad + c]), acc);
+            if (o_sh) acc = fmaf(w_sh[t], __bfloat162float(o_sh[(size_t)t * d_pad + c]), acc);
             yr[c] = __float2bfloat16_rn(acc);
         }
     }
@@ -672,11 +697,49 @@ void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t 
                                                     static_cast<float*>(x_perm), ws.err, check_finite);
 }
 
+// Shared expert gate (Qwen-style): w_sh[t] = sigmoid(x_t . gate)
+// (1 when gate is null), warp per token, fixed-order fp32 reduction; block 0
+// also writes the one-group offsets {0, T} and 128-row tile prefix of the
+// shared expert's grouped GEMMs.
+__global__ void __launch_bounds__(256) shared_gate_kernel(const __nv_bfloat16* __restrict__ x, uint32_t T, uint32_t d,
+                                                          const float* __restrict__ gate, float* __restrict__ w_sh,
+                                                          uint32_t* __restrict__ sh_off,
+                                                          uint32_t* __restrict__ sh_mprefix) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sh_off[0] = 0;
+        sh_off[1] = T;
+        sh_mprefix[0] = 0;
+        sh_mprefix[1] = (T + kTcBM - 1) / kTcBM;
+        sh_mprefix[2] = 0;  // 256-row (CTA pair) tiles
+        sh_mprefix[3] = (T + 255) / 256;
+    }
+    const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x & 31;
+    if (t >= T) return;
+    if (!gate) {
+        if (lane == 0) w_sh[t] = 1.0f;
+        return;
+    }
+    const __nv_bfloat16* xr = x + (size_t)t * d;
+    float acc = 0.0f;
+    for (uint32_t c = lane; c < d; c += 32) acc = fmaf(__bfloat162float(xr[c]), gate[c], acc);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) w_sh[t] = 1.0f / (1.0f + expf(-acc));
+}
+
+void launch_shared_gate(const void* x, uint32_t T, uint32_t d, const float* gate, float* w_sh, uint32_t* sh_off,
+                        uint32_t* sh_mprefix, cudaStream_t s) {
+    shared_gate_kernel<<<(T + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), T, d, gate, w_sh, sh_off,
+                                                   sh_mprefix);
+}
+
 void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
                     const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
-                    cudaStream_t s) {
+                    cudaStream_t s, const void* o_sh, const float* w_sh, const void* x_res) {
     if (dtype == 1)
         combine_bf16_kernel<<<T, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(o), d, d_pad, slot_row, w, k_max,
+                                              static_cast<const __nv_bfloat16*>(o_sh), w_sh,
+                                              static_cast<const __nv_bfloat16*>(x_res),
                                               static_cast<__nv_bfloat16*>(y));
     else
         combine_f64_kernel<<<T, 256, 0, s>>>(static_cast<const double*>(o), d, d_pad, slot_row, sel, w, k_max, group_S,

@@ -92,6 +92,18 @@ class MoeLayer:
         w = self._f32(w_r)
         check(self.lib.mp_layer_set_router(self.h, _ptr(w)))
 
+    def set_shared_expert(self, w_gate, w_up, w_down, gate=None):
+        """Always-on shared expert (Qwen1.5-MoE style): y += sigmoid(x . gate) * ffn(x).
+        MPEX layout fp32 (w_gate, w_up d x ff_sh; w_down ff_sh x d); gate d fp32 or None (weight 1)."""
+        keep = [self._f32(w) for w in (w_gate, w_up, w_down)]
+        g = None if gate is None else self._f32(gate)
+        ff_sh = (keep[0].size if isinstance(keep[0], np.ndarray) else keep[0].numel()) // self.d
+        check(self.lib.mp_layer_set_shared_expert(self.h, ff_sh, *(_ptr(w) for w in keep), _ptr(g)))
+
+    def set_residual(self, on: bool = True):
+        """Fused residual: forward returns x + MoE(x) (bf16 layers; y must not alias x)."""
+        check(self.lib.mp_layer_set_residual(self.h, int(on)))
+
     def set_gates(self, e: int, r: int, gates: Sequence[Sequence[int]]):
         off = np.zeros(len(gates) + 1, np.uint32)
         for s, g in enumerate(gates):

@@ -75,3 +75,31 @@ def bf16_ok(got, want, tol=2e-2):
 
 def out_ok(got, want, dtype):
     return close_mask(got, want, 1e-5) if dtype == "f32" else bf16_ok(got, want)
+
+
+def torch_layer_reference(torch, gen_expert, parts, S, d, xb, sel, w):
+    """Plain PyTorch fp32 reference of the bf16 layer over ALL tokens:
+    h = bf16(silu(x Wg_s) * (x Wu_s)), o = bf16(h Wd_s), y = sum_slots w * o,
+    weights bf16-rounded, fp32 matmuls (no TF32).  Covers every row of every
+    bucket, including the last (partial) GEMM tile of each sub-expert."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    T = xb.shape[0]
+    xt = torch.from_numpy(xb).cuda()
+    sel_t = torch.from_numpy(sel.astype(np.int64)).cuda()
+    w_t = torch.from_numpy(w).cuda()
+    y = torch.zeros((T, d), dtype=torch.float32, device="cuda")
+    for e, part in enumerate(parts):
+        wg, wu, wd = gen_expert(e)
+        for s in range(S):
+            idx = torch.from_numpy(np.nonzero(part == s)[0]).cuda()
+            hit = sel_t == e * S + s
+            tok = hit.any(dim=1).nonzero().squeeze(1)
+            if tok.numel() == 0:
+                continue
+            slot_w = (w_t * hit).sum(dim=1)[tok]
+            xa = xt[tok]
+            h = torch.nn.functional.silu(xa @ wg[:, idx]) * (xa @ wu[:, idx])
+            h = h.bfloat16().float()
+            o = (h @ wd[idx, :]).bfloat16().float()
+            y.index_add_(0, tok, o * slot_w[:, None])
+    return y.cpu().numpy()

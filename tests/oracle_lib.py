@@ -129,6 +129,19 @@ class Oracle:
         self._check(self.L.orc_toy_ffn_forward(d, ff, wg, wu, wd, np.ascontiguousarray(x, np.float32), len(x), y, a))
         return y, a
 
+    def shared_expert_forward(self, d, ff_sh, wg, wu, wd, gate, x):
+        """Restated shared (always-on) expert, Qwen1.5-MoE style (SURVEY 8(d) C4;
+        no reference counterpart): sigmoid(x . gate) * toy_ffn_forward(x)
+        (inc/expert.hpp:79-96), gate dot product in double, i ascending.
+        Returns float64 (T, d); gate None = weight 1."""
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty(x.shape, np.float64)
+        for t in range(x.shape[0]):
+            y, _ = self.toy_ffn_forward(d, ff_sh, wg, wu, wd, x[t])
+            s = 1.0 if gate is None else 1.0 / (1.0 + np.exp(-np.dot(x[t].astype(np.float64), gate.astype(np.float64))))
+            out[t] = s * y.astype(np.float64)
+        return out
+
     def partitioned_forward(self, d, ff, wg, wu, wd, n_sub, assignment, x, active):
         y = np.empty(d, np.float32)
         act = np.ascontiguousarray(np.asarray(active, np.uint32).reshape(-1))
@@ -295,6 +308,19 @@ class RefLib:
         a = np.empty(ff, np.float32)
         self._check(self.L.ref_toy_ffn_forward(d, ff, wg, wu, wd, np.ascontiguousarray(x, np.float32), len(x), y, a))
         return y, a
+
+    def shared_expert_forward(self, d, ff_sh, wg, wu, wd, gate, x):
+        """Restated shared (always-on) expert, Qwen1.5-MoE style (SURVEY 8(d) C4;
+        no reference counterpart): sigmoid(x . gate) * toy_ffn_forward(x)
+        (inc/expert.hpp:79-96), gate dot product in double, i ascending.
+        Returns float64 (T, d); gate None = weight 1."""
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty(x.shape, np.float64)
+        for t in range(x.shape[0]):
+            y, _ = self.toy_ffn_forward(d, ff_sh, wg, wu, wd, x[t])
+            s = 1.0 if gate is None else 1.0 / (1.0 + np.exp(-np.dot(x[t].astype(np.float64), gate.astype(np.float64))))
+            out[t] = s * y.astype(np.float64)
+        return out
 
     def partitioned_forward(self, d, ff, wg, wu, wd, n_sub, assignment, x, active):
         y = np.empty(d, np.float32)

@@ -1,0 +1,85 @@
+// mma_cost.cu -- microbenchmark: cycles per tcgen05.mma.cta_group::1.kind::f16
+// (M=128, K=16, both operands in shared memory, SW128 K-major) as a function
+// of N, with one or two accumulators per k-step.  One CTA per SM, operands
+// resident in smem (no TMA), throughput measured over many MMAs.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//        -I paper_2510_19366_b200/csrc tests/probes/mma_cost.cu -o tests/probes/mma_cost -lcuda
+#include <cstdio>
+#include <vector>
+
+#include "mp_common.cuh"
+
+using namespace mp;
+
+__global__ void __launch_bounds__(128, 1) mma_cost_kernel(uint32_t n, uint32_t two, uint32_t iters, uint64_t* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = base;              // 128 rows x 64 bf16 (16 KB)
+    uint8_t* sB = base + 16384;      // 256 rows x 64 bf16 (32 KB)
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_slot;
+    for (uint32_t i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(base)[i] = 0x3f803f80u;  // bf16 1.0
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x < 32) tmem_alloc<512>(&tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (threadIdx.x == 0) {
+        const uint32_t idesc = umma_idesc_bf16(128, n);
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+        uint64_t t0 = clock64();
+        for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) {
+                umma_bf16(tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc, 1);
+                if (two) umma_bf16(tmem + 256, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + 16384 + k * 32),
+                                   idesc, 1);
+            }
+        }
+        umma_commit(&bar);
+        mbar_wait(&bar, 0);
+        uint64_t t1 = clock64();
+        out[blockIdx.x] = t1 - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    uint64_t* d_out;
+    cudaMalloc(&d_out, sms * sizeof(uint64_t));
+    const size_t smem = 1024 + 16384 + 32768;
+    cudaFuncSetAttribute(mma_cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint32_t iters = 2000;
+    printf("N,accumulators,cycles_per_mma,floor_N_over_2,flop_per_cycle_per_sm\n");
+    for (uint32_t two = 0; two < 2; ++two)
+        for (uint32_t n : {16u, 32u, 48u, 64u, 96u, 128u, 160u, 192u, 256u}) {
+            mma_cost_kernel<<<sms, 128, smem>>>(n, two, iters, d_out);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) {
+                printf("error %s\n", cudaGetErrorString(e));
+                return 1;
+            }
+            std::vector<uint64_t> h(sms);
+            cudaMemcpy(h.data(), d_out, sms * 8, cudaMemcpyDeviceToHost);
+            double mean = 0;
+            for (auto v : h) mean += v;
+            mean /= sms;
+            const double n_mma = double(iters) * 4 * (two ? 2 : 1);
+            const double cpm = mean / n_mma;
+            printf("%u,%u,%.1f,%.1f,%.0f\n", n, two + 1, cpm, n / 2.0, 2.0 * 128 * n * 16 / cpm);
+        }
+    return 0;
+}

@@ -12,7 +12,8 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from gpu_util import U32, bf16_ok, bf16_round, close_mask, make_layer, out_ok, routing_agreement, toy_setup
+from gpu_util import (U32, bf16_ok, bf16_round, close_mask, make_layer, out_ok, routing_agreement,
+                      torch_layer_reference, toy_setup)
 
 pytestmark = pytest.mark.gpu
 GOLD = Path(__file__).resolve().parent / "golden"
@@ -356,33 +357,6 @@ def test_tensor_core_router_logit_error(oracle, torch_cuda, mixtral):
     assert err.max() < 4e-6  # kRouterGuard (layer.cu): the certification bound must hold
 
 
-def _torch_layer_reference(torch, gen_expert, parts, S, d, xb, sel, w):
-    """Plain PyTorch fp32 reference of the bf16 layer over ALL tokens:
-    h = bf16(silu(x Wg_s) * (x Wu_s)), o = bf16(h Wd_s), y = sum_slots w * o,
-    weights bf16-rounded, fp32 matmuls (no TF32).  Covers every row of every
-    bucket, including the last (partial) GEMM tile of each sub-expert."""
-    torch.backends.cuda.matmul.allow_tf32 = False
-    T = xb.shape[0]
-    xt = torch.from_numpy(xb).cuda()
-    sel_t = torch.from_numpy(sel.astype(np.int64)).cuda()
-    w_t = torch.from_numpy(w).cuda()
-    y = torch.zeros((T, d), dtype=torch.float32, device="cuda")
-    for e, part in enumerate(parts):
-        wg, wu, wd = gen_expert(e)
-        for s in range(S):
-            idx = torch.from_numpy(np.nonzero(part == s)[0]).cuda()
-            hit = sel_t == e * S + s
-            tok = hit.any(dim=1).nonzero().squeeze(1)
-            if tok.numel() == 0:
-                continue
-            slot_w = (w_t * hit).sum(dim=1)[tok]
-            xa = xt[tok]
-            h = torch.nn.functional.silu(xa @ wg[:, idx]) * (xa @ wu[:, idx])
-            h = h.bfloat16().float()
-            o = (h @ wd[idx, :]).bfloat16().float()
-            y.index_add_(0, tok, o * slot_w[:, None])
-    return y.cpu().numpy()
-
 
 @pytest.mark.parametrize("k", [1, 2, 8, "mixed"])
 def test_mixtral_all_tokens_vs_torch(oracle, torch_cuda, k, mixtral):
@@ -412,6 +386,30 @@ def test_mixtral_all_tokens_vs_torch(oracle, torch_cuda, k, mixtral):
             out.append(t.bfloat16().float().view(*shape))
         return out
 
-    want = _torch_layer_reference(torch, gen, parts, S, d, xb, gsel, w.cpu().numpy())
+    want = torch_layer_reference(torch, gen, parts, S, d, xb, gsel, w.cpu().numpy())
     ok = bf16_ok(y.float().cpu().numpy(), want)
     assert ok.all(), f"{(~ok).sum()} elements off in {np.unique(np.nonzero(~ok)[0]).size} tokens"
+
+
+def test_fused_residual(oracle, torch_cuda):
+    """mp_layer_set_residual: forward returns x + MoE(x) (layer-stack step,
+    SURVEY 8(d) C3) with the residual as the combine's accumulator start."""
+    torch = torch_cuda
+    E, S, d, ff, T, K = 4, 4, 256, 512, 96, 4
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    L = make_layer(experts, parts, wr, S, "bf16", k_max=K, max_tokens=T)
+    xd = torch.from_numpy(bf16_round(x)).cuda().to(torch.bfloat16)
+    y0 = L.forward(xd, k=K).float()
+    L.set_residual(True)
+    y1 = L.forward(xd, k=K).float()
+    want = (xd.float() + y0).cpu().numpy()
+    assert bf16_ok(y1.cpu().numpy(), want).all()
+    assert not torch.equal(y1, y0)
+    L.set_residual(False)
+    assert torch.equal(L.forward(xd, k=K).float(), y0)
+    L.close()
+    Lf = make_layer(experts, parts, wr, S, "f32", k_max=K, max_tokens=T)
+    from paper_2510_19366_b200 import ValidationError
+    with pytest.raises(ValidationError, match="bf16"):
+        Lf.set_residual(True)
+    Lf.close()
