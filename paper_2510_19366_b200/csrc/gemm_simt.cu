@@ -68,9 +68,9 @@ __global__ void __launch_bounds__(256) gemm1_simt_kernel(const T* __restrict__ A
         for (uint32_t q = threadIdx.x; q < BN * BK; q += 256) {
             const uint32_t c = q / BK, kk = q % BK;
             const uint32_t cg = c0 + c;
-            const uint32_t rg = (cg / 128) * 256 + (cg % 128);
+            const uint32_t rg = (cg / kIlv) * 2 * kIlv + (cg % kIlv);
             Bg[kk][c] = to_f32(W1[(wbase + rg) * K + k0 + kk]);
-            Bu[kk][c] = to_f32(W1[(wbase + rg + 128) * K + k0 + kk]);
+            Bu[kk][c] = to_f32(W1[(wbase + rg + kIlv) * K + k0 + kk]);
         }
         __syncthreads();
 #pragma unroll

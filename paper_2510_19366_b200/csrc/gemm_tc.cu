@@ -1,11 +1,12 @@
 // gemm_tc.cu -- grouped GEMMs of the sub-expert SwiGLU FFN on the 5th-gen
 // tensor cores (tcgen05.mma, accumulators in TMEM, operands staged by TMA).
 //
-//   gemm1 (SWIGLU=true):  H[r][n*128 + c] = silu(acc[r][c]) * acc[r][128 + c]
+//   gemm1 (SWIGLU=true):  H[r][n*128 + h*64 + c] = silu(acc[r][h*128 + c]) * acc[r][h*128 + 64 + c]
 //       A = x_perm (rows x d_pad), B = W1[g] rows n*256 .. n*256+255
-//       (128 gate rows then the 128 up rows of the same neurons, packed by
-//       pack.cu), so one 128x256 TMEM accumulator holds both halves of the
-//       SwiGLU for 128 neurons and the activation is fused in the epilogue.
+//       (blocks of 64 gate rows then the 64 up rows of the same neurons,
+//       packed by pack.cu, kIlv), so one 128x256 TMEM accumulator holds both
+//       halves of the SwiGLU for 128 neurons and the activation is fused in
+//       the epilogue.
 //   gemm2 (SWIGLU=false): O[r][n*256 + c] = acc[r][c]
 //       A = H (rows x w_pad), B = W2[g] (d_pad x w_pad).
 // Variable-size groups: sub-expert g owns rows [offsets[g], offsets[g+1])
@@ -25,13 +26,12 @@
 // -- both operands stream from HBM/L2 and need >= 4 k-blocks of lookahead.
 // 2 TMEM accumulators of 256 columns (tmem_full / tmem_empty) let the
 // epilogue of tile i overlap the MMAs of tile i+1.
-// Swapped tails (opt-in, MOEPRISM_TC_SWAP=1): the last M tile of a group with
-// r < 128 rows computes D^T = W . X^T as two M=128, N=ceil16(r) MMAs per
-// k-step (gate / up halves of the B tile), so no MMA work is spent on rows of
-// the next group.  Parity-green, but measured SLOWER on B200 (k=8 gemm1
-// 0.98 -> 1.21 ms; MMA-issuer trace: operand waits unchanged, the MMA pipe
-// itself back-pressures): small-N tcgen05.mma has a per-instruction cost well
-// above the N/2-cycle floor, so two N~64 MMAs cost more than one N=256 MMA.
+// Measured and dropped (tests/probes, profiles/r01_mma_cost.csv): swapped
+// tail tiles (D^T = W . X^T with N = rows rounded to 16: slower, k=8 gemm1
+// 0.98 -> 1.21 ms), two N=128 MMAs per k-step (slower: A is read from smem
+// twice), two K-interleaved accumulator chains (MMA issue at the floor, but
+// the epilogue is exposed).  The limiter of this kernel is the operand feed
+// (48 KB of A+B per SM per k-block); gemm_tc2.cu (CTA pairs) halves B.
 #include <cstdio>
 #include <cstdlib>
 
@@ -53,13 +53,7 @@ constexpr uint32_t BM = kTcBM;  // 128
 constexpr uint32_t BN = 256;
 constexpr uint32_t BK = 64;  // one 128-byte swizzle row of bf16
 constexpr uint32_t NA = MP_TC_NA, NB = MP_TC_NB;
-#ifndef MP_TC_KCHAIN
-#define MP_TC_KCHAIN 0
-#endif
-// KCHAIN (experiment): two K-interleaved accumulator chains per tile (TMEM
-// holds one tile, no epilogue overlap) to hide the MMA dependency latency
-constexpr bool KCHAIN = MP_TC_KCHAIN != 0;
-constexpr uint32_t NACC = KCHAIN ? 1 : 2;
+
 constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr uint32_t B_BYTES = BN * BK * 2;
 constexpr uint32_t kThreads = 192;
@@ -68,7 +62,6 @@ constexpr size_t kSmemBytes = 1024 + NA * A_BYTES + NB * B_BYTES + 256;
 
 struct TcParams {
     uint32_t G, K, N_group, n_valid, ld_out, NT;
-    uint32_t swap_tail;  // last M tile of a group with < 128 rows runs swapped (below)
     const uint32_t* offsets;
     const uint32_t* mprefix;
     __nv_bfloat16* out;
@@ -209,13 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t t_start = p.trace ? clock64() : 0;
             uint64_t w_acc = 0, w_full = 0;
             for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
-                const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
-                uint32_t g, m, n;
-                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const uint32_t rows = s_off[g + 1] - s_off[g] - m * BM;
-                const bool swapped = !KCHAIN && p.swap_tail && rows < BM;
-                // swapped tail: D^T = W . X^T, M = 128 weight rows per half, N = rows rounded to 16
-                const uint32_t idesc_sw = umma_idesc_bf16(BM, (rows + 15u) & ~15u);
+                const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
                 uint64_t t0 = p.trace ? clock64() : 0;
                 mbar_wait(&tempty[acc], aph ^ 1u);
                 if (p.trace) w_acc += clock64() - t0;
@@ -231,25 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + sa * A_BYTES);
                     const uint32_t b0 = smem_u32(sB + sb * B_BYTES);
-                    if (!swapped) {
 #pragma unroll
-                        for (uint32_t k = 0; k < BK / 16; ++k) {
-                            if constexpr (KCHAIN)  // even / odd k-steps into two accumulators
-                                umma_bf16(d_tmem + (k & 1u) * BN, umma_desc_sw128(a0 + k * 32),
-                                          umma_desc_sw128(b0 + k * 32), idesc, (kb | (k >> 1)) != 0u);
-                            else
-                                umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                                          (kb | k) != 0u);
-                        }
-                    } else {
-#pragma unroll
-                        for (uint32_t k = 0; k < BK / 16; ++k) {
-                            umma_bf16(d_tmem, umma_desc_sw128(b0 + k * 32), umma_desc_sw128(a0 + k * 32), idesc_sw,
-                                      (kb | k) != 0u);
-                            umma_bf16(d_tmem + BN / 2, umma_desc_sw128(b0 + B_BYTES / 2 + k * 32),
-                                      umma_desc_sw128(a0 + k * 32), idesc_sw, (kb | k) != 0u);
-                        }
-                    }
+                    for (uint32_t k = 0; k < BK / 16; ++k)
+                        umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                                  (kb | k) != 0u);
                     umma_commit(&emptyA[sa]);
                     umma_commit(&emptyB[sb]);
                 }
@@ -270,48 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
             uint32_t g, m, n;
             map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-            const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
+            const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            const uint32_t rows = s_off[g + 1] - s_off[g] - m * BM;
-            if (!KCHAIN && p.swap_tail && rows < BM) {
-                // swapped tail: TMEM lane = weight row, column = token of the tile;
-                // half h (columns [128 h, 128 h + rows)) = weight rows 128 h + lane
-                const uint32_t i = q * 32 + lane;
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN;
-                __nv_bfloat16* obase = p.out + static_cast<size_t>(s_off[g] + m * BM) * p.ld_out;
-#pragma unroll 1
-                for (uint32_t c = 0; c < rows; c += 32) {
-                    uint32_t r0[32], r1[32];
-                    tmem_ld32(taddr + c, r0);
-                    tmem_ld32(taddr + BN / 2 + c, r1);
-                    tmem_ld_wait();
-                    const uint32_t nt = rows - c < 32u ? rows - c : 32u;
-                    if constexpr (SWIGLU) {
-                        __nv_bfloat16* dst = obase + static_cast<size_t>(c) * p.ld_out + n * 128 + i;
-#pragma unroll
-                        for (uint32_t t = 0; t < 32; ++t)
-                            if (t < nt)
-                                dst[static_cast<size_t>(t) * p.ld_out] = __float2bfloat16_rn(
-                                    silu_f32(__uint_as_float(r0[t])) * __uint_as_float(r1[t]));
-                    } else {
-                        const uint32_t col = n * BN + i;
-                        __nv_bfloat16* dst = obase + static_cast<size_t>(c) * p.ld_out + col;
-                        const bool v0 = col < p.n_valid, v1 = col + BN / 2 < p.n_valid;
-#pragma unroll
-                        for (uint32_t t = 0; t < 32; ++t)
-                            if (t < nt) {
-                                if (v0) dst[static_cast<size_t>(t) * p.ld_out] = __float2bfloat16_rn(__uint_as_float(r0[t]));
-                                if (v1)
-                                    dst[static_cast<size_t>(t) * p.ld_out + BN / 2] =
-                                        __float2bfloat16_rn(__uint_as_float(r1[t]));
-                            }
-                    }
-                }
-                tc_fence_before();
-                mbar_arrive(&tempty[acc]);
-                continue;
-            }
             const uint32_t row_local = m * BM + q * 32 + lane;
             const bool valid = row_local < s_off[g + 1] - s_off[g];
             __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
@@ -319,21 +252,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (SWIGLU) {
 #pragma unroll 1
                 for (uint32_t c = 0; c < 4; ++c) {
+                    // neurons n*128 + c*32 .. +31: gate columns (c/2)*128 + (c%2)*32, up + 64
+                    const uint32_t gcol = (c >> 1) * 128 + (c & 1u) * 32;
                     uint32_t gr[32], ur[32];
-                    tmem_ld32(taddr + c * 32, gr);
-                    tmem_ld32(taddr + 128 + c * 32, ur);
+                    tmem_ld32(taddr + gcol, gr);
+                    tmem_ld32(taddr + gcol + kIlv, ur);
                     tmem_ld_wait();
-                    if constexpr (KCHAIN) {
-                        uint32_t g2[32], u2[32];
-                        tmem_ld32(taddr + BN + c * 32, g2);
-                        tmem_ld32(taddr + BN + 128 + c * 32, u2);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            gr[i] = __float_as_uint(__uint_as_float(gr[i]) + __uint_as_float(g2[i]));
-                            ur[i] = __float_as_uint(__uint_as_float(ur[i]) + __uint_as_float(u2[i]));
-                        }
-                    }
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -354,13 +278,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t r[32];
                     tmem_ld32(taddr + c * 32, r);
                     tmem_ld_wait();
-                    if constexpr (KCHAIN) {
-                        uint32_t r2[32];
-                        tmem_ld32(taddr + BN + c * 32, r2);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) + __uint_as_float(r2[i]));
-                    }
                     const uint32_t col = n * BN + c * 32;
                     if (valid && col < p.n_valid) {
                         uint32_t pk[16];
@@ -448,12 +365,7 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.mprefix = mprefix;
     p.out = static_cast<__nv_bfloat16*>(out);
     p.trace = gemm_trace_buffer(swiglu);
-    // MOEPRISM_TC_SWAP=1: swapped tails (opt-in; measured slower, see header)
-    static const uint32_t swap_tail = [] {
-        const char* e = std::getenv("MOEPRISM_TC_SWAP");
-        return (e && e[0] == '1') ? 1u : 0u;
-    }();
-    p.swap_tail = swap_tail;
+
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;

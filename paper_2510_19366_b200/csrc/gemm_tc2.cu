@@ -12,13 +12,18 @@
 // -> SM traffic and shared-memory fill bandwidth for the same MMA work.
 //
 // Layout / semantics are gemm_tc.cu's (same packed weights, same epilogues):
-//   gemm1 (SWIGLU): B tile = W1 rows n*256 .. +255 (128 gate rows, then the
-//     128 up rows of the same neurons); CTA r loads rows n*256 + 128 r .. +127,
-//     so accumulator columns [0,128) are gate, [128,256) up, in both CTAs.
+//   gemm1 (SWIGLU): B tile = W1 rows n*256 .. +255 = [64 gate | 64 up] for
+//     neurons n*128 + 0..63, then the same for + 64..127; CTA r loads rows
+//     n*256 + 128 r .. +127 (accumulator columns [128 r, 128 r + 128)).
 //   gemm2: B tile = W2 rows n*256 .. +255 = output columns; CTA r loads its half.
 // Tiles are (g, n, m) with 256-row m tiles (prefix of ceil(count_g / 256)),
 // m fastest, strided over the clusters of a persistent grid.  Rows past the
-// group end are computed and discarded (masked stores).
+// group end are computed and discarded (masked stores).  A tile with at most
+// 128 valid rows (the tail of a group) issues M=128 pair MMAs instead: 64
+// rows per CTA at half the MMA time, the accumulator in the 2x2 layout (rows
+// in lanes 0-63 with D columns [0,128), the same rows in lanes 64-127 with D
+// columns [128,256)).  With the 64-row gate/up interleave of W1 (kIlv) both
+// halves of a neuron's SwiGLU stay in one lane in either shape.
 //
 // Barriers: full[s] lives in the leader CTA (both CTAs' TMA loads complete_tx
 // on it; the leader's expect_tx covers both); empty[s], tfull[a] are signalled
@@ -32,6 +37,9 @@
 #include "mp_common.cuh"
 #include "mp_kernels.h"
 
+#ifndef MP_PAIR_TRACE  // 1: MMA-issuer timing into the trace buffer (diagnostic builds only)
+#define MP_PAIR_TRACE 0
+#endif
 #ifndef MP_PAIR_STAGES
 #define MP_PAIR_STAGES 6
 #endif
@@ -57,6 +65,8 @@ struct PairParams {
     const uint32_t* offsets;
     const uint32_t* mprefix;  // prefix of ceil(count_g / 256)
     __nv_bfloat16* out;
+    uint64_t* trace;  // [grid][4] MMA-issuer timing of the leaders (diagnostics) or null
+    uint32_t tail128;  // tiles with <= 128 valid rows issue M=128 pair MMAs
 };
 
 MP_DEV uint32_t cluster_rank() {
@@ -200,7 +210,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (uint32_t tile = pair; tile < total; tile += npairs) {
                 uint32_t g, m, n;
                 map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * HM);
+                const bool tail = p.tail128 && s_off[g + 1] - s_off[g] - m * BM <= HM;  // M=128: 64 rows per CTA
+                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * (tail ? HM / 2 : HM));
                 const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN + rank * 128);
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
@@ -214,16 +225,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (rank == 0 && lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+            constexpr uint32_t idesc_full = umma_idesc_bf16(BM, BN);
+            constexpr uint32_t idesc_tail = umma_idesc_bf16(HM, BN);
             uint32_t it = 0, tc = 0;
+#if MP_PAIR_TRACE
+            const uint64_t t_start = clock64();
+            uint64_t w_acc = 0, w_full = 0;
+#endif
             for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
                 const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+                uint32_t g, m, n;
+                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+                const uint32_t idesc = (p.tail128 && s_off[g + 1] - s_off[g] - m * BM <= HM) ? idesc_tail : idesc_full;
+#if MP_PAIR_TRACE
+                uint64_t t0 = clock64();
+#endif
                 mbar_wait_cluster(&tempty[acc], aph ^ 1u);
+#if MP_PAIR_TRACE
+                w_acc += clock64() - t0;
+#endif
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
+#if MP_PAIR_TRACE
+                    t0 = clock64();
+#endif
                     mbar_wait(&full[s], ph);
+#if MP_PAIR_TRACE
+                    w_full += clock64() - t0;
+#endif
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + s * A_BYTES);
                     const uint32_t b0 = smem_u32(sB + s * B_BYTES);
@@ -235,6 +266,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 umma_commit_pair(&tfull[acc]);
             }
+#if MP_PAIR_TRACE
+            if (p.trace) {
+                uint64_t* tr = p.trace + blockIdx.x * 4;
+                tr[0] = clock64() - t_start;
+                tr[1] = w_acc;
+                tr[2] = w_full;
+                tr[3] = tc;
+            }
+#endif
         }
         __syncwarp();
     } else {
@@ -247,19 +287,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            const uint32_t row_local = m * BM + rank * HM + q * 32 + lane;
             const uint32_t cnt = s_off[g + 1] - s_off[g];
+            const bool tail = p.tail128 && cnt - m * BM <= HM;
+            // full tile: lane = row rank*128 + q*32 + lane, all 256 D columns;
+            // tail tile: lane l < 64 = row rank*64 + l with D columns [0,128),
+            //            lane 64 + l = the same row with D columns [128,256)
+            const uint32_t row_local =
+                m * BM + (tail ? rank * 64 + (q & 1u) * 32 + lane : rank * HM + q * 32 + lane);
+            const uint32_t half = tail ? (q >> 1) : 0;  // which 128 D columns this lane holds (tail)
+            const uint32_t nchunk = tail ? 4 : 8;        // 32-column chunks of D held by the lane
             const bool valid = row_local < cnt;
-            const bool any = m * BM + rank * HM + q * 32 < cnt;  // warp has a valid row
+            const bool any = (row_local - lane) < cnt;  // warp has a valid row
             __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
             const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN;
             if (any) {
                 if constexpr (SWIGLU) {
+                    // D chunk pair (gate, up) = columns (h*128 + c2*32, + 64) for
+                    // neurons n*128 + h*64 + c2*32 .. +31
 #pragma unroll 1
-                    for (uint32_t c = 0; c < 4; ++c) {
+                    for (uint32_t c = 0; c < nchunk / 2; ++c) {
+                        const uint32_t h = tail ? half : (c >> 1), c2 = c & 1u;
+                        const uint32_t tcol = (tail ? 0 : h * 128) + c2 * 32;
                         uint32_t gr[32], ur[32];
-                        tmem_ld32(taddr + c * 32, gr);
-                        tmem_ld32(taddr + 128 + c * 32, ur);
+                        tmem_ld32(taddr + tcol, gr);
+                        tmem_ld32(taddr + tcol + kIlv, ur);
                         tmem_ld_wait();
                         uint32_t pk[16];
 #pragma unroll
@@ -269,7 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             pk[i] = pack_bf16x2(silu_f32(g0) * u0, silu_f32(g1) * u1);
                         }
                         if (valid) {
-                            __nv_bfloat16* dst = orow + n * 128 + c * 32;
+                            __nv_bfloat16* dst = orow + n * 128 + h * 64 + c2 * 32;
 #pragma unroll
                             for (int v = 0; v < 4; ++v)
                                 st_global_v4(dst + v * 8,
@@ -278,11 +329,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 } else {
 #pragma unroll 1
-                    for (uint32_t c = 0; c < BN / 32; ++c) {
+                    for (uint32_t c = 0; c < nchunk; ++c) {
                         uint32_t r[32];
                         tmem_ld32(taddr + c * 32, r);
                         tmem_ld_wait();
-                        const uint32_t col = n * BN + c * 32;
+                        const uint32_t col = n * BN + half * 128 + c * 32;
                         if (valid && col < p.n_valid) {
                             uint32_t pk[16];
 #pragma unroll
@@ -317,9 +368,10 @@ size_t gemm_pair_smem_bytes() { return kSmemBytes; }
 
 // tmB: box of 128 rows (each CTA loads half of the 256-row B tile)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s) {
+                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s, bool tail128) {
     PairParams p{sh.G, sh.K, sh.N_group, sh.n_valid, sh.ld_out, (sh.N_group + BN - 1) / BN, offsets, mprefix256,
-                 static_cast<__nv_bfloat16*>(out)};
+                 static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), tail128 ? 1u : 0u};
+    if (p.trace) cudaMemsetAsync(p.trace, 0, 1024 * 4 * sizeof(uint64_t), s);
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;
     if (max_tiles < pairs) pairs = max_tiles;

@@ -325,7 +325,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     // (Mixtral shape: pairs win at k >= 4, lose at k = 2).  Per-token k: k_max.
     {
         const double rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
-        L->tile256 = L->tile_mode == 2 || (L->tile_mode == 0 && rows >= 192.0);
+        L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && rows >= 192.0);
     }
     tm.begin(1);
     mp::launch_bucket_local(sel, T, L->k_max, L->G, L->ws, s);
@@ -340,7 +340,8 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
     if (L->use_tc && L->tile256)
-        mp::launch_gemm_tc2(true, &L->tm_xperm, &L->tm_w1h, L->h, g1, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s);
+        mp::launch_gemm_tc2(true, &L->tm_xperm, &L->tm_w1h, L->h, g1, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s,
+                            L->tile_mode != 3);
     else if (L->use_tc)
         mp::launch_gemm_tc(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
     else
@@ -361,7 +362,8 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     tm.end(3, shared ? 2 : 1);
     tm.begin(4);
     if (L->use_tc && L->tile256)
-        mp::launch_gemm_tc2(false, &L->tm_h, &L->tm_w2h, L->o, g2, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s);
+        mp::launch_gemm_tc2(false, &L->tm_h, &L->tm_w2h, L->o, g2, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s,
+                            false);  // M=128 tail MMAs measured 2-8% slower in gemm2 (profiles/r01_tile_ab.txt)
     else if (L->use_tc)
         mp::launch_gemm_tc(false, &L->tm_h, &L->tm_w2, L->o, g2, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
     else
@@ -370,7 +372,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     if (shared) {
         mp::GemmShape s2{1, L->sh_w_pad, L->d_pad, T, L->d_pad, L->d_pad};
         if (sh_pair)
-            mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, s);
+            mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, s, false);
         else
             mp::launch_gemm_tc(false, &L->tm_hs, &L->tm_w2s, L->sh_o, s2, L->sh_meta, L->sh_meta + 2, L->num_sms, s);
         ck_launch("shared gemm2");
@@ -1116,10 +1118,11 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
 
 // Diagnostics (not in the public header): grouped-GEMM kernel choice of a
 // layer at run time, 0 auto / 1 one-SM 128-row tiles / 2 CTA-pair 256-row
-// tiles, for in-process A/B timing (tests/probes/tile_ab.py).
+// tiles / 3 CTA pairs without the M=128 tail MMA, for in-process A/B timing
+// (tests/probes/tile_ab.py).
 MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {
-        if (!L || mode < 0 || mode > 2) fail(MP_ERR_VALIDATION, "bad argument");
+        if (!L || mode < 0 || mode > 3) fail(MP_ERR_VALIDATION, "bad argument");
         L->tile_mode = mode;
     });
 }

@@ -12,6 +12,11 @@ constexpr uint32_t kRouteTokensPerBlock = 32;  // tokens per router / bucket CTA
 constexpr uint32_t kTcBM = 128;                // tcgen05 grouped GEMM tile M
 constexpr uint32_t kSimtBM = 64;               // SIMT grouped GEMM tile M
 constexpr uint32_t kMaxG = 256;                // max E*S sub-experts (Qwen: 240)
+// W1 gate/up interleave: rows in blocks of 2*kIlv = kIlv gate rows then the
+// kIlv up rows of the same neurons (pack.cu).  64 puts gate and up of a
+// neuron in the same TMEM lane for both the 256-row and the 128-row (tail)
+// CTA-pair MMA shapes (gemm_tc2.cu).
+constexpr uint32_t kIlv = 64;
 
 // Device scratch for the bucketing of one forward.
 struct BucketWs {
@@ -105,7 +110,8 @@ uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s);
+                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
+                     bool tail128 = true);
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point.
 bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,

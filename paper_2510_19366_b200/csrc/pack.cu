@@ -6,8 +6,8 @@
 // (inc/expert.hpp:14-16), so a sub-expert is a set of neurons.  The packer
 // gathers each sub-expert's members (ascending, subexpert_members
 // inc/partition.hpp:49-55) into contiguous K-major blocks:
-//   W1[g] : (2*w_pad) x d_pad, rows in blocks of 256 = 128 gate rows then the
-//           128 up rows of the same neurons (fused SwiGLU epilogue),
+//   W1[g] : (2*w_pad) x d_pad, rows in blocks of 128 = 64 gate rows then the
+//           64 up rows of the same neurons (kIlv; fused SwiGLU epilogue),
 //   W2[g] : d_pad x w_pad (K = neurons contiguous),
 // zero padded: a zero neuron contributes SiLU(0)*0*W_down = 0 exactly.
 #include "mp_common.cuh"
@@ -32,10 +32,10 @@ __global__ void pack_w1_kernel(const float* __restrict__ wg, const float* __rest
         const uint32_t i = i0 + q, r = r0 + tx;
         float v = 0.0f;
         if (i < d && r < rows) {
-            const uint32_t blk = r / 256, within = r % 256;
-            const uint32_t c = blk * 128 + (within % 128);
+            const uint32_t blk = r / (2 * kIlv), within = r % (2 * kIlv);
+            const uint32_t c = blk * kIlv + (within % kIlv);
             const int32_t j = nmap[(size_t)s * w_pad + c];
-            if (j >= 0) v = (within < 128 ? wg : wu)[(size_t)i * ff + j];
+            if (j >= 0) v = (within < kIlv ? wg : wu)[(size_t)i * ff + j];
         }
         tile[tx][q] = v;
     }

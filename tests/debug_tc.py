@@ -59,7 +59,7 @@ def run(E, S, d, ff, T, k, seed=0):
         if r1 == r0:
             continue
         acc = Xp[r0:r1] @ W1[g].T  # rows x 2w_pad
-        acc = acc.view(r1 - r0, w_pad // 128, 2, 128)
+        acc = acc.view(r1 - r0, w_pad // 64, 2, 64)  # kIlv = 64 gate/up interleave
         gate, up = acc[:, :, 0, :].reshape(r1 - r0, w_pad), acc[:, :, 1, :].reshape(r1 - r0, w_pad)
         href = (torch.nn.functional.silu(gate) * up)
         eh = ((H[r0:r1] - href).abs() / (1 + href.abs()))

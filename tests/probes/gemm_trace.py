@@ -7,13 +7,14 @@ from paper_2510_19366_b200 import _lib
 L, xs = bench.build_layer(0, 4096, 16)
 lib = _lib.load()
 lib.mp_debug_gemm_trace.argtypes = [C.c_int, C.c_void_p, C.c_uint32]
-for k in (2, 8, 16):
+for k in [int(a) for a in (sys.argv[1] if len(sys.argv) > 1 else "2,8,16").split(",")]:
     for i in range(3):
         L.forward(xs[i], k=k)
     torch.cuda.synchronize()
     for which, name in ((0, 'gemm1'), (1, 'gemm2')):
         tr = np.zeros((148, 4), np.uint64)
         _lib.check(lib.mp_debug_gemm_trace(which, tr.ctypes.data, 148))
+        tr = tr[tr[:, 0] > 0]  # CTA-pair kernel: leaders only
         tot, wacc, wfull, tiles = (tr[:, i].astype(np.float64) for i in range(4))
         print(f"k={k} {name}: cycles max {tot.max():.0f} mean {tot.mean():.0f} | wait accumulator {100*wacc.sum()/tot.sum():.1f}% "
               f"| wait smem stage {100*wfull.sum()/tot.sum():.1f}% | tiles/CTA {tiles.min():.0f}-{tiles.max():.0f} "

@@ -55,6 +55,66 @@ __global__ void __launch_bounds__(128, 1) mma_cost_kernel(uint32_t n, uint32_t t
     }
 }
 
+// CTA-pair variant: cta_group::2, M in {128, 256}, N = 256, one accumulator chain
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    mma_cost_pair_kernel(uint32_t m, uint32_t two, uint32_t iters, uint64_t* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = base;
+    uint8_t* sB = base + 16384;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_slot;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    for (uint32_t i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(base)[i] = 0x3f803f80u;
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (threadIdx.x == 0 && rank == 0) {
+        const uint32_t idesc = umma_idesc_bf16(m, 256);
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+        uint64_t t0 = clock64();
+        for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k) {
+                const uint32_t d = tmem + ((two && (k & 1)) ? 256 : 0);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                    "l"(umma_desc_sw128(a0 + k * 32)), "l"(umma_desc_sw128(b0 + k * 32)), "r"(idesc), "r"(1u)
+                    : "memory");
+            }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(&bar)),
+            "h"(static_cast<uint16_t>(1))
+            : "memory");
+        mbar_wait(&bar, 0);
+        out[blockIdx.x] = clock64() - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (threadIdx.x < 32) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -66,6 +126,7 @@ int main() {
     printf("N,accumulators,cycles_per_mma,floor_N_over_2,flop_per_cycle_per_sm\n");
     for (uint32_t two = 0; two < 2; ++two)
         for (uint32_t n : {16u, 32u, 48u, 64u, 96u, 128u, 160u, 192u, 256u}) {
+            if (two && n > 128) continue;  // second B operand at smem row 128 (256-row buffer)
             mma_cost_kernel<<<sms, 128, smem>>>(n, two, iters, d_out);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) {
@@ -80,6 +141,26 @@ int main() {
             const double n_mma = double(iters) * 4 * (two ? 2 : 1);
             const double cpm = mean / n_mma;
             printf("%u,%u,%.1f,%.1f,%.0f\n", n, two + 1, cpm, n / 2.0, 2.0 * 128 * n * 16 / cpm);
+        }
+    cudaFuncSetAttribute(mma_cost_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    printf("pair: M,accumulators,cycles_per_mma (N=256),floor\n");
+    for (uint32_t two = 0; two < 2; ++two)
+        for (uint32_t m : {128u, 256u}) {
+            cudaMemset(d_out, 0, sms * 8);
+            mma_cost_pair_kernel<<<sms, 128, smem>>>(m, two, iters, d_out);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) {
+                printf("error %s\n", cudaGetErrorString(e));
+                return 1;
+            }
+            std::vector<uint64_t> h(sms);
+            cudaMemcpy(h.data(), d_out, sms * 8, cudaMemcpyDeviceToHost);
+            double mean = 0;
+            int n = 0;
+            for (auto v : h)
+                if (v) mean += v, ++n;
+            mean /= n;
+            printf("%u,%u,%.1f,%.1f\n", m, two + 1, mean / (double(iters) * 4), m * 256.0 / 512);
         }
     return 0;
 }
