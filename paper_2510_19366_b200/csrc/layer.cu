@@ -131,6 +131,8 @@ struct mp_layer_s {
     void* wr_planes = nullptr;
     double* r_partial = nullptr;
     uint32_t* r_flagged = nullptr;  // [1 + max_tokens]: count, then tokens re-selected in fp64
+    uint32_t* r_ticket = nullptr;   // last-CTA ticket of the fused routing epilogue (left 0)
+    double r_guard = kRouterGuard;  // MOEPRISM_ROUTER_GUARD overrides (tests widen it)
     CUtensorMap tm_wplanes{};
     int32_t* d_nmap = nullptr;
 
@@ -176,7 +178,7 @@ namespace {
 void free_layer(mp_layer_s* L) {
     for (float* p : L->raw)
         if (p) cudaFree(p);
-    void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_flagged, L->d_nmap, L->sel,
+    void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_flagged, L->r_ticket, L->d_nmap, L->sel,
                     L->wsel, L->kpt_dev, L->ws.lrank, L->ws.block_counts, L->ws.block_base, L->ws.offsets,
                     L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.mprefix_tc2, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
                     L->x_perm, L->h, L->o, L->x_stage, L->y_stage, L->W1s, L->W2s, L->sh_gate, L->sh_h,
@@ -319,7 +321,7 @@ void resolve_timings(mp_layer_s* L) {
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
                  cudaStream_t s, StageTimer& tm, bool check_finite = false, bool with_shared = false,
-                 uint32_t kscalar = 0) {
+                 uint32_t kscalar = 0, bool bucketed = false) {
     // CTA-pair tiles pay up to 255 wasted rows per (sub-expert, N tile) against
     // 127 for 128-row tiles; measured break-even near 192 rows per bucket
     // (Mixtral shape: pairs win at k >= 4, lose at k = 2).  Per-token k: k_max.
@@ -327,11 +329,13 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         const double rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
         L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && rows >= 192.0);
     }
-    tm.begin(1);
-    mp::launch_bucket_local(sel, T, L->k_max, L->G, L->ws, s);
-    mp::launch_bucket_scan(T, L->G, L->ws, s);
-    ck_launch("bucket");
-    tm.end(1, 2);
+    if (!bucketed) {
+        tm.begin(1);
+        mp::launch_bucket_local(sel, T, L->k_max, L->G, L->ws, s);
+        mp::launch_bucket_scan(T, L->G, L->ws, s);
+        ck_launch("bucket");
+        tm.end(1, 2);
+    }
     tm.begin(2);
     mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, L->x_perm, s, true);
     ck_launch("dispatch");
@@ -387,8 +391,11 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     tm.end(5, 1);
 }
 
-void route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32_t k, cudaStream_t s,
-           StageTimer& tm, bool with_shared = false) {
+// Returns true when the bucketing of this forward already ran (fused into the
+// tensor-core router's epilogue; requested by fuse_bucket).
+bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32_t k, cudaStream_t s,
+           StageTimer& tm, bool with_shared = false, bool fuse_bucket = false) {
+    bool bucketed = false;
     if (!kpt && (k < 1 || k > L->k_max || k > L->G))
         fail(MP_ERR_VALIDATION, "k_active = " + std::to_string(k) + " out of range [1, " +
                                     std::to_string(std::min(L->k_max, L->G)) + "]");
@@ -417,12 +424,22 @@ void route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             L->r_last_ks = pl.ks;
             L->r_last_T = T;
             ck(cudaMemsetAsync(L->r_flagged, 0, sizeof(uint32_t), s), "memset flagged");
-            mp::launch_partials_topk(L->r_partial, pl.ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
-                                     L->sel, L->wsel, L->ws.err, kRouterGuard, L->r_flagged, s);
-            mp::launch_router_fixup(L->dtype, x, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode, L->sel,
-                                    L->wsel, L->ws.err, L->r_flagged, L->num_sms, s);
-            ck_launch("router(tc)");
-            tm.end(0, 3);
+            if (fuse_bucket && L->has_experts && (L->d % 4) == 0) {
+                // routing epilogue + exact near-tie re-selection + bucketing in one kernel
+                mp::launch_route_bucket(L->r_partial, pl.ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
+                                        L->sel, L->wsel, L->r_guard, x, L->d, L->wrT, L->r_ticket, L->r_flagged,
+                                        L->ws, s);
+                bucketed = true;
+                ck_launch("router(tc)+bucket");
+                tm.end(0, 2);
+            } else {
+                mp::launch_partials_topk(L->r_partial, pl.ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
+                                         L->sel, L->wsel, L->ws.err, L->r_guard, L->r_flagged, s);
+                mp::launch_router_fixup(L->dtype, x, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode,
+                                        L->sel, L->wsel, L->ws.err, L->r_flagged, L->num_sms, s);
+                ck_launch("router(tc)");
+                tm.end(0, 3);
+            }
         } else {
             mp::launch_router_linear(L->dtype, x, T, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode,
                                      L->sel, L->wsel, L->ws.err, s);
@@ -430,6 +447,7 @@ void route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             tm.end(0, 1);
         }
     }
+    return bucketed;
 }
 
 void copy_outputs(mp_layer_s* L, uint32_t T, uint32_t* sel_out, float* w_out, uint32_t* off_out, cudaStream_t s,
@@ -548,6 +566,9 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                     L->wr_planes = dalloc<char>((size_t)3 * L->r_npad * L->d * 2, "router planes");
                     L->r_partial = dalloc<double>((size_t)n_chunks * L->max_tokens * L->r_npad, "router partials");
                     L->r_flagged = dalloc<uint32_t>((size_t)L->max_tokens + 1, "router flagged");
+                    L->r_ticket = dalloc<uint32_t>(1, "router ticket");
+                    ck(cudaMemset(L->r_ticket, 0, sizeof(uint32_t)), "memset ticket");
+                    if (const char* env = std::getenv("MOEPRISM_ROUTER_GUARD")) L->r_guard = std::atof(env);
                     if (!mp::make_tmap_bf16_2d(&L->tm_wplanes, L->wr_planes, 3ull * L->r_npad, L->d, L->r_npad, 64))
                         fail(MP_ERR_CUDA, "router planes tensor map");
                 }
@@ -837,9 +858,9 @@ MP_API mp_status mp_layer_forward(mp_layer_t L, const void* x, uint32_t T, const
         DeviceGuard dg(L->desc.device);
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         StageTimer tm(L, s);
-        route(L, x, T, kpt, k, s, tm, true);
+        const bool bucketed = route(L, x, T, kpt, k, s, tm, true, true);
         run_experts(L, x, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, y, s, tm, false, true,
-                    kpt ? 0 : k);
+                    kpt ? 0 : k, bucketed);
         copy_outputs(L, T, sel_out, w_out, offsets_out, s, cudaMemcpyDeviceToDevice);
         static const int order[] = {0, 1, 2, 3, 4, 5};
         tm.finish(order, 6);
@@ -869,9 +890,9 @@ MP_API mp_status mp_layer_forward_host(mp_layer_t L, const void* x, uint32_t T, 
             kd = L->kpt_dev;
         }
         StageTimer tm(L, s);
-        route(L, L->x_stage, T, kd, k, s, tm, true);
+        const bool bucketed = route(L, L->x_stage, T, kd, k, s, tm, true, true);
         run_experts(L, L->x_stage, T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, L->y_stage, s, tm, true,
-                    true, kpt ? 0 : k);
+                    true, kpt ? 0 : k, bucketed);
         ck(cudaMemcpyAsync(y, L->y_stage, xbytes, cudaMemcpyDeviceToHost, s), "y download");
         copy_outputs(L, T, sel_out, w_out, offsets_out, s, cudaMemcpyDeviceToHost);
         int flags = 0;

@@ -76,6 +76,15 @@ void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const Rout
 void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                           const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
                           double guard, uint32_t* flagged, cudaStream_t s);
+// Fused routing epilogue of the tensor-core router (bf16 x, d % 4 == 0):
+// partials -> top-k -> exact re-selection of near-tie tokens (count added to
+// *n_fixed) -> bucket ranks -> device-wide scans (last CTA; *ticket must be
+// 0 on entry and is left 0).  Replaces partials_topk + router_fixup +
+// bucket_local + bucket_scan.
+void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
+                         const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, double guard,
+                         const void* x, uint32_t d, const float* wrT, uint32_t* ticket, uint32_t* n_fixed,
+                         BucketWs& ws, cudaStream_t s);
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
                          const uint32_t* flagged, int num_sms, cudaStream_t s);

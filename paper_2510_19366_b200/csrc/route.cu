@@ -29,17 +29,22 @@ constexpr uint32_t kRouterThreads = 256;
 // (inc/gating.hpp:143) with their softmax-renormalised weights.
 // Returns (to every lane) the gap between the k-th and (k+1)-th best score
 // (+inf when k == G): the near-tie measure of the routing contract.
+// keys (nullable): selection keys replacing sc for the ranking only (the
+// exact re-selection of near-tie tokens); the weights always use sc.
+// vk_out (nullable): the k-th and (k+1)-th best keys.
 __device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uint32_t k, uint32_t k_max,
-                                  int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row) {
+                                  int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row,
+                                  const double* __restrict__ keys = nullptr, double* vk_out = nullptr) {
     const uint32_t lane = lane_id();
     constexpr int NC = kMaxG / 32;
     const uint32_t nc = (G + 31) / 32;
     double v[NC];
     uint32_t taken = 0;  // bit c: value c of this lane selected
+    const double* kv = keys ? keys : sc;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         const uint32_t g = lane + 32u * c;
-        v[c] = (c < (int)nc && g < G) ? sc[g] : -DBL_MAX;
+        v[c] = (c < (int)nc && g < G) ? kv[g] : -DBL_MAX;
     }
     double vmax = 0.0, vk = 0.0, vk1 = -INFINITY;
     const uint32_t rounds = k < G ? k + 1 : k;
@@ -70,6 +75,24 @@ __device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uin
         }
         vk = bv;
         if (bi != 0xFFFFFFFFu && (bi & 31u) == lane) taken |= 1u << (bi >> 5);
+    }
+    if (vk_out && lane == 0) {
+        vk_out[0] = vk;
+        vk_out[1] = vk1;
+    }
+    if (keys) {  // weights from the logits, max over the selection (contains the top-1)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const uint32_t g = lane + 32u * c;
+            v[c] = (c < (int)nc && g < G) ? sc[g] : -DBL_MAX;
+        }
+        double m = -DBL_MAX;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if ((taken >> c) & 1u) m = fmax(m, v[c]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+        vmax = m;
     }
     // softmax over all G cancels in the renormalisation: w_g = e^(l_g - m) / sum_sel
     double z = 0.0;
@@ -374,13 +397,10 @@ __device__ uint32_t block_exclusive_scan_1024(uint32_t v, uint32_t* total, uint3
     return r;
 }
 
-__global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32_t G,
-                                                           const uint32_t* __restrict__ block_counts,
-                                                           uint32_t* __restrict__ block_base,
-                                                           uint32_t* __restrict__ offsets,
-                                                           uint32_t* __restrict__ mprefix_tc,
-                                                           uint32_t* __restrict__ mprefix_simt,
-                                                           uint32_t* __restrict__ mprefix_tc2) {
+__device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __restrict__ block_counts,
+                                 uint32_t* __restrict__ block_base, uint32_t* __restrict__ offsets,
+                                 uint32_t* __restrict__ mprefix_tc, uint32_t* __restrict__ mprefix_simt,
+                                 uint32_t* __restrict__ mprefix_tc2) {
     // thread (g, q): bucket g, q-th contiguous range of CTA-blocks; consecutive
     // threads read consecutive buckets of one block row (coalesced)
     __shared__ uint32_t part[1024];
@@ -437,6 +457,135 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32
             running += v;
         }
     }
+}
+
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32_t G,
+                                                           const uint32_t* __restrict__ block_counts,
+                                                           uint32_t* __restrict__ block_base,
+                                                           uint32_t* __restrict__ offsets,
+                                                           uint32_t* __restrict__ mprefix_tc,
+                                                           uint32_t* __restrict__ mprefix_simt,
+                                                           uint32_t* __restrict__ mprefix_tc2) {
+    bucket_scan_body(nblk, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt, mprefix_tc2);
+}
+
+// Exact fp64 logit x_t . W_r[:, g] by one warp: bf16 x and fp32 W_r are exact
+// in double, 4 fixed accumulators per lane + a fixed shuffle tree
+// (deterministic).  d % 4 == 0.
+__device__ double warp_exact_logit(const __nv_bfloat16* __restrict__ xr, const float* __restrict__ wrow, uint32_t d) {
+    const uint32_t lane = lane_id();
+    double acc[4] = {0, 0, 0, 0};
+    for (uint32_t i = 4 * lane; i < d; i += 128) {
+        const float4 wv = __ldg(reinterpret_cast<const float4*>(wrow + i));
+        const uint2 xv = __ldg(reinterpret_cast<const uint2*>(xr + i));
+        const float2 x01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
+        const float2 x23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
+        acc[0] = fma((double)x01.x, (double)wv.x, acc[0]);
+        acc[1] = fma((double)x01.y, (double)wv.y, acc[1]);
+        acc[2] = fma((double)x23.x, (double)wv.z, acc[2]);
+        acc[3] = fma((double)x23.y, (double)wv.w, acc[3]);
+    }
+    double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    return a;
+}
+
+// Device-wide exclusive scans of the bucketing, run by one CTA of 1024
+// threads (bucket_scan_kernel, or the last CTA of route_bucket_kernel).
+__device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __restrict__ block_counts,
+                                 uint32_t* __restrict__ block_base, uint32_t* __restrict__ offsets,
+                                 uint32_t* __restrict__ mprefix_tc, uint32_t* __restrict__ mprefix_simt,
+                                 uint32_t* __restrict__ mprefix_tc2);
+
+// Fused routing epilogue of the tensor-core router, CTA = 32 tokens (warp per
+// token), replacing partials_topk + router_fixup + bucket_local + bucket_scan:
+//   1. logits = fixed-order fp64 sum of the K-split partials, top-k, weights;
+//   2. near-tie certification: with a, b the k-th / (k+1)-th logits and
+//      |logit - exact| < guard, a gap a - b < 2 guard leaves only the window
+//      W = {g : b - 2 guard <= logit_g <= a + 2 guard} uncertain (above W:
+//      certainly selected, below: certainly not); W is recomputed in exact
+//      fp64 and the token re-selected on (+inf above W, exact in W, -inf
+//      below) -- the same selection the exact logits give;
+//   3. per-CTA bucket ranks / histogram (bucket_local_kernel's scheme);
+//   4. the last CTA to finish (threadfence + atomic ticket) runs the
+//      device-wide scans, then resets the ticket.
+__global__ void __launch_bounds__(1024) route_bucket_kernel(
+    const double* __restrict__ partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
+    const uint32_t* __restrict__ kpt, uint32_t k_scalar, int weight_mode, uint32_t* __restrict__ sel,
+    float* __restrict__ wout, int* __restrict__ err, double guard, const __nv_bfloat16* __restrict__ x, uint32_t d,
+    const float* __restrict__ wrT, uint32_t* __restrict__ ticket, uint32_t* __restrict__ n_fixed, uint32_t* lrank,
+    uint32_t* block_counts, uint32_t* block_base, uint32_t* offsets, uint32_t* mprefix_tc, uint32_t* mprefix_simt,
+    uint32_t* mprefix_tc2) {
+    extern __shared__ double rsm[];  // [TB][G] logits, then [TB][G] keys
+    double* sc = rsm + (size_t)(threadIdx.x / 32) * G;
+    double* key = rsm + (size_t)(TB + threadIdx.x / 32) * G;
+    __shared__ double vk[TB][2];
+    __shared__ uint32_t msk[TB][kMaxG / 32];
+    __shared__ uint16_t slot_of[TB][kMaxG];
+    __shared__ uint32_t is_last;
+    const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t t0 = blockIdx.x * TB, t = t0 + warp;
+    const uint32_t words = (G + 31) / 32;
+    for (uint32_t q = threadIdx.x; q < TB * words; q += blockDim.x) msk[q / words][q % words] = 0;
+    if (t < T) {
+        for (uint32_t g = lane; g < G; g += 32) {
+            double v = 0.0;
+            for (uint32_t s = 0; s < ks; ++s) v += partial[((size_t)s * T + t) * Npad + g];
+            sc[g] = v;
+        }
+        __syncwarp();
+        const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
+        const double gap = warp_topk_token(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
+                                           wout + (size_t)t * k_max, nullptr, vk[warp]);
+        __syncwarp();
+        if (gap < 2.0 * guard) {
+            const double a = vk[warp][0], b = vk[warp][1];
+            for (uint32_t g0 = 0; g0 < G; g0 += 32) {
+                const uint32_t g = g0 + lane;
+                const double v = g < G ? sc[g] : -DBL_MAX;
+                const bool in_w = g < G && v >= b - 2.0 * guard && v <= a + 2.0 * guard;
+                if (g < G) key[g] = v > a + 2.0 * guard ? DBL_MAX : (in_w ? v : -DBL_MAX);
+                uint32_t bal = __ballot_sync(0xffffffffu, in_w);
+                while (bal) {
+                    const uint32_t j = __ffs(bal) - 1;
+                    bal &= bal - 1;
+                    const double e = warp_exact_logit(x + (size_t)t * d, wrT + (size_t)(g0 + j) * d, d);
+                    if (lane == j) {
+                        key[g] = e;
+                        sc[g] = e;
+                    }
+                }
+            }
+            __syncwarp();
+            warp_topk_token(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max, key);
+            if (lane == 0) atomicAdd(n_fixed, 1u);
+        }
+    }
+    __syncthreads();  // this CTA's selections are visible to the CTA
+    for (uint32_t q = threadIdx.x; q < TB * k_max; q += blockDim.x) {
+        const uint32_t tt = q / k_max, j = q % k_max;
+        if (t0 + tt >= T) continue;
+        const uint32_t g = sel[(size_t)(t0 + tt) * k_max + j];
+        if (g == kSelNone || g >= G) continue;
+        atomicOr(&msk[tt][g >> 5], 1u << (g & 31));
+        slot_of[tt][g] = static_cast<uint16_t>(j);
+    }
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) {
+        uint32_t cnt = 0;
+        for (uint32_t tt = 0; tt < TB && t0 + tt < T; ++tt)
+            if ((msk[tt][g >> 5] >> (g & 31)) & 1u) lrank[(size_t)(t0 + tt) * k_max + slot_of[tt][g]] = cnt++;
+        block_counts[(size_t)blockIdx.x * G + g] = cnt;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    bucket_scan_body(gridDim.x, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt, mprefix_tc2);
+    if (threadIdx.x == 0) *ticket = 0;  // ready for the next forward (stream-ordered)
 }
 
 // ---------------------------------------------------------------- dispatch
@@ -645,6 +794,23 @@ void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32
                           double guard, uint32_t* flagged, cudaStream_t s) {
     partials_topk_kernel<<<(T + 7) / 8, 256, 0, s>>>(partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w,
                                                      err, guard, flagged);
+}
+
+void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
+                         const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, double guard,
+                         const void* x, uint32_t d, const float* wrT, uint32_t* ticket, uint32_t* n_fixed,
+                         BucketWs& ws, cudaStream_t s) {
+    const size_t smem = sizeof(double) * 2 * TB * G;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(route_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * 2 * TB * kMaxG));
+        attr = true;
+    }
+    route_bucket_kernel<<<(T + TB - 1) / TB, 1024, smem, s>>>(
+        partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, guard,
+        static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, n_fixed, ws.lrank, ws.block_counts, ws.block_base,
+        ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2);
 }
 
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
