@@ -370,6 +370,33 @@ def bench_mixed_qos_32k(L32, pk, steps=10):
             "mean_k": kk, "tokens_per_s": T / (ms * 1e-3), "ms_per_step": ms, "roofline": roofline_fb(F, B, ms, pk)}
 
 
+def bench_calibration(pk, B=4096, k_a=1434, steps=5):
+    """SURVEY 8(f).2 on the GPU at the Mixtral expert shape: the activation
+    profile of one expert on B calibration tokens (collect_activation_matrix),
+    its top-k_a binarisation and the 14336 x 14336 co-activation counts."""
+    import torch
+    from paper_2510_19366_b200.calibrate import binarize_topk, coactivation, collect_activations
+    L, xs = build_layer(0, B, 2)
+    act = collect_activations(L, 0, xs[0])
+    bits = binarize_topk(act, k_a)
+    co = coactivation(bits)
+    t_act = time_steps(lambda i: collect_activations(L, i % E, xs[i % N_XBUF]), steps, 2, 1)
+    t_bin = time_steps(lambda i: binarize_topk(act, k_a), steps, 2, 1)
+    t_co = time_steps(lambda i: coactivation(bits), steps, 2, 1)
+    f_act = 4.0 * B * D * FF
+    f_co = 2.0 * FF * FF * B
+    out = {"workload": f"activation profile of one Mixtral expert (d=4096, ffn=14336) on {B} calibration tokens, "
+                       f"top-{k_a} binarisation, {FF}x{FF} co-activation counts",
+           "collect_ms": t_act, "collect_tflops": f_act / (t_act * 1e-3) / 1e12,
+           "binarize_ms": t_bin, "binarize_gbs": B * FF * 5 / (t_bin * 1e-3) / 1e9,
+           "coactivation_ms": t_co, "coactivation_tflops": f_co / (t_co * 1e-3) / 1e12,
+           "peak_tflops": pk["bf16_tflops_sustained"]}
+    del act, bits, co
+    L.close()
+    torch.cuda.synchronize()
+    return out
+
+
 def time_steps(fn, steps, warmup, world):
     import torch
     for i in range(warmup):
@@ -535,7 +562,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-ep", action="store_true", help="run the expert-parallel path even at N=1 (loopback)")
     ap.add_argument("--no-extras", action="store_true",
-                    help="skip the other BASELINE configs (Qwen shape, 32-layer stack, 32k mixed-QoS batch)")
+                    help="skip the other BASELINE configs (Qwen shape, 32-layer stack, 32k mixed-QoS batch) "
+                         "and the calibration timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -639,6 +667,7 @@ def main():
         layers = []
         torch.cuda.empty_cache()
         other["stack32"] = bench_stack(pk)
+        other["calibration"] = bench_calibration(pk)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -213,6 +213,25 @@ mp_status mp_ep_pack(mp_ep_t ep, const void* x, const uint32_t* sel, const float
 /* back: device [sum(send_counts) x d] partial outputs (dtype), in send order. */
 mp_status mp_ep_combine(mp_ep_t ep, const void* back, uint32_t n_tokens, void* y, void* stream);
 
+/* ---- Calibration: the activation profile the offline
+ * refactoring engine partitions experts with, computed on the GPU. ----
+ * mp_layer_collect_activations <- collect_activation_matrix
+ *   (inc/expert.hpp:137-151): act[b][j] = |a_j(x_b)| of expert e, fp32,
+ *   B x d_ff row-major in the ORIGINAL neuron order; x device B x d_model of
+ *   the layer dtype (bf16 layers: the fused SwiGLU GEMM with an |a|
+ *   epilogue, bf16 operands / fp32 accumulation).
+ * mp_binarize_topk <- binarize_topk (inc/activation.hpp:213-240): per row
+ *   the k_a largest magnitudes -> 1, ties to the lower column; device
+ *   act [rows x cols] fp32 -> bits [rows x cols] u8.  Exact.
+ * mp_coactivation <- coactivation (inc/activation.hpp:242-266):
+ *   co[i][j] = #rows with bits i and j set; device bits -> co [cols x cols]
+ *   u32, a tensor-core GEMM over the 0/1 matrix (exact, rows <= 2^24). */
+mp_status mp_layer_collect_activations(mp_layer_t h, uint32_t e, const void* x, uint32_t B, float* act,
+                                       void* stream);
+mp_status mp_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,
+                           void* stream);
+mp_status mp_coactivation(const uint8_t* bits, uint32_t rows, uint32_t cols, uint32_t* co, void* stream);
+
 /* Host-only readers (no GPU touched), format-compatible with the reference.
  * mp_format_read_mpex <- load_toy_expert (inc/io.hpp:225-251): call with
  * null weight pointers to learn the dims, then with d_model*d_ff buffers.
@@ -226,6 +245,11 @@ mp_status mp_format_read_partition_doc(const char* path, size_t index, size_t* n
                                        uint32_t* n_sub, size_t* n, uint32_t* assignment, uint32_t* r,
                                        size_t* n_gate_ids, uint32_t* gate_offsets, uint32_t* gate_ids);
 mp_status mp_validate_partition(uint32_t n_sub, const uint32_t* assignment, size_t n);
+/* MPAM activation matrix <- save_activation_matrix / load_activation_matrix
+ * (inc/io.hpp:147-200, binary): the reader rectifies |v|, rejects trailing
+ * bytes and non-finite values; two-phase (data NULL -> dims only). */
+mp_status mp_format_write_mpam(const char* path, uint32_t rows, uint32_t cols, const float* data);
+mp_status mp_format_read_mpam(const char* path, uint32_t* rows, uint32_t* cols, float* data);
 
 #ifdef __cplusplus
 }

@@ -23,11 +23,13 @@
 #include <thread>
 #include <vector>
 
+#include "moeprism/activation.hpp"
 #include "moeprism/error.hpp"
 #include "moeprism/expert.hpp"
 #include "moeprism/gating.hpp"
 #include "moeprism/io.hpp"
 #include "moeprism/partition.hpp"
+#include "moeprism/perfmodel.hpp"
 #include "moeprism/rng.hpp"
 #include "moeprism/serde.hpp"
 #include "support.hpp"
@@ -329,4 +331,66 @@ int ref_layer_forward(void* h, std::size_t T, const float* x, std::uint32_t k_ma
     return 0;
 }
 
+
+// ---- calibration side, verbatim reference calls ----
+int ref_collect_activation_matrix(std::size_t d, std::size_t ff, const float* wg, const float* wu, const float* wd,
+                                  std::size_t B, const float* x, float* out) {
+    return guarded([&] {
+        ToyExpert e = make_expert(d, ff, wg, wu, wd);
+        std::vector<std::vector<float>> in(B);
+        for (std::size_t b = 0; b < B; ++b) in[b].assign(x + b * d, x + (b + 1) * d);
+        ActivationMatrix m = collect_activation_matrix(e, in);
+        std::memcpy(out, m.data.data(), m.data.size() * sizeof(float));
+    });
+}
+
+int ref_binarize_topk(const float* act, std::size_t rows, std::size_t cols, std::size_t k_a, std::uint8_t* bits) {
+    return guarded([&] {
+        ActivationMatrix m = make_activation_matrix(rows, cols);
+        m.data.assign(act, act + rows * cols);
+        BinaryActivation b = binarize_topk(m, k_a);
+        std::memcpy(bits, b.bits.data(), b.bits.size());
+    });
+}
+
+int ref_coactivation(const std::uint8_t* bits, std::size_t rows, std::size_t cols, std::size_t k_a,
+                     std::uint32_t* co) {
+    return guarded([&] {
+        BinaryActivation b;
+        b.rows = rows;
+        b.cols = cols;
+        b.k_a = k_a;
+        b.bits.assign(bits, bits + rows * cols);
+        CoActivationMatrix c = coactivation(b);
+        std::memcpy(co, c.data.data(), c.data.size() * sizeof(std::uint32_t));
+    });
+}
+
+int ref_save_activation_matrix(const char* path, std::size_t rows, std::size_t cols, const float* data) {
+    return guarded([&] {
+        ActivationMatrix m = make_activation_matrix(rows, cols);
+        m.data.assign(data, data + rows * cols);
+        save_activation_matrix(m, path);
+    });
+}
+
+int ref_load_activation_matrix(const char* path, std::size_t* rows, std::size_t* cols, float* data) {
+    return guarded([&] {
+        ActivationMatrix m = load_activation_matrix(path, MatrixFormat::binary);
+        *rows = m.rows;
+        *cols = m.cols;
+        if (data) std::memcpy(data, m.data.data(), m.data.size() * sizeof(float));
+    });
+}
+
+// load_perf_table (validates the grid) + eval_cost at (batch, k)
+int ref_perf_table_eval(const char* path, std::uint64_t batch, std::uint32_t k, double* cost, std::size_t* n_batch,
+                        std::size_t* n_k) {
+    return guarded([&] {
+        PerfTable t = load_perf_table(path);
+        *cost = eval_cost(t, batch, k);
+        *n_batch = t.batch_axis.size();
+        *n_k = t.k_axis.size();
+    });
+}
 }  // extern "C"

@@ -230,6 +230,52 @@ void validate_partition(uint32_t n_sub, const uint32_t* a, size_t n) {
                                     std::to_string(hi));
 }
 
+// MPAM activation matrix (inc/io.hpp:147-158 save_activation_matrix,
+// :162-200 load_activation_matrix binary branch): "MPAM", u32 version 1,
+// u32 rows, u32 cols, rows*cols little-endian f32 row-major.  The reader
+// rejects trailing bytes and non-finite values and rectifies (|v|) like the
+// reference's loader.
+void write_mpam(const std::string& path, uint32_t rows, uint32_t cols, const float* data) {
+    if (rows < 1 || cols < 1) fail(MP_ERR_VALIDATION, "activation matrix must have at least one row and one column");
+    for (size_t i = 0; i < (size_t)rows * cols; ++i)
+        if (!std::isfinite(data[i]) || data[i] < 0.0f)
+            fail(MP_ERR_VALIDATION, "activation matrix entries must be finite and non-negative");
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) fail(MP_ERR_IO, "cannot open " + path + " for writing");
+    unsigned char hdr[16] = {'M', 'P', 'A', 'M'};
+    const uint32_t v[3] = {1u, rows, cols};
+    for (int i = 0; i < 3; ++i)
+        for (int b = 0; b < 4; ++b) hdr[4 + 4 * i + b] = static_cast<unsigned char>(v[i] >> (8 * b));
+    out.write(reinterpret_cast<const char*>(hdr), 16);
+    out.write(reinterpret_cast<const char*>(data), static_cast<std::streamsize>((size_t)rows * cols * 4));
+    if (!out) fail(MP_ERR_IO, "failed while writing " + path);
+}
+
+std::vector<float> read_mpam(const std::string& path, uint32_t& rows, uint32_t& cols) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) fail(MP_ERR_IO, "cannot open " + path);
+    unsigned char hdr[16];
+    if (!in.read(reinterpret_cast<char*>(hdr), 4) || std::memcmp(hdr, "MPAM", 4) != 0)
+        fail(MP_ERR_VALIDATION, path + " does not start with the 'MPAM' magic");
+    if (!in.read(reinterpret_cast<char*>(hdr + 4), 12)) fail(MP_ERR_VALIDATION, "truncated file while reading header");
+    if (le_u32(hdr + 4) != 1) fail(MP_ERR_VALIDATION, path + " has unsupported version " + std::to_string(le_u32(hdr + 4)));
+    rows = le_u32(hdr + 8);
+    cols = le_u32(hdr + 12);
+    if (rows < 1 || cols < 1) fail(MP_ERR_VALIDATION, path + " declares an empty matrix");
+    std::vector<float> d((size_t)rows * cols);
+    if (!in.read(reinterpret_cast<char*>(d.data()), static_cast<std::streamsize>(d.size() * 4)))
+        fail(MP_ERR_VALIDATION, "truncated file while reading matrix data");
+    char extra;
+    if (in.read(&extra, 1)) fail(MP_ERR_VALIDATION, path + " holds more data than its header declares");
+    for (size_t i = 0; i < d.size(); ++i) {
+        if (!std::isfinite(d[i]))
+            fail(MP_ERR_VALIDATION, path + ": non-finite value at row " + std::to_string(i / cols) + ", col " +
+                                        std::to_string(i % cols));
+        d[i] = std::fabs(d[i]);
+    }
+    return d;
+}
+
 MpexData read_mpex(const std::string& path) {
     std::ifstream in(path, std::ios::binary);
     if (!in) fail(MP_ERR_IO, "cannot open " + path);

@@ -8,6 +8,7 @@
 //       halves of the SwiGLU for 128 neurons and the activation is fused in
 //       the epilogue.
 //   gemm2 (SWIGLU=false): O[r][n*256 + c] = acc[r][c]
+//   calibration epilogues (kEpiActAbs, kEpiCount): see TcParams.
 //       A = H (rows x w_pad), B = W2[g] (d_pad x w_pad).
 // Variable-size groups: sub-expert g owns rows [offsets[g], offsets[g+1])
 // (written by the bucket scan on the device); tiles are enumerated (g, n, m)
@@ -66,6 +67,11 @@ struct TcParams {
     const uint32_t* mprefix;
     __nv_bfloat16* out;
     uint64_t* trace;  // [grid][4] MMA-issuer timing (diagnostics) or null
+    uint32_t b_row0;  // first B row (calibration: one expert of the packed W1)
+    // kEpiActAbs: fp32 |SwiGLU| of packed neuron q to column colmap[q] (< 0: padding)
+    // kEpiCount:  uint32(acc) (exact 0/1 co-activation counts)
+    const int32_t* colmap;
+    void* out32;
 };
 
 __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix, uint32_t G, uint32_t NT,
@@ -91,7 +97,7 @@ struct Cursor {
     int32_t row;  // A row (arow) or B row (brow) of the current tile
 };
 
-template <bool SWIGLU>
+template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -150,7 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (c.tile >= total) return;
                 uint32_t g, m, n;
                 map_tile(c.tile, s_prefix, p.G, p.NT, g, m, n);
-                c.row = is_a ? static_cast<int32_t>(s_off[g] + m * BM) : static_cast<int32_t>(g * p.N_group + n * BN);
+                c.row = is_a ? static_cast<int32_t>(s_off[g] + m * BM)
+                             : static_cast<int32_t>(p.b_row0 + g * p.N_group + n * BN);
             };
             auto advance = [&](Cursor& c, bool is_a) {
                 if (++c.kb == nkb) {
@@ -249,7 +256,50 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool valid = row_local < s_off[g + 1] - s_off[g];
             __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
             const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN;
-            if constexpr (SWIGLU) {
+            if constexpr (EPI == kEpiActAbs) {
+                // calibration profiler: |a| in the original neuron order
+                float* arow = static_cast<float*>(p.out32) + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
+#pragma unroll 1
+                for (uint32_t c = 0; c < 4; ++c) {
+                    const uint32_t gcol = (c >> 1) * 128 + (c & 1u) * 32;
+                    uint32_t gr[32], ur[32];
+                    tmem_ld32(taddr + gcol, gr);
+                    tmem_ld32(taddr + gcol + kIlv, ur);
+                    tmem_ld_wait();
+                    if (valid) {
+                        const int32_t* cm = p.colmap + n * 128 + c * 32;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int32_t j = __ldg(cm + i);
+                            if (j >= 0) arow[j] = fabsf(silu_f32(__uint_as_float(gr[i])) * __uint_as_float(ur[i]));
+                        }
+                    }
+                }
+            } else if constexpr (EPI == kEpiCount) {
+                uint32_t* crow = static_cast<uint32_t*>(p.out32) + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
+#pragma unroll 1
+                for (uint32_t c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(taddr + c * 32, r);
+                    tmem_ld_wait();
+                    const uint32_t col = n * BN + c * 32;
+                    if (valid && col < p.n_valid) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            if (col + i + 3 < p.n_valid && (p.ld_out & 3u) == 0) {
+                                st_global_v4(crow + col + i,
+                                             make_uint4(__float2uint_rn(__uint_as_float(r[i])),
+                                                        __float2uint_rn(__uint_as_float(r[i + 1])),
+                                                        __float2uint_rn(__uint_as_float(r[i + 2])),
+                                                        __float2uint_rn(__uint_as_float(r[i + 3]))));
+                            } else {
+                                for (int u = 0; u < 4; ++u)
+                                    if (col + i + u < p.n_valid) crow[col + i + u] = __float2uint_rn(__uint_as_float(r[i + u]));
+                            }
+                        }
+                    }
+                }
+            } else if constexpr (EPI == kEpiSwiglu) {
 #pragma unroll 1
                 for (uint32_t c = 0; c < 4; ++c) {
                     // neurons n*128 + c*32 .. +31: gate columns (c/2)*128 + (c%2)*32, up + 64
@@ -354,6 +404,13 @@ bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t
 
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s) {
+    launch_gemm_tc_epi(swiglu ? kEpiSwiglu : kEpiPlain, tmA, tmB, out, sh, offsets, mprefix, num_sms, s);
+}
+
+void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
+                        const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
+                        uint32_t b_row0, const int32_t* colmap) {
+    const bool swiglu = epi == kEpiSwiglu;
     TcParams p;
     p.G = sh.G;
     p.K = sh.K;
@@ -364,21 +421,28 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.offsets = offsets;
     p.mprefix = mprefix;
     p.out = static_cast<__nv_bfloat16*>(out);
-    p.trace = gemm_trace_buffer(swiglu);
+    p.trace = (epi == kEpiSwiglu || epi == kEpiPlain) ? gemm_trace_buffer(swiglu) : nullptr;
+    p.b_row0 = b_row0;
+    p.colmap = colmap;
+    p.out32 = out;
 
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
     static bool attr_set = false;  // once per process (device-independent attribute)
     if (!attr_set) {
-        cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<kEpiPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<kEpiSwiglu>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<kEpiActAbs>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_tc_kernel<kEpiCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         attr_set = true;
     }
-    if (swiglu)
-        gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
-    else
-        gemm_tc_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+    switch (epi) {
+        case kEpiSwiglu: gemm_tc_kernel<kEpiSwiglu><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p); break;
+        case kEpiActAbs: gemm_tc_kernel<kEpiActAbs><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p); break;
+        case kEpiCount: gemm_tc_kernel<kEpiCount><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p); break;
+        default: gemm_tc_kernel<kEpiPlain><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p); break;
+    }
 }
 
 }  // namespace mp

@@ -135,6 +135,7 @@ struct mp_layer_s {
     double r_guard = kRouterGuard;  // MOEPRISM_ROUTER_GUARD overrides (tests widen it)
     CUtensorMap tm_wplanes{};
     int32_t* d_nmap = nullptr;
+    int32_t* nmap_all = nullptr;  // [E][S*w_pad] packed neuron -> original neuron (-1 padding), calibration
 
     uint32_t* sel = nullptr;
     float* wsel = nullptr;
@@ -160,6 +161,7 @@ struct mp_layer_s {
     CUtensorMap tm_w1s{}, tm_w2s{}, tm_hs{}, tm_w1sh{}, tm_w2sh{};
 
     bool residual = false;  // mp_layer_set_residual: y = x + MoE(x), fused into the combine
+    uint32_t* cal_meta = nullptr;  // calibration GEMM group offsets / tile prefix
 
     bool profiling = false;
     struct EventSet {
@@ -178,11 +180,11 @@ namespace {
 void free_layer(mp_layer_s* L) {
     for (float* p : L->raw)
         if (p) cudaFree(p);
-    void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_flagged, L->r_ticket, L->d_nmap, L->sel,
+    void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_flagged, L->r_ticket, L->d_nmap, L->nmap_all, L->sel,
                     L->wsel, L->kpt_dev, L->ws.lrank, L->ws.block_counts, L->ws.block_base, L->ws.offsets,
                     L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.mprefix_tc2, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
                     L->x_perm, L->h, L->o, L->x_stage, L->y_stage, L->W1s, L->W2s, L->sh_gate, L->sh_h,
-                    L->sh_o, L->sh_w, L->sh_meta};
+                    L->sh_o, L->sh_w, L->sh_meta, L->cal_meta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (auto* v : {&L->ev_pool, &L->ev_pending})
@@ -205,6 +207,9 @@ void maybe_pack(mp_layer_s* L, uint32_t e) {
         nmap[static_cast<size_t>(s) * L->w_pad + fill[s]++] = static_cast<int32_t>(j);
     }
     ck(cudaMemcpy(L->d_nmap, nmap.data(), nmap.size() * sizeof(int32_t), cudaMemcpyHostToDevice), "nmap upload");
+    ck(cudaMemcpy(L->nmap_all + (size_t)e * nmap.size(), nmap.data(), nmap.size() * sizeof(int32_t),
+                  cudaMemcpyHostToDevice),
+       "nmap keep");
     const size_t n = static_cast<size_t>(L->d) * L->ff;
     const float* wg = L->raw[e];
     const float* wu = wg + n;
@@ -554,6 +559,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 L->W2 = dalloc<char>(w2 * L->esz, "W2");
                 ck(cudaMemset(L->W2, 0, w2 * L->esz), "memset W2");
                 L->d_nmap = dalloc<int32_t>((size_t)L->S * L->w_pad, "nmap");
+                L->nmap_all = dalloc<int32_t>((size_t)L->E * L->S * L->w_pad, "nmap (all experts)");
             }
             if (router) {
                 L->wrT = dalloc<float>((size_t)L->G_pad * L->d, "router");
@@ -1145,5 +1151,103 @@ MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {
         if (!L || mode < 0 || mode > 3) fail(MP_ERR_VALIDATION, "bad argument");
         L->tile_mode = mode;
+    });
+}
+
+// ============================================================== calibration
+// the activation profile the offline refactoring engine
+// partitions experts with, on the GPU.
+
+MP_API mp_status mp_layer_collect_activations(mp_layer_t L, uint32_t e, const void* x, uint32_t B, float* act,
+                                              void* stream) {
+    return guarded([&] {
+        if (!L || (B && (!x || !act))) fail(MP_ERR_VALIDATION, "null argument");
+        if (e >= L->E) fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " out of range");
+        if (!L->has_experts) fail(MP_ERR_VALIDATION, "router-only layer holds no expert weights");
+        if (!L->packed[e]) fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " is not ready");
+        if (!L->use_tc) fail(MP_ERR_VALIDATION, "the activation profiler runs on the bf16 tensor-core layout");
+        if (L->d % 8) fail(MP_ERR_VALIDATION, "the activation profiler needs d_model % 8 == 0");
+        // inc/expert.hpp:141: an empty calibration list is a ValidationError
+        if (B == 0) fail(MP_ERR_VALIDATION, "calibration input list is empty");
+        if (reinterpret_cast<uintptr_t>(x) % 16) fail(MP_ERR_VALIDATION, "x must be 16-byte aligned");
+        DeviceGuard dg(L->desc.device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (!L->cal_meta) L->cal_meta = dalloc<uint32_t>(4, "calibration meta");
+        CUtensorMap tmX;
+        if (!mp::make_tmap_bf16_2d(&tmX, x, B, L->d, 128, 64)) fail(MP_ERR_CUDA, "calibration tensor map");
+        mp::launch_set_group_meta(L->cal_meta, B, s);
+        // one group: all S sub-experts of expert e (S * 2 * w_pad rows of W1), A = x
+        const uint32_t n_rows = L->S * 2 * L->w_pad;
+        mp::GemmShape sh{1, L->d_pad, n_rows, B, L->ff, n_rows};
+        mp::launch_gemm_tc_epi(mp::kEpiActAbs, &tmX, &L->tm_w1, act, sh, L->cal_meta, L->cal_meta + 2, L->num_sms, s,
+                               e * n_rows, L->nmap_all + (size_t)e * L->S * L->w_pad);
+        ck_launch("collect activations");
+        L->launches += 2;
+    });
+}
+
+MP_API mp_status mp_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,
+                                  void* stream) {
+    return guarded([&] {
+        if (!act || !bits) fail(MP_ERR_VALIDATION, "null argument");
+        if (rows < 1 || cols < 1)
+            fail(MP_ERR_VALIDATION, "activation matrix must have at least one row and one column");
+        if (k_a < 1 || k_a > cols)
+            fail(MP_ERR_VALIDATION, "k_a = " + std::to_string(k_a) + " out of range [1, " + std::to_string(cols) + "]");
+        mp::launch_binarize_topk(act, rows, cols, k_a, bits, static_cast<cudaStream_t>(stream));
+        ck_launch("binarize_topk");
+    });
+}
+
+MP_API mp_status mp_coactivation(const uint8_t* bits, uint32_t rows, uint32_t cols, uint32_t* co, void* stream) {
+    return guarded([&] {
+        if (!bits || !co) fail(MP_ERR_VALIDATION, "null argument");
+        if (rows < 1 || cols < 1) fail(MP_ERR_VALIDATION, "binary activation shape is inconsistent");
+        if (rows > (1u << 24)) fail(MP_ERR_VALIDATION, "co-activation counts are exact for at most 2^24 rows");
+        int dev = 0, sms = 0;
+        ck(cudaGetDevice(&dev), "device");
+        ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const uint32_t ld = round_up(rows, 64);
+        void* bt = nullptr;
+        uint32_t* meta = nullptr;
+        ck(cudaMallocAsync(&bt, (size_t)cols * ld * 2, s), "co-activation scratch");
+        cudaError_t e2 = cudaMallocAsync(reinterpret_cast<void**>(&meta), 4 * sizeof(uint32_t), s);
+        if (e2 != cudaSuccess) {
+            cudaFreeAsync(bt, s);
+            ck(e2, "co-activation meta");
+        }
+        mp::launch_bits_to_bf16_t(bits, rows, cols, ld, bt, s);
+        mp::launch_set_group_meta(meta, cols, s);
+        CUtensorMap tA, tB;
+        const bool ok = mp::make_tmap_bf16_2d(&tA, bt, cols, ld, 128, 64) && mp::make_tmap_bf16_2d(&tB, bt, cols, ld, 256, 64);
+        if (ok) {
+            // C[i][j] = sum_r B[r][i] B[r][j]: A = B^T (cols x rows), B operand = B^T
+            mp::GemmShape sh{1, ld, cols, cols, cols, cols};
+            mp::launch_gemm_tc_epi(mp::kEpiCount, &tA, &tB, co, sh, meta, meta + 2, sms, s);
+        }
+        cudaError_t le = cudaGetLastError();
+        cudaFreeAsync(bt, s);
+        cudaFreeAsync(meta, s);
+        if (!ok) fail(MP_ERR_CUDA, "co-activation tensor maps");
+        ck(le, "coactivation");
+    });
+}
+
+MP_API mp_status mp_format_write_mpam(const char* path, uint32_t rows, uint32_t cols, const float* data) {
+    return guarded([&] {
+        if (!path || !data) fail(MP_ERR_VALIDATION, "null argument");
+        mp::write_mpam(path, rows, cols, data);
+    });
+}
+
+MP_API mp_status mp_format_read_mpam(const char* path, uint32_t* rows, uint32_t* cols, float* data) {
+    return guarded([&] {
+        if (!path || !rows || !cols) fail(MP_ERR_VALIDATION, "null argument");
+        uint32_t r = 0, c = 0;
+        std::vector<float> d = mp::read_mpam(path, r, c);
+        *rows = r;
+        *cols = c;
+        if (data) std::memcpy(data, d.data(), d.size() * 4);
     });
 }

@@ -115,12 +115,28 @@ void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s);
 size_t gemm_tc_smem_bytes();
+// Epilogue modes of the 1-SM tensor-core GEMM (gemm_tc.cu).
+constexpr int kEpiPlain = 0;   // bf16 acc
+constexpr int kEpiSwiglu = 1;  // bf16 silu(gate) * up (fused SwiGLU)
+constexpr int kEpiActAbs = 2;  // fp32 |silu(gate) * up| scattered to colmap[packed neuron] (calibration)
+constexpr int kEpiCount = 3;   // uint32 counts (co-activation of 0/1 operands)
+// b_row0: first B row; colmap: kEpiActAbs column map; out: bf16 / f32 / u32 per mode
+void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
+                        const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
+                        uint32_t b_row0 = 0, const int32_t* colmap = nullptr);
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
                      bool tail128 = true);
+
+// Calibration (calib.cu).
+void launch_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,
+                          cudaStream_t s);
+void launch_bits_to_bf16_t(const uint8_t* bits, uint32_t rows, uint32_t cols, uint32_t ld, void* out, cudaStream_t s);
+// meta = {0, rows, 0, ceil(rows / 128)}: offsets + 128-row tile prefix of one group
+void launch_set_group_meta(uint32_t* meta, uint32_t rows, cudaStream_t s);
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point.
 bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,

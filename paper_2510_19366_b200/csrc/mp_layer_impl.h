@@ -39,5 +39,8 @@ MpexData read_mpex(const std::string& path);
 std::vector<PartitionDocHost> read_partition_map(const std::string& path);
 // validate(Partition), inc/partition.hpp:34-46.  Throws Failure.
 void validate_partition(uint32_t n_sub, const uint32_t* assignment, size_t n);
+// MPAM activation matrices (inc/io.hpp:147-200, binary format).  Throws Failure.
+void write_mpam(const std::string& path, uint32_t rows, uint32_t cols, const float* data);
+std::vector<float> read_mpam(const std::string& path, uint32_t& rows, uint32_t& cols);
 
 }  // namespace mp

@@ -257,6 +257,13 @@ class RefLib:
         L.ref_proxy_scores.argtypes = [_f32p, _sz, C.c_uint32, C.c_uint32, _u32p, _u32p, _f64p]
         L.ref_select_topk.argtypes = [_f64p, _sz, C.c_uint32, _u32p]
         L.ref_save_toy_expert.argtypes = [C.c_char_p, _sz, _sz, _f32p, _f32p, _f32p]
+        L.ref_collect_activation_matrix.argtypes = [_sz, _sz, _f32p, _f32p, _f32p, _sz, _f32p, _f32p]
+        L.ref_binarize_topk.argtypes = [_f32p, _sz, _sz, _sz, C.c_void_p]
+        L.ref_coactivation.argtypes = [C.c_void_p, _sz, _sz, _sz, _u32p]
+        L.ref_save_activation_matrix.argtypes = [C.c_char_p, _sz, _sz, _f32p]
+        L.ref_load_activation_matrix.argtypes = [C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.c_void_p]
+        L.ref_perf_table_eval.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_double), C.POINTER(_sz),
+                                          C.POINTER(_sz)]
         L.ref_load_toy_expert.argtypes = [C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_append_partition_doc.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, _sz, _u32p, C.c_double, C.c_uint64, C.c_int]
         L.ref_append_partition_gates_doc.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, _sz, _u32p, C.c_uint32,
@@ -293,6 +300,42 @@ class RefLib:
         out = np.empty(n, np.uint32)
         self._check(self.L.ref_random_balanced_partition(n, n_sub, seed, out))
         return out
+
+    # -- calibration --------------------------------------
+    def collect_activation_matrix(self, d, ff, wg, wu, wd, x):
+        x = np.ascontiguousarray(x, np.float32)
+        out = np.empty((x.shape[0], ff), np.float32)
+        self._check(self.L.ref_collect_activation_matrix(d, ff, wg, wu, wd, x.shape[0], x.reshape(-1), out.reshape(-1)))
+        return out
+
+    def binarize_topk(self, act, k_a):
+        act = np.ascontiguousarray(act, np.float32)
+        bits = np.empty(act.shape, np.uint8)
+        self._check(self.L.ref_binarize_topk(act.reshape(-1), act.shape[0], act.shape[1], k_a, bits.ctypes.data))
+        return bits
+
+    def coactivation(self, bits, k_a):
+        bits = np.ascontiguousarray(bits, np.uint8)
+        co = np.empty((bits.shape[1], bits.shape[1]), np.uint32)
+        self._check(self.L.ref_coactivation(bits.ctypes.data, bits.shape[0], bits.shape[1], k_a, co.reshape(-1)))
+        return co
+
+    def save_activation_matrix(self, path, act):
+        act = np.ascontiguousarray(act, np.float32)
+        self._check(self.L.ref_save_activation_matrix(str(path).encode(), act.shape[0], act.shape[1], act.reshape(-1)))
+
+    def load_activation_matrix(self, path):
+        r, c = _sz(), _sz()
+        self._check(self.L.ref_load_activation_matrix(str(path).encode(), C.byref(r), C.byref(c), None))
+        out = np.empty((r.value, c.value), np.float32)
+        self._check(self.L.ref_load_activation_matrix(str(path).encode(), C.byref(r), C.byref(c), out.ctypes.data))
+        return out
+
+    def perf_table_eval(self, path, batch, k):
+        """load_perf_table (with its grid / monotonicity validation) + eval_cost."""
+        cost, nb, nk = C.c_double(), _sz(), _sz()
+        self._check(self.L.ref_perf_table_eval(str(path).encode(), batch, k, C.byref(cost), C.byref(nb), C.byref(nk)))
+        return cost.value, nb.value, nk.value
 
     def contiguous_partition(self, n, n_sub):
         out = np.empty(max(n, 1), np.uint32)
@@ -426,3 +469,27 @@ class RefLayer:
 
 def have_ref() -> bool:
     return REF_SO.exists()
+
+
+# ---- numpy restatements of the calibration helpers (the checker where the
+# reference build is absent; pinned against it in tests/test_oracle.py) ----
+
+def np_binarize_topk(act, k_a):
+    """binarize_topk (inc/activation.hpp:213-240): per row the k_a largest
+    magnitudes, ties broken by lower column index."""
+    act = np.asarray(act, np.float32)
+    rows, cols = act.shape
+    if not 1 <= k_a <= cols:
+        raise OracleError(1, f"k_a = {k_a} out of range [1, {cols}]")
+    bits = np.zeros((rows, cols), np.uint8)
+    idx = np.arange(cols)
+    for r in range(rows):
+        order = np.lexsort((idx, -act[r].astype(np.float64)))
+        bits[r, order[:k_a]] = 1
+    return bits
+
+
+def np_coactivation(bits):
+    """coactivation (inc/activation.hpp:242-266): C = B^T B over the 0/1 mask."""
+    b = np.asarray(bits, np.int64)
+    return (b.T @ b).astype(np.uint32)
