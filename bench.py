@@ -370,6 +370,35 @@ def bench_mixed_qos_32k(L32, pk, steps=10):
             "mean_k": kk, "tokens_per_s": T / (ms * 1e-3), "ms_per_step": ms, "roofline": roofline_fb(F, B, ms, pk)}
 
 
+def bench_offload(T=16, k=2, cache_units=32, steps=20):
+    """SURVEY 8(f).4 at the Mixtral shape: decode batches of T tokens on a
+    layer whose packed weights live in pinned host memory, with a device
+    cache of `cache_units` of the 64 sub-experts (LRU, cache_step semantics);
+    misses are real host->device copies."""
+    import time
+    import torch
+    L, xs = build_layer(0, T, k)
+    L.enable_offload(cache_units)
+    y = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
+    for i in range(3):
+        L.forward(xs[i % N_XBUF][:T], k=k, y=y)
+    torch.cuda.synchronize()
+    h0, m0, b0, _, _ = L.offload_stats()
+    t0 = time.perf_counter()
+    for i in range(steps):
+        L.forward(xs[i % N_XBUF][:T], k=k, y=y)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    h1, m1, b1, _, _ = L.offload_stats()
+    L.close()
+    return {"workload": f"Mixtral-shape layer with weights offloaded to pinned host memory, device cache of "
+                        f"{cache_units}/64 sub-experts (LRU), decode batches of {T} tokens, k={k}; wall clock "
+                        "(each forward synchronises to read its bucket sizes)",
+            "tokens_per_s": steps * T / dt, "ms_per_step": 1e3 * dt / steps,
+            "hit_ratio": (h1 - h0) / max(1, (h1 - h0) + (m1 - m0)), "h2d_gb_per_s": (b1 - b0) / dt / 1e9,
+            "h2d_mb_per_step": (b1 - b0) / steps / 1e6}
+
+
 def bench_calibration(pk, B=4096, k_a=1434, steps=5):
     """SURVEY 8(f).2 on the GPU at the Mixtral expert shape: the activation
     profile of one expert on B calibration tokens (collect_activation_matrix),
@@ -668,6 +697,7 @@ def main():
         torch.cuda.empty_cache()
         other["stack32"] = bench_stack(pk)
         other["calibration"] = bench_calibration(pk)
+        other["offload"] = bench_offload()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

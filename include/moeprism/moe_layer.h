@@ -213,6 +213,22 @@ mp_status mp_ep_pack(mp_ep_t ep, const void* x, const uint32_t* sel, const float
 /* back: device [sum(send_counts) x d] partial outputs (dtype), in send order. */
 mp_status mp_ep_combine(mp_ep_t ep, const void* back, uint32_t n_tokens, void* y, void* stream);
 
+/* ---- Sub-expert offload cache (the reference simulates it:
+ * cache_step / run_offload_sim, inc/offload.hpp:202-290). ----
+ * mp_layer_enable_offload moves the packed weights to pinned host memory and
+ * keeps a device cache of cache_units units (unit_subexperts = 1: one
+ * sub-expert, "fine"; = S: a whole expert, "monolithic").  Every forward then
+ * reads its bucket sizes back (the stream is synchronised), runs one
+ * cache_step with the reference's LRU policy over the units that received
+ * tokens, copies the misses host->device and computes from the cache.
+ * Outputs are bit-identical to the resident layer.  Fails if one forward
+ * needs more units than the cache holds (the reference's ValidationError).
+ * mp_layer_offload_stats: cumulative hits / misses / bytes, and the last
+ * forward's requested units (ascending) and miss count. */
+mp_status mp_layer_enable_offload(mp_layer_t h, uint32_t unit_subexperts, uint32_t cache_units);
+mp_status mp_layer_offload_stats(mp_layer_t h, uint64_t* hits, uint64_t* misses, uint64_t* bytes_h2d,
+                                 uint32_t* last_units, uint32_t cap, uint32_t* n_last, uint32_t* last_misses);
+
 /* ---- Calibration: the activation profile the offline
  * refactoring engine partitions experts with, computed on the GPU. ----
  * mp_layer_collect_activations <- collect_activation_matrix

@@ -28,6 +28,7 @@
 #include "moeprism/expert.hpp"
 #include "moeprism/gating.hpp"
 #include "moeprism/io.hpp"
+#include "moeprism/offload.hpp"
 #include "moeprism/partition.hpp"
 #include "moeprism/perfmodel.hpp"
 #include "moeprism/rng.hpp"
@@ -391,6 +392,27 @@ int ref_perf_table_eval(const char* path, std::uint64_t batch, std::uint32_t k, 
         *cost = eval_cost(t, batch, k);
         *n_batch = t.batch_axis.size();
         *n_k = t.k_axis.size();
+    });
+}
+
+// cache_step (inc/offload.hpp:202-255) folded over a request sequence, fine
+// granularity, unit bytes 1: the per-step miss counts of the reference LRU.
+int ref_offload_replay(std::uint32_t n_units, std::uint32_t capacity, std::size_t n_steps,
+                       const std::uint32_t* step_off, const std::uint32_t* ids, std::uint64_t* misses) {
+    return guarded([&] {
+        OffloadConfig cfg;
+        cfg.n_experts = n_units;
+        cfg.subexperts_per_expert = 1;
+        cfg.expert_bytes = 1;
+        cfg.vram_bytes = capacity;
+        cfg.pcie_bytes_per_s = 1.0;
+        cfg.compute_s_per_subexpert = 1.0;
+        cfg.granularity = Granularity::fine;
+        CacheState c = make_cache(cfg);
+        for (std::size_t t = 0; t < n_steps; ++t) {
+            std::vector<std::uint32_t> req(ids + step_off[t], ids + step_off[t + 1]);
+            misses[t] = cache_step(c, req, cfg).miss_count;
+        }
     });
 }
 }  // extern "C"

@@ -68,6 +68,7 @@ struct TcParams {
     __nv_bfloat16* out;
     uint64_t* trace;  // [grid][4] MMA-issuer timing (diagnostics) or null
     uint32_t b_row0;  // first B row (calibration: one expert of the packed W1)
+    const uint32_t* gmap;  // nullable: B group of group g (sub-expert offload cache slot), else g
     // kEpiActAbs: fp32 |SwiGLU| of packed neuron q to column colmap[q] (< 0: padding)
     // kEpiCount:  uint32(acc) (exact 0/1 co-activation counts)
     const int32_t* colmap;
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
+    __shared__ uint32_t s_gmap[kMaxG];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sB = base;                 // NB x 32 KB (1024-aligned)
     uint8_t* sA = base + NB * B_BYTES;  // NA x 16 KB
@@ -140,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t q = threadIdx.x; q <= p.G; q += blockDim.x) {
         s_prefix[q] = p.mprefix[q];
         s_off[q] = p.offsets[q];
+        if (q < p.G) s_gmap[q] = p.gmap ? p.gmap[q] : q;
     }
     tc_fence_before();
     __syncthreads();
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t g, m, n;
                 map_tile(c.tile, s_prefix, p.G, p.NT, g, m, n);
                 c.row = is_a ? static_cast<int32_t>(s_off[g] + m * BM)
-                             : static_cast<int32_t>(p.b_row0 + g * p.N_group + n * BN);
+                             : static_cast<int32_t>(p.b_row0 + s_gmap[g] * p.N_group + n * BN);
             };
             auto advance = [&](Cursor& c, bool is_a) {
                 if (++c.kb == nkb) {
@@ -403,13 +406,15 @@ bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t
 }
 
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s) {
-    launch_gemm_tc_epi(swiglu ? kEpiSwiglu : kEpiPlain, tmA, tmB, out, sh, offsets, mprefix, num_sms, s);
+                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
+                    const uint32_t* gmap) {
+    launch_gemm_tc_epi(swiglu ? kEpiSwiglu : kEpiPlain, tmA, tmB, out, sh, offsets, mprefix, num_sms, s, 0, nullptr,
+                       gmap);
 }
 
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                        uint32_t b_row0, const int32_t* colmap) {
+                        uint32_t b_row0, const int32_t* colmap, const uint32_t* gmap) {
     const bool swiglu = epi == kEpiSwiglu;
     TcParams p;
     p.G = sh.G;
@@ -423,6 +428,7 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.out = static_cast<__nv_bfloat16*>(out);
     p.trace = (epi == kEpiSwiglu || epi == kEpiPlain) ? gemm_trace_buffer(swiglu) : nullptr;
     p.b_row0 = b_row0;
+    p.gmap = gmap;
     p.colmap = colmap;
     p.out32 = out;
 

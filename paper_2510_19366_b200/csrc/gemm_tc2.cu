@@ -67,6 +67,7 @@ struct PairParams {
     __nv_bfloat16* out;
     uint64_t* trace;  // [grid][4] MMA-issuer timing of the leaders (diagnostics) or null
     uint32_t tail128;  // tiles with <= 128 valid rows issue M=128 pair MMAs
+    const uint32_t* gmap;  // nullable: B group of group g (sub-expert offload cache slot), else g
 };
 
 MP_DEV uint32_t cluster_rank() {
@@ -160,6 +161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
+    __shared__ uint32_t s_gmap[kMaxG];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // identical offsets in both CTAs (same dynamic smem layout)
     uint8_t* sA = base;                // NS x 16 KB
@@ -194,6 +196,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (uint32_t q = threadIdx.x; q <= p.G; q += blockDim.x) {
         s_prefix[q] = p.mprefix[q];
         s_off[q] = p.offsets[q];
+        if (q < p.G) s_gmap[q] = p.gmap ? p.gmap[q] : q;
     }
     tc_fence_before();
     __syncthreads();
@@ -212,7 +215,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
                 const bool tail = p.tail128 && s_off[g + 1] - s_off[g] - m * BM <= HM;  // M=128: 64 rows per CTA
                 const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * (tail ? HM / 2 : HM));
-                const int32_t brow = static_cast<int32_t>(g * p.N_group + n * BN + rank * 128);
+                const int32_t brow = static_cast<int32_t>(s_gmap[g] * p.N_group + n * BN + rank * 128);
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
@@ -368,9 +371,10 @@ size_t gemm_pair_smem_bytes() { return kSmemBytes; }
 
 // tmB: box of 128 rows (each CTA loads half of the 256-row B tile)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s, bool tail128) {
+                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s, bool tail128,
+                     const uint32_t* gmap) {
     PairParams p{sh.G, sh.K, sh.N_group, sh.n_valid, sh.ld_out, (sh.N_group + BN - 1) / BN, offsets, mprefix256,
-                 static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), tail128 ? 1u : 0u};
+                 static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), tail128 ? 1u : 0u, gmap};
     if (p.trace) cudaMemsetAsync(p.trace, 0, 1024 * 4 * sizeof(uint64_t), s);
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;

@@ -163,6 +163,28 @@ struct mp_layer_s {
     bool residual = false;  // mp_layer_set_residual: y = x + MoE(x), fused into the combine
     uint32_t* cal_meta = nullptr;  // calibration GEMM group offsets / tile prefix
 
+    // Sub-expert offload cache: the packed weights live in
+    // pinned host memory; a device cache of `off_slots` units (a unit = 1
+    // sub-expert "fine" or the S sub-experts of an expert "monolithic") is
+    // managed with the reference's LRU policy (cache_step, inc/offload.hpp:
+    // 202-255) and filled by real host->device copies.
+    bool offload = false;
+    uint32_t off_unit = 1, off_slots = 0;
+    void* W1h = nullptr;  // pinned [G][2 w_pad][d_pad]
+    void* W2h = nullptr;  // pinned [G][d_pad][w_pad]
+    void* W1c = nullptr;  // device [slots * unit][2 w_pad][d_pad]
+    void* W2c = nullptr;  // device [slots * unit][d_pad][w_pad] (+ TMA row padding)
+    CUtensorMap tm_w1c{}, tm_w2c{}, tm_w1ch{}, tm_w2ch{};
+    std::vector<uint32_t> lru;            // resident units, least recent first
+    std::vector<int32_t> slot_of_unit;    // -1 when not resident
+    std::vector<uint32_t> free_slots;
+    uint32_t* gmap_dev = nullptr;         // [G] group -> cache group
+    uint32_t* gmap_host = nullptr;        // pinned [G]
+    uint32_t* off_host = nullptr;         // pinned [G + 1] bucket offsets
+    uint64_t off_hits = 0, off_misses = 0, off_bytes = 0;
+    std::vector<uint32_t> off_last_req;   // requested units of the last forward
+    uint32_t off_last_misses = 0;
+
     bool profiling = false;
     struct EventSet {
         cudaEvent_t ev[kStages + 1];
@@ -187,6 +209,10 @@ void free_layer(mp_layer_s* L) {
                     L->sh_o, L->sh_w, L->sh_meta, L->cal_meta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (void* p : {L->W1c, L->W2c, static_cast<void*>(L->gmap_dev)})
+        if (p) cudaFree(p);
+    for (void* p : {L->W1h, L->W2h, static_cast<void*>(L->gmap_host), static_cast<void*>(L->off_host)})
+        if (p) cudaFreeHost(p);
     for (auto* v : {&L->ev_pool, &L->ev_pending})
         for (auto* es : *v) {
             for (auto& e : es->ev) cudaEventDestroy(e);
@@ -199,6 +225,7 @@ void free_layer(mp_layer_s* L) {
 // expert e once both its weights and its partition are known.
 void maybe_pack(mp_layer_s* L, uint32_t e) {
     if (L->packed[e] || !L->has_part[e] || !L->raw[e]) return;
+    if (L->offload) fail(MP_ERR_VALIDATION, "the layer's weights are offloaded; reload requires a new layer");
     std::vector<int32_t> nmap(static_cast<size_t>(L->S) * L->w_pad, -1);
     std::vector<uint32_t> fill(L->S, 0);
     const auto& a = L->assignment[e];
@@ -323,6 +350,82 @@ void resolve_timings(mp_layer_s* L) {
     L->ev_pending.clear();
 }
 
+// One offload cache step (inc/offload.hpp:202-255 on real transfers): read the
+// bucket sizes back (synchronises the stream), the requested units are those
+// with tokens, misses are evicted-for and copied host->device on the stream,
+// the group -> cache-slot map is uploaded.  LRU order, eviction and
+// most-recent insertion (ascending unit id) follow cache_step exactly.
+void offload_step(mp_layer_s* L, cudaStream_t s) {
+    ck(cudaMemcpyAsync(L->off_host, L->ws.offsets, (size_t)(L->G + 1) * 4, cudaMemcpyDeviceToHost, s), "offsets");
+    ck(cudaStreamSynchronize(s), "offload: bucket sizes");
+    const uint32_t n_units = L->G / L->off_unit;
+    std::vector<uint32_t> req;
+    for (uint32_t u = 0; u < n_units; ++u) {
+        bool any = false;
+        for (uint32_t j = 0; j < L->off_unit; ++j) {
+            const uint32_t g = u * L->off_unit + j;
+            any |= L->off_host[g + 1] > L->off_host[g];
+        }
+        if (any) req.push_back(u);
+    }
+    if (req.size() > L->off_slots)
+        fail(MP_ERR_VALIDATION, "request set of " + std::to_string(req.size()) +
+                                    " units exceeds the cache capacity of " + std::to_string(L->off_slots));
+    std::vector<uint8_t> requested(n_units, 0);
+    uint32_t misses = 0;
+    for (uint32_t u : req) {
+        requested[u] = 1;
+        misses += L->slot_of_unit[u] < 0;
+    }
+    // evict LRU units outside the request until the misses fit
+    size_t need = L->lru.size() + misses;
+    if (need > L->off_slots) {
+        size_t to_evict = need - L->off_slots;
+        std::vector<uint32_t> keep;
+        for (uint32_t u : L->lru) {
+            if (to_evict && !requested[u]) {
+                L->free_slots.push_back(static_cast<uint32_t>(L->slot_of_unit[u]));
+                L->slot_of_unit[u] = -1;
+                --to_evict;
+            } else {
+                keep.push_back(u);
+            }
+        }
+        L->lru.swap(keep);
+    }
+    // requested units become most recent, ascending id; misses take free slots
+    std::vector<uint32_t> rest;
+    for (uint32_t u : L->lru)
+        if (!requested[u]) rest.push_back(u);
+    const size_t b1 = (size_t)2 * L->w_pad * L->d_pad * L->esz;  // W1 bytes per sub-expert
+    const size_t b2 = (size_t)L->d_pad * L->w_pad * L->esz;      // W2 bytes per sub-expert
+    for (uint32_t u : req) {
+        rest.push_back(u);
+        if (L->slot_of_unit[u] >= 0) continue;
+        const uint32_t slot = L->free_slots.back();
+        L->free_slots.pop_back();
+        L->slot_of_unit[u] = static_cast<int32_t>(slot);
+        const size_t n1 = b1 * L->off_unit, n2 = b2 * L->off_unit;
+        ck(cudaMemcpyAsync(static_cast<char*>(L->W1c) + slot * n1, static_cast<char*>(L->W1h) + u * n1, n1,
+                           cudaMemcpyHostToDevice, s),
+           "offload W1");
+        ck(cudaMemcpyAsync(static_cast<char*>(L->W2c) + slot * n2, static_cast<char*>(L->W2h) + u * n2, n2,
+                           cudaMemcpyHostToDevice, s),
+           "offload W2");
+        L->off_bytes += n1 + n2;
+    }
+    L->lru.swap(rest);
+    for (uint32_t g = 0; g < L->G; ++g) {
+        const int32_t sl = L->slot_of_unit[g / L->off_unit];
+        L->gmap_host[g] = sl < 0 ? 0u : static_cast<uint32_t>(sl) * L->off_unit + g % L->off_unit;
+    }
+    ck(cudaMemcpyAsync(L->gmap_dev, L->gmap_host, (size_t)L->G * 4, cudaMemcpyHostToDevice, s), "gmap");
+    L->off_misses += misses;
+    L->off_hits += req.size() - misses;
+    L->off_last_req = req;
+    L->off_last_misses = misses;
+}
+
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
                  cudaStream_t s, StageTimer& tm, bool check_finite = false, bool with_shared = false,
@@ -342,17 +445,20 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         tm.end(1, 2);
     }
     tm.begin(2);
+    if (L->offload) offload_step(L, s);  // transfers counted in the dispatch stage
     mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, L->x_perm, s, true);
     ck_launch("dispatch");
     tm.end(2, 1);
     mp::GemmShape g1{L->G, L->d_pad, 2 * L->w_pad, T * L->k_max, L->w_pad, 2 * L->w_pad};
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
+    const uint32_t* gmap = L->offload ? L->gmap_dev : nullptr;
     if (L->use_tc && L->tile256)
-        mp::launch_gemm_tc2(true, &L->tm_xperm, &L->tm_w1h, L->h, g1, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s,
-                            L->tile_mode != 3);
+        mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
+                            L->ws.mprefix_tc2, L->num_sms, s, L->tile_mode != 3, gmap);
     else if (L->use_tc)
-        mp::launch_gemm_tc(true, &L->tm_xperm, &L->tm_w1, L->h, g1, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
+        mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
+                           L->ws.mprefix_tc, L->num_sms, s, gmap);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
@@ -371,10 +477,13 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     tm.end(3, shared ? 2 : 1);
     tm.begin(4);
     if (L->use_tc && L->tile256)
-        mp::launch_gemm_tc2(false, &L->tm_h, &L->tm_w2h, L->o, g2, L->ws.offsets, L->ws.mprefix_tc2, L->num_sms, s,
-                            false);  // M=128 tail MMAs measured 2-8% slower in gemm2 (profiles/r01_tile_ab.txt)
+        mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
+                            L->ws.mprefix_tc2, L->num_sms, s,
+                            false,  // M=128 tail MMAs measured 2-8% slower in gemm2 (profiles/r01_tile_ab.txt)
+                            gmap);
     else if (L->use_tc)
-        mp::launch_gemm_tc(false, &L->tm_h, &L->tm_w2, L->o, g2, L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s);
+        mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
+                           L->ws.mprefix_tc, L->num_sms, s, gmap);
     else
         mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm2");
@@ -1166,6 +1275,7 @@ MP_API mp_status mp_layer_collect_activations(mp_layer_t L, uint32_t e, const vo
         if (!L->has_experts) fail(MP_ERR_VALIDATION, "router-only layer holds no expert weights");
         if (!L->packed[e]) fail(MP_ERR_VALIDATION, "expert " + std::to_string(e) + " is not ready");
         if (!L->use_tc) fail(MP_ERR_VALIDATION, "the activation profiler runs on the bf16 tensor-core layout");
+        if (L->offload) fail(MP_ERR_VALIDATION, "the activation profiler needs device-resident weights (offload on)");
         if (L->d % 8) fail(MP_ERR_VALIDATION, "the activation profiler needs d_model % 8 == 0");
         // inc/expert.hpp:141: an empty calibration list is a ValidationError
         if (B == 0) fail(MP_ERR_VALIDATION, "calibration input list is empty");
@@ -1249,5 +1359,70 @@ MP_API mp_status mp_format_read_mpam(const char* path, uint32_t* rows, uint32_t*
         *rows = r;
         *cols = c;
         if (data) std::memcpy(data, d.data(), d.size() * 4);
+    });
+}
+
+// ============================================================== offload
+MP_API mp_status mp_layer_enable_offload(mp_layer_t L, uint32_t unit_subexperts, uint32_t cache_units) {
+    return guarded([&] {
+        if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        if (L->offload) fail(MP_ERR_VALIDATION, "offload already enabled");
+        if (!L->use_tc || !L->has_experts || !L->has_router)
+            fail(MP_ERR_VALIDATION, "offload needs a full bf16 tensor-core layer");
+        if (unit_subexperts != 1 && unit_subexperts != L->S)
+            fail(MP_ERR_VALIDATION, "unit must be 1 sub-expert (fine) or S (monolithic expert)");
+        const uint32_t n_units = L->G / unit_subexperts;
+        if (cache_units < 1 || cache_units > n_units)
+            fail(MP_ERR_VALIDATION, "cache capacity must be in [1, " + std::to_string(n_units) + "] units");
+        check_ready(L);
+        DeviceGuard dg(L->desc.device);
+        ck(cudaDeviceSynchronize(), "sync");
+        const size_t w1 = (size_t)L->G * 2 * L->w_pad * L->d_pad * L->esz;
+        const size_t w2 = (size_t)L->G * L->d_pad * L->w_pad * L->esz;
+        const uint32_t cg = cache_units * unit_subexperts;  // cache groups
+        const size_t c1 = (size_t)cg * 2 * L->w_pad * L->d_pad * L->esz;
+        const uint32_t c2_rows = round_up(cg * L->d_pad, 256);
+        const size_t c2 = (size_t)c2_rows * L->w_pad * L->esz;
+        ck(cudaMallocHost(&L->W1h, w1), "pinned W1");
+        ck(cudaMallocHost(&L->W2h, w2), "pinned W2");
+        ck(cudaMemcpy(L->W1h, L->W1, w1, cudaMemcpyDeviceToHost), "W1 to host");
+        ck(cudaMemcpy(L->W2h, L->W2, w2, cudaMemcpyDeviceToHost), "W2 to host");
+        cudaFree(L->W1);
+        cudaFree(L->W2);
+        L->W1 = L->W2 = nullptr;  // the device now holds only the cache
+        L->W1c = dalloc<char>(c1, "W1 cache");
+        L->W2c = dalloc<char>(c2, "W2 cache");
+        ck(cudaMemset(L->W2c, 0, c2), "memset W2 cache");
+        L->gmap_dev = dalloc<uint32_t>(L->G, "gmap");
+        ck(cudaMallocHost(reinterpret_cast<void**>(&L->gmap_host), L->G * 4), "pinned gmap");
+        ck(cudaMallocHost(reinterpret_cast<void**>(&L->off_host), (L->G + 1) * 4), "pinned offsets");
+        const bool ok = mp::make_tmap_bf16_2d(&L->tm_w1c, L->W1c, (uint64_t)cg * 2 * L->w_pad, L->d_pad, 256, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_w1ch, L->W1c, (uint64_t)cg * 2 * L->w_pad, L->d_pad, 128, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_w2c, L->W2c, c2_rows, L->w_pad, 256, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_w2ch, L->W2c, c2_rows, L->w_pad, 128, 64);
+        if (!ok) fail(MP_ERR_CUDA, "offload cache tensor maps");
+        L->off_unit = unit_subexperts;
+        L->off_slots = cache_units;
+        L->slot_of_unit.assign(n_units, -1);
+        L->free_slots.clear();
+        for (uint32_t sl = cache_units; sl-- > 0;) L->free_slots.push_back(sl);  // slot 0 first
+        L->lru.clear();
+        L->off_hits = L->off_misses = L->off_bytes = 0;
+        L->offload = true;
+    });
+}
+
+MP_API mp_status mp_layer_offload_stats(mp_layer_t L, uint64_t* hits, uint64_t* misses, uint64_t* bytes_h2d,
+                                        uint32_t* last_units, uint32_t cap, uint32_t* n_last, uint32_t* last_misses) {
+    return guarded([&] {
+        if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        if (!L->offload) fail(MP_ERR_VALIDATION, "offload is not enabled");
+        if (hits) *hits = L->off_hits;
+        if (misses) *misses = L->off_misses;
+        if (bytes_h2d) *bytes_h2d = L->off_bytes;
+        if (n_last) *n_last = static_cast<uint32_t>(L->off_last_req.size());
+        if (last_misses) *last_misses = L->off_last_misses;
+        if (last_units)
+            for (size_t i = 0; i < L->off_last_req.size() && i < cap; ++i) last_units[i] = L->off_last_req[i];
     });
 }

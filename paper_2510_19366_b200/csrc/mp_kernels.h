@@ -112,8 +112,10 @@ void launch_gemm1_simt(int dtype, const void* A, const void* W1, void* H, const 
                        const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
 void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const GemmShape& sh,
                        const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
+// gmap (nullable): group g's weights are B group gmap[g] (offload cache slots)
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s);
+                    const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
+                    const uint32_t* gmap = nullptr);
 size_t gemm_tc_smem_bytes();
 // Epilogue modes of the 1-SM tensor-core GEMM (gemm_tc.cu).
 constexpr int kEpiPlain = 0;   // bf16 acc
@@ -123,13 +125,13 @@ constexpr int kEpiCount = 3;   // uint32 counts (co-activation of 0/1 operands)
 // b_row0: first B row; colmap: kEpiActAbs column map; out: bf16 / f32 / u32 per mode
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                        uint32_t b_row0 = 0, const int32_t* colmap = nullptr);
+                        uint32_t b_row0 = 0, const int32_t* colmap = nullptr, const uint32_t* gmap = nullptr);
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
-                     bool tail128 = true);
+                     bool tail128 = true, const uint32_t* gmap = nullptr);
 
 // Calibration (calib.cu).
 void launch_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,

@@ -104,6 +104,20 @@ class MoeLayer:
         """Fused residual: forward returns x + MoE(x) (bf16 layers; y must not alias x)."""
         check(self.lib.mp_layer_set_residual(self.h, int(on)))
 
+    def enable_offload(self, cache_units: int, monolithic: bool = False):
+        """Sub-expert offload cache (moe_layer.h): weights to pinned host memory,
+        a device LRU cache of cache_units units (sub-experts, or whole experts)."""
+        check(self.lib.mp_layer_enable_offload(self.h, self.S if monolithic else 1, cache_units))
+
+    def offload_stats(self):
+        """(hits, misses, bytes_h2d, last forward's requested units, last forward's misses)."""
+        h, m, b = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        n, lm = C.c_uint32(), C.c_uint32()
+        units = np.zeros(self.G, np.uint32)
+        check(self.lib.mp_layer_offload_stats(self.h, C.byref(h), C.byref(m), C.byref(b), units.ctypes.data, self.G,
+                                              C.byref(n), C.byref(lm)))
+        return h.value, m.value, b.value, units[:n.value].copy(), lm.value
+
     def set_gates(self, e: int, r: int, gates: Sequence[Sequence[int]]):
         off = np.zeros(len(gates) + 1, np.uint32)
         for s, g in enumerate(gates):

@@ -261,6 +261,7 @@ class RefLib:
         L.ref_binarize_topk.argtypes = [_f32p, _sz, _sz, _sz, C.c_void_p]
         L.ref_coactivation.argtypes = [C.c_void_p, _sz, _sz, _sz, _u32p]
         L.ref_save_activation_matrix.argtypes = [C.c_char_p, _sz, _sz, _f32p]
+        L.ref_offload_replay.argtypes = [C.c_uint32, C.c_uint32, _sz, _u32p, _u32p, _u64p]
         L.ref_load_activation_matrix.argtypes = [C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.c_void_p]
         L.ref_perf_table_eval.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_double), C.POINTER(_sz),
                                           C.POINTER(_sz)]
@@ -329,6 +330,17 @@ class RefLib:
         self._check(self.L.ref_load_activation_matrix(str(path).encode(), C.byref(r), C.byref(c), None))
         out = np.empty((r.value, c.value), np.float32)
         self._check(self.L.ref_load_activation_matrix(str(path).encode(), C.byref(r), C.byref(c), out.ctypes.data))
+        return out
+
+    def offload_replay(self, n_units, capacity, steps):
+        """Per-step miss counts of cache_step (inc/offload.hpp:202-255) over
+        the request sets `steps` (each ascending), cold start."""
+        off = np.zeros(len(steps) + 1, np.uint32)
+        for i, st in enumerate(steps):
+            off[i + 1] = off[i] + len(st)
+        ids = np.ascontiguousarray(np.concatenate([np.asarray(st, np.uint32) for st in steps]), np.uint32)
+        out = np.zeros(len(steps), np.uint64)
+        self._check(self.L.ref_offload_replay(n_units, capacity, len(steps), off, ids, out))
         return out
 
     def perf_table_eval(self, path, batch, k):
