@@ -122,6 +122,94 @@ __device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uin
     return k < G ? vk - vk1 : INFINITY;
 }
 
+// Fast selection for the tensor-core router: keys are the fp32-rounded logits
+// (rounding <= 2e-7 at |logit| < 4, inside the certification guard), packed
+// with the index into one order-preserving u64 (key bits high, ~index low:
+// larger packed value = larger key, then lower index), so each argmax step is
+// one 64-bit shuffle + max.  Weights use the fp64 logits `vals`.  Returns the
+// key gap between the k-th and (k+1)-th best (+inf when k == G); vk_out gets
+// both keys (as double).
+__device__ __forceinline__ uint64_t pack_key(float v, uint32_t g) {
+    uint32_t b = __float_as_uint(v);
+    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);  // order-preserving
+    return (static_cast<uint64_t>(b) << 32) | static_cast<uint32_t>(~g);
+}
+__device__ __forceinline__ float unpack_key(uint64_t p) {
+    uint32_t b = static_cast<uint32_t>(p >> 32);
+    b = (b & 0x80000000u) ? (b & 0x7FFFFFFFu) : ~b;
+    return __uint_as_float(b);
+}
+
+__device__ double warp_topk_fast(const double* __restrict__ vals, uint32_t G, uint32_t k, uint32_t k_max,
+                                 int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row,
+                                 double* vk_out) {
+    const uint32_t lane = lane_id();
+    constexpr int NC = kMaxG / 32;
+    const uint32_t nc = (G + 31) / 32;
+    uint64_t v[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const uint32_t g = lane + 32u * c;
+        v[c] = (c < (int)nc && g < G) ? pack_key(static_cast<float>(vals[g]), g) : 0ull;
+    }
+    uint32_t taken = 0;
+    uint64_t pk = 0, pk1 = 0;
+    const uint32_t rounds = k < G ? k + 1 : k;
+    for (uint32_t r = 0; r < rounds; ++r) {
+        uint64_t best = 0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (!((taken >> c) & 1u) && v[c] > best) best = v[c];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, best, off);
+            best = o > best ? o : best;
+        }
+        if (r == k) {
+            pk1 = best;
+            break;
+        }
+        pk = best;
+        const uint32_t g = ~static_cast<uint32_t>(best);
+        if ((g & 31u) == lane) taken |= 1u << (g >> 5);
+    }
+    const double vk = unpack_key(pk), vk1 = k < G ? (double)unpack_key(pk1) : -INFINITY;
+    if (vk_out && lane == 0) {
+        vk_out[0] = vk;
+        vk_out[1] = vk1;
+    }
+    double m = -DBL_MAX;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if ((taken >> c) & 1u) m = fmax(m, vals[lane + 32u * c]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    double z = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        if ((taken >> c) & 1u) z += exp(vals[lane + 32u * c] - m);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
+    uint32_t base = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (c >= (int)nc) break;
+        const bool mine = (taken >> c) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+        if (mine) {
+            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
+            sel_row[pos] = lane + 32u * c;
+            w_row[pos] = weight_mode == 1 ? static_cast<float>(exp(vals[lane + 32u * c] - m) / z) : 1.0f;
+        }
+        base += __popc(bal);
+    }
+    for (uint32_t j = k + lane; j < k_max; j += 32) {
+        sel_row[j] = kSelNone;
+        w_row[j] = 0.0f;
+    }
+    return k < G ? vk - vk1 : INFINITY;
+}
+
 __device__ __forceinline__ uint32_t token_k(const uint32_t* kpt, uint32_t k, uint32_t t, uint32_t k_max, uint32_t G,
                                             int* err) {
     uint32_t kt = kpt ? kpt[t] : k;
@@ -475,15 +563,27 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32
 __device__ double warp_exact_logit(const __nv_bfloat16* __restrict__ xr, const float* __restrict__ wrow, uint32_t d) {
     const uint32_t lane = lane_id();
     double acc[4] = {0, 0, 0, 0};
-    for (uint32_t i = 4 * lane; i < d; i += 128) {
-        const float4 wv = __ldg(reinterpret_cast<const float4*>(wrow + i));
-        const uint2 xv = __ldg(reinterpret_cast<const uint2*>(xr + i));
-        const float2 x01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.x));
-        const float2 x23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv.y));
-        acc[0] = fma((double)x01.x, (double)wv.x, acc[0]);
-        acc[1] = fma((double)x01.y, (double)wv.y, acc[1]);
-        acc[2] = fma((double)x23.x, (double)wv.z, acc[2]);
-        acc[3] = fma((double)x23.y, (double)wv.w, acc[3]);
+    // 4 independent 16-byte loads per lane in flight: this runs for a handful
+    // of (token, candidate) pairs per forward and is pure load latency
+    constexpr uint32_t U = 4;
+    for (uint32_t i0 = 4 * lane; i0 < d; i0 += U * 128) {
+        float4 wv[U];
+        uint2 xv[U];
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+            const uint32_t i = i0 + u * 128;
+            wv[u] = i < d ? __ldg(reinterpret_cast<const float4*>(wrow + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            xv[u] = i < d ? __ldg(reinterpret_cast<const uint2*>(xr + i)) : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+            const float2 x01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[u].x));
+            const float2 x23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xv[u].y));
+            acc[0] = fma((double)x01.x, (double)wv[u].x, acc[0]);
+            acc[1] = fma((double)x01.y, (double)wv[u].y, acc[1]);
+            acc[2] = fma((double)x23.x, (double)wv[u].z, acc[2]);
+            acc[3] = fma((double)x23.y, (double)wv[u].w, acc[3]);
+        }
     }
     double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
@@ -501,8 +601,9 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
 // Fused routing epilogue of the tensor-core router, CTA = 32 tokens (warp per
 // token), replacing partials_topk + router_fixup + bucket_local + bucket_scan:
 //   1. logits = fixed-order fp64 sum of the K-split partials, top-k, weights;
-//   2. near-tie certification: with a, b the k-th / (k+1)-th logits and
-//      |logit - exact| < guard, a gap a - b < 2 guard leaves only the window
+//   2. near-tie certification: with a, b the k-th / (k+1)-th selection keys
+//      (fp32-rounded tensor-core logits) and |key - exact| < guard, a gap
+//      a - b < 2 guard leaves only the window
 //      W = {g : b - 2 guard <= logit_g <= a + 2 guard} uncertain (above W:
 //      certainly selected, below: certainly not); W is recomputed in exact
 //      fp64 and the token re-selected on (+inf above W, exact in W, -inf
@@ -524,10 +625,18 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     __shared__ uint32_t msk[TB][kMaxG / 32];
     __shared__ uint16_t slot_of[TB][kMaxG];
     __shared__ uint32_t is_last;
+    constexpr uint32_t kMaxPairs = 1024, kPairBatch = 8;
+    __shared__ uint32_t n_pairs;
+    __shared__ uint32_t pair_tg[kMaxPairs];  // (token in CTA << 16) | candidate
+    __shared__ double pair_part[kPairBatch][4];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t t0 = blockIdx.x * TB, t = t0 + warp;
     const uint32_t words = (G + 31) / 32;
     for (uint32_t q = threadIdx.x; q < TB * words; q += blockDim.x) msk[q / words][q % words] = 0;
+    if (threadIdx.x == 0) n_pairs = 0;
+    __syncthreads();
+    bool flagged = false;
+    uint32_t kt = 0;
     if (t < T) {
         for (uint32_t g = lane; g < G; g += 32) {
             double v = 0.0;
@@ -535,32 +644,64 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
             sc[g] = v;
         }
         __syncwarp();
-        const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
-        const double gap = warp_topk_token(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
-                                           wout + (size_t)t * k_max, nullptr, vk[warp]);
+        kt = token_k(kpt, k_scalar, t, k_max, G, err);
+        const double gap = warp_topk_fast(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
+                                          wout + (size_t)t * k_max, vk[warp]);
         __syncwarp();
-        if (gap < 2.0 * guard) {
+        flagged = gap < 2.0 * guard;
+        if (flagged) {  // queue the uncertainty window for the CTA-wide exact pass
             const double a = vk[warp][0], b = vk[warp][1];
             for (uint32_t g0 = 0; g0 < G; g0 += 32) {
                 const uint32_t g = g0 + lane;
-                const double v = g < G ? sc[g] : -DBL_MAX;
+                const double v = g < G ? static_cast<double>(static_cast<float>(sc[g])) : -DBL_MAX;  // the keys
                 const bool in_w = g < G && v >= b - 2.0 * guard && v <= a + 2.0 * guard;
                 if (g < G) key[g] = v > a + 2.0 * guard ? DBL_MAX : (in_w ? v : -DBL_MAX);
-                uint32_t bal = __ballot_sync(0xffffffffu, in_w);
-                while (bal) {
-                    const uint32_t j = __ffs(bal) - 1;
-                    bal &= bal - 1;
-                    const double e = warp_exact_logit(x + (size_t)t * d, wrT + (size_t)(g0 + j) * d, d);
-                    if (lane == j) {
-                        key[g] = e;
-                        sc[g] = e;
-                    }
+                if (in_w) {
+                    const uint32_t slot = atomicAdd(&n_pairs, 1u);
+                    if (slot < kMaxPairs) pair_tg[slot] = (warp << 16) | g;
                 }
             }
-            __syncwarp();
-            warp_topk_token(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max, key);
-            if (lane == 0) atomicAdd(n_fixed, 1u);
         }
+    }
+    __syncthreads();
+    // exact fp64 logits of every queued (token, candidate), 4 warps per pair
+    // (d split in quarters, fixed-order combination: deterministic)
+    const uint32_t np = min(n_pairs, kMaxPairs);
+    if (np) {
+        for (uint32_t p0 = 0; p0 < np; p0 += 8) {
+            const uint32_t pi = p0 + warp / 4, qq = warp % 4;
+            if (pi < np) {
+                const uint32_t tl = pair_tg[pi] >> 16, g = pair_tg[pi] & 0xFFFFu;
+                const uint32_t dq = (d / 4 + 127) / 128 * 128;  // quarter, multiple of 128
+                const uint32_t lo = qq * dq, hi = min(d, lo + dq);
+                const double part = lo < hi ? warp_exact_logit(x + (size_t)(t0 + tl) * d + lo,
+                                                               wrT + (size_t)g * d + lo, hi - lo)
+                                            : 0.0;
+                if (lane == 0) pair_part[pi % kPairBatch][qq] = part;
+            }
+            __syncthreads();
+            for (uint32_t q2 = threadIdx.x; q2 < 8 && p0 + q2 < np; q2 += blockDim.x) {
+                const uint32_t pj = p0 + q2, tl = pair_tg[pj] >> 16, g = pair_tg[pj] & 0xFFFFu;
+                const double* pp = pair_part[pj % kPairBatch];
+                const double e = ((pp[0] + pp[1]) + pp[2]) + pp[3];
+                rsm[(size_t)(TB + tl) * G + g] = e;  // key
+                rsm[(size_t)tl * G + g] = e;         // logit (weights)
+            }
+            __syncthreads();
+        }
+    }
+    if (flagged) {
+        if (n_pairs > kMaxPairs) {  // overflow (only with an absurd guard): serial exact pass
+            for (uint32_t g = 0; g < G; ++g)
+                if (key[g] != DBL_MAX && key[g] != -DBL_MAX) {
+                    const double e = warp_exact_logit(x + (size_t)t * d, wrT + (size_t)g * d, d);
+                    if (lane == 0) key[g] = sc[g] = e;
+                    __syncwarp();
+                }
+        }
+        __syncwarp();
+        warp_topk_token(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max, key);
+        if (lane == 0) atomicAdd(n_fixed, 1u);
     }
     __syncthreads();  // this CTA's selections are visible to the CTA
     for (uint32_t q = threadIdx.x; q < TB * k_max; q += blockDim.x) {
@@ -623,26 +764,42 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
     const Tx* xr = x + (size_t)t * d;
     bool bad = false;
     if (!x_perm && !check_finite) return;  // tables only: the GEMM gathers the rows itself
-    // each 16-byte chunk of the row is read once and stored to every bucket
-    for (uint32_t c0 = 0; c0 < d_pad; c0 += 32 * VE) {
-        const uint32_t c = c0 + lane * VE;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (vec_ok) {
-            if (c < d) v = __ldg(reinterpret_cast<const uint4*>(xr + c));
-        } else {
-            Tx tmp[VE];
+    // each 16-byte chunk of the row is read once and stored to every bucket;
+    // U chunks per lane in flight (memory-level parallelism of the HBM-bound copy)
+    constexpr uint32_t U = 4;
+    for (uint32_t c0 = 0; c0 < d_pad; c0 += U * 32 * VE) {
+        uint4 v[U];
 #pragma unroll
-            for (uint32_t q = 0; q < VE; ++q) tmp[q] = (c + q < d) ? xr[c + q] : from_f32<Tx>(0.0f);
-            v = *reinterpret_cast<uint4*>(tmp);
+        for (uint32_t u = 0; u < U; ++u) {
+            const uint32_t c = c0 + (u * 32 + lane) * VE;
+            v[u] = make_uint4(0, 0, 0, 0);
+            if (vec_ok) {
+                if (c < d) v[u] = __ldg(reinterpret_cast<const uint4*>(xr + c));
+            } else {
+                Tx tmp[VE];
+#pragma unroll
+                for (uint32_t q = 0; q < VE; ++q) tmp[q] = (c + q < d) ? xr[c + q] : from_f32<Tx>(0.0f);
+                v[u] = *reinterpret_cast<uint4*>(tmp);
+            }
         }
-        const Tx* tv = reinterpret_cast<const Tx*>(&v);
+        if (check_finite) {
 #pragma unroll
-        for (uint32_t q = 0; q < VE; ++q) bad |= !isfinite(to_f32(tv[q]));
+            for (uint32_t u = 0; u < U; ++u) {
+                const Tx* tv = reinterpret_cast<const Tx*>(&v[u]);
+#pragma unroll
+                for (uint32_t q = 0; q < VE; ++q) bad |= !isfinite(to_f32(tv[q]));
+            }
+        }
         if (!x_perm) continue;
         for (uint32_t j = 0; j < k_max; ++j) {
             const uint32_t pos = __shfl_sync(0xffffffffu, j < 32 ? pos_a : pos_b, j & 31);
             if (pos == kSelNone) continue;
-            if (c < d_pad) *reinterpret_cast<uint4*>(x_perm + (size_t)pos * d_pad + c) = v;
+            Tx* dst = x_perm + (size_t)pos * d_pad;
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+                const uint32_t c = c0 + (u * 32 + lane) * VE;
+                if (c < d_pad) *reinterpret_cast<uint4*>(dst + c) = v[u];
+            }
         }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0 && err) atomicOr(err, 2);
