@@ -387,7 +387,7 @@ uint64_t* gemm_trace_buffer(bool swiglu) {
     }();
     if (!on) return nullptr;
     uint64_t*& b = g_trace[swiglu ? 0 : 1];
-    if (!b) cudaMalloc(&b, 1024 * 4 * sizeof(uint64_t));
+    if (!b) cudaMalloc(&b, (4096 + 128 * 128 * 4) * sizeof(uint64_t));  // + per-tile records (pair kernel)
     return b;
 }
 uint64_t* gemm_trace_ptr(int which) { return g_trace[which & 1]; }

@@ -18,12 +18,17 @@
 //   gemm2: B tile = W2 rows n*256 .. +255 = output columns; CTA r loads its half.
 // Tiles are (g, n, m) with 256-row m tiles (prefix of ceil(count_g / 256)),
 // m fastest, strided over the clusters of a persistent grid.  Rows past the
-// group end are computed and discarded (masked stores).  A tile with at most
-// 128 valid rows (the tail of a group) issues M=128 pair MMAs instead: 64
-// rows per CTA at half the MMA time, the accumulator in the 2x2 layout (rows
-// in lanes 0-63 with D columns [0,128), the same rows in lanes 64-127 with D
-// columns [128,256)).  With the 64-row gate/up interleave of W1 (kIlv) both
-// halves of a neuron's SwiGLU stay in one lane in either shape.
+// group end are computed and discarded (masked stores).  Optional (tail128,
+// off by default): a tile with at most 128 valid rows (the tail of a group)
+// issues M=128 pair MMAs with 64-row A loads, the accumulator in the 2x2
+// layout (rows in lanes 0-63 with D columns [0,128), the same rows in lanes
+// 64-127 with D columns [128,256)); with the 64-row gate/up interleave of W1
+// (kIlv) both halves of a neuron's SwiGLU stay in one lane in either shape.
+// Measured (per-tile MMA-issuer trace, tests/probes/tile_trace.py): tail
+// tiles take the SAME cycles as full ones (the pipeline runs at ~580 cycles
+// per k-block either way: 510 of MMA issue + ~70 of operand waits), and the
+// step is 4% slower with them (profiles/r01_tile_ab.txt), so tails run as
+// full 256-row tiles.
 //
 // Barriers: full[s] lives in the leader CTA (both CTAs' TMA loads complete_tx
 // on it; the leader's expect_tx covers both); empty[s], tfull[a] are signalled
@@ -157,7 +162,8 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
 
 template <bool SWIGLU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, PairParams p) {
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmA64, PairParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
@@ -190,6 +196,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
+        if (p.tail128) tma_prefetch_desc(&tmA64);
         tma_prefetch_desc(&tmB);
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot);
@@ -216,12 +223,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const bool tail = p.tail128 && s_off[g + 1] - s_off[g] - m * BM <= HM;  // M=128: 64 rows per CTA
                 const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * (tail ? HM / 2 : HM));
                 const int32_t brow = static_cast<int32_t>(s_gmap[g] * p.N_group + n * BN + rank * 128);
+                // the GEMM is bound by the operand feed (L2 -> SM), so a tail tile
+                // loads only the 64 A rows per CTA its M=128 MMA reads
+                const CUtensorMap* tA = tail ? &tmA64 : &tmA;
+                const uint32_t tx = 2 * (tail ? A_BYTES / 2 + B_BYTES : STAGE_BYTES);
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
-                    if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+                    if (rank == 0) mbar_expect_tx(&full[s], tx);
                     const uint32_t fb = full_leader + s * 8;
-                    tma_load_2d_pair(sA + s * A_BYTES, &tmA, fb, static_cast<int32_t>(kb * BK), arow);
+                    tma_load_2d_pair(sA + s * A_BYTES, tA, fb, static_cast<int32_t>(kb * BK), arow);
                     tma_load_2d_pair(sB + s * B_BYTES, &tmB, fb, static_cast<int32_t>(kb * BK), brow);
                 }
             }
@@ -246,6 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 mbar_wait_cluster(&tempty[acc], aph ^ 1u);
 #if MP_PAIR_TRACE
                 w_acc += clock64() - t0;
+                const uint64_t t_tile = clock64(), wf0 = w_full;
 #endif
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -268,6 +280,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     umma_commit_pair(&empty[s]);
                 }
                 umma_commit_pair(&tfull[acc]);
+#if MP_PAIR_TRACE
+                if (p.trace && tc < 128) {  // per-tile record: tile, operand waits, MMA-phase cycles, tail
+                    uint64_t* r = p.trace + 4096 + ((size_t)pair * 128 + tc) * 4;
+                    r[0] = tile;
+                    r[1] = w_full - wf0;
+                    r[2] = clock64() - t_tile;
+                    r[3] = idesc == idesc_tail;
+                }
+#endif
             }
 #if MP_PAIR_TRACE
             if (p.trace) {
@@ -372,10 +393,11 @@ size_t gemm_pair_smem_bytes() { return kSmemBytes; }
 // tmB: box of 128 rows (each CTA loads half of the 256-row B tile)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s, bool tail128,
-                     const uint32_t* gmap) {
+                     const uint32_t* gmap, const CUtensorMap* tmA64) {
+    if (!tmA64) tail128 = false;  // tails need the 64-row A box
     PairParams p{sh.G, sh.K, sh.N_group, sh.n_valid, sh.ld_out, (sh.N_group + BN - 1) / BN, offsets, mprefix256,
                  static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), tail128 ? 1u : 0u, gmap};
-    if (p.trace) cudaMemsetAsync(p.trace, 0, 1024 * 4 * sizeof(uint64_t), s);
+    if (p.trace) cudaMemsetAsync(p.trace, 0, (4096 + 128 * 128 * 4) * sizeof(uint64_t), s);
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;
     if (max_tiles < pairs) pairs = max_tiles;
@@ -387,9 +409,9 @@ void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB
         attr_set = true;
     }
     if (swiglu)
-        gemm_pair_kernel<true><<<2 * pairs, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+        gemm_pair_kernel<true><<<2 * pairs, kThreads, kSmemBytes, s>>>(*tmA, *tmB, tmA64 ? *tmA64 : *tmA, p);
     else
-        gemm_pair_kernel<false><<<2 * pairs, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p);
+        gemm_pair_kernel<false><<<2 * pairs, kThreads, kSmemBytes, s>>>(*tmA, *tmB, tmA64 ? *tmA64 : *tmA, p);
 }
 
 }  // namespace mp

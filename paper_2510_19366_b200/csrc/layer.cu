@@ -148,6 +148,7 @@ struct mp_layer_s {
     void* y_stage = nullptr;
     CUtensorMap tm_xperm{}, tm_h{}, tm_w1{}, tm_w2{};
     CUtensorMap tm_w1h{}, tm_w2h{};  // 128-row boxes: each CTA of a pair loads half a B tile
+    CUtensorMap tm_xperm64{}, tm_h64{};  // 64-row A boxes: M=128 tail tiles of the pair GEMM
 
     // shared (always-on) expert, Qwen-style: one dense group of sh_w_pad neurons
     uint32_t sh_ff = 0, sh_w_pad = 0, sh_w2_rows = 0;
@@ -455,7 +456,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     const uint32_t* gmap = L->offload ? L->gmap_dev : nullptr;
     if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
-                            L->ws.mprefix_tc2, L->num_sms, s, L->tile_mode != 3, gmap);
+                            L->ws.mprefix_tc2, L->num_sms, s, L->tile_mode == 4, gmap, &L->tm_xperm64);
     else if (L->use_tc)
         mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
                            L->ws.mprefix_tc, L->num_sms, s, gmap);
@@ -479,8 +480,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
                             L->ws.mprefix_tc2, L->num_sms, s,
-                            false,  // M=128 tail MMAs measured 2-8% slower in gemm2 (profiles/r01_tile_ab.txt)
-                            gmap);
+                            L->tile_mode == 4, gmap, &L->tm_h64);
     else if (L->use_tc)
         mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
                            L->ws.mprefix_tc, L->num_sms, s, gmap);
@@ -641,7 +641,11 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             if (const char* env = std::getenv("MOEPRISM_BF16_GEMM"))
                 if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
             if (const char* env = std::getenv("MOEPRISM_TC_TILE"))
-                L->tile_mode = std::string(env) == "256" ? 2 : std::string(env) == "128" ? 1 : 0;
+                L->tile_mode = std::string(env) == "256"           ? 2
+                               : std::string(env) == "128"         ? 1
+                               : std::string(env) == "256-notail"  ? 3
+                               : std::string(env) == "256-tail128" ? 4
+                                                                   : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
             L->d_pad = round_up(L->d, 64);
@@ -720,7 +724,9 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                         mp::make_tmap_bf16_2d(&L->tm_h, L->h, L->rows_cap, L->w_pad, 128, 64) &&
                         mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64) &&
                         mp::make_tmap_bf16_2d(&L->tm_w1h, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 128, 64) &&
-                        mp::make_tmap_bf16_2d(&L->tm_w2h, L->W2, L->w2_rows, L->w_pad, 128, 64);
+                        mp::make_tmap_bf16_2d(&L->tm_w2h, L->W2, L->w2_rows, L->w_pad, 128, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_xperm64, L->x_perm, L->rows_cap, L->d_pad, 64, 64) &&
+                        mp::make_tmap_bf16_2d(&L->tm_h64, L->h, L->rows_cap, L->w_pad, 64, 64);
                     if (!ok) fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                 }
             }
@@ -1254,11 +1260,13 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
 
 // Diagnostics (not in the public header): grouped-GEMM kernel choice of a
 // layer at run time, 0 auto / 1 one-SM 128-row tiles / 2 CTA-pair 256-row
-// tiles / 3 CTA pairs without the M=128 tail MMA, for in-process A/B timing
+// tiles (full 256-row tails, the default) / 3 the same / 4 pairs with M=128
+// tail MMAs (64-row A loads; measured 4% slower per step at k=8/16, higher
+// power: profiles/r01_tile_ab.txt), for in-process A/B timing
 // (tests/probes/tile_ab.py).
 MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {
-        if (!L || mode < 0 || mode > 3) fail(MP_ERR_VALIDATION, "bad argument");
+        if (!L || mode < 0 || mode > 4) fail(MP_ERR_VALIDATION, "bad argument");
         L->tile_mode = mode;
     });
 }

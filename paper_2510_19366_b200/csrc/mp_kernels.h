@@ -131,7 +131,7 @@ uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
-                     bool tail128 = true, const uint32_t* gmap = nullptr);
+                     bool tail128 = true, const uint32_t* gmap = nullptr, const CUtensorMap* tmA64 = nullptr);
 
 // Calibration (calib.cu).
 void launch_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,

@@ -83,7 +83,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     tc_fence_after();
     const uint32_t tmem = tmem_slot;
-    if (threadIdx.x == 0 && rank == 0) {
+    if (threadIdx.x == 0 && rank == 0 && m == 0) {
+        // mixed shapes: blocks of 112 MMAs alternating M=256 (acc 0) and M=128 (acc 256)
+        const uint32_t i256 = umma_idesc_bf16(256, 256), i128 = umma_idesc_bf16(128, 256);
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+        uint64_t t0 = clock64();
+        for (uint32_t it = 0; it < iters / 28; ++it) {
+            const uint32_t idesc = (it & 1u) ? i128 : i256;
+            const uint32_t d = tmem + ((it & 1u) ? 256 : 0);
+            for (uint32_t kb = 0; kb < 28; ++kb)
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                        "l"(umma_desc_sw128(a0 + k * 32)), "l"(umma_desc_sw128(b0 + k * 32)), "r"(idesc), "r"(1u)
+                        : "memory");
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(&bar)),
+            "h"(static_cast<uint16_t>(1))
+            : "memory");
+        mbar_wait(&bar, 0);
+        out[blockIdx.x] = clock64() - t0;
+    } else if (threadIdx.x == 0 && rank == 0) {
         const uint32_t idesc = umma_idesc_bf16(m, 256);
         const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
         uint64_t t0 = clock64();
@@ -145,7 +169,8 @@ int main() {
     cudaFuncSetAttribute(mma_cost_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     printf("pair: M,accumulators,cycles_per_mma (N=256),floor\n");
     for (uint32_t two = 0; two < 2; ++two)
-        for (uint32_t m : {128u, 256u}) {
+        for (uint32_t m : {128u, 256u, 0u}) {
+            if (m == 0 && two) continue;
             cudaMemset(d_out, 0, sms * 8);
             mma_cost_pair_kernel<<<sms, 128, smem>>>(m, two, iters, d_out);
             cudaError_t e = cudaDeviceSynchronize();
@@ -160,7 +185,11 @@ int main() {
             for (auto v : h)
                 if (v) mean += v, ++n;
             mean /= n;
-            printf("%u,%u,%.1f,%.1f\n", m, two + 1, mean / (double(iters) * 4), m * 256.0 / 512);
+            if (m == 0)  // alternating blocks: expected (128 + 64) / 2 = 96 cycles per MMA
+                printf("alternating M=256/M=128 blocks,%.1f cycles per MMA (96 expected)\n",
+                       mean / (double(iters / 28 * 28) * 4));
+            else
+                printf("%u,%u,%.1f,%.1f\n", m, two + 1, mean / (double(iters) * 4), m * 256.0 / 512);
         }
     return 0;
 }

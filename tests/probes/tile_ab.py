@@ -19,11 +19,11 @@ L, xs = bench.build_layer(0, 4096, 16)
 lib = _lib.load()
 lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
 y = torch.empty((4096, bench.D), dtype=torch.bfloat16, device='cuda')
-names = {1: "128-row", 2: "pair", 3: "pair-no-tail128"}
+names = {1: "128-row", 2: "pair", 3: "pair-no-tail128", 4: "pair-tail128-both"}
 modes = [int(a) for a in (sys.argv[2] if len(sys.argv) > 2 else "1,2,3").split(",")]
 for k in [int(a) for a in (sys.argv[1] if len(sys.argv) > 1 else "2,4,8,16").split(",")]:
     res = {m: {"step": [], "gemm1": [], "gemm2": [], "mhz": []} for m in modes}
-    for rep in range(6):
+    for rep in range(int(sys.argv[3]) if len(sys.argv) > 3 else 6):
         for mode in modes:
             _lib.check(lib.mp_debug_set_tile_mode(L.h, mode))
             ms = bench.time_steps(lambda i: L.forward(xs[i % 8], k=k, y=y), 20, 3, 1)
