@@ -303,17 +303,14 @@ def bench_stack(pk, n_layers=32, T=4096, ks=(2, 8), steps=10):
 QW = {"E": 60, "S": 4, "d": 2048, "ff": 1408, "ff_sh": 5632}
 
 
-def bench_qwen(pk, steps=30):
-    """BASELINE configs[3] / SURVEY 8(d) C4: Qwen1.5-MoE-A2.7B layer shape (60
-    experts x 4 sub-experts of w=352, E*S=240, plus the always-on shared expert
-    ffn=5632 with a sigmoid gate), decode T=64 and prefill T=8192."""
-    import numpy as np
+def build_qwen_layer(max_tokens):
+    """The Qwen1.5-MoE-A2.7B-shape layer of BASELINE configs[3] (random init,
+    counter-based stream): 60 experts x 4 sub-experts + the shared expert."""
     import torch
     from paper_2510_19366_b200 import MoeLayer, synth_fill
     q = QW
     Eq, Sq, d, ff, ffs = q["E"], q["S"], q["d"], q["ff"], q["ff_sh"]
-    w = ff // Sq
-    L = MoeLayer(Eq, Sq, d, ff, dtype="bf16", k_max=16, max_tokens=8192)
+    L = MoeLayer(Eq, Sq, d, ff, dtype="bf16", k_max=16, max_tokens=max_tokens)
     buf = [torch.empty(d * ff, dtype=torch.float32, device="cuda") for _ in range(3)]
     for e in range(Eq):
         for m, (seed, scale) in enumerate(((300 + 3 * e, 1 / math.sqrt(d)), (301 + 3 * e, 1 / math.sqrt(d)),
@@ -328,6 +325,20 @@ def bench_qwen(pk, steps=30):
     wr = synth_fill(torch.empty(d * Eq * Sq, dtype=torch.float32, device="cuda"), 17, 1 / math.sqrt(d))
     L.set_router(wr)
     del buf, sh
+    return L
+
+
+def bench_qwen(pk, steps=30):
+    """BASELINE configs[3] / SURVEY 8(d) C4: Qwen1.5-MoE-A2.7B layer shape (60
+    experts x 4 sub-experts of w=352, E*S=240, plus the always-on shared expert
+    ffn=5632 with a sigmoid gate), decode T=64 and prefill T=8192."""
+    import numpy as np
+    import torch
+    from paper_2510_19366_b200 import MoeLayer, synth_fill
+    q = QW
+    Eq, Sq, d, ff, ffs = q["E"], q["S"], q["d"], q["ff"], q["ff_sh"]
+    w = ff // Sq
+    L = build_qwen_layer(8192)
     out = []
     for T in (64, 8192):
         xs = [synth_fill(torch.empty((T, d), dtype=torch.bfloat16, device="cuda"), 19 + 1000 * i, 1.0)

@@ -160,6 +160,8 @@ struct mp_layer_s {
     float* sh_w = nullptr;     // [max_tokens]
     uint32_t* sh_meta = nullptr;  // offsets {0, T}, tile prefixes {0, ceil(T/128)}, {0, ceil(T/256)}
     CUtensorMap tm_w1s{}, tm_w2s{}, tm_hs{}, tm_w1sh{}, tm_w2sh{};
+    cudaStream_t sh_stream = nullptr;  // side stream of the shared expert
+    cudaEvent_t sh_fork = nullptr, sh_join = nullptr;
 
     bool residual = false;  // mp_layer_set_residual: y = x + MoE(x), fused into the combine
     uint32_t* cal_meta = nullptr;  // calibration GEMM group offsets / tile prefix
@@ -210,6 +212,9 @@ void free_layer(mp_layer_s* L) {
                     L->sh_o, L->sh_w, L->sh_meta, L->cal_meta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    if (L->sh_stream) cudaStreamDestroy(L->sh_stream);
+    if (L->sh_fork) cudaEventDestroy(L->sh_fork);
+    if (L->sh_join) cudaEventDestroy(L->sh_join);
     for (void* p : {L->W1c, L->W2c, static_cast<void*>(L->gmap_dev)})
         if (p) cudaFree(p);
     for (void* p : {L->W1h, L->W2h, static_cast<void*>(L->gmap_host), static_cast<void*>(L->off_host)})
@@ -427,6 +432,33 @@ void offload_step(mp_layer_s* L, cudaStream_t s) {
     L->off_last_misses = misses;
 }
 
+// The shared expert does not depend on the routing: it runs on a side stream
+// forked from the forward's stream (gate -> gemm1 -> gemm2), overlapping the
+// router / bucketing / dispatch / routed GEMMs, and the combine joins it.
+// Fork / join are events, so the forward stays graph-capturable.
+void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t s) {
+    ck(cudaEventRecord(L->sh_fork, s), "fork shared expert");
+    ck(cudaStreamWaitEvent(L->sh_stream, L->sh_fork, 0), "fork shared expert");
+    cudaStream_t ss = L->sh_stream;
+    mp::launch_shared_gate(x, T, L->d, L->sh_gate, L->sh_w, L->sh_meta, L->sh_meta + 2, ss);
+    CUtensorMap tmX;
+    if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "shared expert tensor map");
+    const bool sh_pair = L->tile_mode >= 2 || (L->tile_mode == 0 && T >= 192);
+    mp::GemmShape s1{1, L->d_pad, 2 * L->sh_w_pad, T, L->sh_w_pad, 2 * L->sh_w_pad};
+    mp::GemmShape s2{1, L->sh_w_pad, L->d_pad, T, L->d_pad, L->d_pad};
+    if (sh_pair) {
+        mp::launch_gemm_tc2(true, &tmX, &L->tm_w1sh, L->sh_h, s1, L->sh_meta, L->sh_meta + 4, L->num_sms, ss, false);
+        mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, ss,
+                            false);
+    } else {
+        mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
+        mp::launch_gemm_tc(false, &L->tm_hs, &L->tm_w2s, L->sh_o, s2, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
+    }
+    ck_launch("shared expert");
+    ck(cudaEventRecord(L->sh_join, ss), "join shared expert");
+    L->launches += 3;
+}
+
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
                  cudaStream_t s, StageTimer& tm, bool check_finite = false, bool with_shared = false,
@@ -464,18 +496,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
     const bool shared = with_shared && L->sh_ff;
-    const bool sh_pair = L->tile_mode == 2 || (L->tile_mode == 0 && T >= 192);
-    if (shared) {  // shared expert: A = x itself (every token), one group
-        CUtensorMap tmX;
-        if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "shared expert tensor map");
-        mp::GemmShape s1{1, L->d_pad, 2 * L->sh_w_pad, T, L->sh_w_pad, 2 * L->sh_w_pad};
-        if (sh_pair)
-            mp::launch_gemm_tc2(true, &tmX, &L->tm_w1sh, L->sh_h, s1, L->sh_meta, L->sh_meta + 4, L->num_sms, s);
-        else
-            mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, L->num_sms, s);
-        ck_launch("shared gemm1");
-    }
-    tm.end(3, shared ? 2 : 1);
+    tm.end(3, 1);
     tm.begin(4);
     if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
@@ -487,15 +508,8 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     else
         mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm2");
-    if (shared) {
-        mp::GemmShape s2{1, L->sh_w_pad, L->d_pad, T, L->d_pad, L->d_pad};
-        if (sh_pair)
-            mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, s, false);
-        else
-            mp::launch_gemm_tc(false, &L->tm_hs, &L->tm_w2s, L->sh_o, s2, L->sh_meta, L->sh_meta + 2, L->num_sms, s);
-        ck_launch("shared gemm2");
-    }
-    tm.end(4, shared ? 2 : 1);
+    tm.end(4, 1);
+    if (shared) ck(cudaStreamWaitEvent(s, L->sh_join, 0), "join shared expert");
     tm.begin(5);
     const uint32_t group_S = unit ? L->S : 0;
     mp::launch_combine(L->dtype, L->o, L->d, L->d_pad, L->ws.slot_row, sel, w, L->k_max, group_S, T, y, s,
@@ -516,8 +530,7 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
     tm.begin(0);
     if (with_shared && L->sh_ff) {
         if (reinterpret_cast<uintptr_t>(x) % 16) fail(MP_ERR_VALIDATION, "shared expert needs 16-byte aligned x");
-        mp::launch_shared_gate(x, T, L->d, L->sh_gate, L->sh_w, L->sh_meta, L->sh_meta + 2, s);
-        L->launches += 1;
+        launch_shared_expert(L, x, T, s);
     }
     if (L->desc.router_mode == MP_ROUTER_PROXY) {
         pack_gates(L);
@@ -918,6 +931,9 @@ MP_API mp_status mp_layer_set_shared_expert(mp_layer_t L, uint32_t ff_sh, const 
                       mp::make_tmap_bf16_2d(&L->tm_w1sh, L->W1s, 2ull * w_pad, L->d_pad, 128, 64) &&
                       mp::make_tmap_bf16_2d(&L->tm_w2sh, L->W2s, w2_rows, w_pad, 128, 64);
             if (!ok) fail(MP_ERR_CUDA, "shared expert tensor maps");
+            ck(cudaStreamCreateWithFlags(&L->sh_stream, cudaStreamNonBlocking), "shared expert stream");
+            ck(cudaEventCreateWithFlags(&L->sh_fork, cudaEventDisableTiming), "shared expert event");
+            ck(cudaEventCreateWithFlags(&L->sh_join, cudaEventDisableTiming), "shared expert event");
             ck(cudaDeviceSynchronize(), "shared pack");
         } catch (...) {
             cudaFree(raw);
