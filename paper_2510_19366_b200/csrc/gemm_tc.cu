@@ -69,6 +69,7 @@ struct TcParams {
     uint64_t* trace;  // [grid][4] MMA-issuer timing (diagnostics) or null
     uint32_t b_row0;  // first B row (calibration: one expert of the packed W1)
     const uint32_t* gmap;  // nullable: B group of group g (sub-expert offload cache slot), else g
+    const uint32_t* starts;  // nullable: group g's rows are [starts[g], offsets[g+1]) (split-schedule tails)
     // kEpiActAbs: fp32 |SwiGLU| of packed neuron q to column colmap[q] (< 0: padding)
     // kEpiCount:  uint32(acc) (exact 0/1 co-activation counts)
     const int32_t* colmap;
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ uint32_t s_prefix[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
     __shared__ uint32_t s_gmap[kMaxG];
+    __shared__ uint32_t s_start[kMaxG];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sB = base;                 // NB x 32 KB (1024-aligned)
     uint8_t* sA = base + NB * B_BYTES;  // NA x 16 KB
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_prefix[q] = p.mprefix[q];
         s_off[q] = p.offsets[q];
         if (q < p.G) s_gmap[q] = p.gmap ? p.gmap[q] : q;
+        if (q < p.G) s_start[q] = p.starts ? p.starts[q] : p.offsets[q];
     }
     tc_fence_before();
     __syncthreads();
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (c.tile >= total) return;
                 uint32_t g, m, n;
                 map_tile(c.tile, s_prefix, p.G, p.NT, g, m, n);
-                c.row = is_a ? static_cast<int32_t>(s_off[g] + m * BM)
+                c.row = is_a ? static_cast<int32_t>(s_start[g] + m * BM)
                              : static_cast<int32_t>(p.b_row0 + s_gmap[g] * p.N_group + n * BN);
             };
             auto advance = [&](Cursor& c, bool is_a) {
@@ -256,12 +259,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
             const uint32_t row_local = m * BM + q * 32 + lane;
-            const bool valid = row_local < s_off[g + 1] - s_off[g];
-            __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
+            const bool valid = row_local < s_off[g + 1] - s_start[g];
+            __nv_bfloat16* orow = p.out + static_cast<size_t>(s_start[g] + row_local) * p.ld_out;
             const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN;
             if constexpr (EPI == kEpiActAbs) {
                 // calibration profiler: |a| in the original neuron order
-                float* arow = static_cast<float*>(p.out32) + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
+                float* arow = static_cast<float*>(p.out32) + static_cast<size_t>(s_start[g] + row_local) * p.ld_out;
 #pragma unroll 1
                 for (uint32_t c = 0; c < 4; ++c) {
                     const uint32_t gcol = (c >> 1) * 128 + (c & 1u) * 32;
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             } else if constexpr (EPI == kEpiCount) {
-                uint32_t* crow = static_cast<uint32_t*>(p.out32) + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
+                uint32_t* crow = static_cast<uint32_t*>(p.out32) + static_cast<size_t>(s_start[g] + row_local) * p.ld_out;
 #pragma unroll 1
                 for (uint32_t c = 0; c < BN / 32; ++c) {
                     uint32_t r[32];
@@ -407,14 +410,14 @@ bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t
 
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                    const uint32_t* gmap) {
+                    const uint32_t* gmap, const uint32_t* starts) {
     launch_gemm_tc_epi(swiglu ? kEpiSwiglu : kEpiPlain, tmA, tmB, out, sh, offsets, mprefix, num_sms, s, 0, nullptr,
-                       gmap);
+                       gmap, starts);
 }
 
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                        uint32_t b_row0, const int32_t* colmap, const uint32_t* gmap) {
+                        uint32_t b_row0, const int32_t* colmap, const uint32_t* gmap, const uint32_t* starts) {
     const bool swiglu = epi == kEpiSwiglu;
     TcParams p;
     p.G = sh.G;
@@ -429,6 +432,7 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.trace = (epi == kEpiSwiglu || epi == kEpiPlain) ? gemm_trace_buffer(swiglu) : nullptr;
     p.b_row0 = b_row0;
     p.gmap = gmap;
+    p.starts = starts;
     p.colmap = colmap;
     p.out32 = out;
 

@@ -466,8 +466,11 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     // CTA-pair tiles pay up to 255 wasted rows per (sub-expert, N tile) against
     // 127 for 128-row tiles; measured break-even near 192 rows per bucket
     // (Mixtral shape: pairs win at k >= 4, lose at k = 2).  Per-token k: k_max.
+    // The split schedule (1-SM tail tiles) pays off from ~384 rows per bucket
+    // (k=8/16: 10-13% per step; k=4: 4% slower -- profiles/r01_tile_ab.txt).
+    double rows = 0.0;
     {
-        const double rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
+        rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
         L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && rows >= 192.0);
     }
     if (!bucketed) {
@@ -486,29 +489,43 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
     const uint32_t* gmap = L->offload ? L->gmap_dev : nullptr;
-    if (L->use_tc && L->tile256)
+    // split schedule (default with pairs): full 256-row blocks (and remainders
+    // > 128 rows) on CTA pairs, remainders <= 128 rows as 128-row tiles on the
+    // 1-SM kernel -- a tail then costs one SM instead of two
+    const bool split = L->tile_mode == 2 || L->tile_mode == 3 || L->tile_mode == 4 || (L->tile_mode == 0 && rows >= 384.0);
+    const uint32_t G1 = L->G + 1;
+    const uint32_t* pre_pair = L->ws.mprefix_tc2 + (split ? G1 : 0);
+    const uint32_t* pre_tail = L->ws.mprefix_tc2 + 2 * G1;
+    const uint32_t* tail_start = L->ws.mprefix_tc2 + 3 * G1;
+    if (L->use_tc && L->tile256) {
         mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
-                            L->ws.mprefix_tc2, L->num_sms, s, L->tile_mode == 4, gmap, &L->tm_xperm64);
-    else if (L->use_tc)
+                            pre_pair, L->num_sms, s, L->tile_mode == 4, gmap, &L->tm_xperm64);
+        if (split)
+            mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
+                               pre_tail, L->num_sms, s, gmap, tail_start);
+    } else if (L->use_tc)
         mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
                            L->ws.mprefix_tc, L->num_sms, s, gmap);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
     const bool shared = with_shared && L->sh_ff;
-    tm.end(3, 1);
+    const int n_gemm = (L->use_tc && L->tile256 && split) ? 2 : 1;
+    tm.end(3, n_gemm);
     tm.begin(4);
-    if (L->use_tc && L->tile256)
+    if (L->use_tc && L->tile256) {
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
-                            L->ws.mprefix_tc2, L->num_sms, s,
-                            L->tile_mode == 4, gmap, &L->tm_h64);
-    else if (L->use_tc)
+                            pre_pair, L->num_sms, s, L->tile_mode == 4, gmap, &L->tm_h64);
+        if (split)
+            mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
+                               pre_tail, L->num_sms, s, gmap, tail_start);
+    } else if (L->use_tc)
         mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
                            L->ws.mprefix_tc, L->num_sms, s, gmap);
     else
         mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm2");
-    tm.end(4, 1);
+    tm.end(4, n_gemm);
     if (shared) ck(cudaStreamWaitEvent(s, L->sh_join, 0), "join shared expert");
     tm.begin(5);
     const uint32_t group_S = unit ? L->S : 0;
@@ -658,6 +675,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                                : std::string(env) == "128"         ? 1
                                : std::string(env) == "256-notail"  ? 3
                                : std::string(env) == "256-tail128" ? 4
+                               : std::string(env) == "256-paironly" ? 5
                                                                    : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
@@ -721,7 +739,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 L->ws.offsets = dalloc<uint32_t>(L->G + 1, "offsets");
                 L->ws.mprefix_tc = dalloc<uint32_t>(L->G + 1, "mprefix");
                 L->ws.mprefix_simt = dalloc<uint32_t>(L->G + 1, "mprefix");
-                L->ws.mprefix_tc2 = dalloc<uint32_t>(L->G + 1, "mprefix");
+                L->ws.mprefix_tc2 = dalloc<uint32_t>(4 * (L->G + 1), "mprefix");
                 L->ws.perm_tok = dalloc<uint32_t>(L->rows_cap, "perm");
                 L->ws.perm_w = dalloc<float>(L->rows_cap, "perm w");
                 L->ws.slot_row = dalloc<uint32_t>(tk, "slot row");
@@ -1276,13 +1294,14 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
 
 // Diagnostics (not in the public header): grouped-GEMM kernel choice of a
 // layer at run time, 0 auto / 1 one-SM 128-row tiles / 2 CTA-pair 256-row
-// tiles (full 256-row tails, the default) / 3 the same / 4 pairs with M=128
-// tail MMAs (64-row A loads; measured 4% slower per step at k=8/16, higher
-// power: profiles/r01_tile_ab.txt), for in-process A/B timing
+// tiles with the split schedule (tails <= 128 rows on the 1-SM kernel) / 3
+// the same / 4 pairs with M=128 tail MMAs (64-row A loads; measured 4% slower
+// per step at k=8/16: profiles/r01_tile_ab.txt) / 5 pairs only (every tail a
+// 256-row pair tile), for in-process A/B timing
 // (tests/probes/tile_ab.py).
 MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {
-        if (!L || mode < 0 || mode > 4) fail(MP_ERR_VALIDATION, "bad argument");
+        if (!L || mode < 0 || mode > 5) fail(MP_ERR_VALIDATION, "bad argument");
         L->tile_mode = mode;
     });
 }

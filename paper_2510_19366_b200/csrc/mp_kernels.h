@@ -26,7 +26,10 @@ struct BucketWs {
     uint32_t* offsets;       // [G+1]
     uint32_t* mprefix_tc;    // [G+1] prefix of ceil(count/128)
     uint32_t* mprefix_simt;  // [G+1] prefix of ceil(count/64)
-    uint32_t* mprefix_tc2;   // [G+1] prefix of ceil(count/256)
+    // [4][G+1]: prefix of ceil(count/256); pair-tile prefix of the split
+    // schedule (count/256 + (count%256 > 128)); its 1-SM tail-tile prefix
+    // (0 < count%256 <= 128); tail_start[g] (first row of that tail tile)
+    uint32_t* mprefix_tc2;
     uint32_t* perm_tok;      // [rows]
     float* perm_w;           // [rows]
     uint32_t* slot_row;      // [T][k_max]
@@ -113,9 +116,10 @@ void launch_gemm1_simt(int dtype, const void* A, const void* W1, void* H, const 
 void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const GemmShape& sh,
                        const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
 // gmap (nullable): group g's weights are B group gmap[g] (offload cache slots)
+// starts (nullable): group g's rows are [starts[g], offsets[g+1]) (tails of the split schedule)
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                    const uint32_t* gmap = nullptr);
+                    const uint32_t* gmap = nullptr, const uint32_t* starts = nullptr);
 size_t gemm_tc_smem_bytes();
 // Epilogue modes of the 1-SM tensor-core GEMM (gemm_tc.cu).
 constexpr int kEpiPlain = 0;   // bf16 acc
@@ -125,7 +129,8 @@ constexpr int kEpiCount = 3;   // uint32 counts (co-activation of 0/1 operands)
 // b_row0: first B row; colmap: kEpiActAbs column map; out: bf16 / f32 / u32 per mode
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                        uint32_t b_row0 = 0, const int32_t* colmap = nullptr, const uint32_t* gmap = nullptr);
+                        uint32_t b_row0 = 0, const int32_t* colmap = nullptr, const uint32_t* gmap = nullptr,
+                        const uint32_t* starts = nullptr);
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)

@@ -534,6 +534,19 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     const uint32_t pre2 = block_exclusive_scan_1024(m2, &tot, wsum);
     if (gi < G) mprefix_tc2[gi] = pre2;
     if (gi == 0) mprefix_tc2[G] = tot;
+    // split schedule (kPairSplit): CTA-pair tiles for the full 256-row blocks
+    // and a remainder > 128 rows; a remainder <= 128 rows goes to one 128-row
+    // 1-SM tile starting at tail_start[g] (half the SM time of a pair tile)
+    const uint32_t rem = c % 256;
+    const uint32_t mpf = gi < G ? c / 256 + (rem > 128 ? 1u : 0u) : 0;
+    const uint32_t prepf = block_exclusive_scan_1024(mpf, &tot, wsum);
+    if (gi < G) mprefix_tc2[(G + 1) + gi] = prepf;
+    if (gi == 0) mprefix_tc2[(G + 1) + G] = tot;
+    const uint32_t mtl = gi < G ? ((rem > 0 && rem <= 128) ? 1u : 0u) : 0;
+    const uint32_t pretl = block_exclusive_scan_1024(mtl, &tot, wsum);
+    if (gi < G) mprefix_tc2[2 * (G + 1) + gi] = pretl;
+    if (gi == 0) mprefix_tc2[2 * (G + 1) + G] = tot;
+    if (gi < G) mprefix_tc2[3 * (G + 1) + gi] = off + c - rem;  // tail_start
     __syncthreads();
     if (gi < G) goff[gi] = off;
     __syncthreads();

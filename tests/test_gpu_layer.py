@@ -334,7 +334,7 @@ def test_profiling_stage_times(oracle, torch_cuda):
     # the bucketing runs inside the tensor-core router's fused epilogue here
     assert st["bucket"][1] == 0 and st["router"][1] == 2
     assert all(v[0] > 0 for name, v in st.items() if v[1])
-    assert L.launch_count() - n0 == sum(v[1] for v in st.values()) == 6
+    assert L.launch_count() - n0 == sum(v[1] for v in st.values()) in (6, 8)  # 8: split GEMM schedule
 
 
 def test_tensor_core_router_logit_error(oracle, torch_cuda, mixtral):
