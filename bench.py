@@ -487,11 +487,13 @@ def kernel_roofline(stage_ms_per_step, T, k, pk, touched_groups):
     t_tc = flops / (pk["bf16_tflops_sustained"] * 1e12)
     t_hbm = (wbytes + abytes) / (pk["hbm_gbs"] * 1e9)
     traffic = None
-    prof = ROOT / "profiles" / "ncu_summary_r01.json"
+    # DRAM bytes of the kernel per launch from the committed ncu --set full
+    # capture of the same workload (tests/probes/ncu_summary.py)
+    prof = ROOT / "profiles" / "ncu_summary_r01c.json"
     if prof.exists():
         try:
             j = json.loads(prof.read_text())
-            traffic = j.get("kernels", {}).get(name, {}).get(f"dram_bytes_k{k}")
+            traffic = j.get(name, {}).get(f"dram_bytes_k{k}")
         except Exception:
             traffic = None
     if t_tc >= t_hbm:

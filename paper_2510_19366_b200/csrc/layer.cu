@@ -466,8 +466,6 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     // CTA-pair tiles pay up to 255 wasted rows per (sub-expert, N tile) against
     // 127 for 128-row tiles; measured break-even near 192 rows per bucket
     // (Mixtral shape: pairs win at k >= 4, lose at k = 2).  Per-token k: k_max.
-    // The split schedule (1-SM tail tiles) pays off from ~384 rows per bucket
-    // (k=8/16: 10-13% per step; k=4: 4% slower -- profiles/r01_tile_ab.txt).
     double rows = 0.0;
     {
         rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
@@ -489,10 +487,14 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
     const uint32_t* gmap = L->offload ? L->gmap_dev : nullptr;
-    // split schedule (default with pairs): full 256-row blocks (and remainders
-    // > 128 rows) on CTA pairs, remainders <= 128 rows as 128-row tiles on the
-    // 1-SM kernel -- a tail then costs one SM instead of two
-    const bool split = L->tile_mode == 2 || L->tile_mode == 3 || L->tile_mode == 4 || (L->tile_mode == 0 && rows >= 384.0);
+    // split schedule (opt-in): full 256-row blocks (and remainders > 128 rows)
+    // on CTA pairs, remainders <= 128 rows as 128-row tiles on the 1-SM kernel
+    // Measured against (ncu, profiles/ncu_summary_r01b.json): the 1-SM tail
+    // kernel re-streams the tails' weight tiles from HBM (+0.9 GB at k=8 for
+    // gemm1; in the pair-only order the tail tile follows the full tiles of
+    // the same (sub-expert, N tile) and hits L2), so it is opt-in (mode 5).
+    const bool split = L->tile_mode == 5;
+    (void)rows;
     const uint32_t G1 = L->G + 1;
     const uint32_t* pre_pair = L->ws.mprefix_tc2 + (split ? G1 : 0);
     const uint32_t* pre_tail = L->ws.mprefix_tc2 + 2 * G1;
@@ -675,7 +677,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                                : std::string(env) == "128"         ? 1
                                : std::string(env) == "256-notail"  ? 3
                                : std::string(env) == "256-tail128" ? 4
-                               : std::string(env) == "256-paironly" ? 5
+                               : std::string(env) == "256-split"   ? 5
                                                                    : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
@@ -1294,10 +1296,10 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
 
 // Diagnostics (not in the public header): grouped-GEMM kernel choice of a
 // layer at run time, 0 auto / 1 one-SM 128-row tiles / 2 CTA-pair 256-row
-// tiles with the split schedule (tails <= 128 rows on the 1-SM kernel) / 3
-// the same / 4 pairs with M=128 tail MMAs (64-row A loads; measured 4% slower
-// per step at k=8/16: profiles/r01_tile_ab.txt) / 5 pairs only (every tail a
-// 256-row pair tile), for in-process A/B timing
+// tiles (the default order) / 3 the same / 4 pairs with M=128 tail MMAs
+// (64-row A loads; measured 4% slower per step: profiles/r01_tile_ab.txt) / 5
+// the split schedule (tails <= 128 rows on the 1-SM kernel; +0.9 GB of DRAM
+// weight re-reads at k=8: profiles/ncu_summary_r01b.json), for A/B timing
 // (tests/probes/tile_ab.py).
 MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {

@@ -3,7 +3,7 @@ Under the 1000 W cap the clock follows power, so wall time alone is noisy
 across blocks; energy per step (NVML total energy) is the power-robust
 metric: at the cap, throughput ~ P_cap / energy_per_step.
   python tests/probes/tile_ab.py <k-list> <mode-list> [reps] [steps-per-block]
-modes: 1 128-row 1-SM, 2 pairs + 1-SM tails (split), 4 pairs with M=128 tails, 5 pairs only"""
+modes: 1 128-row 1-SM, 2 pairs, 4 pairs with M=128 tails, 5 pairs + 1-SM tails (split)"""
 import ctypes as C, statistics, sys
 import torch
 sys.path.insert(0, '.')
@@ -16,7 +16,7 @@ L, xs = bench.build_layer(0, 4096, 16)
 lib = _lib.load()
 lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
 y = torch.empty((4096, bench.D), dtype=torch.bfloat16, device='cuda')
-names = {1: "128-row", 2: "split", 3: "split", 4: "pair-tail128", 5: "pair-only"}
+names = {1: "128-row", 2: "pair", 3: "pair", 4: "pair-tail128", 5: "split"}
 ks = [int(a) for a in sys.argv[1].split(",")]
 modes = [int(a) for a in sys.argv[2].split(",")]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 6
