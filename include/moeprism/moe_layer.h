@@ -148,6 +148,15 @@ mp_status mp_layer_forward_host(mp_layer_t h, const void* x, uint32_t n_tokens, 
                                 uint32_t k, void* y, uint32_t* sel_out, float* w_out, uint32_t* offsets_out,
                                 void* stream);
 
+/* A sequence of forwards on HOST buffers with the copies pipelined against
+ * the compute: batch i's upload (own stream) and download (own stream)
+ * overlap the compute of its neighbours through two device staging slots.
+ * xs[i], ys[i]: host n_tokens[i] x d_model buffers of the layer dtype (pinned
+ * for the copies to overlap); one k for every token.  Synchronises before
+ * returning; device validation flags raise like mp_layer_forward_host. */
+mp_status mp_layer_forward_host_batches(mp_layer_t h, uint32_t n_batches, const void* const* xs,
+                                        const uint32_t* n_tokens, uint32_t k, void* const* ys, void* stream);
+
 /* Forward with an explicit selection (device, T x k_max, ascending global
  * sub-expert ids e*S+s, MP_SEL_NONE padded; duplicates rejected on the
  * host path).  w (device, nullable): per-slot weights; NULL = unit weights,

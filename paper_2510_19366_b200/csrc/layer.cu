@@ -164,6 +164,12 @@ struct mp_layer_s {
     cudaEvent_t sh_fork = nullptr, sh_join = nullptr;
 
     bool residual = false;  // mp_layer_set_residual: y = x + MoE(x), fused into the combine
+    // pipelined host-buffer forwards (mp_layer_forward_host_batches): two
+    // staging slots, copy streams and slot events
+    void* px[2] = {nullptr, nullptr};
+    void* py[2] = {nullptr, nullptr};
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_xready[2] = {}, ev_computed[2] = {}, ev_ydone[2] = {};
     uint32_t* cal_meta = nullptr;  // calibration GEMM group offsets / tile prefix
 
     // Sub-expert offload cache: the packed weights live in
@@ -213,6 +219,14 @@ void free_layer(mp_layer_s* L) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (L->sh_stream) cudaStreamDestroy(L->sh_stream);
+    for (cudaStream_t st : {L->h2d, L->d2h})
+        if (st) cudaStreamDestroy(st);
+    for (int i = 0; i < 2; ++i) {
+        for (cudaEvent_t ev : {L->ev_xready[i], L->ev_computed[i], L->ev_ydone[i]})
+            if (ev) cudaEventDestroy(ev);
+        if (L->px[i] && L->px[i] != L->x_stage) cudaFree(L->px[i]);
+        if (L->py[i] && L->py[i] != L->y_stage) cudaFree(L->py[i]);
+    }
     if (L->sh_fork) cudaEventDestroy(L->sh_fork);
     if (L->sh_join) cudaEventDestroy(L->sh_join);
     for (void* p : {L->W1c, L->W2c, static_cast<void*>(L->gmap_dev)})
@@ -1055,6 +1069,72 @@ MP_API mp_status mp_layer_forward_host(mp_layer_t L, const void* x, uint32_t T, 
         int flags = 0;
         ck(cudaMemcpyAsync(&flags, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost, s), "flags");
         ck(cudaStreamSynchronize(s), "forward");
+        static const int order[] = {0, 1, 2, 3, 4, 5};
+        tm.finish(order, 6);
+        raise_device_errors(flags);
+    });
+}
+
+// Pipelined host-buffer forwards: batch i's host->device copy (H2D stream),
+// compute (the caller's stream) and device->host copy (D2H stream) run
+// concurrently with batches i-1 / i+1 through two staging slots, ordered by
+// events: a slot's x is not overwritten before the compute that reads it is
+// done, its y not before the previous download of that slot completed.
+MP_API mp_status mp_layer_forward_host_batches(mp_layer_t L, uint32_t n, const void* const* xs,
+                                               const uint32_t* n_tokens, uint32_t k, void* const* ys,
+                                               void* stream) {
+    return guarded([&] {
+        if (!L || (n && (!xs || !ys || !n_tokens))) fail(MP_ERR_VALIDATION, "null argument");
+        check_ready(L);
+        if (k < 1 || k > L->k_max || k > L->G)
+            fail(MP_ERR_VALIDATION, "k_active = " + std::to_string(k) + " out of range [1, " +
+                                        std::to_string(std::min(L->k_max, L->G)) + "]");
+        for (uint32_t i = 0; i < n; ++i) {
+            check_tokens(L, n_tokens[i]);
+            if (n_tokens[i] && (!xs[i] || !ys[i])) fail(MP_ERR_VALIDATION, "null batch buffer");
+        }
+        if (n == 0) return;
+        DeviceGuard dg(L->desc.device);
+        if (!L->h2d) {
+            ck(cudaStreamCreateWithFlags(&L->h2d, cudaStreamNonBlocking), "h2d stream");
+            ck(cudaStreamCreateWithFlags(&L->d2h, cudaStreamNonBlocking), "d2h stream");
+            for (int i = 0; i < 2; ++i) {
+                ck(cudaEventCreateWithFlags(&L->ev_xready[i], cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&L->ev_computed[i], cudaEventDisableTiming), "event");
+                ck(cudaEventCreateWithFlags(&L->ev_ydone[i], cudaEventDisableTiming), "event");
+            }
+            const size_t bytes = (size_t)L->max_tokens * L->d * L->esz;
+            L->px[0] = L->x_stage;
+            L->py[0] = L->y_stage;
+            L->px[1] = dalloc<char>(bytes, "x stage 2");
+            L->py[1] = dalloc<char>(bytes, "y stage 2");
+        }
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        ck(cudaMemsetAsync(L->ws.err, 0, sizeof(int), s), "memset err");
+        // the slots may still be in use by an earlier call's copies
+        ck(cudaStreamSynchronize(L->d2h), "d2h");
+        StageTimer tm(L, s);
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t T = n_tokens[i], sl = i & 1u;
+            if (T == 0) continue;
+            const size_t bytes = (size_t)T * L->d * L->esz;
+            if (i >= 2) ck(cudaStreamWaitEvent(L->h2d, L->ev_computed[sl], 0), "wait compute");
+            ck(cudaMemcpyAsync(L->px[sl], xs[i], bytes, cudaMemcpyHostToDevice, L->h2d), "x upload");
+            ck(cudaEventRecord(L->ev_xready[sl], L->h2d), "event");
+            ck(cudaStreamWaitEvent(s, L->ev_xready[sl], 0), "wait x");
+            if (i >= 2) ck(cudaStreamWaitEvent(s, L->ev_ydone[sl], 0), "wait y");
+            const bool bucketed = route(L, L->px[sl], T, nullptr, k, s, tm, true, true);
+            run_experts(L, L->px[sl], T, L->sel, L->wsel, L->desc.weight_mode == MP_WEIGHT_UNIT, L->py[sl], s, tm,
+                        true, true, k, bucketed);
+            ck(cudaEventRecord(L->ev_computed[sl], s), "event");
+            ck(cudaStreamWaitEvent(L->d2h, L->ev_computed[sl], 0), "wait compute");
+            ck(cudaMemcpyAsync(ys[i], L->py[sl], bytes, cudaMemcpyDeviceToHost, L->d2h), "y download");
+            ck(cudaEventRecord(L->ev_ydone[sl], L->d2h), "event");
+        }
+        int flags = 0;
+        ck(cudaMemcpyAsync(&flags, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost, s), "flags");
+        ck(cudaStreamSynchronize(s), "forward");
+        ck(cudaStreamSynchronize(L->d2h), "download");
         static const int order[] = {0, 1, 2, 3, 4, 5};
         tm.finish(order, 6);
         raise_device_errors(flags);

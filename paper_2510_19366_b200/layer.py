@@ -169,6 +169,19 @@ class MoeLayer:
                                              _ptr(off), _stream_handle(stream)))
         return (y, sel, w, off) if return_routing else y
 
+    def forward_host_batches(self, xs, k: int, ys=None, stream=None):
+        """Pipelined forwards over host batches (pinned torch tensors): uploads,
+        compute and downloads of neighbouring batches overlap.  Returns ys."""
+        torch = _torch()
+        if ys is None:
+            ys = [torch.empty((x.shape[0], self.d), dtype=x.dtype, pin_memory=x.is_pinned()) for x in xs]
+        n = len(xs)
+        xp = (C.c_void_p * n)(*[x.data_ptr() for x in xs])
+        yp = (C.c_void_p * n)(*[y.data_ptr() for y in ys])
+        nt = (C.c_uint32 * n)(*[x.shape[0] for x in xs])
+        check(self.lib.mp_layer_forward_host_batches(self.h, n, xp, nt, k, yp, _stream_handle(stream)))
+        return ys
+
     def forward_selected(self, x, sel, w=None, y=None, return_offsets: bool = False, stream=None):
         """Explicit selection (T x k_max global ids, MP_SEL_NONE padded); w None = unit weights."""
         torch = _torch()

@@ -447,3 +447,22 @@ def test_router_exact_reselection_window(oracle, torch_cuda, k, monkeypatch):
     assert np.array_equal(_u32(off), ooff)
     assert np.allclose(w.cpu().numpy()[:, :k], ow[:, :k], rtol=1e-5, atol=1e-6)
     L.close()
+
+
+def test_forward_host_batches_pipelined(oracle, torch_cuda):
+    """mp_layer_forward_host_batches == per-batch device forwards, bit for bit,
+    for ragged batch sizes (uploads / compute / downloads overlapped)."""
+    torch = torch_cuda
+    E, S, d, ff = 4, 4, 256, 512
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, 8)
+    L = make_layer(experts, parts, wr, S, "bf16", k_max=4, max_tokens=96)
+    sizes = [96, 17, 64, 1, 80, 33, 96]
+    xs = [torch.from_numpy(bf16_round(oracle.uniform_pm1(50 + i, n * d))).reshape(n, d).to(torch.bfloat16).pin_memory()
+          for i, n in enumerate(sizes)]
+    ys = L.forward_host_batches(xs, k=3)
+    for xh, yh in zip(xs, ys):
+        yd = L.forward(xh.cuda(), k=3)
+        assert torch.equal(yd.cpu(), yh)
+    ys2 = L.forward_host_batches(xs[:2], k=3)  # a second call reuses the slots
+    assert all(torch.equal(a, b) for a, b in zip(ys2, ys[:2]))
+    L.close()
