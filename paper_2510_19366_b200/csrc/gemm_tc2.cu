@@ -45,6 +45,13 @@
 #ifndef MP_PAIR_TRACE  // 1: MMA-issuer timing into the trace buffer (diagnostic builds only)
 #define MP_PAIR_TRACE 0
 #endif
+// L2 policies on the operand loads (diagnostic builds): bit 0 B evict_first,
+// bit 1 A evict_last.  Measured (ncu DRAM bytes, k=8/16): evict_first on the
+// weights raises DRAM reads 28-68% (concurrent m-tile pairs reuse them),
+// evict_last on A saves 2-4%: both off.
+#ifndef MP_PAIR_HINTS
+#define MP_PAIR_HINTS 0
+#endif
 #ifndef MP_PAIR_STAGES
 #define MP_PAIR_STAGES 6
 #endif
@@ -114,6 +121,14 @@ MP_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t bar_clust
         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
         "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster)
+        : "memory");
+}
+MP_DEV void tma_load_2d_pair_hint(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int32_t c0, int32_t c1,
+                                  uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.cta_group::2.L2::cache_hint "
+        "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_cluster), "l"(policy)
         : "memory");
 }
 MP_DEV void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
@@ -216,6 +231,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             const uint32_t full_leader = mapa(&full[0], 0);  // full[s] of the leader: + 8 s
+#if MP_PAIR_HINTS
+            const uint64_t pol_b = l2_policy_evict_first(), pol_a = l2_policy_evict_last();
+            (void)pol_a;
+            (void)pol_b;
+#endif
             uint32_t it = 0;
             for (uint32_t tile = pair; tile < total; tile += npairs) {
                 uint32_t g, m, n;
@@ -232,8 +252,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mbar_wait(&empty[s], ph ^ 1u);
                     if (rank == 0) mbar_expect_tx(&full[s], tx);
                     const uint32_t fb = full_leader + s * 8;
+#if MP_PAIR_HINTS & 2
+                    tma_load_2d_pair_hint(sA + s * A_BYTES, tA, fb, static_cast<int32_t>(kb * BK), arow, pol_a);
+#else
                     tma_load_2d_pair(sA + s * A_BYTES, tA, fb, static_cast<int32_t>(kb * BK), arow);
+#endif
+#if MP_PAIR_HINTS & 1
+                    tma_load_2d_pair_hint(sB + s * B_BYTES, &tmB, fb, static_cast<int32_t>(kb * BK), brow, pol_b);
+#else
                     tma_load_2d_pair(sB + s * B_BYTES, &tmB, fb, static_cast<int32_t>(kb * BK), brow);
+#endif
                 }
             }
         }
