@@ -213,6 +213,13 @@ typedef struct mp_ep_s* mp_ep_t;
 mp_status mp_ep_create(uint32_t world, uint32_t rank, uint32_t experts_per_rank, uint32_t n_subexperts,
                        uint32_t d_model, uint32_t k_max, uint32_t max_tokens, uint32_t dtype, int32_t device,
                        mp_ep_t* out);
+/* Sub-expert-granularity sharding (SURVEY 8(e), E not divisible by the world
+ * size, e.g. Qwen 240 sub-experts over 8 GPUs): rank r owns global ids
+ * [r*per_rank, (r+1)*per_rank); its experts-only layer holds parent experts
+ * floor(r*per_rank/S) .. floor(((r+1)*per_rank-1)/S) and receives selections
+ * in local ids g - floor(r*per_rank/S)*S.  mp_ep_create == per_rank = epr*S. */
+mp_status mp_ep_create_subexpert(uint32_t world, uint32_t rank, uint32_t per_rank, uint32_t S, uint32_t d,
+                                 uint32_t k_max, uint32_t max_tokens, uint32_t dtype, int32_t device, mp_ep_t* out);
 mp_status mp_ep_destroy(mp_ep_t ep);
 /* sel: device [T x k_max] global ids.  send_counts: HOST [world] (synchronises). */
 mp_status mp_ep_plan(mp_ep_t ep, const uint32_t* sel, uint32_t n_tokens, uint32_t* send_counts, void* stream);

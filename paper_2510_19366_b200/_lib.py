@@ -32,7 +32,7 @@ EXPORTS = (
     "mp_layer_forward_selected", "mp_layer_route", "mp_layer_check_errors", "mp_layer_set_profiling",
     "mp_layer_stage_times", "mp_layer_reset_stage_times", "mp_layer_launch_count", "mp_synth_fill",
     "mp_format_read_mpex", "mp_format_read_partition_doc", "mp_validate_partition", "mp_layer_forward_selected_host",
-    "mp_ep_create", "mp_ep_destroy", "mp_ep_plan", "mp_ep_pack", "mp_ep_combine",
+    "mp_ep_create", "mp_ep_create_subexpert", "mp_ep_destroy", "mp_ep_plan", "mp_ep_pack", "mp_ep_combine",
 )
 
 
@@ -100,6 +100,7 @@ def _sig(L):
     L.mp_validate_partition.argtypes = [u32, vp, sz]
     L.mp_layer_forward_selected_host.argtypes = [vp, vp, u32, vp, vp, vp, vp]
     L.mp_ep_create.argtypes = [u32, u32, u32, u32, u32, u32, u32, u32, i32, C.POINTER(vp)]
+    L.mp_ep_create_subexpert.argtypes = [u32, u32, u32, u32, u32, u32, u32, u32, i32, C.POINTER(vp)]
     L.mp_ep_destroy.argtypes = [vp]
     L.mp_ep_plan.argtypes = [vp, vp, u32, vp, vp]
     L.mp_ep_pack.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp]

@@ -1,7 +1,10 @@
 // ep.cu -- expert-parallel token dispatch / combine.
 //
-// Sub-experts are sharded by parent expert: rank r owns global ids
-// [r*epr*S, (r+1)*epr*S).  A token is sent ONCE to every rank owning at least
+// Sub-experts are sharded in contiguous global-id ranges: rank r owns
+// [r*per_rank, (r+1)*per_rank) -- whole parent experts when per_rank is a
+// multiple of S, else sub-expert granularity (Qwen: 240 / 8 = 30 per rank,
+// SURVEY 8(e)); a rank's experts-only layer then holds the parent experts its
+// range touches and numbers sub-experts from base(r) = floor(r*per_rank/S)*S.  A token is sent ONCE to every rank owning at least
 // one of its selected sub-experts (dedup), together with its selection
 // re-expressed in that rank's local ids and the combine weights; the owner
 // returns one weighted partial per (token, rank) and the source sums them in
@@ -54,7 +57,7 @@ __global__ void ep_slot_kernel(const uint32_t* __restrict__ dest, const uint32_t
 template <typename Tx>
 __global__ void __launch_bounds__(256) ep_pack_kernel(const Tx* __restrict__ x, const uint32_t* __restrict__ sel,
                                                       const float* __restrict__ w, uint32_t T, uint32_t d,
-                                                      uint32_t k_max, uint32_t per_rank, uint32_t world,
+                                                      uint32_t k_max, uint32_t per_rank, uint32_t S, uint32_t world,
                                                       const uint32_t* __restrict__ dest,
                                                       const uint32_t* __restrict__ slot_row, Tx* __restrict__ send_x,
                                                       uint32_t* __restrict__ send_sel, float* __restrict__ send_w) {
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(256) ep_pack_kernel(const Tx* __restrict__ x, 
             for (uint32_t q = 0; q < k_max; ++q) {
                 const uint32_t g = sel[(size_t)t * k_max + q];
                 if (g != kSelNone && g / per_rank == r) {
-                    send_sel[(size_t)pos * k_max + n] = g - r * per_rank;
+                    send_sel[(size_t)pos * k_max + n] = g - (r * per_rank / S) * S;  // local id on rank r
                     send_w[(size_t)pos * k_max + n] = w ? w[(size_t)t * k_max + q] : 1.0f;
                     ++n;
                 }
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(const Tx* __restrict__ 
 }  // namespace mp
 
 struct mp_ep_s {
-    uint32_t world, rank, epr, S, d, k_max, max_tokens, dtype;
+    uint32_t world, rank, per_rank, S, d, k_max, max_tokens, dtype;
     int device;
     uint32_t* dest = nullptr;
     mp::BucketWs ws{};
@@ -168,16 +171,17 @@ int ep_guarded(F&& f) {
 }
 }  // namespace
 
-MP_API mp_status mp_ep_create(uint32_t world, uint32_t rank, uint32_t epr, uint32_t S, uint32_t d, uint32_t k_max,
-                              uint32_t max_tokens, uint32_t dtype, int32_t device, mp_ep_t* out) {
+MP_API mp_status mp_ep_create_subexpert(uint32_t world, uint32_t rank, uint32_t per_rank, uint32_t S, uint32_t d,
+                                        uint32_t k_max, uint32_t max_tokens, uint32_t dtype, int32_t device,
+                                        mp_ep_t* out) {
     return ep_guarded([&] {
         if (!out) ep_fail(MP_ERR_VALIDATION, "null argument");
         if (world < 1 || world > 32 || rank >= world) ep_fail(MP_ERR_VALIDATION, "bad world / rank");
-        if (epr < 1 || S < 1 || d < 1 || k_max < 1 || k_max > 64 || max_tokens < 1)
+        if (per_rank < 1 || S < 1 || d < 1 || k_max < 1 || k_max > 64 || max_tokens < 1)
             ep_fail(MP_ERR_VALIDATION, "bad expert-parallel shape");
         if (dtype != MP_DTYPE_F32 && dtype != MP_DTYPE_BF16) ep_fail(MP_ERR_VALIDATION, "unknown dtype");
         ep_ck(cudaSetDevice(device), "cudaSetDevice");
-        auto* E = new mp_ep_s{world, rank, epr, S, d, k_max, max_tokens, dtype, device};
+        auto* E = new mp_ep_s{world, rank, per_rank, S, d, k_max, max_tokens, dtype, device};
         try {
             const size_t tw = (size_t)max_tokens * world;
             const uint32_t nblk = (max_tokens + mp::kRouteTokensPerBlock - 1) / mp::kRouteTokensPerBlock;
@@ -202,6 +206,15 @@ MP_API mp_status mp_ep_create(uint32_t world, uint32_t rank, uint32_t epr, uint3
     });
 }
 
+MP_API mp_status mp_ep_create(uint32_t world, uint32_t rank, uint32_t epr, uint32_t S, uint32_t d, uint32_t k_max,
+                              uint32_t max_tokens, uint32_t dtype, int32_t device, mp_ep_t* out) {
+    if (epr < 1 || S < 1) {
+        mp_internal_set_error("bad expert-parallel shape");
+        return MP_ERR_VALIDATION;
+    }
+    return mp_ep_create_subexpert(world, rank, epr * S, S, d, k_max, max_tokens, dtype, device, out);
+}
+
 MP_API mp_status mp_ep_destroy(mp_ep_t E) {
     return ep_guarded([&] {
         if (E) {
@@ -222,7 +235,7 @@ MP_API mp_status mp_ep_plan(mp_ep_t E, const uint32_t* sel, uint32_t T, uint32_t
             return;
         }
         cudaStream_t s = static_cast<cudaStream_t>(stream);
-        mp::launch_ep_dest(sel, T, E->k_max, E->epr * E->S, E->world, E->dest, s);
+        mp::launch_ep_dest(sel, T, E->k_max, E->per_rank, E->world, E->dest, s);
         mp::launch_bucket_local(E->dest, T, E->world, E->world, E->ws, s);
         mp::launch_bucket_scan(T, E->world, E->ws, s);
         mp::launch_ep_slot(E->dest, E->ws.lrank, E->ws.block_base, T, E->world, E->ws.slot_row, s);
@@ -240,8 +253,8 @@ MP_API mp_status mp_ep_pack(mp_ep_t E, const void* x, const uint32_t* sel, const
         if (!E || (T && (!x || !sel || !send_x || !send_sel || !send_w))) ep_fail(MP_ERR_VALIDATION, "null argument");
         if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_pack must follow mp_ep_plan for the same tokens");
         if (T == 0) return;
-        mp::launch_ep_pack(E->dtype, x, sel, w, T, E->d, E->k_max, E->epr * E->S, E->world, E->dest, E->ws.slot_row,
-                           send_x, send_sel, send_w, static_cast<cudaStream_t>(stream));
+        mp::launch_ep_pack(E->dtype, x, sel, w, T, E->d, E->k_max, E->per_rank, E->S, E->world, E->dest,
+                           E->ws.slot_row, send_x, send_sel, send_w, static_cast<cudaStream_t>(stream));
         ep_ck(cudaGetLastError(), "ep pack");
     });
 }
@@ -266,15 +279,15 @@ void launch_ep_slot(const uint32_t* dest, const uint32_t* lrank, const uint32_t*
     ep_slot_kernel<<<(T * world + 255) / 256, 256, 0, s>>>(dest, lrank, block_base, T, world, slot_row);
 }
 void launch_ep_pack(int dtype, const void* x, const uint32_t* sel, const float* w, uint32_t T, uint32_t d,
-                    uint32_t k_max, uint32_t per_rank, uint32_t world, const uint32_t* dest, const uint32_t* slot_row,
-                    void* send_x, uint32_t* send_sel, float* send_w, cudaStream_t s) {
+                    uint32_t k_max, uint32_t per_rank, uint32_t S, uint32_t world, const uint32_t* dest,
+                    const uint32_t* slot_row, void* send_x, uint32_t* send_sel, float* send_w, cudaStream_t s) {
     if (dtype == 1)
         ep_pack_kernel<__nv_bfloat16><<<(T + 7) / 8, 256, 0, s>>>(
-            static_cast<const __nv_bfloat16*>(x), sel, w, T, d, k_max, per_rank, world, dest, slot_row,
+            static_cast<const __nv_bfloat16*>(x), sel, w, T, d, k_max, per_rank, S, world, dest, slot_row,
             static_cast<__nv_bfloat16*>(send_x), send_sel, send_w);
     else
         ep_pack_kernel<float><<<(T + 7) / 8, 256, 0, s>>>(static_cast<const float*>(x), sel, w, T, d, k_max, per_rank,
-                                                          world, dest, slot_row, static_cast<float*>(send_x),
+                                                          S, world, dest, slot_row, static_cast<float*>(send_x),
                                                           send_sel, send_w);
 }
 void launch_ep_combine(int dtype, const void* back, uint32_t T, uint32_t d, uint32_t world, const uint32_t* slot_row,

@@ -40,15 +40,23 @@ class CudaEpOps:
         import torch
         self.torch = torch
         self.rank, self.world, self.d, self.k_max = rank, world, d, k_max
-        self.epr = E // world
+        G = E * S
+        if G % world:
+            raise ValueError(f"{G} sub-experts do not shard evenly over {world} ranks")
+        # contiguous sub-expert ranges: whole experts when E % world == 0, else
+        # sub-expert granularity (the boundary expert is held by both ranks)
+        self.per_rank = G // world
+        self.first_e = (self.per_rank * rank) // S
+        self.last_e = (self.per_rank * (rank + 1) - 1) // S
+        self.epr = self.last_e - self.first_e + 1
         self.router = MoeLayer(E, S, d, ff, dtype=dtype, k_max=k_max, max_tokens=max_tokens, device=device,
                                flags=MP_LAYER_ROUTER_ONLY)
         self.local = MoeLayer(self.epr, S, d, ff, dtype=dtype, weights="softmax_renorm", k_max=k_max,
                               max_tokens=max_tokens * world, device=device, flags=MP_LAYER_EXPERTS_ONLY)
         self.dtype = self.router.torch_dtype
         h = C.c_void_p()
-        check(_lib.load().mp_ep_create(world, rank, self.epr, S, d, k_max, max_tokens,
-                                       1 if self.dtype == torch.bfloat16 else 0, device, C.byref(h)))
+        check(_lib.load().mp_ep_create_subexpert(world, rank, self.per_rank, S, d, k_max, max_tokens,
+                                                 1 if self.dtype == torch.bfloat16 else 0, device, C.byref(h)))
         self.ep = h
 
     def route(self, x, k, k_per_token):
@@ -80,15 +88,15 @@ class CudaEpOps:
 
     # weights: experts are addressed by their GLOBAL id; non-owned ones are skipped
     def owns(self, e):
-        return e // self.epr == self.rank
+        return self.first_e <= e <= self.last_e
 
     def load_expert(self, e, wg, wu, wd):
         if self.owns(e):
-            self.local.load_expert(e - self.rank * self.epr, wg, wu, wd)
+            self.local.load_expert(e - self.first_e, wg, wu, wd)
 
     def set_partition(self, e, assignment):
         if self.owns(e):
-            self.local.set_partition(e - self.rank * self.epr, assignment)
+            self.local.set_partition(e - self.first_e, assignment)
 
     def set_router(self, w_r):
         self.router.set_router(w_r)

@@ -15,7 +15,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 U32 = 0xFFFFFFFF
-E, S, D, FF, K_MAX = 4, 4, 32, 64, 8
+S, D, FF, K_MAX = 4, 32, 64, 8
 
 
 def _free_port():
@@ -24,7 +24,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _data(oracle):
+def _data(oracle, E):
     experts = []
     for e in range(E):
         wg, wu, wd = oracle.random_expert(D, FF, 300 + e)
@@ -41,12 +41,15 @@ class OracleEpOps:
     def __init__(self, oracle, experts, parts, wr, rank, world):
         self.o, self.rank, self.world = oracle, rank, world
         self.ex, self.parts, self.wr = experts, parts, wr
-        self.epr = E // world
-        self.per_rank = self.epr * S
+        self.E = len(experts)
+        # contiguous sub-expert ranges (ep.py / ep.cu): whole experts or sub-expert granularity
+        self.per_rank = self.E * S // world
+        self.first_e = self.per_rank * rank // S
+        self.last_e = (self.per_rank * (rank + 1) - 1) // S
 
     def route(self, x, k, kpt):
         xn = x.numpy()
-        logits = self.o.router_logits(xn, self.wr, xn.shape[0], D, E * S)
+        logits = self.o.router_logits(xn, self.wr, xn.shape[0], D, self.E * S)
         sel, w, _ = self.o.route(logits, k, K_MAX, 1, k_per_token=None if kpt is None else kpt.numpy())
         return torch.from_numpy(sel.view(np.int32).copy()), torch.from_numpy(w)
 
@@ -69,7 +72,8 @@ class OracleEpOps:
                 if r not in dl:
                     continue
                 self.pos[(t, r)] = len(rows)
-                ids = [(int(g) - r * self.per_rank, wn[t, j]) for j, g in enumerate(s[t])
+                base = (r * self.per_rank // S) * S  # local ids on rank r
+                ids = [(int(g) - base, wn[t, j]) for j, g in enumerate(s[t])
                        if g != U32 and int(g) // self.per_rank == r]
                 rows.append(x[t].numpy())
                 ssel.append([i for i, _ in ids] + [U32] * (K_MAX - len(ids)))
@@ -82,8 +86,8 @@ class OracleEpOps:
     def experts(self, recv_x, recv_sel, recv_w):
         if recv_x.shape[0] == 0:
             return recv_x.new_empty((0, D))
-        lo = self.rank * self.epr
-        y = self.o.layer_forward(self.ex[lo:lo + self.epr], self.parts[lo:lo + self.epr], S,
+        lo, hi = self.first_e, self.last_e + 1
+        y = self.o.layer_forward(self.ex[lo:hi], self.parts[lo:hi], S,
                                  recv_x.numpy(), recv_sel.numpy().view(np.uint32), recv_w.numpy(), 1)
         return torch.from_numpy(y)
 
@@ -98,7 +102,7 @@ class OracleEpOps:
         return torch.from_numpy(y)
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, E):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -109,7 +113,7 @@ def _worker(rank, world, port, out_dir):
     from oracle_lib import Oracle
     from paper_2510_19366_b200.ep import ExpertParallelLayer
     o = Oracle()
-    experts, parts, wr = _data(o)
+    experts, parts, wr = _data(o, E)
     T = 20 + 7 * rank  # ragged: ranks hold different token counts
     x = torch.from_numpy(o.uniform_pm1(50 + rank, T * D).reshape(T, D))
     kpt = torch.from_numpy(np.random.default_rng(rank).choice([1, 2, 4, 8], size=T).astype(np.int32))
@@ -120,10 +124,10 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_expert_parallel_gloo_matches_single_process(oracle, tmp_path, world):
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
-    experts, parts, wr = _data(oracle)
+@pytest.mark.parametrize("world,E", [(2, 4), (2, 3)])  # E=3: sub-expert granularity (6 of 12 per rank)
+def test_expert_parallel_gloo_matches_single_process(oracle, tmp_path, world, E):
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), E), nprocs=world, join=True)
+    experts, parts, wr = _data(oracle, E)
     res = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
     # the counts each rank sends are what the peers receive
     for r in range(world):

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 E, S, D, FF, T, K_MAX = 4, 4, 256, 512, 96, 8
 
 
-def _setup(oracle):
+def _setup(oracle, E=E):
     experts = [tuple(a / np.float32(math.sqrt(D if i < 2 else FF)) for i, a in enumerate(oracle.random_expert(D, FF, 70 + e)))
                for e in range(E)]
     parts = [oracle.random_balanced_partition(FF, S, 80 + e) for e in range(E)]
@@ -23,6 +23,7 @@ def _setup(oracle):
 
 def _ops(world, rank, experts, parts, wr):
     from paper_2510_19366_b200.ep import CudaEpOps
+    E = len(experts)
     ops = CudaEpOps(E, S, D, FF, rank, world, dtype="bf16", k_max=K_MAX, max_tokens=T, device=0)
     for e in range(E):
         ops.set_partition(e, parts[e])
@@ -50,10 +51,11 @@ def test_ep_world1_loopback_bitwise(oracle, cuda_lib):
     assert torch.equal(y, y_ref)
 
 
-def test_ep_world2_emulated(oracle, cuda_lib):
+@pytest.mark.parametrize("E", [4, 3])  # E=3: sub-expert-granularity sharding (6 of 12 sub-experts per rank)
+def test_ep_world2_emulated(oracle, cuda_lib, E):
     import torch
     from paper_2510_19366_b200 import MoeLayer
-    experts, parts, wr = _setup(oracle)
+    experts, parts, wr = _setup(oracle, E)
     ref = MoeLayer(E, S, D, FF, dtype="bf16", k_max=K_MAX, max_tokens=T)
     for e in range(E):
         ref.set_partition(e, parts[e])
@@ -70,7 +72,7 @@ def test_ep_world2_emulated(oracle, cuda_lib):
         sends.append(ops.pack(xs[r], sel, w, sum(c)))
         # dedup: each (token, destination rank) appears once
         s = sel.cpu().numpy().view(np.uint32)
-        dests = sum(len({int(g) // (2 * S) for g in row if g != 0xFFFFFFFF}) for row in s)
+        dests = sum(len({int(g) // (E * S // 2) for g in row if g != 0xFFFFFFFF}) for row in s)
         assert dests == sum(c)
     # emulated all-to-all: rank q receives the q-th segment of every rank's send
     def seg(r, q):
