@@ -480,10 +480,22 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     // CTA-pair tiles pay up to 255 wasted rows per (sub-expert, N tile) against
     // 127 for 128-row tiles; measured break-even near 192 rows per bucket
     // (Mixtral shape: pairs win at k >= 4, lose at k = 2).  Per-token k: k_max.
+    // Auto choice: the kernel with fewer padded rows per bucket (expected over
+    // bucket sizes M +- sqrt(M), M = T k / G), CTA pairs credited 10% for
+    // their lower operand traffic.  Mixtral: pairs at k >= 8; Qwen (w=352,
+    // buckets of 136-546 rows at prefill): 128-row tiles.
     double rows = 0.0;
     {
         rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
-        L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && rows >= 192.0);
+        const double sd = std::sqrt(rows > 1.0 ? rows : 1.0);
+        double pad128 = 0.0, pad256 = 0.0;
+        for (double m : {rows - sd, rows, rows + sd}) {
+            const double mm = m < 1.0 ? 1.0 : m;
+            pad128 += std::ceil(mm / 128.0) * 128.0;
+            pad256 += std::ceil(mm / 256.0) * 256.0;
+        }
+        const bool pairs_win = pad256 / 1.1 < pad128;
+        L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && rows >= 192.0 && pairs_win);
     }
     if (!bucketed) {
         tm.begin(1);
