@@ -506,7 +506,8 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     }
     tm.begin(2);
     if (L->offload) offload_step(L, s);  // transfers counted in the dispatch stage
-    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, L->x_perm, s, true);
+    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, L->x_perm, s, true,
+                        bucketed ? mp::route_tokens_per_block(T) : mp::kRouteTokensPerBlock);
     ck_launch("dispatch");
     tm.end(2, 1);
     mp::GemmShape g1{L->G, L->d_pad, 2 * L->w_pad, T * L->k_max, L->w_pad, 2 * L->w_pad};
@@ -597,10 +598,18 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             L->r_last_T = T;
             ck(cudaMemsetAsync(L->r_flagged, 0, sizeof(uint32_t), s), "memset flagged");
             if (fuse_bucket && L->has_experts && (L->d % 4) == 0) {
-                // routing epilogue + exact near-tie re-selection + bucketing in one kernel
-                mp::launch_route_bucket(L->r_partial, pl.ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
+                // routing epilogue + exact near-tie re-selection + bucketing in one kernel;
+                // many K splits (small batches): reduce them first across (token, g) warps
+                uint32_t ks = pl.ks;
+                if (ks > 8) {
+                    mp::launch_partials_reduce(L->r_partial, ks, T, L->G, pl.Npad, s);
+                    ks = 1;
+                    L->r_last_ks = 1;  // plane 0 now holds the logits
+                    L->launches += 1;
+                }
+                mp::launch_route_bucket(L->r_partial, ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
                                         L->sel, L->wsel, L->r_guard, x, L->d, L->wrT, L->r_ticket, L->r_flagged,
-                                        L->ws, s);
+                                        L->ws, s, mp::route_tokens_per_block(T));
                 bucketed = true;
                 ck_launch("router(tc)+bucket");
                 tm.end(0, 2);
@@ -740,9 +749,14 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                     if (std::string(env) == "simt") L->router_tc = false;  // diagnostics only
                 if (L->router_tc) {
                     L->r_npad = round_up(L->G, 32);
-                    const uint32_t n_chunks = (L->d + 255) / 256;  // upper bound of the router's K splits
+                    // K-split partials [ks][T][Npad]: 256-deep splits, or 64-deep ones
+                    // when few token tiles (plan_router_tc) -- size for both
+                    const uint32_t n256 = (L->d + 255) / 256, n64 = (L->d + 63) / 64;
+                    const uint32_t small_tiles = (static_cast<uint32_t>(L->num_sms) / 2 + n256 - 1) / n256;
+                    const size_t rows_small = std::min<size_t>(L->max_tokens, (size_t)small_tiles * 128);
+                    const size_t n_part = std::max((size_t)n256 * L->max_tokens, (size_t)n64 * rows_small);
                     L->wr_planes = dalloc<char>((size_t)3 * L->r_npad * L->d * 2, "router planes");
-                    L->r_partial = dalloc<double>((size_t)n_chunks * L->max_tokens * L->r_npad, "router partials");
+                    L->r_partial = dalloc<double>(n_part * L->r_npad, "router partials");
                     L->r_flagged = dalloc<uint32_t>((size_t)L->max_tokens + 1, "router flagged");
                     L->r_ticket = dalloc<uint32_t>(1, "router ticket");
                     ck(cudaMemset(L->r_ticket, 0, sizeof(uint32_t)), "memset ticket");
@@ -753,7 +767,9 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 if (D.router_mode == MP_ROUTER_PROXY) L->gate_off = dalloc<uint32_t>(L->G + 1, "gate offsets");
             }
             const size_t tk = (size_t)L->max_tokens * L->k_max;
-            const uint32_t nblk = (L->max_tokens + mp::kRouteTokensPerBlock - 1) / mp::kRouteTokensPerBlock;
+            // bucketing blocks: 32 tokens, or 8 in the fused router for small batches
+            const uint32_t nblk = std::max((L->max_tokens + mp::kRouteTokensPerBlock - 1) / mp::kRouteTokensPerBlock,
+                                           (std::min<uint32_t>(L->max_tokens, 1024) + 7) / 8);
             L->sel = dalloc<uint32_t>(tk, "sel");
             L->wsel = dalloc<float>(tk, "w");
             L->kpt_dev = dalloc<uint32_t>(L->max_tokens, "k per token");

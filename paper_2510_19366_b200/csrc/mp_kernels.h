@@ -49,9 +49,11 @@ void launch_bucket_local(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32
 void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s);
 // x_perm == null: permutation tables only (the GEMM gathers the rows itself)
 // check_finite: also scan x for non-finite values (err bit 2)
+// tb: tokens per bucketing block of the ranks / bases (kRouteTokensPerBlock,
+// or the fused router's smaller blocks for small batches)
 void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t d_pad, const uint32_t* sel,
                      const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s,
-                     bool check_finite = true);
+                     bool check_finite = true, uint32_t tb = kRouteTokensPerBlock);
 // group_S > 0: unit-weight semantics, round once per parent expert (fp32 mode)
 // o_sh / w_sh (bf16 only, nullable): shared-expert output rows [T][d_pad] and
 // per-token weights, added after the routed sub-experts; x_res (bf16 only,
@@ -66,7 +68,7 @@ void launch_shared_gate(const void* x, uint32_t T, uint32_t d, const float* gate
 // Tensor-core linear router (router_tc.cu): plan, weight split, launch, and
 // the fixed-order fp64 reduction of the K-split partials + top-k (route.cu).
 struct RouterTcPlan {
-    uint32_t Npad, kb_total, kb_per_split, ks, m_tiles, stages;
+    uint32_t Npad, kb_total, kb_per_split, ks, m_tiles, stages, chunk_kb;
     size_t smem;
 };
 RouterTcPlan plan_router_tc(uint32_t T, uint32_t d, uint32_t G, int num_sms);
@@ -87,7 +89,11 @@ void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32
 void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, double guard,
                          const void* x, uint32_t d, const float* wrT, uint32_t* ticket, uint32_t* n_fixed,
-                         BucketWs& ws, cudaStream_t s);
+                         BucketWs& ws, cudaStream_t s, uint32_t tb = kRouteTokensPerBlock);
+// tokens per CTA of the fused routing epilogue: 8 for small batches (more CTAs)
+inline uint32_t route_tokens_per_block(uint32_t T) { return T <= 1024 ? 8u : kRouteTokensPerBlock; }
+// in-place fixed-order sum of the K-split router partials into plane 0
+void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, cudaStream_t s);
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
                          const uint32_t* flagged, int num_sms, cudaStream_t s);

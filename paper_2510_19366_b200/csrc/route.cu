@@ -95,10 +95,14 @@ __device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uin
         vmax = m;
     }
     // softmax over all G cancels in the renormalisation: w_g = e^(l_g - m) / sum_sel
+    // (each exponential evaluated once)
     double z = 0.0;
+    double ex[NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-        if ((taken >> c) & 1u) z += exp(v[c] - vmax);
+    for (int c = 0; c < NC; ++c) {
+        ex[c] = ((taken >> c) & 1u) ? exp(v[c] - vmax) : 0.0;
+        z += ex[c];
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
     // ascending-index emission: index order is (c, lane)
@@ -111,7 +115,7 @@ __device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uin
         if (mine) {
             const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
             sel_row[pos] = lane + 32u * c;
-            w_row[pos] = weight_mode == 1 ? static_cast<float>(exp(v[c] - vmax) / z) : 1.0f;
+            w_row[pos] = weight_mode == 1 ? static_cast<float>(ex[c] / z) : 1.0f;
         }
         base += __popc(bal);
     }
@@ -185,9 +189,12 @@ __device__ double warp_topk_fast(const double* __restrict__ vals, uint32_t G, ui
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
     double z = 0.0;
+    double ex[NC];  // each exponential evaluated once
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-        if ((taken >> c) & 1u) z += exp(vals[lane + 32u * c] - m);
+    for (int c = 0; c < NC; ++c) {
+        ex[c] = ((taken >> c) & 1u) ? exp(vals[lane + 32u * c] - m) : 0.0;
+        z += ex[c];
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
     uint32_t base = 0;
@@ -199,7 +206,7 @@ __device__ double warp_topk_fast(const double* __restrict__ vals, uint32_t G, ui
         if (mine) {
             const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
             sel_row[pos] = lane + 32u * c;
-            w_row[pos] = weight_mode == 1 ? static_cast<float>(exp(vals[lane + 32u * c] - m) / z) : 1.0f;
+            w_row[pos] = weight_mode == 1 ? static_cast<float>(ex[c] / z) : 1.0f;
         }
         base += __popc(bal);
     }
@@ -630,7 +637,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     float* __restrict__ wout, int* __restrict__ err, double guard, const __nv_bfloat16* __restrict__ x, uint32_t d,
     const float* __restrict__ wrT, uint32_t* __restrict__ ticket, uint32_t* __restrict__ n_fixed, uint32_t* lrank,
     uint32_t* block_counts, uint32_t* block_base, uint32_t* offsets, uint32_t* mprefix_tc, uint32_t* mprefix_simt,
-    uint32_t* mprefix_tc2) {
+    uint32_t* mprefix_tc2, uint32_t tb) {
     extern __shared__ double rsm[];  // [TB][G] logits, then [TB][G] keys
     double* sc = rsm + (size_t)(threadIdx.x / 32) * G;
     double* key = rsm + (size_t)(TB + threadIdx.x / 32) * G;
@@ -643,7 +650,9 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     __shared__ uint32_t pair_tg[kMaxPairs];  // (token in CTA << 16) | candidate
     __shared__ double pair_part[kPairBatch][4];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t t0 = blockIdx.x * TB, t = t0 + warp;
+    // tb tokens per CTA (warps >= tb only help with the CTA-wide phases):
+    // small batches use tb = 8 so the token work spreads over 4x the SMs
+    const uint32_t t0 = blockIdx.x * tb, t = warp < tb ? t0 + warp : T;
     const uint32_t words = (G + 31) / 32;
     for (uint32_t q = threadIdx.x; q < TB * words; q += blockDim.x) msk[q / words][q % words] = 0;
     if (threadIdx.x == 0) n_pairs = 0;
@@ -717,7 +726,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         if (lane == 0) atomicAdd(n_fixed, 1u);
     }
     __syncthreads();  // this CTA's selections are visible to the CTA
-    for (uint32_t q = threadIdx.x; q < TB * k_max; q += blockDim.x) {
+    for (uint32_t q = threadIdx.x; q < tb * k_max; q += blockDim.x) {
         const uint32_t tt = q / k_max, j = q % k_max;
         if (t0 + tt >= T) continue;
         const uint32_t g = sel[(size_t)(t0 + tt) * k_max + j];
@@ -728,7 +737,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     __syncthreads();
     for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) {
         uint32_t cnt = 0;
-        for (uint32_t tt = 0; tt < TB && t0 + tt < T; ++tt)
+        for (uint32_t tt = 0; tt < tb && t0 + tt < T; ++tt)
             if ((msk[tt][g >> 5] >> (g & 31)) & 1u) lrank[(size_t)(t0 + tt) * k_max + slot_of[tt][g]] = cnt++;
         block_counts[(size_t)blockIdx.x * G + g] = cnt;
     }
@@ -753,11 +762,11 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
                                                        const uint32_t* __restrict__ block_base,
                                                        uint32_t* __restrict__ perm_tok, float* __restrict__ perm_w,
                                                        uint32_t* __restrict__ slot_row, Tx* __restrict__ x_perm,
-                                                       int* __restrict__ err, bool check_finite) {
+                                                       int* __restrict__ err, bool check_finite, uint32_t tb) {
     const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32;
     const uint32_t lane = threadIdx.x & 31;
     if (t >= T) return;
-    const uint32_t blk = t / TB;
+    const uint32_t blk = t / tb;
     for (uint32_t j = lane; j < k_max; j += 32) {
         const uint32_t g = sel[(size_t)t * k_max + j];
         uint32_t pos = kSelNone;
@@ -966,10 +975,32 @@ void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32
                                                      err, guard, flagged);
 }
 
+// In-place fixed-order reduction of the K-split router partials into plane 0
+// (ascending split order, the same sum route_bucket_kernel forms): for small
+// batches the splits are many (64-deep chunks) and the tokens few, so the
+// reduction is spread over (token, 32 sub-experts) warps instead of one warp
+// per token.
+__global__ void __launch_bounds__(256) partials_reduce_kernel(double* __restrict__ partial, uint32_t ks, uint32_t T,
+                                                              uint32_t G, uint32_t Npad) {
+    const uint32_t gw = (G + 31) / 32;
+    const uint32_t wid = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (wid >= T * gw) return;
+    const uint32_t t = wid / gw, g = (wid % gw) * 32 + lane;
+    if (g >= G) return;
+    double v = 0.0;
+    for (uint32_t s = 0; s < ks; ++s) v += partial[((size_t)s * T + t) * Npad + g];
+    partial[(size_t)t * Npad + g] = v;
+}
+
+void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, cudaStream_t s) {
+    const uint32_t warps = T * ((G + 31) / 32);
+    partials_reduce_kernel<<<(warps + 7) / 8, 256, 0, s>>>(partial, ks, T, G, Npad);
+}
+
 void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, double guard,
                          const void* x, uint32_t d, const float* wrT, uint32_t* ticket, uint32_t* n_fixed,
-                         BucketWs& ws, cudaStream_t s) {
+                         BucketWs& ws, cudaStream_t s, uint32_t tb) {
     const size_t smem = sizeof(double) * 2 * TB * G;
     static bool attr = false;
     if (!attr) {
@@ -977,10 +1008,10 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
                              (int)(sizeof(double) * 2 * TB * kMaxG));
         attr = true;
     }
-    route_bucket_kernel<<<(T + TB - 1) / TB, 1024, smem, s>>>(
+    route_bucket_kernel<<<(T + tb - 1) / tb, 1024, smem, s>>>(
         partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, guard,
         static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, n_fixed, ws.lrank, ws.block_counts, ws.block_base,
-        ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2);
+        ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb);
 }
 
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
@@ -1021,16 +1052,16 @@ void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s) {
 
 void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t d_pad, const uint32_t* sel,
                      const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s,
-                     bool check_finite) {
+                     bool check_finite, uint32_t tb) {
     const dim3 grid((T + 7) / 8);
     if (dtype == 1)
         dispatch_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
             static_cast<const __nv_bfloat16*>(x), T, d, d_pad, sel, w, k_max, G, ws.lrank, ws.block_base,
-            ws.perm_tok, ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), ws.err, check_finite);
+            ws.perm_tok, ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), ws.err, check_finite, tb);
     else
         dispatch_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), T, d, d_pad, sel, w, k_max, G,
                                                     ws.lrank, ws.block_base, ws.perm_tok, ws.perm_w, ws.slot_row,
-                                                    static_cast<float*>(x_perm), ws.err, check_finite);
+                                                    static_cast<float*>(x_perm), ws.err, check_finite, tb);
 }
 
 // Shared expert gate (Qwen-style): w_sh[t] = sigmoid(x_t . gate)

@@ -23,12 +23,12 @@ namespace mp {
 
 namespace {
 
-constexpr uint32_t BM = 128, BK = 64, kChunkKb = 4;  // 256-deep chunks
+constexpr uint32_t BM = 128, BK = 64, kChunkKb = 4;  // 256-deep chunks (64-deep for few token tiles)
 constexpr uint32_t kThreads = 192;
 constexpr uint32_t kMaxStages = 6;
 
 struct RouterTcParams {
-    uint32_t T, Npad, kb_total, kb_per_split, stages;
+    uint32_t T, Npad, kb_total, kb_per_split, stages, chunk_kb;
     double* partial;  // [KS][T][Npad]
 };
 
@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t s = it % p.stages, ph = (it / p.stages) & 1u;
                 mbar_wait(&full[s], ph);
                 tc_fence_after();
-                const uint32_t chunk = (kb - kb0) / kChunkKb;
-                const bool first = ((kb - kb0) % kChunkKb) == 0;
+                const uint32_t chunk = (kb - kb0) / p.chunk_kb;
+                const bool first = ((kb - kb0) % p.chunk_kb) == 0;
                 // hi plane and (mid + lo) planes in separate accumulators: the
                 // small planes never round at the hi accumulator's ulp
                 const uint32_t d_hi = tmem_base + chunk * 2 * p.Npad;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(tfull, 0);
         tc_fence_after();
         const uint32_t t = m0 + q * 32 + lane;
-        const uint32_t nchunks = (kb1 - kb0 + kChunkKb - 1) / kChunkKb;
+        const uint32_t nchunks = (kb1 - kb0 + p.chunk_kb - 1) / p.chunk_kb;
         double* out = p.partial + (static_cast<size_t>(blockIdx.y) * p.T + t) * p.Npad;
         for (uint32_t grp = 0; grp < p.Npad / 32; ++grp) {
             double acc[32];
@@ -169,7 +169,11 @@ RouterTcPlan plan_router_tc(uint32_t T, uint32_t d, uint32_t G, int num_sms) {
     pl.Npad = ((G + 31) / 32) * 32;
     pl.kb_total = (d + BK - 1) / BK;
     const uint32_t m_tiles = (T + BM - 1) / BM;
-    const uint32_t n_chunks = (pl.kb_total + kChunkKb - 1) / kChunkKb;
+    // few token tiles (decode): 64-deep chunks give 4x the K splits (CTAs),
+    // cutting the per-CTA operand stream that bounds small-batch latency
+    pl.chunk_kb = m_tiles * ((pl.kb_total + kChunkKb - 1) / kChunkKb) < static_cast<uint32_t>(num_sms) / 2 ? 1
+                                                                                                          : kChunkKb;
+    const uint32_t n_chunks = (pl.kb_total + pl.chunk_kb - 1) / pl.chunk_kb;
     const uint32_t max_chunks_per_cta = 512 / (2 * pl.Npad);
     uint32_t ks = (static_cast<uint32_t>(num_sms) + m_tiles - 1) / m_tiles;
     ks = ks < 1 ? 1 : ks;
@@ -177,7 +181,7 @@ RouterTcPlan plan_router_tc(uint32_t T, uint32_t d, uint32_t G, int num_sms) {
     const uint32_t ks_min = (n_chunks + max_chunks_per_cta - 1) / max_chunks_per_cta;
     if (ks < ks_min) ks = ks_min;
     const uint32_t chunks_per_split = (n_chunks + ks - 1) / ks;
-    pl.kb_per_split = chunks_per_split * kChunkKb;
+    pl.kb_per_split = chunks_per_split * pl.chunk_kb;
     pl.ks = (pl.kb_total + pl.kb_per_split - 1) / pl.kb_per_split;
     pl.m_tiles = m_tiles;
     const uint32_t stage_bytes = BM * BK * 2 + 3 * pl.Npad * BK * 2;
@@ -193,7 +197,7 @@ void launch_split_router(const float* wr, uint32_t d, uint32_t G, uint32_t Npad,
 
 void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const RouterTcPlan& pl, uint32_t T,
                       double* partial, cudaStream_t s) {
-    RouterTcParams p{T, pl.Npad, pl.kb_total, pl.kb_per_split, pl.stages, partial};
+    RouterTcParams p{T, pl.Npad, pl.kb_total, pl.kb_per_split, pl.stages, pl.chunk_kb, partial};
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
