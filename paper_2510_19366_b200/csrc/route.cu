@@ -8,6 +8,8 @@
 // bucketing / combine are SURVEY 8(a) a14/a15.  All HBM-bound: coalesced
 // 16-byte vector accesses, no atomics, fixed reduction orders (deterministic).
 #include <cfloat>
+#include <cstdlib>
+#include <string>
 #include <cmath>
 #include <type_traits>
 
@@ -827,6 +829,72 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
     if (__any_sync(0xffffffffu, bad) && lane == 0 && err) atomicOr(err, 2);
 }
 
+// Bulk-copy dispatch (bf16, d == d_pad, rows 16-byte multiples): warp per
+// token; lane 0 pulls the token's row into shared memory with one bulk copy
+// and pushes it to each of its k bucket rows with k bulk stores -- the copy
+// engine streams at HBM rate with no per-16-byte instructions; the warp checks
+// the row for non-finite values from shared memory meanwhile.
+constexpr uint32_t kBulkRowMax = 16384;  // bytes of one staged row (d <= 8192 bf16)
+__global__ void __launch_bounds__(128) dispatch_bulk_kernel(const __nv_bfloat16* __restrict__ x, uint32_t T,
+                                                            uint32_t d, const uint32_t* __restrict__ sel,
+                                                            const float* __restrict__ w, uint32_t k_max, uint32_t G,
+                                                            const uint32_t* __restrict__ lrank,
+                                                            const uint32_t* __restrict__ block_base,
+                                                            uint32_t* __restrict__ perm_tok,
+                                                            float* __restrict__ perm_w,
+                                                            uint32_t* __restrict__ slot_row,
+                                                            __nv_bfloat16* __restrict__ x_perm,
+                                                            int* __restrict__ err, uint32_t tb) {
+    extern __shared__ __align__(128) uint8_t drow[];  // [4 warps][row bytes]
+    __shared__ __align__(8) uint64_t bar[4];
+    const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const uint32_t t = blockIdx.x * 4 + warp;
+    const uint32_t row_bytes = d * 2;
+    uint8_t* srow = drow + (size_t)warp * row_bytes;
+    if (lane == 0) {
+        mbar_init(&bar[warp], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    if (t >= T) return;
+    if (lane == 0) {
+        mbar_expect_tx(&bar[warp], row_bytes);
+        bulk_load_g2s(srow, x + (size_t)t * d, row_bytes, &bar[warp]);
+    }
+    const uint32_t blk = t / tb;
+    uint32_t pos_a = kSelNone, pos_b = kSelNone;
+    for (uint32_t j = lane; j < k_max; j += 32) {
+        const uint32_t g = sel[(size_t)t * k_max + j];
+        uint32_t pos = kSelNone;
+        if (g != kSelNone && g < G) {
+            pos = block_base[(size_t)blk * G + g] + lrank[(size_t)t * k_max + j];
+            perm_tok[pos] = t;
+            perm_w[pos] = w ? w[(size_t)t * k_max + j] : 1.0f;
+        }
+        slot_row[(size_t)t * k_max + j] = pos;
+        if (j < 32) pos_a = pos;
+        else pos_b = pos;
+    }
+    mbar_wait(&bar[warp], 0);
+    // lane 0 issues one bulk store per selected slot (positions via shuffles)
+    for (uint32_t j = 0; j < k_max; ++j) {
+        const uint32_t pos = __shfl_sync(0xffffffffu, j < 32 ? pos_a : pos_b, j & 31);
+        if (pos != kSelNone && lane == 0) bulk_store_s2g(x_perm + (size_t)pos * d, srow, row_bytes);
+    }
+    if (lane == 0) bulk_commit();
+    // non-finite scan of the staged row (the reference's check_input)
+    bool bad = false;
+    for (uint32_t c = lane * 8; c < d; c += 256) {
+        const uint4 v = *reinterpret_cast<const uint4*>(srow + (size_t)c * 2);
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) bad |= !isfinite(__bfloat162float(h[q]));
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && err) atomicOr(err, 2);
+    if (lane == 0) bulk_wait0();  // stores complete (smem read out, global written) before the CTA exits
+    __syncwarp();
+}
+
 // ---------------------------------------------------------------- combine
 // y[t] = sum_{j ascending} w[t][j] * o[slot_row[t][j]] in a fixed order
 // (ascending sub-expert id), no atomics.  CTA per token.
@@ -1053,6 +1121,24 @@ void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s) {
 void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t d_pad, const uint32_t* sel,
                      const float* w, uint32_t k_max, uint32_t G, BucketWs& ws, void* x_perm, cudaStream_t s,
                      bool check_finite, uint32_t tb) {
+    static const bool bulk_env = [] {  // MOEPRISM_DISPATCH=vector: the 16-byte vector kernel (A/B)
+        const char* e = std::getenv("MOEPRISM_DISPATCH");
+        return !(e && std::string(e) == "vector");
+    }();
+    if (dtype == 1 && x_perm && d == d_pad && (d % 8) == 0 && d * 2 <= kBulkRowMax && bulk_env &&
+        (reinterpret_cast<uintptr_t>(x) % 16) == 0) {
+        const size_t smem = 4 * (size_t)d * 2;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(4 * kBulkRowMax));
+            attr = true;
+        }
+        dispatch_bulk_kernel<<<(T + 3) / 4, 128, smem, s>>>(
+            static_cast<const __nv_bfloat16*>(x), T, d, sel, w, k_max, G, ws.lrank, ws.block_base, ws.perm_tok,
+            ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), check_finite ? ws.err : nullptr, tb);
+        return;
+    }
     const dim3 grid((T + 7) / 8);
     if (dtype == 1)
         dispatch_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
