@@ -34,11 +34,13 @@ constexpr uint32_t kRouterThreads = 256;
 // keys (nullable): selection keys replacing sc for the ranking only (the
 // exact re-selection of near-tie tokens); the weights always use sc.
 // vk_out (nullable): the k-th and (k+1)-th best keys.
+// NC: 32-candidate chunks per lane held in registers (G <= 32 NC); smaller NC
+// for small G trims the unrolled per-round work (Mixtral: G = 64 -> NC = 2)
+template <int NC = kMaxG / 32>
 __device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uint32_t k, uint32_t k_max,
                                   int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row,
                                   const double* __restrict__ keys = nullptr, double* vk_out = nullptr) {
     const uint32_t lane = lane_id();
-    constexpr int NC = kMaxG / 32;
     const uint32_t nc = (G + 31) / 32;
     double v[NC];
     uint32_t taken = 0;  // bit c: value c of this lane selected
@@ -146,11 +148,11 @@ __device__ __forceinline__ float unpack_key(uint64_t p) {
     return __uint_as_float(b);
 }
 
+template <int NC = kMaxG / 32>
 __device__ double warp_topk_fast(const double* __restrict__ vals, uint32_t G, uint32_t k, uint32_t k_max,
                                  int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row,
                                  double* vk_out) {
     const uint32_t lane = lane_id();
-    constexpr int NC = kMaxG / 32;
     const uint32_t nc = (G + 31) / 32;
     uint64_t v[NC];
 #pragma unroll
@@ -633,6 +635,7 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
 //   3. per-CTA bucket ranks / histogram (bucket_local_kernel's scheme);
 //   4. the last CTA to finish (threadfence + atomic ticket) runs the
 //      device-wide scans, then resets the ticket.
+template <int NC>
 __global__ void __launch_bounds__(1024) route_bucket_kernel(
     const double* __restrict__ partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
     const uint32_t* __restrict__ kpt, uint32_t k_scalar, int weight_mode, uint32_t* __restrict__ sel,
@@ -669,7 +672,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         }
         __syncwarp();
         kt = token_k(kpt, k_scalar, t, k_max, G, err);
-        const double gap = warp_topk_fast(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
+        const double gap = warp_topk_fast<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
                                           wout + (size_t)t * k_max, vk[warp]);
         __syncwarp();
         flagged = gap < 2.0 * guard;
@@ -724,7 +727,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
                 }
         }
         __syncwarp();
-        warp_topk_token(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max, key);
+        warp_topk_token<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max, key);
         if (lane == 0) atomicAdd(n_fixed, 1u);
     }
     __syncthreads();  // this CTA's selections are visible to the CTA
@@ -1070,16 +1073,24 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
                          const void* x, uint32_t d, const float* wrT, uint32_t* ticket, uint32_t* n_fixed,
                          BucketWs& ws, cudaStream_t s, uint32_t tb) {
     const size_t smem = sizeof(double) * 2 * TB * G;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(route_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(sizeof(double) * 2 * TB * kMaxG));
-        attr = true;
-    }
-    route_bucket_kernel<<<(T + tb - 1) / tb, 1024, smem, s>>>(
-        partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, guard,
-        static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, n_fixed, ws.lrank, ws.block_counts, ws.block_base,
-        ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb);
+    static bool attr_set[3] = {false, false, false};
+    auto launch = [&](auto kern, int which) {
+        if (!attr_set[which]) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(double) * 2 * TB * kMaxG));
+            attr_set[which] = true;
+        }
+        kern<<<(T + tb - 1) / tb, 1024, smem, s>>>(
+            partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, guard,
+            static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, n_fixed, ws.lrank, ws.block_counts, ws.block_base,
+            ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb);
+    };
+    if (G <= 64)
+        launch(route_bucket_kernel<2>, 0);
+    else if (G <= 128)
+        launch(route_bucket_kernel<4>, 1);
+    else
+        launch(route_bucket_kernel<8>, 2);
 }
 
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
