@@ -466,3 +466,33 @@ def test_forward_host_batches_pipelined(oracle, torch_cuda):
     ys2 = L.forward_host_batches(xs[:2], k=3)  # a second call reuses the slots
     assert all(torch.equal(a, b) for a, b in zip(ys2, ys[:2]))
     L.close()
+
+
+def test_forward_is_cuda_graph_capturable(oracle, torch_cuda):
+    """The stream-ordered forward (router, fused routing epilogue, bulk
+    dispatch, grouped GEMMs, combine, shared-expert fork/join) captures into a
+    CUDA graph; replays equal eager forwards bit for bit (decode serving)."""
+    torch = torch_cuda
+    E, S, d, ff, T = 4, 4, 256, 512, 48
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T)
+    L = make_layer(experts, parts, wr, S, "bf16", k_max=4, max_tokens=T)
+    L.set_shared_expert(*(oracle.random_expert(d, 256, 9)), gate=oracle.uniform_pm1(3, d, 0.1))
+    xs = [torch.from_numpy(bf16_round(oracle.uniform_pm1(60 + i, T * d))).reshape(T, d).cuda().to(torch.bfloat16)
+          for i in range(2)]
+    ys = [torch.empty_like(xs[0]) for _ in range(2)]
+    want = [L.forward(xs[i], k=3).clone() for i in range(2)]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        L.forward(xs[0], k=3, y=ys[0])  # warm-up on the capture stream
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(2):
+                L.forward(xs[i], k=3, y=ys[i])
+    for _ in range(3):
+        ys[0].zero_()
+        ys[1].zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(ys[0], want[0]) and torch.equal(ys[1], want[1])
+    L.close()
