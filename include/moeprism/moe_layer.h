@@ -263,6 +263,18 @@ mp_status mp_layer_collect_activations(mp_layer_t h, uint32_t e, const void* x, 
 mp_status mp_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,
                            void* stream);
 mp_status mp_coactivation(const uint8_t* bits, uint32_t rows, uint32_t cols, uint32_t* co, void* stream);
+/* select_gate_neurons (inc/gating.hpp:72-103) on a device co-activation
+ * matrix: per sub-expert the r most central members (co-activation with the
+ * other members, diagonal excluded, ties to the lower neuron), ascending; host
+ * outputs gate_offsets[n_sub+1], gate_ids[...] (capacity <= dim). Exact. */
+mp_status mp_select_gate_neurons(const uint32_t* co, uint32_t dim, uint32_t n_sub, const uint32_t* assignment,
+                                 uint32_t r, uint32_t* gate_offsets, uint32_t* gate_ids, void* stream);
+/* gating_fidelity (inc/gating.hpp:149-174): mean top-k recall of the proxy
+ * selection against the true sub-expert norms over the rows of a device
+ * activation matrix; partition and gate set (CSR) on the host. */
+mp_status mp_gating_fidelity(const float* act, uint32_t rows, uint32_t cols, uint32_t n_sub,
+                             const uint32_t* assignment, const uint32_t* gate_offsets, const uint32_t* gate_ids,
+                             uint32_t k, double* out, void* stream);
 
 /* Host-only readers (no GPU touched), format-compatible with the reference.
  * mp_format_read_mpex <- load_toy_expert (inc/io.hpp:225-251): call with

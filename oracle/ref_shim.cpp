@@ -415,4 +415,54 @@ int ref_offload_replay(std::uint32_t n_units, std::uint32_t capacity, std::size_
         }
     });
 }
+
+// ---- gate construction / fidelity (inc/gating.hpp:28-174) and the C4 fixtures ----
+std::size_t ref_default_binarize_count(std::size_t cols) { return default_binarize_count(cols); }
+
+int ref_random_matrix(std::size_t rows, std::size_t cols, std::uint64_t seed, float* out) {
+    return guarded([&] {
+        ActivationMatrix m = testsupport::random_matrix(rows, cols, seed);
+        std::memcpy(out, m.data.data(), m.data.size() * sizeof(float));
+    });
+}
+
+int ref_planted_cluster(std::size_t tokens, std::uint32_t n_sub, std::size_t group, std::uint64_t seed, float* matrix,
+                        std::uint32_t* assignment) {
+    return guarded([&] {
+        auto pc = testsupport::planted_cluster(tokens, n_sub, group, seed);
+        std::memcpy(matrix, pc.matrix.data.data(), pc.matrix.data.size() * sizeof(float));
+        std::memcpy(assignment, pc.partition.assignment.data(), pc.partition.assignment.size() * 4);
+    });
+}
+
+int ref_select_gate_neurons(const std::uint32_t* co, std::size_t dim, std::uint32_t n_sub,
+                            const std::uint32_t* assignment, std::uint32_t r, std::uint32_t* offsets,
+                            std::uint32_t* ids) {
+    return guarded([&] {
+        CoActivationMatrix c;
+        c.dim = dim;
+        c.data.assign(co, co + dim * dim);
+        GateSet g = select_gate_neurons(c, make_partition(n_sub, dim, assignment), r);
+        offsets[0] = 0;
+        for (std::uint32_t q = 0; q < n_sub; ++q) {
+            offsets[q + 1] = offsets[q] + static_cast<std::uint32_t>(g.gate_neurons[q].size());
+            std::copy(g.gate_neurons[q].begin(), g.gate_neurons[q].end(), ids + offsets[q]);
+        }
+    });
+}
+
+int ref_gating_fidelity(const float* act, std::size_t rows, std::size_t cols, std::uint32_t n_sub,
+                        const std::uint32_t* assignment, std::uint32_t r, const std::uint32_t* offsets,
+                        const std::uint32_t* ids, std::uint32_t k, double* out) {
+    return guarded([&] {
+        ActivationMatrix m = make_activation_matrix(rows, cols);
+        m.data.assign(act, act + rows * cols);
+        GateSet g;
+        g.n_subexperts = n_sub;
+        g.r = r;
+        g.gate_neurons.resize(n_sub);
+        for (std::uint32_t q = 0; q < n_sub; ++q) g.gate_neurons[q].assign(ids + offsets[q], ids + offsets[q + 1]);
+        *out = gating_fidelity(m, make_partition(n_sub, cols, assignment), g, k);
+    });
+}
 }  // extern "C"

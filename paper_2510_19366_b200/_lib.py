@@ -28,7 +28,8 @@ EXPORTS = (
     "mp_layer_load_expert", "mp_layer_load_expert_file", "mp_layer_set_partition", "mp_layer_load_partition_map",
     "mp_layer_set_router", "mp_layer_set_gates", "mp_layer_set_shared_expert", "mp_layer_set_residual",
     "mp_layer_collect_activations", "mp_binarize_topk", "mp_coactivation", "mp_format_write_mpam", "mp_format_read_mpam",
-    "mp_layer_enable_offload", "mp_layer_offload_stats", "mp_layer_forward_host_batches", "mp_layer_forward", "mp_layer_forward_host",
+    "mp_layer_enable_offload", "mp_layer_offload_stats", "mp_layer_forward_host_batches",
+    "mp_select_gate_neurons", "mp_gating_fidelity", "mp_layer_forward", "mp_layer_forward_host",
     "mp_layer_forward_selected", "mp_layer_route", "mp_layer_check_errors", "mp_layer_set_profiling",
     "mp_layer_stage_times", "mp_layer_reset_stage_times", "mp_layer_launch_count", "mp_synth_fill",
     "mp_format_read_mpex", "mp_format_read_partition_doc", "mp_validate_partition", "mp_layer_forward_selected_host",
@@ -82,6 +83,8 @@ def _sig(L):
     L.mp_format_read_mpam.argtypes = [C.c_char_p, C.POINTER(u32), C.POINTER(u32), vp]
     L.mp_layer_enable_offload.argtypes = [vp, u32, u32]
     L.mp_layer_forward_host_batches.argtypes = [vp, u32, vp, vp, u32, vp, vp]
+    L.mp_select_gate_neurons.argtypes = [vp, u32, u32, vp, u32, vp, vp, vp]
+    L.mp_gating_fidelity.argtypes = [vp, u32, u32, u32, vp, vp, vp, u32, C.POINTER(C.c_double), vp]
     L.mp_layer_offload_stats.argtypes = [vp, vp, vp, vp, vp, u32, vp, vp]
     L.mp_layer_forward.argtypes = [vp, vp, u32, vp, u32, vp, vp, vp, vp, vp]
     L.mp_layer_forward_host.argtypes = [vp, vp, u32, vp, u32, vp, vp, vp, vp, vp]

@@ -4,6 +4,8 @@ through the C-ABI (libmoeprism_b200.so):
   collect_activations <- collect_activation_matrix (inc/expert.hpp:137-151)
   binarize_topk       <- binarize_topk             (inc/activation.hpp:213-240)
   coactivation        <- coactivation              (inc/activation.hpp:242-266)
+  select_gate_neurons <- select_gate_neurons       (inc/gating.hpp:72-103)
+  gating_fidelity     <- gating_fidelity           (inc/gating.hpp:149-174)
   write_mpam/read_mpam<- save_/load_activation_matrix (inc/io.hpp:147-200)
   measure_perf_table  -> the "batch,k,latency_s" CSV that load_perf_table
                          (inc/perfmodel.hpp:122-201) reads: the measured cost
@@ -63,6 +65,32 @@ def coactivation(bits, stream=None):
     co = torch.empty((cols, cols), dtype=torch.int32, device=bits.device)
     check(_lib.load().mp_coactivation(bits.data_ptr(), rows, cols, co.data_ptr(), _stream(stream)))
     return co
+
+
+def select_gate_neurons(co, assignment, n_sub: int, r: int, stream=None):
+    """select_gate_neurons (inc/gating.hpp:72-103) on a device co-activation
+    matrix; returns the per-sub-expert ascending gate neuron lists."""
+    a = np.ascontiguousarray(assignment, np.uint32)
+    dim = a.size
+    off = np.zeros(n_sub + 1, np.uint32)
+    ids = np.zeros(max(dim, 1), np.uint32)
+    check(_lib.load().mp_select_gate_neurons(co.data_ptr(), dim, n_sub, a.ctypes.data, r, off.ctypes.data,
+                                            ids.ctypes.data, _stream(stream)))
+    return [ids[off[q]:off[q + 1]].tolist() for q in range(n_sub)]
+
+
+def gating_fidelity(act, assignment, n_sub: int, gates, k: int, stream=None) -> float:
+    """gating_fidelity (inc/gating.hpp:149-174) over a device activation matrix."""
+    a = np.ascontiguousarray(assignment, np.uint32)
+    off = np.zeros(n_sub + 1, np.uint32)
+    for q, g in enumerate(gates):
+        off[q + 1] = off[q] + len(g)
+    ids = np.ascontiguousarray(np.concatenate([np.asarray(g, np.uint32) for g in gates]), np.uint32)
+    out = C.c_double()
+    act = act.contiguous()
+    check(_lib.load().mp_gating_fidelity(act.data_ptr(), act.shape[0], act.shape[1], n_sub, a.ctypes.data,
+                                        off.ctypes.data, ids.ctypes.data, k, C.byref(out), _stream(stream)))
+    return out.value
 
 
 def write_mpam(path, act: np.ndarray):

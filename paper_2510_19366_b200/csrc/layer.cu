@@ -1579,3 +1579,122 @@ MP_API mp_status mp_layer_offload_stats(mp_layer_t L, uint64_t* hits, uint64_t* 
             for (size_t i = 0; i < L->off_last_req.size() && i < cap; ++i) last_units[i] = L->off_last_req[i];
     });
 }
+
+// ---- proxy-gate construction and its fidelity (inc/gating.hpp:47-174) ----
+namespace {
+// ascending member lists of a partition as CSR (subexpert_members, inc/partition.hpp:49-55)
+void members_csr(uint32_t n_sub, const uint32_t* a, uint32_t n, std::vector<uint32_t>& off,
+                 std::vector<uint32_t>& mem) {
+    off.assign(n_sub + 1, 0);
+    for (uint32_t c = 0; c < n; ++c) ++off[a[c] + 1];
+    for (uint32_t s = 0; s < n_sub; ++s) off[s + 1] += off[s];
+    mem.assign(n, 0);
+    std::vector<uint32_t> fill(off.begin(), off.end() - 1);
+    for (uint32_t c = 0; c < n; ++c) mem[fill[a[c]]++] = c;
+}
+template <class T>
+T* upload_async(const std::vector<T>& v, cudaStream_t s, std::vector<void*>& owned) {
+    void* p = nullptr;
+    ck(cudaMallocAsync(&p, std::max<size_t>(v.size(), 1) * sizeof(T), s), "calibration scratch");
+    owned.push_back(p);
+    if (!v.empty()) ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "upload");
+    return static_cast<T*>(p);
+}
+void* scratch_async(size_t bytes, cudaStream_t s, std::vector<void*>& owned) {
+    void* p = nullptr;
+    ck(cudaMallocAsync(&p, std::max<size_t>(bytes, 1), s), "calibration scratch");
+    owned.push_back(p);
+    return p;
+}
+struct ScratchGuard {
+    std::vector<void*> owned;
+    cudaStream_t s;
+    ~ScratchGuard() {
+        for (void* p : owned) cudaFreeAsync(p, s);
+    }
+};
+}  // namespace
+
+// select_gate_neurons (inc/gating.hpp:72-103) over a device co-activation
+// matrix [dim][dim] u32: per sub-expert the r most central members (centrality
+// = co-activation with the other members, diagonal excluded; ties to the lower
+// neuron), ascending.  Outputs on the host: gate_offsets[n_sub + 1] and
+// gate_ids[gate_offsets[n_sub]] (capacity sum_s min(r, |group s|) <= dim).
+MP_API mp_status mp_select_gate_neurons(const uint32_t* co, uint32_t dim, uint32_t n_sub, const uint32_t* assignment,
+                                        uint32_t r, uint32_t* gate_offsets, uint32_t* gate_ids, void* stream) {
+    return guarded([&] {
+        if (!co || !assignment || !gate_offsets || !gate_ids) fail(MP_ERR_VALIDATION, "null argument");
+        mp::validate_partition(n_sub, assignment, dim);
+        if (r < 1) fail(MP_ERR_VALIDATION, "gate neuron count r must be >= 1");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        std::vector<uint32_t> off, mem, label(assignment, assignment + dim), out_off(n_sub + 1, 0);
+        members_csr(n_sub, assignment, dim, off, mem);
+        for (uint32_t q = 0; q < n_sub; ++q) out_off[q + 1] = out_off[q] + std::min(r, off[q + 1] - off[q]);
+        ScratchGuard sg{{}, s};
+        uint32_t* d_label = upload_async(label, s, sg.owned);
+        uint32_t* d_off = upload_async(off, s, sg.owned);
+        uint32_t* d_mem = upload_async(mem, s, sg.owned);
+        uint32_t* d_oo = upload_async(out_off, s, sg.owned);
+        auto* d_score = static_cast<unsigned long long*>(scratch_async((size_t)dim * 8, s, sg.owned));
+        auto* d_out = static_cast<uint32_t*>(scratch_async((size_t)out_off[n_sub] * 4, s, sg.owned));
+        mp::launch_centrality(co, dim, d_label, d_off, d_mem, d_score, s);
+        mp::launch_gate_select(d_score, d_off, d_mem, n_sub, r, d_oo, d_out, s);
+        ck_launch("select_gate_neurons");
+        ck(cudaMemcpyAsync(gate_ids, d_out, (size_t)out_off[n_sub] * 4, cudaMemcpyDeviceToHost, s), "gate ids");
+        ck(cudaStreamSynchronize(s), "select_gate_neurons");
+        std::copy(out_off.begin(), out_off.end(), gate_offsets);
+    });
+}
+
+// gating_fidelity (inc/gating.hpp:149-174): mean over rows of the top-k recall
+// of the proxy selection (mean |a| over each sub-expert's gate neurons)
+// against the selection on the true sub-expert norms (subexpert_norms,
+// inc/partition.hpp:78-95).  act: device [rows][cols] fp32; the partition and
+// the gate set (CSR, ascending ids) on the host.  Same double sums in the
+// same order as the reference; the row recalls are summed in row order.
+MP_API mp_status mp_gating_fidelity(const float* act, uint32_t rows, uint32_t cols, uint32_t n_sub,
+                                    const uint32_t* assignment, const uint32_t* gate_offsets,
+                                    const uint32_t* gate_ids, uint32_t k, double* out, void* stream) {
+    return guarded([&] {
+        if (!act || !assignment || !gate_offsets || !gate_ids || !out) fail(MP_ERR_VALIDATION, "null argument");
+        if (rows < 1 || cols < 1)
+            fail(MP_ERR_VALIDATION, "activation matrix must have at least one row and one column");
+        mp::validate_partition(n_sub, assignment, cols);
+        if (n_sub > 256) fail(MP_ERR_VALIDATION, "at most 256 sub-experts per expert");
+        for (uint32_t q = 0; q < n_sub; ++q) {  // validate(GateSet), inc/gating.hpp:33-43
+            if (gate_offsets[q + 1] <= gate_offsets[q])
+                fail(MP_ERR_VALIDATION, "every sub-expert needs at least one gate neuron");
+            for (uint32_t g = gate_offsets[q]; g < gate_offsets[q + 1]; ++g) {
+                if (gate_ids[g] >= cols)
+                    fail(MP_ERR_VALIDATION, "gate neuron " + std::to_string(gate_ids[g]) +
+                                                " out of range for activation vector of length " +
+                                                std::to_string(cols));
+                if (g > gate_offsets[q] && gate_ids[g] < gate_ids[g - 1])
+                    fail(MP_ERR_VALIDATION, "gate neuron lists must be ascending");
+            }
+        }
+        if (k < 1 || k > n_sub)
+            fail(MP_ERR_VALIDATION,
+                 "k_active = " + std::to_string(k) + " out of range [1, " + std::to_string(n_sub) + "]");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        std::vector<uint32_t> off, mem;
+        members_csr(n_sub, assignment, cols, off, mem);
+        std::vector<uint32_t> goff(gate_offsets, gate_offsets + n_sub + 1), gids(gate_ids, gate_ids + goff[n_sub]);
+        ScratchGuard sg{{}, s};
+        uint32_t* d_off = upload_async(off, s, sg.owned);
+        uint32_t* d_mem = upload_async(mem, s, sg.owned);
+        uint32_t* d_goff = upload_async(goff, s, sg.owned);
+        uint32_t* d_gids = upload_async(gids, s, sg.owned);
+        auto* d_norm = static_cast<double*>(scratch_async((size_t)rows * n_sub * 8, s, sg.owned));
+        auto* d_proxy = static_cast<double*>(scratch_async((size_t)rows * n_sub * 8, s, sg.owned));
+        auto* d_recall = static_cast<double*>(scratch_async((size_t)rows * 8, s, sg.owned));
+        mp::launch_fidelity(act, rows, cols, n_sub, d_off, d_mem, d_goff, d_gids, k, d_norm, d_proxy, d_recall, s);
+        ck_launch("gating_fidelity");
+        std::vector<double> recall(rows);
+        ck(cudaMemcpyAsync(recall.data(), d_recall, (size_t)rows * 8, cudaMemcpyDeviceToHost, s), "recall");
+        ck(cudaStreamSynchronize(s), "gating_fidelity");
+        double total = 0.0;
+        for (double v : recall) total += v;
+        *out = total / static_cast<double>(rows);
+    });
+}

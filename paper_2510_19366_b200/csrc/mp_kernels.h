@@ -148,6 +148,13 @@ void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB
 void launch_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,
                           cudaStream_t s);
 void launch_bits_to_bf16_t(const uint8_t* bits, uint32_t rows, uint32_t cols, uint32_t ld, void* out, cudaStream_t s);
+void launch_centrality(const uint32_t* co, uint32_t dim, const uint32_t* label, const uint32_t* mem_off,
+                       const uint32_t* members, unsigned long long* score, cudaStream_t s);
+void launch_gate_select(const unsigned long long* score, const uint32_t* mem_off, const uint32_t* members,
+                        uint32_t n_sub, uint32_t r, const uint32_t* out_off, uint32_t* out, cudaStream_t s);
+void launch_fidelity(const float* act, uint32_t rows, uint32_t cols, uint32_t n_sub, const uint32_t* mem_off,
+                     const uint32_t* members, const uint32_t* gate_off, const uint32_t* gate_ids, uint32_t k,
+                     double* norm, double* proxy, double* recall, cudaStream_t s);
 // meta = {0, rows, 0, ceil(rows / 128)}: offsets + 128-row tile prefix of one group
 void launch_set_group_meta(uint32_t* meta, uint32_t rows, cudaStream_t s);
 

@@ -262,6 +262,13 @@ class RefLib:
         L.ref_coactivation.argtypes = [C.c_void_p, _sz, _sz, _sz, _u32p]
         L.ref_save_activation_matrix.argtypes = [C.c_char_p, _sz, _sz, _f32p]
         L.ref_offload_replay.argtypes = [C.c_uint32, C.c_uint32, _sz, _u32p, _u32p, _u64p]
+        L.ref_default_binarize_count.argtypes = [_sz]
+        L.ref_default_binarize_count.restype = _sz
+        L.ref_random_matrix.argtypes = [_sz, _sz, C.c_uint64, _f32p]
+        L.ref_planted_cluster.argtypes = [_sz, C.c_uint32, _sz, C.c_uint64, _f32p, _u32p]
+        L.ref_select_gate_neurons.argtypes = [_u32p, _sz, C.c_uint32, _u32p, C.c_uint32, _u32p, _u32p]
+        L.ref_gating_fidelity.argtypes = [_f32p, _sz, _sz, C.c_uint32, _u32p, C.c_uint32, _u32p, _u32p, C.c_uint32,
+                                          C.POINTER(C.c_double)]
         L.ref_load_activation_matrix.argtypes = [C.c_char_p, C.POINTER(_sz), C.POINTER(_sz), C.c_void_p]
         L.ref_perf_table_eval.argtypes = [C.c_char_p, C.c_uint64, C.c_uint32, C.POINTER(C.c_double), C.POINTER(_sz),
                                           C.POINTER(_sz)]
@@ -342,6 +349,40 @@ class RefLib:
         out = np.zeros(len(steps), np.uint64)
         self._check(self.L.ref_offload_replay(n_units, capacity, len(steps), off, ids, out))
         return out
+
+    def default_binarize_count(self, cols):
+        return int(self.L.ref_default_binarize_count(cols))
+
+    def random_matrix(self, rows, cols, seed):
+        out = np.empty((rows, cols), np.float32)
+        self._check(self.L.ref_random_matrix(rows, cols, seed, out.reshape(-1)))
+        return out
+
+    def planted_cluster(self, tokens, n_sub, group, seed):
+        m = np.empty((tokens, n_sub * group), np.float32)
+        a = np.empty(n_sub * group, np.uint32)
+        self._check(self.L.ref_planted_cluster(tokens, n_sub, group, seed, m.reshape(-1), a))
+        return m, a
+
+    def select_gate_neurons(self, co, assignment, n_sub, r):
+        co = np.ascontiguousarray(co, np.uint32)
+        a = np.ascontiguousarray(assignment, np.uint32)
+        off = np.zeros(n_sub + 1, np.uint32)
+        ids = np.zeros(max(a.size, 1), np.uint32)
+        self._check(self.L.ref_select_gate_neurons(co.reshape(-1), a.size, n_sub, a, r, off, ids))
+        return [ids[off[q]:off[q + 1]].tolist() for q in range(n_sub)]
+
+    def gating_fidelity(self, act, assignment, n_sub, gates, r, k):
+        act = np.ascontiguousarray(act, np.float32)
+        a = np.ascontiguousarray(assignment, np.uint32)
+        off = np.zeros(n_sub + 1, np.uint32)
+        for q, g in enumerate(gates):
+            off[q + 1] = off[q] + len(g)
+        ids = np.ascontiguousarray(np.concatenate([np.asarray(g, np.uint32) for g in gates]), np.uint32)
+        out = C.c_double()
+        self._check(self.L.ref_gating_fidelity(act.reshape(-1), act.shape[0], act.shape[1], n_sub, a, r, off, ids, k,
+                                               C.byref(out)))
+        return out.value
 
     def perf_table_eval(self, path, batch, k):
         """load_perf_table (with its grid / monotonicity validation) + eval_cost."""

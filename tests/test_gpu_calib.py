@@ -105,3 +105,69 @@ def test_perf_table_measured_loads_in_reference(oracle, torch_cuda, tmp_path):
         cost, nb, nk = RefLib().perf_table_eval(tmp_path / "perf.csv", 128, 4)
         assert (nb, nk) == (3, 4) and math.isclose(cost, lat[(128, 4)], rel_tol=1e-6)
     L.close()
+
+
+def test_acceptance_c4_gating_fidelity_on_gpu(ref, torch_cuda):
+    """Acceptance C4 (tests/acceptance.cpp:166-206) through the GPU pipeline:
+    binarize_topk -> coactivation -> select_gate_neurons -> gating_fidelity,
+    every stage equal to the reference; saturated gates (r = group size) give
+    fidelity exactly 1 for every k, planted clusters recall >= 0.95 with r = 1."""
+    torch = torch_cuda
+    from paper_2510_19366_b200.calibrate import binarize_topk, coactivation, gating_fidelity, select_gate_neurons
+    for trial in range(20):
+        rng = np.random.default_rng(4000 + trial)  # shapes only (the reference draws its own with mt19937_64)
+        n = int(rng.integers(2, 6))
+        group = int(rng.integers(2, 7))
+        cols, rows = n * group, int(rng.integers(8, 33))
+        m = ref.random_matrix(rows, cols, 9000 + trial)
+        part = ref.random_balanced_partition(cols, n, 9500 + trial)
+        k_a = ref.default_binarize_count(cols)
+        md = torch.from_numpy(m).cuda()
+        bits = binarize_topk(md, k_a)
+        assert np.array_equal(bits.cpu().numpy(), ref.binarize_topk(m, k_a))
+        co = coactivation(bits)
+        co_ref = ref.coactivation(bits.cpu().numpy(), k_a)
+        assert np.array_equal(co.cpu().numpy().view(np.uint32), co_ref)
+        gates = select_gate_neurons(co, part, n, group)
+        assert gates == ref.select_gate_neurons(co_ref, part, n, group)
+        for k in range(1, n + 1):
+            f = gating_fidelity(md, part, n, gates, k)
+            assert f == ref.gating_fidelity(m, part, n, gates, group, k) == 1.0
+    recalls = []
+    for trial in range(20):
+        m, part = ref.planted_cluster(64, 4, 8, 10000 + trial)
+        md = torch.from_numpy(m).cuda()
+        bits = binarize_topk(md, ref.default_binarize_count(m.shape[1]))
+        co = coactivation(bits)
+        gates = select_gate_neurons(co, part, 4, 1)
+        assert gates == ref.select_gate_neurons(co.cpu().numpy().view(np.uint32), part, 4, 1)
+        f = gating_fidelity(md, part, 4, gates, 1)
+        assert f == ref.gating_fidelity(m, part, 4, gates, 1, 1)
+        recalls.append(f)
+    assert min(recalls) >= 0.95
+
+
+def test_gate_selection_and_fidelity_mixtral_expert(oracle, torch_cuda):
+    """The proxy-gate pipeline at the Mixtral expert shape (14336 neurons, 8
+    sub-experts of 1792) on 512 calibration tokens: gates equal the reference's
+    select_gate_neurons on the same co-activation matrix; fidelity equals the
+    reference's on the same activations (when the reference build is present)."""
+    torch = torch_cuda
+    import bench
+    from oracle_lib import RefLib, have_ref
+    from paper_2510_19366_b200.calibrate import (binarize_topk, coactivation, collect_activations, gating_fidelity,
+                                                select_gate_neurons)
+    L, xs = bench.build_layer(0, 512, 2)
+    act = collect_activations(L, 2, xs[0])
+    co = coactivation(binarize_topk(act, 1434))
+    part = bench.balanced_partition(14336, 8, 6002)
+    gates = select_gate_neurons(co, part, 8, 4)
+    assert all(len(g) == 4 and g == sorted(g) and all(part[j] == s for j in g) for s, g in enumerate(gates))
+    f = gating_fidelity(act, part, 8, gates, 2)
+    assert 0.0 <= f <= 1.0
+    if have_ref():
+        r = RefLib()
+        c = co.cpu().numpy().view(np.uint32)
+        assert gates == r.select_gate_neurons(c, part, 8, 4)
+        assert f == r.gating_fidelity(act.cpu().numpy(), part, 8, gates, 4, 2)
+    L.close()
