@@ -150,7 +150,7 @@ def build_layer(local, T, k_max):
     return L, xs
 
 
-def build_ep_layer(local, rank, world, T, k_max=16):
+def build_ep_layer(local, rank, world, T, k_max=16, transport="nccl"):
     """Expert-parallel layer: E/world parent experts on this rank,
     the router replicated, tokens exchanged by NCCL all-to-all."""
     import torch
@@ -178,6 +178,9 @@ def build_ep_layer(local, rank, world, T, k_max=16):
         synth_fill(x, 11 + 1000 * i + 100000 * rank, 1.0)
         xs.append(x)
     torch.cuda.synchronize()
+    if transport == "p2p":
+        from paper_2510_19366_b200.ep import PeerExpertParallelLayer
+        return PeerExpertParallelLayer(ops), ops, xs
     return ExpertParallelLayer(ops), ops, xs
 
 
@@ -582,8 +585,9 @@ def workload_config(args, world):
                         "8 experts x 8 sub-experts (w=1792), linear fp32 router, softmax-renormalised top-k",
             "d_model": D, "d_ff": FF, "experts": E, "subexperts_per_expert": S, "tokens_per_gpu": args.tokens,
             "k": args.k, "global_tokens": args.tokens * world,
-            "parallelism": (f"ep{world} (experts sharded, NCCL all-to-all)" if world > 1 or args.force_ep
-                            else "single"),
+            "parallelism": ((f"ep{world} (experts sharded, "
+                             + ("peer-memory stores" if args.ep_transport == "p2p" else "NCCL all-to-all") + ")")
+                            if world > 1 or args.force_ep else "single"),
             "l2": f"x rotates over {N_XBUF} buffers ({N_XBUF * args.tokens * D * 2 / 1e6:.0f} MB) + 2.8 GB weights, "
                   "both > 126 MB L2"}
 
@@ -603,6 +607,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-ep", action="store_true", help="run the expert-parallel path even at N=1 (loopback)")
+    ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "p2p"],
+                    help="N>1 token exchange: NCCL all-to-all, or direct peer-memory stores (CUDA IPC / NVLink)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the other BASELINE configs (Qwen shape, 32-layer stack, 32k mixed-QoS batch) "
                          "and the calibration timing")
@@ -632,7 +638,7 @@ def main():
         def fwd(x, k, kpt, y=None):
             return L.forward(x, k=k, k_per_token=kpt, y=y)
     else:
-        ep_layer, ops, xs = build_ep_layer(local, rank, world, T)
+        ep_layer, ops, xs = build_ep_layer(local, rank, world, T, transport=args.ep_transport)
         layers = [ops.router, ops.local]
 
         def fwd(x, k, kpt, y=None):
@@ -649,7 +655,8 @@ def main():
     ms = time_steps(step, args.steps, args.warmup, world)
     launches = (sum(x.launch_count() for x in layers) - n0) // (args.steps + args.warmup) * args.steps
     if use_ep:
-        launches += 6 * args.steps  # mp_ep_plan (4 kernels), mp_ep_pack, mp_ep_combine per step
+        # mp_ep_plan (4 kernels), pack, combine (+ the peer-memory return kernel) per step
+        launches += (7 if args.ep_transport == "p2p" else 6) * args.steps
     value = world * T / (ms * 1e-3)
 
     # per-stage device times (CUDA events on the forward's stream), the sweep

@@ -276,6 +276,28 @@ mp_status mp_gating_fidelity(const float* act, uint32_t rows, uint32_t cols, uin
                              const uint32_t* assignment, const uint32_t* gate_offsets, const uint32_t* gate_ids,
                              uint32_t k, double* out, void* stream);
 
+/* Peer-memory exchange (the all-to-alls as direct stores into the peers'
+ * buffers: CUDA IPC handles, NVLink between the GPUs of a node).
+ * setup: allocates this rank's receive (x rows, selection, weights) and
+ *   return buffers and writes their 4 IPC handles (4 x 64 bytes) to `handles`;
+ * open: all_handles = every rank's 4 handles, rank-major (world x 256 bytes);
+ * p2p_pack: after mp_ep_plan, with counts = the all-gathered plan
+ *   (world x world, counts[s*world + d] = rows s sends to d): writes this
+ *   rank's rows straight into each destination's receive buffer; *n_recv =
+ *   rows this rank will receive.  The caller then makes every rank's pack
+ *   complete (stream sync + a host barrier) before the expert layers read;
+ * recv_buffers: the receive buffers (rows grouped by source rank, ascending);
+ * p2p_return: the expert partials (n_recv x d) go straight back into the
+ *   sources' return buffers; barrier again; p2p_combine: as mp_ep_combine
+ *   from this rank's return buffer. */
+mp_status mp_ep_p2p_setup(mp_ep_t ep, uint32_t max_recv_rows, uint8_t* handles);
+mp_status mp_ep_p2p_open(mp_ep_t ep, const uint8_t* all_handles);
+mp_status mp_ep_p2p_pack(mp_ep_t ep, const void* x, const uint32_t* sel, const float* w, uint32_t n_tokens,
+                         const uint32_t* counts, uint32_t* n_recv, void* stream);
+mp_status mp_ep_p2p_recv_buffers(mp_ep_t ep, void** recv_x, uint32_t** recv_sel, float** recv_w);
+mp_status mp_ep_p2p_return(mp_ep_t ep, const void* part, uint32_t n_recv, void* stream);
+mp_status mp_ep_p2p_combine(mp_ep_t ep, uint32_t n_tokens, void* y, void* stream);
+
 /* Host-only readers (no GPU touched), format-compatible with the reference.
  * mp_format_read_mpex <- load_toy_expert (inc/io.hpp:225-251): call with
  * null weight pointers to learn the dims, then with d_model*d_ff buffers.

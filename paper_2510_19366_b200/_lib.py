@@ -29,7 +29,9 @@ EXPORTS = (
     "mp_layer_set_router", "mp_layer_set_gates", "mp_layer_set_shared_expert", "mp_layer_set_residual",
     "mp_layer_collect_activations", "mp_binarize_topk", "mp_coactivation", "mp_format_write_mpam", "mp_format_read_mpam",
     "mp_layer_enable_offload", "mp_layer_offload_stats", "mp_layer_forward_host_batches",
-    "mp_select_gate_neurons", "mp_gating_fidelity", "mp_layer_forward", "mp_layer_forward_host",
+    "mp_select_gate_neurons", "mp_gating_fidelity",
+    "mp_ep_p2p_setup", "mp_ep_p2p_open", "mp_ep_p2p_pack", "mp_ep_p2p_recv_buffers", "mp_ep_p2p_return",
+    "mp_ep_p2p_combine", "mp_layer_forward", "mp_layer_forward_host",
     "mp_layer_forward_selected", "mp_layer_route", "mp_layer_check_errors", "mp_layer_set_profiling",
     "mp_layer_stage_times", "mp_layer_reset_stage_times", "mp_layer_launch_count", "mp_synth_fill",
     "mp_format_read_mpex", "mp_format_read_partition_doc", "mp_validate_partition", "mp_layer_forward_selected_host",
@@ -105,6 +107,12 @@ def _sig(L):
     L.mp_ep_create.argtypes = [u32, u32, u32, u32, u32, u32, u32, u32, i32, C.POINTER(vp)]
     L.mp_ep_create_subexpert.argtypes = [u32, u32, u32, u32, u32, u32, u32, u32, i32, C.POINTER(vp)]
     L.mp_ep_destroy.argtypes = [vp]
+    L.mp_ep_p2p_setup.argtypes = [vp, u32, vp]
+    L.mp_ep_p2p_open.argtypes = [vp, vp]
+    L.mp_ep_p2p_pack.argtypes = [vp, vp, vp, vp, u32, vp, C.POINTER(u32), vp]
+    L.mp_ep_p2p_recv_buffers.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]
+    L.mp_ep_p2p_return.argtypes = [vp, vp, u32, vp]
+    L.mp_ep_p2p_combine.argtypes = [vp, u32, vp, vp]
     L.mp_ep_plan.argtypes = [vp, vp, u32, vp, vp]
     L.mp_ep_pack.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp]
     L.mp_ep_combine.argtypes = [vp, vp, u32, vp, vp]

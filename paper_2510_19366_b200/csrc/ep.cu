@@ -54,20 +54,34 @@ __global__ void ep_slot_kernel(const uint32_t* __restrict__ dest, const uint32_t
                                 : block_base[(size_t)(t / kRouteTokensPerBlock) * world + r] + lrank[q];
 }
 
+// Destinations of the packed rows: with P2P, rank r's rows go straight into
+// rank r's receive buffers (CUDA IPC / NVLink peer pointers) at row
+// base[r] + (pos - send_off[r]); locally (NCCL path) every destination is the
+// one send buffer with base[r] = send_off[r], i.e. row = pos.
+struct EpDest {
+    void* const* x;           // [world] row buffers
+    uint32_t* const* sel;     // [world] selection buffers
+    float* const* w;          // [world] weight buffers
+    const uint32_t* base;     // [world] first row of this rank's segment in the destination
+    const uint32_t* send_off; // [world + 1] send-order offsets (bucket offsets, buckets = ranks)
+};
+
 template <typename Tx>
 __global__ void __launch_bounds__(256) ep_pack_kernel(const Tx* __restrict__ x, const uint32_t* __restrict__ sel,
                                                       const float* __restrict__ w, uint32_t T, uint32_t d,
                                                       uint32_t k_max, uint32_t per_rank, uint32_t S, uint32_t world,
                                                       const uint32_t* __restrict__ dest,
-                                                      const uint32_t* __restrict__ slot_row, Tx* __restrict__ send_x,
-                                                      uint32_t* __restrict__ send_sel, float* __restrict__ send_w) {
+                                                      const uint32_t* __restrict__ slot_row, EpDest D) {
     const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32;
     const uint32_t lane = threadIdx.x & 31;
     if (t >= T) return;
     for (uint32_t j = 0; j < world; ++j) {
         const uint32_t r = dest[(size_t)t * world + j];
         if (r == kSelNone) break;
-        const uint32_t pos = slot_row[(size_t)t * world + j];
+        const uint32_t pos = D.base[r] + slot_row[(size_t)t * world + j] - D.send_off[r];
+        Tx* send_x = static_cast<Tx*>(D.x[r]);
+        uint32_t* send_sel = D.sel[r];
+        float* send_w = D.w[r];
         // metadata: the token's selection restricted to rank r, local ids
         if (lane == 0) {
             uint32_t n = 0;
@@ -116,6 +130,29 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(const Tx* __restrict__ 
     }
 }
 
+// P2P return: received row q (from source s = segment of q in roff) goes back
+// into source s's back buffer at row dbase[s] + (q - roff[s]) -- the source's
+// send position, so its combine reads it like the NCCL path's return.
+template <typename Tx>
+__global__ void __launch_bounds__(256) ep_return_kernel(const Tx* __restrict__ part, uint32_t n_recv, uint32_t d,
+                                                        uint32_t world, const uint32_t* __restrict__ roff,
+                                                        const uint32_t* __restrict__ dbase, void* const* back) {
+    const uint32_t q = blockIdx.x * 8 + threadIdx.x / 32;
+    const uint32_t lane = threadIdx.x & 31;
+    if (q >= n_recv) return;
+    uint32_t s = 0;
+    while (s + 1 < world && roff[s + 1] <= q) ++s;
+    Tx* dst = static_cast<Tx*>(back[s]) + (size_t)(dbase[s] + q - roff[s]) * d;
+    const Tx* src = part + (size_t)q * d;
+    constexpr uint32_t VE = 16 / sizeof(Tx);
+    if ((d % VE) == 0) {
+        for (uint32_t c = lane * VE; c < d; c += 32 * VE)
+            *reinterpret_cast<uint4*>(dst + c) = __ldg(reinterpret_cast<const uint4*>(src + c));
+    } else {
+        for (uint32_t c = lane; c < d; c += 32) dst[c] = src[c];
+    }
+}
+
 }  // namespace
 }  // namespace mp
 
@@ -125,6 +162,17 @@ struct mp_ep_s {
     uint32_t* dest = nullptr;
     mp::BucketWs ws{};
     uint32_t last_T = 0;
+    // peer-memory exchange (mp_ep_p2p_*): own receive / return buffers, the
+    // peers' (CUDA IPC) and device tables of [world] pointers
+    uint32_t max_recv = 0;
+    void* recv_x = nullptr;
+    uint32_t* recv_sel = nullptr;
+    float* recv_w = nullptr;
+    void* back = nullptr;
+    std::vector<void*> opened;  // IPC mappings to close
+    void** d_px = nullptr;      // device [4][world]: x, sel, w, back
+    uint32_t* d_meta = nullptr; // device [4][world + 1]: base, roff, dbase, ones
+    bool p2p = false;
 };
 
 namespace {
@@ -140,8 +188,10 @@ void ep_ck(cudaError_t e, const char* what) {
 template <class F>
 int ep_guarded(F&& f);
 void ep_free(mp_ep_s* E) {
+    for (void* p : E->opened) cudaIpcCloseMemHandle(p);
     void* ptrs[] = {E->dest, E->ws.lrank, E->ws.block_counts, E->ws.block_base, E->ws.offsets, E->ws.mprefix_tc,
-                    E->ws.mprefix_simt, E->ws.mprefix_tc2, E->ws.perm_tok, E->ws.perm_w, E->ws.slot_row, E->ws.err};
+                    E->ws.mprefix_simt, E->ws.mprefix_tc2, E->ws.perm_tok, E->ws.perm_w, E->ws.slot_row, E->ws.err,
+                    E->recv_x, E->recv_sel, E->recv_w, E->back, E->d_px, E->d_meta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete E;
@@ -168,6 +218,15 @@ int ep_guarded(F&& f) {
         mp_internal_set_error(e.msg.c_str());
         return e.code;
     }
+}
+}  // namespace
+
+namespace {
+// device pointer tables: [0, 4w) peers (x, sel, w, back), [4w, 7w) local send
+// destinations; meta [4][w+1]
+void ensure_tables(mp_ep_s* E) {
+    if (!E->d_px) E->d_px = ep_alloc<void*>(8 * (size_t)E->world);
+    if (!E->d_meta) E->d_meta = ep_alloc<uint32_t>(4 * ((size_t)E->world + 1));
 }
 }  // namespace
 
@@ -253,9 +312,136 @@ MP_API mp_status mp_ep_pack(mp_ep_t E, const void* x, const uint32_t* sel, const
         if (!E || (T && (!x || !sel || !send_x || !send_sel || !send_w))) ep_fail(MP_ERR_VALIDATION, "null argument");
         if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_pack must follow mp_ep_plan for the same tokens");
         if (T == 0) return;
+        // identity destinations: every rank's segment of the one send buffer
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        ensure_tables(E);
+        std::vector<void*> px(4 * (size_t)E->world);
+        for (uint32_t r = 0; r < E->world; ++r) {
+            px[r] = send_x;
+            px[E->world + r] = send_sel;
+            px[2 * E->world + r] = send_w;
+        }
+        ep_ck(cudaMemcpyAsync(E->d_px + 4 * E->world, px.data(), 3 * E->world * sizeof(void*), cudaMemcpyHostToDevice,
+                              s),
+              "ep tables");
         mp::launch_ep_pack(E->dtype, x, sel, w, T, E->d, E->k_max, E->per_rank, E->S, E->world, E->dest,
-                           E->ws.slot_row, send_x, send_sel, send_w, static_cast<cudaStream_t>(stream));
+                           E->ws.slot_row, E->d_px + 4 * E->world, E->ws.offsets, E->ws.offsets, s);
         ep_ck(cudaGetLastError(), "ep pack");
+    });
+}
+
+// ---- peer-memory exchange (CUDA IPC handles; NVLink peer stores between GPUs) ----
+
+MP_API mp_status mp_ep_p2p_setup(mp_ep_t E, uint32_t max_recv_rows, uint8_t* handles) {
+    return ep_guarded([&] {
+        if (!E || !handles) ep_fail(MP_ERR_VALIDATION, "null argument");
+        if (E->p2p || E->recv_x) ep_fail(MP_ERR_VALIDATION, "peer-memory exchange already set up");
+        if (max_recv_rows < 1) ep_fail(MP_ERR_VALIDATION, "max_recv_rows must be >= 1");
+        ep_ck(cudaSetDevice(E->device), "cudaSetDevice");
+        const size_t esz = E->dtype == MP_DTYPE_BF16 ? 2 : 4;
+        E->max_recv = max_recv_rows;
+        E->recv_x = ep_alloc<char>((size_t)max_recv_rows * E->d * esz);
+        E->recv_sel = ep_alloc<uint32_t>((size_t)max_recv_rows * E->k_max);
+        E->recv_w = ep_alloc<float>((size_t)max_recv_rows * E->k_max);
+        E->back = ep_alloc<char>((size_t)E->max_tokens * E->world * E->d * esz);
+        void* bufs[4] = {E->recv_x, E->recv_sel, E->recv_w, E->back};
+        for (int i = 0; i < 4; ++i) {
+            cudaIpcMemHandle_t h;
+            ep_ck(cudaIpcGetMemHandle(&h, bufs[i]), "cudaIpcGetMemHandle");
+            std::memcpy(handles + i * sizeof(cudaIpcMemHandle_t), &h, sizeof(h));
+        }
+        ensure_tables(E);
+    });
+}
+
+MP_API mp_status mp_ep_p2p_open(mp_ep_t E, const uint8_t* all_handles) {
+    return ep_guarded([&] {
+        if (!E || !all_handles) ep_fail(MP_ERR_VALIDATION, "null argument");
+        if (!E->recv_x) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_setup first");
+        ep_ck(cudaSetDevice(E->device), "cudaSetDevice");
+        const size_t hs = sizeof(cudaIpcMemHandle_t);
+        std::vector<void*> px(4 * (size_t)E->world);
+        void* own[4] = {E->recv_x, E->recv_sel, E->recv_w, E->back};
+        for (uint32_t r = 0; r < E->world; ++r)
+            for (int i = 0; i < 4; ++i) {
+                void* p = own[i];
+                if (r != E->rank) {
+                    cudaIpcMemHandle_t h;
+                    std::memcpy(&h, all_handles + (r * 4 + i) * hs, hs);
+                    ep_ck(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+                    E->opened.push_back(p);
+                }
+                px[i * E->world + r] = p;
+            }
+        ep_ck(cudaMemcpy(E->d_px, px.data(), px.size() * sizeof(void*), cudaMemcpyHostToDevice), "peer table");
+        E->p2p = true;
+    });
+}
+
+namespace {
+// counts[s * world + d] = rows rank s sends to rank d (the all-gathered plan)
+void p2p_meta(mp_ep_s* E, const uint32_t* counts, cudaStream_t s, uint32_t& n_recv) {
+    const uint32_t W = E->world, me = E->rank;
+    std::vector<uint32_t> meta(4 * ((size_t)W + 1), 0);
+    uint32_t* base = meta.data();           // my first row in rank r's receive buffer
+    uint32_t* roff = base + (W + 1);        // my receive segments, per source
+    uint32_t* dbase = roff + (W + 1);       // source s's send position of its rows for me
+    for (uint32_t r = 0; r < W; ++r)
+        for (uint32_t q = 0; q < me; ++q) base[r] += counts[(size_t)q * W + r];
+    for (uint32_t q = 0; q < W; ++q) roff[q + 1] = roff[q] + counts[(size_t)q * W + me];
+    for (uint32_t q = 0; q < W; ++q)
+        for (uint32_t r = 0; r < me; ++r) dbase[q] += counts[(size_t)q * W + r];
+    n_recv = roff[W];
+    if (n_recv > E->max_recv) ep_fail(MP_ERR_VALIDATION, "received rows exceed max_recv_rows");
+    ep_ck(cudaMemcpyAsync(E->d_meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, s), "p2p meta");
+}
+}  // namespace
+
+MP_API mp_status mp_ep_p2p_pack(mp_ep_t E, const void* x, const uint32_t* sel, const float* w, uint32_t T,
+                                const uint32_t* counts, uint32_t* n_recv, void* stream) {
+    return ep_guarded([&] {
+        if (!E || !counts || !n_recv || (T && (!x || !sel))) ep_fail(MP_ERR_VALIDATION, "null argument");
+        if (!E->p2p) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_open first");
+        if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_pack must follow mp_ep_plan for the same tokens");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        uint32_t nr = 0;
+        p2p_meta(E, counts, s, nr);
+        *n_recv = nr;
+        if (T == 0) return;
+        mp::launch_ep_pack(E->dtype, x, sel, w, T, E->d, E->k_max, E->per_rank, E->S, E->world, E->dest,
+                           E->ws.slot_row, E->d_px, E->d_meta, E->ws.offsets, s);
+        ep_ck(cudaGetLastError(), "ep p2p pack");
+    });
+}
+
+MP_API mp_status mp_ep_p2p_recv_buffers(mp_ep_t E, void** recv_x, uint32_t** recv_sel, float** recv_w) {
+    return ep_guarded([&] {
+        if (!E || !E->recv_x) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_setup first");
+        if (recv_x) *recv_x = E->recv_x;
+        if (recv_sel) *recv_sel = E->recv_sel;
+        if (recv_w) *recv_w = E->recv_w;
+    });
+}
+
+MP_API mp_status mp_ep_p2p_return(mp_ep_t E, const void* part, uint32_t n_recv, void* stream) {
+    return ep_guarded([&] {
+        if (!E || (n_recv && !part)) ep_fail(MP_ERR_VALIDATION, "null argument");
+        if (!E->p2p) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_open first");
+        const uint32_t W = E->world;
+        mp::launch_ep_return(E->dtype, part, n_recv, E->d, W, E->d_meta + (W + 1), E->d_meta + 2 * (W + 1),
+                             E->d_px + 3 * W, static_cast<cudaStream_t>(stream));
+        ep_ck(cudaGetLastError(), "ep p2p return");
+    });
+}
+
+MP_API mp_status mp_ep_p2p_combine(mp_ep_t E, uint32_t T, void* y, void* stream) {
+    return ep_guarded([&] {
+        if (!E || (T && !y)) ep_fail(MP_ERR_VALIDATION, "null argument");
+        if (!E->p2p) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_open first");
+        if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_combine must follow mp_ep_plan for the same tokens");
+        if (T == 0) return;
+        mp::launch_ep_combine(E->dtype, E->back, T, E->d, E->world, E->ws.slot_row, y, static_cast<cudaStream_t>(stream));
+        ep_ck(cudaGetLastError(), "ep p2p combine");
     });
 }
 
@@ -280,15 +466,26 @@ void launch_ep_slot(const uint32_t* dest, const uint32_t* lrank, const uint32_t*
 }
 void launch_ep_pack(int dtype, const void* x, const uint32_t* sel, const float* w, uint32_t T, uint32_t d,
                     uint32_t k_max, uint32_t per_rank, uint32_t S, uint32_t world, const uint32_t* dest,
-                    const uint32_t* slot_row, void* send_x, uint32_t* send_sel, float* send_w, cudaStream_t s) {
+                    const uint32_t* slot_row, void* const* dst_tables, const uint32_t* base, const uint32_t* send_off,
+                    cudaStream_t s) {
+    EpDest D{dst_tables, reinterpret_cast<uint32_t* const*>(dst_tables + world),
+             reinterpret_cast<float* const*>(dst_tables + 2 * world), base, send_off};
     if (dtype == 1)
-        ep_pack_kernel<__nv_bfloat16><<<(T + 7) / 8, 256, 0, s>>>(
-            static_cast<const __nv_bfloat16*>(x), sel, w, T, d, k_max, per_rank, S, world, dest, slot_row,
-            static_cast<__nv_bfloat16*>(send_x), send_sel, send_w);
+        ep_pack_kernel<__nv_bfloat16><<<(T + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x), sel, w, T, d,
+                                                                  k_max, per_rank, S, world, dest, slot_row, D);
     else
         ep_pack_kernel<float><<<(T + 7) / 8, 256, 0, s>>>(static_cast<const float*>(x), sel, w, T, d, k_max, per_rank,
-                                                          S, world, dest, slot_row, static_cast<float*>(send_x),
-                                                          send_sel, send_w);
+                                                          S, world, dest, slot_row, D);
+}
+void launch_ep_return(int dtype, const void* part, uint32_t n_recv, uint32_t d, uint32_t world, const uint32_t* roff,
+                      const uint32_t* dbase, void* const* back, cudaStream_t s) {
+    if (n_recv == 0) return;
+    if (dtype == 1)
+        ep_return_kernel<__nv_bfloat16><<<(n_recv + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(part),
+                                                                         n_recv, d, world, roff, dbase, back);
+    else
+        ep_return_kernel<float><<<(n_recv + 7) / 8, 256, 0, s>>>(static_cast<const float*>(part), n_recv, d, world,
+                                                                 roff, dbase, back);
 }
 void launch_ep_combine(int dtype, const void* back, uint32_t T, uint32_t d, uint32_t world, const uint32_t* slot_row,
                        void* y, cudaStream_t s) {

@@ -170,9 +170,14 @@ void launch_ep_dest(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32_t pe
                     cudaStream_t s);
 void launch_ep_slot(const uint32_t* dest, const uint32_t* lrank, const uint32_t* block_base, uint32_t T, uint32_t world,
                     uint32_t* slot_row, cudaStream_t s);
+// dst_tables: device [3][world] destination pointers (x rows, sel, w); rows of
+// rank r land at base[r] + (send position - send_off[r])
 void launch_ep_pack(int dtype, const void* x, const uint32_t* sel, const float* w, uint32_t T, uint32_t d,
                     uint32_t k_max, uint32_t per_rank, uint32_t S, uint32_t world, const uint32_t* dest,
-                    const uint32_t* slot_row, void* send_x, uint32_t* send_sel, float* send_w, cudaStream_t s);
+                    const uint32_t* slot_row, void* const* dst_tables, const uint32_t* base, const uint32_t* send_off,
+                    cudaStream_t s);
+void launch_ep_return(int dtype, const void* part, uint32_t n_recv, uint32_t d, uint32_t world, const uint32_t* roff,
+                      const uint32_t* dbase, void* const* back, cudaStream_t s);
 void launch_ep_combine(int dtype, const void* back, uint32_t T, uint32_t d, uint32_t world, const uint32_t* slot_row,
                        void* y, cudaStream_t s);
 }  // namespace mp

@@ -157,3 +157,68 @@ class ExpertParallelLayer:
         if return_routing:
             return y, sel, w, counts, recv_counts
         return y
+
+
+class PeerExpertParallelLayer:
+    """Expert parallelism with both exchanges as peer-memory stores instead of
+    NCCL all-to-alls: the pack kernel writes every token row straight into the
+    destination rank's receive buffer (CUDA IPC mapping; NVLink between the
+    GPUs of a node) and the return kernel writes the expert partials straight
+    back into the source ranks' return buffers.  Host-side, per layer: one
+    all-gather of the world x world plan and two barriers (every rank's writes
+    complete before the readers launch)."""
+
+    def __init__(self, ops, group=None, max_recv_rows=None):
+        import torch
+        self.ops, self.group = ops, group
+        self.lib = _lib.load()
+        dist = _dist()
+        world = ops.world
+        max_recv = max_recv_rows or ops.local.max_tokens
+        handles = (C.c_uint8 * 256)()
+        check(self.lib.mp_ep_p2p_setup(ops.ep, max_recv, handles))
+        mine = bytes(handles)
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            gathered = [None] * world
+            dist.all_gather_object(gathered, mine, group=group)
+        else:
+            gathered = [mine]
+        allh = (C.c_uint8 * (256 * world)).from_buffer_copy(b"".join(gathered))
+        check(self.lib.mp_ep_p2p_open(ops.ep, allh))
+        self.torch = torch
+
+    def _sync(self):
+        dist = _dist()
+        self.torch.cuda.current_stream().synchronize()
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.barrier(group=self.group)
+
+    def _plan_matrix(self, counts):
+        dist = _dist()
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            gathered = [None] * self.ops.world
+            dist.all_gather_object(gathered, list(counts), group=self.group)
+        else:
+            gathered = [list(counts)]
+        return [c for row in gathered for c in row]
+
+    def forward(self, x, k: int = 0, k_per_token=None):
+        torch, ops, lib = self.torch, self.ops, self.lib
+        T = x.shape[0]
+        sel, w = ops.route(x, k, k_per_token)
+        counts = ops.plan(sel)
+        mat = (C.c_uint32 * (ops.world * ops.world))(*self._plan_matrix(counts))
+        n_recv = C.c_uint32()
+        stream = _stream_handle(None)
+        check(lib.mp_ep_p2p_pack(ops.ep, _ptr(x), _ptr(sel), _ptr(w), T, mat, C.byref(n_recv), stream))
+        self._sync()  # every rank's rows are in place
+        rx, rs, rw = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib.mp_ep_p2p_recv_buffers(ops.ep, C.byref(rx), C.byref(rs), C.byref(rw)))
+        part = torch.empty((max(n_recv.value, 1), ops.d), dtype=ops.dtype, device=x.device)
+        if n_recv.value:
+            check(lib.mp_layer_forward_selected(ops.local.h, rx, n_recv.value, rs, rw, _ptr(part), None, stream))
+        check(lib.mp_ep_p2p_return(ops.ep, _ptr(part), n_recv.value, stream))
+        self._sync()  # every partial is back at its source
+        y = torch.empty((T, ops.d), dtype=ops.dtype, device=x.device)
+        check(lib.mp_ep_p2p_combine(ops.ep, T, _ptr(y), stream))
+        return y
