@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmB);
     }
     if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+    griddep_wait();  // group metadata comes from the routing epilogue
+    griddep_launch();
     for (uint32_t q = threadIdx.x; q <= p.G; q += blockDim.x) {
         s_prefix[q] = p.mprefix[q];
         s_off[q] = p.offsets[q];
@@ -448,10 +450,10 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
         attr_set = true;
     }
     switch (epi) {
-        case kEpiSwiglu: gemm_tc_kernel<kEpiSwiglu><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p); break;
-        case kEpiActAbs: gemm_tc_kernel<kEpiActAbs><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p); break;
-        case kEpiCount: gemm_tc_kernel<kEpiCount><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p); break;
-        default: gemm_tc_kernel<kEpiPlain><<<grid, kThreads, kSmemBytes, s>>>(*tmA, *tmB, p); break;
+        case kEpiSwiglu: launch_k(gemm_tc_kernel<kEpiSwiglu>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
+        case kEpiActAbs: launch_k(gemm_tc_kernel<kEpiActAbs>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
+        case kEpiCount: launch_k(gemm_tc_kernel<kEpiCount>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
+        default: launch_k(gemm_tc_kernel<kEpiPlain>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
     }
 }
 

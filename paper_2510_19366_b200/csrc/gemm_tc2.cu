@@ -215,6 +215,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tmB);
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot);
+    griddep_wait();  // group metadata comes from the routing epilogue
+    griddep_launch();
     for (uint32_t q = threadIdx.x; q <= p.G; q += blockDim.x) {
         s_prefix[q] = p.mprefix[q];
         s_off[q] = p.offsets[q];
@@ -437,9 +439,9 @@ void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB
         attr_set = true;
     }
     if (swiglu)
-        gemm_pair_kernel<true><<<2 * pairs, kThreads, kSmemBytes, s>>>(*tmA, *tmB, tmA64 ? *tmA64 : *tmA, p);
+        launch_k(gemm_pair_kernel<true>, dim3(2 * pairs), dim3(kThreads), kSmemBytes, s, *tmA, *tmB, tmA64 ? *tmA64 : *tmA, p);
     else
-        gemm_pair_kernel<false><<<2 * pairs, kThreads, kSmemBytes, s>>>(*tmA, *tmB, tmA64 ? *tmA64 : *tmA, p);
+        launch_k(gemm_pair_kernel<false>, dim3(2 * pairs), dim3(kThreads), kSmemBytes, s, *tmA, *tmB, tmA64 ? *tmA64 : *tmA, p);
 }
 
 }  // namespace mp

@@ -18,6 +18,16 @@
 
 #define MP_API extern "C" __attribute__((visibility("default")))
 
+namespace mp {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MOEPRISM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+}  // namespace mp
+
 namespace {
 
 thread_local std::string g_err;
@@ -593,10 +603,12 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             const mp::RouterTcPlan pl = mp::plan_router_tc(T, L->d, L->G, L->num_sms);
             CUtensorMap tmX;
             if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "router tensor map");
+            // zeroed before the router so the router -> routing-epilogue boundary
+            // is kernel to kernel (programmatic dependent launch)
+            ck(cudaMemsetAsync(L->r_flagged, 0, sizeof(uint32_t), s), "memset flagged");
             mp::launch_router_tc(&tmX, &L->tm_wplanes, pl, T, L->r_partial, s);
             L->r_last_ks = pl.ks;
             L->r_last_T = T;
-            ck(cudaMemsetAsync(L->r_flagged, 0, sizeof(uint32_t), s), "memset flagged");
             if (fuse_bucket && L->has_experts && (L->d % 4) == 0) {
                 // routing epilogue + exact near-tie re-selection + bucketing in one kernel;
                 // many K splits (small batches): reduce them first across (token, g) warps

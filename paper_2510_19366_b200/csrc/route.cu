@@ -661,6 +661,8 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     const uint32_t words = (G + 31) / 32;
     for (uint32_t q = threadIdx.x; q < TB * words; q += blockDim.x) msk[q / words][q % words] = 0;
     if (threadIdx.x == 0) n_pairs = 0;
+    griddep_wait();
+    griddep_launch();
     __syncthreads();
     bool flagged = false;
     uint32_t kt = 0;
@@ -770,6 +772,8 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
                                                        int* __restrict__ err, bool check_finite, uint32_t tb) {
     const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32;
     const uint32_t lane = threadIdx.x & 31;
+    griddep_wait();  // every CTA waits before exiting: completion stays transitive
+    griddep_launch();
     if (t >= T) return;
     const uint32_t blk = t / tb;
     for (uint32_t j = lane; j < k_max; j += 32) {
@@ -859,6 +863,8 @@ __global__ void __launch_bounds__(128) dispatch_bulk_kernel(const __nv_bfloat16*
         fence_mbar_init();
     }
     __syncwarp();
+    griddep_wait();
+    griddep_launch();
     if (t >= T) return;
     if (lane == 0) {
         mbar_expect_tx(&bar[warp], row_bytes);
@@ -912,6 +918,8 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
     __shared__ uint32_t rows[64];
     __shared__ float wts[64];
     const uint32_t t = blockIdx.x;
+    griddep_wait();
+    griddep_launch();
     for (uint32_t j = threadIdx.x; j < k_max; j += blockDim.x) {
         rows[j] = slot_row[(size_t)t * k_max + j];
         wts[j] = w ? w[(size_t)t * k_max + j] : 1.0f;
@@ -987,6 +995,8 @@ __global__ void __launch_bounds__(256) combine_f64_kernel(const double* __restri
     __shared__ uint32_t gid[64];
     __shared__ float wts[64];
     const uint32_t t = blockIdx.x;
+    griddep_wait();
+    griddep_launch();
     for (uint32_t j = threadIdx.x; j < k_max; j += blockDim.x) {
         rows[j] = slot_row[(size_t)t * k_max + j];
         gid[j] = sel[(size_t)t * k_max + j];
@@ -1055,6 +1065,8 @@ __global__ void __launch_bounds__(256) partials_reduce_kernel(double* __restrict
                                                               uint32_t G, uint32_t Npad) {
     const uint32_t gw = (G + 31) / 32;
     const uint32_t wid = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    griddep_wait();
+    griddep_launch();
     if (wid >= T * gw) return;
     const uint32_t t = wid / gw, g = (wid % gw) * 32 + lane;
     if (g >= G) return;
@@ -1065,7 +1077,7 @@ __global__ void __launch_bounds__(256) partials_reduce_kernel(double* __restrict
 
 void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, cudaStream_t s) {
     const uint32_t warps = T * ((G + 31) / 32);
-    partials_reduce_kernel<<<(warps + 7) / 8, 256, 0, s>>>(partial, ks, T, G, Npad);
+    launch_k(partials_reduce_kernel, dim3((warps + 7) / 8), dim3(256), 0, s, partial, ks, T, G, Npad);
 }
 
 void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
@@ -1080,7 +1092,7 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
                                  (int)(sizeof(double) * 2 * TB * kMaxG));
             attr_set[which] = true;
         }
-        kern<<<(T + tb - 1) / tb, 1024, smem, s>>>(
+        launch_k(kern, dim3((T + tb - 1) / tb), dim3(1024), smem, s,
             partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, guard,
             static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, n_fixed, ws.lrank, ws.block_counts, ws.block_base,
             ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb);
@@ -1145,18 +1157,18 @@ void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t 
                                  (int)(4 * kBulkRowMax));
             attr = true;
         }
-        dispatch_bulk_kernel<<<(T + 3) / 4, 128, smem, s>>>(
+        launch_k(dispatch_bulk_kernel, dim3((T + 3) / 4), dim3(128), smem, s,
             static_cast<const __nv_bfloat16*>(x), T, d, sel, w, k_max, G, ws.lrank, ws.block_base, ws.perm_tok,
             ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), check_finite ? ws.err : nullptr, tb);
         return;
     }
     const dim3 grid((T + 7) / 8);
     if (dtype == 1)
-        dispatch_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        launch_k(dispatch_kernel<__nv_bfloat16>, grid, dim3(256), 0, s,
             static_cast<const __nv_bfloat16*>(x), T, d, d_pad, sel, w, k_max, G, ws.lrank, ws.block_base,
             ws.perm_tok, ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), ws.err, check_finite, tb);
     else
-        dispatch_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), T, d, d_pad, sel, w, k_max, G,
+        launch_k(dispatch_kernel<float>, grid, dim3(256), 0, s, static_cast<const float*>(x), T, d, d_pad, sel, w, k_max, G,
                                                     ws.lrank, ws.block_base, ws.perm_tok, ws.perm_w, ws.slot_row,
                                                     static_cast<float*>(x_perm), ws.err, check_finite, tb);
 }
@@ -1201,7 +1213,8 @@ void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const 
                     const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
                     cudaStream_t s, const void* o_sh, const float* w_sh, const void* x_res) {
     if (dtype == 1)
-        combine_bf16_kernel<<<T, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(o), d, d_pad, slot_row, w, k_max,
+        launch_k(combine_bf16_kernel, dim3(T), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(o), d, d_pad,
+                 slot_row, w, k_max,
                                               static_cast<const __nv_bfloat16*>(o_sh), w_sh,
                                               static_cast<const __nv_bfloat16*>(x_res),
                                               static_cast<__nv_bfloat16*>(y));

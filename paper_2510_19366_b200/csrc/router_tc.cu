@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    griddep_wait();
+    griddep_launch();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -203,7 +205,7 @@ void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const Rout
         cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr_set = true;
     }
-    router_tc_kernel<<<dim3(pl.m_tiles, pl.ks), kThreads, pl.smem, s>>>(*tmX, *tmW, p);
+    launch_k(router_tc_kernel, dim3(pl.m_tiles, pl.ks), dim3(kThreads), pl.smem, s, *tmX, *tmW, p);
 }
 
 }  // namespace mp
