@@ -64,13 +64,29 @@ constexpr uint32_t BM = 256;  // rows per pair tile (128 per CTA)
 constexpr uint32_t HM = 128;
 constexpr uint32_t BN = 256;
 constexpr uint32_t BK = 64;
-constexpr uint32_t NS = MP_PAIR_STAGES;
+constexpr uint32_t NSP = MP_PAIR_STAGES;
 constexpr uint32_t A_BYTES = HM * BK * 2;   // 16 KB per CTA
 constexpr uint32_t B_BYTES = 128 * BK * 2;  // 16 KB per CTA (half of the 256-row B tile)
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr uint32_t kThreads = 192;  // warp 0 TMA, warp 1 TMEM alloc + MMA (leader), warps 2..5 epilogue
+#ifndef MP_PAIR_EPI_WARPS
+#define MP_PAIR_EPI_WARPS 4
+#endif
+// warp 0 TMA, warp 1 TMEM alloc + MMA (leader), warps 2.. epilogue: 4 or 8
+// (two per TMEM lane quarter, each taking half of the accumulator columns).
+// Measured (tile_trace.py, k=8): 8 warps halve the SwiGLU epilogue (13.7k ->
+// 6.1k cycles per tile) but it is hidden behind the next tile's MMAs anyway,
+// and the extra polling warps slow gemm2 by 9%: 4.
+constexpr uint32_t kEpiWarps = MP_PAIR_EPI_WARPS;
+constexpr uint32_t kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
-constexpr size_t kSmemBytes = 1024 + NS * STAGE_BYTES + 256;
+constexpr size_t kSmemBytes = 1024 + NSP * STAGE_BYTES + 256;
+// extended-tile kernel: + 64 A rows per CTA per stage (the M=128 MMA of a
+// merged remainder), 5 stages of 40 KB
+constexpr uint32_t NSX = 5;
+constexpr uint32_t X_BYTES = 64 * BK * 2;
+constexpr size_t kSmemBytesX = 1024 + NSX * (STAGE_BYTES + X_BYTES) + 256;
+template <bool EXT>
+constexpr size_t smem_bytes() { return EXT ? kSmemBytesX : kSmemBytes; }
 
 struct PairParams {
     uint32_t G, K, N_group, n_valid, ld_out, NT;
@@ -79,6 +95,7 @@ struct PairParams {
     __nv_bfloat16* out;
     uint64_t* trace;  // [grid][4] MMA-issuer timing of the leaders (diagnostics) or null
     uint32_t tail128;  // tiles with <= 128 valid rows issue M=128 pair MMAs
+    uint32_t ext;      // mprefix is the merged schedule: 257..384-row extended tiles
     const uint32_t* gmap;  // nullable: B group of group g (sub-expert offload cache slot), else g
 };
 
@@ -175,10 +192,12 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
     m = local - n * mt;
 }
 
-template <bool SWIGLU>
+template <bool SWIGLU, bool EXT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmA64, PairParams p) {
+    constexpr uint32_t NS = EXT ? NSX : NSP;
+    constexpr uint32_t XB = EXT ? X_BYTES : 0u;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
@@ -186,8 +205,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // identical offsets in both CTAs (same dynamic smem layout)
     uint8_t* sA = base;                // NS x 16 KB
-    uint8_t* sB = base + NS * A_BYTES;  // NS x 16 KB
-    uint64_t* full = reinterpret_cast<uint64_t*>(base + NS * STAGE_BYTES);
+    uint8_t* sX = base + NS * A_BYTES;  // NS x 8 KB (EXT: the remainder's 64 rows per CTA)
+    uint8_t* sB = sX + NS * XB;         // NS x 16 KB
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + NS * B_BYTES);
     uint64_t* empty = full + NS;
     uint64_t* tfull = empty + NS;
     uint64_t* tempty = tfull + 2;
@@ -205,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (uint32_t a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+            mbar_init(&tempty[a], 2 * kEpiWarps);  // epilogue warps x 2 CTAs
         }
         fence_mbar_init();
     }
@@ -242,18 +262,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (uint32_t tile = pair; tile < total; tile += npairs) {
                 uint32_t g, m, n;
                 map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const bool tail = p.tail128 && s_off[g + 1] - s_off[g] - m * BM <= HM;  // M=128: 64 rows per CTA
+                const uint32_t rows = s_off[g + 1] - s_off[g] - m * BM;
+                const bool tail = p.tail128 && rows <= HM;  // M=128: 64 rows per CTA
+                const bool ext = EXT && rows > BM && rows <= BM + HM;  // + remainder rows 256 .. 383
                 const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * (tail ? HM / 2 : HM));
+                const int32_t xrow = static_cast<int32_t>(s_off[g] + m * BM + BM + rank * 64);
                 const int32_t brow = static_cast<int32_t>(s_gmap[g] * p.N_group + n * BN + rank * 128);
                 // the GEMM is bound by the operand feed (L2 -> SM), so a tail tile
                 // loads only the 64 A rows per CTA its M=128 MMA reads
                 const CUtensorMap* tA = tail ? &tmA64 : &tmA;
-                const uint32_t tx = 2 * (tail ? A_BYTES / 2 + B_BYTES : STAGE_BYTES);
+                const uint32_t tx = 2 * (tail ? A_BYTES / 2 + B_BYTES : STAGE_BYTES + (ext ? X_BYTES : 0u));
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
                     if (rank == 0) mbar_expect_tx(&full[s], tx);
                     const uint32_t fb = full_leader + s * 8;
+                    if (ext) tma_load_2d_pair(sX + s * XB, &tmA64, fb, static_cast<int32_t>(kb * BK), xrow);
 #if MP_PAIR_HINTS & 2
                     tma_load_2d_pair_hint(sA + s * A_BYTES, tA, fb, static_cast<int32_t>(kb * BK), arow, pol_a);
 #else
@@ -272,25 +296,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             constexpr uint32_t idesc_full = umma_idesc_bf16(BM, BN);
             constexpr uint32_t idesc_tail = umma_idesc_bf16(HM, BN);
             uint32_t it = 0, tc = 0;
+            uint32_t use0 = 0, use1 = 0;  // acquisitions of each 256-column accumulator buffer
+            auto acquire = [&](uint32_t b) {  // acquisition u waits for release u - 1 (phase parity)
+                const uint32_t u = b ? use1++ : use0++;
+                mbar_wait_cluster(&tempty[b], (u & 1u) ^ 1u);
+            };
 #if MP_PAIR_TRACE
             const uint64_t t_start = clock64();
             uint64_t w_acc = 0, w_full = 0;
 #endif
             for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
-                const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+                const uint32_t acc = tc & 1u;
                 uint32_t g, m, n;
                 map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const uint32_t idesc = (p.tail128 && s_off[g + 1] - s_off[g] - m * BM <= HM) ? idesc_tail : idesc_full;
+                const uint32_t rows = s_off[g + 1] - s_off[g] - m * BM;
+                const uint32_t idesc = (p.tail128 && rows <= HM) ? idesc_tail : idesc_full;
+                const bool ext = EXT && rows > BM && rows <= BM + HM;
 #if MP_PAIR_TRACE
                 uint64_t t0 = clock64();
 #endif
-                mbar_wait_cluster(&tempty[acc], aph ^ 1u);
+                acquire(acc);
+                // an extended tile also takes the first 128 columns of the other
+                // buffer for its M=128 remainder accumulator
+                if (ext) acquire(acc ^ 1u);
 #if MP_PAIR_TRACE
                 w_acc += clock64() - t0;
                 const uint64_t t_tile = clock64(), wf0 = w_full;
 #endif
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t x_tmem = tmem_base + (acc ^ 1u) * BN;
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
 #if MP_PAIR_TRACE
@@ -307,6 +342,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     for (uint32_t k = 0; k < BK / 16; ++k)
                         umma_bf16_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
                                        (kb | k) != 0u);
+                    if (ext) {
+                        const uint32_t x0 = smem_u32(sX + s * XB);
+#pragma unroll
+                        for (uint32_t k = 0; k < BK / 16; ++k)
+                            umma_bf16_pair(x_tmem, umma_desc_sw128(x0 + k * 32), umma_desc_sw128(b0 + k * 32),
+                                           idesc_tail, (kb | k) != 0u);
+                    }
                     umma_commit_pair(&empty[s]);
                 }
                 umma_commit_pair(&tfull[acc]);
@@ -316,7 +358,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     r[0] = tile;
                     r[1] = w_full - wf0;
                     r[2] = clock64() - t_tile;
-                    r[3] = idesc == idesc_tail;
+                    r[3] = (idesc == idesc_tail ? 1u : 0u) | (ext ? 2u : 0u);
                 }
 #endif
             }
@@ -333,79 +375,114 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
     } else {
         const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
+        const uint32_t part = (warp - 2) / 4, nparts = kEpiWarps / 4;  // column share of this warp
         const uint32_t tempty_leader = mapa(&tempty[0], 0);
-        uint32_t tc = 0;
-        for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
-            uint32_t g, m, n;
-            map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-            const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
-            mbar_wait(&tfull[acc], aph);
-            tc_fence_after();
-            const uint32_t cnt = s_off[g + 1] - s_off[g];
-            const bool tail = p.tail128 && cnt - m * BM <= HM;
-            // full tile: lane = row rank*128 + q*32 + lane, all 256 D columns;
-            // tail tile: lane l < 64 = row rank*64 + l with D columns [0,128),
-            //            lane 64 + l = the same row with D columns [128,256)
-            const uint32_t row_local =
-                m * BM + (tail ? rank * 64 + (q & 1u) * 32 + lane : rank * HM + q * 32 + lane);
-            const uint32_t half = tail ? (q >> 1) : 0;  // which 128 D columns this lane holds (tail)
-            const uint32_t nchunk = tail ? 4 : 8;        // 32-column chunks of D held by the lane
+        // One accumulator to bf16 rows of the group.  full (M=256) shape: lane =
+        // row rank*128 + q*32 + lane, all 256 D columns; half (M=128) shape:
+        // lane l < 64 = row rank*64 + l with D columns [0,128), lane 64 + l =
+        // the same row with D columns [128,256).
+        auto emit = [&](uint32_t buf, uint32_t row0, bool m128, uint32_t g, uint32_t n, uint32_t cnt) {
+            const uint32_t row_local = row0 + (m128 ? rank * 64 + (q & 1u) * 32 + lane : rank * HM + q * 32 + lane);
+            const uint32_t half = m128 ? (q >> 1) : 0;  // which 128 D columns this lane holds (M=128)
+            const uint32_t nchunk = m128 ? 4 : 8;        // 32-column chunks of D held by the lane
             const bool valid = row_local < cnt;
             const bool any = (row_local - lane) < cnt;  // warp has a valid row
             __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN;
-            if (any) {
-                if constexpr (SWIGLU) {
-                    // D chunk pair (gate, up) = columns (h*128 + c2*32, + 64) for
-                    // neurons n*128 + h*64 + c2*32 .. +31
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN;
+            if (!any) return;
+            if constexpr (SWIGLU) {
+                // D chunk pair (gate, up) = columns (h*128 + c2*32, + 64) for
+                // neurons n*128 + h*64 + c2*32 .. +31
 #pragma unroll 1
-                    for (uint32_t c = 0; c < nchunk / 2; ++c) {
-                        const uint32_t h = tail ? half : (c >> 1), c2 = c & 1u;
-                        const uint32_t tcol = (tail ? 0 : h * 128) + c2 * 32;
-                        uint32_t gr[32], ur[32];
-                        tmem_ld32(taddr + tcol, gr);
-                        tmem_ld32(taddr + tcol + kIlv, ur);
-                        tmem_ld_wait();
+                for (uint32_t c = part; c < nchunk / 2; c += nparts) {
+                    const uint32_t h = m128 ? half : (c >> 1), c2 = c & 1u;
+                    const uint32_t tcol = (m128 ? 0 : h * 128) + c2 * 32;
+                    uint32_t gr[32], ur[32];
+                    tmem_ld32(taddr + tcol, gr);
+                    tmem_ld32(taddr + tcol + kIlv, ur);
+                    tmem_ld_wait();
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const float g0 = __uint_as_float(gr[2 * i]), g1 = __uint_as_float(gr[2 * i + 1]);
+                        const float u0 = __uint_as_float(ur[2 * i]), u1 = __uint_as_float(ur[2 * i + 1]);
+                        pk[i] = pack_bf16x2(silu_f32(g0) * u0, silu_f32(g1) * u1);
+                    }
+                    if (valid) {
+                        __nv_bfloat16* dst = orow + n * 128 + h * 64 + c2 * 32;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v)
+                            st_global_v4(dst + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (uint32_t c = part; c < nchunk; c += nparts) {
+                    uint32_t r[32];
+                    tmem_ld32(taddr + c * 32, r);
+                    tmem_ld_wait();
+                    const uint32_t col = n * BN + half * 128 + c * 32;
+                    if (valid && col < p.n_valid) {
                         uint32_t pk[16];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const float g0 = __uint_as_float(gr[2 * i]), g1 = __uint_as_float(gr[2 * i + 1]);
-                            const float u0 = __uint_as_float(ur[2 * i]), u1 = __uint_as_float(ur[2 * i + 1]);
-                            pk[i] = pack_bf16x2(silu_f32(g0) * u0, silu_f32(g1) * u1);
-                        }
-                        if (valid) {
-                            __nv_bfloat16* dst = orow + n * 128 + h * 64 + c2 * 32;
+                        for (int i = 0; i < 16; ++i)
+                            pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+                        __nv_bfloat16* dst = orow + col;
 #pragma unroll
-                            for (int v = 0; v < 4; ++v)
-                                st_global_v4(dst + v * 8,
-                                             make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
-                        }
-                    }
-                } else {
-#pragma unroll 1
-                    for (uint32_t c = 0; c < nchunk; ++c) {
-                        uint32_t r[32];
-                        tmem_ld32(taddr + c * 32, r);
-                        tmem_ld_wait();
-                        const uint32_t col = n * BN + half * 128 + c * 32;
-                        if (valid && col < p.n_valid) {
-                            uint32_t pk[16];
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-                            __nv_bfloat16* dst = orow + col;
-#pragma unroll
-                            for (int v = 0; v < 4; ++v)
-                                st_global_v4(dst + v * 8,
-                                             make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
-                        }
+                        for (int v = 0; v < 4; ++v)
+                            st_global_v4(dst + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
                     }
                 }
             }
+        };
+        auto release = [&](uint32_t buf) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_remote(tempty_leader + acc * 8);
+            if (lane == 0) mbar_arrive_remote(tempty_leader + buf * 8);
+        };
+        uint32_t tc = 0;
+#if MP_PAIR_TRACE
+        uint64_t e_busy = 0, e_ext = 0, e_wait = 0;
+#endif
+        for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
+            uint32_t g, m, n;
+            map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+            const uint32_t acc = tc & 1u;
+#if MP_PAIR_TRACE
+            const uint64_t e0 = clock64();
+#endif
+            mbar_wait(&tfull[acc], (tc >> 1) & 1u);  // one commit per tile on its main buffer
+            tc_fence_after();
+#if MP_PAIR_TRACE
+            const uint64_t e1 = clock64();
+            e_wait += e1 - e0;
+#endif
+            const uint32_t cnt = s_off[g + 1] - s_off[g];
+            const uint32_t rows = cnt - m * BM;
+            if (EXT && rows > BM && rows <= BM + HM) {  // the group's last tile, merged remainder
+                // remainder first: the next tile's MMAs wait for that buffer
+                emit(acc ^ 1u, m * BM + BM, true, g, n, cnt);
+                release(acc ^ 1u);
+            }
+#if MP_PAIR_TRACE
+            const uint64_t e2 = clock64();
+            e_ext += e2 - e1;
+#endif
+            emit(acc, m * BM, p.tail128 && rows <= HM, g, n, cnt);
+            release(acc);
+#if MP_PAIR_TRACE
+            e_busy += clock64() - e1;
+#endif
         }
+#if MP_PAIR_TRACE
+        if (p.trace && warp == 2 && lane == 0) {  // epilogue timing of one warp per CTA
+            uint64_t* tr = p.trace + 2048 + blockIdx.x * 4;
+            tr[0] = e_busy;
+            tr[1] = e_ext;
+            tr[2] = e_wait;
+            tr[3] = tc;
+        }
+#endif
     }
     tc_fence_before();
     __syncthreads();
@@ -418,15 +495,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-size_t gemm_pair_smem_bytes() { return kSmemBytes; }
+size_t gemm_pair_smem_bytes() { return kSmemBytesX > kSmemBytes ? kSmemBytesX : kSmemBytes; }
 
-// tmB: box of 128 rows (each CTA loads half of the 256-row B tile)
+// tmB: box of 128 rows (each CTA loads half of the 256-row B tile).  variant:
+// kPairPlain (prefix of ceil(count/256)), kPairTail128 (<= 128-row tails as
+// M=128 MMAs), kPairExt (merged prefix: <= 128-row remainders ride on the
+// previous tile as an extra M=128 MMA sharing its B tile).  tmA64: 64-row A box.
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s, bool tail128,
+                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s, int variant,
                      const uint32_t* gmap, const CUtensorMap* tmA64) {
-    if (!tmA64) tail128 = false;  // tails need the 64-row A box
+    if (!tmA64) variant = kPairPlain;  // tails / remainders need the 64-row A box
     PairParams p{sh.G, sh.K, sh.N_group, sh.n_valid, sh.ld_out, (sh.N_group + BN - 1) / BN, offsets, mprefix256,
-                 static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), tail128 ? 1u : 0u, gmap};
+                 static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), variant == kPairTail128 ? 1u : 0u,
+                 variant == kPairExt ? 1u : 0u, gmap};
     if (p.trace) cudaMemsetAsync(p.trace, 0, (4096 + 128 * 128 * 4) * sizeof(uint64_t), s);
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;
@@ -434,14 +515,25 @@ void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB
     if (pairs == 0) pairs = 1;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(gemm_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_pair_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_pair_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        cudaFuncSetAttribute(gemm_pair_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesX);
+        cudaFuncSetAttribute(gemm_pair_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesX);
         attr_set = true;
     }
-    if (swiglu)
-        launch_k(gemm_pair_kernel<true>, dim3(2 * pairs), dim3(kThreads), kSmemBytes, s, *tmA, *tmB, tmA64 ? *tmA64 : *tmA, p);
-    else
-        launch_k(gemm_pair_kernel<false>, dim3(2 * pairs), dim3(kThreads), kSmemBytes, s, *tmA, *tmB, tmA64 ? *tmA64 : *tmA, p);
+    const CUtensorMap& a64 = tmA64 ? *tmA64 : *tmA;
+    const dim3 grid(2 * pairs), block(kThreads);
+    if (p.ext) {
+        if (swiglu)
+            launch_k(gemm_pair_kernel<true, true>, grid, block, kSmemBytesX, s, *tmA, *tmB, a64, p);
+        else
+            launch_k(gemm_pair_kernel<false, true>, grid, block, kSmemBytesX, s, *tmA, *tmB, a64, p);
+    } else {
+        if (swiglu)
+            launch_k(gemm_pair_kernel<true, false>, grid, block, kSmemBytes, s, *tmA, *tmB, a64, p);
+        else
+            launch_k(gemm_pair_kernel<false, false>, grid, block, kSmemBytes, s, *tmA, *tmB, a64, p);
+    }
 }
 
 }  // namespace mp

@@ -471,9 +471,8 @@ void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t
     mp::GemmShape s1{1, L->d_pad, 2 * L->sh_w_pad, T, L->sh_w_pad, 2 * L->sh_w_pad};
     mp::GemmShape s2{1, L->sh_w_pad, L->d_pad, T, L->d_pad, L->d_pad};
     if (sh_pair) {
-        mp::launch_gemm_tc2(true, &tmX, &L->tm_w1sh, L->sh_h, s1, L->sh_meta, L->sh_meta + 4, L->num_sms, ss, false);
-        mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, ss,
-                            false);
+        mp::launch_gemm_tc2(true, &tmX, &L->tm_w1sh, L->sh_h, s1, L->sh_meta, L->sh_meta + 4, L->num_sms, ss);
+        mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, ss);
     } else {
         mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
         mp::launch_gemm_tc(false, &L->tm_hs, &L->tm_w2s, L->sh_o, s2, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
@@ -491,9 +490,12 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     // 127 for 128-row tiles; measured break-even near 192 rows per bucket
     // (Mixtral shape: pairs win at k >= 4, lose at k = 2).  Per-token k: k_max.
     // Auto choice: the kernel with fewer padded rows per bucket (expected over
-    // bucket sizes M +- sqrt(M), M = T k / G), CTA pairs credited 10% for
-    // their lower operand traffic.  Mixtral: pairs at k >= 8; Qwen (w=352,
-    // buckets of 136-546 rows at prefill): 128-row tiles.
+    // bucket sizes M +- sqrt(M), M = T k / G), CTA pairs credited 5% for
+    // their lower operand traffic (tests/probes/tile_ab.py: 128-row tiles win
+    // at k <= 8, pairs at k = 16 and the 32k-token mixed batch).  Opt-in
+    // merged schedule (mode 6): a remainder of <= 128 rows rides on the
+    // previous tile as an M=128 MMA sharing its B tile.
+    const bool ext = L->tile_mode == 6;
     double rows = 0.0;
     {
         rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
@@ -502,9 +504,14 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         for (double m : {rows - sd, rows, rows + sd}) {
             const double mm = m < 1.0 ? 1.0 : m;
             pad128 += std::ceil(mm / 128.0) * 128.0;
-            pad256 += std::ceil(mm / 256.0) * 256.0;
+            if (ext) {
+                const double t = std::max(1.0, std::floor((mm + 127.0) / 256.0));
+                pad256 += (t + (mm > 256.0 * t ? 0.35 : 0.0)) * 256.0;
+            } else {
+                pad256 += std::ceil(mm / 256.0) * 256.0;
+            }
         }
-        const bool pairs_win = pad256 / 1.1 < pad128;
+        const bool pairs_win = pad256 / 1.05 < pad128;
         L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && rows >= 192.0 && pairs_win);
     }
     if (!bucketed) {
@@ -533,12 +540,13 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     const bool split = L->tile_mode == 5;
     (void)rows;
     const uint32_t G1 = L->G + 1;
-    const uint32_t* pre_pair = L->ws.mprefix_tc2 + (split ? G1 : 0);
+    const uint32_t* pre_pair = L->ws.mprefix_tc2 + (split ? G1 : ext ? 4 * G1 : 0);
+    const int variant = ext ? mp::kPairExt : L->tile_mode == 4 ? mp::kPairTail128 : mp::kPairPlain;
     const uint32_t* pre_tail = L->ws.mprefix_tc2 + 2 * G1;
     const uint32_t* tail_start = L->ws.mprefix_tc2 + 3 * G1;
     if (L->use_tc && L->tile256) {
         mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
-                            pre_pair, L->num_sms, s, L->tile_mode == 4, gmap, &L->tm_xperm64);
+                            pre_pair, L->num_sms, s, variant, gmap, &L->tm_xperm64);
         if (split)
             mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
                                pre_tail, L->num_sms, s, gmap, tail_start);
@@ -554,7 +562,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     tm.begin(4);
     if (L->use_tc && L->tile256) {
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
-                            pre_pair, L->num_sms, s, L->tile_mode == 4, gmap, &L->tm_h64);
+                            pre_pair, L->num_sms, s, variant, gmap, &L->tm_h64);
         if (split)
             mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
                                pre_tail, L->num_sms, s, gmap, tail_start);
@@ -725,6 +733,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                                : std::string(env) == "256-notail"  ? 3
                                : std::string(env) == "256-tail128" ? 4
                                : std::string(env) == "256-split"   ? 5
+                               : std::string(env) == "256-merged"  ? 6
                                                                    : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
@@ -795,7 +804,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 L->ws.offsets = dalloc<uint32_t>(L->G + 1, "offsets");
                 L->ws.mprefix_tc = dalloc<uint32_t>(L->G + 1, "mprefix");
                 L->ws.mprefix_simt = dalloc<uint32_t>(L->G + 1, "mprefix");
-                L->ws.mprefix_tc2 = dalloc<uint32_t>(4 * (L->G + 1), "mprefix");
+                L->ws.mprefix_tc2 = dalloc<uint32_t>(5 * (L->G + 1), "mprefix");
                 L->ws.perm_tok = dalloc<uint32_t>(L->rows_cap, "perm");
                 L->ws.perm_w = dalloc<float>(L->rows_cap, "perm w");
                 L->ws.slot_row = dalloc<uint32_t>(tk, "slot row");
@@ -1419,11 +1428,14 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
 // tiles (the default order) / 3 the same / 4 pairs with M=128 tail MMAs
 // (64-row A loads; measured 4% slower per step: profiles/r01_tile_ab.txt) / 5
 // the split schedule (tails <= 128 rows on the 1-SM kernel; +0.9 GB of DRAM
-// weight re-reads at k=8: profiles/ncu_summary_r01b.json), for A/B timing
-// (tests/probes/tile_ab.py).
+// weight re-reads at k=8: profiles/ncu_summary_r01b.json) / 6 pairs with
+// merged remainders (<= 128-row remainders as an extra M=128 MMA on the
+// group's previous tile; measured slower: the remainder accumulator takes
+// the other TMEM buffer, exposing an epilogue per merged tile), for A/B
+// timing (tests/probes/tile_ab.py).
 MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {
-        if (!L || mode < 0 || mode > 5) fail(MP_ERR_VALIDATION, "bad argument");
+        if (!L || mode < 0 || mode > 6) fail(MP_ERR_VALIDATION, "bad argument");
         L->tile_mode = mode;
     });
 }

@@ -34,7 +34,9 @@ MP_DEV uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-MP_DEV float silu_f32(float g) { return g / (1.0f + __expf(-g)); }
+// approximate reciprocal (rcp.approx, ~1 ulp): the GEMM epilogues round the
+// product to bf16 right after
+MP_DEV float silu_f32(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 MP_DEV uint32_t lane_id() {
     uint32_t r;

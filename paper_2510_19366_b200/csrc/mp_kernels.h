@@ -26,9 +26,10 @@ struct BucketWs {
     uint32_t* offsets;       // [G+1]
     uint32_t* mprefix_tc;    // [G+1] prefix of ceil(count/128)
     uint32_t* mprefix_simt;  // [G+1] prefix of ceil(count/64)
-    // [4][G+1]: prefix of ceil(count/256); pair-tile prefix of the split
+    // [5][G+1]: prefix of ceil(count/256); pair-tile prefix of the split
     // schedule (count/256 + (count%256 > 128)); its 1-SM tail-tile prefix
-    // (0 < count%256 <= 128); tail_start[g] (first row of that tail tile)
+    // (0 < count%256 <= 128); tail_start[g] (first row of that tail tile);
+    // merged (extended-tile) prefix max(1, (count + 127) / 256) (0 if empty)
     uint32_t* mprefix_tc2;
     uint32_t* perm_tok;      // [rows]
     float* perm_w;           // [rows]
@@ -140,9 +141,10 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
+constexpr int kPairPlain = 0, kPairTail128 = 1, kPairExt = 2;
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
-                     bool tail128 = true, const uint32_t* gmap = nullptr, const CUtensorMap* tmA64 = nullptr);
+                     int variant = kPairPlain, const uint32_t* gmap = nullptr, const CUtensorMap* tmA64 = nullptr);
 
 // Calibration (calib.cu).
 void launch_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,

@@ -558,6 +558,13 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     if (gi < G) mprefix_tc2[2 * (G + 1) + gi] = pretl;
     if (gi == 0) mprefix_tc2[2 * (G + 1) + G] = tot;
     if (gi < G) mprefix_tc2[3 * (G + 1) + gi] = off + c - rem;  // tail_start
+    // merged schedule (pair kernel default): a remainder <= 128 rows rides on
+    // the group's previous 256-row tile as an extra M=128 MMA sharing its B
+    // operand ("extended" tile of 257..384 rows); groups of <= 256 rows: 1 tile
+    const uint32_t mx = gi < G ? (c == 0 ? 0u : max(1u, (c + 127) / 256)) : 0;
+    const uint32_t prex = block_exclusive_scan_1024(mx, &tot, wsum);
+    if (gi < G) mprefix_tc2[4 * (G + 1) + gi] = prex;
+    if (gi == 0) mprefix_tc2[4 * (G + 1) + G] = tot;
     __syncthreads();
     if (gi < G) goff[gi] = off;
     __syncthreads();

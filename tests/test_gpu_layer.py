@@ -496,3 +496,32 @@ def test_forward_is_cuda_graph_capturable(oracle, torch_cuda):
         torch.cuda.synchronize()
         assert torch.equal(ys[0], want[0]) and torch.equal(ys[1], want[1])
     L.close()
+
+
+@pytest.mark.parametrize("k", [4, 8])
+def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
+    """Every GEMM schedule (1-SM 128-row tiles, CTA pairs plain / merged
+    remainders / M=128 tails / split tails) gives the same layer output: the
+    merged schedule's extended tiles (257..384 rows: an M=256 and an M=128 MMA
+    sharing one B tile) are exercised at these bucket sizes."""
+    import ctypes as C
+    torch = torch_cuda
+    from paper_2510_19366_b200 import _lib
+    L, x_dev, *_ = mixtral
+    lib = _lib.load()
+    lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
+    outs = {}
+    try:
+        for mode in (3, 1, 6, 4, 5):  # 256-plain, 128, 256-merged, 256-tail128, 256-split
+            _lib.check(lib.mp_debug_set_tile_mode(L.h, mode))
+            y, sel, w, off = L.forward(x_dev, k=k, return_routing=True)
+            torch.cuda.synchronize()
+            outs[mode] = y.float().cpu().numpy()
+    finally:
+        _lib.check(lib.mp_debug_set_tile_mode(L.h, 0))
+    cnt = np.diff(off.cpu().numpy().view(np.uint32).astype(np.int64))
+    assert ((cnt > 256) & (cnt % 256 > 0) & (cnt % 256 <= 128)).any()  # extended tiles occur
+    ref = outs[3]
+    for mode, y in outs.items():
+        ok = bf16_ok(y, ref)
+        assert ok.all(), f"mode {mode}: {(~ok).sum()} elements off"
