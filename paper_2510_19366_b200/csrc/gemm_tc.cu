@@ -331,11 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             } else {
-#pragma unroll 1
-                for (uint32_t c = 0; c < BN / 32; ++c) {
-                    uint32_t r[32];
-                    tmem_ld32(taddr + c * 32, r);
-                    tmem_ld_wait();
+                // two register sets: the TMEM load of chunk c + 1 is in flight
+                // while chunk c is converted and stored (short-K GEMMs, e.g.
+                // Qwen's K = 384 down projection, are epilogue-bound)
+                auto store = [&](uint32_t c, const uint32_t* r) {
                     const uint32_t col = n * BN + c * 32;
                     if (valid && col < p.n_valid) {
                         uint32_t pk[16];
@@ -347,6 +346,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int v = 0; v < 4; ++v)
                             st_global_v4(dst + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
                     }
+                };
+                uint32_t ra[32], rb[32];
+                tmem_ld32(taddr, ra);
+                tmem_ld_wait();
+#pragma unroll 1
+                for (uint32_t c = 0; c < BN / 32; c += 2) {
+                    tmem_ld32(taddr + (c + 1) * 32, rb);
+                    store(c, ra);
+                    tmem_ld_wait();
+                    if (c + 2 < BN / 32) tmem_ld32(taddr + (c + 2) * 32, ra);
+                    store(c + 1, rb);
+                    tmem_ld_wait();
                 }
             }
             tc_fence_before();

@@ -416,11 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 }
             } else {
-#pragma unroll 1
-                for (uint32_t c = part; c < nchunk; c += nparts) {
-                    uint32_t r[32];
-                    tmem_ld32(taddr + c * 32, r);
-                    tmem_ld_wait();
+                auto store = [&](uint32_t c, const uint32_t* r) {
                     const uint32_t col = n * BN + half * 128 + c * 32;
                     if (valid && col < p.n_valid) {
                         uint32_t pk[16];
@@ -432,6 +428,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         for (int v = 0; v < 4; ++v)
                             st_global_v4(dst + v * 8, make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]));
                     }
+                };
+                // the TMEM load of the next chunk overlaps this chunk's stores
+                uint32_t ra[32], rb[32];
+                tmem_ld32(taddr + part * 32, ra);
+                tmem_ld_wait();
+#pragma unroll 1
+                for (uint32_t c = part; c < nchunk; c += 2 * nparts) {
+                    const bool more = c + nparts < nchunk;
+                    if (more) tmem_ld32(taddr + (c + nparts) * 32, rb);
+                    store(c, ra);
+                    tmem_ld_wait();
+                    if (!more) break;
+                    if (c + 2 * nparts < nchunk) tmem_ld32(taddr + (c + 2 * nparts) * 32, ra);
+                    store(c + nparts, rb);
+                    tmem_ld_wait();
                 }
             }
         };

@@ -782,15 +782,17 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                     L->r_ticket = dalloc<uint32_t>(1, "router ticket");
                     ck(cudaMemset(L->r_ticket, 0, sizeof(uint32_t)), "memset ticket");
                     if (const char* env = std::getenv("MOEPRISM_ROUTER_GUARD")) L->r_guard = std::atof(env);
-                    if (!mp::make_tmap_bf16_2d(&L->tm_wplanes, L->wr_planes, 3ull * L->r_npad, L->d, L->r_npad, 64))
+                    if (!mp::make_tmap_bf16_2d(&L->tm_wplanes, L->wr_planes, 3ull * L->r_npad, L->d,
+                                               mp::router_tc_cols_per_cta(L->G), 64))
                         fail(MP_ERR_CUDA, "router planes tensor map");
                 }
                 if (D.router_mode == MP_ROUTER_PROXY) L->gate_off = dalloc<uint32_t>(L->G + 1, "gate offsets");
             }
             const size_t tk = (size_t)L->max_tokens * L->k_max;
-            // bucketing blocks: 32 tokens, or 8 in the fused router for small batches
-            const uint32_t nblk = std::max((L->max_tokens + mp::kRouteTokensPerBlock - 1) / mp::kRouteTokensPerBlock,
-                                           (std::min<uint32_t>(L->max_tokens, 1024) + 7) / 8);
+            // bucketing blocks: 32 tokens, or 8 / 2 in the fused router for small batches
+            const uint32_t nblk = std::max({(L->max_tokens + mp::kRouteTokensPerBlock - 1) / mp::kRouteTokensPerBlock,
+                                            (std::min<uint32_t>(L->max_tokens, 1024) + 7) / 8,
+                                            (std::min<uint32_t>(L->max_tokens, 256) + 1) / 2});
             L->sel = dalloc<uint32_t>(tk, "sel");
             L->wsel = dalloc<float>(tk, "w");
             L->kpt_dev = dalloc<uint32_t>(L->max_tokens, "k per token");

@@ -69,10 +69,11 @@ void launch_shared_gate(const void* x, uint32_t T, uint32_t d, const float* gate
 // Tensor-core linear router (router_tc.cu): plan, weight split, launch, and
 // the fixed-order fp64 reduction of the K-split partials + top-k (route.cu).
 struct RouterTcPlan {
-    uint32_t Npad, kb_total, kb_per_split, ks, m_tiles, stages, chunk_kb;
+    uint32_t Npad, kb_total, kb_per_split, ks, m_tiles, stages, chunk_kb, ncta, nsplit;
     size_t smem;
 };
 RouterTcPlan plan_router_tc(uint32_t T, uint32_t d, uint32_t G, int num_sms);
+uint32_t router_tc_cols_per_cta(uint32_t G);  // TMA box rows of the weight-plane tensor map
 void launch_split_router(const float* wr, uint32_t d, uint32_t G, uint32_t Npad, void* planes, cudaStream_t s);
 void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const RouterTcPlan& pl, uint32_t T,
                       double* partial, cudaStream_t s);
@@ -91,8 +92,8 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, double guard,
                          const void* x, uint32_t d, const float* wrT, uint32_t* ticket, uint32_t* n_fixed,
                          BucketWs& ws, cudaStream_t s, uint32_t tb = kRouteTokensPerBlock);
-// tokens per CTA of the fused routing epilogue: 8 for small batches (more CTAs)
-inline uint32_t route_tokens_per_block(uint32_t T) { return T <= 1024 ? 8u : kRouteTokensPerBlock; }
+// tokens per CTA of the fused routing epilogue: fewer for small batches (more CTAs)
+inline uint32_t route_tokens_per_block(uint32_t T) { return T <= 256 ? 2u : T <= 1024 ? 8u : kRouteTokensPerBlock; }
 // in-place fixed-order sum of the K-split router partials into plane 0
 void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, cudaStream_t s);
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,

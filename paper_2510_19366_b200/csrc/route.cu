@@ -496,24 +496,85 @@ __device__ uint32_t block_exclusive_scan_1024(uint32_t v, uint32_t* total, uint3
     return r;
 }
 
+#if MP_ROUTE_TRACE
+__device__ unsigned long long g_scan_tr[8];
+#define MP_SCAN_STAMP(i) \
+    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_scan_tr[i]))
+#else
+#define MP_SCAN_STAMP(i)
+#endif
+// V independent exclusive scans over the 1024 threads of the CTA with one
+// set of barriers (the bucket offsets and the GEMM tile prefixes)
+template <int V>
+__device__ void block_exclusive_scan_1024_multi(uint32_t (&v)[V], uint32_t (&total)[V], uint32_t (*wsum)[32]) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) inc[j] = v[j];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            const uint32_t n = __shfl_up_sync(0xffffffffu, inc[j], off);
+            if (lane >= (uint32_t)off) inc[j] += n;
+        }
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) wsum[j][warp] = inc[j];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t sv[V], si[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) sv[j] = si[j] = wsum[j][lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                const uint32_t n = __shfl_up_sync(0xffffffffu, si[j], off);
+                if (lane >= (uint32_t)off) si[j] += n;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) wsum[j][lane] = si[j] - sv[j];
+        if (lane == 31) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) wsum[V][j] = si[j];  // totals row
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        total[j] = wsum[V][j];
+        v[j] = wsum[j][warp] + inc[j] - v[j];
+    }
+    __syncthreads();
+}
+
 __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __restrict__ block_counts,
                                  uint32_t* __restrict__ block_base, uint32_t* __restrict__ offsets,
                                  uint32_t* __restrict__ mprefix_tc, uint32_t* __restrict__ mprefix_simt,
                                  uint32_t* __restrict__ mprefix_tc2) {
     // thread (g, q): bucket g, q-th contiguous range of CTA-blocks; consecutive
     // threads read consecutive buckets of one block row (coalesced)
+    constexpr int V = 7;
     __shared__ uint32_t part[1024];
     __shared__ uint32_t goff[kMaxG];
-    __shared__ uint32_t wsum[32];
-    __shared__ uint32_t tot;
+    __shared__ uint32_t wsum[V + 1][32];
     const uint32_t Q = blockDim.x / G;
     const uint32_t g = threadIdx.x % G, q = threadIdx.x / G;
     const bool active = q < Q;
     const uint32_t per = (nblk + Q - 1) / Q;
     const uint32_t b0 = q * per, b1 = min(b0 + per, nblk);
+    MP_SCAN_STAMP(0);
     uint32_t sum = 0;
-    if (active)
+    // independent loads in flight (Qwen prefill: 256 blocks x 240 buckets,
+    // 64 blocks per thread): the last CTA's scan is on the critical path
+    if (active) {
+#pragma unroll 16
         for (uint32_t b = b0; b < b1; ++b) sum += block_counts[(size_t)b * G + g];
+    }
     part[threadIdx.x] = sum;
     __syncthreads();
     // exclusive prefix over the Q ranges of each bucket, and bucket totals
@@ -530,50 +591,59 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     if (active && q == 0) goff[g] = total;
     __syncthreads();
     const uint32_t c = gi < G ? goff[gi] : 0;
-    const uint32_t off = block_exclusive_scan_1024(c, &tot, wsum);
-    if (gi < G) offsets[gi] = off;
-    if (gi == 0) offsets[G] = tot;
-    const uint32_t mt = gi < G ? (c + kTcBM - 1) / kTcBM : 0;
-    const uint32_t mpre = block_exclusive_scan_1024(mt, &tot, wsum);
-    if (gi < G) mprefix_tc[gi] = mpre;
-    if (gi == 0) mprefix_tc[G] = tot;
-    const uint32_t ms = gi < G ? (c + kSimtBM - 1) / kSimtBM : 0;
-    const uint32_t spre = block_exclusive_scan_1024(ms, &tot, wsum);
-    if (gi < G) mprefix_simt[gi] = spre;
-    if (gi == 0) mprefix_simt[G] = tot;
-    const uint32_t m2 = gi < G ? (c + 255) / 256 : 0;
-    const uint32_t pre2 = block_exclusive_scan_1024(m2, &tot, wsum);
-    if (gi < G) mprefix_tc2[gi] = pre2;
-    if (gi == 0) mprefix_tc2[G] = tot;
-    // split schedule (kPairSplit): CTA-pair tiles for the full 256-row blocks
-    // and a remainder > 128 rows; a remainder <= 128 rows goes to one 128-row
-    // 1-SM tile starting at tail_start[g] (half the SM time of a pair tile)
+    MP_SCAN_STAMP(1);
+    // bucket offsets and the GEMM tile prefixes, scanned together:
+    //   offsets (rows), 128-row tiles, 64-row SIMT tiles, 256-row pair tiles,
+    //   the split schedule's pair tiles (full 256-row blocks + a remainder
+    //   > 128 rows) and 1-SM tail tiles (remainder <= 128 rows), and the
+    //   merged schedule (a remainder <= 128 rows rides on the previous tile
+    //   as an extra M=128 MMA; groups of <= 256 rows: 1 tile)
     const uint32_t rem = c % 256;
-    const uint32_t mpf = gi < G ? c / 256 + (rem > 128 ? 1u : 0u) : 0;
-    const uint32_t prepf = block_exclusive_scan_1024(mpf, &tot, wsum);
-    if (gi < G) mprefix_tc2[(G + 1) + gi] = prepf;
-    if (gi == 0) mprefix_tc2[(G + 1) + G] = tot;
-    const uint32_t mtl = gi < G ? ((rem > 0 && rem <= 128) ? 1u : 0u) : 0;
-    const uint32_t pretl = block_exclusive_scan_1024(mtl, &tot, wsum);
-    if (gi < G) mprefix_tc2[2 * (G + 1) + gi] = pretl;
-    if (gi == 0) mprefix_tc2[2 * (G + 1) + G] = tot;
-    if (gi < G) mprefix_tc2[3 * (G + 1) + gi] = off + c - rem;  // tail_start
-    // merged schedule (pair kernel default): a remainder <= 128 rows rides on
-    // the group's previous 256-row tile as an extra M=128 MMA sharing its B
-    // operand ("extended" tile of 257..384 rows); groups of <= 256 rows: 1 tile
-    const uint32_t mx = gi < G ? (c == 0 ? 0u : max(1u, (c + 127) / 256)) : 0;
-    const uint32_t prex = block_exclusive_scan_1024(mx, &tot, wsum);
-    if (gi < G) mprefix_tc2[4 * (G + 1) + gi] = prex;
-    if (gi == 0) mprefix_tc2[4 * (G + 1) + G] = tot;
+    uint32_t sv[V] = {c,
+                      gi < G ? (c + kTcBM - 1) / kTcBM : 0u,
+                      gi < G ? (c + kSimtBM - 1) / kSimtBM : 0u,
+                      gi < G ? (c + 255) / 256 : 0u,
+                      gi < G ? c / 256 + (rem > 128 ? 1u : 0u) : 0u,
+                      gi < G ? ((rem > 0 && rem <= 128) ? 1u : 0u) : 0u,
+                      gi < G ? (c == 0 ? 0u : max(1u, (c + 127) / 256)) : 0u};
+    uint32_t tot[V];
+    block_exclusive_scan_1024_multi<V>(sv, tot, wsum);
+    const uint32_t off = sv[0];
+    if (gi < G) {
+        offsets[gi] = off;
+        mprefix_tc[gi] = sv[1];
+        mprefix_simt[gi] = sv[2];
+        mprefix_tc2[gi] = sv[3];
+        mprefix_tc2[(G + 1) + gi] = sv[4];
+        mprefix_tc2[2 * (G + 1) + gi] = sv[5];
+        mprefix_tc2[3 * (G + 1) + gi] = off + c - rem;  // tail_start
+        mprefix_tc2[4 * (G + 1) + gi] = sv[6];
+    }
+    if (gi == 0) {
+        offsets[G] = tot[0];
+        mprefix_tc[G] = tot[1];
+        mprefix_simt[G] = tot[2];
+        mprefix_tc2[G] = tot[3];
+        mprefix_tc2[(G + 1) + G] = tot[4];
+        mprefix_tc2[2 * (G + 1) + G] = tot[5];
+        mprefix_tc2[4 * (G + 1) + G] = tot[6];
+    }
     __syncthreads();
     if (gi < G) goff[gi] = off;
     __syncthreads();
+    MP_SCAN_STAMP(2);
     if (active) {
         uint32_t running = goff[g] + qbase;
-        for (uint32_t b = b0; b < b1; ++b) {
-            const uint32_t v = block_counts[(size_t)b * G + g];
-            block_base[(size_t)b * G + g] = running;
-            running += v;
+        constexpr uint32_t U = 16;
+        for (uint32_t b = b0; b < b1; b += U) {
+            uint32_t v[U];
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) v[u] = b + u < b1 ? block_counts[(size_t)(b + u) * G + g] : 0u;
+#pragma unroll
+            for (uint32_t u = 0; u < U; ++u) {
+                if (b + u < b1) block_base[(size_t)(b + u) * G + g] = running;
+                running += v[u];
+            }
         }
     }
 }
@@ -650,9 +720,9 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     const float* __restrict__ wrT, uint32_t* __restrict__ ticket, uint32_t* __restrict__ n_fixed, uint32_t* lrank,
     uint32_t* block_counts, uint32_t* block_base, uint32_t* offsets, uint32_t* mprefix_tc, uint32_t* mprefix_simt,
     uint32_t* mprefix_tc2, uint32_t tb) {
-    extern __shared__ double rsm[];  // [TB][G] logits, then [TB][G] keys
-    double* sc = rsm + (size_t)(threadIdx.x / 32) * G;
-    double* key = rsm + (size_t)(TB + threadIdx.x / 32) * G;
+    extern __shared__ double rsm[];  // [tb][G] logits, then [tb][G] keys
+    double* sc = rsm + (size_t)(threadIdx.x / 32) * G;        // used by warps < tb only
+    double* key = rsm + (size_t)(tb + threadIdx.x / 32) * G;
     __shared__ double vk[TB][2];
     __shared__ uint32_t msk[TB][kMaxG / 32];
     __shared__ uint16_t slot_of[TB][kMaxG];
@@ -662,6 +732,15 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     __shared__ uint32_t pair_tg[kMaxPairs];  // (token in CTA << 16) | candidate
     __shared__ double pair_part[kPairBatch][4];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#if MP_ROUTE_TRACE
+    uint64_t tr_[8];
+    uint32_t ntr_ = 0;
+    auto stamp = [&]() { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_[ntr_++])); };
+    stamp();
+#define MP_RT_STAMP() stamp()
+#else
+#define MP_RT_STAMP()
+#endif
     // tb tokens per CTA (warps >= tb only help with the CTA-wide phases):
     // small batches use tb = 8 so the token work spreads over 4x the SMs
     const uint32_t t0 = blockIdx.x * tb, t = warp < tb ? t0 + warp : T;
@@ -674,11 +753,24 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     bool flagged = false;
     uint32_t kt = 0;
     if (t < T) {
-        for (uint32_t g = lane; g < G; g += 32) {
-            double v = 0.0;
-            for (uint32_t s = 0; s < ks; ++s) v += partial[((size_t)s * T + t) * Npad + g];
-            sc[g] = v;
+        // fixed-order sum over the K splits; all NC loads of a split in flight
+        // (the partials come from L2 / HBM: a load per candidate in turn left
+        // this phase latency-bound, 7 us for 240 candidates)
+        double v[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c] = 0.0;
+        const double* prow = partial + (size_t)t * Npad + lane;
+#pragma unroll 2
+        for (uint32_t s = 0; s < ks; ++s) {
+            double u[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) u[c] = lane + 32u * c < G ? __ldcg(prow + (size_t)s * T * Npad + 32u * c) : 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) v[c] += u[c];
         }
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+            if (lane + 32u * c < G) sc[lane + 32u * c] = v[c];
         __syncwarp();
         kt = token_k(kpt, k_scalar, t, k_max, G, err);
         const double gap = warp_topk_fast<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
@@ -700,6 +792,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         }
     }
     __syncthreads();
+    MP_RT_STAMP();  // 1: top-k done
     // exact fp64 logits of every queued (token, candidate), 4 warps per pair
     // (d split in quarters, fixed-order combination: deterministic)
     const uint32_t np = min(n_pairs, kMaxPairs);
@@ -720,7 +813,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
                 const uint32_t pj = p0 + q2, tl = pair_tg[pj] >> 16, g = pair_tg[pj] & 0xFFFFu;
                 const double* pp = pair_part[pj % kPairBatch];
                 const double e = ((pp[0] + pp[1]) + pp[2]) + pp[3];
-                rsm[(size_t)(TB + tl) * G + g] = e;  // key
+                rsm[(size_t)(tb + tl) * G + g] = e;  // key
                 rsm[(size_t)tl * G + g] = e;         // logit (weights)
             }
             __syncthreads();
@@ -740,6 +833,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         if (lane == 0) atomicAdd(n_fixed, 1u);
     }
     __syncthreads();  // this CTA's selections are visible to the CTA
+    MP_RT_STAMP();    // 2: exact pass done
     for (uint32_t q = threadIdx.x; q < tb * k_max; q += blockDim.x) {
         const uint32_t tt = q / k_max, j = q % k_max;
         if (t0 + tt >= T) continue;
@@ -757,11 +851,28 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     }
     __threadfence();
     __syncthreads();
+    MP_RT_STAMP();  // 3: ranks done
     if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     __syncthreads();
+    MP_RT_STAMP();  // 4: ticket taken
+#if MP_ROUTE_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0 && !is_last)
+        printf("route_bucket blk %u: topk %llu exact %llu ranks %llu ticket %llu ns (start %llu)\n", blockIdx.x,
+               tr_[1] - tr_[0], tr_[2] - tr_[1], tr_[3] - tr_[2], tr_[4] - tr_[3], tr_[0]);
+#endif
     if (!is_last) return;
     __threadfence();
     bucket_scan_body(gridDim.x, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt, mprefix_tc2);
+#if MP_ROUTE_TRACE
+    __syncthreads();
+    MP_RT_STAMP();  // 5: scan done
+    if (threadIdx.x == 0)
+        printf("route_bucket last blk %u: topk %llu exact %llu ranks %llu ticket %llu scan %llu ns [fence %llu counts "
+               "%llu scans %llu base %llu] (start %llu)\n",
+               blockIdx.x, tr_[1] - tr_[0], tr_[2] - tr_[1], tr_[3] - tr_[2], tr_[4] - tr_[3], tr_[5] - tr_[4],
+               g_scan_tr[0] - tr_[4], g_scan_tr[1] - g_scan_tr[0], g_scan_tr[2] - g_scan_tr[1],
+               tr_[5] - g_scan_tr[2], tr_[0]);
+#endif
     if (threadIdx.x == 0) *ticket = 0;  // ready for the next forward (stream-ordered)
 }
 
@@ -1091,12 +1202,15 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, double guard,
                          const void* x, uint32_t d, const float* wrT, uint32_t* ticket, uint32_t* n_fixed,
                          BucketWs& ws, cudaStream_t s, uint32_t tb) {
-    const size_t smem = sizeof(double) * 2 * TB * G;
+    const size_t smem = sizeof(double) * 2 * tb * G;
     static bool attr_set[3] = {false, false, false};
     auto launch = [&](auto kern, int which) {
         if (!attr_set[which]) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(double) * 2 * TB * kMaxG));
+            // same shared-memory carveout as the GEMMs around it: no L1/smem
+            // reconfiguration between the kernels of the chain
+            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
             attr_set[which] = true;
         }
         launch_k(kern, dim3((T + tb - 1) / tb), dim3(1024), smem, s,

@@ -29,7 +29,8 @@ constexpr uint32_t kMaxStages = 6;
 
 struct RouterTcParams {
     uint32_t T, Npad, kb_total, kb_per_split, stages, chunk_kb;
-    double* partial;  // [KS][T][Npad]
+    uint32_t ncta, nsplit;  // columns per CTA, column splits (blockIdx.y = K split * nsplit + column split)
+    double* partial;        // [KS][T][Npad]
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -38,7 +39,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t a_bytes = BM * BK * 2;
-    const uint32_t plane_bytes = p.Npad * BK * 2;
+    const uint32_t plane_bytes = p.ncta * BK * 2;
+    const uint32_t ksplit = blockIdx.y / p.nsplit, n0 = (blockIdx.y % p.nsplit) * p.ncta;
     const uint32_t stage_bytes = a_bytes + 3 * plane_bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + p.stages * stage_bytes);
     uint64_t* empty = full + kMaxStages;
@@ -47,7 +49,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t m0 = blockIdx.x * BM;
-    const uint32_t kb0 = blockIdx.y * p.kb_per_split;
+    const uint32_t kb0 = ksplit * p.kb_per_split;
     const uint32_t kb1 = min(kb0 + p.kb_per_split, p.kb_total);
 
     if (threadIdx.x == 0) {
@@ -80,12 +82,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d(st, &tmX, &full[s], static_cast<int32_t>(kb * BK), static_cast<int32_t>(m0));
                 for (uint32_t q = 0; q < 3; ++q)
                     tma_load_2d(st + a_bytes + q * plane_bytes, &tmW, &full[s], static_cast<int32_t>(kb * BK),
-                                static_cast<int32_t>(q * p.Npad));
+                                static_cast<int32_t>(q * p.Npad + n0));
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = umma_idesc_bf16(BM, p.Npad);
+            const uint32_t idesc = umma_idesc_bf16(BM, p.ncta);
             for (uint32_t kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
                 const uint32_t s = it % p.stages, ph = (it / p.stages) & 1u;
                 mbar_wait(&full[s], ph);
@@ -94,8 +96,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool first = ((kb - kb0) % p.chunk_kb) == 0;
                 // hi plane and (mid + lo) planes in separate accumulators: the
                 // small planes never round at the hi accumulator's ulp
-                const uint32_t d_hi = tmem_base + chunk * 2 * p.Npad;
-                const uint32_t d_ml = d_hi + p.Npad;
+                const uint32_t d_hi = tmem_base + chunk * 2 * p.ncta;
+                const uint32_t d_ml = d_hi + p.ncta;
                 const uint32_t a0 = smem_u32(base + s * stage_bytes);
 #pragma unroll
                 for (uint32_t k = 0; k < BK / 16; ++k) {
@@ -116,16 +118,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t t = m0 + q * 32 + lane;
         const uint32_t nchunks = (kb1 - kb0 + p.chunk_kb - 1) / p.chunk_kb;
-        double* out = p.partial + (static_cast<size_t>(blockIdx.y) * p.T + t) * p.Npad;
-        for (uint32_t grp = 0; grp < p.Npad / 32; ++grp) {
+        double* out = p.partial + (static_cast<size_t>(ksplit) * p.T + t) * p.Npad + n0;
+        for (uint32_t grp = 0; grp < p.ncta / 32 && n0 + grp * 32 < p.Npad; ++grp) {
             double acc[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] = 0.0;
             for (uint32_t c = 0; c < nchunks; ++c) {
                 uint32_t rh[32], rl[32];
-                const uint32_t col = tmem_base + ((q * 32u) << 16) + c * 2 * p.Npad + grp * 32;
+                const uint32_t col = tmem_base + ((q * 32u) << 16) + c * 2 * p.ncta + grp * 32;
                 tmem_ld32(col, rh);
-                tmem_ld32(col + p.Npad, rl);
+                tmem_ld32(col + p.ncta, rl);
                 tmem_ld_wait();
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
@@ -166,18 +168,30 @@ __global__ void split_router_kernel(const float* __restrict__ wr, uint32_t d, ui
 
 }  // namespace
 
+uint32_t router_tc_cols_per_cta(uint32_t G) {
+    const uint32_t npad = ((G + 31) / 32) * 32;
+    const uint32_t nsplit = (npad + 127) / 128;
+    return ((npad / nsplit + 31) / 32) * 32;
+}
+
 RouterTcPlan plan_router_tc(uint32_t T, uint32_t d, uint32_t G, int num_sms) {
     RouterTcPlan pl{};
     pl.Npad = ((G + 31) / 32) * 32;
+    // > 128 sub-experts (Qwen: 240): columns split over CTAs, so a stage of
+    // the three weight planes stays <= 48 KB (3 stages instead of 1) and two
+    // 256-deep chunks fit in TMEM (half the K splits and partials)
+    pl.ncta = router_tc_cols_per_cta(G);
+    pl.nsplit = (pl.Npad + pl.ncta - 1) / pl.ncta;
     pl.kb_total = (d + BK - 1) / BK;
     const uint32_t m_tiles = (T + BM - 1) / BM;
+    const uint32_t mn_tiles = m_tiles * pl.nsplit;
     // few token tiles (decode): 64-deep chunks give 4x the K splits (CTAs),
     // cutting the per-CTA operand stream that bounds small-batch latency
-    pl.chunk_kb = m_tiles * ((pl.kb_total + kChunkKb - 1) / kChunkKb) < static_cast<uint32_t>(num_sms) / 2 ? 1
-                                                                                                          : kChunkKb;
+    pl.chunk_kb = mn_tiles * ((pl.kb_total + kChunkKb - 1) / kChunkKb) < static_cast<uint32_t>(num_sms) / 2 ? 1
+                                                                                                           : kChunkKb;
     const uint32_t n_chunks = (pl.kb_total + pl.chunk_kb - 1) / pl.chunk_kb;
-    const uint32_t max_chunks_per_cta = 512 / (2 * pl.Npad);
-    uint32_t ks = (static_cast<uint32_t>(num_sms) + m_tiles - 1) / m_tiles;
+    const uint32_t max_chunks_per_cta = 512 / (2 * pl.ncta);
+    uint32_t ks = (static_cast<uint32_t>(num_sms) + mn_tiles - 1) / mn_tiles;
     ks = ks < 1 ? 1 : ks;
     ks = ks > n_chunks ? n_chunks : ks;
     const uint32_t ks_min = (n_chunks + max_chunks_per_cta - 1) / max_chunks_per_cta;
@@ -186,7 +200,7 @@ RouterTcPlan plan_router_tc(uint32_t T, uint32_t d, uint32_t G, int num_sms) {
     pl.kb_per_split = chunks_per_split * pl.chunk_kb;
     pl.ks = (pl.kb_total + pl.kb_per_split - 1) / pl.kb_per_split;
     pl.m_tiles = m_tiles;
-    const uint32_t stage_bytes = BM * BK * 2 + 3 * pl.Npad * BK * 2;
+    const uint32_t stage_bytes = BM * BK * 2 + 3 * pl.ncta * BK * 2;
     uint32_t stages = (200u * 1024u) / stage_bytes;
     pl.stages = stages > kMaxStages ? kMaxStages : stages;
     pl.smem = 1024 + pl.stages * stage_bytes + 256;
@@ -199,13 +213,13 @@ void launch_split_router(const float* wr, uint32_t d, uint32_t G, uint32_t Npad,
 
 void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const RouterTcPlan& pl, uint32_t T,
                       double* partial, cudaStream_t s) {
-    RouterTcParams p{T, pl.Npad, pl.kb_total, pl.kb_per_split, pl.stages, pl.chunk_kb, partial};
+    RouterTcParams p{T, pl.Npad, pl.kb_total, pl.kb_per_split, pl.stages, pl.chunk_kb, pl.ncta, pl.nsplit, partial};
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr_set = true;
     }
-    launch_k(router_tc_kernel, dim3(pl.m_tiles, pl.ks), dim3(kThreads), pl.smem, s, *tmX, *tmW, p);
+    launch_k(router_tc_kernel, dim3(pl.m_tiles, pl.ks * pl.nsplit), dim3(kThreads), pl.smem, s, *tmX, *tmW, p);
 }
 
 }  // namespace mp
