@@ -24,7 +24,8 @@ for r in rows[2:]:
     name = r[h.index("Kernel Name")]
     short = name.split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "").split("::")[-1]
     if "gemm_pair_kernel" in short or "gemm_tc_kernel" in short:
-        short += "<swiglu>" if "<1>" in name or "<(int)1>" in name or "ILi1E" in name else "<plain>"
+        sw = any(t in name for t in ("<1>", "<(int)1>", "ILi1E", "<true", "<1, ", "ILb1E"))
+        short += "<swiglu>" if sw else "<plain>"
     ent = {}
     for w, i in idx.items():
         try:

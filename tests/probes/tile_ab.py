@@ -2,8 +2,9 @@
 Under the 1000 W cap the clock follows power, so wall time alone is noisy
 across blocks; energy per step (NVML total energy) is the power-robust
 metric: at the cap, throughput ~ P_cap / energy_per_step.
-  python tests/probes/tile_ab.py <k-list> <mode-list> [reps] [steps-per-block]
-modes: 1 128-row 1-SM, 2 pairs, 4 pairs with M=128 tails, 5 pairs + 1-SM tails (split)"""
+  python tests/probes/tile_ab.py <k-list> <mode-list> [reps] [steps-per-block] [qwen]
+modes: 1 128-row 1-SM, 2 pairs, 4 pairs with M=128 tails, 5 pairs + 1-SM tails (split),
+6 pairs with merged remainders; "qwen": the Qwen layer at T=8192 instead of Mixtral T=4096"""
 import ctypes as C, statistics, sys
 import torch
 sys.path.insert(0, '.')
@@ -12,10 +13,18 @@ from paper_2510_19366_b200 import _lib
 import pynvml
 pynvml.nvmlInit()
 hnd = pynvml.nvmlDeviceGetHandleByIndex(0)
-L, xs = bench.build_layer(0, 4096, 16)
+if len(sys.argv) > 5 and sys.argv[5] == "qwen":
+    from paper_2510_19366_b200 import synth_fill
+    T = 8192
+    L = bench.build_qwen_layer(T)
+    xs = [synth_fill(torch.empty((T, bench.QW["d"]), dtype=torch.bfloat16, device="cuda"), 19 + i, 1.0)
+          for i in range(8)]
+else:
+    T = 4096
+    L, xs = bench.build_layer(0, T, 16)
 lib = _lib.load()
 lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
-y = torch.empty((4096, bench.D), dtype=torch.bfloat16, device='cuda')
+y = torch.empty_like(xs[0])
 names = {0: "auto", 1: "128-row", 2: "pair", 3: "pair", 4: "pair-tail128", 5: "split", 6: "pair-merged"}
 ks = [int(a) for a in sys.argv[1].split(",")]
 modes = [int(a) for a in sys.argv[2].split(",")]
