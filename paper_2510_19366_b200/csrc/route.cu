@@ -469,33 +469,6 @@ __global__ void __launch_bounds__(256) bucket_local_kernel(const uint32_t* __res
 
 // Exclusive scans: over CTAs per bucket (-> block_base), over buckets
 // (-> offsets), and the GEMM tile prefixes.  One CTA of 1024 threads.
-__device__ uint32_t block_exclusive_scan_1024(uint32_t v, uint32_t* total, uint32_t* wsum) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t inc = v;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t n = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= (uint32_t)off) inc += n;
-    }
-    if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t s = wsum[lane];
-        uint32_t si = s;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t n = __shfl_up_sync(0xffffffffu, si, off);
-            if (lane >= (uint32_t)off) si += n;
-        }
-        wsum[lane] = si - s;
-        if (lane == 31) *total = si;
-    }
-    __syncthreads();
-    const uint32_t r = wsum[warp] + inc - v;
-    __syncthreads();
-    return r;
-}
-
 #if MP_ROUTE_TRACE
 __device__ unsigned long long g_scan_tr[8];
 #define MP_SCAN_STAMP(i) \
@@ -503,6 +476,7 @@ __device__ unsigned long long g_scan_tr[8];
 #else
 #define MP_SCAN_STAMP(i)
 #endif
+
 // V independent exclusive scans over the 1024 threads of the CTA with one
 // set of barriers (the bucket offsets and the GEMM tile prefixes)
 template <int V>
