@@ -621,7 +621,11 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
                 // routing epilogue + exact near-tie re-selection + bucketing in one kernel;
                 // many K splits (small batches): reduce them first across (token, g) warps
                 uint32_t ks = pl.ks;
-                if (ks > 8) {
+                static const uint32_t reduce_above = [] {  // MOEPRISM_PARTIALS_REDUCE_ABOVE (A/B)
+                    const char* e = std::getenv("MOEPRISM_PARTIALS_REDUCE_ABOVE");
+                    return e ? static_cast<uint32_t>(std::atoi(e)) : 8u;
+                }();
+                if (ks > reduce_above) {
                     mp::launch_partials_reduce(L->r_partial, ks, T, L->G, pl.Npad, s);
                     ks = 1;
                     L->r_last_ks = 1;  // plane 0 now holds the logits

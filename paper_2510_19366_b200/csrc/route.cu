@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
 #pragma unroll
         for (int c = 0; c < NC; ++c) v[c] = 0.0;
         const double* prow = partial + (size_t)t * Npad + lane;
-#pragma unroll 2
+#pragma unroll 4
         for (uint32_t s = 0; s < ks; ++s) {
             double u[NC];
 #pragma unroll
@@ -992,7 +992,9 @@ __global__ void __launch_bounds__(128) dispatch_bulk_kernel(const __nv_bfloat16*
         for (int q = 0; q < 8; ++q) bad |= !isfinite(__bfloat162float(h[q]));
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0 && err) atomicOr(err, 2);
-    if (lane == 0) bulk_wait0();  // stores complete (smem read out, global written) before the CTA exits
+    // the staged row must stay until the bulk stores have read it out; their
+    // global writes are visible to the next kernel at the grid boundary
+    if (lane == 0) bulk_wait_read0();
     __syncwarp();
 }
 
