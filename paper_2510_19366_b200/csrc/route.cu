@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
 // engine streams at HBM rate with no per-16-byte instructions; the warp checks
 // the row for non-finite values from shared memory meanwhile.
 constexpr uint32_t kBulkRowMax = 16384;  // bytes of one staged row (d <= 8192 bf16)
-__global__ void __launch_bounds__(128) dispatch_bulk_kernel(const __nv_bfloat16* __restrict__ x, uint32_t T,
+__global__ void __launch_bounds__(256) dispatch_bulk_kernel(const __nv_bfloat16* __restrict__ x, uint32_t T,
                                                             uint32_t d, const uint32_t* __restrict__ sel,
                                                             const float* __restrict__ w, uint32_t k_max, uint32_t G,
                                                             const uint32_t* __restrict__ lrank,
@@ -944,10 +944,10 @@ __global__ void __launch_bounds__(128) dispatch_bulk_kernel(const __nv_bfloat16*
                                                             uint32_t* __restrict__ slot_row,
                                                             __nv_bfloat16* __restrict__ x_perm,
                                                             int* __restrict__ err, uint32_t tb) {
-    extern __shared__ __align__(128) uint8_t drow[];  // [4 warps][row bytes]
-    __shared__ __align__(8) uint64_t bar[4];
+    extern __shared__ __align__(128) uint8_t drow[];  // [warps][row bytes]
+    __shared__ __align__(8) uint64_t bar[8];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const uint32_t t = blockIdx.x * 4 + warp;
+    const uint32_t t = blockIdx.x * (blockDim.x / 32) + warp;
     const uint32_t row_bytes = d * 2;
     uint8_t* srow = drow + (size_t)warp * row_bytes;
     if (lane == 0) {
@@ -1247,14 +1247,24 @@ void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t 
     }();
     if (dtype == 1 && x_perm && d == d_pad && (d % 8) == 0 && d * 2 <= kBulkRowMax && bulk_env &&
         (reinterpret_cast<uintptr_t>(x) % 16) == 0) {
-        const size_t smem = 4 * (size_t)d * 2;
+        // warps (staged rows) per CTA.  Measured (ncu, Mixtral T=4096, medians
+        // of 5): 3 -> 50.6 / 90.8 us at k=8 / 16, 4 -> 57.7 / 94.7, 2 -> 53.4 /
+        // 93.2, 1 -> 54.0 / 94.4 (9 CTAs x 3 rows of 8 KB per SM)
+        static const uint32_t wpc = [] {
+            const char* e = std::getenv("MOEPRISM_DISPATCH_WARPS");
+            const int v = e ? std::atoi(e) : 3;
+            return static_cast<uint32_t>(v < 1 ? 1 : v > 8 ? 8 : v);
+        }();
+        const size_t smem = wpc * (size_t)d * 2;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(4 * kBulkRowMax));
+                                 (int)(8 * kBulkRowMax));
+            cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
             attr = true;
         }
-        launch_k(dispatch_bulk_kernel, dim3((T + 3) / 4), dim3(128), smem, s,
+        launch_k(dispatch_bulk_kernel, dim3((T + wpc - 1) / wpc), dim3(32 * wpc), smem, s,
             static_cast<const __nv_bfloat16*>(x), T, d, sel, w, k_max, G, ws.lrank, ws.block_base, ws.perm_tok,
             ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), check_finite ? ws.err : nullptr, tb);
         return;
