@@ -817,11 +817,13 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         slot_of[tt][g] = static_cast<uint16_t>(j);
     }
     __syncthreads();
-    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) {
-        uint32_t cnt = 0;
-        for (uint32_t tt = 0; tt < tb && t0 + tt < T; ++tt)
-            if ((msk[tt][g >> 5] >> (g & 31)) & 1u) lrank[(size_t)(t0 + tt) * k_max + slot_of[tt][g]] = cnt++;
-        block_counts[(size_t)blockIdx.x * G + g] = cnt;
+    // warp per bucket, lane per token (tb <= 32): the stable rank of token tt
+    // in bucket g is the number of earlier tokens of the CTA selecting g
+    for (uint32_t g = warp; g < G; g += blockDim.x / 32) {
+        const bool has = lane < tb && t0 + lane < T && ((msk[lane][g >> 5] >> (g & 31)) & 1u);
+        const uint32_t bal = __ballot_sync(0xffffffffu, has);
+        if (has) lrank[(size_t)(t0 + lane) * k_max + slot_of[lane][g]] = __popc(bal & ((1u << lane) - 1u));
+        if (lane == 0) block_counts[(size_t)blockIdx.x * G + g] = __popc(bal);
     }
     __threadfence();
     __syncthreads();
