@@ -96,6 +96,8 @@ struct PairParams {
     uint64_t* trace;  // [grid][4] MMA-issuer timing of the leaders (diagnostics) or null
     uint32_t tail128;  // tiles with <= 128 valid rows issue M=128 pair MMAs
     uint32_t ext;      // mprefix is the merged schedule: 257..384-row extended tiles
+    uint32_t wide;     // wide-tail schedule: mprefix = pair tiles per n, tprefix = <= 128-row tails
+    const uint32_t* tprefix;
     const uint32_t* gmap;  // nullable: B group of group g (sub-expert offload cache slot), else g
 };
 
@@ -192,6 +194,47 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
     m = local - n * mt;
 }
 
+// Tile kinds: full M=256 pair tile; M=128 tail (64 A rows per CTA); EXT: full
+// tile + merged M=128 remainder; WIDE: a <= 128-row remainder over two N
+// tiles at once (two M=128 MMAs sharing the A stage, one 256-column buffer).
+enum : uint32_t { kFull = 0, kTail = 1, kExt = 2, kWide = 3 };
+struct TileInfo {
+    uint32_t g, m, n, kind;
+};
+
+// Wide-tail schedule, per group g: for each pair of N tiles (n0, n0 + 1): the
+// full tiles of n0 (m fastest), those of n0 + 1, then the remainder tile over
+// both (its B slices were just streamed: L2-hot).  mpf[g] = full tiles per N
+// tile (count/256, + 1 for a remainder > 128), tl[g] = 1 for a remainder of
+// 1..128 rows.
+__device__ __forceinline__ TileInfo decode_wide(uint32_t tile, const uint32_t* s_pf, const uint32_t* s_tl,
+                                                uint32_t G, uint32_t NT) {
+    const uint32_t NTh = (NT + 1) / 2;
+    uint32_t lo = 0, hi = G;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_pf[mid] * NT + s_tl[mid] * NTh <= tile)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    TileInfo t;
+    t.g = lo - 1;
+    const uint32_t local = tile - (s_pf[t.g] * NT + s_tl[t.g] * NTh);
+    const uint32_t mpf = s_pf[t.g + 1] - s_pf[t.g], tl = s_tl[t.g + 1] - s_tl[t.g];
+    const uint32_t bs = 2 * mpf + tl;
+    const uint32_t np = local / bs, r = local - np * bs, n0 = 2 * np;
+    const bool two = n0 + 1 < NT;
+    if (r < mpf) {
+        t.n = n0, t.m = r, t.kind = kFull;
+    } else if (two && r < 2 * mpf) {
+        t.n = n0 + 1, t.m = r - mpf, t.kind = kFull;
+    } else {
+        t.n = n0, t.m = mpf, t.kind = two ? kWide : kTail;
+    }
+    return t;
+}
+
 template <bool SWIGLU, bool EXT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -200,6 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     constexpr uint32_t XB = EXT ? X_BYTES : 0u;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
+    __shared__ uint32_t s_tpre[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
     __shared__ uint32_t s_gmap[kMaxG];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -231,7 +275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
-        if (p.tail128) tma_prefetch_desc(&tmA64);
+        if (p.tail128 || p.wide || EXT) tma_prefetch_desc(&tmA64);
         tma_prefetch_desc(&tmB);
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot);
@@ -239,6 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     griddep_launch();
     for (uint32_t q = threadIdx.x; q <= p.G; q += blockDim.x) {
         s_prefix[q] = p.mprefix[q];
+        s_tpre[q] = p.wide ? p.tprefix[q] : 0u;
         s_off[q] = p.offsets[q];
         if (q < p.G) s_gmap[q] = p.gmap ? p.gmap[q] : q;
     }
@@ -247,8 +292,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync();  // peer barriers initialised before any remote signal
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t total = s_prefix[p.G] * p.NT;
+    const uint32_t total = s_prefix[p.G] * p.NT + s_tpre[p.G] * ((p.NT + 1) / 2);
     const uint32_t nkb = p.K / BK;
+    auto decode = [&](uint32_t tile) -> TileInfo {
+        if (p.wide) return decode_wide(tile, s_prefix, s_tpre, p.G, p.NT);
+        TileInfo t;
+        map_tile(tile, s_prefix, p.G, p.NT, t.g, t.m, t.n);
+        const uint32_t rows = s_off[t.g + 1] - s_off[t.g] - t.m * BM;
+        t.kind = (p.tail128 && rows <= HM) ? kTail : (EXT && rows > BM && rows <= BM + HM) ? kExt : kFull;
+        return t;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
@@ -260,11 +313,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
             uint32_t it = 0;
             for (uint32_t tile = pair; tile < total; tile += npairs) {
-                uint32_t g, m, n;
-                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const uint32_t rows = s_off[g + 1] - s_off[g] - m * BM;
-                const bool tail = p.tail128 && rows <= HM;  // M=128: 64 rows per CTA
-                const bool ext = EXT && rows > BM && rows <= BM + HM;  // + remainder rows 256 .. 383
+                const TileInfo ti = decode(tile);
+                const uint32_t g = ti.g, m = ti.m, n = ti.n;
+                const bool tail = ti.kind == kTail || ti.kind == kWide;  // M=128: 64 rows per CTA
+                const bool ext = EXT && ti.kind == kExt;                // + remainder rows 256 .. 383
+                const bool wide = ti.kind == kWide;
                 const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * (tail ? HM / 2 : HM));
                 const int32_t xrow = static_cast<int32_t>(s_off[g] + m * BM + BM + rank * 64);
                 const int32_t brow = static_cast<int32_t>(s_gmap[g] * p.N_group + n * BN + rank * 128);
@@ -277,6 +330,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     mbar_wait(&empty[s], ph ^ 1u);
                     if (rank == 0) mbar_expect_tx(&full[s], tx);
                     const uint32_t fb = full_leader + s * 8;
+                    if (wide) {
+                        // the second N tile's B half rides in the next ring slot
+                        // (A slot unused): the MMA consumes both slots per k-block
+                        tma_load_2d_pair(sA + s * A_BYTES, &tmA64, fb, static_cast<int32_t>(kb * BK), arow);
+                        tma_load_2d_pair(sB + s * B_BYTES, &tmB, fb, static_cast<int32_t>(kb * BK), brow);
+                        ++it;
+                        const uint32_t s2 = it % NS, ph2 = (it / NS) & 1u;
+                        mbar_wait(&empty[s2], ph2 ^ 1u);
+                        if (rank == 0) mbar_expect_tx(&full[s2], 2 * B_BYTES);
+                        tma_load_2d_pair(sB + s2 * B_BYTES, &tmB, full_leader + s2 * 8, static_cast<int32_t>(kb * BK),
+                                         brow + static_cast<int32_t>(BN));
+                        continue;
+                    }
                     if (ext) tma_load_2d_pair(sX + s * XB, &tmA64, fb, static_cast<int32_t>(kb * BK), xrow);
 #if MP_PAIR_HINTS & 2
                     tma_load_2d_pair_hint(sA + s * A_BYTES, tA, fb, static_cast<int32_t>(kb * BK), arow, pol_a);
@@ -307,11 +373,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
             for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
                 const uint32_t acc = tc & 1u;
-                uint32_t g, m, n;
-                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const uint32_t rows = s_off[g + 1] - s_off[g] - m * BM;
-                const uint32_t idesc = (p.tail128 && rows <= HM) ? idesc_tail : idesc_full;
-                const bool ext = EXT && rows > BM && rows <= BM + HM;
+                const TileInfo ti = decode(tile);
+                const uint32_t idesc = (ti.kind == kTail || ti.kind == kWide) ? idesc_tail : idesc_full;
+                const bool ext = EXT && ti.kind == kExt;
+                const bool wide = ti.kind == kWide;
 #if MP_PAIR_TRACE
                 uint64_t t0 = clock64();
 #endif
@@ -332,6 +397,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     t0 = clock64();
 #endif
                     mbar_wait(&full[s], ph);
+                    if (wide) {
+                        ++it;
+                        const uint32_t s2 = it % NS, ph2 = (it / NS) & 1u;
+                        mbar_wait(&full[s2], ph2);
+#if MP_PAIR_TRACE
+                        w_full += clock64() - t0;
+#endif
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(sA + s * A_BYTES);
+                        const uint32_t b0 = smem_u32(sB + s * B_BYTES), b1 = smem_u32(sB + s2 * B_BYTES);
+                        // two M=128 accumulators (128 TMEM columns each) in this buffer
+#pragma unroll
+                        for (uint32_t k = 0; k < BK / 16; ++k) {
+                            const uint64_t ad = umma_desc_sw128(a0 + k * 32);
+                            umma_bf16_pair(d_tmem, ad, umma_desc_sw128(b0 + k * 32), idesc_tail, (kb | k) != 0u);
+                            umma_bf16_pair(d_tmem + HM, ad, umma_desc_sw128(b1 + k * 32), idesc_tail,
+                                           (kb | k) != 0u);
+                        }
+                        umma_commit_pair(&empty[s]);
+                        umma_commit_pair(&empty[s2]);
+                        continue;
+                    }
 #if MP_PAIR_TRACE
                     w_full += clock64() - t0;
 #endif
@@ -358,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     r[0] = tile;
                     r[1] = w_full - wf0;
                     r[2] = clock64() - t_tile;
-                    r[3] = (idesc == idesc_tail ? 1u : 0u) | (ext ? 2u : 0u);
+                    r[3] = ti.kind;
                 }
 #endif
             }
@@ -381,14 +468,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // row rank*128 + q*32 + lane, all 256 D columns; half (M=128) shape:
         // lane l < 64 = row rank*64 + l with D columns [0,128), lane 64 + l =
         // the same row with D columns [128,256).
-        auto emit = [&](uint32_t buf, uint32_t row0, bool m128, uint32_t g, uint32_t n, uint32_t cnt) {
+        auto emit = [&](uint32_t buf, uint32_t col0, uint32_t row0, bool m128, uint32_t g, uint32_t n, uint32_t cnt) {
             const uint32_t row_local = row0 + (m128 ? rank * 64 + (q & 1u) * 32 + lane : rank * HM + q * 32 + lane);
             const uint32_t half = m128 ? (q >> 1) : 0;  // which 128 D columns this lane holds (M=128)
             const uint32_t nchunk = m128 ? 4 : 8;        // 32-column chunks of D held by the lane
             const bool valid = row_local < cnt;
             const bool any = (row_local - lane) < cnt;  // warp has a valid row
             __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN;
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN + col0;
             if (!any) return;
             if constexpr (SWIGLU) {
                 // D chunk pair (gate, up) = columns (h*128 + c2*32, + 64) for
@@ -456,8 +543,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint64_t e_busy = 0, e_ext = 0, e_wait = 0;
 #endif
         for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
-            uint32_t g, m, n;
-            map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+            const TileInfo ti = decode(tile);
+            const uint32_t g = ti.g, m = ti.m, n = ti.n;
             const uint32_t acc = tc & 1u;
 #if MP_PAIR_TRACE
             const uint64_t e0 = clock64();
@@ -469,17 +556,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             e_wait += e1 - e0;
 #endif
             const uint32_t cnt = s_off[g + 1] - s_off[g];
-            const uint32_t rows = cnt - m * BM;
-            if (EXT && rows > BM && rows <= BM + HM) {  // the group's last tile, merged remainder
+            if (EXT && ti.kind == kExt) {  // the group's last tile, merged remainder
                 // remainder first: the next tile's MMAs wait for that buffer
-                emit(acc ^ 1u, m * BM + BM, true, g, n, cnt);
+                emit(acc ^ 1u, 0, m * BM + BM, true, g, n, cnt);
                 release(acc ^ 1u);
             }
+            if (ti.kind == kWide) emit(acc, HM, m * BM, true, g, n + 1, cnt);  // second N tile
 #if MP_PAIR_TRACE
             const uint64_t e2 = clock64();
             e_ext += e2 - e1;
 #endif
-            emit(acc, m * BM, p.tail128 && rows <= HM, g, n, cnt);
+            emit(acc, 0, m * BM, ti.kind == kTail || ti.kind == kWide, g, n, cnt);
             release(acc);
 #if MP_PAIR_TRACE
             e_busy += clock64() - e1;
@@ -514,11 +601,11 @@ size_t gemm_pair_smem_bytes() { return kSmemBytesX > kSmemBytes ? kSmemBytesX : 
 // previous tile as an extra M=128 MMA sharing its B tile).  tmA64: 64-row A box.
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s, int variant,
-                     const uint32_t* gmap, const CUtensorMap* tmA64) {
-    if (!tmA64) variant = kPairPlain;  // tails / remainders need the 64-row A box
+                     const uint32_t* gmap, const CUtensorMap* tmA64, const uint32_t* tprefix) {
+    if (!tmA64 || (variant == kPairWide && !tprefix)) variant = kPairPlain;  // tails need the 64-row A box
     PairParams p{sh.G, sh.K, sh.N_group, sh.n_valid, sh.ld_out, (sh.N_group + BN - 1) / BN, offsets, mprefix256,
                  static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), variant == kPairTail128 ? 1u : 0u,
-                 variant == kPairExt ? 1u : 0u, gmap};
+                 variant == kPairExt ? 1u : 0u, variant == kPairWide ? 1u : 0u, tprefix, gmap};
     if (p.trace) cudaMemsetAsync(p.trace, 0, (4096 + 128 * 128 * 4) * sizeof(uint64_t), s);
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;

@@ -540,13 +540,17 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     const bool split = L->tile_mode == 5;
     (void)rows;
     const uint32_t G1 = L->G + 1;
-    const uint32_t* pre_pair = L->ws.mprefix_tc2 + (split ? G1 : ext ? 4 * G1 : 0);
-    const int variant = ext ? mp::kPairExt : L->tile_mode == 4 ? mp::kPairTail128 : mp::kPairPlain;
+    const bool wide = L->tile_mode == 7;
+    const uint32_t* pre_pair = L->ws.mprefix_tc2 + ((split || wide) ? G1 : ext ? 4 * G1 : 0);
+    const int variant = ext    ? mp::kPairExt
+                        : wide ? mp::kPairWide
+                        : L->tile_mode == 4 ? mp::kPairTail128
+                                            : mp::kPairPlain;
     const uint32_t* pre_tail = L->ws.mprefix_tc2 + 2 * G1;
     const uint32_t* tail_start = L->ws.mprefix_tc2 + 3 * G1;
     if (L->use_tc && L->tile256) {
         mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
-                            pre_pair, L->num_sms, s, variant, gmap, &L->tm_xperm64);
+                            pre_pair, L->num_sms, s, variant, gmap, &L->tm_xperm64, pre_tail);
         if (split)
             mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
                                pre_tail, L->num_sms, s, gmap, tail_start);
@@ -562,7 +566,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     tm.begin(4);
     if (L->use_tc && L->tile256) {
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
-                            pre_pair, L->num_sms, s, variant, gmap, &L->tm_h64);
+                            pre_pair, L->num_sms, s, variant, gmap, &L->tm_h64, pre_tail);
         if (split)
             mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
                                pre_tail, L->num_sms, s, gmap, tail_start);
@@ -738,6 +742,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                                : std::string(env) == "256-tail128" ? 4
                                : std::string(env) == "256-split"   ? 5
                                : std::string(env) == "256-merged"  ? 6
+                               : std::string(env) == "256-wide"    ? 7
                                                                    : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
@@ -1437,11 +1442,13 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
 // weight re-reads at k=8: profiles/ncu_summary_r01b.json) / 6 pairs with
 // merged remainders (<= 128-row remainders as an extra M=128 MMA on the
 // group's previous tile; measured slower: the remainder accumulator takes
-// the other TMEM buffer, exposing an epilogue per merged tile), for A/B
-// timing (tests/probes/tile_ab.py).
+// the other TMEM buffer, exposing an epilogue per merged tile) / 7 pairs
+// with wide tails (a <= 128-row remainder over two N tiles; measured slower:
+// the shared-memory operand traffic of two M=128 MMAs), for A/B timing
+// (tests/probes/tile_ab.py).
 MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {
-        if (!L || mode < 0 || mode > 6) fail(MP_ERR_VALIDATION, "bad argument");
+        if (!L || mode < 0 || mode > 7) fail(MP_ERR_VALIDATION, "bad argument");
         L->tile_mode = mode;
     });
 }

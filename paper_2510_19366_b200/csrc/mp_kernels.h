@@ -142,10 +142,13 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
-constexpr int kPairPlain = 0, kPairTail128 = 1, kPairExt = 2;
+constexpr int kPairPlain = 0, kPairTail128 = 1, kPairExt = 2, kPairWide = 3;
+// kPairWide: mprefix256 = the split schedule's pair-tile prefix, tprefix = its
+// <= 128-row remainder prefix (mprefix_tc2 + (G+1), + 2 (G+1))
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
-                     int variant = kPairPlain, const uint32_t* gmap = nullptr, const CUtensorMap* tmA64 = nullptr);
+                     int variant = kPairPlain, const uint32_t* gmap = nullptr, const CUtensorMap* tmA64 = nullptr,
+                     const uint32_t* tprefix = nullptr);
 
 // Calibration (calib.cu).
 void launch_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,

@@ -25,7 +25,7 @@ else:
 lib = _lib.load()
 lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
 y = torch.empty_like(xs[0])
-names = {0: "auto", 1: "128-row", 2: "pair", 3: "pair", 4: "pair-tail128", 5: "split", 6: "pair-merged"}
+names = {0: "auto", 1: "128-row", 2: "pair", 3: "pair", 4: "pair-tail128", 5: "split", 6: "pair-merged", 7: "pair-wide"}
 ks = [int(a) for a in sys.argv[1].split(",")]
 modes = [int(a) for a in sys.argv[2].split(",")]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 6

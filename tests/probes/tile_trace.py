@@ -18,7 +18,7 @@ for k in [int(a) for a in sys.argv[1].split(",")]:
         _lib.check(lib.mp_debug_gemm_trace(which, tr.ctypes.data, N))
         rec = tr[1024:].reshape(-1, 4)
         rec = rec[rec[:, 2] > 0]
-        for kind, lab in ((0, 'full '), (1, 'tail '), (2, 'ext  ')):
+        for kind, lab in ((0, 'full '), (1, 'tail '), (2, 'ext  '), (3, 'wide ')):
             r = rec[rec[:, 3] == kind]
             if len(r):
                 print(f"k={k} {name} {lab}: tiles {len(r)}  MMA-phase cycles mean {r[:, 2].mean():.0f} "

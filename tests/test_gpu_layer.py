@@ -501,9 +501,10 @@ def test_forward_is_cuda_graph_capturable(oracle, torch_cuda):
 @pytest.mark.parametrize("k", [4, 8])
 def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
     """Every GEMM schedule (1-SM 128-row tiles, CTA pairs plain / merged
-    remainders / M=128 tails / split tails) gives the same layer output: the
-    merged schedule's extended tiles (257..384 rows: an M=256 and an M=128 MMA
-    sharing one B tile) are exercised at these bucket sizes."""
+    remainders / M=128 tails / split tails / wide tails) gives the same layer
+    output: the merged schedule's extended tiles (257..384 rows: an M=256 and
+    an M=128 MMA sharing one B tile) and the wide tails (a <= 128-row
+    remainder over two N tiles) are exercised at these bucket sizes."""
     import ctypes as C
     torch = torch_cuda
     from paper_2510_19366_b200 import _lib
@@ -512,7 +513,7 @@ def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
     lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
     outs = {}
     try:
-        for mode in (3, 1, 6, 4, 5):  # 256-plain, 128, 256-merged, 256-tail128, 256-split
+        for mode in (3, 1, 6, 4, 5, 7):  # 256-plain, 128, 256-merged, 256-tail128, 256-split, 256-wide
             _lib.check(lib.mp_debug_set_tile_mode(L.h, mode))
             y, sel, w, off = L.forward(x_dev, k=k, return_routing=True)
             torch.cuda.synchronize()
