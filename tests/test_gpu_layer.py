@@ -526,3 +526,14 @@ def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
     for mode, y in outs.items():
         ok = bf16_ok(y, ref)
         assert ok.all(), f"mode {mode}: {(~ok).sum()} elements off"
+
+
+def test_zero_tokens(oracle, torch_cuda, mixtral):
+    """An empty batch is a no-op: (0, d) output, no error, no launches."""
+    torch = torch_cuda
+    L, x_dev, *_ = mixtral
+    n0 = L.launch_count()
+    y = L.forward(x_dev[:0], k=8)
+    torch.cuda.synchronize()
+    assert tuple(y.shape) == (0, x_dev.shape[1])
+    assert L.launch_count() == n0

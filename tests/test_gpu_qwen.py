@@ -76,13 +76,14 @@ def _oracle_experts(oracle):
     return _EXPERTS
 
 
-@pytest.mark.parametrize("k", [4, 8, 16])
-def test_qwen_decode_batch_vs_oracle(oracle, qwen, k):
-    """T=64 decode batch: routing bit-exact, bucket offsets bit-exact, every
-    token's output (routed + shared) against the oracle on bf16-rounded inputs."""
+@pytest.mark.parametrize("k,T", [(4, 64), (8, 64), (16, 64), (8, 1), (8, 3), (16, 129)])
+def test_qwen_decode_batch_vs_oracle(oracle, qwen, k, T):
+    """Decode batches (64 tokens, and ragged 1 / 3 / 129 crossing the 2-token
+    routing CTAs and the 128-token router tiles): routing bit-exact, bucket
+    offsets bit-exact, every token's output (routed + shared) against the
+    oracle on bf16-rounded inputs."""
     import torch
     L, parts, wr, gate = qwen
-    T = 64
     x = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
     from paper_2510_19366_b200 import synth_fill
     synth_fill(x, 19, 1.0)
