@@ -30,6 +30,15 @@
 // step is 4% slower with them (profiles/r01_tile_ab.txt), so tails run as
 // full 256-row tiles.
 //
+// Two more opt-in remainder schedules (tile decoder below): EXT merges a
+// <= 128-row remainder into the group's previous tile as an extra M=128 MMA on
+// the same B stage (257..384-row tiles, 5 x 40 KB stages, the remainder
+// accumulator in the other TMEM buffer); WIDE runs a <= 128-row remainder over
+// two N tiles at once (two M=128 MMAs sharing the A stage, the second B half
+// in the next ring slot).  Both re-read an operand from shared memory, which
+// bounds these kernels (operand reads + TMA writes ~128 B/cycle per SM at the
+// full tile's MMA rate), and measured slower per step.
+//
 // Barriers: full[s] lives in the leader CTA (both CTAs' TMA loads complete_tx
 // on it; the leader's expect_tx covers both); empty[s], tfull[a] are signalled
 // in both CTAs by a multicast tcgen05.commit; tempty[a] lives in the leader and
