@@ -24,6 +24,8 @@ def test_random_layer_config(oracle, cuda_lib, seed):
     rng = np.random.default_rng(7000 + seed)
     E = int(rng.integers(1, 9))
     S = int(rng.integers(1, 9))
+    if seed % 7 == 3:  # > 128 sub-experts: the router's column split, the 8-chunk top-k
+        E, S = int(rng.integers(33, 65)), 4
     d = int(rng.choice([40, 64, 96, 136, 200, 256, 312]))
     ff = int(rng.integers(S, 300))
     T = int(rng.integers(1, 1500 if seed % 5 == 0 else 300))  # crosses the 2 / 8 / 32-token routing CTAs
