@@ -112,13 +112,20 @@ class CudaEpOps:
 class ExpertParallelLayer:
     """A MoE-Prism layer sharded expert-parallel over the process group."""
 
-    def __init__(self, ops, group=None):
+    def __init__(self, ops, group=None, force_collectives=False):
         self.ops = ops
         self.group = group
+        # run the NCCL collectives even in a 1-rank group (tests the exchange
+        # path on one GPU); otherwise a 1-rank group short-cuts to copies
+        self.force = force_collectives
+
+    def _collective(self):
+        dist = _dist()
+        return dist.is_initialized() and (self.force or dist.get_world_size(self.group) > 1)
 
     def _a2a(self, out, inp, out_splits, in_splits):
         dist = _dist()
-        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+        if self._collective():
             dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits,
                                    group=self.group)
         else:
@@ -129,7 +136,7 @@ class ExpertParallelLayer:
         import torch
         dist = _dist()
         send = torch.tensor(counts, dtype=torch.int64, device=device)
-        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+        if self._collective():
             recv = torch.empty_like(send)
             dist.all_to_all_single(recv, send, group=self.group)
             return [int(v) for v in recv.tolist()]

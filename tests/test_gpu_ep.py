@@ -97,3 +97,36 @@ def test_ep_world2_emulated(oracle, cuda_lib, E):
         assert bf16_ok(y.float().cpu().numpy(), y_ref.float().cpu().numpy()).all()
     for ops in ranks:
         ops.close()
+
+
+def test_ep_nccl_collectives_world1(oracle, cuda_lib):
+    """The NCCL exchange path itself (all_to_all_single of counts, bf16 rows,
+    int32 metadata and the partials) in a 1-rank NCCL process group: equal to
+    the single layer bit for bit, like the copy loopback."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2510_19366_b200 import MoeLayer
+    from paper_2510_19366_b200.ep import ExpertParallelLayer
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        experts, parts, wr = _setup(oracle)
+        x = torch.from_numpy(oracle.uniform_pm1(6, T * D).reshape(T, D)).cuda().to(torch.bfloat16)
+        ref = MoeLayer(E, S, D, FF, dtype="bf16", k_max=K_MAX, max_tokens=T)
+        for e in range(E):
+            ref.set_partition(e, parts[e])
+            ref.load_expert(e, *experts[e])
+        ref.set_router(wr)
+        y_ref = ref.forward(x, k=4)
+        layer = ExpertParallelLayer(_ops(1, 0, experts, parts, wr), force_collectives=True)
+        y = layer.forward(x, k=4)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_ref)
+    finally:
+        dist.destroy_process_group()
