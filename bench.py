@@ -95,7 +95,10 @@ class ClockSampler:
                                    default=None)}
 
 
-def dist_setup(n_gpus):
+def dist_setup(n_gpus, force=False):
+    """force: a 1-rank NCCL process group even without torchrun (exercises the
+    multi-rank code path -- barriers, max over ranks, the NCCL exchange -- on
+    one GPU)."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -104,19 +107,33 @@ def dist_setup(n_gpus):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif force:
+        import socket
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
 
 
+def _dist_on():
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized()
+
+
 def barrier(world):
-    if world > 1:
+    if _dist_on():
         import torch.distributed as dist
         dist.barrier()
 
 
 def max_over_ranks(v, world):
-    if world == 1:
+    if not _dist_on():
         return v
     import torch
     import torch.distributed as dist
@@ -150,7 +167,7 @@ def build_layer(local, T, k_max):
     return L, xs
 
 
-def build_ep_layer(local, rank, world, T, k_max=16, transport="nccl"):
+def build_ep_layer(local, rank, world, T, k_max=16, transport="nccl", force_collectives=False):
     """Expert-parallel layer: E/world parent experts on this rank,
     the router replicated, tokens exchanged by NCCL all-to-all."""
     import torch
@@ -181,7 +198,7 @@ def build_ep_layer(local, rank, world, T, k_max=16, transport="nccl"):
     if transport == "p2p":
         from paper_2510_19366_b200.ep import PeerExpertParallelLayer
         return PeerExpertParallelLayer(ops), ops, xs
-    return ExpertParallelLayer(ops), ops, xs
+    return ExpertParallelLayer(ops, force_collectives=force_collectives), ops, xs
 
 
 def balanced_partition(n, n_sub, seed):
@@ -607,6 +624,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-ep", action="store_true", help="run the expert-parallel path even at N=1 (loopback)")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="N=1 with a 1-rank NCCL process group and the expert-parallel path through real NCCL "
+                         "collectives (the multi-rank code path on one GPU)")
     ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "p2p"],
                     help="N>1 token exchange: NCCL all-to-all, or direct peer-memory stores (CUDA IPC / NVLink)")
     ap.add_argument("--no-extras", action="store_true",
@@ -615,10 +635,12 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
-    world, rank, local = dist_setup(args.gpus)
+    if args.force_dist:
+        args.force_ep = True
+    world, rank, local = dist_setup(args.gpus, force=args.force_dist)
     if args.impl == "reference":
         run_reference_arm(args, world, rank)
-        if world > 1:
+        if _dist_on():
             import torch.distributed as dist
             dist.destroy_process_group()
         return
@@ -638,7 +660,8 @@ def main():
         def fwd(x, k, kpt, y=None):
             return L.forward(x, k=k, k_per_token=kpt, y=y)
     else:
-        ep_layer, ops, xs = build_ep_layer(local, rank, world, T, transport=args.ep_transport)
+        ep_layer, ops, xs = build_ep_layer(local, rank, world, T, transport=args.ep_transport,
+                                           force_collectives=args.force_dist)
         layers = [ops.router, ops.local]
 
         def fwd(x, k, kpt, y=None):
@@ -764,7 +787,7 @@ def main():
         print(json.dumps(line), flush=True)
     for x in layers:
         x.close()
-    if world > 1:
+    if _dist_on():
         import torch.distributed as dist
         dist.destroy_process_group()
 
