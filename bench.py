@@ -527,6 +527,37 @@ def kernel_roofline(stage_ms_per_step, T, k, pk, touched_groups):
             "peak_source": pk["source"]}
 
 
+def stage_rooflines(stage_ms, T, k, pk):
+    """Every stage against its bound (SURVEY 8(d) per-kernel bytes): router,
+    dispatch and combine in HBM GB/s of algorithmic bytes, the two GEMMs in
+    TFLOP/s -- the north_star's "tensor-pipe utilisation for the GEMMs and
+    achieved HBM GB/s for routing, permute and combine, each against peak".
+    Stage times are CUDA-event times per step on the forward's stream."""
+    G = E * S
+    b = 2.0  # bf16
+    algo = {
+        "router": ("hbm", T * D * b + 4.0 * D * G + 8.0 * T * k),   # x in, W_r, sel/w out
+        "dispatch": ("hbm", T * D * b + T * k * D * b),             # x in, k bucket rows out
+        "combine": ("hbm", T * k * D * b + 4.0 * T * k + T * D * b),  # partials + weights in, y out
+        "gemm1": ("tensor", 4.0 * D * W_SUB * T * k),
+        "gemm2": ("tensor", 2.0 * D * W_SUB * T * k),
+    }
+    out = {}
+    for name, (bound, work) in algo.items():
+        ms = stage_ms.get(name)
+        if not ms:
+            continue
+        if bound == "hbm":
+            ach = work / (ms * 1e-3) / 1e9
+            out[name] = {"bound": "hbm", "ms": ms, "algorithmic_bytes": work, "achieved": ach, "unit": "GB/s",
+                         "frac": ach / pk["hbm_gbs"]}
+        else:
+            ach = work / (ms * 1e-3) / 1e12
+            out[name] = {"bound": "tensor", "ms": ms, "algorithmic_flops": work, "achieved": ach,
+                         "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"]}
+    return out
+
+
 def cpu_reference_sample(k, T_sample, nthreads, seed_tokens=11):
     """The reference CPU path (oracle/_ref = reference headers compiled
     verbatim): router restated in double + select_topk_subexperts +
@@ -780,6 +811,8 @@ def main():
                 "layer_roofline": layer_roofline(T, args.k, ms, pk, touched),
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
                 "stages_ms": stages_main, "sweep": sweep_out}
+        if not use_ep:
+            line["stage_roofline"] = stage_rooflines(stages_main, T, args.k, pk)
         if other:
             line["other_configs"] = other
         if main_k:
