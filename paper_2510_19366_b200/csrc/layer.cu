@@ -621,7 +621,11 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             mp::launch_router_tc(&tmX, &L->tm_wplanes, pl, T, L->r_partial, s);
             L->r_last_ks = pl.ks;
             L->r_last_T = T;
-            if (fuse_bucket && L->has_experts && (L->d % 4) == 0) {
+            static const bool fuse_env = [] {  // MOEPRISM_FUSE_BUCKET=0: separate top-k / fixup / bucketing (A/B)
+                const char* e = std::getenv("MOEPRISM_FUSE_BUCKET");
+                return !(e && e[0] == '0');
+            }();
+            if (fuse_bucket && fuse_env && L->has_experts && (L->d % 4) == 0) {
                 // routing epilogue + exact near-tie re-selection + bucketing in one kernel;
                 // many K splits (small batches): reduce them first across (token, g) warps
                 uint32_t ks = pl.ks;
