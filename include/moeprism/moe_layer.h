@@ -59,6 +59,7 @@ extern "C" {
 #define MP_WEIGHT_SOFTMAX_RENORM 1 /* y = sum p_g / sum_sel p * o_g */
 
 #define MP_SEL_NONE 0xFFFFFFFFu /* padding in [T x k_max] selection arrays */
+#define MP_MAX_SUBEXPERTS 256u  /* max E*S sub-experts of one layer (Qwen: 240) */
 
 typedef int mp_status;
 typedef struct mp_layer_s* mp_layer_t;
@@ -171,6 +172,14 @@ mp_status mp_layer_forward_selected_host(mp_layer_t h, const void* x, uint32_t n
 /* Router only: selection + weights (device outputs, T x k_max). */
 mp_status mp_layer_route(mp_layer_t h, const void* x, uint32_t n_tokens, const uint32_t* k_per_token, uint32_t k,
                          uint32_t* sel_out, float* w_out, void* stream);
+
+/* Routing statistics of the last mp_layer_forward / mp_layer_route on this
+ * handle (synchronises `stream`): reselected = tokens whose tensor-core
+ * selection was not certified by the per-token error bound (or that may be a
+ * near tie) and were re-selected from exact fp64 logits; near_ties = tokens
+ * whose exact k-th/(k+1)-th logit gap is < 1e-6 (the routing contract's
+ * near-tie window, reported separately).  Either pointer may be NULL. */
+mp_status mp_layer_route_stats(mp_layer_t h, uint32_t* reselected, uint32_t* near_ties, void* stream);
 
 /* Device-side validation flags raised by forwards on device buffers (k out of
  * range, duplicate / out-of-range selection, non-finite input): synchronises

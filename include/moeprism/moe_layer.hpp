@@ -2,13 +2,27 @@
 // in the reference's style (value types, std::span inputs, ValidationError /
 // IoError exceptions; inc/error.hpp:8-16), over the C-ABI in moe_layer.h.
 //
-//   moeprism::MoeLayer           the layer: weights / partitions / router or
-//                                gates loaded from the offline engine's
-//                                artefacts, forward(tokens, k) -> hidden.
-//   moeprism::moe_forward        free-function form of MoeLayer::forward.
-//   moeprism::partitioned_forward  drop-in for inc/expert.hpp:101-135 with the
-//                                reference's exact signature and validation
-//                                verdicts, computed on the GPU.
+//   moeprism::b200::MoeLayer      the layer: weights / partitions / router or
+//                                 gates loaded from the offline engine's
+//                                 artefacts, forward(tokens, k) -> hidden.
+//   moeprism::b200::moe_forward   free-function form of MoeLayer::forward.
+//   moeprism::b200::partitioned_forward
+//                                 drop-in for inc/expert.hpp:101-135 with the
+//                                 reference's exact signature and validation
+//                                 verdicts, computed on the GPU.
+//
+// Coexistence with the reference headers (proj/include/moeprism/*.hpp):
+//   * when they are on the include path (detected by <moeprism/partition.hpp>,
+//     or forced with -DMOEPRISM_WITH_REFERENCE_HEADERS), this header includes
+//     them and uses their ToyExpert / Partition / GateSet / validate /
+//     ValidationError / IoError -- one set of value types, no redefinitions;
+//   * otherwise it defines the same types itself, field for field, and
+//     exports the b200 API into namespace moeprism (moeprism::MoeLayer,
+//     moeprism::partitioned_forward, ...);
+//   * include/moeprism/dropin/moeprism/expert.hpp shadows the reference's
+//     expert.hpp so that code written against the reference (its own test
+//     suites: tests/cpp/ref_expert_suite.cpp) calls the GPU partitioned_forward
+//     unchanged.
 // Header-only; link libmoeprism_b200.so.  No CPU fallback: compute calls
 // throw std::runtime_error (status 3) when no sm_100a device is usable.
 #pragma once
@@ -27,10 +41,20 @@
 
 #include "moeprism/moe_layer.h"
 
+#if !defined(MOEPRISM_WITH_REFERENCE_HEADERS) && defined(__has_include)
+#if __has_include(<moeprism/partition.hpp>)
+#define MOEPRISM_WITH_REFERENCE_HEADERS 1
+#endif
+#endif
+
+#ifdef MOEPRISM_WITH_REFERENCE_HEADERS
+#include <moeprism/error.hpp>
+#include <moeprism/expert.hpp>
+#include <moeprism/gating.hpp>
+#include <moeprism/partition.hpp>
+#else
 namespace moeprism {
 
-#ifndef MOEPRISM_ERROR_TYPES_DEFINED
-#define MOEPRISM_ERROR_TYPES_DEFINED
 // Same taxonomy as the reference (inc/error.hpp:9-16).
 struct ValidationError : std::runtime_error {
     explicit ValidationError(const std::string& what) : std::runtime_error(what) {}
@@ -38,7 +62,6 @@ struct ValidationError : std::runtime_error {
 struct IoError : std::runtime_error {
     explicit IoError(const std::string& what) : std::runtime_error(what) {}
 };
-#endif
 
 // The reference's value types (inc/expert.hpp:17-23, inc/partition.hpp:15-20,
 // inc/gating.hpp:19-23), field for field.
@@ -61,6 +84,36 @@ struct GateSet {
     std::uint32_t r = 0;
     std::vector<std::vector<std::uint32_t>> gate_neurons;
 };
+
+// validate(ToyExpert), inc/expert.hpp:25-39 -- same verdicts and messages.
+inline void validate(const ToyExpert& e) {
+    if (e.d_model < 1 || e.d_ff < 1) throw ValidationError("toy expert needs d_model >= 1 and d_ff >= 1");
+    if (e.w_gate.size() != e.d_model * e.d_ff || e.w_up.size() != e.d_model * e.d_ff ||
+        e.w_down.size() != e.d_ff * e.d_model)
+        throw ValidationError("toy expert weight shapes do not match d_model=" + std::to_string(e.d_model) +
+                              ", d_ff=" + std::to_string(e.d_ff));
+    for (const auto* w : {&e.w_gate, &e.w_up, &e.w_down})
+        for (float v : *w)
+            if (!std::isfinite(v)) throw ValidationError("toy expert weight is not finite");
+}
+
+// validate(Partition), inc/partition.hpp:34-46 (the library's own checker).
+inline void validate(const Partition& p) {
+    const mp_status rc = mp_validate_partition(p.n_subexperts, p.assignment.data(), p.assignment.size());
+    if (rc == MP_ERR_VALIDATION) throw ValidationError(mp_last_error());
+    if (rc != MP_OK) throw std::runtime_error(mp_last_error());
+}
+
+}  // namespace moeprism
+#endif
+
+namespace moeprism::b200 {
+
+using ::moeprism::GateSet;
+using ::moeprism::IoError;
+using ::moeprism::Partition;
+using ::moeprism::ToyExpert;
+using ::moeprism::ValidationError;
 
 enum class Dtype : std::uint32_t { f32 = MP_DTYPE_F32, bf16 = MP_DTYPE_BF16 };
 enum class RouterMode : std::uint32_t { linear = MP_ROUTER_LINEAR, proxy = MP_ROUTER_PROXY };
@@ -104,23 +157,6 @@ inline float from_bf16(std::uint16_t h) {
 }
 
 }  // namespace detail
-
-// validate(ToyExpert), inc/expert.hpp:25-39 -- same verdicts and messages.
-inline void validate(const ToyExpert& e) {
-    if (e.d_model < 1 || e.d_ff < 1) throw ValidationError("toy expert needs d_model >= 1 and d_ff >= 1");
-    if (e.w_gate.size() != e.d_model * e.d_ff || e.w_up.size() != e.d_model * e.d_ff ||
-        e.w_down.size() != e.d_ff * e.d_model)
-        throw ValidationError("toy expert weight shapes do not match d_model=" + std::to_string(e.d_model) +
-                              ", d_ff=" + std::to_string(e.d_ff));
-    for (const auto* w : {&e.w_gate, &e.w_up, &e.w_down})
-        for (float v : *w)
-            if (!std::isfinite(v)) throw ValidationError("toy expert weight is not finite");
-}
-
-// validate(Partition), inc/partition.hpp:34-46.
-inline void validate(const Partition& p) {
-    detail::check(mp_validate_partition(p.n_subexperts, p.assignment.data(), p.assignment.size()));
-}
 
 class MoeLayer {
 public:
@@ -250,10 +286,14 @@ inline std::vector<float> moe_forward(const MoeLayer& layer, std::span<const flo
 }
 
 // Drop-in for partitioned_forward (inc/expert.hpp:101-135): same signature,
-// same ValidationError verdicts, unweighted sum over the active sub-experts,
-// computed by the fp32 (fp64-accumulating) GPU path -- within 1e-5 * (1 + |y|)
-// of the reference.  One single-expert layer per call (weights uploaded and
-// packed each time): a compatibility entry point, not the serving path.
+// same ValidationError verdicts in the same order, unweighted sum over the
+// active sub-experts, computed by the fp32 (fp64-accumulating) GPU path --
+// within 1e-5 * (1 + |y|) of the reference.  One single-expert layer per call
+// (weights uploaded and packed each time): a compatibility entry point, not
+// the serving path.  Any reference-valid partition is accepted: up to
+// MP_MAX_SUBEXPERTS sub-experts the layer holds the partition itself; beyond
+// that the active neurons (ascending, the reference's summation order) are
+// gathered into one sub-expert of a one-expert layer.
 inline std::vector<float> partitioned_forward(const ToyExpert& e, const Partition& p, std::span<const float> x,
                                               std::span<const std::uint32_t> active) {
     validate(e);
@@ -277,21 +317,60 @@ inline std::vector<float> partitioned_forward(const ToyExpert& e, const Partitio
     if (active.empty()) return std::vector<float>(e.d_model, 0.0f);
     LayerConfig c;
     c.n_experts = 1;
-    c.n_subexperts = p.n_subexperts;
     c.d_model = static_cast<std::uint32_t>(e.d_model);
-    c.d_ff = static_cast<std::uint32_t>(e.d_ff);
     c.dtype = Dtype::f32;
     c.weights = WeightMode::unit;
-    c.k_max = p.n_subexperts;
     c.max_tokens = 1;
+    if (p.n_subexperts <= MP_MAX_SUBEXPERTS) {
+        c.n_subexperts = p.n_subexperts;
+        c.d_ff = static_cast<std::uint32_t>(e.d_ff);
+        c.k_max = static_cast<std::uint32_t>(active.size());
+        MoeLayer layer(c);
+        layer.set_partition(0, p);
+        layer.load_expert(0, e);
+        std::vector<std::uint32_t> sel(active.begin(), active.end());
+        std::sort(sel.begin(), sel.end());
+        return layer.forward_selected(x, sel);
+    }
+    ToyExpert g;  // the active neurons in ascending order
+    g.d_model = e.d_model;
+    for (std::size_t j = 0; j < e.d_ff; ++j) g.d_ff += is_active[p.assignment[j]];
+    g.w_gate.resize(g.d_model * g.d_ff);
+    g.w_up.resize(g.d_model * g.d_ff);
+    g.w_down.reserve(g.d_ff * g.d_model);
+    for (std::size_t j = 0, q = 0; j < e.d_ff; ++j) {
+        if (!is_active[p.assignment[j]]) continue;
+        for (std::size_t i = 0; i < e.d_model; ++i) {
+            g.w_gate[i * g.d_ff + q] = e.w_gate[i * e.d_ff + j];
+            g.w_up[i * g.d_ff + q] = e.w_up[i * e.d_ff + j];
+        }
+        g.w_down.insert(g.w_down.end(), e.w_down.begin() + j * e.d_model, e.w_down.begin() + (j + 1) * e.d_model);
+        ++q;
+    }
+    c.n_subexperts = 1;
+    c.d_ff = static_cast<std::uint32_t>(g.d_ff);
+    c.k_max = 1;
     MoeLayer layer(c);
-    layer.set_partition(0, p);
-    layer.load_expert(0, e);
-    std::vector<std::uint32_t> sel(p.n_subexperts, MP_SEL_NONE);
-    std::vector<std::uint32_t> asc(active.begin(), active.end());
-    std::sort(asc.begin(), asc.end());
-    std::copy(asc.begin(), asc.end(), sel.begin());
+    Partition one;
+    one.n_subexperts = 1;
+    one.assignment.assign(g.d_ff, 0u);
+    layer.set_partition(0, one);
+    layer.load_expert(0, g);
+    const std::vector<std::uint32_t> sel{0u};
     return layer.forward_selected(x, sel);
 }
 
+}  // namespace moeprism::b200
+
+#ifndef MOEPRISM_WITH_REFERENCE_HEADERS
+// Without the reference headers the GPU API is the moeprism API.
+namespace moeprism {
+using b200::Dtype;
+using b200::LayerConfig;
+using b200::moe_forward;
+using b200::MoeLayer;
+using b200::partitioned_forward;
+using b200::RouterMode;
+using b200::WeightMode;
 }  // namespace moeprism
+#endif

@@ -36,6 +36,7 @@ EXPORTS = (
     "mp_layer_stage_times", "mp_layer_reset_stage_times", "mp_layer_launch_count", "mp_synth_fill",
     "mp_format_read_mpex", "mp_format_read_partition_doc", "mp_validate_partition", "mp_layer_forward_selected_host",
     "mp_ep_create", "mp_ep_create_subexpert", "mp_ep_destroy", "mp_ep_plan", "mp_ep_pack", "mp_ep_combine",
+    "mp_layer_route_stats",
 )
 
 
@@ -93,6 +94,7 @@ def _sig(L):
     L.mp_layer_forward_selected.argtypes = [vp, vp, u32, vp, vp, vp, vp, vp]
     L.mp_layer_route.argtypes = [vp, vp, u32, vp, u32, vp, vp, vp]
     L.mp_layer_check_errors.argtypes = [vp, vp]
+    L.mp_layer_route_stats.argtypes = [vp, C.POINTER(u32), C.POINTER(u32), vp]
     L.mp_layer_set_profiling.argtypes = [vp, C.c_int]
     L.mp_layer_stage_times.argtypes = [vp, C.c_char_p, sz, vp, vp, C.POINTER(u32), u32]
     L.mp_layer_reset_stage_times.argtypes = [vp]

@@ -236,7 +236,7 @@ MP_API mp_status mp_ep_create_subexpert(uint32_t world, uint32_t rank, uint32_t 
     return ep_guarded([&] {
         if (!out) ep_fail(MP_ERR_VALIDATION, "null argument");
         if (world < 1 || world > 32 || rank >= world) ep_fail(MP_ERR_VALIDATION, "bad world / rank");
-        if (per_rank < 1 || S < 1 || d < 1 || k_max < 1 || k_max > 64 || max_tokens < 1)
+        if (per_rank < 1 || S < 1 || d < 1 || k_max < 1 || k_max > 256 || max_tokens < 1)
             ep_fail(MP_ERR_VALIDATION, "bad expert-parallel shape");
         if (dtype != MP_DTYPE_F32 && dtype != MP_DTYPE_BF16) ep_fail(MP_ERR_VALIDATION, "unknown dtype");
         ep_ck(cudaSetDevice(device), "cudaSetDevice");

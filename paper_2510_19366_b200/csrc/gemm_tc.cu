@@ -452,14 +452,10 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
-    static bool attr_set = false;  // once per process (device-independent attribute)
-    if (!attr_set) {
-        cudaFuncSetAttribute(gemm_tc_kernel<kEpiPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_tc_kernel<kEpiSwiglu>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_tc_kernel<kEpiActAbs>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_tc_kernel<kEpiCount>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        attr_set = true;
-    }
+    func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiPlain>), (int)kSmemBytes);
+    func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiSwiglu>), (int)kSmemBytes);
+    func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiActAbs>), (int)kSmemBytes);
+    func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiCount>), (int)kSmemBytes);
     switch (epi) {
         case kEpiSwiglu: launch_k(gemm_tc_kernel<kEpiSwiglu>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
         case kEpiActAbs: launch_k(gemm_tc_kernel<kEpiActAbs>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;

@@ -620,14 +620,10 @@ void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB
     uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;
     if (max_tiles < pairs) pairs = max_tiles;
     if (pairs == 0) pairs = 1;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(gemm_pair_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_pair_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        cudaFuncSetAttribute(gemm_pair_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesX);
-        cudaFuncSetAttribute(gemm_pair_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesX);
-        attr_set = true;
-    }
+    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<true, false>), (int)kSmemBytes);
+    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<false, false>), (int)kSmemBytes);
+    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<true, true>), (int)kSmemBytesX);
+    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<false, true>), (int)kSmemBytesX);
     const CUtensorMap& a64 = tmA64 ? *tmA64 : *tmA;
     const dim3 grid(2 * pairs), block(kThreads);
     if (p.ext) {

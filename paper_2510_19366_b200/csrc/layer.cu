@@ -18,7 +18,26 @@
 
 #define MP_API extern "C" __attribute__((visibility("default")))
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace mp {
+// Function attributes belong to the current device's context: set them once
+// per (kernel, device), under a lock (handles may live on several devices and
+// be driven from several threads).
+void func_attr_once(const void* func, int max_dyn_smem, bool max_carveout) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done.insert({func, dev}).second) return;
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem);
+    if (max_carveout)
+        cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
 bool pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("MOEPRISM_PDL");
@@ -92,12 +111,6 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-// Error bound used to certify tensor-core router selections (measured max
-// |logit - fp64| is ~1e-7 at d=4096 with 256-deep chunks; 4e-6 leaves a wide
-// margin).  Tokens whose k-th/(k+1)-th gap is < 2 * guard are re-selected from
-// exact fp64 logits.
-constexpr double kRouterGuard = 4e-6;
-
 const char* kStageNames[] = {"router", "bucket", "dispatch", "gemm1", "gemm2", "combine"};
 constexpr int kStages = 6;
 
@@ -131,6 +144,17 @@ struct mp_layer_s {
     uint32_t n_gate_rows = 0;
     bool gates_packed = false;
     double* scores = nullptr;  // [max_tokens][G]
+    // tensor-core proxy path (bf16, d % 8 == 0): [gate; up] rows of the gate
+    // neurons as three bf16 planes through router_tc, certified like the linear
+    // router (proxy.cu); otherwise the exact fp64 path
+    bool proxy_tc = false;
+    uint32_t p_npad = 0;
+    void* p_planes = nullptr;
+    float* p_partial = nullptr;   // fp32 [ks][T][p_npad]
+    double* p_xnorm = nullptr;    // [ks][T]
+    double* p_win = nullptr;      // [max_tokens][3]
+    float p_wmax = 0.0f;
+    CUtensorMap tm_pplanes{};
 
     void* W1 = nullptr;
     void* W2 = nullptr;
@@ -140,9 +164,17 @@ struct mp_layer_s {
     uint32_t r_npad = 0, r_last_ks = 0, r_last_T = 0;
     void* wr_planes = nullptr;
     double* r_partial = nullptr;
-    uint32_t* r_flagged = nullptr;  // [1 + max_tokens]: count, then tokens re-selected in fp64
+    // routing statistics of the last forward: [0] tokens re-selected from exact
+    // fp64 logits, [1] near ties (exact k-th/(k+1)-th gap < 1e-6), then the
+    // re-selected tokens of the non-fused path
+    uint32_t* r_flagged = nullptr;  // [2 + max_tokens]
     uint32_t* r_ticket = nullptr;   // last-CTA ticket of the fused routing epilogue (left 0)
-    double r_guard = kRouterGuard;  // MOEPRISM_ROUTER_GUARD overrides (tests widen it)
+    // Certification of the tensor-core logits (router_tc.cu): per token
+    // guard_t = depth 2^-23 max|W_r| sum|x_t| + 2^-23 max|logit_t|; tokens whose
+    // k-th/(k+1)-th gap is < 2 guard_t are re-selected from exact fp64 logits.
+    double* r_xnorm = nullptr;      // [ks][max_tokens] per-K-split sums of |x|
+    float r_wmax = 0.0f;            // max |W_r|
+    double r_guard_floor = 0.0;     // MOEPRISM_ROUTER_GUARD: extra absolute width (tests widen the window)
     CUtensorMap tm_wplanes{};
     int32_t* d_nmap = nullptr;
     int32_t* nmap_all = nullptr;  // [E][S*w_pad] packed neuron -> original neuron (-1 padding), calibration
@@ -221,7 +253,7 @@ namespace {
 void free_layer(mp_layer_s* L) {
     for (float* p : L->raw)
         if (p) cudaFree(p);
-    void* ptrs[] = {L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_flagged, L->r_ticket, L->d_nmap, L->nmap_all, L->sel,
+    void* ptrs[] = {L->p_planes, L->p_partial, L->p_xnorm, L->p_win, L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_xnorm, L->r_flagged, L->r_ticket, L->d_nmap, L->nmap_all, L->sel,
                     L->wsel, L->kpt_dev, L->ws.lrank, L->ws.block_counts, L->ws.block_base, L->ws.offsets,
                     L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.mprefix_tc2, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
                     L->x_perm, L->h, L->o, L->x_stage, L->y_stage, L->W1s, L->W2s, L->sh_gate, L->sh_h,
@@ -321,6 +353,38 @@ void pack_gates(mp_layer_s* L) {
         ck(cudaDeviceSynchronize(), "pack gates");
     }
     cudaFree(d_neur);
+    // tensor-core path: planes of [gate rows; up rows], partial buffers, max |W|
+    for (void* p : {L->p_planes, static_cast<void*>(L->p_partial), static_cast<void*>(L->p_xnorm),
+                    static_cast<void*>(L->p_win)})
+        if (p) cudaFree(p);
+    L->p_planes = nullptr;
+    L->p_partial = nullptr;
+    L->p_xnorm = nullptr;
+    L->p_win = nullptr;
+    uint32_t max_list = 0;
+    for (uint32_t g = 0; g < L->G; ++g) max_list = std::max(max_list, off[g + 1] - off[g]);
+    L->proxy_tc = L->dtype == MP_DTYPE_BF16 && (L->d % 8) == 0 && L->n_gate_rows <= 1024 && max_list <= 1024;
+    if (const char* env = std::getenv("MOEPRISM_ROUTER"))
+        if (std::string(env) == "simt") L->proxy_tc = false;  // diagnostics only
+    if (L->proxy_tc) {
+        const uint32_t nr2 = 2 * L->n_gate_rows;
+        L->p_npad = round_up(nr2, 32);
+        L->p_planes = dalloc<char>((size_t)3 * L->p_npad * L->d * 2, "proxy planes");
+        mp::launch_split_rows(L->gate_rows, L->up_rows, L->n_gate_rows, L->n_gate_rows, L->d, L->p_npad, L->p_planes, 0);
+        const size_t rows = mp::router_tc_partial_rows(L->max_tokens, L->d, nr2, L->num_sms);
+        L->p_partial = dalloc<float>(rows * L->p_npad, "proxy partials");
+        L->p_xnorm = dalloc<double>(rows, "proxy |x| sums");
+        L->p_win = dalloc<double>((size_t)L->max_tokens * 3, "proxy windows");
+        ck(cudaMemset(L->ws.err + 1, 0, sizeof(int)), "memset");
+        mp::launch_absmax(L->gate_rows, (size_t)L->n_gate_rows * L->d, reinterpret_cast<float*>(L->ws.err + 1), 0);
+        mp::launch_absmax(L->up_rows, (size_t)L->n_gate_rows * L->d, reinterpret_cast<float*>(L->ws.err + 1), 0);
+        ck_launch("proxy planes");
+        ck(cudaMemcpy(&L->p_wmax, L->ws.err + 1, sizeof(float), cudaMemcpyDeviceToHost), "proxy max |W|");
+        ck(cudaMemset(L->ws.err + 1, 0, sizeof(int)), "memset");
+        if (!mp::make_tmap_bf16_2d(&L->tm_pplanes, L->p_planes, 3ull * L->p_npad, L->d,
+                                   mp::router_tc_cols_per_cta(nr2), 64))
+            fail(MP_ERR_CUDA, "proxy planes tensor map");
+    }
     L->gates_packed = true;
 }
 
@@ -596,18 +660,41 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
         fail(MP_ERR_VALIDATION, "k_active = " + std::to_string(k) + " out of range [1, " +
                                     std::to_string(std::min(L->k_max, L->G)) + "]");
     tm.begin(0);
+    // zeroed before the router so the router -> routing-epilogue boundary is
+    // kernel to kernel (programmatic dependent launch)
+    if (L->has_router) ck(cudaMemsetAsync(L->r_flagged, 0, 2 * sizeof(uint32_t), s), "memset routing stats");
     if (with_shared && L->sh_ff) {
         if (reinterpret_cast<uintptr_t>(x) % 16) fail(MP_ERR_VALIDATION, "shared expert needs 16-byte aligned x");
         launch_shared_expert(L, x, T, s);
     }
     if (L->desc.router_mode == MP_ROUTER_PROXY) {
         pack_gates(L);
-        mp::launch_proxy_scores(L->dtype, x, T, L->d, L->gate_rows, L->up_rows, L->gate_off, L->n_gate_rows, L->G,
-                                reinterpret_cast<float*>(L->scores), s);
-        mp::launch_router_scores_topk(reinterpret_cast<const float*>(L->scores), T, L->G, L->k_max, kpt, k,
-                                      L->desc.weight_mode, L->sel, L->wsel, L->ws.err, s);
-        ck_launch("router(proxy)");
-        tm.end(0, 2);
+        if (L->proxy_tc && (reinterpret_cast<uintptr_t>(x) % 16) == 0) {
+            const uint32_t nr2 = 2 * L->n_gate_rows;
+            const mp::RouterTcPlan pl = mp::plan_router_tc(T, L->d, nr2, L->num_sms);
+            CUtensorMap tmX;
+            if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "proxy router tensor map");
+            mp::launch_router_tc(&tmX, &L->tm_pplanes, pl, T, L->p_partial, L->p_xnorm, s, true);
+            // fp32 partials: one more rounding of <= 2^-24 sum|x||W| per token
+            const mp::RouterGuard rg{L->p_xnorm, pl.ks,
+                                     mp::router_guard_coef(pl.chunk_kb * 64, L->p_wmax) + 0x1.0p-24 * L->p_wmax,
+                                     L->r_guard_floor};
+            mp::launch_proxy_tc_topk(L->p_partial, pl.ks, T, L->n_gate_rows, L->p_npad, L->gate_off, L->G, L->k_max,
+                                     kpt, k, L->desc.weight_mode, L->sel, L->wsel, L->ws.err, rg, L->scores, L->p_win,
+                                     L->r_flagged, s);
+            mp::launch_proxy_fixup(x, L->d, L->gate_rows, L->up_rows, L->gate_off, L->G, L->k_max, kpt, k,
+                                   L->desc.weight_mode, L->sel, L->wsel, L->ws.err, L->scores, L->p_win, L->r_flagged,
+                                   L->num_sms, s);
+            ck_launch("router(proxy, tensor core)");
+            tm.end(0, 3);
+        } else {
+            mp::launch_proxy_scores(L->dtype, x, T, L->d, L->gate_rows, L->up_rows, L->gate_off, L->n_gate_rows, L->G,
+                                    reinterpret_cast<float*>(L->scores), s);
+            mp::launch_router_scores_topk(reinterpret_cast<const float*>(L->scores), T, L->G, L->k_max, kpt, k,
+                                          L->desc.weight_mode, L->sel, L->wsel, L->ws.err, L->r_flagged, s);
+            ck_launch("router(proxy)");
+            tm.end(0, 3);
+        }
     } else {
         if (!L->has_router) fail(MP_ERR_VALIDATION, "experts-only layer (MP_LAYER_EXPERTS_ONLY) has no router");
         if (!L->router_set) fail(MP_ERR_VALIDATION, "router weights not set (mp_layer_set_router)");
@@ -615,10 +702,9 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             const mp::RouterTcPlan pl = mp::plan_router_tc(T, L->d, L->G, L->num_sms);
             CUtensorMap tmX;
             if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "router tensor map");
-            // zeroed before the router so the router -> routing-epilogue boundary
-            // is kernel to kernel (programmatic dependent launch)
-            ck(cudaMemsetAsync(L->r_flagged, 0, sizeof(uint32_t), s), "memset flagged");
-            mp::launch_router_tc(&tmX, &L->tm_wplanes, pl, T, L->r_partial, s);
+            mp::launch_router_tc(&tmX, &L->tm_wplanes, pl, T, L->r_partial, L->r_xnorm, s);
+            const mp::RouterGuard rg{L->r_xnorm, pl.ks, mp::router_guard_coef(pl.chunk_kb * 64, L->r_wmax),
+                                     L->r_guard_floor};
             L->r_last_ks = pl.ks;
             L->r_last_T = T;
             static const bool fuse_env = [] {  // MOEPRISM_FUSE_BUCKET=0: separate top-k / fixup / bucketing (A/B)
@@ -640,14 +726,14 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
                     L->launches += 1;
                 }
                 mp::launch_route_bucket(L->r_partial, ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
-                                        L->sel, L->wsel, L->r_guard, x, L->d, L->wrT, L->r_ticket, L->r_flagged,
+                                        L->sel, L->wsel, rg, x, L->d, L->wrT, L->r_ticket, L->r_flagged,
                                         L->ws, s, mp::route_tokens_per_block(T));
                 bucketed = true;
                 ck_launch("router(tc)+bucket");
                 tm.end(0, 2);
             } else {
                 mp::launch_partials_topk(L->r_partial, pl.ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
-                                         L->sel, L->wsel, L->ws.err, L->r_guard, L->r_flagged, s);
+                                         L->sel, L->wsel, L->ws.err, rg, L->r_flagged, s);
                 mp::launch_router_fixup(L->dtype, x, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode,
                                         L->sel, L->wsel, L->ws.err, L->r_flagged, L->num_sms, s);
                 ck_launch("router(tc)");
@@ -655,7 +741,7 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             }
         } else {
             mp::launch_router_linear(L->dtype, x, T, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode,
-                                     L->sel, L->wsel, L->ws.err, s);
+                                     L->sel, L->wsel, L->ws.err, L->r_flagged, s);
             ck_launch("router");
             tm.end(0, 1);
         }
@@ -710,8 +796,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
         if (D.d_ff < D.n_subexperts) fail(MP_ERR_VALIDATION, "partition needs at least as many neurons as sub-experts");
         const uint64_t G = (uint64_t)D.n_experts * D.n_subexperts;
         if (G > mp::kMaxG) fail(MP_ERR_VALIDATION, "E*S = " + std::to_string(G) + " exceeds " + std::to_string(mp::kMaxG));
-        if (D.k_max < 1 || D.k_max > G || D.k_max > 64)
-            fail(MP_ERR_VALIDATION, "k_max must be in [1, min(E*S, 64)]");
+        if (D.k_max < 1 || D.k_max > G) fail(MP_ERR_VALIDATION, "k_max must be in [1, E*S]");
         if (D.dtype != MP_DTYPE_F32 && D.dtype != MP_DTYPE_BF16) fail(MP_ERR_VALIDATION, "unknown dtype");
         if (D.router_mode > MP_ROUTER_PROXY || D.weight_mode > MP_WEIGHT_SOFTMAX_RENORM)
             fail(MP_ERR_VALIDATION, "unknown router / weight mode");
@@ -785,21 +870,20 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                     L->r_npad = round_up(L->G, 32);
                     // K-split partials [ks][T][Npad]: 256-deep splits, or 64-deep ones
                     // when few token tiles (plan_router_tc) -- size for both
-                    const uint32_t n256 = (L->d + 255) / 256, n64 = (L->d + 63) / 64;
-                    const uint32_t small_tiles = (static_cast<uint32_t>(L->num_sms) / 2 + n256 - 1) / n256;
-                    const size_t rows_small = std::min<size_t>(L->max_tokens, (size_t)small_tiles * 128);
-                    const size_t n_part = std::max((size_t)n256 * L->max_tokens, (size_t)n64 * rows_small);
+                    const size_t n_part = mp::router_tc_partial_rows(L->max_tokens, L->d, L->G, L->num_sms);
                     L->wr_planes = dalloc<char>((size_t)3 * L->r_npad * L->d * 2, "router planes");
                     L->r_partial = dalloc<double>(n_part * L->r_npad, "router partials");
-                    L->r_flagged = dalloc<uint32_t>((size_t)L->max_tokens + 1, "router flagged");
+                    L->r_xnorm = dalloc<double>(n_part, "router |x| sums");
                     L->r_ticket = dalloc<uint32_t>(1, "router ticket");
                     ck(cudaMemset(L->r_ticket, 0, sizeof(uint32_t)), "memset ticket");
-                    if (const char* env = std::getenv("MOEPRISM_ROUTER_GUARD")) L->r_guard = std::atof(env);
                     if (!mp::make_tmap_bf16_2d(&L->tm_wplanes, L->wr_planes, 3ull * L->r_npad, L->d,
                                                mp::router_tc_cols_per_cta(L->G), 64))
                         fail(MP_ERR_CUDA, "router planes tensor map");
                 }
                 if (D.router_mode == MP_ROUTER_PROXY) L->gate_off = dalloc<uint32_t>(L->G + 1, "gate offsets");
+                if (const char* env = std::getenv("MOEPRISM_ROUTER_GUARD")) L->r_guard_floor = std::atof(env);
+                L->r_flagged = dalloc<uint32_t>((size_t)L->max_tokens + 2, "routing stats");
+                ck(cudaMemset(L->r_flagged, 0, 2 * sizeof(uint32_t)), "memset routing stats");
             }
             const size_t tk = (size_t)L->max_tokens * L->k_max;
             // bucketing blocks: 32 tokens, or 8 / 2 in the fused router for small batches
@@ -809,8 +893,8 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             L->sel = dalloc<uint32_t>(tk, "sel");
             L->wsel = dalloc<float>(tk, "w");
             L->kpt_dev = dalloc<uint32_t>(L->max_tokens, "k per token");
-            L->ws.err = dalloc<int>(1, "err");
-            ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset err");
+            L->ws.err = dalloc<int>(2, "err");  // [0] flags, [1] scratch (router max |W|)
+            ck(cudaMemset(L->ws.err, 0, 2 * sizeof(int)), "memset err");
             L->x_stage = dalloc<char>((size_t)L->max_tokens * L->d * L->esz, "x stage");
             if (experts) {
                 L->ws.lrank = dalloc<uint32_t>(tk, "lrank");
@@ -963,15 +1047,19 @@ MP_API mp_status mp_layer_set_router(mp_layer_t L, const float* w_r) {
             cudaFree(tmp);
             ck(e1, "router upload");
         }
-        ck(cudaMemset(L->ws.err, 0, sizeof(int)), "memset");
+        ck(cudaMemset(L->ws.err, 0, 2 * sizeof(int)), "memset");
         mp::launch_finite_check(tmp, n, L->ws.err, 0);
+        // max |W_r| (the router's certification bound); ws.err[1] as scratch
+        mp::launch_absmax(tmp, n, reinterpret_cast<float*>(L->ws.err + 1), 0);
         mp::launch_transpose_router(tmp, L->d, L->G, L->G_pad, L->wrT, 0);
         if (L->router_tc) mp::launch_split_router(tmp, L->d, L->G, L->r_npad, L->wr_planes, 0);
         ck_launch("router transpose");
-        int flag = 0;
-        ck(cudaMemcpy(&flag, L->ws.err, sizeof(int), cudaMemcpyDeviceToHost), "flag");
+        int flag[2] = {0, 0};
+        ck(cudaMemcpy(flag, L->ws.err, 2 * sizeof(int), cudaMemcpyDeviceToHost), "flag");
+        ck(cudaMemset(L->ws.err, 0, 2 * sizeof(int)), "memset");
         cudaFree(tmp);
-        if (flag) fail(MP_ERR_VALIDATION, "router weight is not finite");
+        if (flag[0]) fail(MP_ERR_VALIDATION, "router weight is not finite");
+        std::memcpy(&L->r_wmax, &flag[1], sizeof(float));
         L->router_set = true;
     });
 }
@@ -1237,6 +1325,20 @@ MP_API mp_status mp_layer_route(mp_layer_t L, const void* x, uint32_t T, const u
         copy_outputs(L, T, sel_out, w_out, nullptr, s, cudaMemcpyDeviceToDevice);
         static const int order[] = {0};
         tm.finish(order, 1);
+    });
+}
+
+MP_API mp_status mp_layer_route_stats(mp_layer_t L, uint32_t* reselected, uint32_t* near_ties, void* stream) {
+    return guarded([&] {
+        if (!L) fail(MP_ERR_VALIDATION, "null argument");
+        if (!L->has_router) fail(MP_ERR_VALIDATION, "experts-only layer has no router");
+        DeviceGuard dg(L->desc.device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        uint32_t st[2] = {0, 0};
+        ck(cudaMemcpyAsync(st, L->r_flagged, sizeof(st), cudaMemcpyDeviceToHost, s), "routing stats");
+        ck(cudaStreamSynchronize(s), "sync");
+        if (reselected) *reselected = st[0];
+        if (near_ties) *near_ties = st[1];
     });
 }
 

@@ -37,14 +37,40 @@ struct BucketWs {
     int* err;                // device error flags (bit 0: bad k / selection, bit 1: non-finite x)
 };
 
+// Certification bound of the tensor-core router logits for token t:
+//   guard_t = coef * sum_s xnorm[s][t] + 2^-23 * max_g |logit_tg| + floor_abs
+// coef = chunk depth * 2^-23 * max|W_r| * (1 + margin) (router_guard_coef).
+struct RouterGuard {
+    const double* xnorm;  // [ks][T]
+    uint32_t ks;          // K splits of xnorm
+    double coef;
+    double floor_abs;     // MOEPRISM_ROUTER_GUARD (tests widen the window), else 0
+};
+
 // dtype: 0 f32, 1 bf16
 void launch_router_linear(int dtype, const void* x, uint32_t T, uint32_t d, const float* wrT, uint32_t G,
                           uint32_t k_max, const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
-                          int* err, cudaStream_t s);
+                          int* err, uint32_t* stats, cudaStream_t s);
+// stats (nullable): stats[1] += near ties (k-th/(k+1)-th gap < 1e-6)
 void launch_router_scores_topk(const float* scores, uint32_t T, uint32_t G, uint32_t k_max, const uint32_t* kpt,
-                               uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err, cudaStream_t s);
+                               uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err, uint32_t* stats,
+                               cudaStream_t s);
+// Proxy router (proxy.cu).  Exact path: fp64 gate activations in the
+// reference's order -> scores [T][G] (double, at the front of `scores`).
 void launch_proxy_scores(int dtype, const void* x, uint32_t T, uint32_t d, const float* gate_w, const float* up_w,
                          const uint32_t* gate_off, uint32_t n_gate_rows, uint32_t G, float* scores, cudaStream_t s);
+// Tensor-core path: after launch_router_tc over the [gate; up] planes (fp32
+// partials), scores + per-token bound + certified top-k; uncertain tokens to
+// flagged[2..] with their window (a, b, guard) in pwin [T][3], re-selected by
+// launch_proxy_fixup from fp64 gate activations.
+void launch_proxy_tc_topk(const float* partial, uint32_t ks, uint32_t T, uint32_t NR, uint32_t Npad,
+                          const uint32_t* gate_off, uint32_t G, uint32_t k_max, const uint32_t* kpt, uint32_t k,
+                          int weight_mode, uint32_t* sel, float* w, int* err, const RouterGuard& rg, double* pscore,
+                          double* pwin, uint32_t* flagged, cudaStream_t s);
+void launch_proxy_fixup(const void* x, uint32_t d, const float* gate_w, const float* up_w, const uint32_t* gate_off,
+                        uint32_t G, uint32_t k_max, const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel,
+                        float* w, int* err, const double* pscore, const double* pwin, uint32_t* flagged, int num_sms,
+                        cudaStream_t s);
 void launch_bucket_local(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32_t G, BucketWs& ws,
                          cudaStream_t s);
 void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s);
@@ -73,32 +99,44 @@ struct RouterTcPlan {
     size_t smem;
 };
 RouterTcPlan plan_router_tc(uint32_t T, uint32_t d, uint32_t G, int num_sms);
+// rows ([ks][T] products) of the K-split partial buffers over every T <= max_T
+size_t router_tc_partial_rows(uint32_t max_T, uint32_t d, uint32_t G, int num_sms);
 uint32_t router_tc_cols_per_cta(uint32_t G);  // TMA box rows of the weight-plane tensor map
 void launch_split_router(const float* wr, uint32_t d, uint32_t G, uint32_t Npad, void* planes, cudaStream_t s);
+// rows [n_a][d] ++ [n_b][d] (fp32) -> three bf16 planes [3][Npad][d]
+void launch_split_rows(const float* ra, const float* rb, uint32_t n_a, uint32_t n_b, uint32_t d, uint32_t Npad,
+                       void* planes, cudaStream_t s);
+// xnorm: [ks][T] fp64 per-split sums of |x| (written by the column-split-0 CTAs)
+// out_f32: partials rounded to fp32 once per K split (the proxy router's
+// 2*E*S*r gate/up columns; the rounding adds <= 2^-24 sum|x||W| to the bound)
 void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const RouterTcPlan& pl, uint32_t T,
-                      double* partial, cudaStream_t s);
-// guard: tensor-core logit error bound; tokens whose k-th/(k+1)-th gap is below
-// 2*guard are appended to flagged[1..] (count in flagged[0], zeroed by the
-// caller) and re-selected from exact fp64 logits by launch_router_fixup.
+                      void* partial, double* xnorm, cudaStream_t s, bool out_f32 = false);
+double router_guard_coef(uint32_t chunk_depth, float wmax);
+// Routing statistics of a forward (stats / flagged, zeroed by the caller):
+// [0] tokens re-selected from exact fp64 logits, [1] near ties (exact
+// k-th/(k+1)-th gap < 1e-6), then (non-fused path) the re-selected tokens.
+// rg: per-token tensor-core logit error bound; tokens whose k-th/(k+1)-th gap is below
+// 2*guard_t + 1e-6 are appended to flagged[2..] (count in flagged[0]) and
+// re-selected from exact fp64 logits by launch_router_fixup.
 void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                           const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
-                          double guard, uint32_t* flagged, cudaStream_t s);
+                          const RouterGuard& rg, uint32_t* flagged, cudaStream_t s);
 // Fused routing epilogue of the tensor-core router (bf16 x, d % 4 == 0):
 // partials -> top-k -> exact re-selection of near-tie tokens (count added to
 // *n_fixed) -> bucket ranks -> device-wide scans (last CTA; *ticket must be
 // 0 on entry and is left 0).  Replaces partials_topk + router_fixup +
 // bucket_local + bucket_scan.
 void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
-                         const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, double guard,
-                         const void* x, uint32_t d, const float* wrT, uint32_t* ticket, uint32_t* n_fixed,
-                         BucketWs& ws, cudaStream_t s, uint32_t tb = kRouteTokensPerBlock);
+                         const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
+                         const RouterGuard& rg, const void* x, uint32_t d, const float* wrT, uint32_t* ticket,
+                         uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb = kRouteTokensPerBlock);
 // tokens per CTA of the fused routing epilogue: fewer for small batches (more CTAs)
 inline uint32_t route_tokens_per_block(uint32_t T) { return T <= 256 ? 2u : T <= 1024 ? 8u : kRouteTokensPerBlock; }
 // in-place fixed-order sum of the K-split router partials into plane 0
 void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, cudaStream_t s);
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
-                         const uint32_t* flagged, int num_sms, cudaStream_t s);
+                         uint32_t* flagged, int num_sms, cudaStream_t s);
 
 // Packing (load time).
 void launch_pack_w1(int dtype, const float* wg, const float* wu, uint32_t d, uint32_t ff, const int32_t* nmap,
@@ -163,6 +201,12 @@ void launch_fidelity(const float* act, uint32_t rows, uint32_t cols, uint32_t n_
                      double* norm, double* proxy, double* recall, cudaStream_t s);
 // meta = {0, rows, 0, ceil(rows / 128)}: offsets + 128-row tile prefix of one group
 void launch_set_group_meta(uint32_t* meta, uint32_t rows, cudaStream_t s);
+
+// One-time (per kernel, per device) dynamic shared-memory attribute; thread-safe
+// (layer.cu).  max_carveout: also prefer the maximum shared-memory carveout.
+void func_attr_once(const void* func, int max_dyn_smem, bool max_carveout = false);
+// max |p[i]| over n floats into *out (device, must be zeroed; atomic max on the bits)
+void launch_absmax(const float* p, size_t n, float* out, cudaStream_t s);
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point.
 bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,

@@ -100,6 +100,16 @@ __global__ void finite_check_kernel(const float* __restrict__ p, size_t n, int* 
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+__global__ void absmax_kernel(const float* __restrict__ p, size_t n, float* __restrict__ out) {
+    float m = 0.0f;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x)
+        m = fmaxf(m, fabsf(p[q]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    // non-negative floats order like their bit patterns
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(out), __float_as_uint(m));
+}
+
 // Counter-based generator, bit-identical to orc_synth_fill (oracle/moe_oracle.c).
 __device__ __forceinline__ uint64_t sm_mix(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -160,6 +170,10 @@ void launch_pack_gate_rows(const float* wg, const float* wu, uint32_t d, uint32_
 
 void launch_finite_check(const float* p, size_t n, int* flag, cudaStream_t s) {
     finite_check_kernel<<<1184, 256, 0, s>>>(p, n, flag);
+}
+
+void launch_absmax(const float* p, size_t n, float* out, cudaStream_t s) {
+    absmax_kernel<<<592, 256, 0, s>>>(p, n, out);
 }
 
 void launch_synth_fill(void* dst, int dtype, size_t n, uint64_t seed, uint64_t first, double scale, cudaStream_t s) {

@@ -15,6 +15,7 @@
 
 #include "mp_common.cuh"
 #include "mp_kernels.h"
+#include "mp_topk.cuh"
 
 namespace mp {
 
@@ -25,223 +26,34 @@ constexpr uint32_t GB = 64;                    // router outputs per pass
 constexpr uint32_t KC = 32;                    // K chunk staged in smem
 constexpr uint32_t kRouterThreads = 256;
 
-// ---------------------------------------------------------------- top-k
-// One warp selects the k_t best of G scores for one token (score desc,
-// index asc -- inc/gating.hpp:138-141), emits them in ascending index order
-// (inc/gating.hpp:143) with their softmax-renormalised weights.
-// Returns (to every lane) the gap between the k-th and (k+1)-th best score
-// (+inf when k == G): the near-tie measure of the routing contract.
-// keys (nullable): selection keys replacing sc for the ranking only (the
-// exact re-selection of near-tie tokens); the weights always use sc.
-// vk_out (nullable): the k-th and (k+1)-th best keys.
-// NC: 32-candidate chunks per lane held in registers (G <= 32 NC); smaller NC
-// for small G trims the unrolled per-round work (Mixtral: G = 64 -> NC = 2)
-template <int NC = kMaxG / 32>
-__device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uint32_t k, uint32_t k_max,
-                                  int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row,
-                                  const double* __restrict__ keys = nullptr, double* vk_out = nullptr) {
+// Per-token certification bound of the tensor-core router logits (RouterGuard,
+// mp_kernels.h): coef * sum |x_t| + 2^-23 max_g |logit_tg| + floor.  Warp-wide;
+// every lane gets the value.  Non-finite (bad input, raised elsewhere): 0, so
+// nothing is queued for the exact pass.
+__device__ __forceinline__ double warp_router_guard(const RouterGuard& rg, uint32_t T, uint32_t t, double maxabs) {
     const uint32_t lane = lane_id();
-    const uint32_t nc = (G + 31) / 32;
-    double v[NC];
-    uint32_t taken = 0;  // bit c: value c of this lane selected
-    const double* kv = keys ? keys : sc;
+    double xn = 0.0;
+    for (uint32_t s = lane; s < rg.ks; s += 32) xn += rg.xnorm[(size_t)s * T + t];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const uint32_t g = lane + 32u * c;
-        v[c] = (c < (int)nc && g < G) ? kv[g] : -DBL_MAX;
+    for (int off = 16; off > 0; off >>= 1) {
+        xn += __shfl_xor_sync(0xffffffffu, xn, off);
+        maxabs = fmax(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, off));
     }
-    double vmax = 0.0, vk = 0.0, vk1 = -INFINITY;
-    const uint32_t rounds = k < G ? k + 1 : k;
-    for (uint32_t r = 0; r < rounds; ++r) {
-        double bv = -INFINITY;
-        uint32_t bi = 0xFFFFFFFFu;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const uint32_t g = lane + 32u * c;
-            if (c < (int)nc && g < G && !((taken >> c) & 1u) && v[c] > bv) {
-                bv = v[c];
-                bi = g;
-            }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-            const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
-            if (ov > bv || (ov == bv && oi < bi)) {
-                bv = ov;
-                bi = oi;
-            }
-        }
-        if (r == 0) vmax = bv;
-        if (r == k) {  // the (k+1)-th best: measured, not taken
-            vk1 = bv;
-            break;
-        }
-        vk = bv;
-        if (bi != 0xFFFFFFFFu && (bi & 31u) == lane) taken |= 1u << (bi >> 5);
-    }
-    if (vk_out && lane == 0) {
-        vk_out[0] = vk;
-        vk_out[1] = vk1;
-    }
-    if (keys) {  // weights from the logits, max over the selection (contains the top-1)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const uint32_t g = lane + 32u * c;
-            v[c] = (c < (int)nc && g < G) ? sc[g] : -DBL_MAX;
-        }
-        double m = -DBL_MAX;
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-            if ((taken >> c) & 1u) m = fmax(m, v[c]);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-        vmax = m;
-    }
-    // softmax over all G cancels in the renormalisation: w_g = e^(l_g - m) / sum_sel
-    // (each exponential evaluated once)
-    double z = 0.0;
-    double ex[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        ex[c] = ((taken >> c) & 1u) ? exp(v[c] - vmax) : 0.0;
-        z += ex[c];
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
-    // ascending-index emission: index order is (c, lane)
-    uint32_t base = 0;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        if (c >= (int)nc) break;
-        const bool mine = (taken >> c) & 1u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, mine);
-        if (mine) {
-            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
-            sel_row[pos] = lane + 32u * c;
-            w_row[pos] = weight_mode == 1 ? static_cast<float>(ex[c] / z) : 1.0f;
-        }
-        base += __popc(bal);
-    }
-    for (uint32_t j = k + lane; j < k_max; j += 32) {
-        sel_row[j] = kSelNone;
-        w_row[j] = 0.0f;
-    }
-    return k < G ? vk - vk1 : INFINITY;
-}
-
-// Fast selection for the tensor-core router: keys are the fp32-rounded logits
-// (rounding <= 2e-7 at |logit| < 4, inside the certification guard), packed
-// with the index into one order-preserving u64 (key bits high, ~index low:
-// larger packed value = larger key, then lower index), so each argmax step is
-// one 64-bit shuffle + max.  Weights use the fp64 logits `vals`.  Returns the
-// key gap between the k-th and (k+1)-th best (+inf when k == G); vk_out gets
-// both keys (as double).
-__device__ __forceinline__ uint64_t pack_key(float v, uint32_t g) {
-    uint32_t b = __float_as_uint(v);
-    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);  // order-preserving
-    return (static_cast<uint64_t>(b) << 32) | static_cast<uint32_t>(~g);
-}
-__device__ __forceinline__ float unpack_key(uint64_t p) {
-    uint32_t b = static_cast<uint32_t>(p >> 32);
-    b = (b & 0x80000000u) ? (b & 0x7FFFFFFFu) : ~b;
-    return __uint_as_float(b);
-}
-
-template <int NC = kMaxG / 32>
-__device__ double warp_topk_fast(const double* __restrict__ vals, uint32_t G, uint32_t k, uint32_t k_max,
-                                 int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row,
-                                 double* vk_out) {
-    const uint32_t lane = lane_id();
-    const uint32_t nc = (G + 31) / 32;
-    uint64_t v[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const uint32_t g = lane + 32u * c;
-        v[c] = (c < (int)nc && g < G) ? pack_key(static_cast<float>(vals[g]), g) : 0ull;
-    }
-    uint32_t taken = 0;
-    uint64_t pk = 0, pk1 = 0;
-    const uint32_t rounds = k < G ? k + 1 : k;
-    for (uint32_t r = 0; r < rounds; ++r) {
-        uint64_t best = 0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-            if (!((taken >> c) & 1u) && v[c] > best) best = v[c];
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const uint64_t o = __shfl_xor_sync(0xffffffffu, best, off);
-            best = o > best ? o : best;
-        }
-        if (r == k) {
-            pk1 = best;
-            break;
-        }
-        pk = best;
-        const uint32_t g = ~static_cast<uint32_t>(best);
-        if ((g & 31u) == lane) taken |= 1u << (g >> 5);
-    }
-    const double vk = unpack_key(pk), vk1 = k < G ? (double)unpack_key(pk1) : -INFINITY;
-    if (vk_out && lane == 0) {
-        vk_out[0] = vk;
-        vk_out[1] = vk1;
-    }
-    double m = -DBL_MAX;
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-        if ((taken >> c) & 1u) m = fmax(m, vals[lane + 32u * c]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
-    double z = 0.0;
-    double ex[NC];  // each exponential evaluated once
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        ex[c] = ((taken >> c) & 1u) ? exp(vals[lane + 32u * c] - m) : 0.0;
-        z += ex[c];
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
-    uint32_t base = 0;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        if (c >= (int)nc) break;
-        const bool mine = (taken >> c) & 1u;
-        const uint32_t bal = __ballot_sync(0xffffffffu, mine);
-        if (mine) {
-            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
-            sel_row[pos] = lane + 32u * c;
-            w_row[pos] = weight_mode == 1 ? static_cast<float>(ex[c] / z) : 1.0f;
-        }
-        base += __popc(bal);
-    }
-    for (uint32_t j = k + lane; j < k_max; j += 32) {
-        sel_row[j] = kSelNone;
-        w_row[j] = 0.0f;
-    }
-    return k < G ? vk - vk1 : INFINITY;
-}
-
-__device__ __forceinline__ uint32_t token_k(const uint32_t* kpt, uint32_t k, uint32_t t, uint32_t k_max, uint32_t G,
-                                            int* err) {
-    uint32_t kt = kpt ? kpt[t] : k;
-    if (kt < 1 || kt > k_max || kt > G) {
-        if (err) atomicOr(err, 1);
-        kt = kt < 1 ? 1 : (kt > k_max ? k_max : kt);
-        if (kt > G) kt = G;
-    }
-    return kt;
+    const double g = rg.coef * xn + 0x1.0p-23 * maxabs + rg.floor_abs;
+    return isfinite(g) ? g : 0.0;
 }
 
 // ---------------------------------------------------------------- linear router
-// logits[t][g] = sum_i x[t][i] * W_r[i][g].  fp32 FFMA partials over 16
-// consecutive i (products exact inside the FMA), accumulated in fp64 in
-// ascending i: |error| ~1e-7, well under the 1e-6 near-tie window of the
-// bit-exact routing contract.  CTA: 32 tokens x all G.
+// logits[t][g] = sum_i x[t][i] * W_r[i][g] with fp64 FMAs in ascending i
+// (products of fp32 / bf16 inputs are exact in fp64): the oracle's own
+// arithmetic, so the selection is exact up to fp64 rounding -- no
+// certification pass is needed.  Used for fp32 layers and for bf16 layers the
+// tensor-core router cannot take (d % 8 != 0).  CTA: 32 tokens x all G.
 template <typename Tx>
 __global__ void __launch_bounds__(kRouterThreads) router_linear_kernel(
     const Tx* __restrict__ x, uint32_t T, uint32_t d, const float* __restrict__ wrT, uint32_t G, uint32_t k_max,
     const uint32_t* __restrict__ kpt, uint32_t k_scalar, int weight_mode, uint32_t* __restrict__ sel,
-    float* __restrict__ wout, int* __restrict__ err) {
+    float* __restrict__ wout, int* __restrict__ err, uint32_t* __restrict__ stats) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* lg = reinterpret_cast<double*>(smem_raw);                 // [TB][G]
     float* xs = reinterpret_cast<float*>(lg + TB * G);                // [KC][TB+1]
@@ -253,7 +65,6 @@ __global__ void __launch_bounds__(kRouterThreads) router_linear_kernel(
 
     for (uint32_t g0 = 0; g0 < G; g0 += GB) {
         double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-        float part[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
         for (uint32_t k0 = 0; k0 < d; k0 += KC) {
             __syncthreads();
             for (uint32_t q = tid; q < TB * KC; q += kRouterThreads) {
@@ -277,33 +88,11 @@ __global__ void __launch_bounds__(kRouterThreads) router_linear_kernel(
                 const float xa = xs[kk * (TB + 1) + 2 * ty];
                 const float xb = xs[kk * (TB + 1) + 2 * ty + 1];
                 const float4 wv = *reinterpret_cast<const float4*>(&ws[kk * (GB + 4) + 4 * tx]);
-                if constexpr (sizeof(Tx) == 4) {
-                    // fp32 (reference-exact) mode: fp64 accumulation like the
-                    // oracle, so the softmax weights round to the same floats
-                    const double wvd[4] = {wv.x, wv.y, wv.z, wv.w};
+                const double wvd[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        acc[0][b] = fma(static_cast<double>(xa), wvd[b], acc[0][b]);
-                        acc[1][b] = fma(static_cast<double>(xb), wvd[b], acc[1][b]);
-                    }
-                    continue;
-                }
-                part[0][0] = fmaf(xa, wv.x, part[0][0]);
-                part[0][1] = fmaf(xa, wv.y, part[0][1]);
-                part[0][2] = fmaf(xa, wv.z, part[0][2]);
-                part[0][3] = fmaf(xa, wv.w, part[0][3]);
-                part[1][0] = fmaf(xb, wv.x, part[1][0]);
-                part[1][1] = fmaf(xb, wv.y, part[1][1]);
-                part[1][2] = fmaf(xb, wv.z, part[1][2]);
-                part[1][3] = fmaf(xb, wv.w, part[1][3]);
-                if ((kk & 15u) == 15u) {
-#pragma unroll
-                    for (int a = 0; a < 2; ++a)
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) {
-                            acc[a][b] += static_cast<double>(part[a][b]);
-                            part[a][b] = 0.0f;
-                        }
+                for (int b = 0; b < 4; ++b) {
+                    acc[0][b] = fma(static_cast<double>(xa), wvd[b], acc[0][b]);
+                    acc[1][b] = fma(static_cast<double>(xb), wvd[b], acc[1][b]);
                 }
             }
         }
@@ -322,7 +111,9 @@ __global__ void __launch_bounds__(kRouterThreads) router_linear_kernel(
         const uint32_t tg = t0 + t;
         if (tg >= T) break;
         const uint32_t kt = token_k(kpt, k_scalar, tg, k_max, G, err);
-        warp_topk_token(lg + t * G, G, kt, k_max, weight_mode, sel + (size_t)tg * k_max, wout + (size_t)tg * k_max);
+        const double gap = warp_topk_token(lg + t * G, G, kt, k_max, weight_mode, sel + (size_t)tg * k_max,
+                                           wout + (size_t)tg * k_max);
+        if (stats && gap < kNearTie && (tid & 31) == 0) atomicAdd(stats + 1, 1u);
     }
 }
 
@@ -331,12 +122,13 @@ __global__ void __launch_bounds__(256) scores_topk_kernel(const double* __restri
                                                           uint32_t k_max, const uint32_t* __restrict__ kpt,
                                                           uint32_t k_scalar, int weight_mode,
                                                           uint32_t* __restrict__ sel, float* __restrict__ wout,
-                                                          int* __restrict__ err) {
+                                                          int* __restrict__ err, uint32_t* __restrict__ stats) {
     const uint32_t t = blockIdx.x * 8 + threadIdx.x / 32;
     if (t >= T) return;
     const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
-    warp_topk_token(scores + (size_t)t * G, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
-                    wout + (size_t)t * k_max);
+    const double gap = warp_topk_token(scores + (size_t)t * G, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
+                                       wout + (size_t)t * k_max);
+    if (stats && gap < kNearTie && (threadIdx.x & 31) == 0) atomicAdd(stats + 1, 1u);
 }
 
 // Tensor-core router epilogue: logits[t][g] = sum_{s ascending} partial[s][t][g]
@@ -346,23 +138,26 @@ __global__ void __launch_bounds__(256) partials_topk_kernel(const double* __rest
                                                             const uint32_t* __restrict__ kpt, uint32_t k_scalar,
                                                             int weight_mode, uint32_t* __restrict__ sel,
                                                             float* __restrict__ wout, int* __restrict__ err,
-                                                            double guard, uint32_t* __restrict__ flagged) {
+                                                            RouterGuard rg, uint32_t* __restrict__ flagged) {
     __shared__ double sc[8][kMaxG];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t t = blockIdx.x * 8 + warp;
     if (t >= T) return;
+    double maxabs = 0.0;
     for (uint32_t g = lane; g < G; g += 32) {
         double v = 0.0;
         for (uint32_t s = 0; s < ks; ++s) v += partial[((size_t)s * T + t) * Npad + g];
         sc[warp][g] = v;
+        maxabs = fmax(maxabs, fabs(v));
     }
+    const double guard = warp_router_guard(rg, T, t, maxabs);
     __syncwarp();
     const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
     const double gap = warp_topk_token(sc[warp], G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
                                        wout + (size_t)t * k_max);
     // the selection is certified only when the k-th / (k+1)-th gap exceeds
     // twice the tensor-core error bound; otherwise recompute exactly (fp64)
-    if (gap < 2.0 * guard && lane == 0) flagged[1 + atomicAdd(&flagged[0], 1u)] = t;
+    if (gap < 2.0 * guard + kNearTie && lane == 0) flagged[2 + atomicAdd(&flagged[0], 1u)] = t;
 }
 
 // Exact fp64 logits for the flagged tokens (x bf16/f32 . W_r fp32, products
@@ -375,13 +170,13 @@ __global__ void __launch_bounds__(1024) router_fixup_kernel(const Tx* __restrict
                                                            const uint32_t* __restrict__ kpt, uint32_t k_scalar,
                                                            int weight_mode, uint32_t* __restrict__ sel,
                                                            float* __restrict__ wout, int* __restrict__ err,
-                                                           const uint32_t* __restrict__ flagged) {
+                                                           uint32_t* __restrict__ flagged) {
     extern __shared__ double xs_d[];  // [d]
     __shared__ double lg[kMaxG];
     const uint32_t n = flagged[0];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     for (uint32_t f = blockIdx.x; f < n; f += gridDim.x) {
-        const uint32_t t = flagged[1 + f];
+        const uint32_t t = flagged[2 + f];
         const Tx* xr = x + (size_t)t * d;
         for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) xs_d[i] = static_cast<double>(to_f32(xr[i]));
         __syncthreads();
@@ -424,7 +219,9 @@ __global__ void __launch_bounds__(1024) router_fixup_kernel(const Tx* __restrict
         __syncthreads();
         if (warp == 0) {
             const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
-            warp_topk_token(lg, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max);
+            const double gap =
+                warp_topk_token(lg, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max);
+            if (gap < kNearTie && lane == 0) atomicAdd(const_cast<uint32_t*>(flagged) + 1, 1u);
         }
         __syncthreads();
     }
@@ -690,8 +487,8 @@ template <int NC>
 __global__ void __launch_bounds__(1024) route_bucket_kernel(
     const double* __restrict__ partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
     const uint32_t* __restrict__ kpt, uint32_t k_scalar, int weight_mode, uint32_t* __restrict__ sel,
-    float* __restrict__ wout, int* __restrict__ err, double guard, const __nv_bfloat16* __restrict__ x, uint32_t d,
-    const float* __restrict__ wrT, uint32_t* __restrict__ ticket, uint32_t* __restrict__ n_fixed, uint32_t* lrank,
+    float* __restrict__ wout, int* __restrict__ err, RouterGuard rg, const __nv_bfloat16* __restrict__ x, uint32_t d,
+    const float* __restrict__ wrT, uint32_t* __restrict__ ticket, uint32_t* __restrict__ stats, uint32_t* lrank,
     uint32_t* block_counts, uint32_t* block_base, uint32_t* offsets, uint32_t* mprefix_tc, uint32_t* mprefix_simt,
     uint32_t* mprefix_tc2, uint32_t tb) {
     extern __shared__ double rsm[];  // [tb][G] logits, then [tb][G] keys
@@ -726,6 +523,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     __syncthreads();
     bool flagged = false;
     uint32_t kt = 0;
+    double guard = 0.0;
     if (t < T) {
         // fixed-order sum over the K splits; all NC loads of a split in flight
         // (the partials come from L2 / HBM: a load per candidate in turn left
@@ -742,15 +540,22 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
 #pragma unroll
             for (int c = 0; c < NC; ++c) v[c] += u[c];
         }
+        double maxabs = 0.0;
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-            if (lane + 32u * c < G) sc[lane + 32u * c] = v[c];
+            if (lane + 32u * c < G) {
+                sc[lane + 32u * c] = v[c];
+                maxabs = fmax(maxabs, fabs(v[c]));
+            }
+        guard = warp_router_guard(rg, T, t, maxabs);
         __syncwarp();
         kt = token_k(kpt, k_scalar, t, k_max, G, err);
         const double gap = warp_topk_fast<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
                                           wout + (size_t)t * k_max, vk[warp]);
         __syncwarp();
-        flagged = gap < 2.0 * guard;
+        // the exact pass also takes every token that may be an oracle near tie
+        // (exact gap < 1e-6), so near ties are counted exactly
+        flagged = gap < 2.0 * guard + kNearTie;
         if (flagged) {  // queue the uncertainty window for the CTA-wide exact pass
             const double a = vk[warp][0], b = vk[warp][1];
             for (uint32_t g0 = 0; g0 < G; g0 += 32) {
@@ -803,8 +608,13 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
                 }
         }
         __syncwarp();
-        warp_topk_token<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max, wout + (size_t)t * k_max, key);
-        if (lane == 0) atomicAdd(n_fixed, 1u);
+        // the k-th and (k+1)-th exact keys both lie in the window: gap is exact
+        const double egap = warp_topk_token<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
+                                                wout + (size_t)t * k_max, key);
+        if (lane == 0) {
+            atomicAdd(stats, 1u);
+            if (egap < kNearTie) atomicAdd(stats + 1, 1u);
+        }
     }
     __syncthreads();  // this CTA's selections are visible to the CTA
     MP_RT_STAMP();    // 2: exact pass done
@@ -881,7 +691,8 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
         slot_row[(size_t)t * k_max + j] = pos;
     }
     __syncwarp();
-    // slot positions in registers (k_max <= 64): lane j holds slots j, j + 32
+    // slot positions in registers for the first 64 slots (lane j holds slots j,
+    // j + 32); slots >= 64 (k_max up to E*S) are read back from slot_row
     uint32_t pos_a = lane < k_max ? slot_row[(size_t)t * k_max + lane] : kSelNone;
     uint32_t pos_b = lane + 32 < k_max ? slot_row[(size_t)t * k_max + lane + 32] : kSelNone;
     constexpr uint32_t VE = 16 / sizeof(Tx);  // elements per 16-byte vector
@@ -917,7 +728,8 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const Tx* __restrict__ x,
         }
         if (!x_perm) continue;
         for (uint32_t j = 0; j < k_max; ++j) {
-            const uint32_t pos = __shfl_sync(0xffffffffu, j < 32 ? pos_a : pos_b, j & 31);
+            const uint32_t pos =
+                j < 64 ? __shfl_sync(0xffffffffu, j < 32 ? pos_a : pos_b, j & 31) : slot_row[(size_t)t * k_max + j];
             if (pos == kSelNone) continue;
             Tx* dst = x_perm + (size_t)pos * d_pad;
 #pragma unroll
@@ -1011,8 +823,8 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
                                                            const float* __restrict__ w_sh,
                                                            const __nv_bfloat16* __restrict__ x_res,
                                                            __nv_bfloat16* __restrict__ y) {
-    __shared__ uint32_t rows[64];
-    __shared__ float wts[64];
+    __shared__ uint32_t rows[kMaxG];
+    __shared__ float wts[kMaxG];
     const uint32_t t = blockIdx.x;
     griddep_wait();
     griddep_launch();
@@ -1087,9 +899,9 @@ __global__ void __launch_bounds__(256) combine_f64_kernel(const double* __restri
                                                           const uint32_t* __restrict__ sel,
                                                           const float* __restrict__ w, uint32_t k_max,
                                                           uint32_t group_S, float* __restrict__ y) {
-    __shared__ uint32_t rows[64];
-    __shared__ uint32_t gid[64];
-    __shared__ float wts[64];
+    __shared__ uint32_t rows[kMaxG];
+    __shared__ uint32_t gid[kMaxG];
+    __shared__ float wts[kMaxG];
     const uint32_t t = blockIdx.x;
     griddep_wait();
     griddep_launch();
@@ -1129,27 +941,27 @@ __global__ void __launch_bounds__(256) combine_f64_kernel(const double* __restri
 
 void launch_router_linear(int dtype, const void* x, uint32_t T, uint32_t d, const float* wrT, uint32_t G,
                           uint32_t k_max, const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
-                          int* err, cudaStream_t s) {
+                          int* err, uint32_t* stats, cudaStream_t s) {
     const size_t smem = sizeof(double) * TB * G + sizeof(float) * (KC * (TB + 1) + KC * (GB + 4));
     const dim3 grid((T + TB - 1) / TB);
     if (dtype == 1) {
         auto kern = router_linear_kernel<__nv_bfloat16>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        func_attr_once(reinterpret_cast<const void*>(kern), (int)(sizeof(double) * TB * kMaxG + 16 * 1024));
         kern<<<grid, kRouterThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(x), T, d, wrT, G, k_max, kpt, k,
-                                                weight_mode, sel, w, err);
+                                                weight_mode, sel, w, err, stats);
     } else {
         auto kern = router_linear_kernel<float>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        func_attr_once(reinterpret_cast<const void*>(kern), (int)(sizeof(double) * TB * kMaxG + 16 * 1024));
         kern<<<grid, kRouterThreads, smem, s>>>(static_cast<const float*>(x), T, d, wrT, G, k_max, kpt, k,
-                                                weight_mode, sel, w, err);
+                                                weight_mode, sel, w, err, stats);
     }
 }
 
 void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                           const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
-                          double guard, uint32_t* flagged, cudaStream_t s) {
+                          const RouterGuard& rg, uint32_t* flagged, cudaStream_t s) {
     partials_topk_kernel<<<(T + 7) / 8, 256, 0, s>>>(partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w,
-                                                     err, guard, flagged);
+                                                     err, rg, flagged);
 }
 
 // In-place fixed-order reduction of the K-split router partials into plane 0
@@ -1177,44 +989,33 @@ void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G
 }
 
 void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
-                         const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, double guard,
-                         const void* x, uint32_t d, const float* wrT, uint32_t* ticket, uint32_t* n_fixed,
-                         BucketWs& ws, cudaStream_t s, uint32_t tb) {
+                         const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
+                         const RouterGuard& rg, const void* x, uint32_t d, const float* wrT, uint32_t* ticket,
+                         uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb) {
     const size_t smem = sizeof(double) * 2 * tb * G;
-    static bool attr_set[3] = {false, false, false};
-    auto launch = [&](auto kern, int which) {
-        if (!attr_set[which]) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(double) * 2 * TB * kMaxG));
-            // same shared-memory carveout as the GEMMs around it: no L1/smem
-            // reconfiguration between the kernels of the chain
-            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-            attr_set[which] = true;
-        }
+    auto launch = [&](auto kern) {
+        // same shared-memory carveout as the GEMMs around it: no L1/smem
+        // reconfiguration between the kernels of the chain
+        func_attr_once(reinterpret_cast<const void*>(kern), (int)(sizeof(double) * 2 * TB * kMaxG), true);
         launch_k(kern, dim3((T + tb - 1) / tb), dim3(1024), smem, s,
-            partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, guard,
-            static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, n_fixed, ws.lrank, ws.block_counts, ws.block_base,
+            partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, rg,
+            static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, stats, ws.lrank, ws.block_counts, ws.block_base,
             ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb);
     };
     if (G <= 64)
-        launch(route_bucket_kernel<2>, 0);
+        launch(route_bucket_kernel<2>);
     else if (G <= 128)
-        launch(route_bucket_kernel<4>, 1);
+        launch(route_bucket_kernel<4>);
     else
-        launch(route_bucket_kernel<8>, 2);
+        launch(route_bucket_kernel<8>);
 }
 
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
-                         const uint32_t* flagged, int num_sms, cudaStream_t s) {
+                         uint32_t* flagged, int num_sms, cudaStream_t s) {
     const size_t smem = sizeof(double) * d;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(router_fixup_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        cudaFuncSetAttribute(router_fixup_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    func_attr_once(reinterpret_cast<const void*>(router_fixup_kernel<__nv_bfloat16>), 200 * 1024);
+    func_attr_once(reinterpret_cast<const void*>(router_fixup_kernel<float>), 200 * 1024);
     if (dtype == 1)
         router_fixup_kernel<__nv_bfloat16><<<num_sms, 1024, smem, s>>>(static_cast<const __nv_bfloat16*>(x), d, wrT,
                                                                       G, k_max, kpt, k, weight_mode, sel, w, err,
@@ -1225,9 +1026,10 @@ void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT,
 }
 
 void launch_router_scores_topk(const float* scores, uint32_t T, uint32_t G, uint32_t k_max, const uint32_t* kpt,
-                               uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err, cudaStream_t s) {
+                               uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err, uint32_t* stats,
+                               cudaStream_t s) {
     scores_topk_kernel<<<(T + 7) / 8, 256, 0, s>>>(reinterpret_cast<const double*>(scores), T, G, k_max, kpt, k,
-                                                   weight_mode, sel, w, err);
+                                                   weight_mode, sel, w, err, stats);
 }
 
 void launch_bucket_local(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32_t G, BucketWs& ws,
@@ -1258,14 +1060,7 @@ void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t 
             return static_cast<uint32_t>(v < 1 ? 1 : v > 8 ? 8 : v);
         }();
         const size_t smem = wpc * (size_t)d * 2;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(8 * kBulkRowMax));
-            cudaFuncSetAttribute(dispatch_bulk_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared);
-            attr = true;
-        }
+        func_attr_once(reinterpret_cast<const void*>(dispatch_bulk_kernel), (int)(8 * kBulkRowMax), true);
         launch_k(dispatch_bulk_kernel, dim3((T + wpc - 1) / wpc), dim3(32 * wpc), smem, s,
             static_cast<const __nv_bfloat16*>(x), T, d, sel, w, k_max, G, ws.lrank, ws.block_base, ws.perm_tok,
             ws.perm_w, ws.slot_row, static_cast<__nv_bfloat16*>(x_perm), check_finite ? ws.err : nullptr, tb);

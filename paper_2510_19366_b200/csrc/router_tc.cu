@@ -7,12 +7,17 @@
 // every product x * plane is exact in the MMA and
 //     logits = x.hi + x.mid + x.lo
 // differs from the fp64 oracle only by the accumulation rounding (the MMA adds
-// into fp32 with truncation).  That is bounded by giving every 256-deep K
-// chunk its own fresh TMEM accumulators (one for the hi plane, one for mid+lo),
-// adding the chunk sums in fp64 in the epilogue, and -- because a bound is not
-// bit-exactness -- by re-selecting every token whose k-th/(k+1)-th gap is
-// within twice that bound from exact fp64 logits (route.cu
-// router_fixup_kernel): the selection is certified for every token.
+// into fp32).  Every 256-deep K chunk (64-deep for few token tiles) gets its
+// own fresh TMEM accumulators (one for the hi plane, one for mid+lo) and the
+// chunk sums are added in fp64 in the epilogue, so the error of a logit is at
+// most depth * 2^-23 * sum_i |x_i| |W_ig| (every fp32 addition inside a
+// chunk, however the MMA orders them, loses at most one ulp of a running sum
+// bounded by the chunk's sum of |products|; 2^-23 also covers truncation).
+// The kernel emits the per-token sum |x| of each K split for that bound
+// (route.cu warp_router_guard), and -- because a bound is not bit-exactness --
+// every token whose k-th/(k+1)-th gap is within twice its bound is re-selected
+// from exact fp64 logits (route.cu route_bucket_kernel / router_fixup_kernel):
+// the selection is certified for every token, at any input scale.
 // K is further split across CTAs (grid = token tiles x K splits ~ 148 CTAs);
 // the per-split fp64 partials are added in a fixed order by the top-k kernel
 // (deterministic, no atomics).  Warp roles and pipelines as in gemm_tc.cu.
@@ -30,7 +35,9 @@ constexpr uint32_t kMaxStages = 6;
 struct RouterTcParams {
     uint32_t T, Npad, kb_total, kb_per_split, stages, chunk_kb;
     uint32_t ncta, nsplit;  // columns per CTA, column splits (blockIdx.y = K split * nsplit + column split)
-    double* partial;        // [KS][T][Npad]
+    void* partial;          // [KS][T][Npad] fp64, or fp32 when out_f32 (rounded once per split)
+    double* xnorm;          // [KS][T] partial sums of |x| over each K split (the error bound's input)
+    uint32_t out_f32;
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -52,10 +59,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t kb0 = ksplit * p.kb_per_split;
     const uint32_t kb1 = min(kb0 + p.kb_per_split, p.kb_total);
 
+    // the column-split-0 CTA of a K split also sums |x| per token over its K
+    // range: its 4 epilogue warps (idle until the accumulators are complete)
+    // read each A stage before it is released, so a stage's empty barrier
+    // then waits for the MMA commit and those 4 warps
+    const bool do_norm = n0 == 0;
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], do_norm ? 5u : 1u);
         }
         mbar_init(tfull, 1);
         fence_mbar_init();
@@ -114,11 +126,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
     } else {
         const uint32_t q = warp & 3u;
+        if (do_norm) {
+            // row r of a stage's A tile is 128 contiguous bytes (SW128 permutes
+            // its 16-byte chunks, which a row sum does not care about)
+            double nrm = 0.0;
+            const uint32_t r = q * 32 + lane;
+            for (uint32_t kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
+                const uint32_t s = it % p.stages, ph = (it / p.stages) & 1u;
+                mbar_wait(&full[s], ph);
+                const uint4* row = reinterpret_cast<const uint4*>(base + s * stage_bytes + r * 128u);
+                float acc = 0.0f;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const uint4 v = row[c];
+                    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        acc += fabsf(__uint_as_float(wv[h] << 16));
+                        acc += fabsf(__uint_as_float(wv[h] & 0xFFFF0000u));
+                    }
+                }
+                nrm += static_cast<double>(acc);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            const uint32_t t = m0 + r;
+            if (t < p.T) p.xnorm[static_cast<size_t>(ksplit) * p.T + t] = nrm;
+        }
         mbar_wait(tfull, 0);
         tc_fence_after();
         const uint32_t t = m0 + q * 32 + lane;
         const uint32_t nchunks = (kb1 - kb0 + p.chunk_kb - 1) / p.chunk_kb;
-        double* out = p.partial + (static_cast<size_t>(ksplit) * p.T + t) * p.Npad + n0;
+        const size_t orow = (static_cast<size_t>(ksplit) * p.T + t) * p.Npad + n0;
         for (uint32_t grp = 0; grp < p.ncta / 32 && n0 + grp * 32 < p.Npad; ++grp) {
             double acc[32];
 #pragma unroll
@@ -133,10 +172,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 32; ++i)
                     acc[i] += static_cast<double>(__uint_as_float(rh[i])) + static_cast<double>(__uint_as_float(rl[i]));
             }
-            if (t < p.T) {
+            if (t < p.T && p.out_f32) {
+                float* out = static_cast<float*>(p.partial) + orow + grp * 32;
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                    *reinterpret_cast<float4*>(out + i) = make_float4(static_cast<float>(acc[i]), static_cast<float>(acc[i + 1]),
+                                                                      static_cast<float>(acc[i + 2]), static_cast<float>(acc[i + 3]));
+            } else if (t < p.T) {
+                double* out = static_cast<double*>(p.partial) + orow + grp * 32;
 #pragma unroll
                 for (int i = 0; i < 32; i += 2)
-                    *reinterpret_cast<double2*>(out + grp * 32 + i) = make_double2(acc[i], acc[i + 1]);
+                    *reinterpret_cast<double2*>(out + i) = make_double2(acc[i], acc[i + 1]);
             }
         }
     }
@@ -166,7 +212,48 @@ __global__ void split_router_kernel(const float* __restrict__ wr, uint32_t d, ui
     }
 }
 
+// Two fp32 row blocks ([n_a][d] then [n_b][d], row-major) -> three bf16 planes
+// [3][Npad][d]: the proxy router's gate and up columns of its gate neurons.
+__global__ void split_rows_kernel(const float* __restrict__ ra, const float* __restrict__ rb, uint32_t n_a,
+                                  uint32_t n_b, uint32_t d, uint32_t Npad, __nv_bfloat16* __restrict__ planes) {
+    const size_t n = static_cast<size_t>(Npad) * d;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n; q += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t g = q / d, i = q % d;
+        const float w = g < n_a ? ra[q] : (g < n_a + n_b ? rb[static_cast<size_t>(g - n_a) * d + i] : 0.0f);
+        const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+        const float r1 = w - __bfloat162float(hi);
+        const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+        const float r2 = r1 - __bfloat162float(mid);
+        planes[q] = hi;
+        planes[n + q] = mid;
+        planes[2 * n + q] = __float2bfloat16_rn(r2);
+    }
+}
+
 }  // namespace
+
+void launch_split_rows(const float* ra, const float* rb, uint32_t n_a, uint32_t n_b, uint32_t d, uint32_t Npad,
+                       void* planes, cudaStream_t s) {
+    split_rows_kernel<<<592, 256, 0, s>>>(ra, rb, n_a, n_b, d, Npad, static_cast<__nv_bfloat16*>(planes));
+}
+
+size_t router_tc_partial_rows(uint32_t max_T, uint32_t d, uint32_t G, int num_sms) {
+    size_t best = 0;
+    for (uint32_t m = 1; (m - 1) * BM < max_T; ++m) {
+        const uint32_t T = m * BM < max_T ? m * BM : max_T;
+        const RouterTcPlan pl = plan_router_tc(T, d, G, num_sms);
+        const size_t rows = static_cast<size_t>(pl.ks) * T;
+        if (rows > best) best = rows;
+    }
+    return best;
+}
+
+// chunk depth x 2^-23 per unit of sum|x| max|W|, times 1.02 for the mid/lo
+// accumulator (2 x depth additions of terms <= 2^-8 |x W|) and the fp32 |x|
+// sums (relative error < 2^-16), and max|hi| <= max|W| (1 + 2^-9).
+double router_guard_coef(uint32_t chunk_depth, float wmax) {
+    return static_cast<double>(chunk_depth) * 0x1.0p-23 * 1.02 * static_cast<double>(wmax);
+}
 
 uint32_t router_tc_cols_per_cta(uint32_t G) {
     const uint32_t npad = ((G + 31) / 32) * 32;
@@ -212,13 +299,10 @@ void launch_split_router(const float* wr, uint32_t d, uint32_t G, uint32_t Npad,
 }
 
 void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const RouterTcPlan& pl, uint32_t T,
-                      double* partial, cudaStream_t s) {
-    RouterTcParams p{T, pl.Npad, pl.kb_total, pl.kb_per_split, pl.stages, pl.chunk_kb, pl.ncta, pl.nsplit, partial};
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr_set = true;
-    }
+                      void* partial, double* xnorm, cudaStream_t s, bool out_f32) {
+    RouterTcParams p{T,       pl.Npad,   pl.kb_total, pl.kb_per_split, pl.stages, pl.chunk_kb, pl.ncta, pl.nsplit,
+                     partial, xnorm, out_f32 ? 1u : 0u};
+    func_attr_once(reinterpret_cast<const void*>(router_tc_kernel), 227 * 1024);
     launch_k(router_tc_kernel, dim3(pl.m_tiles, pl.ks * pl.nsplit), dim3(kThreads), pl.smem, s, *tmX, *tmW, p);
 }
 

@@ -205,6 +205,12 @@ class MoeLayer:
         check(self.lib.mp_layer_route(self.h, _ptr(x), T, _ptr(kpt), k, _ptr(sel), _ptr(w), _stream_handle(stream)))
         return sel, w
 
+    def route_stats(self, stream=None):
+        """(tokens re-selected from exact fp64 logits, near ties with exact gap < 1e-6) of the last forward."""
+        r, n = C.c_uint32(), C.c_uint32()
+        check(self.lib.mp_layer_route_stats(self.h, C.byref(r), C.byref(n), _stream_handle(stream)))
+        return r.value, n.value
+
     def check_errors(self, stream=None):
         check(self.lib.mp_layer_check_errors(self.h, _stream_handle(stream)))
 

@@ -179,6 +179,27 @@ int main() {
         }
         std::printf("PASS acceptance C1 (30 trials)\n");
     }
+    {  // reference-valid partitions with more than 64 / more than 256 sub-experts
+        for (std::uint32_t n : {100u, 300u}) {
+            const std::size_t d = 16, ff = 3 * n + 7;
+            const ToyExpert e = random_expert(d, ff, 70 + n);
+            const Partition p = random_balanced_partition(ff, n, 80 + n);
+            std::mt19937_64 rng(90 + n);
+            std::vector<float> x(d);
+            for (auto& v : x) v = static_cast<float>(uniform01(rng) * 2.0 - 1.0);
+            std::vector<std::uint32_t> act;
+            for (std::uint32_t s2 = 0; s2 < n; s2 += 3) act.push_back(s2);
+            act.push_back(n - 1);
+            std::vector<std::uint32_t> all(n);
+            std::iota(all.begin(), all.end(), 0u);
+            const auto y = partitioned_forward(e, p, x, act);
+            const auto want = part_sum(e, p, x, act);
+            const auto ya = partitioned_forward(e, p, x, all);
+            const auto wa = part_sum(e, p, x, all);
+            for (std::size_t i = 0; i < d; ++i) CHECK(close(y[i], want[i]) && close(ya[i], wa[i]));
+        }
+        std::printf("PASS partitions with 100 and 300 sub-experts\n");
+    }
     {  // MoeLayer: unit weights, every sub-expert of 2 experts (k = E*S) == sum of full experts
         LayerConfig c;
         c.n_experts = 2;
