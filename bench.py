@@ -169,12 +169,14 @@ def build_layer(local, T, k_max):
 
 def build_ep_layer(local, rank, world, T, k_max=16, transport="nccl", force_collectives=False):
     """Expert-parallel layer: E/world parent experts on this rank,
-    the router replicated, tokens exchanged by NCCL all-to-all."""
+    the router replicated.  transport "nccl": the C++ host path (mp_ep_forward,
+    the library's own NCCL communicator); "torch": the same protocol driven
+    from Python with torch.distributed all-to-alls; "p2p": peer-memory stores."""
     import torch
     from paper_2510_19366_b200 import synth_fill
-    from paper_2510_19366_b200.ep import CudaEpOps, ExpertParallelLayer
-    if E % world:
-        raise SystemExit(f"--gpus {world} must divide the {E} experts")
+    from paper_2510_19366_b200.ep import CudaEpOps, ExpertParallelLayer, NcclExpertParallelLayer
+    if (E * S) % world:
+        raise SystemExit(f"--gpus {world} must divide the {E * S} sub-experts")
     ops = CudaEpOps(E, S, D, FF, rank, world, dtype="bf16", k_max=k_max, max_tokens=T, device=local)
     buf = [torch.empty(D * FF, dtype=torch.float32, device="cuda") for _ in range(3)]
     for e in range(E):
@@ -198,7 +200,83 @@ def build_ep_layer(local, rank, world, T, k_max=16, transport="nccl", force_coll
     if transport == "p2p":
         from paper_2510_19366_b200.ep import PeerExpertParallelLayer
         return PeerExpertParallelLayer(ops), ops, xs
-    return ExpertParallelLayer(ops, force_collectives=force_collectives), ops, xs
+    if transport == "torch":
+        return ExpertParallelLayer(ops, force_collectives=force_collectives), ops, xs
+    return NcclExpertParallelLayer(ops), ops, xs
+
+
+def bench_stack_ep(pk, local, rank, world, n_layers=32, T=4096, ks=(2, 8), steps=10):
+    """BASELINE configs[2] / SURVEY 8(d) C3: the Mixtral 32-layer MoE stack,
+    expert-parallel over the ranks (E*S/world sub-experts of every layer per
+    GPU, 90/world GB of weights), x_{l+1} = x_l + MoE_l(x_l) with the residual
+    fused into the combine, T tokens per GPU (weak scaling).  Every layer runs
+    through mp_ep_forward on one shared expert-parallel handle (one NCCL
+    communicator); the layers' token scratch is shared (MP_LAYER_SHARED_SCRATCH)."""
+    import ctypes as C
+    import torch
+    from paper_2510_19366_b200 import MoeLayer, _lib, synth_fill
+    from paper_2510_19366_b200._lib import (MP_EP_RESIDUAL, MP_LAYER_EXPERTS_ONLY, MP_LAYER_ROUTER_ONLY,
+                                            MP_LAYER_SHARED_SCRATCH, check)
+    from paper_2510_19366_b200.layer import _ptr, _stream_handle
+    lib = _lib.load()
+    G = E * S
+    per_rank = G // world
+    first_e, last_e = per_rank * rank // S, (per_rank * (rank + 1) - 1) // S
+    k_max = max(ks)
+    routers, experts = [], []
+    buf = [torch.empty(D * FF, dtype=torch.float32, device="cuda") for _ in range(3)]
+    for l in range(n_layers):
+        R = MoeLayer(E, S, D, FF, dtype="bf16", k_max=k_max, max_tokens=T, device=local,
+                     flags=MP_LAYER_ROUTER_ONLY)
+        X = MoeLayer(last_e - first_e + 1, S, D, FF, dtype="bf16", weights="softmax_renorm", k_max=k_max,
+                     max_tokens=T * world, device=local, flags=MP_LAYER_EXPERTS_ONLY | MP_LAYER_SHARED_SCRATCH)
+        for e in range(first_e, last_e + 1):
+            for m, (seed, scale) in enumerate(((100 + 3 * e, 1 / math.sqrt(D)), (101 + 3 * e, 1 / math.sqrt(D)),
+                                               (102 + 3 * e, 1 / math.sqrt(FF)))):
+                synth_fill(buf[m], seed + 7919 * l, scale)
+            X.set_partition(e - first_e, balanced_partition(FF, S, 6000 + e + 64 * l))
+            X.load_expert(e - first_e, *buf)
+        synth_fill(buf[0][:D * G], 7 + 7919 * l, 1 / math.sqrt(D))
+        R.set_router(buf[0][:D * G])
+        routers.append(R)
+        experts.append(X)
+    del buf
+    ep = C.c_void_p()
+    check(lib.mp_ep_create_subexpert(world, rank, per_rank, S, D, k_max, T, 1, local, C.byref(ep)))
+    uid = (C.c_uint8 * 128)()
+    if rank == 0:
+        check(lib.mp_ep_nccl_unique_id(uid))
+    if _dist_on():
+        import torch.distributed as dist
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+    check(lib.mp_ep_nccl_init(ep, uid))
+    xa = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
+    synth_fill(xa, 11 + 100000 * rank, 1.0)
+    xb = torch.empty_like(xa)
+    out = []
+    for k in ks:
+        def step(i, k=k):
+            x, y = xa, xb
+            for R, X in zip(routers, experts):
+                check(lib.mp_ep_forward(ep, R.h, X.h, _ptr(x), T, None, k, _ptr(y), MP_EP_RESIDUAL,
+                                        _stream_handle(None)))
+                x, y = y, x
+        ms = time_steps(step, steps, 3, world)
+        F = n_layers * 6.0 * D * W_SUB * T * k * world
+        B = n_layers * (G * 3.0 * D * W_SUB * 2 + 2.0 * T * world * D * 2)
+        r = roofline_fb(F, B, ms, {**pk, "bf16_tflops_sustained": pk["bf16_tflops_sustained"] * world,
+                                   "hbm_gbs": pk["hbm_gbs"] * world})
+        out.append({"k": k, "tokens_per_s": world * T / (ms * 1e-3), "ms_per_pass": ms, "roofline": r})
+    lib.mp_ep_destroy(ep)
+    for L in routers + experts:
+        L.close()
+    torch.cuda.synchronize()
+    return {"workload": f"Mixtral-8x7B {n_layers}-layer MoE stack, expert-parallel over {world} GPU(s) (BASELINE "
+                        f"configs[2]), {T} tokens per GPU (weak), residual fused, C++ NCCL transport "
+                        "(mp_ep_forward), shared layer scratch",
+            "weights_gb_per_gpu": n_layers * per_rank * 3 * D * W_SUB * 2 / 1e9, "sweep": out}
 
 
 def balanced_partition(n, n_sub, seed):
@@ -401,6 +479,68 @@ def bench_mixed_qos_32k(L32, pk, steps=10):
             "mean_k": kk, "tokens_per_s": T / (ms * 1e-3), "ms_per_step": ms, "roofline": roofline_fb(F, B, ms, pk)}
 
 
+def bench_c1_gpu(pk, steps=50):
+    """BASELINE configs[0] / SURVEY 8(d) C1 on the GPU: the toy layer (8 experts
+    x 4 sub-experts, d=512, ffn=1024, k=4, 256 tokens), fp32 (reference-exact
+    mode) and bf16, weights U(-1,1) from the counter-based stream."""
+    import torch
+    from paper_2510_19366_b200 import MoeLayer, synth_fill
+    Ec, Sc, dc, ffc, Tc, kc = 8, 4, 512, 1024, 256, 4
+    out = {}
+    for dt in ("f32", "bf16"):
+        L = MoeLayer(Ec, Sc, dc, ffc, dtype=dt, k_max=kc, max_tokens=Tc)
+        buf = [torch.empty(dc * ffc, dtype=torch.float32, device="cuda") for _ in range(3)]
+        for e in range(Ec):
+            for m in range(3):
+                synth_fill(buf[m], 5000 + 3 * e + m, 1.0)
+            L.set_partition(e, balanced_partition(ffc, Sc, 6000 + e))
+            L.load_expert(e, *buf)
+        L.set_router(synth_fill(torch.empty(dc * Ec * Sc, dtype=torch.float32, device="cuda"), 7, 1 / math.sqrt(dc)))
+        xs = [synth_fill(torch.empty((Tc, dc), dtype=L.torch_dtype, device="cuda"), 11 + i, 1.0) for i in range(4)]
+        y = torch.empty((Tc, dc), dtype=L.torch_dtype, device="cuda")
+        ms = time_steps(lambda i: L.forward(xs[i % 4], k=kc, y=y), steps, 3, 1)
+        out[dt] = {"tokens_per_s": Tc / (ms * 1e-3), "ms_per_step": ms}
+        L.close()
+    return {"workload": "C1 toy layer (BASELINE configs[0]) on the GPU: 8 experts x 4 sub-experts, d=512, "
+                        "ffn=1024, k=4, 256 tokens; fp32 = reference-exact fp64-accumulating SIMT path, "
+                        "bf16 = tcgen05 path (launch-bound at this size)", **out}
+
+
+def bench_proxy(pk, T=4096, k=8, r=4, steps=30):
+    """the proxy-gate router at the Mixtral layer shape (r = 4
+    gate neurons per sub-expert, E*S*r = 256 gate neurons): tensor-core
+    gate/up columns with certified selection.  Route-only and full-layer
+    times, and how many tokens the certification sent to the exact pass."""
+    import numpy as np
+    import torch
+    from paper_2510_19366_b200 import MoeLayer, synth_fill
+    L = MoeLayer(E, S, D, FF, dtype="bf16", router="proxy", k_max=16, max_tokens=T)
+    buf = [torch.empty(D * FF, dtype=torch.float32, device="cuda") for _ in range(3)]
+    rng = np.random.default_rng(21)
+    for e in range(E):
+        for m, (seed, scale) in enumerate(((100 + 3 * e, 1 / math.sqrt(D)), (101 + 3 * e, 1 / math.sqrt(D)),
+                                           (102 + 3 * e, 1 / math.sqrt(FF)))):
+            synth_fill(buf[m], seed, scale)
+        part = balanced_partition(FF, S, 6000 + e)
+        L.set_partition(e, part)
+        L.load_expert(e, *buf)
+        L.set_gates(e, r, [sorted(rng.choice(np.flatnonzero(part == s), r, replace=False).tolist())
+                           for s in range(S)])
+    del buf
+    xs = [synth_fill(torch.empty((T, D), dtype=torch.bfloat16, device="cuda"), 11 + 1000 * i, 1.0) for i in range(4)]
+    y = torch.empty((T, D), dtype=torch.bfloat16, device="cuda")
+    ms_route = time_steps(lambda i: L.route(xs[i % 4], k=k), steps, 3, 1)
+    resel, near = L.route_stats()
+    ms_fwd = time_steps(lambda i: L.forward(xs[i % 4], k=k, y=y), steps, 3, 1)
+    L.close()
+    torch.cuda.synchronize()
+    F = 3 * 2.0 * 2 * E * S * r * D * T  # three bf16 planes of the 2 E S r gate/up columns
+    return {"workload": f"proxy-gate router, Mixtral layer shape, {E * S * r} gate neurons (r={r}), T={T}, k={k}",
+            "route_ms": ms_route, "route_tokens_per_s": T / (ms_route * 1e-3), "route_tc_tflops": F / (ms_route * 1e-3) / 1e12,
+            "forward_ms": ms_fwd, "forward_tokens_per_s": T / (ms_fwd * 1e-3),
+            "reselected_exact": resel, "near_ties_lt_1e-6": near}
+
+
 def bench_offload(T=16, k=2, cache_units=32, steps=20):
     """SURVEY 8(f).4 at the Mixtral shape: decode batches of T tokens on a
     layer whose packed weights live in pinned host memory, with a device
@@ -593,6 +733,37 @@ def cpu_reference_sample(k, T_sample, nthreads, seed_tokens=11):
     return T_sample / dt, kind, dt
 
 
+def cpu_reference_c1(nthreads):
+    """BASELINE configs[0] / SURVEY 8(d) C1 timed in full on the reference CPU
+    path: toy layer fp32, 8 experts x 4 sub-experts, d=512, ffn=1024, k=4,
+    256 tokens (reference fixtures: random_expert, random_balanced_partition,
+    W_r = U(-1,1)/sqrt(d), x = U(-1,1))."""
+    import numpy as np
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import Oracle, RefLayer, RefLib, have_ref
+    orc = Oracle()
+    Ec, Sc, dc, ffc, Tc, kc = 8, 4, 512, 1024, 256, 4
+    experts = [orc.random_expert(dc, ffc, 5000 + e) for e in range(Ec)]
+    parts = [orc.random_balanced_partition(ffc, Sc, 6000 + e) for e in range(Ec)]
+    wr = orc.uniform_pm1(7, dc * Ec * Sc, 1.0 / math.sqrt(dc))
+    x = orc.uniform_pm1(11, Tc * dc).reshape(Tc, dc)
+    t0 = time.perf_counter()
+    if have_ref():
+        rl = RefLayer(RefLib(), experts, parts, Sc)
+        sel, w = rl.route(x, wr, kc, kc, 1)
+        y = rl.forward(x, sel, w, 1, nthreads=nthreads)
+        kind = "reference"
+    else:
+        logits = orc.router_logits(x, wr, Tc, dc, Ec * Sc)
+        sel, w, _ = orc.route(logits, kc, kc, 1)
+        y = orc.layer_forward(experts, parts, Sc, x, sel, w, 1, nthreads=nthreads)
+        kind = "port"
+    dt = time.perf_counter() - t0
+    assert np.isfinite(y).all()
+    return {"value": Tc / dt, "unit": "tokens/s", "cores": nthreads, "kind": kind, "seconds": dt,
+            "sample": "C1 toy layer in full: 256 tokens, k=4, 8x4 sub-experts, d=512, ffn=1024, fp32"}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -625,7 +796,7 @@ def run_reference_arm(args, world, rank):
                              "sample": f"{T_sample} tokens per step (one per thread), k={args.k}, "
                                        f"Mixtral layer shape fp32 weights; CPU {cpu_model()}"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def workload_config(args, world):
@@ -634,7 +805,8 @@ def workload_config(args, world):
             "d_model": D, "d_ff": FF, "experts": E, "subexperts_per_expert": S, "tokens_per_gpu": args.tokens,
             "k": args.k, "global_tokens": args.tokens * world,
             "parallelism": ((f"ep{world} (experts sharded, "
-                             + ("peer-memory stores" if args.ep_transport == "p2p" else "NCCL all-to-all") + ")")
+                             + {"p2p": "peer-memory stores", "torch": "torch.distributed NCCL all-to-all",
+                                "nccl": "C++ host, NCCL all-to-allv (mp_ep_forward)"}[args.ep_transport] + ")")
                             if world > 1 or args.force_ep else "single"),
             "l2": f"x rotates over {N_XBUF} buffers ({N_XBUF * args.tokens * D * 2 / 1e6:.0f} MB) + 2.8 GB weights, "
                   "both > 126 MB L2"}
@@ -644,22 +816,38 @@ def use_ep_flag(args, world):
     return world > 1 or args.force_ep
 
 
+_OUT = None
+
+
+def emit(line):
+    """The one JSON line on stdout (bench contract); everything else the
+    process prints -- NCCL's version banner, library diagnostics -- goes to
+    stderr (main() moves fd 1 there)."""
+    print(json.dumps(line), file=_OUT or sys.stdout, flush=True)
+
+
 def main():
+    global _OUT
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--tokens", type=int, default=4096)
-    ap.add_argument("--sweep", default="2,4,8,16")
+    ap.add_argument("--sweep", default=",".join(str(k) for k in range(2, 17)))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-ep", action="store_true", help="run the expert-parallel path even at N=1 (loopback)")
     ap.add_argument("--force-dist", action="store_true",
                     help="N=1 with a 1-rank NCCL process group and the expert-parallel path through real NCCL "
                          "collectives (the multi-rank code path on one GPU)")
-    ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "p2p"],
-                    help="N>1 token exchange: NCCL all-to-all, or direct peer-memory stores (CUDA IPC / NVLink)")
+    ap.add_argument("--ep-transport", default="nccl", choices=["nccl", "torch", "p2p"],
+                    help="N>1 token exchange: the C++ NCCL path (mp_ep_forward, default), the same protocol with "
+                         "torch.distributed all-to-alls, or direct peer-memory stores (CUDA IPC / NVLink)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the other BASELINE configs (Qwen shape, 32-layer stack, 32k mixed-QoS batch) "
                          "and the calibration timing")
@@ -696,6 +884,8 @@ def main():
         layers = [ops.router, ops.local]
 
         def fwd(x, k, kpt, y=None):
+            if args.ep_transport == "nccl":
+                return ep_layer.forward(x, k=k, k_per_token=kpt, y=y)
             return ep_layer.forward(x, k=k, k_per_token=kpt)
     touched = E * S // world  # sub-experts whose weights this GPU streams (all receive tokens at 4096/GPU)
 
@@ -709,9 +899,18 @@ def main():
     ms = time_steps(step, args.steps, args.warmup, world)
     launches = (sum(x.launch_count() for x in layers) - n0) // (args.steps + args.warmup) * args.steps
     if use_ep:
-        # mp_ep_plan (4 kernels), pack, combine (+ the peer-memory return kernel) per step
-        launches += (7 if args.ep_transport == "p2p" else 6) * args.steps
+        # plan (4 kernels), pack, combine (+ the count kernel of mp_ep_forward / the
+        # peer-memory return kernel) per step
+        launches += (6 if args.ep_transport == "torch" else 7) * args.steps
     value = world * T / (ms * 1e-3)
+    # steady state: a driver run of a few steps sits at burst clocks; the
+    # serving figure is a long loop under the 1000 W cap
+    steady = None
+    if args.steps < 300:
+        n_ss = 600
+        ms_ss = time_steps(step, n_ss, 3, world)
+        steady = {"steps": n_ss, "ms_per_step": ms_ss, "value": world * T / (ms_ss * 1e-3), "unit": "tokens/s",
+                  "layer_roofline": layer_roofline(T, args.k, ms_ss, pk, touched)}
 
     # per-stage device times (CUDA events on the forward's stream), the sweep
     sweep_out = []
@@ -727,8 +926,10 @@ def main():
         msk = time_steps(lambda i: step(i, k=0 if kpt is not None else k, kpt=kpt), max(args.steps // 2, 10), 3,
                          world)
         per_step = stage_profile(layers, fwd, xs, 0 if kpt is not None else k, kpt=kpt)
+        resel, near = layers[0].route_stats()  # the last forward's routing (4096 tokens)
         ent = {"k": k, "tokens_per_s": world * T / (msk * 1e-3), "ms_per_step": msk,
-               "layer_roofline": layer_roofline(T, kk, msk, pk, touched), "stages_ms": per_step}
+               "layer_roofline": layer_roofline(T, kk, msk, pk, touched), "stages_ms": per_step,
+               "routing": {"tokens": T, "reselected_exact": resel, "near_ties_lt_1e-6": near}}
         if k != "mixed":
             ent["kernel_roofline"] = kernel_roofline(per_step, T, k, pk, touched)
         sweep_out.append(ent)
@@ -779,9 +980,20 @@ def main():
     clk = clocks.stop()  # sampled across the main timed loop, the k sweep and the e2e loop
 
     other = None
+    if use_ep and not args.no_extras:
+        # C3: the 32-layer stack, expert-parallel over the ranks (C5's mixed-QoS
+        # tiers at 4096 tokens per GPU are the sweep's "mixed" entry)
+        for x in layers:
+            x.close()
+        ops.close()
+        layers = []
+        torch.cuda.empty_cache()
+        other = {"stack32_ep": bench_stack_ep(pk, local, rank, world)}
     if extras:
         other = {"mixed_qos_32k": bench_mixed_qos_32k(L, pk)}
         other["qwen"] = bench_qwen(pk)
+        other["c1_toy_gpu"] = bench_c1_gpu(pk)
+        other["proxy_router"] = bench_proxy(pk)
         L.close()
         layers = []
         torch.cuda.empty_cache()
@@ -797,6 +1009,10 @@ def main():
             cpu = {"value": v, "unit": "tokens/s", "cores": nthreads, "kind": kind,
                    "sample": f"{nthreads} tokens (one per thread), k={args.k}, Mixtral layer shape, fp32 weights, "
                              f"{dt:.1f} s; CPU {cpu_model()}"}
+            v1, kind1, dt1 = cpu_reference_sample(args.k, 1, 1, seed_tokens=12)
+            cpu["one_thread"] = {"value": v1, "unit": "tokens/s", "cores": 1, "kind": kind1,
+                                 "sample": f"1 token, k={args.k}, Mixtral layer shape, {dt1:.1f} s"}
+            cpu["c1_full"] = {"threads_1": cpu_reference_c1(1), f"threads_{nthreads}": cpu_reference_c1(nthreads)}
         except Exception as exc:  # report, never fabricate
             cpu = {"value": None, "unit": "tokens/s", "cores": nthreads, "kind": None, "sample": f"failed: {exc}"}
 
@@ -810,14 +1026,14 @@ def main():
                 "roofline": kernel_roofline(stages_main, T, args.k, pk, touched),
                 "layer_roofline": layer_roofline(T, args.k, ms, pk, touched),
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-                "stages_ms": stages_main, "sweep": sweep_out}
+                "stages_ms": stages_main, "sweep": sweep_out, "steady_state": steady}
         if not use_ep:
             line["stage_roofline"] = stage_rooflines(stages_main, T, args.k, pk)
         if other:
             line["other_configs"] = other
         if main_k:
             line["roofline"] = main_k.get("kernel_roofline", line["roofline"])
-        print(json.dumps(line), flush=True)
+        emit(line)
     for x in layers:
         x.close()
     if _dist_on():

@@ -84,6 +84,11 @@ typedef struct {
  * on the tokens received from all ranks. */
 #define MP_LAYER_ROUTER_ONLY 1u  /* no expert storage; mp_layer_route only */
 #define MP_LAYER_EXPERTS_ONLY 2u /* no router; mp_layer_forward_selected only */
+/* The per-forward token scratch (permuted rows, SwiGLU activations, expert
+ * outputs: GBs at serving sizes) comes from a per-device pool shared by every
+ * layer with this flag and the same shapes -- for layer stacks whose layers
+ * run one after the other on one stream (32 layers). */
+#define MP_LAYER_SHARED_SCRATCH 4u
 
 /* Library / device info.  mp_device_check fails (3) unless device `dev` is an
  * sm_100 part this build has code for. */
@@ -237,6 +242,32 @@ mp_status mp_ep_pack(mp_ep_t ep, const void* x, const uint32_t* sel, const float
                      void* send_x, uint32_t* send_sel, float* send_w, void* stream);
 /* back: device [sum(send_counts) x d] partial outputs (dtype), in send order. */
 mp_status mp_ep_combine(mp_ep_t ep, const void* back, uint32_t n_tokens, void* y, void* stream);
+
+/* ---- expert-parallel layer forward with an NCCL transport (C++ host) ----
+ * The whole layer on this rank's tokens in one call, no Python on the path:
+ *   mp_layer_route (router: a MP_LAYER_ROUTER_ONLY layer, replicated) ->
+ *   plan (destination ranks per token, deduplicated) -> count matrix
+ *   (ncclAllGather; the layer's one host synchronisation -- NCCL needs the
+ *   all-to-allv sizes on the host) -> pack -> rows + selections + weights by
+ *   grouped ncclSend/ncclRecv (all-to-allv over NVLink/NVSwitch) ->
+ *   mp_layer_forward_selected (experts: this rank's MP_LAYER_EXPERTS_ONLY
+ *   layer, max_tokens >= world * ep max_tokens) -> partials returned the same
+ *   way -> combine in ascending rank order (deterministic).
+ * The communicator: rank 0 calls mp_ep_nccl_unique_id, the host runtime
+ * broadcasts the 128 bytes (MPI, a TCP store, torch.distributed), every rank
+ * calls mp_ep_nccl_init (collective).  NCCL is loaded at run time
+ * (libnccl.so.2; the process's own copy when one is loaded).
+ * flags: MP_EP_RESIDUAL -> y = x + MoE(x) (layer stacks).
+ * x, y: device [n_tokens x d_model] of the ep dtype; k_per_token: device or
+ * NULL.  mp_ep_last_counts: rows sent to / received from each rank by the
+ * last mp_ep_forward (host arrays of `world` entries, either may be NULL). */
+#define MP_EP_NCCL_ID_BYTES 128
+#define MP_EP_RESIDUAL 1u
+mp_status mp_ep_nccl_unique_id(uint8_t* id);
+mp_status mp_ep_nccl_init(mp_ep_t ep, const uint8_t* id);
+mp_status mp_ep_forward(mp_ep_t ep, mp_layer_t router, mp_layer_t experts, const void* x, uint32_t n_tokens,
+                        const uint32_t* k_per_token, uint32_t k, void* y, uint32_t flags, void* stream);
+mp_status mp_ep_last_counts(mp_ep_t ep, uint32_t* send_rows, uint32_t* recv_rows);
 
 /* ---- Sub-expert offload cache (the reference simulates it:
  * cache_step / run_offload_sim, inc/offload.hpp:202-290). ----

@@ -130,6 +130,7 @@ struct LayerConfig {
     std::uint32_t k_max = 16;
     std::uint32_t max_tokens = 4096;
     int device = 0;
+    std::uint32_t flags = 0;  // MP_LAYER_ROUTER_ONLY / MP_LAYER_EXPERTS_ONLY (expert parallelism)
 };
 
 namespace detail {
@@ -163,7 +164,7 @@ public:
     explicit MoeLayer(const LayerConfig& c) : cfg_(c) {
         const mp_layer_desc d{c.n_experts, c.n_subexperts, c.d_model, c.d_ff, static_cast<std::uint32_t>(c.dtype),
                               static_cast<std::uint32_t>(c.router), static_cast<std::uint32_t>(c.weights), c.k_max,
-                              c.max_tokens, c.device, 0u};
+                              c.max_tokens, c.device, c.flags};
         detail::check(mp_layer_create(&d, &h_));
     }
     ~MoeLayer() {
@@ -280,6 +281,83 @@ private:
     mp_layer_t h_ = nullptr;
 };
 
+// One rank of an expert-parallel layer on the C++ host: the
+// replicated router, this rank's contiguous range of sub-experts, and the
+// NCCL transport (moe_layer.h mp_ep_forward).  Rank r of `world` owns global
+// sub-experts [r * G / world, (r + 1) * G / world) -- whole experts when
+// world divides E, else sub-expert granularity.  Typical use:
+//   ExpertParallelLayer ep(cfg, world, rank);
+//   std::array<std::uint8_t, MP_EP_NCCL_ID_BYTES> id{};
+//   if (rank == 0) id = ExpertParallelLayer::unique_id();
+//   broadcast(id);                  // MPI_Bcast / a TCP store / ...
+//   ep.connect(id);                 // collective
+//   for e owned: ep.load_expert(e, ...); ep.set_partition(e, ...);
+//   ep.set_router(w_r);
+//   ep.forward_device(x, T, k, y, stream);
+class ExpertParallelLayer {
+public:
+    ExpertParallelLayer(const LayerConfig& c, std::uint32_t world, std::uint32_t rank)
+        : cfg_(c), world_(world), rank_(rank), per_rank_(shard(c, world, rank)),
+          first_e_(per_rank_ * rank / c.n_subexperts), last_e_((per_rank_ * (rank + 1) - 1) / c.n_subexperts),
+          router_(role(c, MP_LAYER_ROUTER_ONLY, 0, 0)), experts_(role(c, MP_LAYER_EXPERTS_ONLY, first_e_, last_e_)) {
+        detail::check(mp_ep_create_subexpert(world, rank, per_rank_, c.n_subexperts, c.d_model, c.k_max, c.max_tokens,
+                                             static_cast<std::uint32_t>(c.dtype), c.device, &ep_));
+    }
+    ~ExpertParallelLayer() {
+        if (ep_) mp_ep_destroy(ep_);
+    }
+    ExpertParallelLayer(const ExpertParallelLayer&) = delete;
+    ExpertParallelLayer& operator=(const ExpertParallelLayer&) = delete;
+
+    static std::vector<std::uint8_t> unique_id() {
+        std::vector<std::uint8_t> id(MP_EP_NCCL_ID_BYTES);
+        detail::check(mp_ep_nccl_unique_id(id.data()));
+        return id;
+    }
+    void connect(std::span<const std::uint8_t> id) {
+        if (id.size() != MP_EP_NCCL_ID_BYTES) throw ValidationError("NCCL unique id must be 128 bytes");
+        detail::check(mp_ep_nccl_init(ep_, id.data()));
+    }
+    bool owns(std::uint32_t e) const { return e >= first_e_ && e <= last_e_; }
+    void load_expert(std::uint32_t e, const ToyExpert& x) {
+        if (owns(e)) experts_.load_expert(e - first_e_, x);
+    }
+    void set_partition(std::uint32_t e, const Partition& p) {
+        if (owns(e)) experts_.set_partition(e - first_e_, p);
+    }
+    void set_router(std::span<const float> w_r) { router_.set_router(w_r); }
+    // x, y: device [T x d_model] of the layer dtype; residual: y = x + MoE(x)
+    void forward_device(const void* x, std::uint32_t T, std::uint32_t k, void* y, void* stream = nullptr,
+                        const std::uint32_t* k_per_token_dev = nullptr, bool residual = false) {
+        detail::check(mp_ep_forward(ep_, router_.handle(), experts_.handle(), x, T, k_per_token_dev, k, y,
+                                    residual ? MP_EP_RESIDUAL : 0u, stream));
+    }
+    mp_ep_t handle() const { return ep_; }
+
+private:
+    static std::uint32_t shard(const LayerConfig& c, std::uint32_t world, std::uint32_t rank) {
+        const std::uint32_t G = c.n_experts * c.n_subexperts;
+        if (world < 1 || rank >= world || G % world)
+            throw ValidationError("the E*S sub-experts must shard evenly over the ranks");
+        return G / world;
+    }
+    LayerConfig role(const LayerConfig& c, std::uint32_t flags, std::uint32_t first, std::uint32_t last) const {
+        LayerConfig r = c;
+        r.flags = flags;
+        if (flags == MP_LAYER_EXPERTS_ONLY) {
+            r.n_experts = last - first + 1;
+            r.weights = WeightMode::softmax_renorm;  // the owner applies the routing weights
+            r.max_tokens = c.max_tokens * world_;    // rows from every rank
+        }
+        return r;
+    }
+
+    LayerConfig cfg_;
+    std::uint32_t world_, rank_, per_rank_, first_e_, last_e_;
+    MoeLayer router_, experts_;
+    mp_ep_t ep_ = nullptr;
+};
+
 inline std::vector<float> moe_forward(const MoeLayer& layer, std::span<const float> x,
                                       std::span<const std::uint32_t> k_per_token) {
     return layer.forward(x, k_per_token);
@@ -366,6 +444,7 @@ inline std::vector<float> partitioned_forward(const ToyExpert& e, const Partitio
 // Without the reference headers the GPU API is the moeprism API.
 namespace moeprism {
 using b200::Dtype;
+using b200::ExpertParallelLayer;
 using b200::LayerConfig;
 using b200::moe_forward;
 using b200::MoeLayer;

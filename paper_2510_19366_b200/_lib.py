@@ -19,7 +19,8 @@ MP_DTYPE_F32, MP_DTYPE_BF16 = 0, 1
 MP_ROUTER_LINEAR, MP_ROUTER_PROXY = 0, 1
 MP_WEIGHT_UNIT, MP_WEIGHT_SOFTMAX_RENORM = 0, 1
 MP_SEL_NONE = 0xFFFFFFFF
-MP_LAYER_ROUTER_ONLY, MP_LAYER_EXPERTS_ONLY = 1, 2
+MP_LAYER_ROUTER_ONLY, MP_LAYER_EXPERTS_ONLY, MP_LAYER_SHARED_SCRATCH = 1, 2, 4
+MP_EP_NCCL_ID_BYTES, MP_EP_RESIDUAL = 128, 1
 
 # The exported C-ABI (include/moeprism/moe_layer.h); tests check the .so
 # exports every one of these.
@@ -36,7 +37,7 @@ EXPORTS = (
     "mp_layer_stage_times", "mp_layer_reset_stage_times", "mp_layer_launch_count", "mp_synth_fill",
     "mp_format_read_mpex", "mp_format_read_partition_doc", "mp_validate_partition", "mp_layer_forward_selected_host",
     "mp_ep_create", "mp_ep_create_subexpert", "mp_ep_destroy", "mp_ep_plan", "mp_ep_pack", "mp_ep_combine",
-    "mp_layer_route_stats",
+    "mp_layer_route_stats", "mp_ep_nccl_unique_id", "mp_ep_nccl_init", "mp_ep_forward", "mp_ep_last_counts",
 )
 
 
@@ -118,6 +119,10 @@ def _sig(L):
     L.mp_ep_plan.argtypes = [vp, vp, u32, vp, vp]
     L.mp_ep_pack.argtypes = [vp, vp, vp, vp, u32, vp, vp, vp, vp]
     L.mp_ep_combine.argtypes = [vp, vp, u32, vp, vp]
+    L.mp_ep_nccl_unique_id.argtypes = [vp]
+    L.mp_ep_nccl_init.argtypes = [vp, vp]
+    L.mp_ep_forward.argtypes = [vp, vp, vp, vp, u32, vp, u32, vp, u32, vp]
+    L.mp_ep_last_counts.argtypes = [vp, vp, vp]
 
 
 def load():

@@ -13,6 +13,8 @@
 // rows are grouped by rank, tokens ascending -- the layout an NCCL
 // all-to-allv (grouped ncclSend/ncclRecv) consumes directly.
 #include <cstring>
+#include <exception>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -111,16 +113,17 @@ __global__ void __launch_bounds__(256) ep_pack_kernel(const Tx* __restrict__ x, 
     }
 }
 
+// y[t] = (x_res[t] +) sum of the token's partials in ascending rank order
 template <typename Tx>
 __global__ void __launch_bounds__(256) ep_combine_kernel(const Tx* __restrict__ back, uint32_t T, uint32_t d,
                                                          uint32_t world, const uint32_t* __restrict__ slot_row,
-                                                         Tx* __restrict__ y) {
+                                                         const Tx* __restrict__ x_res, Tx* __restrict__ y) {
     __shared__ uint32_t rows[32];
     const uint32_t t = blockIdx.x;
     if (threadIdx.x < world) rows[threadIdx.x] = slot_row[(size_t)t * world + threadIdx.x];
     __syncthreads();
     for (uint32_t c = threadIdx.x; c < d; c += blockDim.x) {
-        float acc = 0.0f;  // partials summed in ascending rank order
+        float acc = x_res ? to_f32(x_res[(size_t)t * d + c]) : 0.0f;  // fused residual: the start value
         for (uint32_t j = 0; j < world; ++j) {
             const uint32_t r = rows[j];
             if (r == kSelNone) break;
@@ -156,24 +159,7 @@ __global__ void __launch_bounds__(256) ep_return_kernel(const Tx* __restrict__ p
 }  // namespace
 }  // namespace mp
 
-struct mp_ep_s {
-    uint32_t world, rank, per_rank, S, d, k_max, max_tokens, dtype;
-    int device;
-    uint32_t* dest = nullptr;
-    mp::BucketWs ws{};
-    uint32_t last_T = 0;
-    // peer-memory exchange (mp_ep_p2p_*): own receive / return buffers, the
-    // peers' (CUDA IPC) and device tables of [world] pointers
-    uint32_t max_recv = 0;
-    void* recv_x = nullptr;
-    uint32_t* recv_sel = nullptr;
-    float* recv_w = nullptr;
-    void* back = nullptr;
-    std::vector<void*> opened;  // IPC mappings to close
-    void** d_px = nullptr;      // device [4][world]: x, sel, w, back
-    uint32_t* d_meta = nullptr; // device [4][world + 1]: base, roff, dbase, ones
-    bool p2p = false;
-};
+#include "mp_ep_impl.h"
 
 namespace {
 thread_local std::string g_ep_err;
@@ -188,6 +174,7 @@ void ep_ck(cudaError_t e, const char* what) {
 template <class F>
 int ep_guarded(F&& f);
 void ep_free(mp_ep_s* E) {
+    if (E->nccl) mp_ep_nccl_free(E);
     for (void* p : E->opened) cudaIpcCloseMemHandle(p);
     void* ptrs[] = {E->dest, E->ws.lrank, E->ws.block_counts, E->ws.block_base, E->ws.offsets, E->ws.mprefix_tc,
                     E->ws.mprefix_simt, E->ws.mprefix_tc2, E->ws.perm_tok, E->ws.perm_w, E->ws.slot_row, E->ws.err,
@@ -217,8 +204,27 @@ int ep_guarded(F&& f) {
     } catch (const EpErr& e) {
         mp_internal_set_error(e.msg.c_str());
         return e.code;
+    } catch (const std::bad_alloc&) {
+        mp_internal_set_error("host out of memory");
+        return MP_ERR_CUDA;
+    } catch (const std::exception& e) {
+        mp_internal_set_error(e.what());
+        return MP_ERR_CUDA;
     }
 }
+
+// Every entry point runs on the handle's device and restores the caller's.
+struct EpDeviceGuard {
+    int prev = -1;
+    explicit EpDeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) ep_ck(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~EpDeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
 }  // namespace
 
 namespace {
@@ -239,7 +245,7 @@ MP_API mp_status mp_ep_create_subexpert(uint32_t world, uint32_t rank, uint32_t 
         if (per_rank < 1 || S < 1 || d < 1 || k_max < 1 || k_max > 256 || max_tokens < 1)
             ep_fail(MP_ERR_VALIDATION, "bad expert-parallel shape");
         if (dtype != MP_DTYPE_F32 && dtype != MP_DTYPE_BF16) ep_fail(MP_ERR_VALIDATION, "unknown dtype");
-        ep_ck(cudaSetDevice(device), "cudaSetDevice");
+        EpDeviceGuard dg(device);
         auto* E = new mp_ep_s{world, rank, per_rank, S, d, k_max, max_tokens, dtype, device};
         try {
             const size_t tw = (size_t)max_tokens * world;
@@ -277,7 +283,7 @@ MP_API mp_status mp_ep_create(uint32_t world, uint32_t rank, uint32_t epr, uint3
 MP_API mp_status mp_ep_destroy(mp_ep_t E) {
     return ep_guarded([&] {
         if (E) {
-            cudaSetDevice(E->device);
+            EpDeviceGuard dg(E->device);
             cudaDeviceSynchronize();
             ep_free(E);
         }
@@ -287,6 +293,7 @@ MP_API mp_status mp_ep_destroy(mp_ep_t E) {
 MP_API mp_status mp_ep_plan(mp_ep_t E, const uint32_t* sel, uint32_t T, uint32_t* send_counts, void* stream) {
     return ep_guarded([&] {
         if (!E || !send_counts || (T && !sel)) ep_fail(MP_ERR_VALIDATION, "null argument");
+        EpDeviceGuard dg(E->device);
         if (T > E->max_tokens) ep_fail(MP_ERR_VALIDATION, "n_tokens exceeds max_tokens");
         E->last_T = T;
         if (T == 0) {
@@ -310,6 +317,7 @@ MP_API mp_status mp_ep_pack(mp_ep_t E, const void* x, const uint32_t* sel, const
                             uint32_t* send_sel, float* send_w, void* stream) {
     return ep_guarded([&] {
         if (!E || (T && (!x || !sel || !send_x || !send_sel || !send_w))) ep_fail(MP_ERR_VALIDATION, "null argument");
+        EpDeviceGuard dg(E->device);
         if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_pack must follow mp_ep_plan for the same tokens");
         if (T == 0) return;
         // identity destinations: every rank's segment of the one send buffer
@@ -337,7 +345,7 @@ MP_API mp_status mp_ep_p2p_setup(mp_ep_t E, uint32_t max_recv_rows, uint8_t* han
         if (!E || !handles) ep_fail(MP_ERR_VALIDATION, "null argument");
         if (E->p2p || E->recv_x) ep_fail(MP_ERR_VALIDATION, "peer-memory exchange already set up");
         if (max_recv_rows < 1) ep_fail(MP_ERR_VALIDATION, "max_recv_rows must be >= 1");
-        ep_ck(cudaSetDevice(E->device), "cudaSetDevice");
+        EpDeviceGuard dg(E->device);
         const size_t esz = E->dtype == MP_DTYPE_BF16 ? 2 : 4;
         E->max_recv = max_recv_rows;
         E->recv_x = ep_alloc<char>((size_t)max_recv_rows * E->d * esz);
@@ -358,7 +366,7 @@ MP_API mp_status mp_ep_p2p_open(mp_ep_t E, const uint8_t* all_handles) {
     return ep_guarded([&] {
         if (!E || !all_handles) ep_fail(MP_ERR_VALIDATION, "null argument");
         if (!E->recv_x) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_setup first");
-        ep_ck(cudaSetDevice(E->device), "cudaSetDevice");
+        EpDeviceGuard dg(E->device);
         const size_t hs = sizeof(cudaIpcMemHandle_t);
         std::vector<void*> px(4 * (size_t)E->world);
         void* own[4] = {E->recv_x, E->recv_sel, E->recv_w, E->back};
@@ -392,7 +400,17 @@ void p2p_meta(mp_ep_s* E, const uint32_t* counts, cudaStream_t s, uint32_t& n_re
     for (uint32_t q = 0; q < W; ++q)
         for (uint32_t r = 0; r < me; ++r) dbase[q] += counts[(size_t)q * W + r];
     n_recv = roff[W];
-    if (n_recv > E->max_recv) ep_fail(MP_ERR_VALIDATION, "received rows exceed max_recv_rows");
+    // every rank holds the whole plan: check EVERY destination's receive
+    // count (all ranks use the same max_recv_rows), so all ranks fail the same
+    // way before any peer store -- no rank writes past a peer's buffer and none
+    // is left waiting in a barrier the others skip
+    for (uint32_t r = 0; r < W; ++r) {
+        uint64_t col = 0;
+        for (uint32_t q = 0; q < W; ++q) col += counts[(size_t)q * W + r];
+        if (col > E->max_recv)
+            ep_fail(MP_ERR_VALIDATION, "rank " + std::to_string(r) + " would receive " + std::to_string(col) +
+                                           " rows, more than max_recv_rows " + std::to_string(E->max_recv));
+    }
     ep_ck(cudaMemcpyAsync(E->d_meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, s), "p2p meta");
 }
 }  // namespace
@@ -401,6 +419,7 @@ MP_API mp_status mp_ep_p2p_pack(mp_ep_t E, const void* x, const uint32_t* sel, c
                                 const uint32_t* counts, uint32_t* n_recv, void* stream) {
     return ep_guarded([&] {
         if (!E || !counts || !n_recv || (T && (!x || !sel))) ep_fail(MP_ERR_VALIDATION, "null argument");
+        EpDeviceGuard dg(E->device);
         if (!E->p2p) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_open first");
         if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_pack must follow mp_ep_plan for the same tokens");
         cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -426,6 +445,7 @@ MP_API mp_status mp_ep_p2p_recv_buffers(mp_ep_t E, void** recv_x, uint32_t** rec
 MP_API mp_status mp_ep_p2p_return(mp_ep_t E, const void* part, uint32_t n_recv, void* stream) {
     return ep_guarded([&] {
         if (!E || (n_recv && !part)) ep_fail(MP_ERR_VALIDATION, "null argument");
+        EpDeviceGuard dg(E->device);
         if (!E->p2p) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_open first");
         const uint32_t W = E->world;
         mp::launch_ep_return(E->dtype, part, n_recv, E->d, W, E->d_meta + (W + 1), E->d_meta + 2 * (W + 1),
@@ -437,6 +457,7 @@ MP_API mp_status mp_ep_p2p_return(mp_ep_t E, const void* part, uint32_t n_recv, 
 MP_API mp_status mp_ep_p2p_combine(mp_ep_t E, uint32_t T, void* y, void* stream) {
     return ep_guarded([&] {
         if (!E || (T && !y)) ep_fail(MP_ERR_VALIDATION, "null argument");
+        EpDeviceGuard dg(E->device);
         if (!E->p2p) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_open first");
         if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_p2p_combine must follow mp_ep_plan for the same tokens");
         if (T == 0) return;
@@ -448,6 +469,7 @@ MP_API mp_status mp_ep_p2p_combine(mp_ep_t E, uint32_t T, void* y, void* stream)
 MP_API mp_status mp_ep_combine(mp_ep_t E, const void* back, uint32_t T, void* y, void* stream) {
     return ep_guarded([&] {
         if (!E || (T && (!back || !y))) ep_fail(MP_ERR_VALIDATION, "null argument");
+        EpDeviceGuard dg(E->device);
         if (T != E->last_T) ep_fail(MP_ERR_VALIDATION, "mp_ep_combine must follow mp_ep_plan for the same tokens");
         if (T == 0) return;
         mp::launch_ep_combine(E->dtype, back, T, E->d, E->world, E->ws.slot_row, y, static_cast<cudaStream_t>(stream));
@@ -488,12 +510,13 @@ void launch_ep_return(int dtype, const void* part, uint32_t n_recv, uint32_t d, 
                                                                  roff, dbase, back);
 }
 void launch_ep_combine(int dtype, const void* back, uint32_t T, uint32_t d, uint32_t world, const uint32_t* slot_row,
-                       void* y, cudaStream_t s) {
+                       void* y, cudaStream_t s, const void* x_res) {
     if (dtype == 1)
         ep_combine_kernel<__nv_bfloat16><<<T, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(back), T, d, world,
-                                                           slot_row, static_cast<__nv_bfloat16*>(y));
+                                                           slot_row, static_cast<const __nv_bfloat16*>(x_res),
+                                                           static_cast<__nv_bfloat16*>(y));
     else
         ep_combine_kernel<float><<<T, 256, 0, s>>>(static_cast<const float*>(back), T, d, world, slot_row,
-                                                   static_cast<float*>(y));
+                                                   static_cast<const float*>(x_res), static_cast<float*>(y));
 }
 }  // namespace mp

@@ -92,6 +92,53 @@ struct DeviceGuard {
     }
 };
 
+// Per-device pool of the big per-forward scratch buffers (x_perm, h, o) for
+// layers created with MP_LAYER_SHARED_SCRATCH: layers that run one after the
+// other on one stream (a layer stack) share one allocation of each exact size,
+// reference counted.
+struct ScratchPool {
+    struct Ent {
+        int dev;
+        size_t bytes;
+        void* p;
+        int refs;
+    };
+    std::mutex mu;
+    std::vector<Ent> ents;
+};
+ScratchPool& scratch_pool() {
+    static ScratchPool pool;
+    return pool;
+}
+
+void* scratch_acquire(size_t bytes, const char* what) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ScratchPool& P = scratch_pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    for (auto& e : P.ents)
+        if (e.dev == dev && e.bytes == bytes) {
+            ++e.refs;
+            return e.p;
+        }
+    void* p = nullptr;
+    ck(cudaMalloc(&p, bytes ? bytes : 1), what);
+    P.ents.push_back({dev, bytes, p, 1});
+    return p;
+}
+void scratch_release(void* p) {
+    ScratchPool& P = scratch_pool();
+    std::lock_guard<std::mutex> lk(P.mu);
+    for (size_t i = 0; i < P.ents.size(); ++i)
+        if (P.ents[i].p == p) {
+            if (--P.ents[i].refs == 0) {
+                cudaFree(p);
+                P.ents.erase(P.ents.begin() + i);
+            }
+            return;
+        }
+}
+
 template <class T>
 T* dalloc(size_t n, const char* what) {
     void* p = nullptr;
@@ -186,6 +233,7 @@ struct mp_layer_s {
     void* x_perm = nullptr;
     void* h = nullptr;
     void* o = nullptr;
+    bool shared_scratch = false;  // MP_LAYER_SHARED_SCRATCH: x_perm / h / o from the device pool
     void* x_stage = nullptr;
     void* y_stage = nullptr;
     CUtensorMap tm_xperm{}, tm_h{}, tm_w1{}, tm_w2{};
@@ -253,10 +301,12 @@ namespace {
 void free_layer(mp_layer_s* L) {
     for (float* p : L->raw)
         if (p) cudaFree(p);
+    for (void* p : {L->x_perm, L->h, L->o})
+        if (p) L->shared_scratch ? scratch_release(p) : (void)cudaFree(p);
     void* ptrs[] = {L->p_planes, L->p_partial, L->p_xnorm, L->p_win, L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_xnorm, L->r_flagged, L->r_ticket, L->d_nmap, L->nmap_all, L->sel,
                     L->wsel, L->kpt_dev, L->ws.lrank, L->ws.block_counts, L->ws.block_base, L->ws.offsets,
                     L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.mprefix_tc2, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
-                    L->x_perm, L->h, L->o, L->x_stage, L->y_stage, L->W1s, L->W2s, L->sh_gate, L->sh_h,
+                    L->x_stage, L->y_stage, L->W1s, L->W2s, L->sh_gate, L->sh_h,
                     L->sh_o, L->sh_w, L->sh_meta, L->cal_meta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -801,8 +851,8 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
         if (D.router_mode > MP_ROUTER_PROXY || D.weight_mode > MP_WEIGHT_SOFTMAX_RENORM)
             fail(MP_ERR_VALIDATION, "unknown router / weight mode");
         if (D.max_tokens < 1) fail(MP_ERR_VALIDATION, "max_tokens must be >= 1");
-        if (D.flags & ~(MP_LAYER_ROUTER_ONLY | MP_LAYER_EXPERTS_ONLY) ||
-            D.flags == (MP_LAYER_ROUTER_ONLY | MP_LAYER_EXPERTS_ONLY))
+        if (D.flags & ~(MP_LAYER_ROUTER_ONLY | MP_LAYER_EXPERTS_ONLY | MP_LAYER_SHARED_SCRATCH) ||
+            (D.flags & (MP_LAYER_ROUTER_ONLY | MP_LAYER_EXPERTS_ONLY)) == (MP_LAYER_ROUTER_ONLY | MP_LAYER_EXPERTS_ONLY))
             fail(MP_ERR_VALIDATION, "invalid layer role flags");
         {
             int rc = mp_device_check(D.device);
@@ -907,10 +957,19 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 L->ws.perm_tok = dalloc<uint32_t>(L->rows_cap, "perm");
                 L->ws.perm_w = dalloc<float>(L->rows_cap, "perm w");
                 L->ws.slot_row = dalloc<uint32_t>(tk, "slot row");
-                L->x_perm = dalloc<char>((size_t)L->rows_cap * L->d_pad * L->esz, "x_perm");
-                L->h = dalloc<char>((size_t)L->rows_cap * L->w_pad * L->esz, "h");
+                const size_t bx = (size_t)L->rows_cap * L->d_pad * L->esz, bh = (size_t)L->rows_cap * L->w_pad * L->esz;
                 // fp32 mode keeps sub-expert outputs in double until the combine rounds them
-                L->o = dalloc<char>((size_t)L->rows_cap * L->d_pad * (L->dtype == MP_DTYPE_F32 ? 8 : L->esz), "o");
+                const size_t bo = (size_t)L->rows_cap * L->d_pad * (L->dtype == MP_DTYPE_F32 ? 8 : L->esz);
+                L->shared_scratch = (D.flags & MP_LAYER_SHARED_SCRATCH) != 0;
+                if (L->shared_scratch) {
+                    L->x_perm = scratch_acquire(bx, "x_perm (shared)");
+                    L->h = scratch_acquire(bh, "h (shared)");
+                    L->o = scratch_acquire(bo, "o (shared)");
+                } else {
+                    L->x_perm = dalloc<char>(bx, "x_perm");
+                    L->h = dalloc<char>(bh, "h");
+                    L->o = dalloc<char>(bo, "o");
+                }
                 L->y_stage = dalloc<char>((size_t)L->max_tokens * L->d * L->esz, "y stage");
                 if (L->use_tc) {
                     bool ok =

@@ -229,5 +229,5 @@ void launch_ep_pack(int dtype, const void* x, const uint32_t* sel, const float* 
 void launch_ep_return(int dtype, const void* part, uint32_t n_recv, uint32_t d, uint32_t world, const uint32_t* roff,
                       const uint32_t* dbase, void* const* back, cudaStream_t s);
 void launch_ep_combine(int dtype, const void* back, uint32_t T, uint32_t d, uint32_t world, const uint32_t* slot_row,
-                       void* y, cudaStream_t s);
+                       void* y, cudaStream_t s, const void* x_res = nullptr);
 }  // namespace mp

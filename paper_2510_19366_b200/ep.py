@@ -166,6 +166,49 @@ class ExpertParallelLayer:
         return y
 
 
+class NcclExpertParallelLayer:
+    """The production expert-parallel layer: the whole per-layer sequence
+    (route, plan, count exchange, pack, NCCL all-to-allv dispatch, experts,
+    NCCL return, deterministic combine) runs in C++ inside
+    libmoeprism_b200.so (mp_ep_forward) on a communicator the library owns.
+    Python only hands the 128-byte NCCL unique id from rank 0 to the others
+    (torch.distributed object broadcast) -- the exchange itself never touches
+    torch.distributed, and each layer costs one host synchronisation (the
+    count matrix)."""
+
+    def __init__(self, ops, group=None, residual: bool = False):
+        import torch
+        self.ops, self.torch = ops, torch
+        self.lib = _lib.load()
+        self.flags = _lib.MP_EP_RESIDUAL if residual else 0
+        uid = (C.c_uint8 * _lib.MP_EP_NCCL_ID_BYTES)()
+        dist = _dist() if ops.world > 1 else None
+        if ops.rank == 0:
+            check(self.lib.mp_ep_nccl_unique_id(uid))
+        if dist is not None and dist.is_initialized():
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = (C.c_uint8 * _lib.MP_EP_NCCL_ID_BYTES).from_buffer_copy(box[0])
+        check(self.lib.mp_ep_nccl_init(ops.ep, uid))
+
+    def forward(self, x, k: int = 0, k_per_token=None, y=None, stream=None):
+        torch, ops = self.torch, self.ops
+        T = x.shape[0]
+        if y is None:
+            y = torch.empty((T, ops.d), dtype=ops.dtype, device=x.device)
+        kpt = None if k_per_token is None else k_per_token.to(device=x.device, dtype=torch.int32).contiguous()
+        check(self.lib.mp_ep_forward(ops.ep, ops.router.h, ops.local.h, _ptr(x), T, _ptr(kpt), k, _ptr(y), self.flags,
+                                     _stream_handle(stream)))
+        return y
+
+    def last_counts(self):
+        """(rows sent to each rank, rows received from each rank) of the last forward."""
+        s = (C.c_uint32 * self.ops.world)()
+        r = (C.c_uint32 * self.ops.world)()
+        check(self.lib.mp_ep_last_counts(self.ops.ep, s, r))
+        return list(s), list(r)
+
+
 class PeerExpertParallelLayer:
     """Expert parallelism with both exchanges as peer-memory stores instead of
     NCCL all-to-alls: the pack kernel writes every token row straight into the

@@ -189,7 +189,7 @@ int main() {
             for (auto& v : x) v = static_cast<float>(uniform01(rng) * 2.0 - 1.0);
             std::vector<std::uint32_t> act;
             for (std::uint32_t s2 = 0; s2 < n; s2 += 3) act.push_back(s2);
-            act.push_back(n - 1);
+            if (act.back() != n - 1) act.push_back(n - 1);
             std::vector<std::uint32_t> all(n);
             std::iota(all.begin(), all.end(), 0u);
             const auto y = partitioned_forward(e, p, x, act);

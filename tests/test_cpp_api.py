@@ -10,15 +10,29 @@ ROOT = Path(__file__).resolve().parent.parent
 PKG = ROOT / "paper_2510_19366_b200"
 
 
-def _build(out: Path):
-    cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(ROOT / "tests" / "cpp" / "test_dropin.cpp"),
-           f"-L{PKG}", "-lmoeprism_b200", f"-Wl,-rpath,{PKG}", "-o", str(out)]
+def _build(out: Path, src: str = "test_dropin.cpp"):
+    cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", "-I/usr/local/cuda/include",
+           str(ROOT / "tests" / "cpp" / src), f"-L{PKG}", "-lmoeprism_b200", f"-Wl,-rpath,{PKG}",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-o", str(out)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
 
 
 def test_cpp_header_compiles_and_links(tmp_path):
     _build(tmp_path / "test_dropin")
+    _build(tmp_path / "test_ep_nccl", "test_ep_nccl.cpp")
+
+
+@pytest.mark.gpu
+def test_cpp_expert_parallel_nccl_on_gpu(tmp_path, cuda_lib):
+    """ExpertParallelLayer (C++ host, NCCL transport) == MoeLayer bit for bit
+    in a 1-rank communicator, for scalar k, fused residual and per-token k."""
+    exe = tmp_path / "test_ep_nccl"
+    _build(exe, "test_ep_nccl.cpp")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ALL PASSED" in r.stdout
 
 
 @pytest.mark.gpu

@@ -130,3 +130,38 @@ def test_ep_nccl_collectives_world1(oracle, cuda_lib):
         assert torch.equal(y, y_ref)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("residual", [False, True])
+def test_ep_cpp_nccl_transport_world1(oracle, cuda_lib, residual):
+    """The production path: mp_ep_forward (C++ host, the library's own NCCL
+    communicator, grouped ncclSend/ncclRecv all-to-allv) in a 1-rank world,
+    bit-identical to the single layer over several calls (buffer reuse) and
+    per-token k.  With the residual, the expert-parallel combine adds x to the
+    bf16 partial of each rank (the single layer adds it inside its fp32
+    accumulator), so the reference is bf16(x + bf16(MoE(x))), bit for bit."""
+    import torch
+    from paper_2510_19366_b200 import MoeLayer
+    from paper_2510_19366_b200.ep import NcclExpertParallelLayer
+    experts, parts, wr = _setup(oracle)
+    ref = MoeLayer(E, S, D, FF, dtype="bf16", k_max=K_MAX, max_tokens=T)
+    for e in range(E):
+        ref.set_partition(e, parts[e])
+        ref.load_expert(e, *experts[e])
+    ref.set_router(wr)
+    ops = _ops(1, 0, experts, parts, wr)
+    layer = NcclExpertParallelLayer(ops, residual=residual)
+    for i, Tn in enumerate((T, 17, 1, T)):
+        x = torch.from_numpy(oracle.uniform_pm1(50 + i, Tn * D).reshape(Tn, D)).cuda().to(torch.bfloat16)
+        kpt = torch.from_numpy(np.random.default_rng(i).choice([1, 2, 4, 8], size=Tn).astype(np.int32)).cuda()
+        for kk, kp in ((4, None), (0, kpt)):
+            y_ref = ref.forward(x, k=kk, k_per_token=kp)
+            if residual:
+                y_ref = (x.float() + y_ref.float()).to(torch.bfloat16)
+            y = layer.forward(x, k=kk, k_per_token=kp)
+            torch.cuda.synchronize()
+            assert torch.equal(y, y_ref), (Tn, kk)
+        sent, recv = layer.last_counts()
+        assert sent == [Tn] and recv == [Tn]
+    ops.close()
+    ref.close()
