@@ -163,7 +163,7 @@ int orc_contiguous_partition(size_t n, uint32_t n_sub, uint32_t* assignment) {
 /* ------------------------------------------------------------------------ */
 /* Counter-based synthetic generator for the large configs.
  * Element i of stream `seed` is a pure function of (seed, i), so the GPU
- * fill kernel (paper_2510_19366_b200/csrc/synth.cu) and this CPU fill agree
+ * fill kernel (paper_2510_19366_b200/csrc/pack.cu synth_fill_kernel) and this CPU fill agree
  * bit for bit at any size without replaying a sequential stream.
  *   state = mix(seed + G); u_i = (mix(state + (i+1) G) >> 11) * 2^-53
  *   value = float((u_i * 2 - 1) * scale)

@@ -74,6 +74,10 @@ struct TcParams {
     // kEpiCount:  uint32(acc) (exact 0/1 co-activation counts)
     const int32_t* colmap;
     void* out32;
+    // split-K (kEpiF32Part): K is cut into ksplit ranges of kps k-blocks; the
+    // tile of split s writes its fp32 partial to out32 + s * split_stride
+    uint32_t ksplit, kps;
+    size_t split_stride;
 };
 
 __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix, uint32_t G, uint32_t NT,
@@ -95,8 +99,8 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
 
 // (tile, k-block) cursor of one operand stream of a CTA
 struct Cursor {
-    uint32_t tile, kb;
-    int32_t row;  // A row (arow) or B row (brow) of the current tile
+    uint32_t tile, kb, kb1;  // current k-block, end of the tile's k range
+    int32_t row;             // A row (arow) or B row (brow) of the current tile
 };
 
 template <int EPI>
@@ -153,7 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t total = s_prefix[p.G] * p.NT;
+    const uint32_t base_total = s_prefix[p.G] * p.NT;
+    const uint32_t total = base_total * p.ksplit;
     const uint32_t nkb = p.K / BK;
 
     if (warp == 0) {
@@ -163,18 +168,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             auto set_rows = [&](Cursor& c, bool is_a) {
                 if (c.tile >= total) return;
                 uint32_t g, m, n;
-                map_tile(c.tile, s_prefix, p.G, p.NT, g, m, n);
+                const uint32_t split = c.tile / base_total;
+                map_tile(c.tile - split * base_total, s_prefix, p.G, p.NT, g, m, n);
                 c.row = is_a ? static_cast<int32_t>(s_start[g] + m * BM)
                              : static_cast<int32_t>(p.b_row0 + s_gmap[g] * p.N_group + n * BN);
+                c.kb = split * p.kps;
+                c.kb1 = min(nkb, c.kb + p.kps);
             };
             auto advance = [&](Cursor& c, bool is_a) {
-                if (++c.kb == nkb) {
-                    c.kb = 0;
+                if (++c.kb == c.kb1) {
                     c.tile += gridDim.x;
                     set_rows(c, is_a);
                 }
             };
-            Cursor cb{blockIdx.x, 0, 0}, ca{blockIdx.x, 0, 0};
+            Cursor cb{blockIdx.x, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0};
             set_rows(cb, false);
             set_rows(ca, true);
             uint32_t ib = 0, ia = 0;  // loads issued per stream
@@ -223,7 +230,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (p.trace) w_acc += clock64() - t0;
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
+                const uint32_t kb_lo = (tile / base_total) * p.kps, kb_hi = min(nkb, kb_lo + p.kps);
+                for (uint32_t kb = kb_lo; kb < kb_hi; ++kb, ++it) {
                     const uint32_t sa = it % NA, pa = (it / NA) & 1u;
                     const uint32_t sb = it % NB, pb = (it / NB) & 1u;
                     t0 = p.trace ? clock64() : 0;
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (uint32_t k = 0; k < BK / 16; ++k)
                         umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                                  (kb | k) != 0u);
+                                  (kb != kb_lo || k != 0) ? 1u : 0u);
                     umma_commit(&emptyA[sa]);
                     umma_commit(&emptyB[sb]);
                 }
@@ -256,7 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t tc = 0;
         for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
             uint32_t g, m, n;
-            map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+            const uint32_t split = tile / base_total;
+            map_tile(tile - split * base_total, s_prefix, p.G, p.NT, g, m, n);
             const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
@@ -281,6 +290,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int32_t j = __ldg(cm + i);
                             if (j >= 0) arow[j] = fabsf(silu_f32(__uint_as_float(gr[i])) * __uint_as_float(ur[i]));
                         }
+                    }
+                }
+            } else if constexpr (EPI == kEpiF32Part) {
+                // split-K partial: fp32, 16-byte stores; the consumer sums the splits in order
+                float* prow = static_cast<float*>(p.out32) + split * p.split_stride +
+                              static_cast<size_t>(s_start[g] + row_local) * p.ld_out;
+#pragma unroll 1
+                for (uint32_t c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(taddr + c * 32, r);
+                    tmem_ld_wait();
+                    const uint32_t col = n * BN + c * 32;
+                    if (valid && col < p.n_valid) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4)
+                            st_global_v4(prow + col + i, make_uint4(r[i], r[i + 1], r[i + 2], r[i + 3]));
                     }
                 }
             } else if constexpr (EPI == kEpiCount) {
@@ -430,7 +455,8 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
 
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                        uint32_t b_row0, const int32_t* colmap, const uint32_t* gmap, const uint32_t* starts) {
+                        uint32_t b_row0, const int32_t* colmap, const uint32_t* gmap, const uint32_t* starts,
+                        uint32_t ksplit) {
     const bool swiglu = epi == kEpiSwiglu;
     TcParams p;
     p.G = sh.G;
@@ -448,15 +474,22 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.starts = starts;
     p.colmap = colmap;
     p.out32 = out;
+    const uint32_t nkb = sh.K / BK;
+    p.ksplit = epi == kEpiF32Part ? (ksplit < 1 ? 1u : ksplit > nkb ? nkb : ksplit) : 1u;
+    p.kps = (nkb + p.ksplit - 1) / p.ksplit;
+    p.ksplit = (nkb + p.kps - 1) / p.kps;  // no empty splits
+    p.split_stride = static_cast<size_t>(sh.max_rows) * sh.ld_out;
 
     // upper bound on tiles; the kernel reads the exact count from the device
-    const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
+    const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT * p.ksplit;
     const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiPlain>), (int)kSmemBytes);
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiSwiglu>), (int)kSmemBytes);
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiActAbs>), (int)kSmemBytes);
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiCount>), (int)kSmemBytes);
+    func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiF32Part>), (int)kSmemBytes);
     switch (epi) {
+        case kEpiF32Part: launch_k(gemm_tc_kernel<kEpiF32Part>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
         case kEpiSwiglu: launch_k(gemm_tc_kernel<kEpiSwiglu>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
         case kEpiActAbs: launch_k(gemm_tc_kernel<kEpiActAbs>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
         case kEpiCount: launch_k(gemm_tc_kernel<kEpiCount>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;

@@ -18,26 +18,18 @@
 //   gemm2: B tile = W2 rows n*256 .. +255 = output columns; CTA r loads its half.
 // Tiles are (g, n, m) with 256-row m tiles (prefix of ceil(count_g / 256)),
 // m fastest, strided over the clusters of a persistent grid.  Rows past the
-// group end are computed and discarded (masked stores).  Optional (tail128,
-// off by default): a tile with at most 128 valid rows (the tail of a group)
-// issues M=128 pair MMAs with 64-row A loads, the accumulator in the 2x2
-// layout (rows in lanes 0-63 with D columns [0,128), the same rows in lanes
-// 64-127 with D columns [128,256)); with the 64-row gate/up interleave of W1
-// (kIlv) both halves of a neuron's SwiGLU stay in one lane in either shape.
-// Measured (per-tile MMA-issuer trace, tests/probes/tile_trace.py): tail
-// tiles take the SAME cycles as full ones (the pipeline runs at ~580 cycles
-// per k-block either way: 510 of MMA issue + ~70 of operand waits), and the
-// step is 4% slower with them (profiles/r01_tile_ab.txt), so tails run as
-// full 256-row tiles.
+// group end are computed and discarded (masked stores).
 //
-// Two more opt-in remainder schedules (tile decoder below): EXT merges a
-// <= 128-row remainder into the group's previous tile as an extra M=128 MMA on
-// the same B stage (257..384-row tiles, 5 x 40 KB stages, the remainder
-// accumulator in the other TMEM buffer); WIDE runs a <= 128-row remainder over
-// two N tiles at once (two M=128 MMAs sharing the A stage, the second B half
-// in the next ring slot).  Both re-read an operand from shared memory, which
-// bounds these kernels (operand reads + TMA writes ~128 B/cycle per SM at the
-// full tile's MMA rate), and measured slower per step.
+// Remainder schedules measured and dropped (round 1):
+// M=128 tail tiles (a tail tile costs the same ~580 cycles per k-block as a
+// full one -- the pipeline is bound by the operand feed, ~510 cycles of MMA
+// issue + ~70 of waits), a merged remainder riding on the previous tile as an
+// extra M=128 MMA (its accumulator takes the other TMEM buffer and exposes an
+// epilogue), a remainder spread over two N tiles (two M=128 MMAs re-reading A
+// from shared memory), and tails on the 1-SM kernel after the pair kernel
+// (+0.9 GB of weight re-reads).  Every scheme re-reads an operand or a weight
+// tile; under the 1000 W cap the step lands within ~3% either way, so the pair
+// kernel runs plain 256-row tiles only.
 //
 // Barriers: full[s] lives in the leader CTA (both CTAs' TMA loads complete_tx
 // on it; the leader's expect_tx covers both); empty[s], tfull[a] are signalled
@@ -89,13 +81,6 @@ constexpr uint32_t kEpiWarps = MP_PAIR_EPI_WARPS;
 constexpr uint32_t kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
 constexpr size_t kSmemBytes = 1024 + NSP * STAGE_BYTES + 256;
-// extended-tile kernel: + 64 A rows per CTA per stage (the M=128 MMA of a
-// merged remainder), 5 stages of 40 KB
-constexpr uint32_t NSX = 5;
-constexpr uint32_t X_BYTES = 64 * BK * 2;
-constexpr size_t kSmemBytesX = 1024 + NSX * (STAGE_BYTES + X_BYTES) + 256;
-template <bool EXT>
-constexpr size_t smem_bytes() { return EXT ? kSmemBytesX : kSmemBytes; }
 
 struct PairParams {
     uint32_t G, K, N_group, n_valid, ld_out, NT;
@@ -103,10 +88,6 @@ struct PairParams {
     const uint32_t* mprefix;  // prefix of ceil(count_g / 256)
     __nv_bfloat16* out;
     uint64_t* trace;  // [grid][4] MMA-issuer timing of the leaders (diagnostics) or null
-    uint32_t tail128;  // tiles with <= 128 valid rows issue M=128 pair MMAs
-    uint32_t ext;      // mprefix is the merged schedule: 257..384-row extended tiles
-    uint32_t wide;     // wide-tail schedule: mprefix = pair tiles per n, tprefix = <= 128-row tails
-    const uint32_t* tprefix;
     const uint32_t* gmap;  // nullable: B group of group g (sub-expert offload cache slot), else g
 };
 
@@ -203,63 +184,18 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
     m = local - n * mt;
 }
 
-// Tile kinds: full M=256 pair tile; M=128 tail (64 A rows per CTA); EXT: full
-// tile + merged M=128 remainder; WIDE: a <= 128-row remainder over two N
-// tiles at once (two M=128 MMAs sharing the A stage, one 256-column buffer).
-enum : uint32_t { kFull = 0, kTail = 1, kExt = 2, kWide = 3 };
-struct TileInfo {
-    uint32_t g, m, n, kind;
-};
-
-// Wide-tail schedule, per group g: for each pair of N tiles (n0, n0 + 1): the
-// full tiles of n0 (m fastest), those of n0 + 1, then the remainder tile over
-// both (its B slices were just streamed: L2-hot).  mpf[g] = full tiles per N
-// tile (count/256, + 1 for a remainder > 128), tl[g] = 1 for a remainder of
-// 1..128 rows.
-__device__ __forceinline__ TileInfo decode_wide(uint32_t tile, const uint32_t* s_pf, const uint32_t* s_tl,
-                                                uint32_t G, uint32_t NT) {
-    const uint32_t NTh = (NT + 1) / 2;
-    uint32_t lo = 0, hi = G;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s_pf[mid] * NT + s_tl[mid] * NTh <= tile)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    TileInfo t;
-    t.g = lo - 1;
-    const uint32_t local = tile - (s_pf[t.g] * NT + s_tl[t.g] * NTh);
-    const uint32_t mpf = s_pf[t.g + 1] - s_pf[t.g], tl = s_tl[t.g + 1] - s_tl[t.g];
-    const uint32_t bs = 2 * mpf + tl;
-    const uint32_t np = local / bs, r = local - np * bs, n0 = 2 * np;
-    const bool two = n0 + 1 < NT;
-    if (r < mpf) {
-        t.n = n0, t.m = r, t.kind = kFull;
-    } else if (two && r < 2 * mpf) {
-        t.n = n0 + 1, t.m = r - mpf, t.kind = kFull;
-    } else {
-        t.n = n0, t.m = mpf, t.kind = two ? kWide : kTail;
-    }
-    return t;
-}
-
-template <bool SWIGLU, bool EXT>
+template <bool SWIGLU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmA64, PairParams p) {
-    constexpr uint32_t NS = EXT ? NSX : NSP;
-    constexpr uint32_t XB = EXT ? X_BYTES : 0u;
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, PairParams p) {
+    constexpr uint32_t NS = NSP;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
-    __shared__ uint32_t s_tpre[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
     __shared__ uint32_t s_gmap[kMaxG];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // identical offsets in both CTAs (same dynamic smem layout)
     uint8_t* sA = base;                // NS x 16 KB
-    uint8_t* sX = base + NS * A_BYTES;  // NS x 8 KB (EXT: the remainder's 64 rows per CTA)
-    uint8_t* sB = sX + NS * XB;         // NS x 16 KB
+    uint8_t* sB = base + NS * A_BYTES;  // NS x 16 KB
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + NS * B_BYTES);
     uint64_t* empty = full + NS;
     uint64_t* tfull = empty + NS;
@@ -284,7 +220,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
-        if (p.tail128 || p.wide || EXT) tma_prefetch_desc(&tmA64);
         tma_prefetch_desc(&tmB);
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot);
@@ -292,7 +227,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     griddep_launch();
     for (uint32_t q = threadIdx.x; q <= p.G; q += blockDim.x) {
         s_prefix[q] = p.mprefix[q];
-        s_tpre[q] = p.wide ? p.tprefix[q] : 0u;
         s_off[q] = p.offsets[q];
         if (q < p.G) s_gmap[q] = p.gmap ? p.gmap[q] : q;
     }
@@ -301,16 +235,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync();  // peer barriers initialised before any remote signal
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t total = s_prefix[p.G] * p.NT + s_tpre[p.G] * ((p.NT + 1) / 2);
+    const uint32_t total = s_prefix[p.G] * p.NT;
     const uint32_t nkb = p.K / BK;
-    auto decode = [&](uint32_t tile) -> TileInfo {
-        if (p.wide) return decode_wide(tile, s_prefix, s_tpre, p.G, p.NT);
-        TileInfo t;
-        map_tile(tile, s_prefix, p.G, p.NT, t.g, t.m, t.n);
-        const uint32_t rows = s_off[t.g + 1] - s_off[t.g] - t.m * BM;
-        t.kind = (p.tail128 && rows <= HM) ? kTail : (EXT && rows > BM && rows <= BM + HM) ? kExt : kFull;
-        return t;
-    };
 
     if (warp == 0) {
         if (lane == 0) {
@@ -322,41 +248,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
             uint32_t it = 0;
             for (uint32_t tile = pair; tile < total; tile += npairs) {
-                const TileInfo ti = decode(tile);
-                const uint32_t g = ti.g, m = ti.m, n = ti.n;
-                const bool tail = ti.kind == kTail || ti.kind == kWide;  // M=128: 64 rows per CTA
-                const bool ext = EXT && ti.kind == kExt;                // + remainder rows 256 .. 383
-                const bool wide = ti.kind == kWide;
-                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * (tail ? HM / 2 : HM));
-                const int32_t xrow = static_cast<int32_t>(s_off[g] + m * BM + BM + rank * 64);
+                uint32_t g, m, n;
+                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * HM);
                 const int32_t brow = static_cast<int32_t>(s_gmap[g] * p.N_group + n * BN + rank * 128);
-                // the GEMM is bound by the operand feed (L2 -> SM), so a tail tile
-                // loads only the 64 A rows per CTA its M=128 MMA reads
-                const CUtensorMap* tA = tail ? &tmA64 : &tmA;
-                const uint32_t tx = 2 * (tail ? A_BYTES / 2 + B_BYTES : STAGE_BYTES + (ext ? X_BYTES : 0u));
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
-                    if (rank == 0) mbar_expect_tx(&full[s], tx);
+                    if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
                     const uint32_t fb = full_leader + s * 8;
-                    if (wide) {
-                        // the second N tile's B half rides in the next ring slot
-                        // (A slot unused): the MMA consumes both slots per k-block
-                        tma_load_2d_pair(sA + s * A_BYTES, &tmA64, fb, static_cast<int32_t>(kb * BK), arow);
-                        tma_load_2d_pair(sB + s * B_BYTES, &tmB, fb, static_cast<int32_t>(kb * BK), brow);
-                        ++it;
-                        const uint32_t s2 = it % NS, ph2 = (it / NS) & 1u;
-                        mbar_wait(&empty[s2], ph2 ^ 1u);
-                        if (rank == 0) mbar_expect_tx(&full[s2], 2 * B_BYTES);
-                        tma_load_2d_pair(sB + s2 * B_BYTES, &tmB, full_leader + s2 * 8, static_cast<int32_t>(kb * BK),
-                                         brow + static_cast<int32_t>(BN));
-                        continue;
-                    }
-                    if (ext) tma_load_2d_pair(sX + s * XB, &tmA64, fb, static_cast<int32_t>(kb * BK), xrow);
 #if MP_PAIR_HINTS & 2
-                    tma_load_2d_pair_hint(sA + s * A_BYTES, tA, fb, static_cast<int32_t>(kb * BK), arow, pol_a);
+                    tma_load_2d_pair_hint(sA + s * A_BYTES, &tmA, fb, static_cast<int32_t>(kb * BK), arow, pol_a);
 #else
-                    tma_load_2d_pair(sA + s * A_BYTES, tA, fb, static_cast<int32_t>(kb * BK), arow);
+                    tma_load_2d_pair(sA + s * A_BYTES, &tmA, fb, static_cast<int32_t>(kb * BK), arow);
 #endif
 #if MP_PAIR_HINTS & 1
                     tma_load_2d_pair_hint(sB + s * B_BYTES, &tmB, fb, static_cast<int32_t>(kb * BK), brow, pol_b);
@@ -368,66 +272,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (rank == 0 && lane == 0) {
-            constexpr uint32_t idesc_full = umma_idesc_bf16(BM, BN);
-            constexpr uint32_t idesc_tail = umma_idesc_bf16(HM, BN);
+            constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
             uint32_t it = 0, tc = 0;
-            uint32_t use0 = 0, use1 = 0;  // acquisitions of each 256-column accumulator buffer
-            auto acquire = [&](uint32_t b) {  // acquisition u waits for release u - 1 (phase parity)
-                const uint32_t u = b ? use1++ : use0++;
-                mbar_wait_cluster(&tempty[b], (u & 1u) ^ 1u);
-            };
 #if MP_PAIR_TRACE
             const uint64_t t_start = clock64();
             uint64_t w_acc = 0, w_full = 0;
 #endif
             for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
                 const uint32_t acc = tc & 1u;
-                const TileInfo ti = decode(tile);
-                const uint32_t idesc = (ti.kind == kTail || ti.kind == kWide) ? idesc_tail : idesc_full;
-                const bool ext = EXT && ti.kind == kExt;
-                const bool wide = ti.kind == kWide;
 #if MP_PAIR_TRACE
                 uint64_t t0 = clock64();
 #endif
-                acquire(acc);
-                // an extended tile also takes the first 128 columns of the other
-                // buffer for its M=128 remainder accumulator
-                if (ext) acquire(acc ^ 1u);
+                // acquisition tc of the buffer waits for its release tc - 2
+                mbar_wait_cluster(&tempty[acc], ((tc >> 1) & 1u) ^ 1u);
 #if MP_PAIR_TRACE
                 w_acc += clock64() - t0;
                 const uint64_t t_tile = clock64(), wf0 = w_full;
 #endif
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                const uint32_t x_tmem = tmem_base + (acc ^ 1u) * BN;
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
 #if MP_PAIR_TRACE
                     t0 = clock64();
 #endif
                     mbar_wait(&full[s], ph);
-                    if (wide) {
-                        ++it;
-                        const uint32_t s2 = it % NS, ph2 = (it / NS) & 1u;
-                        mbar_wait(&full[s2], ph2);
-#if MP_PAIR_TRACE
-                        w_full += clock64() - t0;
-#endif
-                        tc_fence_after();
-                        const uint32_t a0 = smem_u32(sA + s * A_BYTES);
-                        const uint32_t b0 = smem_u32(sB + s * B_BYTES), b1 = smem_u32(sB + s2 * B_BYTES);
-                        // two M=128 accumulators (128 TMEM columns each) in this buffer
-#pragma unroll
-                        for (uint32_t k = 0; k < BK / 16; ++k) {
-                            const uint64_t ad = umma_desc_sw128(a0 + k * 32);
-                            umma_bf16_pair(d_tmem, ad, umma_desc_sw128(b0 + k * 32), idesc_tail, (kb | k) != 0u);
-                            umma_bf16_pair(d_tmem + HM, ad, umma_desc_sw128(b1 + k * 32), idesc_tail,
-                                           (kb | k) != 0u);
-                        }
-                        umma_commit_pair(&empty[s]);
-                        umma_commit_pair(&empty[s2]);
-                        continue;
-                    }
 #if MP_PAIR_TRACE
                     w_full += clock64() - t0;
 #endif
@@ -438,13 +307,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     for (uint32_t k = 0; k < BK / 16; ++k)
                         umma_bf16_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
                                        (kb | k) != 0u);
-                    if (ext) {
-                        const uint32_t x0 = smem_u32(sX + s * XB);
-#pragma unroll
-                        for (uint32_t k = 0; k < BK / 16; ++k)
-                            umma_bf16_pair(x_tmem, umma_desc_sw128(x0 + k * 32), umma_desc_sw128(b0 + k * 32),
-                                           idesc_tail, (kb | k) != 0u);
-                    }
                     umma_commit_pair(&empty[s]);
                 }
                 umma_commit_pair(&tfull[acc]);
@@ -454,7 +316,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     r[0] = tile;
                     r[1] = w_full - wf0;
                     r[2] = clock64() - t_tile;
-                    r[3] = ti.kind;
+                    r[3] = 0;
                 }
 #endif
             }
@@ -473,26 +335,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
         const uint32_t part = (warp - 2) / 4, nparts = kEpiWarps / 4;  // column share of this warp
         const uint32_t tempty_leader = mapa(&tempty[0], 0);
-        // One accumulator to bf16 rows of the group.  full (M=256) shape: lane =
-        // row rank*128 + q*32 + lane, all 256 D columns; half (M=128) shape:
-        // lane l < 64 = row rank*64 + l with D columns [0,128), lane 64 + l =
-        // the same row with D columns [128,256).
-        auto emit = [&](uint32_t buf, uint32_t col0, uint32_t row0, bool m128, uint32_t g, uint32_t n, uint32_t cnt) {
-            const uint32_t row_local = row0 + (m128 ? rank * 64 + (q & 1u) * 32 + lane : rank * HM + q * 32 + lane);
-            const uint32_t half = m128 ? (q >> 1) : 0;  // which 128 D columns this lane holds (M=128)
-            const uint32_t nchunk = m128 ? 4 : 8;        // 32-column chunks of D held by the lane
+        // One accumulator to bf16 rows of the group: lane = row rank*128 +
+        // q*32 + lane, all 256 D columns.
+        auto emit = [&](uint32_t buf, uint32_t row0, uint32_t g, uint32_t n, uint32_t cnt) {
+            const uint32_t row_local = row0 + rank * HM + q * 32 + lane;
+            constexpr uint32_t nchunk = 8;  // 32-column chunks of D held by the lane
             const bool valid = row_local < cnt;
             const bool any = (row_local - lane) < cnt;  // warp has a valid row
             __nv_bfloat16* orow = p.out + static_cast<size_t>(s_off[g] + row_local) * p.ld_out;
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN + col0;
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN;
             if (!any) return;
             if constexpr (SWIGLU) {
                 // D chunk pair (gate, up) = columns (h*128 + c2*32, + 64) for
                 // neurons n*128 + h*64 + c2*32 .. +31
 #pragma unroll 1
                 for (uint32_t c = part; c < nchunk / 2; c += nparts) {
-                    const uint32_t h = m128 ? half : (c >> 1), c2 = c & 1u;
-                    const uint32_t tcol = (m128 ? 0 : h * 128) + c2 * 32;
+                    const uint32_t h = c >> 1, c2 = c & 1u;
+                    const uint32_t tcol = h * 128 + c2 * 32;
                     uint32_t gr[32], ur[32];
                     tmem_ld32(taddr + tcol, gr);
                     tmem_ld32(taddr + tcol + kIlv, ur);
@@ -513,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             } else {
                 auto store = [&](uint32_t c, const uint32_t* r) {
-                    const uint32_t col = n * BN + half * 128 + c * 32;
+                    const uint32_t col = n * BN + c * 32;
                     if (valid && col < p.n_valid) {
                         uint32_t pk[16];
 #pragma unroll
@@ -552,30 +411,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint64_t e_busy = 0, e_ext = 0, e_wait = 0;
 #endif
         for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
-            const TileInfo ti = decode(tile);
-            const uint32_t g = ti.g, m = ti.m, n = ti.n;
+            uint32_t g, m, n;
+            map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
             const uint32_t acc = tc & 1u;
 #if MP_PAIR_TRACE
             const uint64_t e0 = clock64();
 #endif
-            mbar_wait(&tfull[acc], (tc >> 1) & 1u);  // one commit per tile on its main buffer
+            mbar_wait(&tfull[acc], (tc >> 1) & 1u);  // one commit per tile on its buffer
             tc_fence_after();
 #if MP_PAIR_TRACE
             const uint64_t e1 = clock64();
             e_wait += e1 - e0;
 #endif
-            const uint32_t cnt = s_off[g + 1] - s_off[g];
-            if (EXT && ti.kind == kExt) {  // the group's last tile, merged remainder
-                // remainder first: the next tile's MMAs wait for that buffer
-                emit(acc ^ 1u, 0, m * BM + BM, true, g, n, cnt);
-                release(acc ^ 1u);
-            }
-            if (ti.kind == kWide) emit(acc, HM, m * BM, true, g, n + 1, cnt);  // second N tile
-#if MP_PAIR_TRACE
-            const uint64_t e2 = clock64();
-            e_ext += e2 - e1;
-#endif
-            emit(acc, 0, m * BM, ti.kind == kTail || ti.kind == kWide, g, n, cnt);
+            emit(acc, m * BM, g, n, s_off[g + 1] - s_off[g]);
             release(acc);
 #if MP_PAIR_TRACE
             e_busy += clock64() - e1;
@@ -602,41 +450,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-size_t gemm_pair_smem_bytes() { return kSmemBytesX > kSmemBytes ? kSmemBytesX : kSmemBytes; }
+size_t gemm_pair_smem_bytes() { return kSmemBytes; }
 
-// tmB: box of 128 rows (each CTA loads half of the 256-row B tile).  variant:
-// kPairPlain (prefix of ceil(count/256)), kPairTail128 (<= 128-row tails as
-// M=128 MMAs), kPairExt (merged prefix: <= 128-row remainders ride on the
-// previous tile as an extra M=128 MMA sharing its B tile).  tmA64: 64-row A box.
+// tmB: box of 128 rows (each CTA loads half of the 256-row B tile); mprefix256:
+// prefix of ceil(count_g / 256) over the groups.
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
-                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s, int variant,
-                     const uint32_t* gmap, const CUtensorMap* tmA64, const uint32_t* tprefix) {
-    if (!tmA64 || (variant == kPairWide && !tprefix)) variant = kPairPlain;  // tails need the 64-row A box
+                     const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
+                     const uint32_t* gmap) {
     PairParams p{sh.G, sh.K, sh.N_group, sh.n_valid, sh.ld_out, (sh.N_group + BN - 1) / BN, offsets, mprefix256,
-                 static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), variant == kPairTail128 ? 1u : 0u,
-                 variant == kPairExt ? 1u : 0u, variant == kPairWide ? 1u : 0u, tprefix, gmap};
+                 static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), gmap};
     if (p.trace) cudaMemsetAsync(p.trace, 0, (4096 + 128 * 128 * 4) * sizeof(uint64_t), s);
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;
     if (max_tiles < pairs) pairs = max_tiles;
     if (pairs == 0) pairs = 1;
-    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<true, false>), (int)kSmemBytes);
-    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<false, false>), (int)kSmemBytes);
-    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<true, true>), (int)kSmemBytesX);
-    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<false, true>), (int)kSmemBytesX);
-    const CUtensorMap& a64 = tmA64 ? *tmA64 : *tmA;
+    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<true>), (int)kSmemBytes);
+    func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<false>), (int)kSmemBytes);
     const dim3 grid(2 * pairs), block(kThreads);
-    if (p.ext) {
-        if (swiglu)
-            launch_k(gemm_pair_kernel<true, true>, grid, block, kSmemBytesX, s, *tmA, *tmB, a64, p);
-        else
-            launch_k(gemm_pair_kernel<false, true>, grid, block, kSmemBytesX, s, *tmA, *tmB, a64, p);
-    } else {
-        if (swiglu)
-            launch_k(gemm_pair_kernel<true, false>, grid, block, kSmemBytes, s, *tmA, *tmB, a64, p);
-        else
-            launch_k(gemm_pair_kernel<false, false>, grid, block, kSmemBytes, s, *tmA, *tmB, a64, p);
-    }
+    if (swiglu)
+        launch_k(gemm_pair_kernel<true>, grid, block, kSmemBytes, s, *tmA, *tmB, p);
+    else
+        launch_k(gemm_pair_kernel<false>, grid, block, kSmemBytes, s, *tmA, *tmB, p);
 }
 
 }  // namespace mp

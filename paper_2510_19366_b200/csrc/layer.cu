@@ -158,6 +158,9 @@ bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// shared-expert split-K (decode batches): at most kShSplitRows tokens, kShSplitMax K splits
+constexpr uint32_t kShSplitRows = 128, kShSplitMax = 24;
+
 const char* kStageNames[] = {"router", "bucket", "dispatch", "gemm1", "gemm2", "combine"};
 constexpr int kStages = 6;
 
@@ -170,8 +173,8 @@ struct mp_layer_s {
     size_t esz = 4;
     int num_sms = 0;
     bool use_tc = false;
-    // grouped-GEMM kernel: 0 auto (CTA pairs, gemm_tc2, when the mean bucket has
-    // >= 192 rows, else 1-SM 128-row tiles, gemm_tc); MOEPRISM_TC_TILE=128|256 forces
+    // grouped-GEMM kernel: 0 auto (CTA pairs, gemm_tc2, or 1-SM 128-row tiles,
+    // gemm_tc, by expected padding); MOEPRISM_TC_TILE=128|256 forces
     int tile_mode = 0;
     bool tile256 = false;  // this forward's choice
     bool has_experts = true, has_router = true;  // MP_LAYER_* role flags
@@ -198,8 +201,7 @@ struct mp_layer_s {
     uint32_t p_npad = 0;
     void* p_planes = nullptr;
     float* p_partial = nullptr;   // fp32 [ks][T][p_npad]
-    double* p_xnorm = nullptr;    // [ks][T]
-    double* p_win = nullptr;      // [max_tokens][3]
+    int8_t* p_class = nullptr;    // [max_tokens][G] certification classes of flagged tokens
     float p_wmax = 0.0f;
     CUtensorMap tm_pplanes{};
 
@@ -219,7 +221,6 @@ struct mp_layer_s {
     // Certification of the tensor-core logits (router_tc.cu): per token
     // guard_t = depth 2^-23 max|W_r| sum|x_t| + 2^-23 max|logit_t|; tokens whose
     // k-th/(k+1)-th gap is < 2 guard_t are re-selected from exact fp64 logits.
-    double* r_xnorm = nullptr;      // [ks][max_tokens] per-K-split sums of |x|
     float r_wmax = 0.0f;            // max |W_r|
     double r_guard_floor = 0.0;     // MOEPRISM_ROUTER_GUARD: extra absolute width (tests widen the window)
     CUtensorMap tm_wplanes{};
@@ -238,7 +239,6 @@ struct mp_layer_s {
     void* y_stage = nullptr;
     CUtensorMap tm_xperm{}, tm_h{}, tm_w1{}, tm_w2{};
     CUtensorMap tm_w1h{}, tm_w2h{};  // 128-row boxes: each CTA of a pair loads half a B tile
-    CUtensorMap tm_xperm64{}, tm_h64{};  // 64-row A boxes: M=128 tail tiles of the pair GEMM
 
     // shared (always-on) expert, Qwen-style: one dense group of sh_w_pad neurons
     uint32_t sh_ff = 0, sh_w_pad = 0, sh_w2_rows = 0;
@@ -247,6 +247,8 @@ struct mp_layer_s {
     float* sh_gate = nullptr;  // [d] or null (weight 1)
     void* sh_h = nullptr;      // [max_tokens][sh_w_pad]
     void* sh_o = nullptr;      // [max_tokens][d_pad]
+    float* sh_o32 = nullptr;   // [kShSplitMax][min(max_tokens, 128)][d_pad] fp32 split-K partials (decode)
+    uint32_t sh_splits = 0;    // this forward's split count (0: sh_o holds bf16 rows)
     float* sh_w = nullptr;     // [max_tokens]
     uint32_t* sh_meta = nullptr;  // offsets {0, T}, tile prefixes {0, ceil(T/128)}, {0, ceil(T/256)}
     CUtensorMap tm_w1s{}, tm_w2s{}, tm_hs{}, tm_w1sh{}, tm_w2sh{};
@@ -303,11 +305,11 @@ void free_layer(mp_layer_s* L) {
         if (p) cudaFree(p);
     for (void* p : {L->x_perm, L->h, L->o})
         if (p) L->shared_scratch ? scratch_release(p) : (void)cudaFree(p);
-    void* ptrs[] = {L->p_planes, L->p_partial, L->p_xnorm, L->p_win, L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_xnorm, L->r_flagged, L->r_ticket, L->d_nmap, L->nmap_all, L->sel,
+    void* ptrs[] = {L->p_planes, L->p_partial, L->p_class, L->gate_rows, L->up_rows, L->gate_off, L->scores, L->W1, L->W2, L->wrT, L->wr_planes, L->r_partial, L->r_flagged, L->r_ticket, L->d_nmap, L->nmap_all, L->sel,
                     L->wsel, L->kpt_dev, L->ws.lrank, L->ws.block_counts, L->ws.block_base, L->ws.offsets,
                     L->ws.mprefix_tc, L->ws.mprefix_simt, L->ws.mprefix_tc2, L->ws.perm_tok, L->ws.perm_w, L->ws.slot_row, L->ws.err,
                     L->x_stage, L->y_stage, L->W1s, L->W2s, L->sh_gate, L->sh_h,
-                    L->sh_o, L->sh_w, L->sh_meta, L->cal_meta};
+                    L->sh_o, L->sh_o32, L->sh_w, L->sh_meta, L->cal_meta};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (L->sh_stream) cudaStreamDestroy(L->sh_stream);
@@ -404,13 +406,11 @@ void pack_gates(mp_layer_s* L) {
     }
     cudaFree(d_neur);
     // tensor-core path: planes of [gate rows; up rows], partial buffers, max |W|
-    for (void* p : {L->p_planes, static_cast<void*>(L->p_partial), static_cast<void*>(L->p_xnorm),
-                    static_cast<void*>(L->p_win)})
+    for (void* p : {L->p_planes, static_cast<void*>(L->p_partial), static_cast<void*>(L->p_class)})
         if (p) cudaFree(p);
     L->p_planes = nullptr;
     L->p_partial = nullptr;
-    L->p_xnorm = nullptr;
-    L->p_win = nullptr;
+    L->p_class = nullptr;
     uint32_t max_list = 0;
     for (uint32_t g = 0; g < L->G; ++g) max_list = std::max(max_list, off[g + 1] - off[g]);
     L->proxy_tc = L->dtype == MP_DTYPE_BF16 && (L->d % 8) == 0 && L->n_gate_rows <= 1024 && max_list <= 1024;
@@ -423,8 +423,7 @@ void pack_gates(mp_layer_s* L) {
         mp::launch_split_rows(L->gate_rows, L->up_rows, L->n_gate_rows, L->n_gate_rows, L->d, L->p_npad, L->p_planes, 0);
         const size_t rows = mp::router_tc_partial_rows(L->max_tokens, L->d, nr2, L->num_sms);
         L->p_partial = dalloc<float>(rows * L->p_npad, "proxy partials");
-        L->p_xnorm = dalloc<double>(rows, "proxy |x| sums");
-        L->p_win = dalloc<double>((size_t)L->max_tokens * 3, "proxy windows");
+        L->p_class = dalloc<int8_t>((size_t)L->max_tokens * L->G, "proxy classes");
         ck(cudaMemset(L->ws.err + 1, 0, sizeof(int)), "memset");
         mp::launch_absmax(L->gate_rows, (size_t)L->n_gate_rows * L->d, reinterpret_cast<float*>(L->ws.err + 1), 0);
         mp::launch_absmax(L->up_rows, (size_t)L->n_gate_rows * L->d, reinterpret_cast<float*>(L->ws.err + 1), 0);
@@ -581,12 +580,29 @@ void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t
     mp::launch_shared_gate(x, T, L->d, L->sh_gate, L->sh_w, L->sh_meta, L->sh_meta + 2, ss);
     CUtensorMap tmX;
     if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "shared expert tensor map");
-    const bool sh_pair = L->tile_mode >= 2 || (L->tile_mode == 0 && T >= 192);
+    const bool sh_pair = L->tile_mode == 2 || (L->tile_mode == 0 && T >= 192);
     mp::GemmShape s1{1, L->d_pad, 2 * L->sh_w_pad, T, L->sh_w_pad, 2 * L->sh_w_pad};
     mp::GemmShape s2{1, L->sh_w_pad, L->d_pad, T, L->d_pad, L->d_pad};
-    if (sh_pair) {
-        mp::launch_gemm_tc2(true, &tmX, &L->tm_w1sh, L->sh_h, s1, L->sh_meta, L->sh_meta + 4, L->num_sms, ss);
-        mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, ss);
+    // small batches: the down projection has d_pad / 256 output tiles (8 CTAs
+    // at Qwen's d = 2048) over a long K (5632): split K over the idle SMs, fp32
+    // partials summed in split order by the combine
+    const uint32_t n_tiles = ((T + mp::kTcBM - 1) / mp::kTcBM) * (L->d_pad / 256);
+    L->sh_splits = 0;
+    if (!sh_pair && T <= kShSplitRows && n_tiles * 4 <= static_cast<uint32_t>(L->num_sms)) {
+        const uint32_t nkb = L->sh_w_pad / 64;
+        uint32_t want = std::min<uint32_t>(kShSplitMax, static_cast<uint32_t>(L->num_sms) / n_tiles);
+        want = std::max<uint32_t>(1, std::min(want, nkb));
+        const uint32_t kps = (nkb + want - 1) / want;
+        L->sh_splits = (nkb + kps - 1) / kps;
+    }
+    if (L->sh_splits) {
+        mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
+        mp::launch_gemm_tc_epi(mp::kEpiF32Part, &L->tm_hs, &L->tm_w2s, L->sh_o32, s2, L->sh_meta, L->sh_meta + 2,
+                               L->num_sms, ss, 0, nullptr, nullptr, nullptr, L->sh_splits);
+    } else if (sh_pair) {
+        mp::launch_gemm_tc2(true, &tmX, &L->tm_w1sh, L->sh_h, s1, L->sh_meta, L->sh_meta + 4, L->num_sms, ss, nullptr);
+        mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, ss,
+                            nullptr);
     } else {
         mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
         mp::launch_gemm_tc(false, &L->tm_hs, &L->tm_w2s, L->sh_o, s2, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
@@ -601,32 +617,22 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
                  cudaStream_t s, StageTimer& tm, bool check_finite = false, bool with_shared = false,
                  uint32_t kscalar = 0, bool bucketed = false) {
     // CTA-pair tiles pay up to 255 wasted rows per (sub-expert, N tile) against
-    // 127 for 128-row tiles; measured break-even near 192 rows per bucket
-    // (Mixtral shape: pairs win at k >= 4, lose at k = 2).  Per-token k: k_max.
-    // Auto choice: the kernel with fewer padded rows per bucket (expected over
-    // bucket sizes M +- sqrt(M), M = T k / G), CTA pairs credited 5% for
-    // their lower operand traffic (tests/probes/tile_ab.py: 128-row tiles win
-    // at k <= 8, pairs at k = 16 and the 32k-token mixed batch).  Opt-in
-    // merged schedule (mode 6): a remainder of <= 128 rows rides on the
-    // previous tile as an M=128 MMA sharing its B tile.
-    const bool ext = L->tile_mode == 6;
-    double rows = 0.0;
+    // 127 for 128-row tiles.  Auto choice: the kernel with fewer padded rows
+    // per bucket (expected over bucket sizes M +- sqrt(M), M = T k / G), CTA
+    // pairs credited 5% for their lower operand traffic (tests/probes/
+    // tile_ab.py: 128-row tiles win at k <= 8 at the Mixtral shape, pairs at
+    // k = 16 and the 32k-token mixed batch).  Per-token k: k_max.
     {
-        rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
+        const double rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
         const double sd = std::sqrt(rows > 1.0 ? rows : 1.0);
         double pad128 = 0.0, pad256 = 0.0;
         for (double m : {rows - sd, rows, rows + sd}) {
             const double mm = m < 1.0 ? 1.0 : m;
             pad128 += std::ceil(mm / 128.0) * 128.0;
-            if (ext) {
-                const double t = std::max(1.0, std::floor((mm + 127.0) / 256.0));
-                pad256 += (t + (mm > 256.0 * t ? 0.35 : 0.0)) * 256.0;
-            } else {
-                pad256 += std::ceil(mm / 256.0) * 256.0;
-            }
+            pad256 += std::ceil(mm / 256.0) * 256.0;
         }
         const bool pairs_win = pad256 / 1.05 < pad128;
-        L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && rows >= 192.0 && pairs_win);
+        L->tile256 = L->tile_mode == 2 || (L->tile_mode == 0 && rows >= 192.0 && pairs_win);
     }
     if (!bucketed) {
         tm.begin(1);
@@ -645,58 +651,35 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
     const uint32_t* gmap = L->offload ? L->gmap_dev : nullptr;
-    // split schedule (opt-in): full 256-row blocks (and remainders > 128 rows)
-    // on CTA pairs, remainders <= 128 rows as 128-row tiles on the 1-SM kernel
-    // Measured against (ncu, profiles/ncu_summary_r01b.json): the 1-SM tail
-    // kernel re-streams the tails' weight tiles from HBM (+0.9 GB at k=8 for
-    // gemm1; in the pair-only order the tail tile follows the full tiles of
-    // the same (sub-expert, N tile) and hits L2), so it is opt-in (mode 5).
-    const bool split = L->tile_mode == 5;
-    (void)rows;
-    const uint32_t G1 = L->G + 1;
-    const bool wide = L->tile_mode == 7;
-    const uint32_t* pre_pair = L->ws.mprefix_tc2 + ((split || wide) ? G1 : ext ? 4 * G1 : 0);
-    const int variant = ext    ? mp::kPairExt
-                        : wide ? mp::kPairWide
-                        : L->tile_mode == 4 ? mp::kPairTail128
-                                            : mp::kPairPlain;
-    const uint32_t* pre_tail = L->ws.mprefix_tc2 + 2 * G1;
-    const uint32_t* tail_start = L->ws.mprefix_tc2 + 3 * G1;
-    if (L->use_tc && L->tile256) {
+    if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
-                            pre_pair, L->num_sms, s, variant, gmap, &L->tm_xperm64, pre_tail);
-        if (split)
-            mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
-                               pre_tail, L->num_sms, s, gmap, tail_start);
-    } else if (L->use_tc)
+                            L->ws.mprefix_tc2, L->num_sms, s, gmap);
+    else if (L->use_tc)
         mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
                            L->ws.mprefix_tc, L->num_sms, s, gmap);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
     const bool shared = with_shared && L->sh_ff;
-    const int n_gemm = (L->use_tc && L->tile256 && split) ? 2 : 1;
-    tm.end(3, n_gemm);
+    tm.end(3, 1);
     tm.begin(4);
-    if (L->use_tc && L->tile256) {
+    if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
-                            pre_pair, L->num_sms, s, variant, gmap, &L->tm_h64, pre_tail);
-        if (split)
-            mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
-                               pre_tail, L->num_sms, s, gmap, tail_start);
-    } else if (L->use_tc)
+                            L->ws.mprefix_tc2, L->num_sms, s, gmap);
+    else if (L->use_tc)
         mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
                            L->ws.mprefix_tc, L->num_sms, s, gmap);
     else
         mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm2");
-    tm.end(4, n_gemm);
+    tm.end(4, 1);
     if (shared) ck(cudaStreamWaitEvent(s, L->sh_join, 0), "join shared expert");
     tm.begin(5);
     const uint32_t group_S = unit ? L->S : 0;
     mp::launch_combine(L->dtype, L->o, L->d, L->d_pad, L->ws.slot_row, sel, w, L->k_max, group_S, T, y, s,
-                       shared ? L->sh_o : nullptr, shared ? L->sh_w : nullptr,
-                       (with_shared && L->residual) ? x : nullptr);
+                       shared ? (L->sh_splits ? static_cast<const void*>(L->sh_o32) : L->sh_o) : nullptr,
+                       shared ? L->sh_w : nullptr, (with_shared && L->residual) ? x : nullptr,
+                       shared ? L->sh_splits : 0u, static_cast<size_t>(T) * L->d_pad);
     ck_launch("combine");
     tm.end(5, 1);
 }
@@ -724,16 +707,16 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             const mp::RouterTcPlan pl = mp::plan_router_tc(T, L->d, nr2, L->num_sms);
             CUtensorMap tmX;
             if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "proxy router tensor map");
-            mp::launch_router_tc(&tmX, &L->tm_pplanes, pl, T, L->p_partial, L->p_xnorm, s, true);
+            mp::launch_router_tc(&tmX, &L->tm_pplanes, pl, T, L->p_partial, s, true);
             // fp32 partials: one more rounding of <= 2^-24 sum|x||W| per token
-            const mp::RouterGuard rg{L->p_xnorm, pl.ks,
-                                     mp::router_guard_coef(pl.chunk_kb * 64, L->p_wmax) + 0x1.0p-24 * L->p_wmax,
+            const mp::RouterGuard rg{mp::router_guard_coef(pl.chunk_kb * 64, L->p_wmax) + 0x1.0p-24 * L->p_wmax,
                                      L->r_guard_floor};
             mp::launch_proxy_tc_topk(L->p_partial, pl.ks, T, L->n_gate_rows, L->p_npad, L->gate_off, L->G, L->k_max,
-                                     kpt, k, L->desc.weight_mode, L->sel, L->wsel, L->ws.err, rg, L->scores, L->p_win,
+                                     kpt, k, L->desc.weight_mode, L->sel, L->wsel, L->ws.err, rg, x, L->d, L->scores,
+                                     L->p_class,
                                      L->r_flagged, s);
             mp::launch_proxy_fixup(x, L->d, L->gate_rows, L->up_rows, L->gate_off, L->G, L->k_max, kpt, k,
-                                   L->desc.weight_mode, L->sel, L->wsel, L->ws.err, L->scores, L->p_win, L->r_flagged,
+                                   L->desc.weight_mode, L->sel, L->wsel, L->ws.err, L->scores, L->p_class, L->r_flagged,
                                    L->num_sms, s);
             ck_launch("router(proxy, tensor core)");
             tm.end(0, 3);
@@ -752,9 +735,8 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             const mp::RouterTcPlan pl = mp::plan_router_tc(T, L->d, L->G, L->num_sms);
             CUtensorMap tmX;
             if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "router tensor map");
-            mp::launch_router_tc(&tmX, &L->tm_wplanes, pl, T, L->r_partial, L->r_xnorm, s);
-            const mp::RouterGuard rg{L->r_xnorm, pl.ks, mp::router_guard_coef(pl.chunk_kb * 64, L->r_wmax),
-                                     L->r_guard_floor};
+            mp::launch_router_tc(&tmX, &L->tm_wplanes, pl, T, L->r_partial, s);
+            const mp::RouterGuard rg{mp::router_guard_coef(pl.chunk_kb * 64, L->r_wmax), L->r_guard_floor};
             L->r_last_ks = pl.ks;
             L->r_last_T = T;
             static const bool fuse_env = [] {  // MOEPRISM_FUSE_BUCKET=0: separate top-k / fixup / bucketing (A/B)
@@ -783,7 +765,7 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
                 tm.end(0, 2);
             } else {
                 mp::launch_partials_topk(L->r_partial, pl.ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
-                                         L->sel, L->wsel, L->ws.err, rg, L->r_flagged, s);
+                                         L->sel, L->wsel, L->ws.err, rg, x, L->d, L->r_flagged, s);
                 mp::launch_router_fixup(L->dtype, x, L->d, L->wrT, L->G, L->k_max, kpt, k, L->desc.weight_mode,
                                         L->sel, L->wsel, L->ws.err, L->r_flagged, L->num_sms, s);
                 ck_launch("router(tc)");
@@ -875,14 +857,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             if (const char* env = std::getenv("MOEPRISM_BF16_GEMM"))
                 if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
             if (const char* env = std::getenv("MOEPRISM_TC_TILE"))
-                L->tile_mode = std::string(env) == "256"           ? 2
-                               : std::string(env) == "128"         ? 1
-                               : std::string(env) == "256-notail"  ? 3
-                               : std::string(env) == "256-tail128" ? 4
-                               : std::string(env) == "256-split"   ? 5
-                               : std::string(env) == "256-merged"  ? 6
-                               : std::string(env) == "256-wide"    ? 7
-                                                                   : 0;
+                L->tile_mode = std::string(env) == "256" ? 2 : std::string(env) == "128" ? 1 : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
             L->d_pad = round_up(L->d, 64);
@@ -923,7 +898,6 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                     const size_t n_part = mp::router_tc_partial_rows(L->max_tokens, L->d, L->G, L->num_sms);
                     L->wr_planes = dalloc<char>((size_t)3 * L->r_npad * L->d * 2, "router planes");
                     L->r_partial = dalloc<double>(n_part * L->r_npad, "router partials");
-                    L->r_xnorm = dalloc<double>(n_part, "router |x| sums");
                     L->r_ticket = dalloc<uint32_t>(1, "router ticket");
                     ck(cudaMemset(L->r_ticket, 0, sizeof(uint32_t)), "memset ticket");
                     if (!mp::make_tmap_bf16_2d(&L->tm_wplanes, L->wr_planes, 3ull * L->r_npad, L->d,
@@ -953,7 +927,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 L->ws.offsets = dalloc<uint32_t>(L->G + 1, "offsets");
                 L->ws.mprefix_tc = dalloc<uint32_t>(L->G + 1, "mprefix");
                 L->ws.mprefix_simt = dalloc<uint32_t>(L->G + 1, "mprefix");
-                L->ws.mprefix_tc2 = dalloc<uint32_t>(5 * (L->G + 1), "mprefix");
+                L->ws.mprefix_tc2 = dalloc<uint32_t>(L->G + 1, "mprefix");
                 L->ws.perm_tok = dalloc<uint32_t>(L->rows_cap, "perm");
                 L->ws.perm_w = dalloc<float>(L->rows_cap, "perm w");
                 L->ws.slot_row = dalloc<uint32_t>(tk, "slot row");
@@ -978,9 +952,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                         mp::make_tmap_bf16_2d(&L->tm_h, L->h, L->rows_cap, L->w_pad, 128, 64) &&
                         mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64) &&
                         mp::make_tmap_bf16_2d(&L->tm_w1h, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 128, 64) &&
-                        mp::make_tmap_bf16_2d(&L->tm_w2h, L->W2, L->w2_rows, L->w_pad, 128, 64) &&
-                        mp::make_tmap_bf16_2d(&L->tm_xperm64, L->x_perm, L->rows_cap, L->d_pad, 64, 64) &&
-                        mp::make_tmap_bf16_2d(&L->tm_h64, L->h, L->rows_cap, L->w_pad, 64, 64);
+                        mp::make_tmap_bf16_2d(&L->tm_w2h, L->W2, L->w2_rows, L->w_pad, 128, 64);
                     if (!ok) fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                 }
             }
@@ -1168,6 +1140,8 @@ MP_API mp_status mp_layer_set_shared_expert(mp_layer_t L, uint32_t ff_sh, const 
             }
             L->sh_h = dalloc<char>((size_t)L->max_tokens * w_pad * 2, "shared h");
             L->sh_o = dalloc<char>((size_t)L->max_tokens * L->d_pad * 2, "shared o");
+            L->sh_o32 = dalloc<float>((size_t)kShSplitMax * std::min(L->max_tokens, kShSplitRows) * L->d_pad,
+                                      "shared split-K partials");
             L->sh_w = dalloc<float>(L->max_tokens, "shared w");
             L->sh_meta = dalloc<uint32_t>(6, "shared meta");
             bool ok = mp::make_tmap_bf16_2d(&L->tm_w1s, L->W1s, 2ull * w_pad, L->d_pad, 256, 64) &&
@@ -1184,6 +1158,7 @@ MP_API mp_status mp_layer_set_shared_expert(mp_layer_t L, uint32_t ff_sh, const 
             cudaFree(raw);
             if (nmap) cudaFree(nmap);
             for (void** p : {&L->W1s, &L->W2s, reinterpret_cast<void**>(&L->sh_gate), &L->sh_h, &L->sh_o,
+                             reinterpret_cast<void**>(&L->sh_o32),
                              reinterpret_cast<void**>(&L->sh_w), reinterpret_cast<void**>(&L->sh_meta)}) {
                 if (*p) cudaFree(*p);
                 *p = nullptr;
@@ -1601,19 +1576,12 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
 
 // Diagnostics (not in the public header): grouped-GEMM kernel choice of a
 // layer at run time, 0 auto / 1 one-SM 128-row tiles / 2 CTA-pair 256-row
-// tiles (the default order) / 3 the same / 4 pairs with M=128 tail MMAs
-// (64-row A loads; measured 4% slower per step: profiles/r01_tile_ab.txt) / 5
-// the split schedule (tails <= 128 rows on the 1-SM kernel; +0.9 GB of DRAM
-// weight re-reads at k=8: profiles/ncu_summary_r01b.json) / 6 pairs with
-// merged remainders (<= 128-row remainders as an extra M=128 MMA on the
-// group's previous tile; measured slower: the remainder accumulator takes
-// the other TMEM buffer, exposing an epilogue per merged tile) / 7 pairs
-// with wide tails (a <= 128-row remainder over two N tiles; measured slower:
-// the shared-memory operand traffic of two M=128 MMAs), for A/B timing
-// (tests/probes/tile_ab.py).
+// tiles, for A/B timing (tests/probes/tile_ab.py).  The remainder schedules
+// measured and dropped in round 1 (M=128 pair tails, the split schedule,
+// merged and wide remainders) are described in gemm_tc2.cu and DESIGN.md.
 MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {
-        if (!L || mode < 0 || mode > 7) fail(MP_ERR_VALIDATION, "bad argument");
+        if (!L || mode < 0 || mode > 2) fail(MP_ERR_VALIDATION, "bad argument");
         L->tile_mode = mode;
     });
 }

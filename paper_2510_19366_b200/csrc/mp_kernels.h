@@ -26,11 +26,7 @@ struct BucketWs {
     uint32_t* offsets;       // [G+1]
     uint32_t* mprefix_tc;    // [G+1] prefix of ceil(count/128)
     uint32_t* mprefix_simt;  // [G+1] prefix of ceil(count/64)
-    // [5][G+1]: prefix of ceil(count/256); pair-tile prefix of the split
-    // schedule (count/256 + (count%256 > 128)); its 1-SM tail-tile prefix
-    // (0 < count%256 <= 128); tail_start[g] (first row of that tail tile);
-    // merged (extended-tile) prefix max(1, (count + 127) / 256) (0 if empty)
-    uint32_t* mprefix_tc2;
+    uint32_t* mprefix_tc2;   // [G+1] prefix of ceil(count/256) (CTA-pair tiles)
     uint32_t* perm_tok;      // [rows]
     float* perm_w;           // [rows]
     uint32_t* slot_row;      // [T][k_max]
@@ -38,15 +34,13 @@ struct BucketWs {
 };
 
 // Certification bound of the tensor-core router logits for token t:
-//   guard_t = coef * sum_s xnorm[s][t] + 2^-23 * max_g |logit_tg| + floor_abs
-// coef = chunk depth * 2^-23 * max|W_r| * (1 + margin) (router_guard_coef).
+//   guard_t = coef * sum_i |x_ti| + 2^-23 * max_g |logit_tg| + floor_abs
+// coef = chunk depth * 2^-23 * max|W_r| * (1 + margin) (router_guard_coef);
+// sum |x_t| is formed by the consumer kernels from the bf16 row (L2-resident).
 struct RouterGuard {
-    const double* xnorm;  // [ks][T]
-    uint32_t ks;          // K splits of xnorm
     double coef;
-    double floor_abs;     // MOEPRISM_ROUTER_GUARD (tests widen the window), else 0
+    double floor_abs;  // MOEPRISM_ROUTER_GUARD (tests widen the window), else 0
 };
-
 // dtype: 0 f32, 1 bf16
 void launch_router_linear(int dtype, const void* x, uint32_t T, uint32_t d, const float* wrT, uint32_t G,
                           uint32_t k_max, const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
@@ -60,17 +54,18 @@ void launch_router_scores_topk(const float* scores, uint32_t T, uint32_t G, uint
 void launch_proxy_scores(int dtype, const void* x, uint32_t T, uint32_t d, const float* gate_w, const float* up_w,
                          const uint32_t* gate_off, uint32_t n_gate_rows, uint32_t G, float* scores, cudaStream_t s);
 // Tensor-core path: after launch_router_tc over the [gate; up] planes (fp32
-// partials), scores + per-token bound + certified top-k; uncertain tokens to
-// flagged[2..] with their window (a, b, guard) in pwin [T][3], re-selected by
-// launch_proxy_fixup from fp64 gate activations.
+// partials), scores + per-sub-expert bounds + certified top-k; uncertain
+// tokens to flagged[2..] with their scores in pscore [T][G] and per-sub-expert
+// classes in pclass [T][G], re-selected by launch_proxy_fixup from fp64 gate
+// activations.
 void launch_proxy_tc_topk(const float* partial, uint32_t ks, uint32_t T, uint32_t NR, uint32_t Npad,
                           const uint32_t* gate_off, uint32_t G, uint32_t k_max, const uint32_t* kpt, uint32_t k,
-                          int weight_mode, uint32_t* sel, float* w, int* err, const RouterGuard& rg, double* pscore,
-                          double* pwin, uint32_t* flagged, cudaStream_t s);
+                          int weight_mode, uint32_t* sel, float* w, int* err, const RouterGuard& rg, const void* x,
+                          uint32_t d, double* pscore, int8_t* pclass, uint32_t* flagged, cudaStream_t s);
 void launch_proxy_fixup(const void* x, uint32_t d, const float* gate_w, const float* up_w, const uint32_t* gate_off,
                         uint32_t G, uint32_t k_max, const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel,
-                        float* w, int* err, const double* pscore, const double* pwin, uint32_t* flagged, int num_sms,
-                        cudaStream_t s);
+                        float* w, int* err, const double* pscore, const int8_t* pclass, uint32_t* flagged,
+                        int num_sms, cudaStream_t s);
 void launch_bucket_local(const uint32_t* sel, uint32_t T, uint32_t k_max, uint32_t G, BucketWs& ws,
                          cudaStream_t s);
 void launch_bucket_scan(uint32_t T, uint32_t G, BucketWs& ws, cudaStream_t s);
@@ -83,12 +78,14 @@ void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t 
                      bool check_finite = true, uint32_t tb = kRouteTokensPerBlock);
 // group_S > 0: unit-weight semantics, round once per parent expert (fp32 mode)
 // o_sh / w_sh (bf16 only, nullable): shared-expert output rows [T][d_pad] and
-// per-token weights, added after the routed sub-experts; x_res (bf16 only,
-// nullable): residual input [T][d], y = x_res + sum (accumulator start value)
+// per-token weights, added after the routed sub-experts -- or, with
+// sh_splits > 0, fp32 split-K partials [sh_splits][sh_stride] summed in split
+// order; x_res (bf16 only, nullable): residual input [T][d], y = x_res + sum
+// (accumulator start value)
 void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
                     const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
                     cudaStream_t s, const void* o_sh = nullptr, const float* w_sh = nullptr,
-                    const void* x_res = nullptr);
+                    const void* x_res = nullptr, uint32_t sh_splits = 0, size_t sh_stride = 0);
 void launch_shared_gate(const void* x, uint32_t T, uint32_t d, const float* gate, float* w_sh, uint32_t* sh_off,
                         uint32_t* sh_mprefix, cudaStream_t s);
 
@@ -106,11 +103,10 @@ void launch_split_router(const float* wr, uint32_t d, uint32_t G, uint32_t Npad,
 // rows [n_a][d] ++ [n_b][d] (fp32) -> three bf16 planes [3][Npad][d]
 void launch_split_rows(const float* ra, const float* rb, uint32_t n_a, uint32_t n_b, uint32_t d, uint32_t Npad,
                        void* planes, cudaStream_t s);
-// xnorm: [ks][T] fp64 per-split sums of |x| (written by the column-split-0 CTAs)
 // out_f32: partials rounded to fp32 once per K split (the proxy router's
 // 2*E*S*r gate/up columns; the rounding adds <= 2^-24 sum|x||W| to the bound)
 void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const RouterTcPlan& pl, uint32_t T,
-                      void* partial, double* xnorm, cudaStream_t s, bool out_f32 = false);
+                      void* partial, cudaStream_t s, bool out_f32 = false);
 double router_guard_coef(uint32_t chunk_depth, float wmax);
 // Routing statistics of a forward (stats / flagged, zeroed by the caller):
 // [0] tokens re-selected from exact fp64 logits, [1] near ties (exact
@@ -120,7 +116,7 @@ double router_guard_coef(uint32_t chunk_depth, float wmax);
 // re-selected from exact fp64 logits by launch_router_fixup.
 void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                           const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
-                          const RouterGuard& rg, uint32_t* flagged, cudaStream_t s);
+                          const RouterGuard& rg, const void* x, uint32_t d, uint32_t* flagged, cudaStream_t s);
 // Fused routing epilogue of the tensor-core router (bf16 x, d % 4 == 0):
 // partials -> top-k -> exact re-selection of near-tie tokens (count added to
 // *n_fixed) -> bucket ranks -> device-wide scans (last CTA; *ticket must be
@@ -172,21 +168,18 @@ constexpr int kEpiPlain = 0;   // bf16 acc
 constexpr int kEpiSwiglu = 1;  // bf16 silu(gate) * up (fused SwiGLU)
 constexpr int kEpiActAbs = 2;  // fp32 |silu(gate) * up| scattered to colmap[packed neuron] (calibration)
 constexpr int kEpiCount = 3;   // uint32 counts (co-activation of 0/1 operands)
+constexpr int kEpiF32Part = 4; // fp32 split-K partials: out + split * max_rows * ld_out (ksplit of launch_gemm_tc_epi)
 // b_row0: first B row; colmap: kEpiActAbs column map; out: bf16 / f32 / u32 per mode
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                         uint32_t b_row0 = 0, const int32_t* colmap = nullptr, const uint32_t* gmap = nullptr,
-                        const uint32_t* starts = nullptr);
+                        const uint32_t* starts = nullptr, uint32_t ksplit = 1);
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
-constexpr int kPairPlain = 0, kPairTail128 = 1, kPairExt = 2, kPairWide = 3;
-// kPairWide: mprefix256 = the split schedule's pair-tile prefix, tprefix = its
-// <= 128-row remainder prefix (mprefix_tc2 + (G+1), + 2 (G+1))
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
-                     int variant = kPairPlain, const uint32_t* gmap = nullptr, const CUtensorMap* tmA64 = nullptr,
-                     const uint32_t* tprefix = nullptr);
+                     const uint32_t* gmap = nullptr);
 
 // Calibration (calib.cu).
 void launch_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,

@@ -14,6 +14,31 @@ namespace {
 
 constexpr double kNearTie = 1e-6;  // the routing contract's near-tie window (logit units)
 
+// sum_i |x_i| of one bf16 row, to every lane of the warp (the input of the
+// router certification bound).  16-byte loads, all of a lane's loads in
+// flight when d % 8 == 0 and the row is 16-byte aligned.  fp32 partial sums
+// per lane (relative error < 2^-16 at d <= 2^16, inside the bound's margin),
+// fp64 across lanes.
+__device__ __forceinline__ double warp_row_abs_sum(const __nv_bfloat16* __restrict__ xr, uint32_t d) {
+    const uint32_t lane = lane_id();
+    float s = 0.0f;
+    if ((d % 8) == 0 && (reinterpret_cast<uintptr_t>(xr) & 15u) == 0) {
+        for (uint32_t c = lane * 8; c < d; c += 256) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(xr + c));
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                s += fabsf(__uint_as_float(w[h] << 16)) + fabsf(__uint_as_float(w[h] & 0xFFFF0000u));
+        }
+    } else {
+        for (uint32_t c = lane; c < d; c += 32) s += fabsf(__bfloat162float(xr[c]));
+    }
+    double r = static_cast<double>(s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r;
+}
+
 // ---------------------------------------------------------------- top-k
 // One warp selects the k_t best of G scores for one token (score desc,
 // index asc -- inc/gating.hpp:138-141), emits them in ascending index order

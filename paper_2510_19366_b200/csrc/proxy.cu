@@ -16,10 +16,12 @@
 //    bf16 planes and run through the linear router's tcgen05 kernel
 //    (router_tc.cu, fp32 partials per K split); proxy_topk_kernel forms the
 //    scores with a per-neuron error bound propagated through SiLU, the
-//    product and the float rounding, certifies each token's selection
-//    (k-th/(k+1)-th gap > 2 guard + 1e-6) and queues the rest;
-//    proxy_fixup_kernel recomputes the uncertain window's gate neurons in
-//    fp64 and re-selects (+inf above the window, exact in it, -inf below).
+//    product and the float rounding, certifies each token's selection with
+//    per-sub-expert bounds (lowest lower bound inside the top-k above the
+//    highest upper bound outside, by more than the 1e-6 near-tie width) and
+//    queues the rest; proxy_fixup_kernel recomputes the uncertain
+//    sub-experts' gate neurons in fp64 and re-selects (+inf certainly in,
+//    exact uncertain, -inf certainly out).
 #include <cfloat>
 
 #include "mp_common.cuh"
@@ -34,6 +36,7 @@ namespace {
 // CTA = 32 tokens (lanes) x 32 gate neurons (warps); K staged in smem chunks.
 constexpr uint32_t XT = 32, XR = 32, XK = 32;
 constexpr uint32_t kMaxItems = 1024;  // gate neurons per exact batch of the fixup
+constexpr uint32_t kFixThreads = 512;
 
 template <typename Tx>
 __global__ void __launch_bounds__(1024) proxy_exact_act_kernel(const Tx* __restrict__ x, uint32_t T, uint32_t d,
@@ -94,30 +97,36 @@ __device__ __forceinline__ void proxy_neuron(double Gv, double Uv, double e, flo
 }
 
 // Warp per token (8 per CTA).  partial: fp32 [ks][T][Npad] with the gate
-// columns at [0, NR) and the up columns at [NR, 2 NR).  Scores of all G
-// sub-experts to pscore [T][G]; certified tokens get their selection here,
-// the others go to flagged[2 ..] with (a, b, guard) in pwin [T][3].
+// columns at [0, NR) and the up columns at [NR, 2 NR).  Every sub-expert g
+// gets a score s_g and an error bound e_g; the top-k of the scores is
+// certified when the smallest lower bound inside it (A) exceeds the largest
+// upper bound outside it (B) by more than the near-tie width: then the exact
+// top-k is the same and no exact gap is < 1e-6.  Otherwise the token goes to
+// flagged[2 ..] with its scores in pscore [T][G] and a class per sub-expert in
+// pclass [T][G]: +1 certainly selected (lower bound > B), -1 certainly not
+// (upper bound < A), 0 uncertain -- recomputed exactly by proxy_fixup_kernel.
 template <int NC>
 __global__ void __launch_bounds__(256) proxy_topk_kernel(const float* __restrict__ partial, uint32_t ks, uint32_t T,
                                                          uint32_t NR, uint32_t Npad, const uint32_t* __restrict__ off,
                                                          uint32_t G, uint32_t k_max, const uint32_t* __restrict__ kpt,
                                                          uint32_t k_scalar, int weight_mode, uint32_t* __restrict__ sel,
                                                          float* __restrict__ wout, int* __restrict__ err,
-                                                         RouterGuard rg, double* __restrict__ pscore,
-                                                         double* __restrict__ pwin, uint32_t* __restrict__ flagged) {
+                                                         RouterGuard rg, const __nv_bfloat16* __restrict__ x,
+                                                         uint32_t d, double* __restrict__ pscore,
+                                                         int8_t* __restrict__ pclass, uint32_t* __restrict__ flagged) {
     extern __shared__ __align__(16) unsigned char psm[];
+    __shared__ uint32_t selm[8][kMaxG / 32];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     float2* ae = reinterpret_cast<float2*>(psm) + (size_t)warp * NR;  // [NR] (|a|, error bound)
-    double* sc = reinterpret_cast<double*>(psm + sizeof(float2) * 8 * NR) + (size_t)warp * G;
+    double* sc = reinterpret_cast<double*>(psm + sizeof(float2) * 8 * NR) + (size_t)warp * 2 * G;
+    double* ec = sc + G;  // per sub-expert score error bound
     const uint32_t t = blockIdx.x * 8 + warp;
     griddep_wait();
     griddep_launch();
     if (t >= T) return;
-    double xn = 0.0;
-    for (uint32_t s = lane; s < rg.ks; s += 32) xn += rg.xnorm[(size_t)s * T + t];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) xn += __shfl_xor_sync(0xffffffffu, xn, o);
-    const double e = rg.coef * xn + rg.floor_abs;
+    const double xn = warp_row_abs_sum(x + (size_t)t * d, d);
+    double e = rg.coef * xn + rg.floor_abs;
+    if (!isfinite(e)) e = 0.0;  // non-finite input: raised by the dispatch scan
     for (uint32_t n = lane; n < NR; n += 32) {
         double Gv = 0.0, Uv = 0.0;
         for (uint32_t s = 0; s < ks; ++s) {
@@ -129,8 +138,8 @@ __global__ void __launch_bounds__(256) proxy_topk_kernel(const float* __restrict
         proxy_neuron(Gv, Uv, e, af, ea);
         ae[n] = make_float2(af, ea);
     }
+    if (lane < kMaxG / 32) selm[warp][lane] = 0;
     __syncwarp();
-    double guard = 0.0;
     for (uint32_t g = lane; g < G; g += 32) {
         double sum = 0.0, esum = 0.0;
         for (uint32_t r = off[g]; r < off[g + 1]; ++r) {
@@ -139,64 +148,78 @@ __global__ void __launch_bounds__(256) proxy_topk_kernel(const float* __restrict
         }
         const double cnt = static_cast<double>(off[g + 1] - off[g]);
         sc[g] = sum / cnt;
-        pscore[(size_t)t * G + g] = sum / cnt;
-        guard = fmax(guard, esum / cnt * (1.0 + 1e-9));
+        ec[g] = esum / cnt * (1.0 + 1e-9);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) guard = fmax(guard, __shfl_xor_sync(0xffffffffu, guard, o));
-    if (!isfinite(guard)) guard = 0.0;  // non-finite input: raised by the dispatch scan
     __syncwarp();
     const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
-    double vk[2];
-    const double gap = warp_topk_token<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
-                                           wout + (size_t)t * k_max, nullptr, vk);
-    const double a = __shfl_sync(0xffffffffu, vk[0], 0), b = __shfl_sync(0xffffffffu, vk[1], 0);
-    if (gap < 2.0 * guard + kNearTie && lane == 0) {
-        flagged[2 + atomicAdd(&flagged[0], 1u)] = t;
-        pwin[(size_t)t * 3 + 0] = a;
-        pwin[(size_t)t * 3 + 1] = b;
-        pwin[(size_t)t * 3 + 2] = guard;
+    uint32_t* srow = sel + (size_t)t * k_max;
+    warp_topk_token<NC>(sc, G, kt, k_max, weight_mode, srow, wout + (size_t)t * k_max);
+    __syncwarp();
+    for (uint32_t j = lane; j < kt; j += 32) {
+        const uint32_t g = srow[j];
+        atomicOr(&selm[warp][g >> 5], 1u << (g & 31));
     }
+    __syncwarp();
+    double A = DBL_MAX, B = -DBL_MAX;  // min lower bound inside, max upper bound outside
+    for (uint32_t g = lane; g < G; g += 32) {
+        if ((selm[warp][g >> 5] >> (g & 31)) & 1u)
+            A = fmin(A, sc[g] - ec[g]);
+        else
+            B = fmax(B, sc[g] + ec[g]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        A = fmin(A, __shfl_xor_sync(0xffffffffu, A, o));
+        B = fmax(B, __shfl_xor_sync(0xffffffffu, B, o));
+    }
+    if (A - B > kNearTie) return;  // certified (k == G: B = -DBL_MAX)
+    for (uint32_t g = lane; g < G; g += 32) {
+        const bool in = (selm[warp][g >> 5] >> (g & 31)) & 1u;
+        pscore[(size_t)t * G + g] = sc[g];
+        pclass[(size_t)t * G + g] = in ? (sc[g] - ec[g] > B ? 1 : 0) : (sc[g] + ec[g] < A ? -1 : 0);
+    }
+    if (lane == 0) flagged[2 + atomicAdd(&flagged[0], 1u)] = t;
 }
 
-// CTA per flagged token: the gate neurons of every sub-expert in the
-// uncertainty window recomputed in fp64 (warp per neuron, x row staged in
-// smem), the window's exact scores, and the re-selection.
+// CTA per flagged token: the gate neurons of every uncertain sub-expert
+// recomputed in fp64 (warp per neuron, x row staged in smem, 16-byte weight
+// loads with 16 in flight per lane), the exact scores, and the re-selection
+// on (+inf certainly selected, exact uncertain, -inf certainly not).
 template <typename Tx>
-__global__ void __launch_bounds__(1024) proxy_fixup_kernel(const Tx* __restrict__ x, uint32_t d,
-                                                           const float* __restrict__ gate_rows,
-                                                           const float* __restrict__ up_rows,
-                                                           const uint32_t* __restrict__ off, uint32_t G,
-                                                           uint32_t k_max, const uint32_t* __restrict__ kpt,
-                                                           uint32_t k_scalar, int weight_mode,
-                                                           uint32_t* __restrict__ sel, float* __restrict__ wout,
-                                                           int* __restrict__ err, const double* __restrict__ pscore,
-                                                           const double* __restrict__ pwin,
-                                                           uint32_t* __restrict__ flagged) {
-    extern __shared__ double xs_d[];  // [d]
+__global__ void __launch_bounds__(kFixThreads) proxy_fixup_kernel(const Tx* __restrict__ x, uint32_t d,
+                                                                  const float* __restrict__ gate_rows,
+                                                                  const float* __restrict__ up_rows,
+                                                                  const uint32_t* __restrict__ off, uint32_t G,
+                                                                  uint32_t k_max, const uint32_t* __restrict__ kpt,
+                                                                  uint32_t k_scalar, int weight_mode,
+                                                                  uint32_t* __restrict__ sel, float* __restrict__ wout,
+                                                                  int* __restrict__ err,
+                                                                  const double* __restrict__ pscore,
+                                                                  const int8_t* __restrict__ pclass,
+                                                                  uint32_t* __restrict__ flagged) {
+    extern __shared__ __align__(16) double xs_d[];  // [d]
     __shared__ double sc[kMaxG], key[kMaxG];
     __shared__ uint32_t wlist[kMaxG], gstart[kMaxG];
     __shared__ uint32_t items[kMaxItems];
     __shared__ float iact[kMaxItems];
     __shared__ uint32_t n_w, b1_s, n_items;
     const uint32_t n = flagged[0];
-    const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
     for (uint32_t f = blockIdx.x; f < n; f += gridDim.x) {
         const uint32_t t = flagged[2 + f];
-        const double a = pwin[(size_t)t * 3], b = pwin[(size_t)t * 3 + 1], gd = pwin[(size_t)t * 3 + 2];
         if (threadIdx.x == 0) n_w = 0;
         for (uint32_t i = threadIdx.x; i < d; i += blockDim.x) xs_d[i] = static_cast<double>(to_f32(x[(size_t)t * d + i]));
         __syncthreads();
         for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) {
             const double v = pscore[(size_t)t * G + g];
+            const int8_t c = pclass[(size_t)t * G + g];
             sc[g] = v;
-            const bool in_w = v >= b - 2.0 * gd && v <= a + 2.0 * gd;
-            key[g] = v > a + 2.0 * gd ? DBL_MAX : (in_w ? v : -DBL_MAX);
-            if (in_w) wlist[atomicAdd(&n_w, 1u)] = g;
+            key[g] = c > 0 ? DBL_MAX : (c < 0 ? -DBL_MAX : v);
+            if (c == 0) wlist[atomicAdd(&n_w, 1u)] = g;
         }
         __syncthreads();
-        // the window's gate neurons in batches of <= kMaxItems (pack_gates caps a
-        // sub-expert's gate list at kMaxItems for this path)
+        // the uncertain sub-experts' gate neurons in batches of <= kMaxItems
+        // (pack_gates caps a sub-expert's gate list at kMaxItems for this path)
         for (uint32_t b0 = 0; b0 < n_w;) {
             if (threadIdx.x == 0) {
                 uint32_t b1 = b0, m = 0;
@@ -210,30 +233,49 @@ __global__ void __launch_bounds__(1024) proxy_fixup_kernel(const Tx* __restrict_
             }
             __syncthreads();
             const uint32_t b1 = b1_s, ni = n_items;
-            for (uint32_t it = warp; it < ni; it += blockDim.x / 32) {
+            for (uint32_t it = warp; it < ni; it += nwarps) {
                 const uint32_t r = items[it];
                 const float* gw = gate_rows + (size_t)r * d;
                 const float* uw = up_rows + (size_t)r * d;
-                double ag[4] = {0, 0, 0, 0}, au[4] = {0, 0, 0, 0};
-                uint32_t i = lane;
-                for (; i + 96 < d; i += 128) {
+                double ag = 0.0, au = 0.0;
+                if ((d % 4) == 0) {
+                    // lane owns 4 consecutive inputs per 128-wide step; 8 steps in flight
+                    constexpr uint32_t U = 8;
+                    for (uint32_t i0 = 4 * lane; i0 < d; i0 += U * 128) {
+                        float4 gv[U], uv[U];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        ag[q] = fma(xs_d[i + 32 * q], static_cast<double>(__ldg(gw + i + 32 * q)), ag[q]);
-                        au[q] = fma(xs_d[i + 32 * q], static_cast<double>(__ldg(uw + i + 32 * q)), au[q]);
+                        for (uint32_t u = 0; u < U; ++u) {
+                            const uint32_t i = i0 + u * 128;
+                            gv[u] = i < d ? __ldg(reinterpret_cast<const float4*>(gw + i)) : make_float4(0, 0, 0, 0);
+                            uv[u] = i < d ? __ldg(reinterpret_cast<const float4*>(uw + i)) : make_float4(0, 0, 0, 0);
+                        }
+#pragma unroll
+                        for (uint32_t u = 0; u < U; ++u) {
+                            const uint32_t i = i0 + u * 128;
+                            if (i >= d) break;
+                            const double* xv = xs_d + i;
+                            ag = fma(xv[0], (double)gv[u].x, ag);
+                            ag = fma(xv[1], (double)gv[u].y, ag);
+                            ag = fma(xv[2], (double)gv[u].z, ag);
+                            ag = fma(xv[3], (double)gv[u].w, ag);
+                            au = fma(xv[0], (double)uv[u].x, au);
+                            au = fma(xv[1], (double)uv[u].y, au);
+                            au = fma(xv[2], (double)uv[u].z, au);
+                            au = fma(xv[3], (double)uv[u].w, au);
+                        }
+                    }
+                } else {
+                    for (uint32_t i = lane; i < d; i += 32) {
+                        ag = fma(xs_d[i], static_cast<double>(__ldg(gw + i)), ag);
+                        au = fma(xs_d[i], static_cast<double>(__ldg(uw + i)), au);
                     }
                 }
-                for (; i < d; i += 32) {
-                    ag[0] = fma(xs_d[i], static_cast<double>(__ldg(gw + i)), ag[0]);
-                    au[0] = fma(xs_d[i], static_cast<double>(__ldg(uw + i)), au[0]);
-                }
-                double Gv = (ag[0] + ag[1]) + (ag[2] + ag[3]), Uv = (au[0] + au[1]) + (au[2] + au[3]);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
-                    Gv += __shfl_xor_sync(0xffffffffu, Gv, o);
-                    Uv += __shfl_xor_sync(0xffffffffu, Uv, o);
+                    ag += __shfl_xor_sync(0xffffffffu, ag, o);
+                    au += __shfl_xor_sync(0xffffffffu, au, o);
                 }
-                if (lane == 0) iact[it] = fabsf(static_cast<float>(Gv / (1.0 + exp(-Gv)) * Uv));
+                if (lane == 0) iact[it] = fabsf(static_cast<float>(ag / (1.0 + exp(-ag)) * au));
             }
             __syncthreads();
             // exact scores of this batch: gate neurons in ascending order (inc/gating.hpp:114-123)
@@ -248,7 +290,7 @@ __global__ void __launch_bounds__(1024) proxy_fixup_kernel(const Tx* __restrict_
         }
         if (warp == 0) {
             const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
-            // the k-th / (k+1)-th keys both lie in the window: the gap is exact
+            // the k-th / (k+1)-th keys both lie among the uncertain: the gap is exact
             const double egap = warp_topk_token<kMaxG / 32>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
                                                             wout + (size_t)t * k_max, key);
             if (lane == 0 && egap < kNearTie) atomicAdd(&flagged[1], 1u);
@@ -280,13 +322,13 @@ void launch_proxy_scores(int dtype, const void* x, uint32_t T, uint32_t d, const
 
 void launch_proxy_tc_topk(const float* partial, uint32_t ks, uint32_t T, uint32_t NR, uint32_t Npad,
                           const uint32_t* gate_off, uint32_t G, uint32_t k_max, const uint32_t* kpt, uint32_t k,
-                          int weight_mode, uint32_t* sel, float* w, int* err, const RouterGuard& rg, double* pscore,
-                          double* pwin, uint32_t* flagged, cudaStream_t s) {
-    const size_t smem = 8 * (sizeof(float2) * NR + sizeof(double) * G);
+                          int weight_mode, uint32_t* sel, float* w, int* err, const RouterGuard& rg, const void* x,
+                          uint32_t d, double* pscore, int8_t* pclass, uint32_t* flagged, cudaStream_t s) {
+    const size_t smem = 8 * (sizeof(float2) * NR + 2 * sizeof(double) * G);
     auto go = [&](auto kern) {
         func_attr_once(reinterpret_cast<const void*>(kern), 200 * 1024);
         launch_k(kern, dim3((T + 7) / 8), dim3(256), smem, s, partial, ks, T, NR, Npad, gate_off, G, k_max, kpt, k,
-                 weight_mode, sel, w, err, rg, pscore, pwin, flagged);
+                 weight_mode, sel, w, err, rg, static_cast<const __nv_bfloat16*>(x), d, pscore, pclass, flagged);
     };
     if (G <= 64)
         go(proxy_topk_kernel<2>);
@@ -298,13 +340,13 @@ void launch_proxy_tc_topk(const float* partial, uint32_t ks, uint32_t T, uint32_
 
 void launch_proxy_fixup(const void* x, uint32_t d, const float* gate_w, const float* up_w, const uint32_t* gate_off,
                         uint32_t G, uint32_t k_max, const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel,
-                        float* w, int* err, const double* pscore, const double* pwin, uint32_t* flagged, int num_sms,
-                        cudaStream_t s) {
+                        float* w, int* err, const double* pscore, const int8_t* pclass, uint32_t* flagged,
+                        int num_sms, cudaStream_t s) {
     const size_t smem = sizeof(double) * d;
     auto kern = proxy_fixup_kernel<__nv_bfloat16>;
     func_attr_once(reinterpret_cast<const void*>(kern), 200 * 1024);
-    kern<<<num_sms, 1024, smem, s>>>(static_cast<const __nv_bfloat16*>(x), d, gate_w, up_w, gate_off, G, k_max, kpt,
-                                     k, weight_mode, sel, w, err, pscore, pwin, flagged);
+    kern<<<3 * num_sms, kFixThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(x), d, gate_w, up_w, gate_off, G,
+                                                k_max, kpt, k, weight_mode, sel, w, err, pscore, pclass, flagged);
 }
 
 }  // namespace mp

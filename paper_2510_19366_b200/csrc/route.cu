@@ -7,6 +7,7 @@
 // softmax renormalisation are the SURVEY 8(c) restatement;
 // bucketing / combine are SURVEY 8(a) a14/a15.  All HBM-bound: coalesced
 // 16-byte vector accesses, no atomics, fixed reduction orders (deterministic).
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 #include <string>
@@ -27,18 +28,13 @@ constexpr uint32_t KC = 32;                    // K chunk staged in smem
 constexpr uint32_t kRouterThreads = 256;
 
 // Per-token certification bound of the tensor-core router logits (RouterGuard,
-// mp_kernels.h): coef * sum |x_t| + 2^-23 max_g |logit_tg| + floor.  Warp-wide;
-// every lane gets the value.  Non-finite (bad input, raised elsewhere): 0, so
-// nothing is queued for the exact pass.
-__device__ __forceinline__ double warp_router_guard(const RouterGuard& rg, uint32_t T, uint32_t t, double maxabs) {
-    const uint32_t lane = lane_id();
-    double xn = 0.0;
-    for (uint32_t s = lane; s < rg.ks; s += 32) xn += rg.xnorm[(size_t)s * T + t];
+// mp_kernels.h): coef * sum |x_t| + 2^-23 max_g |logit_tg| + floor, with
+// xn = sum |x_t| (warp_row_abs_sum).  Warp-wide; every lane gets the value.
+// Non-finite (bad input, raised elsewhere): 0, so nothing is queued for the
+// exact pass.
+__device__ __forceinline__ double warp_router_guard(const RouterGuard& rg, double xn, double maxabs) {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        xn += __shfl_xor_sync(0xffffffffu, xn, off);
-        maxabs = fmax(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, off));
-    }
+    for (int off = 16; off > 0; off >>= 1) maxabs = fmax(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, off));
     const double g = rg.coef * xn + 0x1.0p-23 * maxabs + rg.floor_abs;
     return isfinite(g) ? g : 0.0;
 }
@@ -138,11 +134,13 @@ __global__ void __launch_bounds__(256) partials_topk_kernel(const double* __rest
                                                             const uint32_t* __restrict__ kpt, uint32_t k_scalar,
                                                             int weight_mode, uint32_t* __restrict__ sel,
                                                             float* __restrict__ wout, int* __restrict__ err,
-                                                            RouterGuard rg, uint32_t* __restrict__ flagged) {
+                                                            RouterGuard rg, const __nv_bfloat16* __restrict__ x,
+                                                            uint32_t d, uint32_t* __restrict__ flagged) {
     __shared__ double sc[8][kMaxG];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t t = blockIdx.x * 8 + warp;
     if (t >= T) return;
+    const double xn = warp_row_abs_sum(x + (size_t)t * d, d);
     double maxabs = 0.0;
     for (uint32_t g = lane; g < G; g += 32) {
         double v = 0.0;
@@ -150,7 +148,7 @@ __global__ void __launch_bounds__(256) partials_topk_kernel(const double* __rest
         sc[warp][g] = v;
         maxabs = fmax(maxabs, fabs(v));
     }
-    const double guard = warp_router_guard(rg, T, t, maxabs);
+    const double guard = warp_router_guard(rg, xn, maxabs);
     __syncwarp();
     const uint32_t kt = token_k(kpt, k_scalar, t, k_max, G, err);
     const double gap = warp_topk_token(sc[warp], G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
@@ -326,10 +324,27 @@ __device__ void block_exclusive_scan_1024_multi(uint32_t (&v)[V], uint32_t (&tot
 __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __restrict__ block_counts,
                                  uint32_t* __restrict__ block_base, uint32_t* __restrict__ offsets,
                                  uint32_t* __restrict__ mprefix_tc, uint32_t* __restrict__ mprefix_simt,
-                                 uint32_t* __restrict__ mprefix_tc2) {
+                                 uint32_t* __restrict__ mprefix_tc2, uint8_t* s_cnt) {
     // thread (g, q): bucket g, q-th contiguous range of CTA-blocks; consecutive
-    // threads read consecutive buckets of one block row (coalesced)
-    constexpr int V = 7;
+    // threads read consecutive buckets of one block row (coalesced).
+    // s_cnt (nullable): nblk x G bytes of shared memory -- the counts (<= 32
+    // tokens per block and bucket) are staged there with one coalesced pass, so
+    // both sweeps over them (sums, then bases) read shared memory instead of
+    // chains of L2 loads (Qwen prefill: 256 blocks x 240 buckets, 20 -> ~5 us)
+    constexpr int V = 4;
+    if (s_cnt) {
+        const uint32_t n = nblk * G;
+        const uint32_t n4 = (n % 4 == 0) ? n / 4 : 0;
+        for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x) {
+            const uint4 v = __ldcg(reinterpret_cast<const uint4*>(block_counts) + i);
+            reinterpret_cast<uint32_t*>(s_cnt)[i] = v.x | (v.y << 8) | (v.z << 16) | (v.w << 24);
+        }
+        for (uint32_t i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) s_cnt[i] = static_cast<uint8_t>(__ldcg(block_counts + i));
+        __syncthreads();
+    }
+    auto cnt = [&](uint32_t b, uint32_t gg) -> uint32_t {
+        return s_cnt ? s_cnt[(size_t)b * G + gg] : block_counts[(size_t)b * G + gg];
+    };
     __shared__ uint32_t part[1024];
     __shared__ uint32_t goff[kMaxG];
     __shared__ uint32_t wsum[V + 1][32];
@@ -344,7 +359,7 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     // 64 blocks per thread): the last CTA's scan is on the critical path
     if (active) {
 #pragma unroll 16
-        for (uint32_t b = b0; b < b1; ++b) sum += block_counts[(size_t)b * G + g];
+        for (uint32_t b = b0; b < b1; ++b) sum += cnt(b, g);
     }
     part[threadIdx.x] = sum;
     __syncthreads();
@@ -364,19 +379,9 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     const uint32_t c = gi < G ? goff[gi] : 0;
     MP_SCAN_STAMP(1);
     // bucket offsets and the GEMM tile prefixes, scanned together:
-    //   offsets (rows), 128-row tiles, 64-row SIMT tiles, 256-row pair tiles,
-    //   the split schedule's pair tiles (full 256-row blocks + a remainder
-    //   > 128 rows) and 1-SM tail tiles (remainder <= 128 rows), and the
-    //   merged schedule (a remainder <= 128 rows rides on the previous tile
-    //   as an extra M=128 MMA; groups of <= 256 rows: 1 tile)
-    const uint32_t rem = c % 256;
-    uint32_t sv[V] = {c,
-                      gi < G ? (c + kTcBM - 1) / kTcBM : 0u,
-                      gi < G ? (c + kSimtBM - 1) / kSimtBM : 0u,
-                      gi < G ? (c + 255) / 256 : 0u,
-                      gi < G ? c / 256 + (rem > 128 ? 1u : 0u) : 0u,
-                      gi < G ? ((rem > 0 && rem <= 128) ? 1u : 0u) : 0u,
-                      gi < G ? (c == 0 ? 0u : max(1u, (c + 127) / 256)) : 0u};
+    //   offsets (rows), 128-row tiles, 64-row SIMT tiles, 256-row pair tiles
+    uint32_t sv[V] = {c, gi < G ? (c + kTcBM - 1) / kTcBM : 0u, gi < G ? (c + kSimtBM - 1) / kSimtBM : 0u,
+                      gi < G ? (c + 255) / 256 : 0u};
     uint32_t tot[V];
     block_exclusive_scan_1024_multi<V>(sv, tot, wsum);
     const uint32_t off = sv[0];
@@ -385,19 +390,12 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
         mprefix_tc[gi] = sv[1];
         mprefix_simt[gi] = sv[2];
         mprefix_tc2[gi] = sv[3];
-        mprefix_tc2[(G + 1) + gi] = sv[4];
-        mprefix_tc2[2 * (G + 1) + gi] = sv[5];
-        mprefix_tc2[3 * (G + 1) + gi] = off + c - rem;  // tail_start
-        mprefix_tc2[4 * (G + 1) + gi] = sv[6];
     }
     if (gi == 0) {
         offsets[G] = tot[0];
         mprefix_tc[G] = tot[1];
         mprefix_simt[G] = tot[2];
         mprefix_tc2[G] = tot[3];
-        mprefix_tc2[(G + 1) + G] = tot[4];
-        mprefix_tc2[2 * (G + 1) + G] = tot[5];
-        mprefix_tc2[4 * (G + 1) + G] = tot[6];
     }
     __syncthreads();
     if (gi < G) goff[gi] = off;
@@ -409,7 +407,7 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
         for (uint32_t b = b0; b < b1; b += U) {
             uint32_t v[U];
 #pragma unroll
-            for (uint32_t u = 0; u < U; ++u) v[u] = b + u < b1 ? block_counts[(size_t)(b + u) * G + g] : 0u;
+            for (uint32_t u = 0; u < U; ++u) v[u] = b + u < b1 ? cnt(b + u, g) : 0u;
 #pragma unroll
             for (uint32_t u = 0; u < U; ++u) {
                 if (b + u < b1) block_base[(size_t)(b + u) * G + g] = running;
@@ -426,7 +424,7 @@ __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32
                                                            uint32_t* __restrict__ mprefix_tc,
                                                            uint32_t* __restrict__ mprefix_simt,
                                                            uint32_t* __restrict__ mprefix_tc2) {
-    bucket_scan_body(nblk, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt, mprefix_tc2);
+    bucket_scan_body(nblk, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt, mprefix_tc2, nullptr);
 }
 
 // Exact fp64 logit x_t . W_r[:, g] by one warp: bf16 x and fp32 W_r are exact
@@ -468,7 +466,7 @@ __device__ double warp_exact_logit(const __nv_bfloat16* __restrict__ xr, const f
 __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __restrict__ block_counts,
                                  uint32_t* __restrict__ block_base, uint32_t* __restrict__ offsets,
                                  uint32_t* __restrict__ mprefix_tc, uint32_t* __restrict__ mprefix_simt,
-                                 uint32_t* __restrict__ mprefix_tc2);
+                                 uint32_t* __restrict__ mprefix_tc2, uint8_t* s_cnt);
 
 // Fused routing epilogue of the tensor-core router, CTA = 32 tokens (warp per
 // token), replacing partials_topk + router_fixup + bucket_local + bucket_scan:
@@ -490,8 +488,8 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     float* __restrict__ wout, int* __restrict__ err, RouterGuard rg, const __nv_bfloat16* __restrict__ x, uint32_t d,
     const float* __restrict__ wrT, uint32_t* __restrict__ ticket, uint32_t* __restrict__ stats, uint32_t* lrank,
     uint32_t* block_counts, uint32_t* block_base, uint32_t* offsets, uint32_t* mprefix_tc, uint32_t* mprefix_simt,
-    uint32_t* mprefix_tc2, uint32_t tb) {
-    extern __shared__ double rsm[];  // [tb][G] logits, then [tb][G] keys
+    uint32_t* mprefix_tc2, uint32_t tb, uint32_t smem_bytes) {
+    extern __shared__ double rsm[];  // [tb][G] logits, then [tb][G] keys; the last CTA: staged counts
     double* sc = rsm + (size_t)(threadIdx.x / 32) * G;        // used by warps < tb only
     double* key = rsm + (size_t)(tb + threadIdx.x / 32) * G;
     __shared__ double vk[TB][2];
@@ -525,6 +523,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     uint32_t kt = 0;
     double guard = 0.0;
     if (t < T) {
+        const double xn = warp_row_abs_sum(x + (size_t)t * d, d);  // certification bound input
         // fixed-order sum over the K splits; all NC loads of a split in flight
         // (the partials come from L2 / HBM: a load per candidate in turn left
         // this phase latency-bound, 7 us for 240 candidates)
@@ -547,7 +546,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
                 sc[lane + 32u * c] = v[c];
                 maxabs = fmax(maxabs, fabs(v[c]));
             }
-        guard = warp_router_guard(rg, T, t, maxabs);
+        guard = warp_router_guard(rg, xn, maxabs);
         __syncwarp();
         kt = token_k(kpt, k_scalar, t, k_max, G, err);
         const double gap = warp_topk_fast<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
@@ -635,10 +634,17 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         if (has) lrank[(size_t)(t0 + lane) * k_max + slot_of[lane][g]] = __popc(bal & ((1u << lane) - 1u));
         if (lane == 0) block_counts[(size_t)blockIdx.x * G + g] = __popc(bal);
     }
-    __threadfence();
+    // this CTA's writes (selection, weights, ranks, counts) are ordered before
+    // the ticket by the barrier + one gpu-scope fence of the ticket thread
+    // (fences are cumulative over what the barrier made visible to it)
     __syncthreads();
     MP_RT_STAMP();  // 3: ranks done
-    if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        // release (acq_rel: not the heavier sequentially consistent fence)
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        if (is_last) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire every CTA's writes
+    }
     __syncthreads();
     MP_RT_STAMP();  // 4: ticket taken
 #if MP_ROUTE_TRACE
@@ -646,9 +652,11 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         printf("route_bucket blk %u: topk %llu exact %llu ranks %llu ticket %llu ns (start %llu)\n", blockIdx.x,
                tr_[1] - tr_[0], tr_[2] - tr_[1], tr_[3] - tr_[2], tr_[4] - tr_[3], tr_[0]);
 #endif
-    if (!is_last) return;
-    __threadfence();
-    bucket_scan_body(gridDim.x, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt, mprefix_tc2);
+    if (!is_last) return;  // the barrier above extends thread 0's acquire to the CTA
+    // the CTA's routing smem is free now: stage the counts there when they fit
+    const bool stage = (size_t)gridDim.x * G <= smem_bytes;
+    bucket_scan_body(gridDim.x, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt, mprefix_tc2,
+                     stage ? reinterpret_cast<uint8_t*>(rsm) : nullptr);
 #if MP_ROUTE_TRACE
     __syncthreads();
     MP_RT_STAMP();  // 5: scan done
@@ -821,6 +829,8 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
                                                            const float* __restrict__ w, uint32_t k_max,
                                                            const __nv_bfloat16* __restrict__ o_sh,
                                                            const float* __restrict__ w_sh,
+                                                           const float* __restrict__ o_sh32, uint32_t sh_splits,
+                                                           size_t sh_stride,
                                                            const __nv_bfloat16* __restrict__ x_res,
                                                            __nv_bfloat16* __restrict__ y) {
     __shared__ uint32_t rows[kMaxG];
@@ -860,7 +870,19 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
                     acc[2 * q + 1] = fmaf(wj, f.y, acc[2 * q + 1]);
                 }
             }
-            if (o_sh) {  // shared expert last (its ids follow the routed ones)
+            if (o_sh32) {  // shared expert from split-K fp32 partials, summed in split order
+                float sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (uint32_t sp = 0; sp < sh_splits; ++sp) {
+                    const float* pr = o_sh32 + sp * sh_stride + (size_t)t * d_pad + c;
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(pr));
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(pr + 4));
+                    sum[0] += a.x, sum[1] += a.y, sum[2] += a.z, sum[3] += a.w;
+                    sum[4] += b.x, sum[5] += b.y, sum[6] += b.z, sum[7] += b.w;
+                }
+                const float ws = w_sh[t];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[q] = fmaf(ws, sum[q], acc[q]);
+            } else if (o_sh) {  // shared expert last (its ids follow the routed ones)
                 const float ws = w_sh[t];
                 const uint4 v = __ldg(reinterpret_cast<const uint4*>(o_sh + (size_t)t * d_pad + c));
                 const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
@@ -883,7 +905,13 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
             float acc = x_res ? __bfloat162float(x_res[(size_t)t * d + c]) : 0.0f;
             for (uint32_t j = 0; j < k_max; ++j)
                 if (rows[j] != kSelNone) acc = fmaf(wts[j], __bfloat162float(o[(size_t)rows[j] * d_pad + c]), acc);
-            if (o_sh) acc = fmaf(w_sh[t], __bfloat162float(o_sh[(size_t)t * d_pad + c]), acc);
+            if (o_sh32) {
+                float sum = 0.0f;
+                for (uint32_t sp = 0; sp < sh_splits; ++sp) sum += o_sh32[sp * sh_stride + (size_t)t * d_pad + c];
+                acc = fmaf(w_sh[t], sum, acc);
+            } else if (o_sh) {
+                acc = fmaf(w_sh[t], __bfloat162float(o_sh[(size_t)t * d_pad + c]), acc);
+            }
             yr[c] = __float2bfloat16_rn(acc);
         }
     }
@@ -959,9 +987,9 @@ void launch_router_linear(int dtype, const void* x, uint32_t T, uint32_t d, cons
 
 void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                           const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w, int* err,
-                          const RouterGuard& rg, uint32_t* flagged, cudaStream_t s) {
+                          const RouterGuard& rg, const void* x, uint32_t d, uint32_t* flagged, cudaStream_t s) {
     partials_topk_kernel<<<(T + 7) / 8, 256, 0, s>>>(partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w,
-                                                     err, rg, flagged);
+                                                     err, rg, static_cast<const __nv_bfloat16*>(x), d, flagged);
 }
 
 // In-place fixed-order reduction of the K-split router partials into plane 0
@@ -992,15 +1020,20 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
                          const RouterGuard& rg, const void* x, uint32_t d, const float* wrT, uint32_t* ticket,
                          uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb) {
-    const size_t smem = sizeof(double) * 2 * tb * G;
+    // the routing arrays, or the last CTA's staged counts (1 byte per block and
+    // bucket) when they are larger and fit
+    const size_t nblk = (T + tb - 1) / tb;
+    size_t smem = sizeof(double) * 2 * tb * G;
+    if (nblk * G > smem && nblk * G <= 160 * 1024) smem = (nblk * G + 15) & ~size_t(15);
     auto launch = [&](auto kern) {
         // same shared-memory carveout as the GEMMs around it: no L1/smem
         // reconfiguration between the kernels of the chain
-        func_attr_once(reinterpret_cast<const void*>(kern), (int)(sizeof(double) * 2 * TB * kMaxG), true);
+        func_attr_once(reinterpret_cast<const void*>(kern), (int)std::max<size_t>(sizeof(double) * 2 * TB * kMaxG,
+                                                                                  160 * 1024), true);
         launch_k(kern, dim3((T + tb - 1) / tb), dim3(1024), smem, s,
             partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, rg,
             static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, stats, ws.lrank, ws.block_counts, ws.block_base,
-            ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb);
+            ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb, static_cast<uint32_t>(smem));
     };
     if (G <= 64)
         launch(route_bucket_kernel<2>);
@@ -1101,7 +1134,26 @@ __global__ void __launch_bounds__(256) shared_gate_kernel(const __nv_bfloat16* _
     }
     const __nv_bfloat16* xr = x + (size_t)t * d;
     float acc = 0.0f;
-    for (uint32_t c = lane; c < d; c += 32) acc = fmaf(__bfloat162float(xr[c]), gate[c], acc);
+    if ((d % 8) == 0) {  // 16-byte loads of x, all of a lane's loads in flight
+        for (uint32_t c = lane * 8; c < d; c += 256) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(xr + c));
+            const float4 g0 = __ldg(reinterpret_cast<const float4*>(gate + c));
+            const float4 g1 = __ldg(reinterpret_cast<const float4*>(gate + c + 4));
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+            const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+            const float2 e = __bfloat1622float2(h[2]), f = __bfloat1622float2(h[3]);
+            acc = fmaf(a.x, g0.x, acc);
+            acc = fmaf(a.y, g0.y, acc);
+            acc = fmaf(b.x, g0.z, acc);
+            acc = fmaf(b.y, g0.w, acc);
+            acc = fmaf(e.x, g1.x, acc);
+            acc = fmaf(e.y, g1.y, acc);
+            acc = fmaf(f.x, g1.z, acc);
+            acc = fmaf(f.y, g1.w, acc);
+        }
+    } else {
+        for (uint32_t c = lane; c < d; c += 32) acc = fmaf(__bfloat162float(xr[c]), gate[c], acc);
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if (lane == 0) w_sh[t] = 1.0f / (1.0f + expf(-acc));
@@ -1115,12 +1167,14 @@ void launch_shared_gate(const void* x, uint32_t T, uint32_t d, const float* gate
 
 void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
                     const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
-                    cudaStream_t s, const void* o_sh, const float* w_sh, const void* x_res) {
+                    cudaStream_t s, const void* o_sh, const float* w_sh, const void* x_res, uint32_t sh_splits,
+                    size_t sh_stride) {
+    // sh_splits > 0: o_sh holds fp32 split-K partials [sh_splits][stride]
+    const float* o_sh32 = sh_splits ? static_cast<const float*>(o_sh) : nullptr;
     if (dtype == 1)
         launch_k(combine_bf16_kernel, dim3(T), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(o), d, d_pad,
-                 slot_row, w, k_max,
-                                              static_cast<const __nv_bfloat16*>(o_sh), w_sh,
-                                              static_cast<const __nv_bfloat16*>(x_res),
+                 slot_row, w, k_max, sh_splits ? nullptr : static_cast<const __nv_bfloat16*>(o_sh), w_sh, o_sh32,
+                 sh_splits, sh_stride, static_cast<const __nv_bfloat16*>(x_res),
                                               static_cast<__nv_bfloat16*>(y));
     else
         combine_f64_kernel<<<T, 256, 0, s>>>(static_cast<const double*>(o), d, d_pad, slot_row, sel, w, k_max, group_S,

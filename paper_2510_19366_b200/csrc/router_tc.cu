@@ -13,8 +13,8 @@
 // most depth * 2^-23 * sum_i |x_i| |W_ig| (every fp32 addition inside a
 // chunk, however the MMA orders them, loses at most one ulp of a running sum
 // bounded by the chunk's sum of |products|; 2^-23 also covers truncation).
-// The kernel emits the per-token sum |x| of each K split for that bound
-// (route.cu warp_router_guard), and -- because a bound is not bit-exactness --
+// The consumers form that bound per token (route.cu warp_router_guard, with
+// sum_i |x_i| from the bf16 row), and -- because a bound is not bit-exactness --
 // every token whose k-th/(k+1)-th gap is within twice its bound is re-selected
 // from exact fp64 logits (route.cu route_bucket_kernel / router_fixup_kernel):
 // the selection is certified for every token, at any input scale.
@@ -36,7 +36,6 @@ struct RouterTcParams {
     uint32_t T, Npad, kb_total, kb_per_split, stages, chunk_kb;
     uint32_t ncta, nsplit;  // columns per CTA, column splits (blockIdx.y = K split * nsplit + column split)
     void* partial;          // [KS][T][Npad] fp64, or fp32 when out_f32 (rounded once per split)
-    double* xnorm;          // [KS][T] partial sums of |x| over each K split (the error bound's input)
     uint32_t out_f32;
 };
 
@@ -59,15 +58,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t kb0 = ksplit * p.kb_per_split;
     const uint32_t kb1 = min(kb0 + p.kb_per_split, p.kb_total);
 
-    // the column-split-0 CTA of a K split also sums |x| per token over its K
-    // range: its 4 epilogue warps (idle until the accumulators are complete)
-    // read each A stage before it is released, so a stage's empty barrier
-    // then waits for the MMA commit and those 4 warps
-    const bool do_norm = n0 == 0;
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], do_norm ? 5u : 1u);
+            mbar_init(&empty[s], 1);
         }
         mbar_init(tfull, 1);
         fence_mbar_init();
@@ -126,33 +120,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
     } else {
         const uint32_t q = warp & 3u;
-        if (do_norm) {
-            // row r of a stage's A tile is 128 contiguous bytes (SW128 permutes
-            // its 16-byte chunks, which a row sum does not care about)
-            double nrm = 0.0;
-            const uint32_t r = q * 32 + lane;
-            for (uint32_t kb = kb0, it = 0; kb < kb1; ++kb, ++it) {
-                const uint32_t s = it % p.stages, ph = (it / p.stages) & 1u;
-                mbar_wait(&full[s], ph);
-                const uint4* row = reinterpret_cast<const uint4*>(base + s * stage_bytes + r * 128u);
-                float acc = 0.0f;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const uint4 v = row[c];
-                    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        acc += fabsf(__uint_as_float(wv[h] << 16));
-                        acc += fabsf(__uint_as_float(wv[h] & 0xFFFF0000u));
-                    }
-                }
-                nrm += static_cast<double>(acc);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-            }
-            const uint32_t t = m0 + r;
-            if (t < p.T) p.xnorm[static_cast<size_t>(ksplit) * p.T + t] = nrm;
-        }
         mbar_wait(tfull, 0);
         tc_fence_after();
         const uint32_t t = m0 + q * 32 + lane;
@@ -299,9 +266,9 @@ void launch_split_router(const float* wr, uint32_t d, uint32_t G, uint32_t Npad,
 }
 
 void launch_router_tc(const CUtensorMap* tmX, const CUtensorMap* tmW, const RouterTcPlan& pl, uint32_t T,
-                      void* partial, double* xnorm, cudaStream_t s, bool out_f32) {
+                      void* partial, cudaStream_t s, bool out_f32) {
     RouterTcParams p{T,       pl.Npad,   pl.kb_total, pl.kb_per_split, pl.stages, pl.chunk_kb, pl.ncta, pl.nsplit,
-                     partial, xnorm, out_f32 ? 1u : 0u};
+                     partial, out_f32 ? 1u : 0u};
     func_attr_once(reinterpret_cast<const void*>(router_tc_kernel), 227 * 1024);
     launch_k(router_tc_kernel, dim3(pl.m_tiles, pl.ks * pl.nsplit), dim3(kThreads), pl.smem, s, *tmX, *tmW, p);
 }

@@ -29,7 +29,7 @@ def layer(E, S, d, ff, T, k_max, shared=0):
 
 x = synth_fill(torch.empty((1024, 512), dtype=torch.bfloat16, device="cuda"), 11, 1.0)
 L = layer(4, 4, 512, 1024, 1024, 16)
-for mode in (0, 1, 3, 4, 5, 6):
+for mode in (0, 1, 2):
     _lib.check(lib.mp_debug_set_tile_mode(L.h, mode))
     for k in (4, 16):
         L.forward(x, k=k)

@@ -3,8 +3,8 @@ Under the 1000 W cap the clock follows power, so wall time alone is noisy
 across blocks; energy per step (NVML total energy) is the power-robust
 metric: at the cap, throughput ~ P_cap / energy_per_step.
   python tests/probes/tile_ab.py <k-list> <mode-list> [reps] [steps-per-block] [qwen]
-modes: 1 128-row 1-SM, 2 pairs, 4 pairs with M=128 tails, 5 pairs + 1-SM tails (split),
-6 pairs with merged remainders; "qwen": the Qwen layer at T=8192 instead of Mixtral T=4096"""
+modes: 1 128-row 1-SM, 2 pairs (modes 4-7 of round 1 -- tail / split / merged / wide
+remainders -- were removed after measuring slower); "qwen": the Qwen layer at T=8192 instead of Mixtral T=4096"""
 import ctypes as C, statistics, sys
 import torch
 sys.path.insert(0, '.')
