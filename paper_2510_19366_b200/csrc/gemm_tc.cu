@@ -78,6 +78,7 @@ struct TcParams {
     // tile of split s writes its fp32 partial to out32 + s * split_stride
     uint32_t ksplit, kps;
     size_t split_stride;
+    uint32_t small_a;  // the short-box A maps are valid
 };
 
 __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix, uint32_t G, uint32_t NT,
@@ -101,11 +102,20 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
 struct Cursor {
     uint32_t tile, kb, kb1;  // current k-block, end of the tile's k range
     int32_t row;             // A row (arow) or B row (brow) of the current tile
+    uint32_t rows;           // A: valid rows of the tile (<= BM)
 };
 
+// tmA16 / tmA32 / tmA64: the A operand with 16- / 32- / 64-row boxes.  A tile
+// with at most that many valid rows (decode batches: a few rows per
+// sub-expert) loads only those rows; the rest of the 128-row slot keeps stale
+// rows whose outputs are discarded (masked stores), so the L2 -> SM feed
+// carries the weight tile and little else.  SW128 swizzle repeats every 8
+// rows, so a short box lands exactly like the first rows of a full one.
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmA16, const __grid_constant__ CUtensorMap tmA32,
+                   const __grid_constant__ CUtensorMap tmA64, TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
@@ -143,6 +153,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        if (p.small_a) {
+            tma_prefetch_desc(&tmA16);
+            tma_prefetch_desc(&tmA32);
+            tma_prefetch_desc(&tmA64);
+        }
     }
     if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
     griddep_wait();  // group metadata comes from the routing epilogue
@@ -172,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 map_tile(c.tile - split * base_total, s_prefix, p.G, p.NT, g, m, n);
                 c.row = is_a ? static_cast<int32_t>(s_start[g] + m * BM)
                              : static_cast<int32_t>(p.b_row0 + s_gmap[g] * p.N_group + n * BN);
+                c.rows = min(BM, s_off[g + 1] - s_start[g] - m * BM);
                 c.kb = split * p.kps;
                 c.kb1 = min(nkb, c.kb + p.kps);
             };
@@ -181,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     set_rows(c, is_a);
                 }
             };
-            Cursor cb{blockIdx.x, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0};
+            Cursor cb{blockIdx.x, 0, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0, 0};
             set_rows(cb, false);
             set_rows(ca, true);
             uint32_t ib = 0, ia = 0;  // loads issued per stream
@@ -196,8 +212,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             auto issue_a = [&]() {
                 const uint32_t s = ia % NA, ph = (ia / NA) & 1u;
                 mbar_wait(&emptyA[s], ph ^ 1u);
-                mbar_expect_tx(&fullA[s], A_BYTES);
-                tma_load_2d(sA + s * A_BYTES, &tmA, &fullA[s], static_cast<int32_t>(ca.kb * BK), ca.row);
+                const uint32_t box = !p.small_a ? BM : ca.rows <= 16 ? 16u : ca.rows <= 32 ? 32u : ca.rows <= 64 ? 64u : BM;
+                const CUtensorMap* tA = box == 16 ? &tmA16 : box == 32 ? &tmA32 : box == 64 ? &tmA64 : &tmA;
+                mbar_expect_tx(&fullA[s], box * BK * 2);
+                tma_load_2d(sA + s * A_BYTES, tA, &fullA[s], static_cast<int32_t>(ca.kb * BK), ca.row);
                 advance(ca, true);
                 ++ia;
             };
@@ -448,15 +466,15 @@ bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t
 
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                    const uint32_t* gmap, const uint32_t* starts) {
+                    const uint32_t* gmap, const uint32_t* starts, const CUtensorMap* tmA_small) {
     launch_gemm_tc_epi(swiglu ? kEpiSwiglu : kEpiPlain, tmA, tmB, out, sh, offsets, mprefix, num_sms, s, 0, nullptr,
-                       gmap, starts);
+                       gmap, starts, 1, tmA_small);
 }
 
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                         uint32_t b_row0, const int32_t* colmap, const uint32_t* gmap, const uint32_t* starts,
-                        uint32_t ksplit) {
+                        uint32_t ksplit, const CUtensorMap* tmA_small) {
     const bool swiglu = epi == kEpiSwiglu;
     TcParams p;
     p.G = sh.G;
@@ -479,6 +497,10 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.kps = (nkb + p.ksplit - 1) / p.ksplit;
     p.ksplit = (nkb + p.kps - 1) / p.kps;  // no empty splits
     p.split_stride = static_cast<size_t>(sh.max_rows) * sh.ld_out;
+    p.small_a = tmA_small ? 1u : 0u;
+    const CUtensorMap& a16 = tmA_small ? tmA_small[0] : *tmA;
+    const CUtensorMap& a32 = tmA_small ? tmA_small[1] : *tmA;
+    const CUtensorMap& a64 = tmA_small ? tmA_small[2] : *tmA;
 
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT * p.ksplit;
@@ -489,11 +511,11 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiCount>), (int)kSmemBytes);
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiF32Part>), (int)kSmemBytes);
     switch (epi) {
-        case kEpiF32Part: launch_k(gemm_tc_kernel<kEpiF32Part>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
-        case kEpiSwiglu: launch_k(gemm_tc_kernel<kEpiSwiglu>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
-        case kEpiActAbs: launch_k(gemm_tc_kernel<kEpiActAbs>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
-        case kEpiCount: launch_k(gemm_tc_kernel<kEpiCount>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
-        default: launch_k(gemm_tc_kernel<kEpiPlain>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, p); break;
+        case kEpiF32Part: launch_k(gemm_tc_kernel<kEpiF32Part>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
+        case kEpiSwiglu: launch_k(gemm_tc_kernel<kEpiSwiglu>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
+        case kEpiActAbs: launch_k(gemm_tc_kernel<kEpiActAbs>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
+        case kEpiCount: launch_k(gemm_tc_kernel<kEpiCount>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
+        default: launch_k(gemm_tc_kernel<kEpiPlain>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
     }
 }
 

@@ -159,7 +159,7 @@ bool is_device_ptr(const void* p) {
 }
 
 // shared-expert split-K (decode batches): at most kShSplitRows tokens, kShSplitMax K splits
-constexpr uint32_t kShSplitRows = 128, kShSplitMax = 24;
+constexpr uint32_t kShSplitRows = 128, kShSplitMax = 12;
 
 const char* kStageNames[] = {"router", "bucket", "dispatch", "gemm1", "gemm2", "combine"};
 constexpr int kStages = 6;
@@ -238,6 +238,7 @@ struct mp_layer_s {
     void* x_stage = nullptr;
     void* y_stage = nullptr;
     CUtensorMap tm_xperm{}, tm_h{}, tm_w1{}, tm_w2{};
+    CUtensorMap tm_xperm_s[3]{}, tm_h_s[3]{};  // 16 / 32 / 64-row A boxes (short tiles of the 1-SM GEMM)
     CUtensorMap tm_w1h{}, tm_w2h{};  // 128-row boxes: each CTA of a pair loads half a B tile
 
     // shared (always-on) expert, Qwen-style: one dense group of sh_w_pad neurons
@@ -254,6 +255,11 @@ struct mp_layer_s {
     CUtensorMap tm_w1s{}, tm_w2s{}, tm_hs{}, tm_w1sh{}, tm_w2sh{};
     cudaStream_t sh_stream = nullptr;  // side stream of the shared expert
     cudaEvent_t sh_fork = nullptr, sh_join = nullptr;
+    // decode batches: the routed weights the first gemm1 wave reads are
+    // prefetched into L2 while the (latency-bound) routing chain runs
+    cudaStream_t pf_stream = nullptr;
+    cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
+    bool pf_pending = false;
 
     bool residual = false;  // mp_layer_set_residual: y = x + MoE(x), fused into the combine
     // pipelined host-buffer forwards (mp_layer_forward_host_batches): two
@@ -323,6 +329,9 @@ void free_layer(mp_layer_s* L) {
     }
     if (L->sh_fork) cudaEventDestroy(L->sh_fork);
     if (L->sh_join) cudaEventDestroy(L->sh_join);
+    if (L->pf_stream) cudaStreamDestroy(L->pf_stream);
+    if (L->pf_fork) cudaEventDestroy(L->pf_fork);
+    if (L->pf_join) cudaEventDestroy(L->pf_join);
     for (void* p : {L->W1c, L->W2c, static_cast<void*>(L->gmap_dev)})
         if (p) cudaFree(p);
     for (void* p : {L->W1h, L->W2h, static_cast<void*>(L->gmap_host), static_cast<void*>(L->off_host)})
@@ -612,6 +621,30 @@ void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t
     L->launches += 3;
 }
 
+// Decode batches (T * k_max <= 8 rows per sub-expert on average): nearly every
+// sub-expert receives a token, gemm1 reads its weights group by group in tile
+// order, and the routing chain before it leaves HBM idle.  Prefetch the W1
+// tiles of the first groups (<= 64 MB, well inside the 126 MB L2) on a side
+// stream meanwhile; joined before the combine (graph-capturable).
+void prefetch_routed_weights(mp_layer_s* L, uint32_t T, cudaStream_t s) {
+    L->pf_pending = false;
+    if (!L->use_tc || L->offload || !L->has_experts || (size_t)T * L->k_max > (size_t)8 * L->G) return;
+    if (!L->pf_stream) {
+        ck(cudaStreamCreateWithFlags(&L->pf_stream, cudaStreamNonBlocking), "prefetch stream");
+        ck(cudaEventCreateWithFlags(&L->pf_fork, cudaEventDisableTiming), "prefetch event");
+        ck(cudaEventCreateWithFlags(&L->pf_join, cudaEventDisableTiming), "prefetch event");
+    }
+    const size_t w1_group = (size_t)2 * L->w_pad * L->d_pad * L->esz;
+    const size_t bytes = std::min<size_t>((size_t)L->G * w1_group, (size_t)64 << 20);
+    ck(cudaEventRecord(L->pf_fork, s), "prefetch fork");
+    ck(cudaStreamWaitEvent(L->pf_stream, L->pf_fork, 0), "prefetch fork");
+    mp::launch_l2_prefetch(L->W1, bytes, L->pf_stream);
+    ck_launch("l2 prefetch");
+    ck(cudaEventRecord(L->pf_join, L->pf_stream), "prefetch join");
+    L->pf_pending = true;
+    L->launches += 1;
+}
+
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
                  cudaStream_t s, StageTimer& tm, bool check_finite = false, bool with_shared = false,
@@ -656,7 +689,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
                             L->ws.mprefix_tc2, L->num_sms, s, gmap);
     else if (L->use_tc)
         mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
-                           L->ws.mprefix_tc, L->num_sms, s, gmap);
+                           L->ws.mprefix_tc, L->num_sms, s, gmap, nullptr, L->tm_xperm_s);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
@@ -668,12 +701,16 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
                             L->ws.mprefix_tc2, L->num_sms, s, gmap);
     else if (L->use_tc)
         mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
-                           L->ws.mprefix_tc, L->num_sms, s, gmap);
+                           L->ws.mprefix_tc, L->num_sms, s, gmap, nullptr, L->tm_h_s);
     else
         mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm2");
     tm.end(4, 1);
     if (shared) ck(cudaStreamWaitEvent(s, L->sh_join, 0), "join shared expert");
+    if (L->pf_pending) {
+        ck(cudaStreamWaitEvent(s, L->pf_join, 0), "join prefetch");
+        L->pf_pending = false;
+    }
     tm.begin(5);
     const uint32_t group_S = unit ? L->S : 0;
     mp::launch_combine(L->dtype, L->o, L->d, L->d_pad, L->ws.slot_row, sel, w, L->k_max, group_S, T, y, s,
@@ -700,6 +737,7 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
         if (reinterpret_cast<uintptr_t>(x) % 16) fail(MP_ERR_VALIDATION, "shared expert needs 16-byte aligned x");
         launch_shared_expert(L, x, T, s);
     }
+    if (with_shared) prefetch_routed_weights(L, T, s);
     if (L->desc.router_mode == MP_ROUTER_PROXY) {
         pack_gates(L);
         if (L->proxy_tc && (reinterpret_cast<uintptr_t>(x) % 16) == 0) {
@@ -953,6 +991,9 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                         mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64) &&
                         mp::make_tmap_bf16_2d(&L->tm_w1h, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 128, 64) &&
                         mp::make_tmap_bf16_2d(&L->tm_w2h, L->W2, L->w2_rows, L->w_pad, 128, 64);
+                    for (int b = 0; b < 3 && ok; ++b)
+                        ok = mp::make_tmap_bf16_2d(&L->tm_xperm_s[b], L->x_perm, L->rows_cap, L->d_pad, 16u << b, 64) &&
+                             mp::make_tmap_bf16_2d(&L->tm_h_s[b], L->h, L->rows_cap, L->w_pad, 16u << b, 64);
                     if (!ok) fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                 }
             }

@@ -126,8 +126,11 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
                          const RouterGuard& rg, const void* x, uint32_t d, const float* wrT, uint32_t* ticket,
                          uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb = kRouteTokensPerBlock);
-// tokens per CTA of the fused routing epilogue: fewer for small batches (more CTAs)
-inline uint32_t route_tokens_per_block(uint32_t T) { return T <= 256 ? 2u : T <= 1024 ? 8u : kRouteTokensPerBlock; }
+// tokens per CTA of the fused routing epilogue: fewer for small batches (more
+// CTAs; measured: one or two 32-token CTAs at T = 64 are slower)
+inline uint32_t route_tokens_per_block(uint32_t T) {
+    return T <= 256 ? 2u : T <= 1024 ? 8u : kRouteTokensPerBlock;
+}
 // in-place fixed-order sum of the K-split router partials into plane 0
 void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, cudaStream_t s);
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,
@@ -158,10 +161,12 @@ void launch_gemm1_simt(int dtype, const void* A, const void* W1, void* H, const 
 void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const GemmShape& sh,
                        const uint32_t* offsets, const uint32_t* mprefix, cudaStream_t s);
 // gmap (nullable): group g's weights are B group gmap[g] (offload cache slots)
-// starts (nullable): group g's rows are [starts[g], offsets[g+1]) (tails of the split schedule)
+// starts (nullable): group g's rows are [starts[g], offsets[g+1])
+// tmA_small (nullable): [3] maps of A with 16 / 32 / 64-row boxes (short tiles load only their rows)
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                    const uint32_t* gmap = nullptr, const uint32_t* starts = nullptr);
+                    const uint32_t* gmap = nullptr, const uint32_t* starts = nullptr,
+                    const CUtensorMap* tmA_small = nullptr);
 size_t gemm_tc_smem_bytes();
 // Epilogue modes of the 1-SM tensor-core GEMM (gemm_tc.cu).
 constexpr int kEpiPlain = 0;   // bf16 acc
@@ -173,7 +178,8 @@ constexpr int kEpiF32Part = 4; // fp32 split-K partials: out + split * max_rows 
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                         uint32_t b_row0 = 0, const int32_t* colmap = nullptr, const uint32_t* gmap = nullptr,
-                        const uint32_t* starts = nullptr, uint32_t ksplit = 1);
+                        const uint32_t* starts = nullptr, uint32_t ksplit = 1,
+                        const CUtensorMap* tmA_small = nullptr);
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
@@ -198,6 +204,8 @@ void launch_set_group_meta(uint32_t* meta, uint32_t rows, cudaStream_t s);
 // One-time (per kernel, per device) dynamic shared-memory attribute; thread-safe
 // (layer.cu).  max_carveout: also prefer the maximum shared-memory carveout.
 void func_attr_once(const void* func, int max_dyn_smem, bool max_carveout = false);
+// L2 prefetch of [p, p + bytes) with bulk prefetches (no data movement to SMs)
+void launch_l2_prefetch(const void* p, size_t bytes, cudaStream_t s);
 // max |p[i]| over n floats into *out (device, must be zeroed; atomic max on the bits)
 void launch_absmax(const float* p, size_t n, float* out, cudaStream_t s);
 

@@ -172,6 +172,21 @@ void launch_finite_check(const float* p, size_t n, int* flag, cudaStream_t s) {
     finite_check_kernel<<<1184, 256, 0, s>>>(p, n, flag);
 }
 
+__global__ void l2_prefetch_kernel(const char* __restrict__ p, size_t bytes) {
+    constexpr size_t kChunk = 32768;
+    for (size_t off = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * kChunk; off < bytes;
+         off += (size_t)gridDim.x * blockDim.x * kChunk) {
+        const uint32_t n = static_cast<uint32_t>(bytes - off < kChunk ? bytes - off : kChunk) & ~15u;
+        if (n)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p + off)), "r"(n)
+                         : "memory");
+    }
+}
+
+void launch_l2_prefetch(const void* p, size_t bytes, cudaStream_t s) {
+    l2_prefetch_kernel<<<16, 128, 0, s>>>(static_cast<const char*>(p), bytes);
+}
+
 void launch_absmax(const float* p, size_t n, float* out, cudaStream_t s) {
     absmax_kernel<<<592, 256, 0, s>>>(p, n, out);
 }

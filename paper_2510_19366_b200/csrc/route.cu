@@ -872,6 +872,7 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
             }
             if (o_sh32) {  // shared expert from split-K fp32 partials, summed in split order
                 float sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
                 for (uint32_t sp = 0; sp < sh_splits; ++sp) {
                     const float* pr = o_sh32 + sp * sh_stride + (size_t)t * d_pad + c;
                     const float4 a = __ldg(reinterpret_cast<const float4*>(pr));

@@ -539,3 +539,42 @@ def test_zero_tokens(oracle, torch_cuda, mixtral):
     torch.cuda.synchronize()
     assert tuple(y.shape) == (0, x_dev.shape[1])
     assert L.launch_count() == n0
+
+
+def test_shared_scratch_layers(oracle, torch_cuda):
+    """MP_LAYER_SHARED_SCRATCH: layers with the same shapes share the token
+    scratch (x_perm / h / o) from a per-device pool; a two-layer stack run on
+    one stream gives the same outputs as two layers with private scratch, and
+    closing one sharer leaves the other working."""
+    torch = torch_cuda
+    from paper_2510_19366_b200 import MoeLayer
+    from paper_2510_19366_b200._lib import MP_LAYER_SHARED_SCRATCH
+    E, S, d, ff, T, K = 4, 4, 256, 512, 96, 4
+    layers = {}
+    for shared in (False, True):
+        ls = []
+        for l in range(2):
+            experts, parts, wr, _ = toy_setup(oracle, E, S, d, ff, T, seed_w=7000 + 10 * l, seed_r=70 + l)
+            L = MoeLayer(E, S, d, ff, dtype="bf16", k_max=K, max_tokens=T,
+                         flags=MP_LAYER_SHARED_SCRATCH if shared else 0)
+            for e in range(E):
+                L.set_partition(e, parts[e])
+                L.load_expert(e, *experts[e])
+            L.set_router(wr)
+            L.set_residual(True)
+            ls.append(L)
+        layers[shared] = ls
+    x = torch.from_numpy(bf16_round(oracle.uniform_pm1(3, T * d).reshape(T, d))).cuda().to(torch.bfloat16)
+
+    def stack(ls):
+        y = x
+        for L in ls:
+            y = L.forward(y, k=K)
+        return y
+
+    assert torch.equal(stack(layers[True]), stack(layers[False]))
+    layers[True][0].close()
+    assert torch.equal(layers[True][1].forward(x, k=K), layers[False][1].forward(x, k=K))
+    for ls in layers.values():
+        for L in ls:
+            L.close()
