@@ -60,6 +60,7 @@ constexpr uint32_t B_BYTES = BN * BK * 2;
 constexpr uint32_t kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
 constexpr size_t kSmemBytes = 1024 + NA * A_BYTES + NB * B_BYTES + 256;
+constexpr uint32_t kTileCache = 256;  // decoded tiles per CTA kept in shared memory
 
 struct TcParams {
     uint32_t G, K, N_group, n_valid, ld_out, NT;
@@ -103,6 +104,7 @@ struct Cursor {
     uint32_t tile, kb, kb1;  // current k-block, end of the tile's k range
     int32_t row;             // A row (arow) or B row (brow) of the current tile
     uint32_t rows;           // A: valid rows of the tile (<= BM)
+    uint32_t i;              // index of the tile among this CTA's tiles
 };
 
 // tmA16 / tmA32 / tmA64: the A operand with 16- / 32- / 64-row boxes.  A tile
@@ -121,6 +123,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ uint32_t s_off[kMaxG + 1];
     __shared__ uint32_t s_gmap[kMaxG];
     __shared__ uint32_t s_start[kMaxG];
+    // this CTA's tiles decoded once (g | n << 8 | split << 20, m): the
+    // binary search + divisions of map_tile were ~13% of the warp samples of
+    // short-K GEMMs (Qwen's K = 384 down projection, ncu source page)
+    __shared__ uint2 s_tiles[kTileCache];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sB = base;                 // NB x 32 KB (1024-aligned)
     uint8_t* sA = base + NB * B_BYTES;  // NA x 16 KB
@@ -168,13 +174,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (q < p.G) s_gmap[q] = p.gmap ? p.gmap[q] : q;
         if (q < p.G) s_start[q] = p.starts ? p.starts[q] : p.offsets[q];
     }
+    __syncthreads();
+    const uint32_t base_total = s_prefix[p.G] * p.NT;
+    const uint32_t total = base_total * p.ksplit;
+    const uint32_t nkb = p.K / BK;
+    for (uint32_t i = threadIdx.x; i < kTileCache; i += blockDim.x) {
+        const uint32_t tile = blockIdx.x + i * gridDim.x;
+        if (tile >= total) break;
+        uint32_t g, m, n;
+        const uint32_t split = tile / base_total;
+        map_tile(tile - split * base_total, s_prefix, p.G, p.NT, g, m, n);
+        s_tiles[i] = make_uint2(g | (n << 8) | (split << 20), m);
+    }
+    // (tile index of this CTA, i) -> g, m, n, split
+    auto decode = [&](uint32_t tile, uint32_t i, uint32_t& g, uint32_t& m, uint32_t& n, uint32_t& split) {
+        if (i < kTileCache) {
+            const uint2 v = s_tiles[i];
+            g = v.x & 0xFFu;
+            n = (v.x >> 8) & 0xFFFu;
+            split = v.x >> 20;
+            m = v.y;
+        } else {
+            split = tile / base_total;
+            map_tile(tile - split * base_total, s_prefix, p.G, p.NT, g, m, n);
+        }
+    };
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t base_total = s_prefix[p.G] * p.NT;
-    const uint32_t total = base_total * p.ksplit;
-    const uint32_t nkb = p.K / BK;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -182,9 +210,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // its own empty barrier
             auto set_rows = [&](Cursor& c, bool is_a) {
                 if (c.tile >= total) return;
-                uint32_t g, m, n;
-                const uint32_t split = c.tile / base_total;
-                map_tile(c.tile - split * base_total, s_prefix, p.G, p.NT, g, m, n);
+                uint32_t g, m, n, split;
+                decode(c.tile, c.i, g, m, n, split);
                 c.row = is_a ? static_cast<int32_t>(s_start[g] + m * BM)
                              : static_cast<int32_t>(p.b_row0 + s_gmap[g] * p.N_group + n * BN);
                 c.rows = min(BM, s_off[g + 1] - s_start[g] - m * BM);
@@ -194,10 +221,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             auto advance = [&](Cursor& c, bool is_a) {
                 if (++c.kb == c.kb1) {
                     c.tile += gridDim.x;
+                    ++c.i;
                     set_rows(c, is_a);
                 }
             };
-            Cursor cb{blockIdx.x, 0, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0, 0};
+            Cursor cb{blockIdx.x, 0, 0, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0, 0, 0};
             set_rows(cb, false);
             set_rows(ca, true);
             uint32_t ib = 0, ia = 0;  // loads issued per stream
@@ -248,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (p.trace) w_acc += clock64() - t0;
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                const uint32_t kb_lo = (tile / base_total) * p.kps, kb_hi = min(nkb, kb_lo + p.kps);
+                const uint32_t kb_lo = (p.ksplit > 1 ? tile / base_total : 0u) * p.kps, kb_hi = min(nkb, kb_lo + p.kps);
                 for (uint32_t kb = kb_lo; kb < kb_hi; ++kb, ++it) {
                     const uint32_t sa = it % NA, pa = (it / NA) & 1u;
                     const uint32_t sb = it % NB, pb = (it / NB) & 1u;
@@ -281,9 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
         uint32_t tc = 0;
         for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
-            uint32_t g, m, n;
-            const uint32_t split = tile / base_total;
-            map_tile(tile - split * base_total, s_prefix, p.G, p.NT, g, m, n);
+            uint32_t g, m, n, split;
+            decode(tile, tc, g, m, n, split);
             const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();

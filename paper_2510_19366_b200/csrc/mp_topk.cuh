@@ -48,12 +48,17 @@ __device__ __forceinline__ double warp_row_abs_sum(const __nv_bfloat16* __restri
 // keys (nullable): selection keys replacing sc for the ranking only (the
 // exact re-selection of near-tie tokens); the weights always use sc.
 // vk_out (nullable): the k-th and (k+1)-th best keys.
+// msk_row / slot_row16 (nullable, shared memory): the selection as a bit mask
+// over the G ids (ceil(G / 32) words, every word written) and, for each
+// selected id, its slot in sel_row -- the bucketing ranks' input, without
+// reading sel_row back from global memory.
 // NC: 32-candidate chunks per lane held in registers (G <= 32 NC); smaller NC
 // for small G trims the unrolled per-round work (Mixtral: G = 64 -> NC = 2)
 template <int NC = kMaxG / 32>
 __device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uint32_t k, uint32_t k_max,
                                   int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row,
-                                  const double* __restrict__ keys = nullptr, double* vk_out = nullptr) {
+                                  const double* __restrict__ keys = nullptr, double* vk_out = nullptr,
+                                  uint32_t* msk_row = nullptr, uint16_t* slot_row16 = nullptr) {
     const uint32_t lane = lane_id();
     const uint32_t nc = (G + 31) / 32;
     double v[NC];
@@ -130,10 +135,12 @@ __device__ double warp_topk_token(const double* __restrict__ sc, uint32_t G, uin
         if (c >= (int)nc) break;
         const bool mine = (taken >> c) & 1u;
         const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+        if (msk_row && lane == 0) msk_row[c] = bal;  // selection bit mask, word c = ids 32c .. 32c + 31
         if (mine) {
             const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
             sel_row[pos] = lane + 32u * c;
             w_row[pos] = weight_mode == 1 ? static_cast<float>(ex[c] / z) : 1.0f;
+            if (msk_row) slot_row16[lane + 32u * c] = static_cast<uint16_t>(pos);
         }
         base += __popc(bal);
     }
@@ -165,7 +172,7 @@ __device__ __forceinline__ float unpack_key(uint64_t p) {
 template <int NC = kMaxG / 32>
 __device__ double warp_topk_fast(const double* __restrict__ vals, uint32_t G, uint32_t k, uint32_t k_max,
                                  int weight_mode, uint32_t* __restrict__ sel_row, float* __restrict__ w_row,
-                                 double* vk_out) {
+                                 double* vk_out, uint32_t* msk_row = nullptr, uint16_t* slot_row16 = nullptr) {
     const uint32_t lane = lane_id();
     const uint32_t nc = (G + 31) / 32;
     uint64_t v[NC];
@@ -221,10 +228,12 @@ __device__ double warp_topk_fast(const double* __restrict__ vals, uint32_t G, ui
         if (c >= (int)nc) break;
         const bool mine = (taken >> c) & 1u;
         const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+        if (msk_row && lane == 0) msk_row[c] = bal;  // selection bit mask, word c = ids 32c .. 32c + 31
         if (mine) {
             const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
             sel_row[pos] = lane + 32u * c;
             w_row[pos] = weight_mode == 1 ? static_cast<float>(ex[c] / z) : 1.0f;
+            if (msk_row) slot_row16[lane + 32u * c] = static_cast<uint16_t>(pos);
         }
         base += __popc(bal);
     }

@@ -330,8 +330,8 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     // s_cnt (nullable): nblk x G bytes of shared memory -- the counts (<= 32
     // tokens per block and bucket) are staged there with one coalesced pass, so
     // both sweeps over them (sums, then bases) read shared memory instead of
-    // chains of L2 loads (Qwen prefill: 256 blocks x 240 buckets, 20 -> ~5 us)
-    constexpr int V = 4;
+    // chains of L2 loads
+    constexpr int V = 6;
     if (s_cnt) {
         const uint32_t n = nblk * G;
         const uint32_t n4 = (n % 4 == 0) ? n / 4 : 0;
@@ -379,9 +379,19 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     const uint32_t c = gi < G ? goff[gi] : 0;
     MP_SCAN_STAMP(1);
     // bucket offsets and the GEMM tile prefixes, scanned together:
-    //   offsets (rows), 128-row tiles, 64-row SIMT tiles, 256-row pair tiles
-    uint32_t sv[V] = {c, gi < G ? (c + kTcBM - 1) / kTcBM : 0u, gi < G ? (c + kSimtBM - 1) / kSimtBM : 0u,
-                      gi < G ? (c + 255) / 256 : 0u};
+    //   offsets (rows), 128-row tiles, 64-row SIMT tiles, 256-row pair tiles,
+    //   and the hybrid schedule's two disjoint halves: a group whose 256-row
+    //   padding is no larger than its 128-row padding (count % 256 == 0 or
+    //   > 128) runs on CTA pairs, the others on 128-row 1-SM tiles -- every
+    //   group pays 128-row granularity, each group's weights stream in one kernel
+    const uint32_t r256 = c % 256u;
+    const bool to_pair = gi < G && c > 0 && (r256 == 0 || r256 > 128);
+    uint32_t sv[V] = {c,
+                      gi < G ? (c + kTcBM - 1) / kTcBM : 0u,
+                      gi < G ? (c + kSimtBM - 1) / kSimtBM : 0u,
+                      gi < G ? (c + 255) / 256 : 0u,
+                      (gi < G && !to_pair) ? (c + kTcBM - 1) / kTcBM : 0u,
+                      to_pair ? (c + 255) / 256 : 0u};
     uint32_t tot[V];
     block_exclusive_scan_1024_multi<V>(sv, tot, wsum);
     const uint32_t off = sv[0];
@@ -390,12 +400,16 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
         mprefix_tc[gi] = sv[1];
         mprefix_simt[gi] = sv[2];
         mprefix_tc2[gi] = sv[3];
+        mprefix_tc2[(G + 1) + gi] = sv[4];
+        mprefix_tc2[2 * (G + 1) + gi] = sv[5];
     }
     if (gi == 0) {
         offsets[G] = tot[0];
         mprefix_tc[G] = tot[1];
         mprefix_simt[G] = tot[2];
         mprefix_tc2[G] = tot[3];
+        mprefix_tc2[(G + 1) + G] = tot[4];
+        mprefix_tc2[2 * (G + 1) + G] = tot[5];
     }
     __syncthreads();
     if (gi < G) goff[gi] = off;
@@ -550,7 +564,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         __syncwarp();
         kt = token_k(kpt, k_scalar, t, k_max, G, err);
         const double gap = warp_topk_fast<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
-                                          wout + (size_t)t * k_max, vk[warp]);
+                                          wout + (size_t)t * k_max, vk[warp], msk[warp], slot_of[warp]);
         __syncwarp();
         // the exact pass also takes every token that may be an oracle near tie
         // (exact gap < 1e-6), so near ties are counted exactly
@@ -609,7 +623,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         __syncwarp();
         // the k-th and (k+1)-th exact keys both lie in the window: gap is exact
         const double egap = warp_topk_token<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
-                                                wout + (size_t)t * k_max, key);
+                                                wout + (size_t)t * k_max, key, nullptr, msk[warp], slot_of[warp]);
         if (lane == 0) {
             atomicAdd(stats, 1u);
             if (egap < kNearTie) atomicAdd(stats + 1, 1u);
@@ -617,15 +631,8 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     }
     __syncthreads();  // this CTA's selections are visible to the CTA
     MP_RT_STAMP();    // 2: exact pass done
-    for (uint32_t q = threadIdx.x; q < tb * k_max; q += blockDim.x) {
-        const uint32_t tt = q / k_max, j = q % k_max;
-        if (t0 + tt >= T) continue;
-        const uint32_t g = sel[(size_t)(t0 + tt) * k_max + j];
-        if (g == kSelNone || g >= G) continue;
-        atomicOr(&msk[tt][g >> 5], 1u << (g & 31));
-        slot_of[tt][g] = static_cast<uint16_t>(j);
-    }
-    __syncthreads();
+    // (the selection masks / slots were written by the top-k emissions)
+    MP_RT_STAMP();  // 3: selection masks built
     // warp per bucket, lane per token (tb <= 32): the stable rank of token tt
     // in bucket g is the number of earlier tokens of the CTA selecting g
     for (uint32_t g = warp; g < G; g += blockDim.x / 32) {
@@ -638,7 +645,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     // the ticket by the barrier + one gpu-scope fence of the ticket thread
     // (fences are cumulative over what the barrier made visible to it)
     __syncthreads();
-    MP_RT_STAMP();  // 3: ranks done
+    MP_RT_STAMP();  // 4: ranks done
     if (threadIdx.x == 0) {
         // release (acq_rel: not the heavier sequentially consistent fence)
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -646,11 +653,12 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         if (is_last) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire every CTA's writes
     }
     __syncthreads();
-    MP_RT_STAMP();  // 4: ticket taken
+    MP_RT_STAMP();  // 5: ticket taken
 #if MP_ROUTE_TRACE
     if (threadIdx.x == 0 && blockIdx.x == 0 && !is_last)
-        printf("route_bucket blk %u: topk %llu exact %llu ranks %llu ticket %llu ns (start %llu)\n", blockIdx.x,
-               tr_[1] - tr_[0], tr_[2] - tr_[1], tr_[3] - tr_[2], tr_[4] - tr_[3], tr_[0]);
+        printf("route_bucket blk %u: topk %llu exact %llu masks %llu ranks %llu ticket %llu ns (start %llu)\n",
+               blockIdx.x, tr_[1] - tr_[0], tr_[2] - tr_[1], tr_[3] - tr_[2], tr_[4] - tr_[3], tr_[5] - tr_[4],
+               tr_[0]);
 #endif
     if (!is_last) return;  // the barrier above extends thread 0's acquire to the CTA
     // the CTA's routing smem is free now: stage the counts there when they fit
@@ -659,13 +667,13 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
                      stage ? reinterpret_cast<uint8_t*>(rsm) : nullptr);
 #if MP_ROUTE_TRACE
     __syncthreads();
-    MP_RT_STAMP();  // 5: scan done
+    MP_RT_STAMP();  // 6: scan done
     if (threadIdx.x == 0)
-        printf("route_bucket last blk %u: topk %llu exact %llu ranks %llu ticket %llu scan %llu ns [fence %llu counts "
-               "%llu scans %llu base %llu] (start %llu)\n",
+        printf("route_bucket last blk %u: topk %llu exact %llu masks %llu ranks %llu ticket %llu scan %llu ns [stage "
+               "%llu counts %llu scans %llu base %llu] (start %llu)\n",
                blockIdx.x, tr_[1] - tr_[0], tr_[2] - tr_[1], tr_[3] - tr_[2], tr_[4] - tr_[3], tr_[5] - tr_[4],
-               g_scan_tr[0] - tr_[4], g_scan_tr[1] - g_scan_tr[0], g_scan_tr[2] - g_scan_tr[1],
-               tr_[5] - g_scan_tr[2], tr_[0]);
+               tr_[6] - tr_[5], g_scan_tr[0] - tr_[5], g_scan_tr[1] - g_scan_tr[0], g_scan_tr[2] - g_scan_tr[1],
+               tr_[6] - g_scan_tr[2], tr_[0]);
 #endif
     if (threadIdx.x == 0) *ticket = 0;  // ready for the next forward (stream-ordered)
 }
