@@ -257,7 +257,7 @@ MP_API mp_status mp_ep_create_subexpert(uint32_t world, uint32_t rank, uint32_t 
             E->ws.offsets = ep_alloc<uint32_t>(world + 1);
             E->ws.mprefix_tc = ep_alloc<uint32_t>(world + 1);
             E->ws.mprefix_simt = ep_alloc<uint32_t>(world + 1);
-            E->ws.mprefix_tc2 = ep_alloc<uint32_t>(3 * (world + 1));
+            E->ws.mprefix_tc2 = ep_alloc<uint32_t>(world + 1);
             E->ws.perm_tok = ep_alloc<uint32_t>(tw);
             E->ws.perm_w = ep_alloc<float>(tw);
             E->ws.slot_row = ep_alloc<uint32_t>(tw);

@@ -177,7 +177,6 @@ struct mp_layer_s {
     // gemm_tc, by expected padding); MOEPRISM_TC_TILE=128|256 forces
     int tile_mode = 0;
     bool tile256 = false;  // this forward's choice
-    bool hybrid = false;   // this forward runs the hybrid schedule (pairs + 1-SM tiles)
     bool has_experts = true, has_router = true;  // MP_LAYER_* role flags
 
     std::vector<std::vector<uint32_t>> assignment;
@@ -667,7 +666,6 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         }
         const bool pairs_win = pad256 / 1.05 < pad128;
         L->tile256 = L->tile_mode == 2 || (L->tile_mode == 0 && rows >= 192.0 && pairs_win);
-        L->hybrid = L->tile_mode == 3;
     }
     if (!bucketed) {
         tm.begin(1);
@@ -686,17 +684,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
     const uint32_t* gmap = L->offload ? L->gmap_dev : nullptr;
-    const uint32_t G1 = L->G + 1;
-    int n_gemm = 1;
-    if (L->use_tc && L->hybrid) {
-        // hybrid: groups with count % 256 in (0, 128] on 128-row 1-SM tiles,
-        // the others on CTA pairs -- disjoint rows, each group's weights once
-        mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
-                            L->ws.mprefix_tc2 + 2 * G1, L->num_sms, s, gmap);
-        mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
-                           L->ws.mprefix_tc2 + G1, L->num_sms, s, gmap, nullptr, L->tm_xperm_s);
-        n_gemm = 2;
-    } else if (L->use_tc && L->tile256)
+    if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
                             L->ws.mprefix_tc2, L->num_sms, s, gmap);
     else if (L->use_tc)
@@ -706,14 +694,9 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
     const bool shared = with_shared && L->sh_ff;
-    tm.end(3, n_gemm);
+    tm.end(3, 1);
     tm.begin(4);
-    if (L->use_tc && L->hybrid) {
-        mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
-                            L->ws.mprefix_tc2 + 2 * G1, L->num_sms, s, gmap);
-        mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
-                           L->ws.mprefix_tc2 + G1, L->num_sms, s, gmap, nullptr, L->tm_h_s);
-    } else if (L->use_tc && L->tile256)
+    if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
                             L->ws.mprefix_tc2, L->num_sms, s, gmap);
     else if (L->use_tc)
@@ -722,7 +705,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     else
         mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm2");
-    tm.end(4, n_gemm);
+    tm.end(4, 1);
     if (shared) ck(cudaStreamWaitEvent(s, L->sh_join, 0), "join shared expert");
     if (L->pf_pending) {
         ck(cudaStreamWaitEvent(s, L->pf_join, 0), "join prefetch");
@@ -912,10 +895,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             if (const char* env = std::getenv("MOEPRISM_BF16_GEMM"))
                 if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
             if (const char* env = std::getenv("MOEPRISM_TC_TILE"))
-                L->tile_mode = std::string(env) == "256"      ? 2
-                               : std::string(env) == "128"    ? 1
-                               : std::string(env) == "hybrid" ? 3
-                                                              : 0;
+                L->tile_mode = std::string(env) == "256" ? 2 : std::string(env) == "128" ? 1 : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
             L->d_pad = round_up(L->d, 64);
@@ -985,7 +965,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 L->ws.offsets = dalloc<uint32_t>(L->G + 1, "offsets");
                 L->ws.mprefix_tc = dalloc<uint32_t>(L->G + 1, "mprefix");
                 L->ws.mprefix_simt = dalloc<uint32_t>(L->G + 1, "mprefix");
-                L->ws.mprefix_tc2 = dalloc<uint32_t>(3 * (L->G + 1), "mprefix");
+                L->ws.mprefix_tc2 = dalloc<uint32_t>(L->G + 1, "mprefix");
                 L->ws.perm_tok = dalloc<uint32_t>(L->rows_cap, "perm");
                 L->ws.perm_w = dalloc<float>(L->rows_cap, "perm w");
                 L->ws.slot_row = dalloc<uint32_t>(tk, "slot row");
@@ -1637,13 +1617,12 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
 
 // Diagnostics (not in the public header): grouped-GEMM kernel choice of a
 // layer at run time, 0 auto / 1 one-SM 128-row tiles / 2 CTA-pair 256-row
-// tiles / 3 hybrid (per group: CTA pairs when that pads no more rows than
-// 128-row tiles, else 1-SM tiles; two launches), for A/B timing (tests/probes/tile_ab.py).  The remainder schedules
+// tiles, for A/B timing (tests/probes/tile_ab.py).  The remainder schedules
 // measured and dropped in round 1 (M=128 pair tails, the split schedule,
 // merged and wide remainders) are described in gemm_tc2.cu and DESIGN.md.
 MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {
-        if (!L || mode < 0 || mode > 3) fail(MP_ERR_VALIDATION, "bad argument");
+        if (!L || mode < 0 || mode > 2) fail(MP_ERR_VALIDATION, "bad argument");
         L->tile_mode = mode;
     });
 }

@@ -26,10 +26,7 @@ struct BucketWs {
     uint32_t* offsets;       // [G+1]
     uint32_t* mprefix_tc;    // [G+1] prefix of ceil(count/128)
     uint32_t* mprefix_simt;  // [G+1] prefix of ceil(count/64)
-    // [3][G+1]: prefix of ceil(count/256) (CTA-pair tiles); the hybrid
-    // schedule's 1-SM 128-row tile prefix and its CTA-pair tile prefix
-    // (disjoint groups: count % 256 in (0, 128] -> 1-SM, else pairs)
-    uint32_t* mprefix_tc2;
+    uint32_t* mprefix_tc2;   // [G+1] prefix of ceil(count/256) (CTA-pair tiles)
     uint32_t* perm_tok;      // [rows]
     float* perm_w;           // [rows]
     uint32_t* slot_row;      // [T][k_max]

@@ -331,7 +331,7 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     // tokens per block and bucket) are staged there with one coalesced pass, so
     // both sweeps over them (sums, then bases) read shared memory instead of
     // chains of L2 loads
-    constexpr int V = 6;
+    constexpr int V = 4;
     if (s_cnt) {
         const uint32_t n = nblk * G;
         const uint32_t n4 = (n % 4 == 0) ? n / 4 : 0;
@@ -379,19 +379,9 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     const uint32_t c = gi < G ? goff[gi] : 0;
     MP_SCAN_STAMP(1);
     // bucket offsets and the GEMM tile prefixes, scanned together:
-    //   offsets (rows), 128-row tiles, 64-row SIMT tiles, 256-row pair tiles,
-    //   and the hybrid schedule's two disjoint halves: a group whose 256-row
-    //   padding is no larger than its 128-row padding (count % 256 == 0 or
-    //   > 128) runs on CTA pairs, the others on 128-row 1-SM tiles -- every
-    //   group pays 128-row granularity, each group's weights stream in one kernel
-    const uint32_t r256 = c % 256u;
-    const bool to_pair = gi < G && c > 0 && (r256 == 0 || r256 > 128);
-    uint32_t sv[V] = {c,
-                      gi < G ? (c + kTcBM - 1) / kTcBM : 0u,
-                      gi < G ? (c + kSimtBM - 1) / kSimtBM : 0u,
-                      gi < G ? (c + 255) / 256 : 0u,
-                      (gi < G && !to_pair) ? (c + kTcBM - 1) / kTcBM : 0u,
-                      to_pair ? (c + 255) / 256 : 0u};
+    //   offsets (rows), 128-row tiles, 64-row SIMT tiles, 256-row pair tiles
+    uint32_t sv[V] = {c, gi < G ? (c + kTcBM - 1) / kTcBM : 0u, gi < G ? (c + kSimtBM - 1) / kSimtBM : 0u,
+                      gi < G ? (c + 255) / 256 : 0u};
     uint32_t tot[V];
     block_exclusive_scan_1024_multi<V>(sv, tot, wsum);
     const uint32_t off = sv[0];
@@ -400,16 +390,12 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
         mprefix_tc[gi] = sv[1];
         mprefix_simt[gi] = sv[2];
         mprefix_tc2[gi] = sv[3];
-        mprefix_tc2[(G + 1) + gi] = sv[4];
-        mprefix_tc2[2 * (G + 1) + gi] = sv[5];
     }
     if (gi == 0) {
         offsets[G] = tot[0];
         mprefix_tc[G] = tot[1];
         mprefix_simt[G] = tot[2];
         mprefix_tc2[G] = tot[3];
-        mprefix_tc2[(G + 1) + G] = tot[4];
-        mprefix_tc2[2 * (G + 1) + G] = tot[5];
     }
     __syncthreads();
     if (gi < G) goff[gi] = off;

@@ -503,10 +503,9 @@ def test_forward_is_cuda_graph_capturable(oracle, torch_cuda):
 
 @pytest.mark.parametrize("k", [4, 8])
 def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
-    """Every GEMM schedule (1-SM 128-row tiles, CTA-pair 256-row tiles, the
-    hybrid of both over disjoint groups) gives the same layer output; buckets
-    with partial last tiles of both sizes occur at these bucket sizes, so the
-    hybrid sends groups to both kernels."""
+    """Both GEMM kernels (1-SM 128-row tiles, CTA-pair 256-row tiles) give the
+    same layer output; buckets with partial last tiles of both sizes occur at
+    these bucket sizes."""
     import ctypes as C
     torch = torch_cuda
     from paper_2510_19366_b200 import _lib
@@ -515,7 +514,7 @@ def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
     lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
     outs = {}
     try:
-        for mode in (2, 1, 3):  # CTA pairs, 1-SM, hybrid
+        for mode in (2, 1):  # CTA pairs, 1-SM
             _lib.check(lib.mp_debug_set_tile_mode(L.h, mode))
             y, sel, w, off = L.forward(x_dev, k=k, return_routing=True)
             torch.cuda.synchronize()
