@@ -59,7 +59,8 @@ constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr uint32_t B_BYTES = BN * BK * 2;
 constexpr uint32_t kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
-constexpr size_t kSmemBytes = 1024 + NA * A_BYTES + NB * B_BYTES + 256;
+constexpr uint32_t kEpiStage = 32 * 32 * 2;  // one 32-row x 32-column bf16 box of a warp's output slab
+constexpr size_t kSmemBytes = 1024 + NA * A_BYTES + NB * B_BYTES + 256 + 4 * 2 * kEpiStage;
 constexpr uint32_t kTileCache = 256;  // decoded tiles per CTA kept in shared memory
 
 struct TcParams {
@@ -80,6 +81,13 @@ struct TcParams {
     uint32_t ksplit, kps;
     size_t split_stride;
     uint32_t small_a;  // the short-box A maps are valid
+    uint32_t tma_out;  // plain epilogue: tmO is valid (full warp slabs leave through TMA stores)
+    // gemm1 B tail (0: off): valid neurons per group; the 64-neuron blocks
+    // past them are not loaded, the partial one through b_tail_rows-row boxes
+    // (tmBt) -- the padding rows of the packed W1 never leave HBM.  Their smem
+    // rows hold stale data, so the matching h columns are garbage: gemm2 reads
+    // h and W2 through maps whose K extent stops at the valid neurons.
+    uint32_t b_valid, b_tail_rows;
 };
 
 __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix, uint32_t G, uint32_t NT,
@@ -102,6 +110,7 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
 // (tile, k-block) cursor of one operand stream of a CTA
 struct Cursor {
     uint32_t tile, kb, kb1;  // current k-block, end of the tile's k range
+    uint32_t n;              // N tile
     int32_t row;             // A row (arow) or B row (brow) of the current tile
     uint32_t rows;           // A: valid rows of the tile (<= BM)
     uint32_t i;              // index of the tile among this CTA's tiles
@@ -117,7 +126,8 @@ template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA16, const __grid_constant__ CUtensorMap tmA32,
-                   const __grid_constant__ CUtensorMap tmA64, TcParams p) {
+                   const __grid_constant__ CUtensorMap tmA64, const __grid_constant__ CUtensorMap tmO,
+                   const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBt, TcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
     __shared__ uint32_t s_off[kMaxG + 1];
@@ -137,6 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = emptyB + NB;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    // plain-epilogue staging: 2 boxes per epilogue warp (after the barriers)
+    uint8_t* sEpi = reinterpret_cast<uint8_t*>(reinterpret_cast<uintptr_t>(sA + NA * A_BYTES + 256 + 127) & ~uintptr_t(127));
 
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
@@ -159,6 +171,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        if (p.tma_out) tma_prefetch_desc(&tmO);
+        if (p.b_valid) {
+            tma_prefetch_desc(&tmBh);
+            tma_prefetch_desc(&tmBt);
+        }
         if (p.small_a) {
             tma_prefetch_desc(&tmA16);
             tma_prefetch_desc(&tmA32);
@@ -215,6 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 c.row = is_a ? static_cast<int32_t>(s_start[g] + m * BM)
                              : static_cast<int32_t>(p.b_row0 + s_gmap[g] * p.N_group + n * BN);
                 c.rows = min(BM, s_off[g + 1] - s_start[g] - m * BM);
+                c.n = n;
                 c.kb = split * p.kps;
                 c.kb1 = min(nkb, c.kb + p.kps);
             };
@@ -225,15 +243,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                     set_rows(c, is_a);
                 }
             };
-            Cursor cb{blockIdx.x, 0, 0, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0, 0, 0};
+            Cursor cb{blockIdx.x, 0, 0, 0, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0, 0, 0, 0};
             set_rows(cb, false);
             set_rows(ca, true);
             uint32_t ib = 0, ia = 0;  // loads issued per stream
             auto issue_b = [&]() {
                 const uint32_t s = ib % NB, ph = (ib / NB) & 1u;
                 mbar_wait(&emptyB[s], ph ^ 1u);
-                mbar_expect_tx(&fullB[s], B_BYTES);
-                tma_load_2d(sB + s * B_BYTES, &tmB, &fullB[s], static_cast<int32_t>(cb.kb * BK), cb.row);
+                const int32_t kc = static_cast<int32_t>(cb.kb * BK);
+                const uint32_t nb = cb.n * 2;  // first 64-neuron block of the tile (128 rows: gate, up)
+                if (!p.b_valid || p.b_valid >= (nb + 2) * 64) {
+                    mbar_expect_tx(&fullB[s], B_BYTES);
+                    tma_load_2d(sB + s * B_BYTES, &tmB, &fullB[s], kc, cb.row);
+                } else {
+                    uint32_t v[2], bytes = 0;
+#pragma unroll
+                    for (uint32_t hb = 0; hb < 2; ++hb) {
+                        const uint32_t lo = (nb + hb) * 64;
+                        v[hb] = p.b_valid > lo ? min(64u, p.b_valid - lo) : 0u;
+                        bytes += v[hb] == 64 ? 128 * BK * 2 : v[hb] ? 2 * p.b_tail_rows * BK * 2 : 0;
+                    }
+                    mbar_expect_tx(&fullB[s], bytes);
+#pragma unroll
+                    for (uint32_t hb = 0; hb < 2; ++hb) {
+                        uint8_t* dst = sB + s * B_BYTES + hb * (128 * BK * 2);
+                        const int32_t r = cb.row + static_cast<int32_t>(hb * 128);
+                        if (v[hb] == 64) {
+                            tma_load_2d(dst, &tmBh, &fullB[s], kc, r);
+                        } else if (v[hb]) {  // gate rows, then the up rows of the same neurons
+                            tma_load_2d(dst, &tmBt, &fullB[s], kc, r);
+                            tma_load_2d(dst + kIlv * BK * 2, &tmBt, &fullB[s], kc, r + static_cast<int32_t>(kIlv));
+                        }
+                    }
+                }
                 advance(cb, false);
                 ++ib;
             };
@@ -308,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
         const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
         uint32_t tc = 0;
+        uint32_t epi_it = 0;  // TMA-stored chunks of this warp (staging buffer parity)
         for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
             uint32_t g, m, n, split;
             decode(tile, tc, g, m, n, split);
@@ -403,14 +446,37 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else {
                 // two register sets: the TMEM load of chunk c + 1 is in flight
                 // while chunk c is converted and stored (short-K GEMMs, e.g.
-                // Qwen's K = 384 down projection, are epilogue-bound)
+                // Qwen's K = 384 down projection, are epilogue-bound).
+                // A warp whose 32 rows are all valid stages each 32 x 32 chunk
+                // in shared memory and writes it with one TMA store (2 KB of
+                // whole 64-byte row segments) instead of 4 vector stores per
+                // lane that each touch 32 rows; ragged slabs store directly.
+                const bool slab = p.tma_out && m * BM + q * 32 + 32 <= s_off[g + 1] - s_start[g];
+                const int32_t slab_row = static_cast<int32_t>(s_start[g] + m * BM + q * 32);
                 auto store = [&](uint32_t c, const uint32_t* r) {
                     const uint32_t col = n * BN + c * 32;
-                    if (valid && col < p.n_valid) {
-                        uint32_t pk[16];
+                    if (col >= p.n_valid) return;
+                    uint32_t pk[16];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+                    for (int i = 0; i < 16; ++i)
+                        pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+                    if (slab) {
+                        uint8_t* buf = sEpi + (q * 2 + (epi_it & 1u)) * kEpiStage;
+                        if (epi_it >= 2) {  // the store issued from this buffer two chunks ago has read it
+                            if (lane == 0) bulk_wait_read<1>();
+                            __syncwarp();
+                        }
+                        uint4* dst = reinterpret_cast<uint4*>(buf + lane * 64);
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmO, buf, static_cast<int32_t>(col), slab_row);
+                            bulk_commit();
+                        }
+                        ++epi_it;
+                    } else if (valid) {
                         __nv_bfloat16* dst = orow + col;
 #pragma unroll
                         for (int v = 0; v < 4; ++v)
@@ -433,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
         }
+        if (epi_it && lane == 0) bulk_wait0();  // the TMA stores are complete before the CTA retires
     }
     tc_fence_before();
     __syncthreads();
@@ -480,28 +547,39 @@ uint64_t* gemm_trace_ptr(int which) { return g_trace[which & 1]; }
 
 bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                        uint32_t box_cols) {
+    return make_tmap_bf16_2d_ex(m, base, rows, cols, cols, box_rows, box_cols, true);
+}
+
+bool make_tmap_bf16_2d_ex(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch,
+                          uint32_t box_rows, uint32_t box_cols, bool swizzle128, uint32_t l2_promo) {
     EncodeTiledFn enc = get_encode_fn();
     if (!enc) return false;
     const cuuint64_t gdim[2] = {cols, rows};
-    const cuuint64_t gstride[1] = {cols * 2};
+    const cuuint64_t gstride[1] = {pitch * 2};
     const cuuint32_t box[2] = {box_cols, box_rows};
     const cuuint32_t estride[2] = {1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estride,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+               l2_promo == 0    ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+               : l2_promo == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+               : l2_promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                 : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
-                    const uint32_t* gmap, const uint32_t* starts, const CUtensorMap* tmA_small) {
+                    const uint32_t* gmap, const uint32_t* starts, const CUtensorMap* tmA_small,
+                    const CUtensorMap* tmO, const GemmBTail* btail) {
     launch_gemm_tc_epi(swiglu ? kEpiSwiglu : kEpiPlain, tmA, tmB, out, sh, offsets, mprefix, num_sms, s, 0, nullptr,
-                       gmap, starts, 1, tmA_small);
+                       gmap, starts, 1, tmA_small, tmO, btail);
 }
 
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                         uint32_t b_row0, const int32_t* colmap, const uint32_t* gmap, const uint32_t* starts,
-                        uint32_t ksplit, const CUtensorMap* tmA_small) {
+                        uint32_t ksplit, const CUtensorMap* tmA_small, const CUtensorMap* tmO,
+                        const GemmBTail* btail) {
     const bool swiglu = epi == kEpiSwiglu;
     TcParams p;
     p.G = sh.G;
@@ -528,6 +606,17 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
     const CUtensorMap& a16 = tmA_small ? tmA_small[0] : *tmA;
     const CUtensorMap& a32 = tmA_small ? tmA_small[1] : *tmA;
     const CUtensorMap& a64 = tmA_small ? tmA_small[2] : *tmA;
+    static const bool epi_tma = [] {  // MOEPRISM_EPI_TMA=0: direct vector stores only (A/B)
+        const char* e = std::getenv("MOEPRISM_EPI_TMA");
+        return !(e && e[0] == '0');
+    }();
+    p.tma_out = (epi == kEpiPlain && tmO && epi_tma) ? 1u : 0u;
+    const CUtensorMap& o_map = p.tma_out ? *tmO : *tmA;
+    const bool tail = btail && btail->valid && epi == kEpiSwiglu && btail->valid < sh.N_group / 2;
+    p.b_valid = tail ? btail->valid : 0u;
+    p.b_tail_rows = tail ? btail->tail_rows : 0u;
+    const CUtensorMap& bh_map = tail ? btail->half : *tmB;
+    const CUtensorMap& bt_map = tail ? btail->part : *tmB;
 
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT * p.ksplit;
@@ -538,11 +627,11 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiCount>), (int)kSmemBytes);
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiF32Part>), (int)kSmemBytes);
     switch (epi) {
-        case kEpiF32Part: launch_k(gemm_tc_kernel<kEpiF32Part>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
-        case kEpiSwiglu: launch_k(gemm_tc_kernel<kEpiSwiglu>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
-        case kEpiActAbs: launch_k(gemm_tc_kernel<kEpiActAbs>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
-        case kEpiCount: launch_k(gemm_tc_kernel<kEpiCount>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
-        default: launch_k(gemm_tc_kernel<kEpiPlain>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, p); break;
+        case kEpiF32Part: launch_k(gemm_tc_kernel<kEpiF32Part>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, o_map, bh_map, bt_map, p); break;
+        case kEpiSwiglu: launch_k(gemm_tc_kernel<kEpiSwiglu>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, o_map, bh_map, bt_map, p); break;
+        case kEpiActAbs: launch_k(gemm_tc_kernel<kEpiActAbs>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, o_map, bh_map, bt_map, p); break;
+        case kEpiCount: launch_k(gemm_tc_kernel<kEpiCount>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, o_map, bh_map, bt_map, p); break;
+        default: launch_k(gemm_tc_kernel<kEpiPlain>, grid, dim3(kThreads), kSmemBytes, s, *tmA, *tmB, a16, a32, a64, o_map, bh_map, bt_map, p); break;
     }
 }
 

@@ -148,6 +148,11 @@ T* dalloc(size_t n, const char* what) {
 }
 
 uint32_t round_up(uint32_t v, uint32_t m) { return (v + m - 1) / m * m; }
+// L2 promotion of the decode W2 map (MOEPRISM_W2D_PROMO, A/B only; default 64)
+uint32_t w2d_promo() {
+    const char* e = std::getenv("MOEPRISM_W2D_PROMO");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 64u;
+}
 
 bool is_device_ptr(const void* p) {
     cudaPointerAttributes a;
@@ -170,6 +175,7 @@ struct mp_layer_s {
     mp_layer_desc desc{};
     uint32_t E = 0, S = 0, G = 0, d = 0, ff = 0, dtype = 0, k_max = 0, max_tokens = 0;
     uint32_t w_pad = 0, d_pad = 0, G_pad = 0, rows_cap = 0, w2_rows = 0;
+    uint32_t w_sub = 0;  // neurons per sub-expert (the packed width w_pad rounds it up to 128)
     size_t esz = 4;
     int num_sms = 0;
     bool use_tc = false;
@@ -238,6 +244,9 @@ struct mp_layer_s {
     void* x_stage = nullptr;
     void* y_stage = nullptr;
     CUtensorMap tm_xperm{}, tm_h{}, tm_w1{}, tm_w2{};
+    CUtensorMap tm_o{};  // gemm2 output o, 32 x 32 boxes (TMA-store epilogue)
+    CUtensorMap tm_w2d{};  // W2 with K trimmed to w_sub (decode batches)
+    mp::GemmBTail w1_tail{};  // gemm1 reads only the w_sub valid neurons of each packed W1 group
     CUtensorMap tm_xperm_s[3]{}, tm_h_s[3]{};  // 16 / 32 / 64-row A boxes (short tiles of the 1-SM GEMM)
     CUtensorMap tm_w1h{}, tm_w2h{};  // 128-row boxes: each CTA of a pair loads half a B tile
 
@@ -684,12 +693,22 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
     const uint32_t* gmap = L->offload ? L->gmap_dev : nullptr;
+    static const bool tail_env = [] {  // MOEPRISM_W1_TAIL=0: gemm1 reads the padded W1 rows too (A/B)
+        const char* e = std::getenv("MOEPRISM_W1_TAIL");
+        return !(e && e[0] == '0');
+    }();
+    // decode batches (a few rows per sub-expert: HBM-bound on the weights)
+    // skip the W1 / W2 padding of w_sub -> w_pad; measured slower for large
+    // buckets (the tail tile's split B loads), so only there
+    const bool trim = tail_env && !L->offload && L->w_sub < L->w_pad &&
+                      (size_t)T * (kscalar ? kscalar : L->k_max) <= (size_t)64 * L->G;
     if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
                             L->ws.mprefix_tc2, L->num_sms, s, gmap);
     else if (L->use_tc)
         mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
-                           L->ws.mprefix_tc, L->num_sms, s, gmap, nullptr, L->tm_xperm_s);
+                           L->ws.mprefix_tc, L->num_sms, s, gmap, nullptr, L->tm_xperm_s, nullptr,
+                           trim ? &L->w1_tail : nullptr);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");
@@ -700,8 +719,9 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
                             L->ws.mprefix_tc2, L->num_sms, s, gmap);
     else if (L->use_tc)
-        mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : &L->tm_w2, L->o, g2, L->ws.offsets,
-                           L->ws.mprefix_tc, L->num_sms, s, gmap, nullptr, L->tm_h_s);
+        mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : trim ? &L->tm_w2d : &L->tm_w2, L->o, g2,
+                           L->ws.offsets,
+                           L->ws.mprefix_tc, L->num_sms, s, gmap, nullptr, L->tm_h_s, &L->tm_o);
     else
         mp::launch_gemm2_simt(L->dtype, L->h, L->W2, L->o, g2, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm2");
@@ -898,6 +918,7 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                 L->tile_mode = std::string(env) == "256" ? 2 : std::string(env) == "128" ? 1 : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
+            L->w_sub = w_sub;
             L->d_pad = round_up(L->d, 64);
             L->G_pad = round_up(L->G, 64);
             L->rows_cap = round_up(std::max<uint32_t>(L->max_tokens * L->k_max, 1), 128);
@@ -987,13 +1008,29 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                     bool ok =
                         mp::make_tmap_bf16_2d(&L->tm_xperm, L->x_perm, L->rows_cap, L->d_pad, 128, 64) &&
                         mp::make_tmap_bf16_2d(&L->tm_w1, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 256, 64) &&
-                        mp::make_tmap_bf16_2d(&L->tm_h, L->h, L->rows_cap, L->w_pad, 128, 64) &&
+                        // gemm2's A (h) stops at the w_sub valid neurons: its padding columns
+                        // are zero-filled by the TMA, not read (they hold garbage when gemm1
+                        // skipped the padding rows of W1, w1_tail)
+                        mp::make_tmap_bf16_2d_ex(&L->tm_h, L->h, L->rows_cap, L->w_sub, L->w_pad, 128, 64, true) &&
                         mp::make_tmap_bf16_2d(&L->tm_w2, L->W2, L->w2_rows, L->w_pad, 256, 64) &&
+                        // decode batches (HBM-bound): W2 read up to w_sub only, 64-byte L2
+                        // promotion so the trimmed row end does not fetch the padding
+                        mp::make_tmap_bf16_2d_ex(&L->tm_w2d, L->W2, L->w2_rows, L->w_sub, L->w_pad, 256, 64, true, w2d_promo()) &&
                         mp::make_tmap_bf16_2d(&L->tm_w1h, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 128, 64) &&
-                        mp::make_tmap_bf16_2d(&L->tm_w2h, L->W2, L->w2_rows, L->w_pad, 128, 64);
+                        mp::make_tmap_bf16_2d(&L->tm_w2h, L->W2, L->w2_rows, L->w_pad, 128, 64) &&
+                        mp::make_tmap_bf16_2d_ex(&L->tm_o, L->o, L->rows_cap, L->d, L->d_pad, 32, 32, false);
                     for (int b = 0; b < 3 && ok; ++b)
                         ok = mp::make_tmap_bf16_2d(&L->tm_xperm_s[b], L->x_perm, L->rows_cap, L->d_pad, 16u << b, 64) &&
-                             mp::make_tmap_bf16_2d(&L->tm_h_s[b], L->h, L->rows_cap, L->w_pad, 16u << b, 64);
+                             mp::make_tmap_bf16_2d_ex(&L->tm_h_s[b], L->h, L->rows_cap, L->w_sub, L->w_pad, 16u << b, 64,
+                                                      true);
+                    if (ok && L->w_sub < L->w_pad) {  // gemm1: the padding rows of each W1 group are not read
+                        L->w1_tail.valid = L->w_sub;
+                        L->w1_tail.tail_rows = round_up(L->w_sub % mp::kIlv ? L->w_sub % mp::kIlv : mp::kIlv, 8);
+                        ok = mp::make_tmap_bf16_2d(&L->w1_tail.half, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad, 128,
+                                                   64) &&
+                             mp::make_tmap_bf16_2d(&L->w1_tail.part, L->W1, (uint64_t)L->G * 2 * L->w_pad, L->d_pad,
+                                                   L->w1_tail.tail_rows, 64);
+                    }
                     if (!ok) fail(MP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                 }
             }

@@ -118,6 +118,19 @@ MP_DEV void bulk_store_s2g(void* dst, const void* src, uint32_t bytes) {
 MP_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 MP_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 MP_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// at most N bulk groups of this thread still reading their shared-memory source
+template <int N>
+MP_DEV void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// TMA tensor store of one box from shared memory (bulk group; the box is
+// clipped at the tensor map's extents)
+MP_DEV void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
 
 // 16-byte cp.async (L2 only), zero-filling dst beyond src_bytes (0 or 16)
 MP_DEV void cp_async_16(uint32_t dst_smem, const void* src, uint32_t src_bytes) {

@@ -163,10 +163,20 @@ void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const
 // gmap (nullable): group g's weights are B group gmap[g] (offload cache slots)
 // starts (nullable): group g's rows are [starts[g], offsets[g+1])
 // tmA_small (nullable): [3] maps of A with 16 / 32 / 64-row boxes (short tiles load only their rows)
+// tmO (nullable, plain epilogue): map of the output with 32 x 32 boxes, no swizzle
+//   (make_tmap_bf16_2d_ex): full 32-row warp slabs leave through TMA stores
+// gemm1 B tail: the packed W1 rows past `valid` neurons per group (padding to
+// the 128-row tile) are not read; half = 128-row-box map, part = map with
+// tail_rows-row boxes (valid % 64 rounded up to 8) of the packed W1.
+struct GemmBTail {
+    CUtensorMap half, part;
+    uint32_t valid, tail_rows;
+};
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                     const uint32_t* gmap = nullptr, const uint32_t* starts = nullptr,
-                    const CUtensorMap* tmA_small = nullptr);
+                    const CUtensorMap* tmA_small = nullptr, const CUtensorMap* tmO = nullptr,
+                    const GemmBTail* btail = nullptr);
 size_t gemm_tc_smem_bytes();
 // Epilogue modes of the 1-SM tensor-core GEMM (gemm_tc.cu).
 constexpr int kEpiPlain = 0;   // bf16 acc
@@ -179,7 +189,8 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                         uint32_t b_row0 = 0, const int32_t* colmap = nullptr, const uint32_t* gmap = nullptr,
                         const uint32_t* starts = nullptr, uint32_t ksplit = 1,
-                        const CUtensorMap* tmA_small = nullptr);
+                        const CUtensorMap* tmA_small = nullptr, const CUtensorMap* tmO = nullptr,
+                        const GemmBTail* btail = nullptr);
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
@@ -212,6 +223,12 @@ void launch_absmax(const float* p, size_t n, float* out, cudaStream_t s);
 // cuTensorMapEncodeTiled through the runtime's driver entry point.
 bool make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
                        uint32_t box_cols);
+// Same with a row pitch (elements) >= cols -- columns >= cols read as zeros /
+// are not written --, a choice of 128-byte swizzle or none, and the L2
+// promotion of the loads' misses (0 / 64 / 128 / 256 bytes; 256 re-reads
+// up to 192 bytes of padding past a trimmed row end).
+bool make_tmap_bf16_2d_ex(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch,
+                          uint32_t box_rows, uint32_t box_cols, bool swizzle128, uint32_t l2_promo = 256);
 
 }  // namespace mp
 
