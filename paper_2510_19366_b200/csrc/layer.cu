@@ -632,9 +632,11 @@ void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t
 
 // Decode batches (T * k_max <= 8 rows per sub-expert on average): nearly every
 // sub-expert receives a token, gemm1 reads its weights group by group in tile
-// order, and the routing chain before it leaves HBM idle.  Prefetch the W1
-// tiles of the first groups (<= 64 MB, well inside the 126 MB L2) on a side
-// stream meanwhile; joined before the combine (graph-capturable).
+// order, and the routing chain before it leaves HBM idle.  Optionally
+// (MOEPRISM_DECODE_PF_MB > 0) prefetch the W1 tiles of the first groups into
+// L2 on a side stream meanwhile; joined before the combine (graph-capturable).
+// Off by default: measured 3-5% slower at Qwen decode (the prefetch competes
+// with the routing chain; profiles/r02e_pf_sweep.txt).
 void prefetch_routed_weights(mp_layer_s* L, uint32_t T, cudaStream_t s) {
     L->pf_pending = false;
     if (!L->use_tc || L->offload || !L->has_experts || (size_t)T * L->k_max > (size_t)8 * L->G) return;
@@ -644,7 +646,12 @@ void prefetch_routed_weights(mp_layer_s* L, uint32_t T, cudaStream_t s) {
         ck(cudaEventCreateWithFlags(&L->pf_join, cudaEventDisableTiming), "prefetch event");
     }
     const size_t w1_group = (size_t)2 * L->w_pad * L->d_pad * L->esz;
-    const size_t bytes = std::min<size_t>((size_t)L->G * w1_group, (size_t)64 << 20);
+    static const size_t cap = [] {  // MOEPRISM_DECODE_PF_MB: prefetch size (A/B)
+        const char* e = std::getenv("MOEPRISM_DECODE_PF_MB");
+        return (size_t)(e ? std::atoi(e) : 0) << 20;
+    }();
+    const size_t bytes = std::min<size_t>((size_t)L->G * w1_group, cap);
+    if (!bytes) return;
     ck(cudaEventRecord(L->pf_fork, s), "prefetch fork");
     ck(cudaStreamWaitEvent(L->pf_stream, L->pf_fork, 0), "prefetch fork");
     mp::launch_l2_prefetch(L->W1, bytes, L->pf_stream);
@@ -736,7 +743,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     mp::launch_combine(L->dtype, L->o, L->d, L->d_pad, L->ws.slot_row, sel, w, L->k_max, group_S, T, y, s,
                        shared ? (L->sh_splits ? static_cast<const void*>(L->sh_o32) : L->sh_o) : nullptr,
                        shared ? L->sh_w : nullptr, (with_shared && L->residual) ? x : nullptr,
-                       shared ? L->sh_splits : 0u, static_cast<size_t>(T) * L->d_pad);
+                       shared ? L->sh_splits : 0u, static_cast<size_t>(T) * L->d_pad, kscalar, L->num_sms);
     ck_launch("combine");
     tm.end(5, 1);
 }
@@ -802,12 +809,12 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
                 return !(e && e[0] == '0');
             }();
             if (fuse_bucket && fuse_env && L->has_experts && (L->d % 4) == 0) {
-                // routing epilogue + exact near-tie re-selection + bucketing in one kernel;
-                // many K splits (small batches): reduce them first across (token, g) warps
+                // routing epilogue + exact near-tie re-selection + bucketing in one kernel
+                // (many K splits -- small batches -- are summed CTA-wide inside it)
                 uint32_t ks = pl.ks;
-                static const uint32_t reduce_above = [] {  // MOEPRISM_PARTIALS_REDUCE_ABOVE (A/B)
+                static const uint32_t reduce_above = [] {  // MOEPRISM_PARTIALS_REDUCE_ABOVE: separate reduce (A/B)
                     const char* e = std::getenv("MOEPRISM_PARTIALS_REDUCE_ABOVE");
-                    return e ? static_cast<uint32_t>(std::atoi(e)) : 8u;
+                    return e ? static_cast<uint32_t>(std::atoi(e)) : 0xFFFFFFFFu;
                 }();
                 if (ks > reduce_above) {
                     mp::launch_partials_reduce(L->r_partial, ks, T, L->G, pl.Npad, s);
@@ -817,7 +824,7 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
                 }
                 mp::launch_route_bucket(L->r_partial, ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
                                         L->sel, L->wsel, rg, x, L->d, L->wrT, L->r_ticket, L->r_flagged,
-                                        L->ws, s, mp::route_tokens_per_block(T));
+                                        L->ws, s, mp::route_tokens_per_block(T), L->num_sms);
                 bucketed = true;
                 ck_launch("router(tc)+bucket");
                 tm.end(0, 2);
@@ -957,8 +964,8 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
                     const size_t n_part = mp::router_tc_partial_rows(L->max_tokens, L->d, L->G, L->num_sms);
                     L->wr_planes = dalloc<char>((size_t)3 * L->r_npad * L->d * 2, "router planes");
                     L->r_partial = dalloc<double>(n_part * L->r_npad, "router partials");
-                    L->r_ticket = dalloc<uint32_t>(1, "router ticket");
-                    ck(cudaMemset(L->r_ticket, 0, sizeof(uint32_t)), "memset ticket");
+                    L->r_ticket = dalloc<uint32_t>(4, "router ticket");
+                    ck(cudaMemset(L->r_ticket, 0, 4 * sizeof(uint32_t)), "memset ticket");
                     if (!mp::make_tmap_bf16_2d(&L->tm_wplanes, L->wr_planes, 3ull * L->r_npad, L->d,
                                                mp::router_tc_cols_per_cta(L->G), 64))
                         fail(MP_ERR_CUDA, "router planes tensor map");

@@ -85,7 +85,7 @@ void launch_dispatch(int dtype, const void* x, uint32_t T, uint32_t d, uint32_t 
 void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
                     const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
                     cudaStream_t s, const void* o_sh = nullptr, const float* w_sh = nullptr,
-                    const void* x_res = nullptr, uint32_t sh_splits = 0, size_t sh_stride = 0);
+                    const void* x_res = nullptr, uint32_t sh_splits = 0, size_t sh_stride = 0, uint32_t k_hint = 0, int num_sms = 148);
 void launch_shared_gate(const void* x, uint32_t T, uint32_t d, const float* gate, float* w_sh, uint32_t* sh_off,
                         uint32_t* sh_mprefix, cudaStream_t s);
 
@@ -125,12 +125,17 @@ void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32
 void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
                          const RouterGuard& rg, const void* x, uint32_t d, const float* wrT, uint32_t* ticket,
-                         uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb = kRouteTokensPerBlock);
+                         uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb = kRouteTokensPerBlock,
+                         int num_sms = 0);
 // tokens per CTA of the fused routing epilogue: fewer for small batches (more
 // CTAs; measured: one or two 32-token CTAs at T = 64 are slower)
 inline uint32_t route_tokens_per_block(uint32_t T) {
     return T <= 256 ? 2u : T <= 1024 ? 8u : kRouteTokensPerBlock;
 }
+// ticket: 3 zeroed words (last-CTA ticket; grid-barrier arrive / depart
+// counters), left zero.  More than 8 K splits are summed CTA-wide in the
+// kernel.  num_sms: a grid of <= num_sms CTAs forms its bucket bases after a
+// grid barrier.
 // in-place fixed-order sum of the K-split router partials into plane 0
 void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, cudaStream_t s);
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,

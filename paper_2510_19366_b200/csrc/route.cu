@@ -26,6 +26,7 @@ constexpr uint32_t TB = kRouteTokensPerBlock;  // tokens per CTA
 constexpr uint32_t GB = 64;                    // router outputs per pass
 constexpr uint32_t KC = 32;                    // K chunk staged in smem
 constexpr uint32_t kRouterThreads = 256;
+constexpr uint32_t kWarpSplits = 8;  // route_bucket: more router K splits are summed CTA-wide
 
 // Per-token certification bound of the tensor-core router logits (RouterGuard,
 // mp_kernels.h): coef * sum |x_t| + 2^-23 max_g |logit_tg| + floor, with
@@ -417,6 +418,63 @@ __device__ void bucket_scan_body(uint32_t nblk, uint32_t G, const uint32_t* __re
     }
 }
 
+// Grid-scan variant (every CTA b of a co-resident grid, after a grid barrier):
+// block_base[b][g] = offsets[g] + sum_{b' < b} counts[b'][g] for this CTA's
+// row only; offsets / tile prefixes scanned redundantly per CTA, written by
+// CTA 0.  Thread (g, q) sums the q-th range of blocks.
+__device__ void bucket_bases_grid(uint32_t nblk, uint32_t b, uint32_t G, const uint32_t* __restrict__ block_counts,
+                                  uint32_t* __restrict__ block_base, uint32_t* __restrict__ offsets,
+                                  uint32_t* __restrict__ mprefix_tc, uint32_t* __restrict__ mprefix_simt,
+                                  uint32_t* __restrict__ mprefix_tc2) {
+    constexpr int V = 4;
+    __shared__ uint32_t part_all[1024], part_pre[1024];
+    __shared__ uint32_t wsum[V + 1][32];
+    const uint32_t Q = blockDim.x / G;
+    const uint32_t g = threadIdx.x % G, q = threadIdx.x / G;
+    const bool active = q < Q;
+    const uint32_t per = (nblk + Q - 1) / Q;
+    const uint32_t b0 = q * per, b1 = min(b0 + per, nblk);
+    uint32_t all = 0, pre = 0;
+    if (active) {
+#pragma unroll 8
+        for (uint32_t bb = b0; bb < b1; ++bb) {
+            const uint32_t c = __ldcg(block_counts + (size_t)bb * G + g);
+            all += c;
+            pre += bb < b ? c : 0u;
+        }
+    }
+    part_all[threadIdx.x] = all;
+    part_pre[threadIdx.x] = pre;
+    __syncthreads();
+    const uint32_t gi = threadIdx.x;
+    uint32_t total = 0, prefix = 0;
+    if (gi < G) {
+        for (uint32_t r = 0; r < Q; ++r) {
+            total += part_all[r * G + gi];
+            prefix += part_pre[r * G + gi];
+        }
+    }
+    uint32_t sv[V] = {total, gi < G ? (total + kTcBM - 1) / kTcBM : 0u, gi < G ? (total + kSimtBM - 1) / kSimtBM : 0u,
+                      gi < G ? (total + 255) / 256 : 0u};
+    uint32_t tot[V];
+    block_exclusive_scan_1024_multi<V>(sv, tot, wsum);
+    if (gi < G) block_base[(size_t)b * G + gi] = sv[0] + prefix;
+    if (b == 0) {
+        if (gi < G) {
+            offsets[gi] = sv[0];
+            mprefix_tc[gi] = sv[1];
+            mprefix_simt[gi] = sv[2];
+            mprefix_tc2[gi] = sv[3];
+        }
+        if (gi == 0) {
+            offsets[G] = tot[0];
+            mprefix_tc[G] = tot[1];
+            mprefix_simt[G] = tot[2];
+            mprefix_tc2[G] = tot[3];
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024) bucket_scan_kernel(uint32_t nblk, uint32_t G,
                                                            const uint32_t* __restrict__ block_counts,
                                                            uint32_t* __restrict__ block_base,
@@ -488,7 +546,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     float* __restrict__ wout, int* __restrict__ err, RouterGuard rg, const __nv_bfloat16* __restrict__ x, uint32_t d,
     const float* __restrict__ wrT, uint32_t* __restrict__ ticket, uint32_t* __restrict__ stats, uint32_t* lrank,
     uint32_t* block_counts, uint32_t* block_base, uint32_t* offsets, uint32_t* mprefix_tc, uint32_t* mprefix_simt,
-    uint32_t* mprefix_tc2, uint32_t tb, uint32_t smem_bytes) {
+    uint32_t* mprefix_tc2, uint32_t tb, uint32_t smem_bytes, uint32_t grid_scan) {
     extern __shared__ double rsm[];  // [tb][G] logits, then [tb][G] keys; the last CTA: staged counts
     double* sc = rsm + (size_t)(threadIdx.x / 32) * G;        // used by warps < tb only
     double* key = rsm + (size_t)(tb + threadIdx.x / 32) * G;
@@ -518,6 +576,22 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     if (threadIdx.x == 0) n_pairs = 0;
     griddep_wait();
     griddep_launch();
+    // many K splits (small batches: 64-deep router chunks) and few tokens per
+    // CTA: the whole CTA sums the splits, one (token, sub-expert) per thread,
+    // into the logit rows (replaces a separate partials_reduce launch; same
+    // ascending fixed order)
+    const bool coop = ks > kWarpSplits;
+    if (coop) {
+        for (uint32_t q = threadIdx.x; q < tb * G; q += blockDim.x) {
+            const uint32_t tl = q / G, g = q - tl * G;
+            if (t0 + tl >= T) continue;
+            const double* pp = partial + (size_t)(t0 + tl) * Npad + g;
+            double v = 0.0;
+#pragma unroll 8
+            for (uint32_t s = 0; s < ks; ++s) v += __ldcg(pp + (size_t)s * T * Npad);
+            rsm[(size_t)tl * G + g] = v;
+        }
+    }
     __syncthreads();
     bool flagged = false;
     uint32_t kt = 0;
@@ -531,13 +605,18 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
 #pragma unroll
         for (int c = 0; c < NC; ++c) v[c] = 0.0;
         const double* prow = partial + (size_t)t * Npad + lane;
+        if (coop) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) v[c] = lane + 32u * c < G ? sc[lane + 32u * c] : 0.0;
+        } else {
 #pragma unroll 4
-        for (uint32_t s = 0; s < ks; ++s) {
-            double u[NC];
+            for (uint32_t s = 0; s < ks; ++s) {
+                double u[NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) u[c] = lane + 32u * c < G ? __ldcg(prow + (size_t)s * T * Npad + 32u * c) : 0.0;
+                for (int c = 0; c < NC; ++c) u[c] = lane + 32u * c < G ? __ldcg(prow + (size_t)s * T * Npad + 32u * c) : 0.0;
 #pragma unroll
-            for (int c = 0; c < NC; ++c) v[c] += u[c];
+                for (int c = 0; c < NC; ++c) v[c] += u[c];
+            }
         }
         double maxabs = 0.0;
 #pragma unroll
@@ -632,6 +711,37 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     // (fences are cumulative over what the barrier made visible to it)
     __syncthreads();
     MP_RT_STAMP();  // 4: ranks done
+    if (grid_scan) {
+        // grid-wide barrier (the grid fits on the GPU at once: one 1024-thread
+        // CTA per SM, gridDim <= SMs) -- then EVERY CTA forms its own bucket
+        // bases from all CTAs' counts, instead of one last CTA writing all of
+        // them after the others retire
+        if (threadIdx.x == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            atomicAdd(ticket + 1, 1u);
+            uint32_t seen;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ticket + 1) : "memory");
+            } while (seen < gridDim.x);
+        }
+        __syncthreads();
+        MP_RT_STAMP();  // 5: barrier passed
+        bucket_bases_grid(gridDim.x, blockIdx.x, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt,
+                          mprefix_tc2);
+        if (threadIdx.x == 0 && atomicAdd(ticket + 2, 1u) == gridDim.x - 1) {
+            ticket[1] = 0;  // every CTA is past the barrier: reset for the next forward (stream-ordered)
+            ticket[2] = 0;
+        }
+#if MP_ROUTE_TRACE
+        __syncthreads();
+        MP_RT_STAMP();  // 6: bases done
+        if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+            printf("route_bucket(grid) blk %u: topk %llu exact %llu masks %llu ranks %llu barrier %llu bases %llu ns\n",
+                   blockIdx.x, tr_[1] - tr_[0], tr_[2] - tr_[1], tr_[3] - tr_[2], tr_[4] - tr_[3], tr_[5] - tr_[4],
+                   tr_[6] - tr_[5]);
+#endif
+        return;
+    }
     if (threadIdx.x == 0) {
         // release (acq_rel: not the heavier sequentially consistent fence)
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -818,7 +928,8 @@ __global__ void __launch_bounds__(256) dispatch_bulk_kernel(const __nv_bfloat16*
 // y[t] = sum_{j ascending} w[t][j] * o[slot_row[t][j]] in a fixed order
 // (ascending sub-expert id), no atomics.  CTA per token.
 // bf16 mode: o is bf16, fp32 accumulate, 16-byte vector loads / stores.
-__global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* __restrict__ o, uint32_t d,
+template <int U>
+__global__ void __launch_bounds__(256, U >= 8 ? 3 : 5) combine_bf16_kernel(const __nv_bfloat16* __restrict__ o, uint32_t d,
                                                            uint32_t d_pad, const uint32_t* __restrict__ slot_row,
                                                            const float* __restrict__ w, uint32_t k_max,
                                                            const __nv_bfloat16* __restrict__ o_sh,
@@ -832,9 +943,24 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
     const uint32_t t = blockIdx.x;
     griddep_wait();
     griddep_launch();
-    for (uint32_t j = threadIdx.x; j < k_max; j += blockDim.x) {
-        rows[j] = slot_row[(size_t)t * k_max + j];
-        wts[j] = w ? w[(size_t)t * k_max + j] : 1.0f;
+    // the token's selected slots, compacted in ascending slot order (the
+    // summation order); warp 0, k_max <= kMaxG
+    __shared__ uint32_t n_rows;
+    if (threadIdx.x < 32) {
+        uint32_t base = 0;
+        for (uint32_t j0 = 0; j0 < k_max; j0 += 32) {
+            const uint32_t j = j0 + threadIdx.x;
+            const uint32_t r = j < k_max ? slot_row[(size_t)t * k_max + j] : kSelNone;
+            const bool has = r != kSelNone;
+            const uint32_t bal = __ballot_sync(0xffffffffu, has);
+            if (has) {
+                const uint32_t at = base + __popc(bal & ((1u << threadIdx.x) - 1u));
+                rows[at] = r;
+                wts[at] = w ? w[(size_t)t * k_max + j] : 1.0f;
+            }
+            base += __popc(bal);
+        }
+        if (threadIdx.x == 0) n_rows = base;
     }
     __syncthreads();
     __nv_bfloat16* yr = y + (size_t)t * d;
@@ -851,28 +977,47 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
                     acc[2 * q + 1] = f.y;
                 }
             }
-            for (uint32_t j = 0; j < k_max; ++j) {
-                const uint32_t r = rows[j];
-                if (r == kSelNone) continue;
-                const float wj = wts[j];
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(o + (size_t)r * d_pad + c));
-                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+            // U selected rows in flight per lane, then accumulated in
+            // ascending slot order (one load in turn left the kernel
+            // latency-bound: 16 us for a 64-token decode batch)
+            const uint32_t nr = n_rows;
+            for (uint32_t j0 = 0; j0 < nr; j0 += U) {
+                uint4 v[U];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float2 f = __bfloat1622float2(h[q]);
-                    acc[2 * q] = fmaf(wj, f.x, acc[2 * q]);
-                    acc[2 * q + 1] = fmaf(wj, f.y, acc[2 * q + 1]);
+                for (uint32_t u = 0; u < U; ++u)
+                    v[u] = j0 + u < nr ? __ldg(reinterpret_cast<const uint4*>(o + (size_t)rows[j0 + u] * d_pad + c))
+                                       : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                for (uint32_t u = 0; u < U; ++u) {
+                    if (j0 + u >= nr) break;
+                    const float wj = wts[j0 + u];
+                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float2 f = __bfloat1622float2(h[q]);
+                        acc[2 * q] = fmaf(wj, f.x, acc[2 * q]);
+                        acc[2 * q + 1] = fmaf(wj, f.y, acc[2 * q + 1]);
+                    }
                 }
             }
             if (o_sh32) {  // shared expert from split-K fp32 partials, summed in split order
                 float sum[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
-                for (uint32_t sp = 0; sp < sh_splits; ++sp) {
-                    const float* pr = o_sh32 + sp * sh_stride + (size_t)t * d_pad + c;
-                    const float4 a = __ldg(reinterpret_cast<const float4*>(pr));
-                    const float4 b = __ldg(reinterpret_cast<const float4*>(pr + 4));
-                    sum[0] += a.x, sum[1] += a.y, sum[2] += a.z, sum[3] += a.w;
-                    sum[4] += b.x, sum[5] += b.y, sum[6] += b.z, sum[7] += b.w;
+                constexpr uint32_t SU = U >= 8 ? 6 : 2;  // splits in flight
+                for (uint32_t sp0 = 0; sp0 < sh_splits; sp0 += SU) {
+                    float4 a[SU], b[SU];
+#pragma unroll
+                    for (uint32_t u = 0; u < SU; ++u) {
+                        const float* pr = o_sh32 + (sp0 + u) * sh_stride + (size_t)t * d_pad + c;
+                        const bool ok = sp0 + u < sh_splits;
+                        a[u] = ok ? __ldg(reinterpret_cast<const float4*>(pr)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        b[u] = ok ? __ldg(reinterpret_cast<const float4*>(pr + 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (uint32_t u = 0; u < SU; ++u) {
+                        if (sp0 + u >= sh_splits) break;
+                        sum[0] += a[u].x, sum[1] += a[u].y, sum[2] += a[u].z, sum[3] += a[u].w;
+                        sum[4] += b[u].x, sum[5] += b[u].y, sum[6] += b[u].z, sum[7] += b[u].w;
+                    }
                 }
                 const float ws = w_sh[t];
 #pragma unroll
@@ -898,8 +1043,7 @@ __global__ void __launch_bounds__(256) combine_bf16_kernel(const __nv_bfloat16* 
     } else {
         for (uint32_t c = threadIdx.x; c < d; c += blockDim.x) {
             float acc = x_res ? __bfloat162float(x_res[(size_t)t * d + c]) : 0.0f;
-            for (uint32_t j = 0; j < k_max; ++j)
-                if (rows[j] != kSelNone) acc = fmaf(wts[j], __bfloat162float(o[(size_t)rows[j] * d_pad + c]), acc);
+            for (uint32_t j = 0; j < n_rows; ++j) acc = fmaf(wts[j], __bfloat162float(o[(size_t)rows[j] * d_pad + c]), acc);
             if (o_sh32) {
                 float sum = 0.0f;
                 for (uint32_t sp = 0; sp < sh_splits; ++sp) sum += o_sh32[sp * sh_stride + (size_t)t * d_pad + c];
@@ -1014,10 +1158,17 @@ void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G
 void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
                          const RouterGuard& rg, const void* x, uint32_t d, const float* wrT, uint32_t* ticket,
-                         uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb) {
+                         uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb, int num_sms) {
     // the routing arrays, or the last CTA's staged counts (1 byte per block and
     // bucket) when they are larger and fit
     const size_t nblk = (T + tb - 1) / tb;
+    // one 1024-thread CTA per SM: a grid that fits on the GPU at once can
+    // synchronise (grid barrier) and form its bucket bases in parallel
+    static const bool grid_env = [] {  // MOEPRISM_GRID_SCAN=0: last-CTA scans only (A/B)
+        const char* e = std::getenv("MOEPRISM_GRID_SCAN");
+        return !(e && e[0] == '0');
+    }();
+    const bool grid_scan = grid_env && nblk <= static_cast<size_t>(num_sms);
     size_t smem = sizeof(double) * 2 * tb * G;
     if (nblk * G > smem && nblk * G <= 160 * 1024) smem = (nblk * G + 15) & ~size_t(15);
     auto launch = [&](auto kern) {
@@ -1028,7 +1179,8 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
         launch_k(kern, dim3((T + tb - 1) / tb), dim3(1024), smem, s,
             partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, rg,
             static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, stats, ws.lrank, ws.block_counts, ws.block_base,
-            ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb, static_cast<uint32_t>(smem));
+            ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb, static_cast<uint32_t>(smem),
+            grid_scan ? 1u : 0u);
     };
     if (G <= 64)
         launch(route_bucket_kernel<2>);
@@ -1163,15 +1315,29 @@ void launch_shared_gate(const void* x, uint32_t T, uint32_t d, const float* gate
 void launch_combine(int dtype, const void* o, uint32_t d, uint32_t d_pad, const uint32_t* slot_row,
                     const uint32_t* sel, const float* w, uint32_t k_max, uint32_t group_S, uint32_t T, void* y,
                     cudaStream_t s, const void* o_sh, const float* w_sh, const void* x_res, uint32_t sh_splits,
-                    size_t sh_stride) {
+                    size_t sh_stride, uint32_t k_hint, int num_sms) {
     // sh_splits > 0: o_sh holds fp32 split-K partials [sh_splits][stride]
     const float* o_sh32 = sh_splits ? static_cast<const float*>(o_sh) : nullptr;
-    if (dtype == 1)
-        launch_k(combine_bf16_kernel, dim3(T), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(o), d, d_pad,
-                 slot_row, w, k_max, sh_splits ? nullptr : static_cast<const __nv_bfloat16*>(o_sh), w_sh, o_sh32,
-                 sh_splits, sh_stride, static_cast<const __nv_bfloat16*>(x_res),
-                                              static_cast<__nv_bfloat16*>(y));
-    else
+    // rows in flight per lane: many tokens (CTAs) hide the load latency by
+    // occupancy, few (decode) need it per lane; measured (mixtral_quick /
+    // qwen_quick): U = 8 cut a 64-token combine 16 -> 10 us but slowed
+    // 4096-token k <= 4 batches (registers -> fewer resident CTAs)
+    const uint32_t kh = k_hint ? k_hint : k_max;
+    const int U = (T <= 4u * (uint32_t)num_sms || kh >= 12) ? 8 : kh >= 6 ? 4 : 2;
+    auto go = [&](auto kern) {
+        launch_k(kern, dim3(T), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(o), d, d_pad, slot_row, w, k_max,
+                 sh_splits ? nullptr : static_cast<const __nv_bfloat16*>(o_sh), w_sh, o_sh32, sh_splits, sh_stride,
+                 static_cast<const __nv_bfloat16*>(x_res), static_cast<__nv_bfloat16*>(y));
+    };
+    if (dtype == 1) {
+        if (U == 8)
+            go(combine_bf16_kernel<8>);
+        else if (U == 4)
+            go(combine_bf16_kernel<4>);
+        else
+            go(combine_bf16_kernel<2>);
+    }
+    if (dtype != 1)
         combine_f64_kernel<<<T, 256, 0, s>>>(static_cast<const double*>(o), d, d_pad, slot_row, sel, w, k_max, group_S,
                                              static_cast<float*>(y));
 }

@@ -8,7 +8,7 @@ from paper_2510_19366_b200 import synth_fill
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 L = bench.build_qwen_layer(8192)
 d = bench.QW["d"]
-for T in (64, 8192):
+for T in [int(v) for v in __import__("os").environ.get("QWEN_T", "64,8192").split(",")]:
     xs = [synth_fill(torch.empty((T, d), dtype=torch.bfloat16, device='cuda'), 19 + i, 1.0) for i in range(4)]
     y = torch.empty((T, d), dtype=torch.bfloat16, device='cuda')
     for k in (4, 8, 16):
