@@ -88,6 +88,10 @@ struct TcParams {
     // rows hold stale data, so the matching h columns are garbage: gemm2 reads
     // h and W2 through maps whose K extent stops at the valid neurons.
     uint32_t b_valid, b_tail_rows;
+    // gemm1 A gather (nullable): token id of every permuted row; A rows are
+    // then gathered from the token matrix x (tmA: box {64 cols, 1 row}) by
+    // TMA gather4 -- no materialised x_perm (dispatch writes tables only)
+    const uint32_t* gather_tok;
 };
 
 __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix, uint32_t G, uint32_t NT,
@@ -221,7 +225,92 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    // one B stage: the 256-row weight tile, or (gemm1 B tail) its valid blocks
+    auto load_b = [&](uint32_t s, uint32_t ph, uint32_t kb, int32_t row, uint32_t n) {
+        mbar_wait(&emptyB[s], ph ^ 1u);
+        const int32_t kc = static_cast<int32_t>(kb * BK);
+        const uint32_t nb = n * 2;  // first 64-neuron block of the tile (128 rows: gate, up)
+        if (!p.b_valid || p.b_valid >= (nb + 2) * 64) {
+            mbar_expect_tx(&fullB[s], B_BYTES);
+            tma_load_2d(sB + s * B_BYTES, &tmB, &fullB[s], kc, row);
+        } else {
+            uint32_t v[2], bytes = 0;
+#pragma unroll
+            for (uint32_t hb = 0; hb < 2; ++hb) {
+                const uint32_t lo = (nb + hb) * 64;
+                v[hb] = p.b_valid > lo ? min(64u, p.b_valid - lo) : 0u;
+                bytes += v[hb] == 64 ? 128 * BK * 2 : v[hb] ? 2 * p.b_tail_rows * BK * 2 : 0;
+            }
+            mbar_expect_tx(&fullB[s], bytes);
+#pragma unroll
+            for (uint32_t hb = 0; hb < 2; ++hb) {
+                uint8_t* dst = sB + s * B_BYTES + hb * (128 * BK * 2);
+                const int32_t r = row + static_cast<int32_t>(hb * 128);
+                if (v[hb] == 64) {
+                    tma_load_2d(dst, &tmBh, &fullB[s], kc, r);
+                } else if (v[hb]) {  // gate rows, then the up rows of the same neurons
+                    tma_load_2d(dst, &tmBt, &fullB[s], kc, r);
+                    tma_load_2d(dst + kIlv * BK * 2, &tmBt, &fullB[s], kc, r + static_cast<int32_t>(kIlv));
+                }
+            }
+        }
+    };
+    if (warp == 0 && p.gather_tok) {
+        // Gather producer: the whole warp.  Lane 0 streams B and arms the A
+        // barriers; for A, lane q gathers rows 4q..4q+3 of the tile with one
+        // TMA gather4 per k-block (token ids of the tile held in registers).
+        int32_t tok[4] = {0, 0, 0, 0};
+        auto set_rows = [&](Cursor& c, bool is_a) {
+            if (c.tile >= total) return;
+            uint32_t g, m, n, split;
+            decode(c.tile, c.i, g, m, n, split);
+            c.row = is_a ? static_cast<int32_t>(s_start[g] + m * BM)
+                         : static_cast<int32_t>(p.b_row0 + s_gmap[g] * p.N_group + n * BN);
+            c.rows = min(BM, s_off[g + 1] - s_start[g] - m * BM);
+            c.n = n;
+            c.kb = split * p.kps;
+            c.kb1 = min(nkb, c.kb + p.kps);
+            if (is_a) {
+                const uint32_t first = __ldg(p.gather_tok + c.row);  // padding rows repeat a valid token
+#pragma unroll
+                for (uint32_t r = 0; r < 4; ++r) {
+                    const uint32_t rr = lane * 4 + r;
+                    tok[r] = static_cast<int32_t>(rr < c.rows ? __ldg(p.gather_tok + c.row + rr) : first);
+                }
+            }
+        };
+        auto advance = [&](Cursor& c, bool is_a) {
+            if (++c.kb == c.kb1) {
+                c.tile += gridDim.x;
+                ++c.i;
+                set_rows(c, is_a);
+            }
+        };
+        Cursor cb{blockIdx.x, 0, 0, 0, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0, 0, 0, 0};
+        set_rows(cb, false);
+        set_rows(ca, true);
+        uint32_t ib = 0, ia = 0;
+        while (cb.tile < total || ca.tile < total) {
+            if (cb.tile < total) {
+                if (lane == 0) load_b(ib % NB, (ib / NB) & 1u, cb.kb, cb.row, cb.n);
+                advance(cb, false);
+                ++ib;
+            }
+            if (ca.tile < total && (ib >= ia + (NB - NA) || cb.tile >= total)) {
+                const uint32_t s = ia % NA, ph = (ia / NA) & 1u;
+                const uint32_t ng = (ca.rows + 3) / 4;
+                if (lane == 0) {
+                    mbar_wait(&emptyA[s], ph ^ 1u);
+                    mbar_expect_tx(&fullA[s], ng * 4 * BK * 2);
+                }
+                __syncwarp();
+                if (lane < ng) tma_gather4(sA + s * A_BYTES + lane * (4 * BK * 2), &tmA, &fullA[s],
+                                           static_cast<int32_t>(ca.kb * BK), tok);
+                advance(ca, true);
+                ++ia;
+            }
+        }
+    } else if (warp == 0) {
         if (lane == 0) {
             // one ordered issue stream: B(j) then A(j - (NB - NA)), each behind
             // its own empty barrier
@@ -248,34 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             set_rows(ca, true);
             uint32_t ib = 0, ia = 0;  // loads issued per stream
             auto issue_b = [&]() {
-                const uint32_t s = ib % NB, ph = (ib / NB) & 1u;
-                mbar_wait(&emptyB[s], ph ^ 1u);
-                const int32_t kc = static_cast<int32_t>(cb.kb * BK);
-                const uint32_t nb = cb.n * 2;  // first 64-neuron block of the tile (128 rows: gate, up)
-                if (!p.b_valid || p.b_valid >= (nb + 2) * 64) {
-                    mbar_expect_tx(&fullB[s], B_BYTES);
-                    tma_load_2d(sB + s * B_BYTES, &tmB, &fullB[s], kc, cb.row);
-                } else {
-                    uint32_t v[2], bytes = 0;
-#pragma unroll
-                    for (uint32_t hb = 0; hb < 2; ++hb) {
-                        const uint32_t lo = (nb + hb) * 64;
-                        v[hb] = p.b_valid > lo ? min(64u, p.b_valid - lo) : 0u;
-                        bytes += v[hb] == 64 ? 128 * BK * 2 : v[hb] ? 2 * p.b_tail_rows * BK * 2 : 0;
-                    }
-                    mbar_expect_tx(&fullB[s], bytes);
-#pragma unroll
-                    for (uint32_t hb = 0; hb < 2; ++hb) {
-                        uint8_t* dst = sB + s * B_BYTES + hb * (128 * BK * 2);
-                        const int32_t r = cb.row + static_cast<int32_t>(hb * 128);
-                        if (v[hb] == 64) {
-                            tma_load_2d(dst, &tmBh, &fullB[s], kc, r);
-                        } else if (v[hb]) {  // gate rows, then the up rows of the same neurons
-                            tma_load_2d(dst, &tmBt, &fullB[s], kc, r);
-                            tma_load_2d(dst + kIlv * BK * 2, &tmBt, &fullB[s], kc, r + static_cast<int32_t>(kIlv));
-                        }
-                    }
-                }
+                load_b(ib % NB, (ib / NB) & 1u, cb.kb, cb.row, cb.n);
                 advance(cb, false);
                 ++ib;
             };
@@ -570,16 +632,16 @@ bool make_tmap_bf16_2d_ex(CUtensorMap* m, const void* base, uint64_t rows, uint6
 void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                     const uint32_t* gmap, const uint32_t* starts, const CUtensorMap* tmA_small,
-                    const CUtensorMap* tmO, const GemmBTail* btail) {
+                    const CUtensorMap* tmO, const GemmBTail* btail, const uint32_t* gather_tok) {
     launch_gemm_tc_epi(swiglu ? kEpiSwiglu : kEpiPlain, tmA, tmB, out, sh, offsets, mprefix, num_sms, s, 0, nullptr,
-                       gmap, starts, 1, tmA_small, tmO, btail);
+                       gmap, starts, 1, tmA_small, tmO, btail, gather_tok);
 }
 
 void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                         const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                         uint32_t b_row0, const int32_t* colmap, const uint32_t* gmap, const uint32_t* starts,
                         uint32_t ksplit, const CUtensorMap* tmA_small, const CUtensorMap* tmO,
-                        const GemmBTail* btail) {
+                        const GemmBTail* btail, const uint32_t* gather_tok) {
     const bool swiglu = epi == kEpiSwiglu;
     TcParams p;
     p.G = sh.G;
@@ -611,6 +673,7 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
         return !(e && e[0] == '0');
     }();
     p.tma_out = (epi == kEpiPlain && tmO && epi_tma) ? 1u : 0u;
+    p.gather_tok = epi == kEpiSwiglu ? gather_tok : nullptr;
     const CUtensorMap& o_map = p.tma_out ? *tmO : *tmA;
     const bool tail = btail && btail->valid && epi == kEpiSwiglu && btail->valid < sh.N_group / 2;
     p.b_valid = tail ? btail->valid : 0u;

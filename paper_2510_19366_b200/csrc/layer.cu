@@ -690,10 +690,27 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         ck_launch("bucket");
         tm.end(1, 2);
     }
+    // Small batches (<= 16 rows per sub-expert on average): the 1-SM gemm1
+    // gathers its A rows from x itself (TMA gather4, one per 4 rows and
+    // k-block) and dispatch writes only the permutation tables -- no x_perm.
+    // Large batches materialise x_perm: gather4 moves ~5 B/cycle per SM, so a
+    // gathered 128-row A operand left gemm1 2.2-2.7x slower at 4096 Mixtral
+    // tokens (profiles/r02g_gather_ab.txt); decode batches gain 2-3%.
+    static const int gather_env = [] {  // MOEPRISM_GATHER=0 never / 1 always (A/B)
+        const char* e = std::getenv("MOEPRISM_GATHER");
+        return e ? std::atoi(e) : -1;
+    }();
+    const bool gather_shape = gather_env == 1 ||
+                              (gather_env < 0 && (size_t)T * (kscalar ? kscalar : L->k_max) <= (size_t)16 * L->G);
+    const bool gather = gather_shape && L->use_tc && !L->tile256 && (L->d % 8) == 0 &&
+                        (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+    CUtensorMap tmXg;
+    if (gather && !mp::make_tmap_bf16_2d(&tmXg, x, T, L->d, 1, 64)) fail(MP_ERR_CUDA, "gather tensor map");
     tm.begin(2);
     if (L->offload) offload_step(L, s);  // transfers counted in the dispatch stage
-    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, L->x_perm, s, true,
-                        bucketed ? mp::route_tokens_per_block(T) : mp::kRouteTokensPerBlock);
+    // the fused routing kernel already flagged non-finite input rows (sum |x|)
+    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, gather ? nullptr : L->x_perm, s,
+                        !bucketed, bucketed ? mp::route_tokens_per_block(T) : mp::kRouteTokensPerBlock);
     ck_launch("dispatch");
     tm.end(2, 1);
     mp::GemmShape g1{L->G, L->d_pad, 2 * L->w_pad, T * L->k_max, L->w_pad, 2 * L->w_pad};
@@ -713,9 +730,10 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
                             L->ws.mprefix_tc2, L->num_sms, s, gmap);
     else if (L->use_tc)
-        mp::launch_gemm_tc(true, &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1, L->ws.offsets,
-                           L->ws.mprefix_tc, L->num_sms, s, gmap, nullptr, L->tm_xperm_s, nullptr,
-                           trim ? &L->w1_tail : nullptr);
+        mp::launch_gemm_tc(true, gather ? &tmXg : &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1,
+                           L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s, gmap, nullptr,
+                           gather ? nullptr : L->tm_xperm_s, nullptr, trim ? &L->w1_tail : nullptr,
+                           gather ? L->ws.perm_tok : nullptr);
     else
         mp::launch_gemm1_simt(L->dtype, L->x_perm, L->W1, L->h, g1, L->ws.offsets, L->ws.mprefix_simt, s);
     ck_launch("gemm1");

@@ -168,6 +168,9 @@ void launch_gemm2_simt(int dtype, const void* Hm, const void* W2, void* O, const
 // gmap (nullable): group g's weights are B group gmap[g] (offload cache slots)
 // starts (nullable): group g's rows are [starts[g], offsets[g+1])
 // tmA_small (nullable): [3] maps of A with 16 / 32 / 64-row boxes (short tiles load only their rows)
+// gather_tok (nullable, SwiGLU epilogue): A rows gathered from the token
+//   matrix by TMA gather4 (tmA = map of x with {64, 1} boxes), token id of
+//   permuted row r = gather_tok[r]; no x_perm
 // tmO (nullable, plain epilogue): map of the output with 32 x 32 boxes, no swizzle
 //   (make_tmap_bf16_2d_ex): full 32-row warp slabs leave through TMA stores
 // gemm1 B tail: the packed W1 rows past `valid` neurons per group (padding to
@@ -181,7 +184,7 @@ void launch_gemm_tc(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB,
                     const uint32_t* offsets, const uint32_t* mprefix, int num_sms, cudaStream_t s,
                     const uint32_t* gmap = nullptr, const uint32_t* starts = nullptr,
                     const CUtensorMap* tmA_small = nullptr, const CUtensorMap* tmO = nullptr,
-                    const GemmBTail* btail = nullptr);
+                    const GemmBTail* btail = nullptr, const uint32_t* gather_tok = nullptr);
 size_t gemm_tc_smem_bytes();
 // Epilogue modes of the 1-SM tensor-core GEMM (gemm_tc.cu).
 constexpr int kEpiPlain = 0;   // bf16 acc
@@ -195,7 +198,7 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
                         uint32_t b_row0 = 0, const int32_t* colmap = nullptr, const uint32_t* gmap = nullptr,
                         const uint32_t* starts = nullptr, uint32_t ksplit = 1,
                         const CUtensorMap* tmA_small = nullptr, const CUtensorMap* tmO = nullptr,
-                        const GemmBTail* btail = nullptr);
+                        const GemmBTail* btail = nullptr, const uint32_t* gather_tok = nullptr);
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
 // CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)

@@ -598,6 +598,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     double guard = 0.0;
     if (t < T) {
         const double xn = warp_row_abs_sum(x + (size_t)t * d, d);  // certification bound input
+        if (!isfinite(xn) && lane == 0 && err) atomicOr(err, 2);    // the reference's check_input
         // fixed-order sum over the K splits; all NC loads of a split in flight
         // (the partials come from L2 / HBM: a load per candidate in turn left
         // this phase latency-bound, 7 us for 240 candidates)
