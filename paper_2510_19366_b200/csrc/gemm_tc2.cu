@@ -17,8 +17,22 @@
 //     n*256 + 128 r .. +127 (accumulator columns [128 r, 128 r + 128)).
 //   gemm2: B tile = W2 rows n*256 .. +255 = output columns; CTA r loads its half.
 // Tiles are (g, n, m) with 256-row m tiles (prefix of ceil(count_g / 256)),
-// m fastest, strided over the clusters of a persistent grid.  Rows past the
-// group end are computed and discarded (masked stores).
+// m fastest, strided over the clusters of a persistent grid.
+//
+// Remainder tiles (round 2) run with SWAPPED operands: a group's last tile of
+// r < 256 rows computes D^T = W_tile . X_r^T as an M=256 (weight rows) x
+// N=Nt (tokens, Nt = r rounded up to 32) pair MMA.  The weight tile becomes
+// the A operand (each CTA's own 128 rows, read only by its own tensor core)
+// and the r token rows the B operand (Nt/2 per CTA, loaded through 16 / 32 /
+// 64-row TMA boxes).  Per CTA and 64-deep k-block a plain remainder tile moves
+// 32 KB into shared memory and 48 KB out of it (its B half is read by both
+// tensor cores) whatever r is; the swapped one moves 16 KB + 64 Nt in and
+// 16 KB + 128 Nt out (0.47 of that at Nt = 32), and its MMAs cost ~N/2
+// cycles.  The accumulator then holds weight rows in TMEM lanes and tokens
+// in columns: the epilogue transposes 32 x 32 blocks through shared memory
+// (16-byte row stores), and for gemm1 the up rows (lanes 64..127 of a CTA in
+// the [64 gate | 64 up] layout) cross to the gate warps through shared
+// memory before SiLU(gate) * up.
 //
 // Remainder schedules measured and dropped (round 1):
 // M=128 tail tiles (a tail tile costs the same ~580 cycles per k-block as a
@@ -80,7 +94,11 @@ constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t kEpiWarps = MP_PAIR_EPI_WARPS;
 constexpr uint32_t kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
-constexpr size_t kSmemBytes = 1024 + NSP * STAGE_BYTES + 256;
+constexpr uint32_t kXchBytes = 64 * 33 * 4;         // gemm1 swapped tiles: up rows -> gate warps (fp32, padded)
+constexpr uint32_t kStgBytes = 4 * 2 * 32 * 32 * 2;  // per epilogue warp: two 32 x 32 bf16 blocks (TMA-store
+                                                    // staging, double-buffered; swapped tiles' transposes)
+constexpr size_t kSmemBytes = 1024 + NSP * STAGE_BYTES + 256 + kXchBytes + kStgBytes;
+static_assert(kEpiWarps == 4, "the swapped-tail epilogue pairs lane quarters 0/1 with 2/3 (4 epilogue warps)");
 
 struct PairParams {
     uint32_t G, K, N_group, n_valid, ld_out, NT;
@@ -89,7 +107,32 @@ struct PairParams {
     __nv_bfloat16* out;
     uint64_t* trace;  // [grid][4] MMA-issuer timing of the leaders (diagnostics) or null
     const uint32_t* gmap;  // nullable: B group of group g (sub-expert offload cache slot), else g
+    uint32_t swap_tail;    // remainder tiles with swapped operands (needs the short A maps)
+    uint32_t tma_out;      // plain epilogue: tmO valid (whole 32-row warp slabs leave through TMA stores)
 };
+
+// remainder tile: rows r < 256 of the group's last m tile; Nt = tokens per
+// swapped MMA (r rounded up to 32 -> each CTA loads Nt / 2, a multiple of 16)
+MP_DEV uint32_t swap_cols(uint32_t swap, uint32_t cnt, uint32_t m) {
+    const uint32_t r = cnt - m * BM;
+    return (swap && r < BM) ? ((r + 31u) & ~31u) : 0u;
+}
+// Tile order: round i hands tiles i*npairs .. +npairs-1 to the pairs, walked
+// in reverse on odd rounds, so a pair alternates its position inside the
+// (g, n) blocks of [full..., remainder] tiles instead of always drawing the
+// same kind (with 2-tile blocks and an even pair count, plain striding gave
+// half the pairs every full tile and the other half every remainder).
+MP_DEV uint32_t tile_at(uint32_t i, uint32_t pair, uint32_t npairs) {
+    return i * npairs + ((i & 1u) ? npairs - 1u - pair : pair);
+}
+// Independent accumulator chains of a swapped tile: MMAs into one accumulator
+// serialise on it (~91+ cycles each whatever N is, tests/probes/mma_cost.cu;
+// the per-tile trace put Nt = 32 swapped tiles at the full tile's ~610 cycles
+// per k-block with one chain), so narrow tiles spread their k-steps
+// round-robin over 256 / Nt (<= 4) accumulators in the tile's TMEM buffer and
+// the epilogue sums them in chain order.
+MP_DEV uint32_t swap_chains(uint32_t nt) { return nt <= 64 ? 4u : nt <= 128 ? 2u : 1u; }
+MP_DEV void named_bar(uint32_t id, uint32_t n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 MP_DEV uint32_t cluster_rank() {
     uint32_t r;
@@ -186,7 +229,10 @@ __device__ __forceinline__ void map_tile(uint32_t tile, const uint32_t* s_prefix
 
 template <bool SWIGLU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, PairParams p) {
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmA16, const __grid_constant__ CUtensorMap tmA32,
+                     const __grid_constant__ CUtensorMap tmA64, const __grid_constant__ CUtensorMap tmO,
+                     PairParams p) {
     constexpr uint32_t NS = NSP;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint32_t s_prefix[kMaxG + 1];
@@ -201,6 +247,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + NS;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* xch = reinterpret_cast<float*>(base + NS * STAGE_BYTES + 256);
+    uint16_t* stg_all = reinterpret_cast<uint16_t*>(base + NS * STAGE_BYTES + 256 + kXchBytes);
 
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
@@ -221,6 +269,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        if (p.tma_out) tma_prefetch_desc(&tmO);
+        if (p.swap_tail) {
+            tma_prefetch_desc(&tmA16);
+            tma_prefetch_desc(&tmA32);
+            tma_prefetch_desc(&tmA64);
+        }
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot);
     griddep_wait();  // group metadata comes from the routing epilogue
@@ -236,6 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t total = s_prefix[p.G] * p.NT;
+    const uint32_t rounds = (total + npairs - 1) / npairs;
     const uint32_t nkb = p.K / BK;
 
     if (warp == 0) {
@@ -247,25 +302,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             (void)pol_b;
 #endif
             uint32_t it = 0;
-            for (uint32_t tile = pair; tile < total; tile += npairs) {
+            for (uint32_t i = 0; i < rounds; ++i) {
+                const uint32_t tile = tile_at(i, pair, npairs);
+                if (tile >= total) continue;
                 uint32_t g, m, n;
                 map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
-                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * HM);
+                const uint32_t nt = swap_cols(p.swap_tail, s_off[g + 1] - s_off[g], m);
+                const uint32_t half = nt / 2;  // swapped: token rows per CTA
+                const int32_t arow = static_cast<int32_t>(s_off[g] + m * BM + rank * (nt ? half : HM));
                 const int32_t brow = static_cast<int32_t>(s_gmap[g] * p.N_group + n * BN + rank * 128);
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
-                    if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+                    if (rank == 0) mbar_expect_tx(&full[s], 2 * (B_BYTES + (nt ? half * 128u : A_BYTES)));
                     const uint32_t fb = full_leader + s * 8;
+                    const int32_t kc = static_cast<int32_t>(kb * BK);
+                    if (nt && half < HM) {
+                        // token rows through 64 / 32 / 16-row boxes (half is a multiple of 16)
+                        uint32_t done = 0;
+                        if (half & 64u) {
+                            tma_load_2d_pair(sA + s * A_BYTES, &tmA64, fb, kc, arow);
+                            done = 64;
+                        }
+                        if (half & 32u) {
+                            tma_load_2d_pair(sA + s * A_BYTES + done * 128u, &tmA32, fb, kc, arow + (int32_t)done);
+                            done += 32;
+                        }
+                        if (half & 16u)
+                            tma_load_2d_pair(sA + s * A_BYTES + done * 128u, &tmA16, fb, kc, arow + (int32_t)done);
+                    } else {
 #if MP_PAIR_HINTS & 2
-                    tma_load_2d_pair_hint(sA + s * A_BYTES, &tmA, fb, static_cast<int32_t>(kb * BK), arow, pol_a);
+                        tma_load_2d_pair_hint(sA + s * A_BYTES, &tmA, fb, kc, arow, pol_a);
 #else
-                    tma_load_2d_pair(sA + s * A_BYTES, &tmA, fb, static_cast<int32_t>(kb * BK), arow);
+                        tma_load_2d_pair(sA + s * A_BYTES, &tmA, fb, kc, arow);
 #endif
+                    }
 #if MP_PAIR_HINTS & 1
-                    tma_load_2d_pair_hint(sB + s * B_BYTES, &tmB, fb, static_cast<int32_t>(kb * BK), brow, pol_b);
+                    tma_load_2d_pair_hint(sB + s * B_BYTES, &tmB, fb, kc, brow, pol_b);
 #else
-                    tma_load_2d_pair(sB + s * B_BYTES, &tmB, fb, static_cast<int32_t>(kb * BK), brow);
+                    tma_load_2d_pair(sB + s * B_BYTES, &tmB, fb, kc, brow);
 #endif
                 }
             }
@@ -278,7 +353,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t t_start = clock64();
             uint64_t w_acc = 0, w_full = 0;
 #endif
-            for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
+            for (uint32_t i = 0; i < rounds; ++i) {
+                const uint32_t tile = tile_at(i, pair, npairs);
+                if (tile >= total) continue;
                 const uint32_t acc = tc & 1u;
 #if MP_PAIR_TRACE
                 uint64_t t0 = clock64();
@@ -291,6 +368,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
+                uint32_t g, m, n;
+                map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
+                const uint32_t nt = swap_cols(p.swap_tail, s_off[g + 1] - s_off[g], m);
+                const uint32_t id = nt ? umma_idesc_bf16(BM, nt) : idesc;
+                const uint32_t chains = swap_chains(nt);
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
 #if MP_PAIR_TRACE
@@ -301,12 +383,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     w_full += clock64() - t0;
 #endif
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(sA + s * A_BYTES);
-                    const uint32_t b0 = smem_u32(sB + s * B_BYTES);
+                    // swapped remainder: the weight tile is the A operand, the tokens B
+                    const uint32_t a0 = smem_u32(nt ? sB + s * B_BYTES : sA + s * A_BYTES);
+                    const uint32_t b0 = smem_u32(nt ? sA + s * A_BYTES : sB + s * B_BYTES);
+                    if (nt) {
 #pragma unroll
-                    for (uint32_t k = 0; k < BK / 16; ++k)
-                        umma_bf16_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                                       (kb | k) != 0u);
+                        for (uint32_t k = 0; k < BK / 16; ++k) {
+                            const uint32_t j = kb * (BK / 16) + k, a = j % chains;
+                            umma_bf16_pair(d_tmem + a * nt, umma_desc_sw128(a0 + k * 32),
+                                           umma_desc_sw128(b0 + k * 32), id, j >= chains ? 1u : 0u);
+                        }
+                    } else {
+#pragma unroll
+                        for (uint32_t k = 0; k < BK / 16; ++k)
+                            umma_bf16_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), id,
+                                           (kb | k) != 0u);
+                    }
                     umma_commit_pair(&empty[s]);
                 }
                 umma_commit_pair(&tfull[acc]);
@@ -316,9 +408,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     r[0] = tile;
                     r[1] = w_full - wf0;
                     r[2] = clock64() - t_tile;
-                    r[3] = 0;
+                    r[3] = nt;  // 0 full tile, else the swapped remainder's token columns
                 }
 #endif
+                ++tc;
             }
 #if MP_PAIR_TRACE
             if (p.trace) {
@@ -335,6 +428,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
         const uint32_t part = (warp - 2) / 4, nparts = kEpiWarps / 4;  // column share of this warp
         const uint32_t tempty_leader = mapa(&tempty[0], 0);
+        uint16_t* stg = stg_all + (warp - 2) * 2048;  // this warp's two 32 x 32 bf16 staging blocks
+        uint32_t epi_it = 0;                          // TMA-store chunks issued by this warp
         // One accumulator to bf16 rows of the group: lane = row rank*128 +
         // q*32 + lane, all 256 D columns.
         auto emit = [&](uint32_t buf, uint32_t row0, uint32_t g, uint32_t n, uint32_t cnt) {
@@ -371,13 +466,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 }
             } else {
+                // A warp whose 32 rows are all valid stages each 32 x 32 chunk
+                // in shared memory and writes it with one TMA store (whole
+                // 64-byte row segments; short-K GEMMs such as Qwen's K = 384
+                // down projection are epilogue-bound); ragged slabs store directly.
+                const bool slab = p.tma_out && row0 + rank * HM + q * 32 + 32 <= cnt;
+                const int32_t slab_row = static_cast<int32_t>(s_off[g] + row0 + rank * HM + q * 32);
                 auto store = [&](uint32_t c, const uint32_t* r) {
                     const uint32_t col = n * BN + c * 32;
-                    if (valid && col < p.n_valid) {
-                        uint32_t pk[16];
+                    if (col >= p.n_valid) return;
+                    uint32_t pk[16];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+                    for (int i = 0; i < 16; ++i)
+                        pk[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+                    if (slab) {
+                        uint16_t* buf = stg + (epi_it & 1u) * 1024;
+                        if (epi_it >= 2) {  // the store issued from this buffer two chunks ago has read it
+                            if (lane == 0) bulk_wait_read<1>();
+                            __syncwarp();
+                        }
+                        uint4* dst = reinterpret_cast<uint4*>(buf + lane * 32);
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) dst[v] = make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmO, buf, static_cast<int32_t>(col), slab_row);
+                            bulk_commit();
+                        }
+                        ++epi_it;
+                    } else if (valid) {
                         __nv_bfloat16* dst = orow + col;
 #pragma unroll
                         for (int v = 0; v < 4; ++v)
@@ -401,6 +519,76 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
         };
+        // Swapped remainder tile: TMEM lane = weight row (CTA rank's 128 of the
+        // 256-row N tile), column j = token row0 + j (j < nt).  32 x 32 blocks
+        // go through a per-warp transpose buffer and leave as 16-byte row
+        // segments (4 per thread per block).
+        auto put_block = [&](uint32_t row0, uint32_t g, uint32_t cnt, uint32_t c, uint32_t col0, bool col_ok) {
+            __syncwarp();
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) {
+                const uint32_t idx = i * 32 + lane, j = idx >> 2, seg = idx & 3u;
+                const uint32_t row = row0 + c * 32 + j;
+                const uint4 v = *reinterpret_cast<const uint4*>(stg + j * 32 + seg * 8);
+                if (row < cnt && col_ok)
+                    st_global_v4(p.out + static_cast<size_t>(s_off[g] + row) * p.ld_out + col0 + seg * 8, v);
+            }
+            __syncwarp();
+        };
+        auto emit_swapped = [&](uint32_t buf, uint32_t row0, uint32_t g, uint32_t n, uint32_t cnt, uint32_t nt) {
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + buf * BN;
+            if (epi_it) {  // staged TMA stores of earlier tiles have read the buffer
+                if (lane == 0) bulk_wait_read<0>();
+                __syncwarp();
+            }
+            const uint32_t nch = nt / 32, chains = swap_chains(nt);
+            uint32_t r[32];
+            // chunk c of the tile, the accumulator chains summed in chain order
+            auto load_chunk = [&](uint32_t c) {
+                tmem_ld32(taddr + c * 32, r);
+                tmem_ld_wait();
+#pragma unroll 1
+                for (uint32_t a = 1; a < chains; ++a) {
+                    uint32_t t[32];
+                    tmem_ld32(taddr + a * nt + c * 32, t);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(t[j]));
+                }
+            };
+            if constexpr (SWIGLU) {
+                // lanes 0..63 gate, 64..127 up of neurons n*128 + rank*64 + 0..63
+                float* xrow = xch + ((q & 1u) * 32 + lane) * 33;
+#pragma unroll 1
+                for (uint32_t c = 0; c < nch; ++c) {
+                    load_chunk(c);
+                    if (q >= 2) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) xrow[j] = __uint_as_float(r[j]);
+                    }
+                    named_bar(1, 128);
+                    if (q < 2) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float hv = silu_f32(__uint_as_float(r[j])) * xrow[j];
+                            stg[j * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(hv));
+                        }
+                        put_block(row0, g, cnt, c, n * 128 + rank * 64 + q * 32, true);
+                    }
+                    named_bar(2, 128);
+                }
+            } else {
+                const uint32_t col0 = n * BN + rank * HM + q * 32;
+#pragma unroll 1
+                for (uint32_t c = 0; c < nch; ++c) {
+                    load_chunk(c);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        stg[j * 32 + lane] = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(r[j])));
+                    put_block(row0, g, cnt, c, col0, col0 < p.n_valid);
+                }
+            }
+        };
         auto release = [&](uint32_t buf) {
             tc_fence_before();
             __syncwarp();
@@ -410,7 +598,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #if MP_PAIR_TRACE
         uint64_t e_busy = 0, e_ext = 0, e_wait = 0;
 #endif
-        for (uint32_t tile = pair; tile < total; tile += npairs, ++tc) {
+        for (uint32_t i = 0; i < rounds; ++i) {
+            const uint32_t tile = tile_at(i, pair, npairs);
+            if (tile >= total) continue;
             uint32_t g, m, n;
             map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
             const uint32_t acc = tc & 1u;
@@ -423,11 +613,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t e1 = clock64();
             e_wait += e1 - e0;
 #endif
-            emit(acc, m * BM, g, n, s_off[g + 1] - s_off[g]);
+            const uint32_t cnt = s_off[g + 1] - s_off[g];
+            const uint32_t nt = swap_cols(p.swap_tail, cnt, m);
+            if (nt)
+                emit_swapped(acc, m * BM, g, n, cnt, nt);
+            else
+                emit(acc, m * BM, g, n, cnt);
             release(acc);
 #if MP_PAIR_TRACE
             e_busy += clock64() - e1;
 #endif
+            ++tc;
         }
 #if MP_PAIR_TRACE
         if (p.trace && warp == 2 && lane == 0) {  // epilogue timing of one warp per CTA
@@ -438,6 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tr[3] = tc;
         }
 #endif
+        if (epi_it && lane == 0) bulk_wait0();  // the TMA stores are complete before the CTA retires
     }
     tc_fence_before();
     __syncthreads();
@@ -452,13 +649,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 size_t gemm_pair_smem_bytes() { return kSmemBytes; }
 
+bool pair_swap_enabled() {
+    static const bool on = [] {  // MOEPRISM_PAIR_SWAP=0: plain 256-row remainder tiles (A/B)
+        const char* e = std::getenv("MOEPRISM_PAIR_SWAP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // tmB: box of 128 rows (each CTA loads half of the 256-row B tile); mprefix256:
-// prefix of ceil(count_g / 256) over the groups.
+// prefix of ceil(count_g / 256) over the groups; tmA_small (nullable): [3]
+// maps of A with 16 / 32 / 64-row boxes -- remainder tiles run swapped.
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
-                     const uint32_t* gmap) {
+                     const uint32_t* gmap, const CUtensorMap* tmA_small, const CUtensorMap* tmO) {
+    const bool swap = tmA_small != nullptr && pair_swap_enabled();
     PairParams p{sh.G, sh.K, sh.N_group, sh.n_valid, sh.ld_out, (sh.N_group + BN - 1) / BN, offsets, mprefix256,
-                 static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), gmap};
+                 static_cast<__nv_bfloat16*>(out), gemm_trace_buffer(swiglu), gmap, swap ? 1u : 0u,
+                 (!swiglu && tmO) ? 1u : 0u};
+    const CUtensorMap* o_map = p.tma_out ? tmO : tmA;
+    const CUtensorMap* s16 = swap ? &tmA_small[0] : tmA;
+    const CUtensorMap* s32 = swap ? &tmA_small[1] : tmA;
+    const CUtensorMap* s64 = swap ? &tmA_small[2] : tmA;
     if (p.trace) cudaMemsetAsync(p.trace, 0, (4096 + 128 * 128 * 4) * sizeof(uint64_t), s);
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
     uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;
@@ -468,9 +680,9 @@ void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB
     func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<false>), (int)kSmemBytes);
     const dim3 grid(2 * pairs), block(kThreads);
     if (swiglu)
-        launch_k(gemm_pair_kernel<true>, grid, block, kSmemBytes, s, *tmA, *tmB, p);
+        launch_k(gemm_pair_kernel<true>, grid, block, kSmemBytes, s, *tmA, *tmB, *s16, *s32, *s64, *o_map, p);
     else
-        launch_k(gemm_pair_kernel<false>, grid, block, kSmemBytes, s, *tmA, *tmB, p);
+        launch_k(gemm_pair_kernel<false>, grid, block, kSmemBytes, s, *tmA, *tmB, *s16, *s32, *s64, *o_map, p);
 }
 
 }  // namespace mp

@@ -180,7 +180,8 @@ struct mp_layer_s {
     int num_sms = 0;
     bool use_tc = false;
     // grouped-GEMM kernel: 0 auto (CTA pairs, gemm_tc2, or 1-SM 128-row tiles,
-    // gemm_tc, by expected padding); MOEPRISM_TC_TILE=128|256 forces
+    // gemm_tc, by rows per sub-expert); 1 1-SM, 2 pairs, 3 pairs with plain
+    // (unswapped) remainder tiles; MOEPRISM_TC_TILE=128|256|256-plain forces
     int tile_mode = 0;
     bool tile256 = false;  // this forward's choice
     bool has_experts = true, has_router = true;  // MP_LAYER_* role flags
@@ -665,23 +666,34 @@ void prefetch_routed_weights(mp_layer_s* L, uint32_t T, cudaStream_t s) {
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
                  cudaStream_t s, StageTimer& tm, bool check_finite = false, bool with_shared = false,
                  uint32_t kscalar = 0, bool bucketed = false) {
-    // CTA-pair tiles pay up to 255 wasted rows per (sub-expert, N tile) against
-    // 127 for 128-row tiles.  Auto choice: the kernel with fewer padded rows
-    // per bucket (expected over bucket sizes M +- sqrt(M), M = T k / G), CTA
-    // pairs credited 5% for their lower operand traffic (tests/probes/
-    // tile_ab.py: 128-row tiles win at k <= 8 at the Mixtral shape, pairs at
-    // k = 16 and the 32k-token mixed batch).  Per-token k: k_max.
+    // Kernel choice (auto).  With swapped remainder tiles (gemm_tc2.cu) CTA
+    // pairs pad a group's last tile to 32 rows of MMA work; in-process A/B
+    // (tests/probes/tile_ab_k.py, profiles/r02l_tile_ab_k2.txt) puts them
+    // 5-10% ahead of the 1-SM 128-row tiles at the Mixtral shape for
+    // k = 3..16 (tie at k = 5), 10% behind at k = 2 (128 rows per sub-expert:
+    // HBM-bound, every tile a remainder) and level at Qwen prefill: pairs from
+    // 160 rows per sub-expert.  Without the swapped remainders (A/B) the
+    // round-1 rule: the kernel with fewer padded rows per bucket (expected over
+    // bucket sizes M +- sqrt(M), M = T k / G), pairs credited 5%.  Per-token k:
+    // k_max.
     {
         const double rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
-        const double sd = std::sqrt(rows > 1.0 ? rows : 1.0);
-        double pad128 = 0.0, pad256 = 0.0;
-        for (double m : {rows - sd, rows, rows + sd}) {
-            const double mm = m < 1.0 ? 1.0 : m;
-            pad128 += std::ceil(mm / 128.0) * 128.0;
-            pad256 += std::ceil(mm / 256.0) * 256.0;
+        static const double pair_min = [] {  // MOEPRISM_PAIR_MIN_ROWS (A/B)
+            const char* e = std::getenv("MOEPRISM_PAIR_MIN_ROWS");
+            return e ? std::atof(e) : 160.0;
+        }();
+        bool use_pairs = rows >= pair_min;
+        if (!mp::pair_swap_enabled()) {
+            const double sd = std::sqrt(rows > 1.0 ? rows : 1.0);
+            double pad128 = 0.0, pad256 = 0.0;
+            for (double m : {rows - sd, rows, rows + sd}) {
+                const double mm = m < 1.0 ? 1.0 : m;
+                pad128 += std::ceil(mm / 128.0) * 128.0;
+                pad256 += std::ceil(mm / 256.0) * 256.0;
+            }
+            use_pairs = rows >= 192.0 && pad256 / 1.05 < pad128;
         }
-        const bool pairs_win = pad256 / 1.05 < pad128;
-        L->tile256 = L->tile_mode == 2 || (L->tile_mode == 0 && rows >= 192.0 && pairs_win);
+        L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && use_pairs);
     }
     if (!bucketed) {
         tm.begin(1);
@@ -728,7 +740,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
                       (size_t)T * (kscalar ? kscalar : L->k_max) <= (size_t)64 * L->G;
     if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(true, &L->tm_xperm, L->offload ? &L->tm_w1ch : &L->tm_w1h, L->h, g1, L->ws.offsets,
-                            L->ws.mprefix_tc2, L->num_sms, s, gmap);
+                            L->ws.mprefix_tc2, L->num_sms, s, gmap, L->tile_mode == 3 ? nullptr : L->tm_xperm_s);
     else if (L->use_tc)
         mp::launch_gemm_tc(true, gather ? &tmXg : &L->tm_xperm, L->offload ? &L->tm_w1c : &L->tm_w1, L->h, g1,
                            L->ws.offsets, L->ws.mprefix_tc, L->num_sms, s, gmap, nullptr,
@@ -742,7 +754,8 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     tm.begin(4);
     if (L->use_tc && L->tile256)
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
-                            L->ws.mprefix_tc2, L->num_sms, s, gmap);
+                            L->ws.mprefix_tc2, L->num_sms, s, gmap, L->tile_mode == 3 ? nullptr : L->tm_h_s,
+                            &L->tm_o);
     else if (L->use_tc)
         mp::launch_gemm_tc(false, &L->tm_h, L->offload ? &L->tm_w2c : trim ? &L->tm_w2d : &L->tm_w2, L->o, g2,
                            L->ws.offsets,
@@ -940,7 +953,10 @@ MP_API mp_status mp_layer_create(const mp_layer_desc* desc, mp_layer_t* out) {
             if (const char* env = std::getenv("MOEPRISM_BF16_GEMM"))
                 if (std::string(env) == "simt") L->use_tc = false;  // diagnostics only
             if (const char* env = std::getenv("MOEPRISM_TC_TILE"))
-                L->tile_mode = std::string(env) == "256" ? 2 : std::string(env) == "128" ? 1 : 0;
+                L->tile_mode = std::string(env) == "256"         ? 2
+                               : std::string(env) == "128"       ? 1
+                               : std::string(env) == "256-plain" ? 3
+                                                                 : 0;
             const uint32_t w_sub = (L->ff + L->S - 1) / L->S;
             L->w_pad = round_up(w_sub, 128);
             L->w_sub = w_sub;
@@ -1684,7 +1700,7 @@ MP_API mp_status mp_debug_gemm_trace(int which, uint64_t* out, uint32_t n_ctas) 
 // merged and wide remainders) are described in gemm_tc2.cu and DESIGN.md.
 MP_API mp_status mp_debug_set_tile_mode(mp_layer_t L, int mode) {
     return guarded([&] {
-        if (!L || mode < 0 || mode > 2) fail(MP_ERR_VALIDATION, "bad argument");
+        if (!L || mode < 0 || mode > 3) fail(MP_ERR_VALIDATION, "bad argument");
         L->tile_mode = mode;
     });
 }

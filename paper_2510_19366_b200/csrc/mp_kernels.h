@@ -201,10 +201,15 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
                         const GemmBTail* btail = nullptr, const uint32_t* gather_tok = nullptr);
 uint64_t* gemm_trace_buffer(bool swiglu);
 uint64_t* gemm_trace_ptr(int which);
-// CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu)
+// CTA-pair (cta_group::2) 256 x 256 tiles; tmB box of 128 rows (gemm_tc2.cu);
+// tmA_small (nullable): [3] maps of A with 16 / 32 / 64-row boxes -> remainder
+// tiles run with swapped operands; tmO (nullable, plain epilogue): 32 x 32-box
+// map of the output (whole warp slabs leave through TMA stores)
+bool pair_swap_enabled();  // MOEPRISM_PAIR_SWAP (default on)
 void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB, void* out, const GemmShape& sh,
                      const uint32_t* offsets, const uint32_t* mprefix256, int num_sms, cudaStream_t s,
-                     const uint32_t* gmap = nullptr);
+                     const uint32_t* gmap = nullptr, const CUtensorMap* tmA_small = nullptr,
+                     const CUtensorMap* tmO = nullptr);
 
 // Calibration (calib.cu).
 void launch_binarize_topk(const float* act, uint32_t rows, uint32_t cols, uint32_t k_a, uint8_t* bits,

@@ -139,6 +139,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     }
 }
 
+// CTA-pair M=256 with N in {32..256} and 1/2/4 accumulator chains (swapped
+// remainder tiles of gemm_tc2.cu): cycles per MMA, operands resident in smem
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+    mma_cost_pair_n_kernel(uint32_t n, uint32_t chains, uint32_t iters, uint64_t* out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = base;
+    uint8_t* sB = base + 16384;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_slot;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    for (uint32_t i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t*>(base)[i] = 0x3f803f80u;
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    if (threadIdx.x == 0 && rank == 0) {
+        const uint32_t idesc = umma_idesc_bf16(256, n);
+        const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+        uint64_t t0 = clock64();
+        uint32_t j = 0;
+        for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k, ++j) {
+                const uint32_t d = tmem + (j % chains) * n;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                    "l"(umma_desc_sw128(a0 + k * 32)), "l"(umma_desc_sw128(b0 + k * 32)), "r"(idesc), "r"(1u)
+                    : "memory");
+            }
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                smem_u32(&bar)),
+            "h"(static_cast<uint16_t>(1))
+            : "memory");
+        mbar_wait(&bar, 0);
+        out[blockIdx.x] = clock64() - t0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (threadIdx.x < 32) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    }
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -190,6 +252,22 @@ int main() {
                        mean / (double(iters / 28 * 28) * 4));
             else
                 printf("%u,%u,%.1f,%.1f\n", m, two + 1, mean / (double(iters) * 4), m * 256.0 / 512);
+        }
+    cudaFuncSetAttribute(mma_cost_pair_n_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    printf("pair M=256: N,chains,cycles_per_mma,floor_N_over_2\n");
+    for (uint32_t chains : {1u, 2u, 4u})
+        for (uint32_t n : {32u, 64u, 128u, 256u}) {
+            if (chains * n > 512) continue;
+            cudaMemset(d_out, 0, sms * 8);
+            mma_cost_pair_n_kernel<<<sms, 128, smem>>>(n, chains, iters, d_out);
+            if (cudaDeviceSynchronize() != cudaSuccess) return 1;
+            std::vector<uint64_t> h(sms);
+            cudaMemcpy(h.data(), d_out, sms * 8, cudaMemcpyDeviceToHost);
+            double mean = 0;
+            int c = 0;
+            for (auto v : h)
+                if (v) mean += v, ++c;
+            printf("%u,%u,%.1f,%.1f\n", n, chains, mean / c / (double(iters) * 4), n / 2.0);
         }
     return 0;
 }

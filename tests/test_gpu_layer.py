@@ -501,11 +501,12 @@ def test_forward_is_cuda_graph_capturable(oracle, torch_cuda):
     L.close()
 
 
-@pytest.mark.parametrize("k", [4, 8])
+@pytest.mark.parametrize("k", [2, 4, 8])
 def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
-    """Both GEMM kernels (1-SM 128-row tiles, CTA-pair 256-row tiles) give the
-    same layer output; buckets with partial last tiles of both sizes occur at
-    these bucket sizes."""
+    """The three GEMM schedules (CTA pairs with swapped-operand remainder
+    tiles, CTA pairs with plain 256-row remainders, 1-SM 128-row tiles) give
+    the same layer output; buckets with partial last tiles of every size class
+    occur at these bucket sizes."""
     import ctypes as C
     torch = torch_cuda
     from paper_2510_19366_b200 import _lib
@@ -514,7 +515,7 @@ def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
     lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
     outs = {}
     try:
-        for mode in (2, 1):  # CTA pairs, 1-SM
+        for mode in (2, 3, 1):  # pairs + swapped tails, pairs plain, 1-SM
             _lib.check(lib.mp_debug_set_tile_mode(L.h, mode))
             y, sel, w, off = L.forward(x_dev, k=k, return_routing=True)
             torch.cuda.synchronize()
@@ -522,12 +523,41 @@ def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
     finally:
         _lib.check(lib.mp_debug_set_tile_mode(L.h, 0))
     cnt = np.diff(off.cpu().numpy().view(np.uint32).astype(np.int64))
-    assert ((cnt > 256) & (cnt % 256 > 0) & (cnt % 256 <= 128)).any()  # partial pair tiles of <= 128 rows
+    assert ((cnt % 256) > 0).any()  # remainder tiles
     assert ((cnt % 128) > 0).any()
-    ref = outs[2]
+    ref = outs[3]
     for mode, y in outs.items():
         ok = bf16_ok(y, ref)
         assert ok.all(), f"mode {mode}: {(~ok).sum()} elements off"
+
+
+@pytest.mark.parametrize("T", [1, 37, 300, 777])
+def test_pair_swapped_tails_ragged(oracle, torch_cuda, T):
+    """CTA pairs with swapped-operand remainder tiles on ragged buckets (every
+    remainder size class: < 32, 32..255 rows, exact multiples) against the
+    oracle: routing bit-exact, outputs within the bf16 tolerance."""
+    import ctypes as C
+    torch = torch_cuda
+    from paper_2510_19366_b200 import _lib
+    E, S, d, ff, K = 4, 4, 512, 1024, 8
+    experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T, seed_x=T)
+    L = make_layer(experts, parts, wr, S, "bf16", k_max=K, max_tokens=T)
+    lib = _lib.load()
+    lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
+    _lib.check(lib.mp_debug_set_tile_mode(L.h, 2))
+    xb = bf16_round(x)
+    y, sel, w, off = L.forward(torch.from_numpy(xb).cuda().to(torch.bfloat16), k=K, return_routing=True)
+    L.check_errors()
+    logits = oracle.router_logits(xb, wr, T, d, E * S)
+    osel, ow, gap = oracle.route(logits, K, K, 1)
+    bad, _ = routing_agreement(_u32(sel), osel, gap, np.full(T, K, np.uint32))
+    assert not bad
+    cnt = np.diff(off.cpu().numpy().view(np.uint32).astype(np.int64))
+    assert cnt.sum() == T * K
+    exs = [tuple(bf16_round(a) for a in e) for e in experts]
+    yo = oracle.layer_forward(exs, parts, S, xb, _u32(sel), w.cpu().numpy(), 1)
+    assert out_ok(y.float().cpu().numpy(), yo, "bf16").all()
+    L.close()
 
 
 def test_zero_tokens(oracle, torch_cuda, mixtral):
