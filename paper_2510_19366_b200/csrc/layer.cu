@@ -666,33 +666,34 @@ void prefetch_routed_weights(mp_layer_s* L, uint32_t T, cudaStream_t s) {
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
                  cudaStream_t s, StageTimer& tm, bool check_finite = false, bool with_shared = false,
                  uint32_t kscalar = 0, bool bucketed = false) {
-    // Kernel choice (auto).  With swapped remainder tiles (gemm_tc2.cu) CTA
-    // pairs pad a group's last tile to 32 rows of MMA work; in-process A/B
-    // (tests/probes/tile_ab_k.py, profiles/r02l_tile_ab_k2.txt) puts them
-    // 5-10% ahead of the 1-SM 128-row tiles at the Mixtral shape for
-    // k = 3..16 (tie at k = 5), 10% behind at k = 2 (128 rows per sub-expert:
-    // HBM-bound, every tile a remainder) and level at Qwen prefill: pairs from
-    // 160 rows per sub-expert.  Without the swapped remainders (A/B) the
-    // round-1 rule: the kernel with fewer padded rows per bucket (expected over
-    // bucket sizes M +- sqrt(M), M = T k / G), pairs credited 5%.  Per-token k:
-    // k_max.
+    // Kernel choice (auto): the kernel with the lower expected SM time per
+    // (sub-expert, 256-column N tile) over bucket sizes M +- sqrt(M), M = T k /
+    // G (per-token k: k_max).  A CTA-pair tile (256 rows; with swapped
+    // remainder tiles, gemm_tc2.cu, a remainder tile costs about a full one:
+    // profiles/r02k_pair_tile_trace.txt) holds 2 SMs for ~612 cycles per
+    // 64-deep k-block; a 1-SM 128-row tile one SM for ~800 (MMA at 684 plus
+    // operand waits).  In-process A/B (tests/probes/tile_ab_k.py,
+    // profiles/r02l_tile_ab_k2.txt): pairs 5-10% ahead at the Mixtral shape
+    // for k = 3, 4, 6..16, 1-SM tiles ahead at k = 2 (every tile a remainder)
+    // and at Qwen prefill k = 8 (273 rows: 2 pair tiles vs 3 1-SM tiles), a
+    // tie at k = 5 -- the cost model picks each of those.  Without the
+    // swapped remainders (A/B) the round-1 rule: pairs credited 5% on padded
+    // rows.
     {
         const double rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
-        static const double pair_min = [] {  // MOEPRISM_PAIR_MIN_ROWS (A/B)
-            const char* e = std::getenv("MOEPRISM_PAIR_MIN_ROWS");
-            return e ? std::atof(e) : 160.0;
-        }();
-        bool use_pairs = rows >= pair_min;
-        if (!mp::pair_swap_enabled()) {
-            const double sd = std::sqrt(rows > 1.0 ? rows : 1.0);
-            double pad128 = 0.0, pad256 = 0.0;
-            for (double m : {rows - sd, rows, rows + sd}) {
-                const double mm = m < 1.0 ? 1.0 : m;
-                pad128 += std::ceil(mm / 128.0) * 128.0;
-                pad256 += std::ceil(mm / 256.0) * 256.0;
-            }
-            use_pairs = rows >= 192.0 && pad256 / 1.05 < pad128;
+        const double sd = std::sqrt(rows > 1.0 ? rows : 1.0);
+        double pad128 = 0.0, pad256 = 0.0;
+        for (double m : {rows - sd, rows, rows + sd}) {
+            const double mm = m < 1.0 ? 1.0 : m;
+            pad128 += std::ceil(mm / 128.0);
+            pad256 += std::ceil(mm / 256.0);
         }
+        static const double pair_cost = [] {  // MOEPRISM_PAIR_COST: SM time of a pair tile / a 1-SM tile (A/B)
+            const char* e = std::getenv("MOEPRISM_PAIR_COST");
+            return e ? std::atof(e) : 1224.0 / 800.0;
+        }();
+        const bool use_pairs = mp::pair_swap_enabled() ? pad256 * pair_cost < pad128
+                                                       : (rows >= 192.0 && pad256 * 256.0 / 1.05 < pad128 * 128.0);
         L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && use_pairs);
     }
     if (!bucketed) {

@@ -568,14 +568,21 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
 #else
 #define MP_RT_STAMP()
 #endif
-    // tb tokens per CTA (warps >= tb only help with the CTA-wide phases):
-    // small batches use tb = 8 so the token work spreads over 4x the SMs
-    const uint32_t t0 = blockIdx.x * tb, t = warp < tb ? t0 + warp : T;
+    // tb tokens per block (warps >= tb only help with the CTA-wide phases):
+    // small batches use tb = 8 so the token work spreads over 4x the SMs.
+    // Grid-scan launches are persistent (grid <= SMs): a CTA takes token
+    // blocks blockIdx.x, + gridDim.x, ... (Qwen prefill: 256 blocks on 148
+    // SMs) so the grid barrier below stays deadlock-free.
+    const uint32_t nblk = (T + tb - 1) / tb;
     const uint32_t words = (G + 31) / 32;
-    for (uint32_t q = threadIdx.x; q < TB * words; q += blockDim.x) msk[q / words][q % words] = 0;
-    if (threadIdx.x == 0) n_pairs = 0;
     griddep_wait();
     griddep_launch();
+    for (uint32_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const bool first_blk = blk == blockIdx.x;
+    const uint32_t t0 = blk * tb, t = warp < tb ? t0 + warp : T;
+    for (uint32_t q = threadIdx.x; q < TB * words; q += blockDim.x) msk[q / words][q % words] = 0;
+    if (threadIdx.x == 0) n_pairs = 0;
+    __syncthreads();
     // many K splits (small batches: 64-deep router chunks) and few tokens per
     // CTA: the whole CTA sums the splits, one (token, sub-expert) per thread,
     // into the logit rows (replaces a separate partials_reduce launch; same
@@ -650,7 +657,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         }
     }
     __syncthreads();
-    MP_RT_STAMP();  // 1: top-k done
+    if (first_blk) MP_RT_STAMP();  // 1: top-k done
     // exact fp64 logits of every queued (token, candidate), 4 warps per pair
     // (d split in quarters, fixed-order combination: deterministic)
     const uint32_t np = min(n_pairs, kMaxPairs);
@@ -696,21 +703,24 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         }
     }
     __syncthreads();  // this CTA's selections are visible to the CTA
-    MP_RT_STAMP();    // 2: exact pass done
-    // (the selection masks / slots were written by the top-k emissions)
-    MP_RT_STAMP();  // 3: selection masks built
+    if (first_blk) {
+        MP_RT_STAMP();  // 2: exact pass done
+        // (the selection masks / slots were written by the top-k emissions)
+        MP_RT_STAMP();  // 3: selection masks built
+    }
     // warp per bucket, lane per token (tb <= 32): the stable rank of token tt
     // in bucket g is the number of earlier tokens of the CTA selecting g
     for (uint32_t g = warp; g < G; g += blockDim.x / 32) {
         const bool has = lane < tb && t0 + lane < T && ((msk[lane][g >> 5] >> (g & 31)) & 1u);
         const uint32_t bal = __ballot_sync(0xffffffffu, has);
         if (has) lrank[(size_t)(t0 + lane) * k_max + slot_of[lane][g]] = __popc(bal & ((1u << lane) - 1u));
-        if (lane == 0) block_counts[(size_t)blockIdx.x * G + g] = __popc(bal);
+        if (lane == 0) block_counts[(size_t)blk * G + g] = __popc(bal);
     }
     // this CTA's writes (selection, weights, ranks, counts) are ordered before
     // the ticket by the barrier + one gpu-scope fence of the ticket thread
     // (fences are cumulative over what the barrier made visible to it)
     __syncthreads();
+    }  // token blocks
     MP_RT_STAMP();  // 4: ranks done
     if (grid_scan) {
         // grid-wide barrier (the grid fits on the GPU at once: one 1024-thread
@@ -727,8 +737,11 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         }
         __syncthreads();
         MP_RT_STAMP();  // 5: barrier passed
-        bucket_bases_grid(gridDim.x, blockIdx.x, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt,
-                          mprefix_tc2);
+        for (uint32_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+            if (blk != blockIdx.x) __syncthreads();  // the previous block's scan scratch is free
+            bucket_bases_grid(nblk, blk, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt,
+                              mprefix_tc2);
+        }
         if (threadIdx.x == 0 && atomicAdd(ticket + 2, 1u) == gridDim.x - 1) {
             ticket[1] = 0;  // every CTA is past the barrier: reset for the next forward (stream-ordered)
             ticket[2] = 0;
@@ -1163,13 +1176,17 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
     // the routing arrays, or the last CTA's staged counts (1 byte per block and
     // bucket) when they are larger and fit
     const size_t nblk = (T + tb - 1) / tb;
-    // one 1024-thread CTA per SM: a grid that fits on the GPU at once can
-    // synchronise (grid barrier) and form its bucket bases in parallel
+    // one 1024-thread CTA per SM: a persistent grid of <= SMs CTAs (each
+    // taking every gridDim-th token block) is on the GPU at once, can
+    // synchronise (grid barrier) and form its bucket bases in parallel; the
+    // last-CTA scan (MOEPRISM_GRID_SCAN=0) took 23-28 us at Qwen prefill
+    // (256 blocks x 240 buckets, profiles/r02e_route_trace.txt)
     static const bool grid_env = [] {  // MOEPRISM_GRID_SCAN=0: last-CTA scans only (A/B)
         const char* e = std::getenv("MOEPRISM_GRID_SCAN");
         return !(e && e[0] == '0');
     }();
-    const bool grid_scan = grid_env && nblk <= static_cast<size_t>(num_sms);
+    const bool grid_scan = grid_env;
+    const size_t grid = grid_scan ? std::min<size_t>(nblk, static_cast<size_t>(num_sms)) : nblk;
     size_t smem = sizeof(double) * 2 * tb * G;
     if (nblk * G > smem && nblk * G <= 160 * 1024) smem = (nblk * G + 15) & ~size_t(15);
     auto launch = [&](auto kern) {
@@ -1177,7 +1194,7 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
         // reconfiguration between the kernels of the chain
         func_attr_once(reinterpret_cast<const void*>(kern), (int)std::max<size_t>(sizeof(double) * 2 * TB * kMaxG,
                                                                                   160 * 1024), true);
-        launch_k(kern, dim3((T + tb - 1) / tb), dim3(1024), smem, s,
+        launch_k(kern, dim3(static_cast<uint32_t>(grid)), dim3(1024), smem, s,
             partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, rg,
             static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, stats, ws.lrank, ws.block_counts, ws.block_base,
             ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb, static_cast<uint32_t>(smem),
