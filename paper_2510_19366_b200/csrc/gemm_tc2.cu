@@ -27,8 +27,14 @@
 // 64-row TMA boxes).  Per CTA and 64-deep k-block a plain remainder tile moves
 // 32 KB into shared memory and 48 KB out of it (its B half is read by both
 // tensor cores) whatever r is; the swapped one moves 16 KB + 64 Nt in and
-// 16 KB + 128 Nt out (0.47 of that at Nt = 32), and its MMAs cost ~N/2
-// cycles.  The accumulator then holds weight rows in TMEM lanes and tokens
+// 16 KB + 128 Nt out (0.47 of that at Nt = 32).  Measured (per-tile trace,
+// profiles/r02k_pair_tile_trace.txt): a swapped Nt = 32 tile still takes a
+// full tile's ~610 cycles per k-block (an M=256 pair MMA costs >= 96 cycles
+// whatever N is, profiles/r02k_mma_cost.csv, and spreading its k-steps over
+// 4 accumulators changed nothing), but it issues 1/8 of the MMA work: under
+// the 1000 W cap the energy saved is clock gained (Mixtral k = 4..16 5-10%
+// faster than plain remainders, profiles/r02k_swap_ab.txt).  The
+// accumulator then holds weight rows in TMEM lanes and tokens
 // in columns: the epilogue transposes 32 x 32 blocks through shared memory
 // (16-byte row stores), and for gemm1 the up rows (lanes 64..127 of a CTA in
 // the [64 gate | 64 up] layout) cross to the gate warps through shared
@@ -125,13 +131,6 @@ MP_DEV uint32_t swap_cols(uint32_t swap, uint32_t cnt, uint32_t m) {
 MP_DEV uint32_t tile_at(uint32_t i, uint32_t pair, uint32_t npairs) {
     return i * npairs + ((i & 1u) ? npairs - 1u - pair : pair);
 }
-// Independent accumulator chains of a swapped tile: MMAs into one accumulator
-// serialise on it (~91+ cycles each whatever N is, tests/probes/mma_cost.cu;
-// the per-tile trace put Nt = 32 swapped tiles at the full tile's ~610 cycles
-// per k-block with one chain), so narrow tiles spread their k-steps
-// round-robin over 256 / Nt (<= 4) accumulators in the tile's TMEM buffer and
-// the epilogue sums them in chain order.
-MP_DEV uint32_t swap_chains(uint32_t nt) { return nt <= 64 ? 4u : nt <= 128 ? 2u : 1u; }
 MP_DEV void named_bar(uint32_t id, uint32_t n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 MP_DEV uint32_t cluster_rank() {
@@ -372,7 +371,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 map_tile(tile, s_prefix, p.G, p.NT, g, m, n);
                 const uint32_t nt = swap_cols(p.swap_tail, s_off[g + 1] - s_off[g], m);
                 const uint32_t id = nt ? umma_idesc_bf16(BM, nt) : idesc;
-                const uint32_t chains = swap_chains(nt);
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
 #if MP_PAIR_TRACE
@@ -386,19 +384,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     // swapped remainder: the weight tile is the A operand, the tokens B
                     const uint32_t a0 = smem_u32(nt ? sB + s * B_BYTES : sA + s * A_BYTES);
                     const uint32_t b0 = smem_u32(nt ? sA + s * A_BYTES : sB + s * B_BYTES);
-                    if (nt) {
 #pragma unroll
-                        for (uint32_t k = 0; k < BK / 16; ++k) {
-                            const uint32_t j = kb * (BK / 16) + k, a = j % chains;
-                            umma_bf16_pair(d_tmem + a * nt, umma_desc_sw128(a0 + k * 32),
-                                           umma_desc_sw128(b0 + k * 32), id, j >= chains ? 1u : 0u);
-                        }
-                    } else {
-#pragma unroll
-                        for (uint32_t k = 0; k < BK / 16; ++k)
-                            umma_bf16_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), id,
-                                           (kb | k) != 0u);
-                    }
+                    for (uint32_t k = 0; k < BK / 16; ++k)
+                        umma_bf16_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), id,
+                                       (kb | k) != 0u);
                     umma_commit_pair(&empty[s]);
                 }
                 umma_commit_pair(&tfull[acc]);
@@ -541,20 +530,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (lane == 0) bulk_wait_read<0>();
                 __syncwarp();
             }
-            const uint32_t nch = nt / 32, chains = swap_chains(nt);
+            const uint32_t nch = nt / 32;
             uint32_t r[32];
-            // chunk c of the tile, the accumulator chains summed in chain order
             auto load_chunk = [&](uint32_t c) {
                 tmem_ld32(taddr + c * 32, r);
                 tmem_ld_wait();
-#pragma unroll 1
-                for (uint32_t a = 1; a < chains; ++a) {
-                    uint32_t t[32];
-                    tmem_ld32(taddr + a * nt + c * 32, t);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(t[j]));
-                }
             };
             if constexpr (SWIGLU) {
                 // lanes 0..63 gate, 64..127 up of neurons n*128 + rank*64 + 0..63

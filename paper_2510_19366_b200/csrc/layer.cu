@@ -599,7 +599,8 @@ void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t
     mp::launch_shared_gate(x, T, L->d, L->sh_gate, L->sh_w, L->sh_meta, L->sh_meta + 2, ss);
     CUtensorMap tmX;
     if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "shared expert tensor map");
-    const bool sh_pair = L->tile_mode == 2 || (L->tile_mode == 0 && T >= 192);
+    // one group of T rows: CTA pairs from 192 rows (the tile mode knobs steer the routed GEMMs only)
+    const bool sh_pair = T >= 192;
     mp::GemmShape s1{1, L->d_pad, 2 * L->sh_w_pad, T, L->sh_w_pad, 2 * L->sh_w_pad};
     mp::GemmShape s2{1, L->sh_w_pad, L->d_pad, T, L->d_pad, L->d_pad};
     // small batches: the down projection has d_pad / 256 output tiles (8 CTAs
@@ -668,32 +669,39 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
                  uint32_t kscalar = 0, bool bucketed = false) {
     // Kernel choice (auto): the kernel with the lower expected SM time per
     // (sub-expert, 256-column N tile) over bucket sizes M +- sqrt(M), M = T k /
-    // G (per-token k: k_max).  A CTA-pair tile (256 rows; with swapped
-    // remainder tiles, gemm_tc2.cu, a remainder tile costs about a full one:
-    // profiles/r02k_pair_tile_trace.txt) holds 2 SMs for ~612 cycles per
-    // 64-deep k-block; a 1-SM 128-row tile one SM for ~800 (MMA at 684 plus
-    // operand waits).  In-process A/B (tests/probes/tile_ab_k.py,
-    // profiles/r02l_tile_ab_k2.txt): pairs 5-10% ahead at the Mixtral shape
-    // for k = 3, 4, 6..16, 1-SM tiles ahead at k = 2 (every tile a remainder)
-    // and at Qwen prefill k = 8 (273 rows: 2 pair tiles vs 3 1-SM tiles), a
-    // tie at k = 5 -- the cost model picks each of those.  Without the
-    // swapped remainders (A/B) the round-1 rule: pairs credited 5% on padded
-    // rows.
+    // G (per-token k: k_max), in units of a 1-SM 128-row tile (one SM, ~800
+    // cycles per 64-deep k-block: MMA at 684 plus operand waits; a partial last
+    // tile of r rows loads only its rows: 0.5 + 0.5 r / 128).  A CTA-pair tile
+    // (256 rows; with swapped remainder tiles, gemm_tc2.cu, a remainder tile
+    // costs about a full one, profiles/r02k_pair_tile_trace.txt) holds 2 SMs
+    // for ~612 cycles per k-block: 1224 / 800, plus a per-tile overhead that
+    // matters at short K (the pair epilogue is twice the SM time of a 1-SM
+    // one): + 1 / (k-blocks of the shorter GEMM).  In-process A/B
+    // (tests/probes/tile_ab_k.py, profiles/r02l_tile_ab_k2.txt,
+    // profiles/r02r_tile_ab_qwen.txt): pairs 5-10% ahead at the Mixtral shape
+    // for k = 3, 4, 6..16; ties at k = 2, 5; 1-SM tiles ahead at Qwen prefill
+    // (K = 384 down projection) for k = 4, 8, 16 by 1.5-5%, a tie at 12 -- the
+    // model picks each of those.  Without the swapped remainders (A/B) the
+    // round-1 rule: pairs credited 5% on padded rows.
     {
         const double rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
         const double sd = std::sqrt(rows > 1.0 ? rows : 1.0);
-        double pad128 = 0.0, pad256 = 0.0;
+        double c128 = 0.0, c256 = 0.0, pad128 = 0.0, pad256 = 0.0;
         for (double m : {rows - sd, rows, rows + sd}) {
             const double mm = m < 1.0 ? 1.0 : m;
-            pad128 += std::ceil(mm / 128.0);
-            pad256 += std::ceil(mm / 256.0);
+            const double full = std::floor(mm / 128.0), r = mm - 128.0 * full;
+            c128 += full + (r > 0.0 ? 0.5 + 0.5 * r / 128.0 : 0.0);
+            c256 += std::ceil(mm / 256.0);
+            pad128 += std::ceil(mm / 128.0) * 128.0;
+            pad256 += std::ceil(mm / 256.0) * 256.0;
         }
         static const double pair_cost = [] {  // MOEPRISM_PAIR_COST: SM time of a pair tile / a 1-SM tile (A/B)
             const char* e = std::getenv("MOEPRISM_PAIR_COST");
             return e ? std::atof(e) : 1224.0 / 800.0;
         }();
-        const bool use_pairs = mp::pair_swap_enabled() ? pad256 * pair_cost < pad128
-                                                       : (rows >= 192.0 && pad256 * 256.0 / 1.05 < pad128 * 128.0);
+        const double nkb_min = std::max(1.0, std::min(L->d_pad, L->w_pad) / 64.0);
+        const bool use_pairs = mp::pair_swap_enabled() ? c256 * (pair_cost + 1.0 / nkb_min) < c128
+                                                       : (rows >= 192.0 && pad256 / 1.05 < pad128);
         L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && use_pairs);
     }
     if (!bucketed) {
