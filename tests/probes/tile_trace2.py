@@ -28,8 +28,9 @@ for which, name in ((0, 'gemm1'), (1, 'gemm2')):
     rec = tr[1024:].reshape(-1, 4)
     rec = rec[rec[:, 2] > 0]
     for nt in sorted(set(rec[:, 3].tolist())):
+        kind = "full" if nt == 0 else (f"twin Nt={nt - 256}" if nt >= 256 and nt != 256 else f"swapped Nt={nt}")
         r = rec[rec[:, 3] == nt]
-        print(f"{name} {'full' if nt == 0 else f'swapped Nt={nt}'}: tiles {len(r)}  MMA-phase cycles mean "
+        print(f"{name} {kind}: tiles {len(r)}  MMA-phase cycles mean "
               f"{r[:, 2].mean():.0f} p50 {np.median(r[:, 2]):.0f}  operand waits mean {r[:, 1].mean():.0f}", flush=True)
     lead = tr[:512].reshape(-1, 4)
     lead = lead[lead[:, 0] > 0]

@@ -531,15 +531,16 @@ def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
         assert ok.all(), f"mode {mode}: {(~ok).sum()} elements off"
 
 
-@pytest.mark.parametrize("T", [1, 37, 300, 777])
-def test_pair_swapped_tails_ragged(oracle, torch_cuda, T):
-    """CTA pairs with swapped-operand remainder tiles on ragged buckets (every
-    remainder size class: < 32, 32..255 rows, exact multiples) against the
-    oracle: routing bit-exact, outputs within the bf16 tolerance."""
+@pytest.mark.parametrize("T,d", [(1, 512), (37, 512), (300, 512), (560, 512), (777, 512), (37, 768), (560, 768)])
+def test_pair_swapped_tails_ragged(oracle, torch_cuda, T, d):
+    """CTA pairs with swapped-operand remainder tiles on ragged buckets against
+    the oracle: every remainder class (< 32, 32..255 rows, with and without
+    full tiles before them, an odd N-tile count at d = 768, exact multiples);
+    routing bit-exact, outputs within the bf16 tolerance."""
     import ctypes as C
     torch = torch_cuda
     from paper_2510_19366_b200 import _lib
-    E, S, d, ff, K = 4, 4, 512, 1024, 8
+    E, S, ff, K = 4, 4, 1024, 8
     experts, parts, wr, x = toy_setup(oracle, E, S, d, ff, T, seed_x=T)
     L = make_layer(experts, parts, wr, S, "bf16", k_max=K, max_tokens=T)
     lib = _lib.load()
