@@ -592,8 +592,8 @@ void offload_step(mp_layer_s* L, cudaStream_t s) {
 // forked from the forward's stream (gate -> gemm1 -> gemm2), overlapping the
 // router / bucketing / dispatch / routed GEMMs, and the combine joins it.
 // Fork / join are events, so the forward stays graph-capturable.
-void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t s) {
-    ck(cudaEventRecord(L->sh_fork, s), "fork shared expert");
+void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t s, bool forked = false) {
+    if (!forked) ck(cudaEventRecord(L->sh_fork, s), "fork shared expert");
     ck(cudaStreamWaitEvent(L->sh_stream, L->sh_fork, 0), "fork shared expert");
     cudaStream_t ss = L->sh_stream;
     mp::launch_shared_gate(x, T, L->d, L->sh_gate, L->sh_w, L->sh_meta, L->sh_meta + 2, ss);
@@ -601,6 +601,7 @@ void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t
     if (!mp::make_tmap_bf16_2d(&tmX, x, T, L->d, 128, 64)) fail(MP_ERR_CUDA, "shared expert tensor map");
     // one group of T rows: CTA pairs from 192 rows (the tile mode knobs steer the routed GEMMs only)
     const bool sh_pair = T >= 192;
+    const int sh_sms = L->num_sms;  // (capping it to leave SMs to the routing chain measured slower)
     mp::GemmShape s1{1, L->d_pad, 2 * L->sh_w_pad, T, L->sh_w_pad, 2 * L->sh_w_pad};
     mp::GemmShape s2{1, L->sh_w_pad, L->d_pad, T, L->d_pad, L->d_pad};
     // small batches: the down projection has d_pad / 256 output tiles (8 CTAs
@@ -616,16 +617,16 @@ void launch_shared_expert(mp_layer_s* L, const void* x, uint32_t T, cudaStream_t
         L->sh_splits = (nkb + kps - 1) / kps;
     }
     if (L->sh_splits) {
-        mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
+        mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, sh_sms, ss);
         mp::launch_gemm_tc_epi(mp::kEpiF32Part, &L->tm_hs, &L->tm_w2s, L->sh_o32, s2, L->sh_meta, L->sh_meta + 2,
-                               L->num_sms, ss, 0, nullptr, nullptr, nullptr, L->sh_splits);
+                               sh_sms, ss, 0, nullptr, nullptr, nullptr, L->sh_splits);
     } else if (sh_pair) {
-        mp::launch_gemm_tc2(true, &tmX, &L->tm_w1sh, L->sh_h, s1, L->sh_meta, L->sh_meta + 4, L->num_sms, ss, nullptr);
-        mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, L->num_sms, ss,
+        mp::launch_gemm_tc2(true, &tmX, &L->tm_w1sh, L->sh_h, s1, L->sh_meta, L->sh_meta + 4, sh_sms, ss, nullptr);
+        mp::launch_gemm_tc2(false, &L->tm_hs, &L->tm_w2sh, L->sh_o, s2, L->sh_meta, L->sh_meta + 4, sh_sms, ss,
                             nullptr);
     } else {
-        mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
-        mp::launch_gemm_tc(false, &L->tm_hs, &L->tm_w2s, L->sh_o, s2, L->sh_meta, L->sh_meta + 2, L->num_sms, ss);
+        mp::launch_gemm_tc(true, &tmX, &L->tm_w1s, L->sh_h, s1, L->sh_meta, L->sh_meta + 2, sh_sms, ss);
+        mp::launch_gemm_tc(false, &L->tm_hs, &L->tm_w2s, L->sh_o, s2, L->sh_meta, L->sh_meta + 2, sh_sms, ss);
     }
     ck_launch("shared expert");
     ck(cudaEventRecord(L->sh_join, ss), "join shared expert");
@@ -800,9 +801,23 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
     // zeroed before the router so the router -> routing-epilogue boundary is
     // kernel to kernel (programmatic dependent launch)
     if (L->has_router) ck(cudaMemsetAsync(L->r_flagged, 0, 2 * sizeof(uint32_t), s), "memset routing stats");
+    // The shared expert forks here (it depends on x only) but its kernels are
+    // enqueued after the routing chain's, so the routing CTAs reach the SMs
+    // first (Qwen prefill: 4-5% at k = 16, <= 1% elsewhere;
+    // profiles/r02u_shared_order_ab.txt).  MOEPRISM_SH_ORDER=0: enqueued first.
+    static const int sh_order = [] {
+        const char* e = std::getenv("MOEPRISM_SH_ORDER");
+        return e ? std::atoi(e) : 1;
+    }();
+    bool sh_deferred = false;
     if (with_shared && L->sh_ff) {
         if (reinterpret_cast<uintptr_t>(x) % 16) fail(MP_ERR_VALIDATION, "shared expert needs 16-byte aligned x");
-        launch_shared_expert(L, x, T, s);
+        if (sh_order == 1) {
+            ck(cudaEventRecord(L->sh_fork, s), "fork shared expert");
+            sh_deferred = true;
+        } else {
+            launch_shared_expert(L, x, T, s);
+        }
     }
     if (with_shared) prefetch_routed_weights(L, T, s);
     if (L->desc.router_mode == MP_ROUTER_PROXY) {
@@ -883,6 +898,7 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
             tm.end(0, 1);
         }
     }
+    if (sh_deferred) launch_shared_expert(L, x, T, s, true);
     return bucketed;
 }
 
