@@ -448,8 +448,27 @@ def bench_qwen(pk, steps=30):
             ms = time_steps(lambda i, k=k: L.forward(xs[i % 4], k=k, y=y), steps, 3, 1)
             F = 6.0 * d * w * T * k + 6.0 * d * ffs * T
             B = touched * 3.0 * d * w * 2 + 3.0 * d * ffs * 2 + 2.0 * T * d * 2
+            st = stage_profile([L], lambda x, kk, kpt, y=y: L.forward(x, k=kk, y=y), xs, k)
+            # routed GEMMs against their bound (CUDA-event stage times on the
+            # forward's stream; the shared expert runs concurrently on a side
+            # stream, so these include its contention): TFLOP/s of 4 d w T k /
+            # 2 d w T k at prefill, GB/s of the touched weights at decode
+            gr = {}
+            for name, fl, wb in (("gemm1", 4.0 * d * w * T * k, touched * 2.0 * d * w * 2),
+                                 ("gemm2", 2.0 * d * w * T * k, touched * 1.0 * d * w * 2)):
+                t = st.get(name, 0.0)
+                if t <= 0:
+                    continue
+                if fl / (pk["bf16_tflops_sustained"] * 1e12) >= wb / (pk["hbm_gbs"] * 1e9):
+                    a = fl / (t * 1e-3) / 1e12
+                    gr[name] = {"bound": "tensor", "achieved": a, "unit": "TFLOP/s", "ms": t,
+                                "frac": a / pk["bf16_tflops_sustained"]}
+                else:
+                    a = wb / (t * 1e-3) / 1e9
+                    gr[name] = {"bound": "hbm", "achieved": a, "unit": "GB/s", "ms": t, "frac": a / pk["hbm_gbs"]}
             out.append({"tokens": T, "k": k, "tokens_per_s": T / (ms * 1e-3), "ms_per_step": ms,
-                        "touched_subexperts": touched, "roofline": roofline_fb(F, B, ms, pk)})
+                        "touched_subexperts": touched, "roofline": roofline_fb(F, B, ms, pk),
+                        "stages_ms": st, "routed_gemm_roofline": gr})
         del xs
     L.close()
     torch.cuda.synchronize()

@@ -10,7 +10,8 @@ for s in j['sweep']:
           "kern", round(kr.get('frac', 0), 3), {a: round(b, 3) for a, b in s['stages_ms'].items()})
 oc = j.get('other_configs', {})
 for s in oc.get('qwen', {}).get('sweep', []):
-    print('qwen', s['tokens'], s['k'], round(s['ms_per_step'], 4), round(s['roofline']['frac'], 3))
+    gr = {a: round(b['frac'], 3) for a, b in s.get('routed_gemm_roofline', {}).items()}
+    print('qwen', s['tokens'], s['k'], round(s['ms_per_step'], 4), round(s['roofline']['frac'], 3), gr)
 for k in ('mixed_qos_32k',):
     if k in oc:
         v = oc[k]
