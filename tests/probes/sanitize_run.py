@@ -1,7 +1,9 @@
 """Small forwards over the kernel variants for compute-sanitizer
-(memcheck / racecheck / synccheck): 1-SM and CTA-pair GEMMs (plain, merged,
-M=128 tails, split), the fused router with > 128 sub-experts (column split),
-the shared expert, per-token k.  python tests/probes/sanitize_run.py"""
+(memcheck / racecheck / synccheck): 1-SM GEMMs, CTA-pair GEMMs with swapped
+remainder tiles (every remainder size: T = 1024 / 300 / 37 tokens) and with
+plain remainders, the fused router with > 128 sub-experts (column split,
+persistent grid-barrier bases), the shared expert, per-token k.
+python tests/probes/sanitize_run.py"""
 import ctypes as C, sys
 import numpy as np
 import torch
@@ -29,10 +31,11 @@ def layer(E, S, d, ff, T, k_max, shared=0):
 
 x = synth_fill(torch.empty((1024, 512), dtype=torch.bfloat16, device="cuda"), 11, 1.0)
 L = layer(4, 4, 512, 1024, 1024, 16)
-for mode in (0, 1, 2):
+for mode in (0, 1, 2, 3):
     _lib.check(lib.mp_debug_set_tile_mode(L.h, mode))
-    for k in (4, 16):
-        L.forward(x, k=k)
+    for T in (1024, 300, 37):
+        for k in (4, 16):
+            L.forward(x[:T], k=k)
 kpt = torch.from_numpy(np.random.default_rng(1).choice([2, 4, 8, 16], size=1024).astype(np.int32)).cuda()
 L.forward(x, k_per_token=kpt)
 torch.cuda.synchronize()
