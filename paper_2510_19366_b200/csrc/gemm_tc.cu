@@ -199,8 +199,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t base_total = s_prefix[p.G] * p.NT;
     const uint32_t total = base_total * p.ksplit;
     const uint32_t nkb = p.K / BK;
+    // balanced rounds: with R = ceil(total / grid) tiles per CTA, only
+    // ceil(total / R) CTAs take tiles, every one exactly R or R - 1 (no last
+    // round on a fraction of the SMs: Qwen decode gemm1, 630 tiles, 106.5 ->
+    // 102 us on 126 instead of 148 CTAs under ncu)
+    const uint32_t per_cta = (total + gridDim.x - 1) / gridDim.x;
+    const uint32_t nact = per_cta ? (total + per_cta - 1) / per_cta : gridDim.x;
+    const uint32_t first = blockIdx.x < nact ? blockIdx.x : total;  // idle CTAs start past the end
     for (uint32_t i = threadIdx.x; i < kTileCache; i += blockDim.x) {
-        const uint32_t tile = blockIdx.x + i * gridDim.x;
+        const uint32_t tile = first + i * nact;
         if (tile >= total) break;
         uint32_t g, m, n;
         const uint32_t split = tile / base_total;
@@ -281,12 +288,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         auto advance = [&](Cursor& c, bool is_a) {
             if (++c.kb == c.kb1) {
-                c.tile += gridDim.x;
+                c.tile += nact;
                 ++c.i;
                 set_rows(c, is_a);
             }
         };
-        Cursor cb{blockIdx.x, 0, 0, 0, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0, 0, 0, 0};
+        Cursor cb{first, 0, 0, 0, 0, 0, 0}, ca{first, 0, 0, 0, 0, 0, 0};
         set_rows(cb, false);
         set_rows(ca, true);
         uint32_t ib = 0, ia = 0;
@@ -327,12 +334,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             auto advance = [&](Cursor& c, bool is_a) {
                 if (++c.kb == c.kb1) {
-                    c.tile += gridDim.x;
+                    c.tile += nact;
                     ++c.i;
                     set_rows(c, is_a);
                 }
             };
-            Cursor cb{blockIdx.x, 0, 0, 0, 0, 0, 0}, ca{blockIdx.x, 0, 0, 0, 0, 0, 0};
+            Cursor cb{first, 0, 0, 0, 0, 0, 0}, ca{first, 0, 0, 0, 0, 0, 0};
             set_rows(cb, false);
             set_rows(ca, true);
             uint32_t ib = 0, ia = 0;  // loads issued per stream
@@ -373,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // waits for accumulators (epilogue) and for operand stages (loads)
             const uint64_t t_start = p.trace ? clock64() : 0;
             uint64_t w_acc = 0, w_full = 0;
-            for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+            for (uint32_t tile = first; tile < total; tile += nact, ++tc) {
                 const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
                 uint64_t t0 = p.trace ? clock64() : 0;
                 mbar_wait(&tempty[acc], aph ^ 1u);
@@ -413,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
         uint32_t tc = 0;
         uint32_t epi_it = 0;  // TMA-stored chunks of this warp (staging buffer parity)
-        for (uint32_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+        for (uint32_t tile = first; tile < total; tile += nact, ++tc) {
             uint32_t g, m, n, split;
             decode(tile, tc, g, m, n, split);
             const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
@@ -683,7 +690,12 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
 
     // upper bound on tiles; the kernel reads the exact count from the device
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT * p.ksplit;
-    const uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
+    static const uint32_t grid_cap = [] {  // MOEPRISM_GEMM_GRID: cap on the 1-SM GEMM grid (diagnostics)
+        const char* e = std::getenv("MOEPRISM_GEMM_GRID");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+    }();
+    uint32_t grid = max_tiles < (uint32_t)num_sms ? max_tiles : (uint32_t)num_sms;
+    if (grid_cap && grid > grid_cap) grid = grid_cap;
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiPlain>), (int)kSmemBytes);
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiSwiglu>), (int)kSmemBytes);
     func_attr_once(reinterpret_cast<const void*>(gemm_tc_kernel<kEpiActAbs>), (int)kSmemBytes);

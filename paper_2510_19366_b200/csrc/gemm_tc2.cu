@@ -252,7 +252,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t warp = threadIdx.x / 32;
     const uint32_t lane = threadIdx.x % 32;
     const uint32_t rank = cluster_rank();
-    const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const uint32_t pair = blockIdx.x >> 1, npairs_grid = gridDim.x >> 1;
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < NS; ++s) {
@@ -289,7 +289,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t total = s_prefix[p.G] * p.NT;
-    const uint32_t rounds = (total + npairs - 1) / npairs;
+    // balanced rounds (as in gemm_tc.cu): only ceil(total / R) pairs take
+    // tiles, R = ceil(total / pairs) each
+    const uint32_t rounds = (total + npairs_grid - 1) / npairs_grid;
+    const uint32_t npairs = rounds ? (total + rounds - 1) / rounds : npairs_grid;
+    const uint32_t my_rounds = pair < npairs ? rounds : 0u;  // idle pairs take no tiles
     const uint32_t nkb = p.K / BK;
 
     if (warp == 0) {
@@ -301,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             (void)pol_b;
 #endif
             uint32_t it = 0;
-            for (uint32_t i = 0; i < rounds; ++i) {
+            for (uint32_t i = 0; i < my_rounds; ++i) {
                 const uint32_t tile = tile_at(i, pair, npairs);
                 if (tile >= total) continue;
                 uint32_t g, m, n;
@@ -352,7 +356,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t t_start = clock64();
             uint64_t w_acc = 0, w_full = 0;
 #endif
-            for (uint32_t i = 0; i < rounds; ++i) {
+            for (uint32_t i = 0; i < my_rounds; ++i) {
                 const uint32_t tile = tile_at(i, pair, npairs);
                 if (tile >= total) continue;
                 const uint32_t acc = tc & 1u;
@@ -578,7 +582,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #if MP_PAIR_TRACE
         uint64_t e_busy = 0, e_ext = 0, e_wait = 0;
 #endif
-        for (uint32_t i = 0; i < rounds; ++i) {
+        for (uint32_t i = 0; i < my_rounds; ++i) {
             const uint32_t tile = tile_at(i, pair, npairs);
             if (tile >= total) continue;
             uint32_t g, m, n;

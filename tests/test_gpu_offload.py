@@ -73,3 +73,26 @@ def test_offload_capacity_error_and_guards(oracle, torch_cuda):
         off.enable_offload(4)
     res.close()
     off.close()
+
+
+@pytest.mark.parametrize("T", [200, 700])
+def test_offload_with_cta_pairs(oracle, torch_cuda, T):
+    """The offload cache under the CTA-pair GEMMs (full tiles and swapped
+    remainder tiles read their weights through the group -> cache-slot map):
+    bitwise equal to the resident layer on the same kernel."""
+    import ctypes as C
+    torch = torch_cuda
+    from paper_2510_19366_b200 import _lib
+    lib = _lib.load()
+    lib.mp_debug_set_tile_mode.argtypes = [C.c_void_p, C.c_int]
+    res, off = _layers(oracle, T)
+    off.enable_offload(E * S)
+    for L in (res, off):
+        _lib.check(lib.mp_debug_set_tile_mode(L.h, 2))
+    x = torch.from_numpy(bf16_round(oracle.uniform_pm1(77, T * D))).reshape(T, D).cuda().to(torch.bfloat16)
+    for k in (1, 4):
+        y0 = res.forward(x, k=k)
+        y1 = off.forward(x, k=k)
+        assert torch.equal(y0, y1)
+    res.close()
+    off.close()
