@@ -657,7 +657,12 @@ void launch_gemm_tc2(bool swiglu, const CUtensorMap* tmA, const CUtensorMap* tmB
     const CUtensorMap* s64 = swap ? &tmA_small[2] : tmA;
     if (p.trace) cudaMemsetAsync(p.trace, 0, (4096 + 128 * 128 * 4) * sizeof(uint64_t), s);
     const uint32_t max_tiles = (sh.max_rows / BM + sh.G) * p.NT;
+    static const uint32_t grid_cap = [] {  // MOEPRISM_PAIR_GRID: cap on the pairs of the grid (diagnostics)
+        const char* e = std::getenv("MOEPRISM_PAIR_GRID");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+    }();
     uint32_t pairs = static_cast<uint32_t>(num_sms) / 2;
+    if (grid_cap && pairs > grid_cap) pairs = grid_cap;
     if (max_tiles < pairs) pairs = max_tiles;
     if (pairs == 0) pairs = 1;
     func_attr_once(reinterpret_cast<const void*>(gemm_pair_kernel<true>), (int)kSmemBytes);
