@@ -73,8 +73,13 @@
 #ifndef MP_PAIR_HINTS
 #define MP_PAIR_HINTS 0
 #endif
+// Pipeline: 3 stages of 128-deep k-blocks (two 64-deep TMA sub-blocks per
+// operand).  Measured against 6 stages of 64-deep k-blocks (the same bytes in
+// flight): the per-k-block barrier round trip and issue overhead halves --
+// leader cycles -14% (gemm1) / -16% (gemm2) at Mixtral k=8, steps -2..-7% at
+// k = 6..16 (profiles/r02ac_kblock128_ab.txt).
 #ifndef MP_PAIR_STAGES
-#define MP_PAIR_STAGES 6
+#define MP_PAIR_STAGES 3
 #endif
 
 namespace mp {
@@ -84,7 +89,13 @@ namespace {
 constexpr uint32_t BM = 256;  // rows per pair tile (128 per CTA)
 constexpr uint32_t HM = 128;
 constexpr uint32_t BN = 256;
-constexpr uint32_t BK = 64;
+#ifndef MP_PAIR_KSUB
+#define MP_PAIR_KSUB 2  // 64-deep TMA sub-blocks per pipeline stage (1: 64-deep k-blocks, with 6 stages)
+#endif
+constexpr uint32_t KSUB = MP_PAIR_KSUB;
+constexpr uint32_t BK = 64 * KSUB;
+constexpr uint32_t SUB_A = HM * 64 * 2;   // one 64-deep sub-block of A / of the B half: 16 KB
+constexpr uint32_t SUB_B = 128 * 64 * 2;
 constexpr uint32_t NSP = MP_PAIR_STAGES;
 constexpr uint32_t A_BYTES = HM * BK * 2;   // 16 KB per CTA
 constexpr uint32_t B_BYTES = 128 * BK * 2;  // 16 KB per CTA (half of the 256-row B tile)
@@ -104,6 +115,7 @@ constexpr uint32_t kXchBytes = 64 * 33 * 4;         // gemm1 swapped tiles: up r
 constexpr uint32_t kStgBytes = 4 * 2 * 32 * 32 * 2;  // per epilogue warp: two 32 x 32 bf16 blocks (TMA-store
                                                     // staging, double-buffered; swapped tiles' transposes)
 constexpr size_t kSmemBytes = 1024 + NSP * STAGE_BYTES + 256 + kXchBytes + kStgBytes;
+static_assert(kSmemBytes + 4096 <= 232448, "pair GEMM shared memory");
 static_assert(kEpiWarps == 4, "the swapped-tail epilogue pairs lane quarters 0/1 with 2/3 (4 epilogue warps)");
 
 struct PairParams {
@@ -294,7 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t rounds = (total + npairs_grid - 1) / npairs_grid;
     const uint32_t npairs = rounds ? (total + rounds - 1) / rounds : npairs_grid;
     const uint32_t my_rounds = pair < npairs ? rounds : 0u;  // idle pairs take no tiles
-    const uint32_t nkb = p.K / BK;
+    const uint32_t nkb = (p.K + BK - 1) / BK;  // a partial last k-block is zero-filled by the TMA
 
     if (warp == 0) {
         if (lane == 0) {
@@ -317,34 +329,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (uint32_t kb = 0; kb < nkb; ++kb, ++it) {
                     const uint32_t s = it % NS, ph = (it / NS) & 1u;
                     mbar_wait(&empty[s], ph ^ 1u);
-                    if (rank == 0) mbar_expect_tx(&full[s], 2 * (B_BYTES + (nt ? half * 128u : A_BYTES)));
+                    if (rank == 0) mbar_expect_tx(&full[s], 2 * KSUB * (SUB_B + (nt ? half * 128u : SUB_A)));
                     const uint32_t fb = full_leader + s * 8;
-                    const int32_t kc = static_cast<int32_t>(kb * BK);
+                    for (uint32_t sb = 0; sb < KSUB; ++sb) {
+                    const int32_t kc = static_cast<int32_t>(kb * BK + sb * 64);
+                    uint8_t* dA = sA + s * A_BYTES + sb * SUB_A;
+                    uint8_t* dB = sB + s * B_BYTES + sb * SUB_B;
                     if (nt && half < HM) {
                         // token rows through 64 / 32 / 16-row boxes (half is a multiple of 16)
                         uint32_t done = 0;
                         if (half & 64u) {
-                            tma_load_2d_pair(sA + s * A_BYTES, &tmA64, fb, kc, arow);
+                            tma_load_2d_pair(dA, &tmA64, fb, kc, arow);
                             done = 64;
                         }
                         if (half & 32u) {
-                            tma_load_2d_pair(sA + s * A_BYTES + done * 128u, &tmA32, fb, kc, arow + (int32_t)done);
+                            tma_load_2d_pair(dA + done * 128u, &tmA32, fb, kc, arow + (int32_t)done);
                             done += 32;
                         }
                         if (half & 16u)
-                            tma_load_2d_pair(sA + s * A_BYTES + done * 128u, &tmA16, fb, kc, arow + (int32_t)done);
+                            tma_load_2d_pair(dA + done * 128u, &tmA16, fb, kc, arow + (int32_t)done);
                     } else {
 #if MP_PAIR_HINTS & 2
-                        tma_load_2d_pair_hint(sA + s * A_BYTES, &tmA, fb, kc, arow, pol_a);
+                        tma_load_2d_pair_hint(dA, &tmA, fb, kc, arow, pol_a);
 #else
-                        tma_load_2d_pair(sA + s * A_BYTES, &tmA, fb, kc, arow);
+                        tma_load_2d_pair(dA, &tmA, fb, kc, arow);
 #endif
                     }
 #if MP_PAIR_HINTS & 1
-                    tma_load_2d_pair_hint(sB + s * B_BYTES, &tmB, fb, kc, brow, pol_b);
+                    tma_load_2d_pair_hint(dB, &tmB, fb, kc, brow, pol_b);
 #else
-                    tma_load_2d_pair(sB + s * B_BYTES, &tmB, fb, kc, brow);
+                    tma_load_2d_pair(dB, &tmB, fb, kc, brow);
 #endif
+                    }
                 }
             }
         }
@@ -389,9 +405,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const uint32_t a0 = smem_u32(nt ? sB + s * B_BYTES : sA + s * A_BYTES);
                     const uint32_t b0 = smem_u32(nt ? sA + s * A_BYTES : sB + s * B_BYTES);
 #pragma unroll
-                    for (uint32_t k = 0; k < BK / 16; ++k)
-                        umma_bf16_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), id,
+                    for (uint32_t k = 0; k < BK / 16; ++k) {
+                        // k-step k: sub-block k / 4 (16 KB apart in both operand slots), 32 bytes per step
+                        const uint32_t off = (k >> 2) * SUB_A + (k & 3u) * 32;
+                        umma_bf16_pair(d_tmem, umma_desc_sw128(a0 + off), umma_desc_sw128(b0 + off), id,
                                        (kb | k) != 0u);
+                    }
                     umma_commit_pair(&empty[s]);
                 }
                 umma_commit_pair(&tfull[acc]);
