@@ -670,19 +670,17 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
                  uint32_t kscalar = 0, bool bucketed = false) {
     // Kernel choice (auto): the kernel with the lower expected SM time per
     // (sub-expert, 256-column N tile) over bucket sizes M +- sqrt(M), M = T k /
-    // G (per-token k: k_max), in units of a 1-SM 128-row tile (one SM, ~800
-    // cycles per 64-deep k-block: MMA at 684 plus operand waits; a partial last
-    // tile of r rows loads only its rows: 0.5 + 0.5 r / 128).  A CTA-pair tile
-    // (256 rows; with swapped remainder tiles, gemm_tc2.cu, a remainder tile
-    // costs about a full one, profiles/r02k_pair_tile_trace.txt) holds 2 SMs
-    // for ~612 cycles per k-block: 1224 / 800, plus a per-tile overhead that
-    // matters at short K (the pair epilogue is twice the SM time of a 1-SM
-    // one): + 1 / (k-blocks of the shorter GEMM).  In-process A/B
-    // (tests/probes/tile_ab_k.py, profiles/r02l_tile_ab_k2.txt,
-    // profiles/r02r_tile_ab_qwen.txt): pairs 5-10% ahead at the Mixtral shape
-    // for k = 3, 4, 6..16; ties at k = 2, 5; 1-SM tiles ahead at Qwen prefill
-    // (K = 384 down projection) for k = 4, 8, 16 by 1.5-5%, a tie at 12 -- the
-    // model picks each of those.  Without the swapped remainders (A/B) the
+    // G (per-token k: k_max), in units of a 1-SM 128-row tile (a partial last
+    // tile of r rows loads only its rows: 0.5 + 0.5 r / 128).  A CTA-pair
+    // tile (256 rows; with swapped remainder tiles, gemm_tc2.cu, a remainder
+    // tile costs about a full one) costs 1.25 of those (2 SMs; round-2
+    // 128-deep pair k-blocks) plus a per-tile overhead that matters at short
+    // K (the pair epilogue is twice the SM time of a 1-SM one): + 2 / (64-deep
+    // k-blocks of the shorter GEMM).  In-process A/B (tests/probes/tile_ab_k.py,
+    // profiles/r02ae_tile_ab.txt): pairs ahead at the Mixtral shape for k >= 3
+    // (4-13%), 1.6% at k = 2 (the model keeps 1-SM tiles there); 1-SM tiles
+    // ahead at Qwen prefill (K = 384 down projection) for k = 8 and 16 by
+    // 6% / 3%, ties at k = 4 and 12.  Without the swapped remainders (A/B) the
     // round-1 rule: pairs credited 5% on padded rows.
     {
         const double rows = double(T) * (kscalar ? kscalar : L->k_max) / L->G;
@@ -698,10 +696,10 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         }
         static const double pair_cost = [] {  // MOEPRISM_PAIR_COST: SM time of a pair tile / a 1-SM tile (A/B)
             const char* e = std::getenv("MOEPRISM_PAIR_COST");
-            return e ? std::atof(e) : 1224.0 / 800.0;
+            return e ? std::atof(e) : 1.25;
         }();
         const double nkb_min = std::max(1.0, std::min(L->d_pad, L->w_pad) / 64.0);
-        const bool use_pairs = mp::pair_swap_enabled() ? c256 * (pair_cost + 1.0 / nkb_min) < c128
+        const bool use_pairs = mp::pair_swap_enabled() ? c256 * (pair_cost + 2.0 / nkb_min) < c128
                                                        : (rows >= 192.0 && pad256 / 1.05 < pad128);
         L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && use_pairs);
     }
