@@ -183,7 +183,7 @@ struct mp_layer_s {
     // gemm_tc, by rows per sub-expert); 1 1-SM, 2 pairs, 3 pairs with plain
     // (unswapped) remainder tiles; MOEPRISM_TC_TILE=128|256|256-plain forces
     int tile_mode = 0;
-    bool tile256 = false;  // this forward's choice
+    bool tile256 = false, tile256_g2 = false;  // this forward's choice for gemm1 / gemm2
     bool has_experts = true, has_router = true;  // MP_LAYER_* role flags
 
     std::vector<std::vector<uint32_t>> assignment;
@@ -698,10 +698,20 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
             const char* e = std::getenv("MOEPRISM_PAIR_COST");
             return e ? std::atof(e) : 1.25;
         }();
-        const double nkb_min = std::max(1.0, std::min(L->d_pad, L->w_pad) / 64.0);
-        const bool use_pairs = mp::pair_swap_enabled() ? c256 * (pair_cost + 2.0 / nkb_min) < c128
-                                                       : (rows >= 192.0 && pad256 / 1.05 < pad128);
-        L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && use_pairs);
+        // per GEMM: its own K (gemm1 d_pad, gemm2 w_pad) in the short-K term
+        auto pairs_for = [&](uint32_t K) {
+            const double nkb = std::max(1.0, K / 64.0);
+            return mp::pair_swap_enabled() ? c256 * (pair_cost + 2.0 / nkb) < c128
+                                           : (rows >= 192.0 && pad256 / 1.05 < pad128);
+        };
+        static const bool per_gemm = [] {  // MOEPRISM_TILE_PER_GEMM=0: one choice for both GEMMs (A/B)
+            const char* e = std::getenv("MOEPRISM_TILE_PER_GEMM");
+            return !(e && e[0] == '0');
+        }();
+        const bool p1 = per_gemm ? pairs_for(L->d_pad) : pairs_for(std::min(L->d_pad, L->w_pad));
+        const bool p2 = per_gemm ? pairs_for(L->w_pad) : p1;
+        L->tile256 = L->tile_mode >= 2 || (L->tile_mode == 0 && p1);
+        L->tile256_g2 = L->tile_mode >= 2 || (L->tile_mode == 0 && p2);
     }
     if (!bucketed) {
         tm.begin(1);
@@ -760,7 +770,7 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
     const bool shared = with_shared && L->sh_ff;
     tm.end(3, 1);
     tm.begin(4);
-    if (L->use_tc && L->tile256)
+    if (L->use_tc && L->tile256_g2)
         mp::launch_gemm_tc2(false, &L->tm_h, L->offload ? &L->tm_w2ch : &L->tm_w2h, L->o, g2, L->ws.offsets,
                             L->ws.mprefix_tc2, L->num_sms, s, gmap, L->tile_mode == 3 ? nullptr : L->tm_h_s,
                             &L->tm_o);
