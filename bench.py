@@ -668,7 +668,7 @@ def kernel_roofline(stage_ms_per_step, T, k, pk, touched_groups):
     traffic = None
     # DRAM bytes of the kernel per launch from the committed ncu --set full
     # capture of the same workload (tests/probes/ncu_summary.py)
-    prof = ROOT / "profiles" / "ncu_summary_r02z.json"
+    prof = ROOT / "profiles" / "ncu_summary_r02af.json"
     if prof.exists():
         try:
             j = json.loads(prof.read_text())
