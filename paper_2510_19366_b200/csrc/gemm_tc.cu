@@ -52,11 +52,20 @@ namespace {
 
 constexpr uint32_t BM = kTcBM;  // 128
 constexpr uint32_t BN = 256;
-constexpr uint32_t BK = 64;  // one 128-byte swizzle row of bf16
+#ifndef MP_TC_KSUB
+// 64-deep TMA sub-blocks per pipeline stage.  2 (with MP_TC_NA=2 MP_TC_NB=2)
+// measured slower: 2 stages expose the load latency (profiles/r02ag_1sm_kblock128_ab.txt).
+// The shared expert's decode split count (layer.cu) assumes 64-deep k-blocks.
+#define MP_TC_KSUB 1
+#endif
+constexpr uint32_t KSUB = MP_TC_KSUB;
+constexpr uint32_t BK = 64 * KSUB;  // k-block depth: KSUB 128-byte swizzle rows of bf16
 constexpr uint32_t NA = MP_TC_NA, NB = MP_TC_NB;
 
 constexpr uint32_t A_BYTES = BM * BK * 2;
 constexpr uint32_t B_BYTES = BN * BK * 2;
+constexpr uint32_t SUBA = BM * 64 * 2;  // one 64-deep sub-block of the A / B stage
+constexpr uint32_t SUBB = BN * 64 * 2;
 constexpr uint32_t kThreads = 192;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kEpiStage = 32 * 32 * 2;  // one 32-row x 32-column bf16 box of a warp's output slab
@@ -198,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     const uint32_t base_total = s_prefix[p.G] * p.NT;
     const uint32_t total = base_total * p.ksplit;
-    const uint32_t nkb = p.K / BK;
+    const uint32_t nkb = (p.K + BK - 1) / BK;  // a partial last k-block is zero-filled by the TMA
     // balanced rounds: with R = ceil(total / grid) tiles per CTA, only
     // ceil(total / R) CTAs take tiles, every one exactly R or R - 1 (no last
     // round on a fraction of the SMs: Qwen decode gemm1, 630 tiles, 106.5 ->
@@ -235,29 +244,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     // one B stage: the 256-row weight tile, or (gemm1 B tail) its valid blocks
     auto load_b = [&](uint32_t s, uint32_t ph, uint32_t kb, int32_t row, uint32_t n) {
         mbar_wait(&emptyB[s], ph ^ 1u);
-        const int32_t kc = static_cast<int32_t>(kb * BK);
         const uint32_t nb = n * 2;  // first 64-neuron block of the tile (128 rows: gate, up)
         if (!p.b_valid || p.b_valid >= (nb + 2) * 64) {
             mbar_expect_tx(&fullB[s], B_BYTES);
-            tma_load_2d(sB + s * B_BYTES, &tmB, &fullB[s], kc, row);
+            for (uint32_t sb = 0; sb < KSUB; ++sb)
+                tma_load_2d(sB + s * B_BYTES + sb * SUBB, &tmB, &fullB[s], static_cast<int32_t>(kb * BK + sb * 64), row);
         } else {
             uint32_t v[2], bytes = 0;
 #pragma unroll
             for (uint32_t hb = 0; hb < 2; ++hb) {
                 const uint32_t lo = (nb + hb) * 64;
                 v[hb] = p.b_valid > lo ? min(64u, p.b_valid - lo) : 0u;
-                bytes += v[hb] == 64 ? 128 * BK * 2 : v[hb] ? 2 * p.b_tail_rows * BK * 2 : 0;
+                bytes += v[hb] == 64 ? 128 * 64 * 2 : v[hb] ? 2 * p.b_tail_rows * 64 * 2 : 0;
             }
-            mbar_expect_tx(&fullB[s], bytes);
+            mbar_expect_tx(&fullB[s], bytes * KSUB);
+            for (uint32_t sb = 0; sb < KSUB; ++sb) {
+                const int32_t kc = static_cast<int32_t>(kb * BK + sb * 64);
 #pragma unroll
-            for (uint32_t hb = 0; hb < 2; ++hb) {
-                uint8_t* dst = sB + s * B_BYTES + hb * (128 * BK * 2);
-                const int32_t r = row + static_cast<int32_t>(hb * 128);
-                if (v[hb] == 64) {
-                    tma_load_2d(dst, &tmBh, &fullB[s], kc, r);
-                } else if (v[hb]) {  // gate rows, then the up rows of the same neurons
-                    tma_load_2d(dst, &tmBt, &fullB[s], kc, r);
-                    tma_load_2d(dst + kIlv * BK * 2, &tmBt, &fullB[s], kc, r + static_cast<int32_t>(kIlv));
+                for (uint32_t hb = 0; hb < 2; ++hb) {
+                    uint8_t* dst = sB + s * B_BYTES + sb * SUBB + hb * (128 * 64 * 2);
+                    const int32_t r = row + static_cast<int32_t>(hb * 128);
+                    if (v[hb] == 64) {
+                        tma_load_2d(dst, &tmBh, &fullB[s], kc, r);
+                    } else if (v[hb]) {  // gate rows, then the up rows of the same neurons
+                        tma_load_2d(dst, &tmBt, &fullB[s], kc, r);
+                        tma_load_2d(dst + kIlv * 64 * 2, &tmBt, &fullB[s], kc, r + static_cast<int32_t>(kIlv));
+                    }
                 }
             }
         }
@@ -308,11 +320,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t ng = (ca.rows + 3) / 4;
                 if (lane == 0) {
                     mbar_wait(&emptyA[s], ph ^ 1u);
-                    mbar_expect_tx(&fullA[s], ng * 4 * BK * 2);
+                    mbar_expect_tx(&fullA[s], ng * 4 * BK * 2);  // KSUB sub-blocks of ng x 4 rows
                 }
                 __syncwarp();
-                if (lane < ng) tma_gather4(sA + s * A_BYTES + lane * (4 * BK * 2), &tmA, &fullA[s],
-                                           static_cast<int32_t>(ca.kb * BK), tok);
+                if (lane < ng)
+                    for (uint32_t sb = 0; sb < KSUB; ++sb)
+                        tma_gather4(sA + s * A_BYTES + sb * SUBA + lane * (4 * 64 * 2), &tmA, &fullA[s],
+                                    static_cast<int32_t>(ca.kb * BK + sb * 64), tok);
                 advance(ca, true);
                 ++ia;
             }
@@ -354,7 +368,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t box = !p.small_a ? BM : ca.rows <= 16 ? 16u : ca.rows <= 32 ? 32u : ca.rows <= 64 ? 64u : BM;
                 const CUtensorMap* tA = box == 16 ? &tmA16 : box == 32 ? &tmA32 : box == 64 ? &tmA64 : &tmA;
                 mbar_expect_tx(&fullA[s], box * BK * 2);
-                tma_load_2d(sA + s * A_BYTES, tA, &fullA[s], static_cast<int32_t>(ca.kb * BK), ca.row);
+                for (uint32_t sb = 0; sb < KSUB; ++sb)
+                    tma_load_2d(sA + s * A_BYTES + sb * SUBA, tA, &fullA[s], static_cast<int32_t>(ca.kb * BK + sb * 64),
+                                ca.row);
                 advance(ca, true);
                 ++ia;
             };
@@ -400,7 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b0 = smem_u32(sB + sb * B_BYTES);
 #pragma unroll
                     for (uint32_t k = 0; k < BK / 16; ++k)
-                        umma_bf16(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                        umma_bf16(d_tmem, umma_desc_sw128(a0 + (k >> 2) * SUBA + (k & 3u) * 32),
+                                  umma_desc_sw128(b0 + (k >> 2) * SUBB + (k & 3u) * 32), idesc,
                                   (kb != kb_lo || k != 0) ? 1u : 0u);
                     umma_commit(&emptyA[sa]);
                     umma_commit(&emptyB[sb]);
@@ -666,7 +683,7 @@ void launch_gemm_tc_epi(int epi, const CUtensorMap* tmA, const CUtensorMap* tmB,
     p.starts = starts;
     p.colmap = colmap;
     p.out32 = out;
-    const uint32_t nkb = sh.K / BK;
+    const uint32_t nkb = (sh.K + BK - 1) / BK;
     p.ksplit = epi == kEpiF32Part ? (ksplit < 1 ? 1u : ksplit > nkb ? nkb : ksplit) : 1u;
     p.kps = (nkb + p.ksplit - 1) / p.ksplit;
     p.ksplit = (nkb + p.kps - 1) / p.kps;  // no empty splits
