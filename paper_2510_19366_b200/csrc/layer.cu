@@ -184,6 +184,7 @@ struct mp_layer_s {
     // (unswapped) remainder tiles; MOEPRISM_TC_TILE=128|256|256-plain forces
     int tile_mode = 0;
     bool tile256 = false, tile256_g2 = false;  // this forward's choice for gemm1 / gemm2
+    bool r_tables = false;  // this forward's route_bucket also wrote the permutation tables (decode)
     bool has_experts = true, has_router = true;  // MP_LAYER_* role flags
 
     std::vector<std::vector<uint32_t>> assignment;
@@ -664,6 +665,21 @@ void prefetch_routed_weights(mp_layer_s* L, uint32_t T, cudaStream_t s) {
     L->launches += 1;
 }
 
+// Small batches (<= 16 rows per sub-expert on average): the 1-SM gemm1
+// gathers its A rows from x itself (TMA gather4, one per 4 rows and k-block)
+// and dispatch writes only the permutation tables -- no x_perm.  Large
+// batches materialise x_perm: gather4 moves ~5 B/cycle per SM, so a gathered
+// 128-row A operand left gemm1 2.2-2.7x slower at 4096 Mixtral tokens
+// (profiles/r02g_gather_ab.txt); decode batches gain 2-3%.
+bool gather_batch(const mp_layer_s* L, const void* x, uint32_t T, uint32_t k_eff) {
+    static const int gather_env = [] {  // MOEPRISM_GATHER=0 never / 1 always (A/B)
+        const char* e = std::getenv("MOEPRISM_GATHER");
+        return e ? std::atoi(e) : -1;
+    }();
+    const bool shape = gather_env == 1 || (gather_env < 0 && (size_t)T * k_eff <= (size_t)16 * L->G);
+    return shape && L->use_tc && (L->d % 8) == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+}
+
 // bucket -> dispatch -> gemm1 -> gemm2 -> combine, given sel / w on the device.
 void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, const float* w, bool unit, void* y,
                  cudaStream_t s, StageTimer& tm, bool check_finite = false, bool with_shared = false,
@@ -720,29 +736,22 @@ void run_experts(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* sel, 
         ck_launch("bucket");
         tm.end(1, 2);
     }
-    // Small batches (<= 16 rows per sub-expert on average): the 1-SM gemm1
-    // gathers its A rows from x itself (TMA gather4, one per 4 rows and
-    // k-block) and dispatch writes only the permutation tables -- no x_perm.
-    // Large batches materialise x_perm: gather4 moves ~5 B/cycle per SM, so a
-    // gathered 128-row A operand left gemm1 2.2-2.7x slower at 4096 Mixtral
-    // tokens (profiles/r02g_gather_ab.txt); decode batches gain 2-3%.
-    static const int gather_env = [] {  // MOEPRISM_GATHER=0 never / 1 always (A/B)
-        const char* e = std::getenv("MOEPRISM_GATHER");
-        return e ? std::atoi(e) : -1;
-    }();
-    const bool gather_shape = gather_env == 1 ||
-                              (gather_env < 0 && (size_t)T * (kscalar ? kscalar : L->k_max) <= (size_t)16 * L->G);
-    const bool gather = gather_shape && L->use_tc && !L->tile256 && (L->d % 8) == 0 &&
-                        (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+    const bool gather = !L->tile256 && gather_batch(L, x, T, kscalar ? kscalar : L->k_max);
     CUtensorMap tmXg;
     if (gather && !mp::make_tmap_bf16_2d(&tmXg, x, T, L->d, 1, 64)) fail(MP_ERR_CUDA, "gather tensor map");
     tm.begin(2);
     if (L->offload) offload_step(L, s);  // transfers counted in the dispatch stage
-    // the fused routing kernel already flagged non-finite input rows (sum |x|)
-    mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws, gather ? nullptr : L->x_perm, s,
-                        !bucketed, bucketed ? mp::route_tokens_per_block(T) : mp::kRouteTokensPerBlock);
-    ck_launch("dispatch");
-    tm.end(2, 1);
+    // the fused routing kernel already flagged non-finite input rows (sum |x|),
+    // and at decode batches wrote the permutation tables too
+    const bool tables_done = bucketed && L->r_tables && gather;
+    L->r_tables = false;
+    if (!tables_done) {
+        mp::launch_dispatch(L->dtype, x, T, L->d, L->d_pad, sel, w, L->k_max, L->G, L->ws,
+                            gather ? nullptr : L->x_perm, s, !bucketed,
+                            bucketed ? mp::route_tokens_per_block(T) : mp::kRouteTokensPerBlock);
+        ck_launch("dispatch");
+    }
+    tm.end(2, tables_done ? 0 : 1);
     mp::GemmShape g1{L->G, L->d_pad, 2 * L->w_pad, T * L->k_max, L->w_pad, 2 * L->w_pad};
     mp::GemmShape g2{L->G, L->w_pad, L->d_pad, T * L->k_max, L->d_pad, L->d_pad};
     tm.begin(3);
@@ -885,9 +894,12 @@ bool route(mp_layer_s* L, const void* x, uint32_t T, const uint32_t* kpt, uint32
                     L->r_last_ks = 1;  // plane 0 now holds the logits
                     L->launches += 1;
                 }
-                mp::launch_route_bucket(L->r_partial, ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
+                // decode batches (gemm1 gathers its rows from x): the permutation
+                // tables come out of the routing kernel and dispatch is skipped
+                L->r_tables = mp::launch_route_bucket(L->r_partial, ks, T, L->G, pl.Npad, L->k_max, kpt, k, L->desc.weight_mode,
                                         L->sel, L->wsel, rg, x, L->d, L->wrT, L->r_ticket, L->r_flagged,
-                                        L->ws, s, mp::route_tokens_per_block(T), L->num_sms);
+                                        L->ws, s, mp::route_tokens_per_block(T), L->num_sms,
+                                        gather_batch(L, x, T, kpt ? L->k_max : k));
                 bucketed = true;
                 ck_launch("router(tc)+bucket");
                 tm.end(0, 2);

@@ -121,12 +121,13 @@ void launch_partials_topk(const double* partial, uint32_t ks, uint32_t T, uint32
 // partials -> top-k -> exact re-selection of near-tie tokens (count added to
 // *n_fixed) -> bucket ranks -> device-wide scans (last CTA; *ticket must be
 // 0 on entry and is left 0).  Replaces partials_topk + router_fixup +
-// bucket_local + bucket_scan.
-void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
+// bucket_local + bucket_scan.  Returns whether it also wrote the permutation
+// tables (tables requested and the grid-barrier path taken).
+bool launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
                          const RouterGuard& rg, const void* x, uint32_t d, const float* wrT, uint32_t* ticket,
                          uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb = kRouteTokensPerBlock,
-                         int num_sms = 0);
+                         int num_sms = 0, bool tables = false);  // tables: also write perm_tok / perm_w / slot_row
 // tokens per CTA of the fused routing epilogue: fewer for small batches (more
 // CTAs; measured: one or two 32-token CTAs at T = 64 are slower)
 inline uint32_t route_tokens_per_block(uint32_t T) {

@@ -546,7 +546,8 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     float* __restrict__ wout, int* __restrict__ err, RouterGuard rg, const __nv_bfloat16* __restrict__ x, uint32_t d,
     const float* __restrict__ wrT, uint32_t* __restrict__ ticket, uint32_t* __restrict__ stats, uint32_t* lrank,
     uint32_t* block_counts, uint32_t* block_base, uint32_t* offsets, uint32_t* mprefix_tc, uint32_t* mprefix_simt,
-    uint32_t* mprefix_tc2, uint32_t tb, uint32_t smem_bytes, uint32_t grid_scan) {
+    uint32_t* mprefix_tc2, uint32_t tb, uint32_t smem_bytes, uint32_t grid_scan, uint32_t* perm_tok, float* perm_w,
+    uint32_t* slot_row) {
     extern __shared__ double rsm[];  // [tb][G] logits, then [tb][G] keys; the last CTA: staged counts
     double* sc = rsm + (size_t)(threadIdx.x / 32) * G;        // used by warps < tb only
     double* key = rsm + (size_t)(tb + threadIdx.x / 32) * G;
@@ -741,6 +742,28 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
             if (blk != blockIdx.x) __syncthreads();  // the previous block's scan scratch is free
             bucket_bases_grid(nblk, blk, G, block_counts, block_base, offsets, mprefix_tc, mprefix_simt,
                               mprefix_tc2);
+        }
+        if (perm_tok) {
+            // the permutation tables of this CTA's tokens (what the dispatch
+            // kernel writes when the GEMM gathers its rows from x itself:
+            // decode batches), from its own bucket bases and ranks
+            __syncthreads();
+            for (uint32_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+                for (uint32_t tl = warp; tl < tb; tl += blockDim.x / 32) {
+                    const uint32_t tt = blk * tb + tl;
+                    if (tt >= T) continue;
+                    for (uint32_t j = lane; j < k_max; j += 32) {
+                        const uint32_t g = sel[(size_t)tt * k_max + j];
+                        uint32_t pos = kSelNone;
+                        if (g != kSelNone && g < G) {
+                            pos = block_base[(size_t)blk * G + g] + lrank[(size_t)tt * k_max + j];
+                            perm_tok[pos] = tt;
+                            perm_w[pos] = wout[(size_t)tt * k_max + j];
+                        }
+                        slot_row[(size_t)tt * k_max + j] = pos;
+                    }
+                }
+            }
         }
         if (threadIdx.x == 0 && atomicAdd(ticket + 2, 1u) == gridDim.x - 1) {
             ticket[1] = 0;  // every CTA is past the barrier: reset for the next forward (stream-ordered)
@@ -1169,10 +1192,10 @@ void launch_partials_reduce(double* partial, uint32_t ks, uint32_t T, uint32_t G
     launch_k(partials_reduce_kernel, dim3((warps + 7) / 8), dim3(256), 0, s, partial, ks, T, G, Npad);
 }
 
-void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
+bool launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_t G, uint32_t Npad, uint32_t k_max,
                          const uint32_t* kpt, uint32_t k, int weight_mode, uint32_t* sel, float* w,
                          const RouterGuard& rg, const void* x, uint32_t d, const float* wrT, uint32_t* ticket,
-                         uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb, int num_sms) {
+                         uint32_t* stats, BucketWs& ws, cudaStream_t s, uint32_t tb, int num_sms, bool tables) {
     // the routing arrays, or the last CTA's staged counts (1 byte per block and
     // bucket) when they are larger and fit
     const size_t nblk = (T + tb - 1) / tb;
@@ -1198,7 +1221,7 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
             partial, ks, T, G, Npad, k_max, kpt, k, weight_mode, sel, w, ws.err, rg,
             static_cast<const __nv_bfloat16*>(x), d, wrT, ticket, stats, ws.lrank, ws.block_counts, ws.block_base,
             ws.offsets, ws.mprefix_tc, ws.mprefix_simt, ws.mprefix_tc2, tb, static_cast<uint32_t>(smem),
-            grid_scan ? 1u : 0u);
+            grid_scan ? 1u : 0u, (tables && grid_scan) ? ws.perm_tok : nullptr, ws.perm_w, ws.slot_row);
     };
     if (G <= 64)
         launch(route_bucket_kernel<2>);
@@ -1206,6 +1229,7 @@ void launch_route_bucket(const double* partial, uint32_t ks, uint32_t T, uint32_
         launch(route_bucket_kernel<4>);
     else
         launch(route_bucket_kernel<8>);
+    return tables && grid_scan;
 }
 
 void launch_router_fixup(int dtype, const void* x, uint32_t d, const float* wrT, uint32_t G, uint32_t k_max,

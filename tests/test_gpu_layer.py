@@ -333,10 +333,13 @@ def test_profiling_stage_times(oracle, torch_cuda):
     L.forward(torch.from_numpy(x).cuda().to(torch.bfloat16), k=4)
     st = L.stage_times()
     assert set(st) == {"router", "bucket", "dispatch", "gemm1", "gemm2", "combine"}
-    # the bucketing runs inside the tensor-core router's fused epilogue here
+    # the bucketing runs inside the tensor-core router's fused epilogue here,
+    # and at this decode-size batch (gemm1 gathers its rows from x) so do the
+    # permutation tables: no dispatch launch
     assert st["bucket"][1] == 0 and st["router"][1] == 2
+    assert st["dispatch"][1] == 0
     assert all(v[0] > 0 for name, v in st.items() if v[1])
-    assert L.launch_count() - n0 == sum(v[1] for v in st.values()) in (6, 8)  # 8: split GEMM schedule
+    assert L.launch_count() - n0 == sum(v[1] for v in st.values()) == 5
 
 
 def test_tensor_core_router_logit_error(oracle, torch_cuda, mixtral):
