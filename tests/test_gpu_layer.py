@@ -534,12 +534,15 @@ def test_gemm_schedules_agree(oracle, torch_cuda, k, mixtral):
         assert ok.all(), f"mode {mode}: {(~ok).sum()} elements off"
 
 
-@pytest.mark.parametrize("T,d", [(1, 512), (37, 512), (300, 512), (560, 512), (777, 512), (37, 768), (560, 768)])
+@pytest.mark.parametrize("T,d", [(1, 512), (37, 512), (300, 512), (560, 512), (777, 512), (37, 768), (560, 768),
+                                 (300, 576), (560, 640)])
 def test_pair_swapped_tails_ragged(oracle, torch_cuda, T, d):
     """CTA pairs with swapped-operand remainder tiles on ragged buckets against
     the oracle: every remainder class (< 32, 32..255 rows, with and without
-    full tiles before them, an odd N-tile count at d = 768, exact multiples);
-    routing bit-exact, outputs within the bf16 tolerance."""
+    full tiles before them, an odd N-tile count at d = 768, exact multiples;
+    d = 576 / 640: K not a multiple of the 128-deep pair k-block, the last one
+    half zero-filled by the TMA); routing bit-exact, outputs within the bf16
+    tolerance."""
     import ctypes as C
     torch = torch_cuda
     from paper_2510_19366_b200 import _lib
