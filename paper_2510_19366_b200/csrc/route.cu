@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
     __shared__ double pair_part[kPairBatch][4];
     const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 #if MP_ROUTE_TRACE
-    uint64_t tr_[8];
+    uint64_t tr_[8], tr_coop = 0, tr_row = 0, tr_topk = 0;
     uint32_t ntr_ = 0;
     auto stamp = [&]() { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_[ntr_++])); };
     stamp();
@@ -601,11 +601,17 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         }
     }
     __syncthreads();
+#if MP_ROUTE_TRACE
+    if (first_blk) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_coop));
+#endif
     bool flagged = false;
     uint32_t kt = 0;
     double guard = 0.0;
     if (t < T) {
         const double xn = warp_row_abs_sum(x + (size_t)t * d, d);  // certification bound input
+#if MP_ROUTE_TRACE
+        if (first_blk) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_row));
+#endif
         if (!isfinite(xn) && lane == 0 && err) atomicOr(err, 2);    // the reference's check_input
         // fixed-order sum over the K splits; all NC loads of a split in flight
         // (the partials come from L2 / HBM: a load per candidate in turn left
@@ -639,6 +645,9 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         kt = token_k(kpt, k_scalar, t, k_max, G, err);
         const double gap = warp_topk_fast<NC>(sc, G, kt, k_max, weight_mode, sel + (size_t)t * k_max,
                                           wout + (size_t)t * k_max, vk[warp], msk[warp], slot_of[warp]);
+#if MP_ROUTE_TRACE
+        if (first_blk) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_topk));
+#endif
         __syncwarp();
         // the exact pass also takes every token that may be an oracle near tie
         // (exact gap < 1e-6), so near ties are counted exactly
@@ -773,9 +782,10 @@ __global__ void __launch_bounds__(1024) route_bucket_kernel(
         __syncthreads();
         MP_RT_STAMP();  // 6: bases done
         if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
-            printf("route_bucket(grid) blk %u: topk %llu exact %llu masks %llu ranks %llu barrier %llu bases %llu ns\n",
-                   blockIdx.x, tr_[1] - tr_[0], tr_[2] - tr_[1], tr_[3] - tr_[2], tr_[4] - tr_[3], tr_[5] - tr_[4],
-                   tr_[6] - tr_[5]);
+            printf("route_bucket(grid) blk %u: topk %llu [partials %llu, warp0 row|x| %llu, warp0 top-k %llu] exact %llu "
+                   "masks %llu ranks %llu barrier %llu bases %llu ns\n",
+                   blockIdx.x, tr_[1] - tr_[0], tr_coop - tr_[0], tr_row - tr_coop, tr_topk - tr_row, tr_[2] - tr_[1],
+                   tr_[3] - tr_[2], tr_[4] - tr_[3], tr_[5] - tr_[4], tr_[6] - tr_[5]);
 #endif
         return;
     }
