@@ -17,7 +17,8 @@
 //     n*256 + 128 r .. +127 (accumulator columns [128 r, 128 r + 128)).
 //   gemm2: B tile = W2 rows n*256 .. +255 = output columns; CTA r loads its half.
 // Tiles are (g, n, m) with 256-row m tiles (prefix of ceil(count_g / 256)),
-// m fastest, strided over the clusters of a persistent grid.
+// m fastest, handed to the clusters of a persistent grid in balanced rounds
+// walked in snake order (tile_at below).
 //
 // Remainder tiles (round 2) run with SWAPPED operands: a group's last tile of
 // r < 256 rows computes D^T = W_tile . X_r^T as an M=256 (weight rows) x
@@ -97,17 +98,18 @@ constexpr uint32_t BK = 64 * KSUB;
 constexpr uint32_t SUB_A = HM * 64 * 2;   // one 64-deep sub-block of A / of the B half: 16 KB
 constexpr uint32_t SUB_B = 128 * 64 * 2;
 constexpr uint32_t NSP = MP_PAIR_STAGES;
-constexpr uint32_t A_BYTES = HM * BK * 2;   // 16 KB per CTA
-constexpr uint32_t B_BYTES = 128 * BK * 2;  // 16 KB per CTA (half of the 256-row B tile)
+constexpr uint32_t A_BYTES = HM * BK * 2;   // per CTA and stage: 128 A rows x BK (32 KB)
+constexpr uint32_t B_BYTES = 128 * BK * 2;  // per CTA and stage: half of the 256-row B tile (32 KB)
 constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 #ifndef MP_PAIR_EPI_WARPS
 #define MP_PAIR_EPI_WARPS 4
 #endif
-// warp 0 TMA, warp 1 TMEM alloc + MMA (leader), warps 2.. epilogue: 4 or 8
-// (two per TMEM lane quarter, each taking half of the accumulator columns).
-// Measured (tile_trace.py, k=8): 8 warps halve the SwiGLU epilogue (13.7k ->
-// 6.1k cycles per tile) but it is hidden behind the next tile's MMAs anyway,
-// and the extra polling warps slow gemm2 by 9%: 4.
+// warp 0 TMA, warp 1 TMEM alloc + MMA (leader), warps 2..5 epilogue (one per
+// TMEM lane quarter).  Measured (round 1, tile_trace.py, k=8): 8 epilogue
+// warps halve the SwiGLU epilogue (13.7k -> 6.1k cycles per tile) but it is
+// hidden behind the next tile's MMAs anyway, and the extra polling warps slow
+// gemm2 by 9%; round 2's 8-warp variant for the short-K Qwen down projection
+// was no faster either.  The swapped-remainder epilogue assumes 4.
 constexpr uint32_t kEpiWarps = MP_PAIR_EPI_WARPS;
 constexpr uint32_t kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kTmemCols = 512;
